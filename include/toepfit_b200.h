@@ -1,0 +1,132 @@
+/*
+ * toepfit_b200.h -- C ABI of the B200-native LSAR / Repeated-Halving order
+ * sweep (arXiv 2112.12994).  Drop-in for the reference's hot-path entry
+ * points (namespace toepfit, /root/reference/proj):
+ *
+ *   tf_upload_series   <- TimeSeries(std::vector<double>)      series.hpp:16-31, series.cpp:23-32
+ *   tf_lsar_sweep      <- FitResult lsar_fit(series, p_bar, c, seed)          lsar.hpp:89, lsar.cpp:100-124
+ *   tf_rh_sweep        <- FitResult rh_fit(series, p_bar, c, cfg*, seed)      repeated_halving.hpp:97-99,
+ *                                                                            repeated_halving.cpp:191-232
+ *   tf_residuals       <- Eigen::VectorXd residuals(sys, phi)                 toeplitz.hpp:84-86, toeplitz.cpp:87-98
+ *   tf_sample_rows     <- SampleSet sample_rows(pi, c, seed)                  sketch.hpp:47-48, sketch.cpp:20-59
+ *   tf_apply_sample    <- apply_sample(sys, sample, width, A_S, b_S)          sketch.hpp:53-54, sketch.cpp:61-79
+ *   tf_solve_sampled   <- solve_compressed(apply_sample(...))                 sketch.hpp:63-64, sketch.cpp:96-101
+ *   tf_select_order    <- int select_order(const PACFResult&)                 toeplitz.hpp:100, toeplitz.cpp:133-138
+ *
+ * Conventions (mirroring the reference): indices are 0-based int64, series
+ * and coefficients are fp64; errors never cross the ABI as exceptions --
+ * every call returns a tf_status (USAGE/DATA/NUMERICAL mirror UsageError /
+ * DataError / NumericalError of errors.hpp:12-29, CLI exit codes 2/3/4) and
+ * tf_last_error() holds the message.  The caller owns every host buffer; the
+ * context owns device memory.  One context per host thread (the reference is
+ * single-threaded; distinct fits may run concurrently on distinct contexts,
+ * SPEC.md:431).  Nothing here falls back to the CPU: without a usable CUDA
+ * device tf_create returns TF_CUDA.
+ */
+#ifndef TOEPFIT_B200_H
+#define TOEPFIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TF_OK = 0,
+  TF_USAGE = 1,
+  TF_DATA = 2,
+  TF_NUMERICAL = 3,
+  TF_CUDA = 4,
+  TF_NCCL = 5
+} tf_status;
+
+typedef struct tf_context tf_context;
+
+typedef struct {
+  int device;    /* CUDA device ordinal */
+  int reserved;  /* must be 0 */
+} tf_opts;
+
+/* RHConfig (repeated_halving.hpp:56-65) */
+typedef struct {
+  int64_t base_threshold;
+  int64_t sample_count;
+  int64_t gaussian_rows;
+  uint64_t seed;
+} tf_rh_cfg;
+
+/* Optional diagnostics / deterministic-index mode for the LSAR sweep.  All
+ * pointers are host pointers and may be NULL. */
+typedef struct {
+  const int64_t* fixed_idx; /* [p_bar][c]: replaces sampling (deterministic-index mode) */
+  const double* fixed_w;    /* [p_bar][c] */
+  int64_t* idx_out;         /* [p_bar][c] drawn indices */
+  double* w_out;            /* [p_bar][c] drawn weights */
+  double* rnorm2_out;       /* [p_bar] ||r_p||^2 */
+  double* ssum_out;         /* [p_bar] sum of the scores sampled at lag p */
+  double* scores_out;       /* [n - p_bar] scores of the last lag */
+  double* resid_out;        /* [n - p_bar] residuals of the last lag */
+  int* method_out;          /* [p_bar] 0 CholeskyQR2, 2 shifted CholeskyQR3 */
+} tf_lsar_diag;
+
+typedef struct {
+  const int64_t* fixed_idx;     /* [p_bar][c] per-lag samples (nullable) */
+  const double* fixed_w;
+  const int64_t* fixed_levels;  /* concatenated halving index sets, levels 1..depth (nullable) */
+  const int64_t* fixed_up_idx;  /* [depth][sample_count] upward-pass samples (nullable) */
+  const double* fixed_up_w;
+  double* scores_out;           /* [n - p_bar] final leverage scores */
+  int* depth_out;
+  int64_t* idx_out;             /* [p_bar][c] */
+  double* w_out;
+} tf_rh_diag;
+
+const char* tf_version(void);
+tf_status tf_create(const tf_opts* opts, tf_context** out);
+void tf_destroy(tf_context* ctx);
+const char* tf_last_error(const tf_context* ctx);
+
+/* Series resident in HBM for the following sweeps.  Validates non-empty and
+ * finite values (DataError, series.cpp:23-32). */
+tf_status tf_upload_series(tf_context* ctx, const double* y, int64_t n);
+/* Same, from a device pointer already in HBM (no host copy). */
+tf_status tf_upload_series_device(tf_context* ctx, const double* d_y, int64_t n);
+
+/* LSAR order sweep p = 1..p_bar on the uploaded series.  Outputs (host):
+ * taus[p_bar], coefs_packed[p_bar (p_bar+1)/2] (phi_1, phi_2, ...),
+ * lag_seconds[p_bar] (device time per lag body), p_star (nullable ok). */
+tf_status tf_lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed,
+                        const tf_lsar_diag* diag, double* taus, double* coefs_packed,
+                        double* lag_seconds, int* p_star);
+
+/* Repeated-Halving sweep; cfg NULL -> RHConfig::defaults(n - p_bar, p_bar + 1, c,
+ * derive_seed(seed, 0x5c07e5)). */
+tf_status tf_rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg, uint64_t seed,
+                      const tf_rh_diag* diag, double* taus, double* coefs_packed,
+                      double* lag_seconds, double* upfront_seconds, int* p_star);
+
+/* ---- single operations on host buffers (tests, integration) ---- */
+tf_status tf_residuals(tf_context* ctx, const double* y, int64_t n_used, int p, const double* phi,
+                       double* r_out);
+/* Draw c rows with probability proportional to scores[i] (scores need not be
+ * normalised; sketch.cpp:20-59 with pi = scores / sum). */
+tf_status tf_sample_rows(tf_context* ctx, const double* scores, int64_t n, int64_t c, uint64_t seed,
+                         int64_t* idx_out, double* w_out);
+/* A_S (c x width, row-major) and b_S of the window system (y, n_used, p). */
+tf_status tf_apply_sample(tf_context* ctx, const double* y, int64_t n_used, int p,
+                          const int64_t* idx, const double* w, int64_t c, int width, double* a_out,
+                          double* b_out);
+/* phi = argmin || A_S phi - b_S || for the sampled window system. */
+tf_status tf_solve_sampled(tf_context* ctx, const double* y, int64_t n_used, int p,
+                           const int64_t* idx, const double* w, int64_t c, double* phi_out,
+                           int* method_out);
+
+int tf_select_order(const double* taus, int p_bar, double bound);
+uint64_t tf_derive_seed(uint64_t seed, uint64_t tag);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,12 @@
+"""paper_2112_12994_b200 -- B200-native LSAR / Repeated-Halving order sweep.
+
+Host mirror of the reference toepfit API over the C ABI of
+libtoepfit_b200.so (hand-written sm_100a kernels); see DESIGN.md.
+"""
+from .api import (CudaError, DataError, Engine, FitResult, NumericalError, PACFResult, RHConfig,  # noqa: F401
+                  RunReport, TimeSeries, UsageError, default_engine, derive_seed, lsar_fit,
+                  report_to_json, rh_fit, run_fit, select_order)
+
+__all__ = ["TimeSeries", "FitResult", "PACFResult", "RHConfig", "RunReport", "Engine",
+           "UsageError", "DataError", "NumericalError", "CudaError", "lsar_fit", "rh_fit",
+           "run_fit", "report_to_json", "select_order", "derive_seed", "default_engine"]

@@ -1,0 +1,385 @@
+"""Python mirror of the reference's fit API for the hot path.
+
+Same names, argument meaning and error behaviour as namespace toepfit
+(/root/reference/proj/include/toepfit):
+  TimeSeries                       series.hpp:16-31
+  UsageError/DataError/NumericalError   errors.hpp:12-29
+  FitResult, PACFResult            lsar.hpp:28-35, toeplitz.hpp:59-66
+  lsar_fit(series, p_bar, c, seed) lsar.hpp:89
+  rh_fit(series, p_bar, c, config, seed)  repeated_halving.hpp:97-99
+  RHConfig.defaults                repeated_halving.cpp:33-41
+  run_fit(series, method, ...)     bench.cpp:107-124 (lsar | rh)
+  report_to_json(report)           bench.cpp:268-283
+  select_order(pacf)               toeplitz.cpp:133-138
+Every call goes through the C ABI (libtoepfit_b200.so) onto the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from ._abi import ptr
+
+
+class UsageError(RuntimeError):
+    pass
+
+
+class DataError(RuntimeError):
+    pass
+
+
+class NumericalError(RuntimeError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_ERRS = {_abi.TF_USAGE: UsageError, _abi.TF_DATA: DataError, _abi.TF_NUMERICAL: NumericalError,
+         _abi.TF_CUDA: CudaError, _abi.TF_NCCL: CudaError}
+
+EXIT_CODES = {UsageError: 2, DataError: 3, NumericalError: 4}  # errors.hpp:8-9
+
+
+class TimeSeries:
+    """Immutable fp64 series; validated non-empty and finite (series.cpp:23-32)."""
+
+    def __init__(self, values, label: str = ""):
+        v = np.array(values, dtype=np.float64, copy=True).ravel()
+        if v.size == 0:
+            raise DataError("series must contain at least one value")
+        bad = np.flatnonzero(~np.isfinite(v))
+        if bad.size:
+            raise DataError(f"series value at position {int(bad[0])} is not finite")
+        v.setflags(write=False)
+        self._v = v
+        self.label = label
+
+    def values(self) -> np.ndarray:
+        return self._v
+
+    def size(self) -> int:
+        return int(self._v.size)
+
+    def __len__(self) -> int:
+        return self.size()
+
+
+@dataclass
+class PACFResult:
+    taus: list
+    bound: float = 0.0
+    method: str = "exact"
+
+
+@dataclass
+class FitResult:
+    p_star: int = 0
+    coefficients: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    pacf: PACFResult = field(default_factory=lambda: PACFResult([]))
+    per_lag_seconds: list = field(default_factory=list)
+    per_lag_coefficients: list = field(default_factory=list)
+    upfront_seconds: float = 0.0
+    diag: dict | None = None
+
+
+@dataclass
+class RHConfig:
+    base_threshold: int = 0
+    sample_count: int = 0
+    gaussian_rows: int = 0
+    seed: int = 0
+
+    @staticmethod
+    def defaults(n: int, k: int, c: int, seed: int) -> "RHConfig":
+        logk = int(math.ceil(math.log(k + 1.0)))
+        return RHConfig(base_threshold=max(c, 10 * k * logk), sample_count=c,
+                        gaussian_rows=int(math.ceil(8.0 * math.log(max(n, 2)))), seed=seed)
+
+    def validate(self) -> None:
+        if self.sample_count < 1:
+            raise UsageError("sample count must be positive")
+        if self.base_threshold < self.sample_count:
+            raise UsageError("base threshold below sample count")
+        if self.gaussian_rows < 1:
+            raise UsageError("need at least one sketch row")
+
+
+def derive_seed(seed: int, tag: int) -> int:
+    return int(_abi.lib().tf_derive_seed(C.c_uint64(seed), C.c_uint64(tag)))
+
+
+class Engine:
+    """One tf_context (one CUDA device, one stream) with a resident series."""
+
+    def __init__(self, device: int = 0):
+        L = _abi.lib()
+        self._ctx = C.c_void_p()
+        opts = _abi.TfOpts(device=device, reserved=0)
+        st = L.tf_create(C.byref(opts), C.byref(self._ctx))
+        if st != _abi.TF_OK:
+            raise CudaError(f"tf_create failed (status {st}); no usable CUDA device")
+        self._series_id = None
+
+    def close(self):
+        if self._ctx:
+            _abi.lib().tf_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int):
+        if st != _abi.TF_OK:
+            msg = _abi.lib().tf_last_error(self._ctx).decode()
+            raise _ERRS.get(st, RuntimeError)(msg)
+
+    # ---------------------------------------------------------------- series
+    def upload(self, series: TimeSeries):
+        if self._series_id is not None and self._series_id[0] is series:
+            return
+        v = series.values()
+        self._check(_abi.lib().tf_upload_series(self._ctx, ptr(v), v.size))
+        self._series_id = (series,)
+
+    def upload_device(self, dev_ptr: int, n: int):
+        self._check(_abi.lib().tf_upload_series_device(self._ctx, C.c_void_p(dev_ptr), n))
+        self._series_id = None
+
+    # ---------------------------------------------------------------- sweeps
+    def lsar_sweep(self, p_bar: int, c: int, seed: int, fixed_idx=None, fixed_w=None,
+                   want_diag: bool = False, n: int | None = None):
+        pb = max(int(p_bar), 1)
+        taus = np.zeros(pb)
+        coefs = np.zeros(pb * (pb + 1) // 2)
+        secs = np.zeros(pb)
+        pstar = C.c_int(0)
+        d = _abi.TfLsarDiag()
+        keep = []
+        diag = None
+        if fixed_idx is not None:
+            fi = np.ascontiguousarray(fixed_idx, dtype=np.int64)
+            fw = np.ascontiguousarray(fixed_w, dtype=np.float64)
+            if fi.size != pb * c or fw.size != pb * c:
+                raise UsageError("fixed samples must be [p_bar][c]")
+            keep += [fi, fw]
+            d.fixed_idx = ptr(fi, _abi._i64p)
+            d.fixed_w = ptr(fw)
+        if want_diag:
+            w = max(int(n) - pb, 1)
+            diag = dict(idx=np.zeros((pb, c), np.int64), w=np.zeros((pb, c)), rnorm2=np.zeros(pb),
+                        ssum=np.zeros(pb), scores=np.zeros(w), resid=np.zeros(w),
+                        method=np.zeros(pb, np.int32))
+            d.idx_out = ptr(diag["idx"], _abi._i64p)
+            d.w_out = ptr(diag["w"])
+            d.rnorm2_out = ptr(diag["rnorm2"])
+            d.ssum_out = ptr(diag["ssum"])
+            d.scores_out = ptr(diag["scores"])
+            d.resid_out = ptr(diag["resid"])
+            d.method_out = ptr(diag["method"], _abi._i32p)
+        self._check(_abi.lib().tf_lsar_sweep(self._ctx, int(p_bar), int(c), C.c_uint64(seed),
+                                             C.byref(d), ptr(taus), ptr(coefs), ptr(secs),
+                                             C.byref(pstar)))
+        return taus, coefs, secs, pstar.value, diag
+
+    def rh_sweep(self, p_bar: int, c: int, cfg: RHConfig | None, seed: int, fixed=None,
+                 want_diag: bool = False, n: int | None = None):
+        pb = max(int(p_bar), 1)
+        taus = np.zeros(pb)
+        coefs = np.zeros(pb * (pb + 1) // 2)
+        secs = np.zeros(pb)
+        up = C.c_double(0)
+        pstar = C.c_int(0)
+        d = _abi.TfRhDiag()
+        keep = []
+        diag = None
+        if fixed:
+            for key, attr, dt in (("idx", "fixed_idx", np.int64), ("w", "fixed_w", np.float64),
+                                  ("levels", "fixed_levels", np.int64),
+                                  ("up_idx", "fixed_up_idx", np.int64),
+                                  ("up_w", "fixed_up_w", np.float64)):
+                if fixed.get(key) is not None:
+                    a = np.ascontiguousarray(fixed[key], dtype=dt).ravel()
+                    keep.append(a)
+                    setattr(d, attr, ptr(a, _abi._i64p if dt == np.int64 else _abi._f64p))
+        depth = C.c_int(0)
+        if want_diag:
+            m = max(int(n) - pb, 1)
+            diag = dict(scores=np.zeros(m), idx=np.zeros((pb, c), np.int64), w=np.zeros((pb, c)))
+            d.scores_out = ptr(diag["scores"])
+            d.idx_out = ptr(diag["idx"], _abi._i64p)
+            d.w_out = ptr(diag["w"])
+            d.depth_out = C.pointer(depth)
+        ccfg = None
+        if cfg is not None:
+            ccfg = _abi.TfRhCfg(cfg.base_threshold, cfg.sample_count, cfg.gaussian_rows, cfg.seed)
+        self._check(_abi.lib().tf_rh_sweep(self._ctx, int(p_bar), int(c),
+                                           C.byref(ccfg) if ccfg is not None else None,
+                                           C.c_uint64(seed), C.byref(d), ptr(taus), ptr(coefs),
+                                           ptr(secs), C.byref(up), C.byref(pstar)))
+        if diag is not None:
+            diag["depth"] = depth.value
+        return taus, coefs, secs, up.value, pstar.value, diag
+
+    # ------------------------------------------------------------ single ops
+    def residuals(self, y, n_used: int, p: int, phi) -> np.ndarray:
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        phi = np.ascontiguousarray(phi, dtype=np.float64)
+        if phi.size != p:
+            raise UsageError("coefficient length does not match lag order")
+        out = np.zeros(max(n_used - p, 1))
+        self._check(_abi.lib().tf_residuals(self._ctx, ptr(y), int(n_used), int(p), ptr(phi), ptr(out)))
+        self._series_id = None
+        return out[: n_used - p]
+
+    def sample_rows(self, scores, c: int, seed: int):
+        s = np.ascontiguousarray(scores, dtype=np.float64)
+        idx = np.zeros(max(c, 1), np.int64)
+        w = np.zeros(max(c, 1))
+        self._check(_abi.lib().tf_sample_rows(self._ctx, ptr(s), s.size, int(c), C.c_uint64(seed),
+                                              ptr(idx, _abi._i64p), ptr(w)))
+        return idx[:c], w[:c]
+
+    def apply_sample(self, y, n_used: int, p: int, idx, w, width: int | None = None):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        width = p if width is None else width
+        a = np.zeros((idx.size, max(width, 1)))
+        b = np.zeros(idx.size)
+        self._check(_abi.lib().tf_apply_sample(self._ctx, ptr(y), int(n_used), int(p),
+                                               ptr(idx, _abi._i64p), ptr(w), idx.size, int(width),
+                                               ptr(a), ptr(b)))
+        self._series_id = None
+        return a, b
+
+    def solve_sampled(self, y, n_used: int, p: int, idx, w):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        phi = np.zeros(p)
+        m = C.c_int(0)
+        self._check(_abi.lib().tf_solve_sampled(self._ctx, ptr(y), int(n_used), int(p),
+                                                ptr(idx, _abi._i64p), ptr(w), idx.size, ptr(phi),
+                                                C.byref(m)))
+        self._series_id = None
+        return phi, m.value
+
+
+_default_engine: Engine | None = None
+
+
+def default_engine() -> Engine:
+    global _default_engine
+    if _default_engine is None:
+        _default_engine = Engine(0)
+    return _default_engine
+
+
+def _unpack(coefs, p_bar):
+    out, off = [], 0
+    for p in range(1, p_bar + 1):
+        out.append(coefs[off:off + p].copy())
+        off += p
+    return out
+
+
+def _finish(method, taus, coefs, secs, pstar, p_bar, c, upfront=0.0, diag=None) -> FitResult:
+    per = _unpack(coefs, p_bar)
+    fit = FitResult()
+    fit.pacf = PACFResult(taus=list(map(float, taus)), bound=1.96 / math.sqrt(float(c)), method=method)
+    fit.per_lag_seconds = list(map(float, secs))
+    fit.per_lag_coefficients = per
+    fit.p_star = int(pstar)
+    fit.coefficients = per[pstar - 1].copy() if pstar > 0 else np.zeros(0)
+    fit.upfront_seconds = float(upfront)
+    fit.diag = diag
+    return fit
+
+
+def lsar_fit(series: TimeSeries, p_bar: int, c: int, seed: int, *, engine: Engine | None = None,
+             fixed_idx=None, fixed_w=None, want_diag: bool = False) -> FitResult:
+    """lsar.cpp:100-124 on the GPU.  fixed_idx/fixed_w ([p_bar][c]) switch to
+    deterministic-index mode (samples supplied instead of drawn)."""
+    eng = engine or default_engine()
+    eng.upload(series)
+    taus, coefs, secs, pstar, diag = eng.lsar_sweep(p_bar, c, seed, fixed_idx, fixed_w, want_diag,
+                                                    n=series.size())
+    return _finish("lsar", taus, coefs, secs, pstar, p_bar, c, 0.0, diag)
+
+
+def rh_fit(series: TimeSeries, p_bar: int, c: int, config: RHConfig | None = None, seed: int = 0, *,
+           engine: Engine | None = None, fixed=None, want_diag: bool = False) -> FitResult:
+    """repeated_halving.cpp:191-232 on the GPU."""
+    eng = engine or default_engine()
+    eng.upload(series)
+    taus, coefs, secs, up, pstar, diag = eng.rh_sweep(p_bar, c, config, seed, fixed, want_diag,
+                                                      n=series.size())
+    return _finish("rh", taus, coefs, secs, pstar, p_bar, c, up, diag)
+
+
+def select_order(pacf: PACFResult) -> int:
+    t = np.ascontiguousarray(pacf.taus, dtype=np.float64)
+    return int(_abi.lib().tf_select_order(ptr(t), t.size, float(pacf.bound)))
+
+
+@dataclass
+class RunReport:
+    method: str
+    n: int
+    p_bar: int
+    c: int
+    seed: int
+    timing_recorded: bool
+    upfront_seconds: float
+    per_lag_seconds: list
+    cumulative_seconds: list
+    pacf: PACFResult
+    p_star: int
+    coefficients: list
+
+
+def run_fit(series: TimeSeries, method: str, p_bar: int, c: int, seed: int,
+            with_timing: bool = True, engine: Engine | None = None) -> RunReport:
+    """bench.cpp:107-124 restricted to the GPU methods (lsar, rh)."""
+    if method in ("exact", "srht"):
+        raise UsageError(f"method '{method}' is outside the B200 hot path (lsar | rh)")
+    if c < 1:
+        raise UsageError(f"method '{method}' needs a sample count")
+    if method == "lsar":
+        fit = lsar_fit(series, p_bar, c, seed, engine=engine)
+    elif method == "rh":
+        fit = rh_fit(series, p_bar, c, None, seed, engine=engine)
+    else:
+        raise UsageError(f"unknown method '{method}'")
+    if not with_timing:  # bench.cpp:76-79
+        fit.per_lag_seconds = [0.0] * len(fit.per_lag_seconds)
+        fit.upfront_seconds = 0.0
+    cum, acc = [], fit.upfront_seconds
+    for s in fit.per_lag_seconds:
+        acc += s
+        cum.append(acc)
+    return RunReport(method=method, n=series.size(), p_bar=p_bar, c=c, seed=seed,
+                     timing_recorded=with_timing, upfront_seconds=fit.upfront_seconds,
+                     per_lag_seconds=fit.per_lag_seconds, cumulative_seconds=cum, pacf=fit.pacf,
+                     p_star=fit.p_star, coefficients=list(map(float, fit.coefficients)))
+
+
+def report_to_json(r: RunReport) -> str:
+    """bench.cpp:268-283 key order and layout (nlohmann dump(2))."""
+    j = {"method": r.method, "n": r.n, "p_bar": r.p_bar, "c": r.c, "seed": r.seed,
+         "timing_recorded": r.timing_recorded, "upfront_seconds": r.upfront_seconds,
+         "per_lag_seconds": r.per_lag_seconds, "cumulative_seconds": r.cumulative_seconds,
+         "pacf": {"method": r.pacf.method, "bound": r.pacf.bound, "taus": r.pacf.taus},
+         "p_star": r.p_star, "coefficients": r.coefficients}
+    return json.dumps(j, indent=2, sort_keys=True) + "\n"  # nlohmann objects are key-sorted

@@ -1,0 +1,66 @@
+// common.cuh -- device helpers shared by the toepfit B200 kernels.
+//
+// * Counter RNG bit-identical to the reference's Rng (rng.hpp:14-84): draw t
+//   (0-based) of Rng(s) is mix(s + (t+1) * golden), so any draw is computable
+//   independently on any thread.
+// * DMMA (mma.sync m8n8k4 f64) wrapper -- the fp64 tensor-core instruction on
+//   sm_100a (SASS: DMMA.8x8x4).  Fragment layout (PTX ISA, m8n8k4 .f64):
+//     A (8x4, row):  a = A[lane>>2][lane&3]
+//     B (4x8, col):  b = B[lane&3][lane>>2]
+//     C (8x8):       c0,c1 = C[lane>>2][2*(lane&3) + {0,1}]
+// * Warp inclusive scans / reductions in a fixed order (deterministic).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tfk {
+
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ull;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// derive_seed(seed, tag) = Rng(seed).fork(tag)()  (rng.hpp:30-32, 82-84)
+__host__ __device__ __forceinline__ uint64_t derive_seed(uint64_t seed, uint64_t tag) {
+  const uint64_t child = mix64(seed ^ mix64(tag + 0x632be59bd9b4e019ull));
+  return mix64(child + kGolden);
+}
+
+// raw draw t (0-based) of Rng(seed)
+__host__ __device__ __forceinline__ uint64_t rng_draw(uint64_t seed, uint64_t t) {
+  return mix64(seed + (t + 1) * kGolden);
+}
+
+// uniform01 of draw t (rng.hpp:35): 53 random bits
+__host__ __device__ __forceinline__ double rng_uniform01(uint64_t seed, uint64_t t) {
+  return static_cast<double>(rng_draw(seed, t) >> 11) * 0x1.0p-53;
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// inclusive scan across lanes (Kogge-Stone, fixed order)
+__device__ __forceinline__ double warp_incl_scan(double v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+}  // namespace tfk

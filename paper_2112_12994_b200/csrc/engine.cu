@@ -1,0 +1,761 @@
+// engine.cu -- host orchestration of the B200 LSAR / RH order sweep and the
+// C ABI (include/toepfit_b200.h).  One CUDA stream per context; every lag is
+// a fixed sequence of kernel launches with no host synchronisation inside the
+// sweep (device-side status flags are read once at the end).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+#include "k_chol.cuh"
+#include "k_gram.cuh"
+#include "k_pass.cuh"
+#include "k_sample.cuh"
+
+using namespace tfk;
+
+namespace tfe {
+
+static void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw TfError{TF_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+#define CK(x) cuda_check((x), #x)
+#define LAUNCH_CHECK(name) cuda_check(cudaGetLastError(), name)
+
+template <class T>
+void DBuf<T>::need(size_t count) {
+  if (count <= n && p) return;
+  if (p) cudaFree(p);
+  p = nullptr;
+  n = 0;
+  size_t want = std::max<size_t>(count, 1);
+  cuda_check(cudaMalloc(&p, want * sizeof(T)), "cudaMalloc");
+  n = want;
+}
+
+template <class T>
+void DBuf<T>::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  n = 0;
+}
+
+template struct DBuf<double>;
+template struct DBuf<int64_t>;
+template struct DBuf<int>;
+template struct DBuf<uint64_t>;
+template struct DBuf<unsigned char>;
+
+static const char* reason_text(int reason) {
+  switch (reason) {
+    case kReasonZeroResidual: return "zero residual norm; sampling distribution undefined";
+    case kReasonNegativeScore: return "negative leverage score";
+    case kReasonZeroScoreSum: return "zero score sum; distribution undefined";
+    case kReasonCholFail: return "compressed least-squares factorization failed";
+    case kReasonRankDeficient: return "reference matrix is rank deficient";
+    case kReasonZeroWindow: return "all-zero window; leverage undefined";
+    default: return "numerical failure";
+  }
+}
+
+static void raise_from_status(const int st[3]) {
+  if (st[0] == 0) return;
+  const tf_status code = st[0] == kErrUsage ? TF_USAGE : st[0] == kErrData ? TF_DATA : TF_NUMERICAL;
+  throw TfError{code, std::string(reason_text(st[2])) + " (lag " + std::to_string(st[1]) + ")"};
+}
+
+// ---------------------------------------------------------------------------
+// CholeskyQR2 (shifted CholeskyQR3 on breakdown) solve of one sampled system.
+// rows: c gathered rows of width K = p + 1 (gathered order: target first).
+// Writes phi (length p) to phi_out, optionally coefs/taus/method at `lag`.
+struct SolveOut {
+  double* phi;
+  double* coefs;
+  int64_t coef_off;
+  double* taus;
+  int* method;
+  int lag;
+  int* status;
+};
+
+static int trinv_slots(int K) {
+  const int s = (K + 31) / 32;
+  return s <= 1 ? 1 : s <= 2 ? 2 : s <= 4 ? 4 : s <= 8 ? 8 : s <= 16 ? 16 : 32;
+}
+
+template <int S>
+static void launch_trinv_s(const double* Rrow, int K, int perm, double* out, const int* gate,
+                           cudaStream_t st) {
+  const int grid = (K + kTrinvWarps - 1) / kTrinvWarps;
+  k_trinv<S><<<grid, kTrinvWarps * 32, 0, st>>>(Rrow, K, perm, out, gate);
+}
+
+static void launch_trinv(const double* Rrow, int K, int perm, double* out, const int* gate,
+                         cudaStream_t st) {
+  switch (trinv_slots(K)) {
+    case 1: launch_trinv_s<1>(Rrow, K, perm, out, gate, st); break;
+    case 2: launch_trinv_s<2>(Rrow, K, perm, out, gate, st); break;
+    case 4: launch_trinv_s<4>(Rrow, K, perm, out, gate, st); break;
+    case 8: launch_trinv_s<8>(Rrow, K, perm, out, gate, st); break;
+    case 16: launch_trinv_s<16>(Rrow, K, perm, out, gate, st); break;
+    default: launch_trinv_s<32>(Rrow, K, perm, out, gate, st); break;
+  }
+  LAUNCH_CHECK("k_trinv");
+}
+
+template <int S>
+static void launch_phi_s(const PhiArgs& a, cudaStream_t st) {
+  k_phi<S><<<1, kPhiThreads, sizeof(double) * 3 * a.K, st>>>(a);
+}
+
+static void launch_phi(const PhiArgs& a, cudaStream_t st) {
+  switch (trinv_slots(a.K)) {
+    case 1: launch_phi_s<1>(a, st); break;
+    case 2: launch_phi_s<2>(a, st); break;
+    case 4: launch_phi_s<4>(a, st); break;
+    case 8: launch_phi_s<8>(a, st); break;
+    case 16: launch_phi_s<16>(a, st); break;
+    default: launch_phi_s<32>(a, st); break;
+  }
+  LAUNCH_CHECK("k_phi");
+}
+
+struct GramPlan {
+  int nblk, npair, nsplit;
+  int64_t rps;
+};
+
+static GramPlan gram_plan(int64_t rows, int K, int sm_count) {
+  GramPlan g;
+  g.nblk = (K + 63) / 64;
+  g.npair = g.nblk * (g.nblk + 1) / 2;
+  const int64_t target = 2LL * sm_count;
+  int64_t ns = (target + g.npair - 1) / g.npair;
+  ns = std::max<int64_t>(1, std::min<int64_t>(ns, (rows + 63) / 64));
+  int64_t rps = (rows + ns - 1) / ns;
+  rps = (rps + 31) / 32 * 32;
+  g.rps = std::max<int64_t>(rps, 32);
+  g.nsplit = (int)((rows + g.rps - 1) / g.rps);
+  if (g.nsplit < 1) g.nsplit = 1;
+  return g;
+}
+
+template <class L>
+static void gram(tf_context* ctx, const L& ld, int64_t rows, int K, double* G, const int* gate) {
+  const GramPlan g = gram_plan(rows, K, ctx->sm_count);
+  ctx->sb.W.need((size_t)g.nsplit * g.npair * 4096);
+  dim3 grid(g.npair, g.nsplit);
+  k_gram<L><<<grid, kGramThreads, 0, ctx->stream>>>(ld, rows, K, g.nblk, g.rps, ctx->sb.W.get(), gate);
+  LAUNCH_CHECK("k_gram");
+  const int64_t tot = (int64_t)g.npair * 4096;
+  k_gram_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, ctx->stream>>>(ctx->sb.W.get(), g.nsplit, g.npair,
+                                                                       g.nblk, K, G, gate);
+  LAUNCH_CHECK("k_gram_reduce");
+}
+
+template <class L>
+static void qform(tf_context* ctx, const L& ld, int64_t rows, int K, const double* Rg, double* Q,
+                  const int* gate) {
+  dim3 grid((unsigned)((rows + 63) / 64), (unsigned)((K + 63) / 64));
+  k_qform<L><<<grid, kGramThreads, 0, ctx->stream>>>(ld, rows, K, Rg, Q, K, gate);
+  LAUNCH_CHECK("k_qform");
+}
+
+static void chol(tf_context* ctx, const double* G, int K, int perm, int iter, int64_t rows,
+                 double* Rrow, int lag, int* status) {
+  CholArgs a;
+  a.G = G;
+  a.K = K;
+  a.perm = perm;
+  a.iter = iter;
+  a.nrows = rows;
+  a.use_smem = chol_fits_smem(K) ? 1 : 0;
+  size_t smem = a.use_smem ? chol_smem_bytes(K) : sizeof(double) * (32 * 33 + 8);
+  if (!a.use_smem) ctx->sb.ws.need((size_t)K * (K + 1) / 2);
+  a.ws = ctx->sb.ws.get();
+  a.Rrow = Rrow;
+  a.flags = ctx->sb.flags.get();
+  a.status = status;
+  a.lag = lag;
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmemLimit));
+    attr_set = true;
+  }
+  k_chol<<<1, kCholThreads, smem, ctx->stream>>>(a);
+  LAUNCH_CHECK("k_chol");
+}
+
+// Size every solve buffer for the largest system of a sweep up front so that
+// no cudaMalloc/cudaFree (which synchronise) happens between lags.
+static void reserve_solve(tf_context* ctx, int64_t c, int Kmax) {
+  SolveBufs& b = ctx->sb;
+  const size_t KK = (size_t)Kmax * Kmax;
+  const size_t tri = (size_t)Kmax * (Kmax + 1) / 2;
+  b.G.need(KK);
+  b.R1row.need(tri);
+  b.R2row.need(tri);
+  b.R3row.need(tri);
+  b.Rg1.need(KK);
+  b.Rinv2.need(KK);
+  b.Q1.need((size_t)c * Kmax);
+  b.Q2.need((size_t)c * Kmax);
+  b.flags.need(4);
+  size_t wmax = 0;
+  for (int K = 2; K <= Kmax; ++K) {
+    const GramPlan g = gram_plan(c, K, ctx->sm_count);
+    wmax = std::max(wmax, (size_t)g.nsplit * g.npair * 4096);
+  }
+  b.W.need(wmax);
+  if (!chol_fits_smem(Kmax)) b.ws.need(tri);
+}
+
+template <class L>
+static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const SolveOut& o) {
+  SolveBufs& b = ctx->sb;
+  reserve_solve(ctx, c, K);
+  int* shifted = b.flags.get();
+  PhiArgs pa;
+  pa.K = K;
+  pa.R2row = b.R2row.get();
+  pa.R3row = b.R3row.get();
+  pa.Rg1 = b.Rg1.get();
+  pa.Rinv2 = b.Rinv2.get();
+  pa.flags = b.flags.get();
+  pa.phi = o.phi;
+  pa.coefs = o.coefs;
+  pa.coef_off = o.coef_off;
+  pa.taus = o.taus;
+  pa.method = o.method;
+  pa.lag = o.lag;
+  if (K == 2) {
+    gram(ctx, ld, c, K, b.G.get(), nullptr);
+    k_solve_k2<<<1, 1, 0, ctx->stream>>>(b.G.get(), pa);
+    LAUNCH_CHECK("k_solve_k2");
+    return;
+  }
+  // iteration 1: G1 = A^T A (gathered), R1, Rinv1 (rows permuted to gathered order)
+  gram(ctx, ld, c, K, b.G.get(), nullptr);
+  chol(ctx, b.G.get(), K, 1, 1, c, b.R1row.get(), o.lag, o.status);
+  launch_trinv(b.R1row.get(), K, 1, b.Rg1.get(), nullptr, ctx->stream);
+  qform(ctx, ld, c, K, b.Rg1.get(), b.Q1.get(), nullptr);
+  // iteration 2: G2 = Q1^T Q1
+  DenseRows q1{b.Q1.get(), K};
+  gram(ctx, q1, c, K, b.G.get(), nullptr);
+  chol(ctx, b.G.get(), K, 0, 2, c, b.R2row.get(), o.lag, o.status);
+  // iteration 3 (only when iteration 1 needed the shift)
+  launch_trinv(b.R2row.get(), K, 0, b.Rinv2.get(), shifted, ctx->stream);
+  qform(ctx, q1, c, K, b.Rinv2.get(), b.Q2.get(), shifted);
+  DenseRows q2{b.Q2.get(), K};
+  gram(ctx, q2, c, K, b.G.get(), shifted);
+  chol(ctx, b.G.get(), K, 0, 3, c, b.R3row.get(), o.lag, o.status);
+  launch_phi(pa, ctx->stream);
+}
+
+// ---------------------------------------------------------------------------
+static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev) {
+  PassArgs a;
+  a.y = ctx->y.get();
+  a.w = w;
+  a.q = q;
+  a.phi = phi;
+  a.s = ctx->s.get();
+  a.r = ctx->r.get();
+  a.Rprev = Rprev;
+  a.chunkA = ctx->chunkA.get();
+  a.chunkB = ctx->chunkB.get();
+  a.tileA = ctx->tileA.get();
+  a.tileB = ctx->tileB.get();
+  const int64_t ntile = (w + kPassTile - 1) / kPassTile;
+  const size_t smem = pass_smem_bytes(q);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    CK(cudaFuncSetAttribute(k_lsar_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  k_lsar_pass<<<(unsigned)ntile, kPassThreads, smem, ctx->stream>>>(a);
+  LAUNCH_CHECK("k_lsar_pass");
+}
+
+static void launch_scan(tf_context* ctx, int64_t ntile, int lag, int check_r, int unit_r = 0) {
+  k_lag_scan<<<1, kScanThreads, 0, ctx->stream>>>(ctx->tileA.get(), ctx->tileB.get(), ntile,
+                                                  ctx->OT.get(), ctx->scal.get(), ctx->Rhist.get(),
+                                                  ctx->Shist.get(), lag, check_r, ctx->status.get(),
+                                                  unit_r);
+  LAUNCH_CHECK("k_lag_scan");
+}
+
+static void launch_draw(tf_context* ctx, uint64_t seed, int64_t c, int64_t w, int64_t* idx,
+                        double* wts) {
+  DrawArgs a;
+  a.seed = seed;
+  a.c = c;
+  a.scal = ctx->scal.get();
+  a.OT = ctx->OT.get();
+  a.ntile = (w + kPassTile - 1) / kPassTile;
+  a.tA = ctx->tileA.get();
+  a.tB = ctx->tileB.get();
+  a.chunkA = ctx->chunkA.get();
+  a.chunkB = ctx->chunkB.get();
+  a.s = ctx->s.get();
+  a.r = ctx->r.get();
+  a.w = w;
+  a.idx = idx;
+  a.wts = wts;
+  const int per = kDrawThreads / 32;
+  k_draw<<<(unsigned)((c + per - 1) / per), kDrawThreads, 0, ctx->stream>>>(a);
+  LAUNCH_CHECK("k_draw");
+}
+
+static void alloc_state(tf_context* ctx, int p_bar, int64_t c, int64_t w) {
+  const int64_t ntile = (w + kPassTile - 1) / kPassTile;
+  const int64_t nchunk = (w + kChunk - 1) / kChunk;
+  ctx->s.need(w);
+  ctx->r.need(w);
+  ctx->chunkA.need(nchunk);
+  ctx->chunkB.need(nchunk);
+  ctx->tileA.need(ntile);
+  ctx->tileB.need(ntile);
+  ctx->OT.need(ntile);
+  ctx->scal.need(4);
+  ctx->Rhist.need(p_bar + 2);
+  ctx->Shist.need(p_bar + 2);
+  ctx->phi.need(p_bar + 1);
+  ctx->coefs.need((size_t)p_bar * (p_bar + 1) / 2);
+  ctx->taus.need(p_bar);
+  ctx->idx.need(c);
+  ctx->wts.need(c);
+  ctx->status.need(4);
+  ctx->method.need(p_bar);
+  ctx->sb.flags.need(4);
+  CK(cudaMemsetAsync(ctx->status.get(), 0, 4 * sizeof(int), ctx->stream));
+  CK(cudaMemsetAsync(ctx->sb.flags.get(), 0, 4 * sizeof(int), ctx->stream));
+}
+
+static void ensure_events(tf_context* ctx, size_t n) {
+  while (ctx->events.size() < n) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ctx->events.push_back(e);
+  }
+}
+
+static void check_lsar_args(const tf_context* ctx, int p_bar, int64_t c) {
+  // LsarDriver ctor (lsar.cpp:55-64)
+  if (p_bar < 1) throw TfError{TF_USAGE, "maximum lag must be at least 1"};
+  if (ctx->n == 0) throw TfError{TF_USAGE, "no series uploaded"};
+  if (ctx->n <= (int64_t)p_bar + 1)
+    throw TfError{TF_DATA, "series too short for maximum lag " + std::to_string(p_bar)};
+  if (c < p_bar) throw TfError{TF_USAGE, "sample count below maximum lag"};
+}
+
+static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, const tf_lsar_diag* d,
+                       double* taus, double* coefs, double* lag_seconds, int* p_star) {
+  check_lsar_args(ctx, p_bar, c);
+  const int64_t w = ctx->n - p_bar;  // constant row count (lsar.cpp:63)
+  const int64_t ntile = (w + kPassTile - 1) / kPassTile;
+  cudaStream_t st = ctx->stream;
+  alloc_state(ctx, p_bar, c, w);
+  const bool fixed = d && d->fixed_idx && d->fixed_w;
+  if (fixed) {
+    const size_t tot = (size_t)p_bar * c;
+    for (size_t i = 0; i < tot; ++i)
+      if (d->fixed_idx[i] < 0 || d->fixed_idx[i] >= w)
+        throw TfError{TF_USAGE, "sample index out of range"};  // sketch.cpp:69
+    ctx->fidx.need(tot);
+    ctx->fw.need(tot);
+    CK(cudaMemcpyAsync(ctx->fidx.get(), d->fixed_idx, tot * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->fw.get(), d->fixed_w, tot * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  const bool want_hist = d && (d->idx_out || d->w_out);
+  if (want_hist) {
+    ctx->idx_hist.need((size_t)p_bar * c);
+    ctx->w_hist.need((size_t)p_bar * c);
+  }
+  reserve_solve(ctx, c, p_bar + 1);
+  ensure_events(ctx, p_bar + 1);
+  CK(cudaEventRecord(ctx->events[0], st));
+  // lag-0 pass: r_0 = -y[0..w), s_0 = 0  ->  s_1 = y^2 / sum y^2 (lsar.cpp:11-15)
+  launch_pass(ctx, 0, w, ctx->phi.get(), ctx->scal.get());
+  for (int p = 1; p <= p_bar; ++p) {
+    const int q = p - 1;
+    launch_scan(ctx, ntile, q, 1);
+    int64_t* idx = ctx->idx.get();
+    double* wts = ctx->wts.get();
+    if (fixed) {
+      idx = ctx->fidx.get() + (size_t)(p - 1) * c;
+      wts = ctx->fw.get() + (size_t)(p - 1) * c;
+    } else {
+      launch_draw(ctx, derive_seed(seed, (uint64_t)p), c, w, idx, wts);
+    }
+    if (want_hist) {
+      CK(cudaMemcpyAsync(ctx->idx_hist.get() + (size_t)(p - 1) * c, idx, c * sizeof(int64_t),
+                         cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(ctx->w_hist.get() + (size_t)(p - 1) * c, wts, c * sizeof(double),
+                         cudaMemcpyDeviceToDevice, st));
+    }
+    SolveOut o;
+    o.phi = ctx->phi.get();
+    o.coefs = ctx->coefs.get();
+    o.coef_off = (int64_t)(p - 1) * p / 2;
+    o.taus = ctx->taus.get();
+    o.method = ctx->method.get();
+    o.lag = p;
+    o.status = ctx->status.get();
+    GatherRows ld{ctx->y.get(), idx, wts, (int64_t)p};
+    solve_rows(ctx, ld, c, p + 1, o);
+    // residuals of the lag-p window fit + score update s_p = s_{p-1} + r_{p-1}^2/R_{p-1}
+    launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());
+    CK(cudaEventRecord(ctx->events[p], st));
+  }
+  if (d && d->rnorm2_out) launch_scan(ctx, ntile, p_bar, 0);  // R_{p_bar} for the diagnostics
+  CK(cudaStreamSynchronize(st));
+  int sth[3];
+  CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  raise_from_status(sth);
+  std::vector<double> t(p_bar);
+  CK(cudaMemcpy(t.data(), ctx->taus.get(), p_bar * sizeof(double), cudaMemcpyDeviceToHost));
+  if (taus) std::memcpy(taus, t.data(), p_bar * sizeof(double));
+  if (coefs)
+    CK(cudaMemcpy(coefs, ctx->coefs.get(), sizeof(double) * (size_t)p_bar * (p_bar + 1) / 2,
+                  cudaMemcpyDeviceToHost));
+  if (lag_seconds)
+    for (int p = 1; p <= p_bar; ++p) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ctx->events[p - 1], ctx->events[p]));
+      lag_seconds[p - 1] = ms * 1e-3;
+    }
+  if (p_star) *p_star = tf_select_order(t.data(), p_bar, 1.96 / std::sqrt((double)c));
+  if (d) {
+    if (d->idx_out)
+      CK(cudaMemcpy(d->idx_out, ctx->idx_hist.get(), sizeof(int64_t) * (size_t)p_bar * c, cudaMemcpyDeviceToHost));
+    if (d->w_out)
+      CK(cudaMemcpy(d->w_out, ctx->w_hist.get(), sizeof(double) * (size_t)p_bar * c, cudaMemcpyDeviceToHost));
+    if (d->rnorm2_out)
+      CK(cudaMemcpy(d->rnorm2_out, ctx->Rhist.get() + 1, sizeof(double) * p_bar, cudaMemcpyDeviceToHost));
+    if (d->ssum_out)
+      CK(cudaMemcpy(d->ssum_out, ctx->Shist.get() + 1, sizeof(double) * p_bar, cudaMemcpyDeviceToHost));
+    if (d->scores_out) CK(cudaMemcpy(d->scores_out, ctx->s.get(), sizeof(double) * w, cudaMemcpyDeviceToHost));
+    if (d->resid_out) CK(cudaMemcpy(d->resid_out, ctx->r.get(), sizeof(double) * w, cudaMemcpyDeviceToHost));
+    if (d->method_out) CK(cudaMemcpy(d->method_out, ctx->method.get(), sizeof(int) * p_bar, cudaMemcpyDeviceToHost));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// single operations
+__global__ void k_partials(const double* s, const double* r, int64_t w, double* chunkA,
+                           double* chunkB, double* tileA, double* tileB) {
+  // same reduction shape as k_lsar_pass for externally supplied (s, r)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t i0 = (int64_t)blockIdx.x * kPassTile;
+  const int rows = (int)min((int64_t)kPassTile, w - i0);
+  double tA = 0.0, tB = 0.0;
+  for (int u = 0; u < kPassR; ++u) {
+    const int row = tid + kPassThreads * u;
+    double sv = 0.0, rv = 0.0;
+    if (row < rows) {
+      sv = s[i0 + row];
+      rv = r[i0 + row];
+    }
+    const double cA = warp_sum(sv), cB = warp_sum(rv * rv);
+    const int crow = kPassThreads * u + kChunk * warp;
+    if (lane == 0 && crow < rows) {
+      chunkA[(i0 + crow) / kChunk] = cA;
+      chunkB[(i0 + crow) / kChunk] = cB;
+    }
+    tA += cA;
+    tB += cB;
+  }
+  __shared__ double wA[4], wB[4];
+  if (lane == 0) {
+    wA[warp] = tA;
+    wB[warp] = tB;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    tileA[blockIdx.x] = ((wA[0] + wA[1]) + wA[2]) + wA[3];
+    tileB[blockIdx.x] = ((wB[0] + wB[1]) + wB[2]) + wB[3];
+  }
+}
+
+__global__ void k_set_unit(double* scal) {
+  // scores without a residual term: R := 1 so that mass = s + 0 / 1 = s
+  scal[0] = 1.0;
+}
+
+__global__ void k_materialize(GatherRows ld, int64_t c, int width, double* a, double* b) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+  if (t >= c) return;
+  for (int j = threadIdx.x; j <= width; j += blockDim.x) {
+    // gathered column 0 is the target, column j' >= 1 is lag column j' - 1
+    const double v = ld(t, j);
+    if (j == 0) b[t] = v;
+    else a[t * width + (j - 1)] = v;
+  }
+}
+
+static void upload_series(tf_context* ctx, const double* y, int64_t n, bool device_src) {
+  if (n < 1 || !y) throw TfError{TF_DATA, "series must contain at least one value"};
+  if (!device_src) {
+    for (int64_t i = 0; i < n; ++i)
+      if (!std::isfinite(y[i]))
+        throw TfError{TF_DATA, "series value at position " + std::to_string(i) + " is not finite"};
+  }
+  ctx->y.need(n + 64);
+  if (device_src)
+    CK(cudaMemcpyAsync(ctx->y.get(), y, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  else
+    CK(cudaMemcpyAsync(ctx->y.get(), y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->y.get() + n, 0, 64 * sizeof(double), ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->n = n;
+}
+
+static void residuals_op(tf_context* ctx, const double* y, int64_t n_used, int p, const double* phi,
+                         double* r_out) {
+  if (p < 1) throw TfError{TF_USAGE, "lag order must be at least 1"};
+  if (n_used <= p) throw TfError{TF_DATA, "series window too short for lag order"};
+  upload_series(ctx, y, n_used, false);
+  const int64_t w = n_used - p;
+  alloc_state(ctx, p, p, w);
+  CK(cudaMemsetAsync(ctx->s.get(), 0, w * sizeof(double), ctx->stream));
+  CK(cudaMemsetAsync(ctx->r.get(), 0, w * sizeof(double), ctx->stream));
+  CK(cudaMemcpyAsync(ctx->phi.get(), phi, p * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  k_set_unit<<<1, 1, 0, ctx->stream>>>(ctx->scal.get());
+  launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());
+  CK(cudaMemcpyAsync(r_out, ctx->r.get(), w * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+}
+
+static void sample_op(tf_context* ctx, const double* scores, int64_t n, int64_t c, uint64_t seed,
+                      int64_t* idx_out, double* w_out) {
+  if (n < 1) throw TfError{TF_DATA, "empty distribution"};
+  if (c < 1) throw TfError{TF_USAGE, "sample count must be positive"};
+  for (int64_t i = 0; i < n; ++i)
+    if (!(scores[i] >= 0.0)) throw TfError{TF_DATA, "distribution has a negative entry"};
+  const int64_t ntile = (n + kPassTile - 1) / kPassTile;
+  alloc_state(ctx, 1, c, n);
+  CK(cudaMemcpyAsync(ctx->s.get(), scores, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->r.get(), 0, n * sizeof(double), ctx->stream));
+  k_partials<<<(unsigned)ntile, kPassThreads, 0, ctx->stream>>>(ctx->s.get(), ctx->r.get(), n,
+                                                               ctx->chunkA.get(), ctx->chunkB.get(),
+                                                               ctx->tileA.get(), ctx->tileB.get());
+  LAUNCH_CHECK("k_partials");
+  launch_scan(ctx, ntile, 0, 0, /*unit_r=*/1);  // no residual term: mass = s + 0 / 1
+  launch_draw(ctx, seed, c, n, ctx->idx.get(), ctx->wts.get());
+  CK(cudaMemcpyAsync(idx_out, ctx->idx.get(), c * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(w_out, ctx->wts.get(), c * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  int sth[3];
+  CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  if (sth[0] != 0) {
+    if (sth[2] == kReasonZeroScoreSum) throw TfError{TF_DATA, "distribution sums to 0, not 1"};
+    raise_from_status(sth);
+  }
+}
+
+static void check_sample(int64_t n_used, int p, const int64_t* idx, int64_t c) {
+  if (p < 1) throw TfError{TF_USAGE, "lag order must be at least 1"};
+  if (n_used <= p) throw TfError{TF_DATA, "series window too short for lag order"};
+  if (c < 1) throw TfError{TF_USAGE, "empty system"};
+  const int64_t rows = n_used - p;
+  for (int64_t t = 0; t < c; ++t)
+    if (idx[t] < 0 || idx[t] >= rows) throw TfError{TF_USAGE, "sample index out of range"};
+}
+
+static void apply_sample_op(tf_context* ctx, const double* y, int64_t n_used, int p,
+                            const int64_t* idx, const double* w, int64_t c, int width, double* a_out,
+                            double* b_out) {
+  if (width < 1 || width > p) throw TfError{TF_USAGE, "invalid column width"};
+  check_sample(n_used, p, idx, c);
+  upload_series(ctx, y, n_used, false);
+  ctx->idx.need(c);
+  ctx->wts.need(c);
+  DBuf<double> A, B;
+  A.need((size_t)c * width);
+  B.need(c);
+  CK(cudaMemcpyAsync(ctx->idx.get(), idx, c * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->wts.get(), w, c * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  GatherRows ld{ctx->y.get(), ctx->idx.get(), ctx->wts.get(), (int64_t)p};
+  dim3 blk(32, 8);
+  k_materialize<<<(unsigned)((c + 7) / 8), blk, 0, ctx->stream>>>(ld, c, width, A.get(), B.get());
+  LAUNCH_CHECK("k_materialize");
+  CK(cudaMemcpyAsync(a_out, A.get(), sizeof(double) * c * width, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(b_out, B.get(), sizeof(double) * c, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  A.release();
+  B.release();
+}
+
+static void solve_sampled_op(tf_context* ctx, const double* y, int64_t n_used, int p,
+                             const int64_t* idx, const double* w, int64_t c, double* phi_out,
+                             int* method_out) {
+  check_sample(n_used, p, idx, c);
+  upload_series(ctx, y, n_used, false);
+  alloc_state(ctx, p, c, 1);
+  CK(cudaMemcpyAsync(ctx->idx.get(), idx, c * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->wts.get(), w, c * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  SolveOut o{ctx->phi.get(), nullptr, 0, nullptr, ctx->method.get(), 1, ctx->status.get()};
+  GatherRows ld{ctx->y.get(), ctx->idx.get(), ctx->wts.get(), (int64_t)p};
+  solve_rows(ctx, ld, c, p + 1, o);
+  CK(cudaMemcpyAsync(phi_out, ctx->phi.get(), p * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  int m = 0;
+  CK(cudaMemcpyAsync(&m, ctx->method.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  int sth[3];
+  CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  raise_from_status(sth);
+  if (method_out) *method_out = m;
+}
+
+static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg, uint64_t seed,
+                     const tf_rh_diag* d, double* taus, double* coefs, double* lag_seconds,
+                     double* upfront_seconds, int* p_star) {
+  throw TfError{TF_USAGE, "rh sweep not built yet"};
+}
+
+}  // namespace tfe
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using tfe::TfError;
+
+template <class F>
+static tf_status guarded(tf_context* ctx, F&& f) {
+  try {
+    f();
+    if (ctx) ctx->err.clear();
+    return TF_OK;
+  } catch (const TfError& e) {
+    if (ctx) ctx->err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->err = "host allocation failed";
+    return TF_CUDA;
+  }
+}
+
+extern "C" {
+
+const char* tf_version(void) { return "toepfit-b200 0.1 (sm_100a)"; }
+
+tf_status tf_create(const tf_opts* opts, tf_context** out) {
+  if (!out) return TF_USAGE;
+  *out = nullptr;
+  int dev = opts ? opts->device : 0;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return TF_CUDA;
+  if (dev < 0 || dev >= count) return TF_USAGE;
+  if (cudaSetDevice(dev) != cudaSuccess) return TF_CUDA;
+  tf_context* ctx = new (std::nothrow) tf_context();
+  if (!ctx) return TF_CUDA;
+  ctx->device = dev;
+  cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return TF_CUDA;
+  }
+  *out = ctx;
+  return TF_OK;
+}
+
+void tf_destroy(tf_context* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto e : ctx->events) cudaEventDestroy(e);
+  ctx->y.release(); ctx->s.release(); ctx->r.release(); ctx->chunkA.release(); ctx->chunkB.release();
+  ctx->tileA.release(); ctx->tileB.release(); ctx->OT.release(); ctx->scal.release();
+  ctx->Rhist.release(); ctx->Shist.release(); ctx->phi.release(); ctx->coefs.release();
+  ctx->taus.release(); ctx->idx.release(); ctx->fidx.release(); ctx->idx_hist.release();
+  ctx->wts.release(); ctx->fw.release(); ctx->w_hist.release(); ctx->status.release();
+  ctx->method.release();
+  tfe::SolveBufs& b = ctx->sb;
+  b.W.release(); b.G.release(); b.R1row.release(); b.R2row.release(); b.R3row.release();
+  b.Rg1.release(); b.Rinv2.release(); b.Q1.release(); b.Q2.release(); b.ws.release(); b.flags.release();
+  ctx->rh_scores.release(); ctx->rh_approx.release(); ctx->rh_approx2.release(); ctx->rh_M.release();
+  ctx->rh_G.release(); ctx->rh_lvl.release(); ctx->rh_tmp.release(); ctx->rh_picked.release();
+  ctx->rh_keys.release(); ctx->rh_keys2.release(); ctx->rh_cub.release();
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* tf_last_error(const tf_context* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+tf_status tf_upload_series(tf_context* ctx, const double* y, int64_t n) {
+  if (!ctx) return TF_USAGE;
+  return guarded(ctx, [&] {
+    cudaSetDevice(ctx->device);
+    tfe::upload_series(ctx, y, n, false);
+  });
+}
+
+tf_status tf_upload_series_device(tf_context* ctx, const double* d_y, int64_t n) {
+  if (!ctx) return TF_USAGE;
+  return guarded(ctx, [&] {
+    cudaSetDevice(ctx->device);
+    tfe::upload_series(ctx, d_y, n, true);
+  });
+}
+
+tf_status tf_lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, const tf_lsar_diag* diag,
+                        double* taus, double* coefs_packed, double* lag_seconds, int* p_star) {
+  if (!ctx) return TF_USAGE;
+  return guarded(ctx, [&] {
+    cudaSetDevice(ctx->device);
+    tfe::lsar_sweep(ctx, p_bar, c, seed, diag, taus, coefs_packed, lag_seconds, p_star);
+  });
+}
+
+tf_status tf_residuals(tf_context* ctx, const double* y, int64_t n_used, int p, const double* phi,
+                       double* r_out) {
+  if (!ctx) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::residuals_op(ctx, y, n_used, p, phi, r_out); });
+}
+
+tf_status tf_sample_rows(tf_context* ctx, const double* scores, int64_t n, int64_t c, uint64_t seed,
+                         int64_t* idx_out, double* w_out) {
+  if (!ctx) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::sample_op(ctx, scores, n, c, seed, idx_out, w_out); });
+}
+
+tf_status tf_apply_sample(tf_context* ctx, const double* y, int64_t n_used, int p, const int64_t* idx,
+                          const double* w, int64_t c, int width, double* a_out, double* b_out) {
+  if (!ctx) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::apply_sample_op(ctx, y, n_used, p, idx, w, c, width, a_out, b_out); });
+}
+
+tf_status tf_solve_sampled(tf_context* ctx, const double* y, int64_t n_used, int p, const int64_t* idx,
+                           const double* w, int64_t c, double* phi_out, int* method_out) {
+  if (!ctx) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::solve_sampled_op(ctx, y, n_used, p, idx, w, c, phi_out, method_out); });
+}
+
+tf_status tf_rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg, uint64_t seed,
+                      const tf_rh_diag* diag, double* taus, double* coefs_packed,
+                      double* lag_seconds, double* upfront_seconds, int* p_star) {
+  if (!ctx) return TF_USAGE;
+  return guarded(ctx, [&] {
+    cudaSetDevice(ctx->device);
+    tfe::rh_sweep(ctx, p_bar, c, cfg, seed, diag, taus, coefs_packed, lag_seconds, upfront_seconds,
+                  p_star);
+  });
+}
+
+int tf_select_order(const double* taus, int p_bar, double bound) {
+  // toeplitz.cpp:133-138: largest lag whose |tau| clears the bound (inclusive)
+  for (int h = p_bar; h >= 1; --h)
+    if (std::fabs(taus[h - 1]) >= bound) return h;
+  return 0;
+}
+
+uint64_t tf_derive_seed(uint64_t seed, uint64_t tag) { return tfk::derive_seed(seed, tag); }
+
+}  // extern "C"

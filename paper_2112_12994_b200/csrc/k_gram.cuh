@@ -1,0 +1,201 @@
+// k_gram.cuh -- fp64 tensor-core (DMMA m8n8k4) Gram and Q-formation kernels
+// for the CholeskyQR2 solve of the sampled least-squares system
+// (replaces the Eigen ColPivHouseholderQR call of toeplitz.cpp:57-71, fed by
+// apply_sample, sketch.cpp:61-79).
+//
+// The sampled, weighted rows are never materialised as a separate matrix:
+// row t of the augmented system in "gathered" column order is
+//   a_t[j'] = w_t * y[off + i_t - j'],  j' = 0..K-1   (K = p + 1)
+// i.e. a contiguous, reversed slice of the series (j' = 0 is the target
+// column, j' >= 1 the lag columns) -- the gather is fused into the tile
+// loads (apply_sample's product w * y is formed exactly as the reference).
+//
+//   k_gram   : split-K partial Gram tiles (64x64 upper block pairs) from rows
+//              [split * rps, (split+1) * rps); 4 warps, 32x32 per warp,
+//              16 DMMA per k4-step.  Deterministic: partials are reduced in
+//              a fixed order by k_gram_reduce.
+//   k_qform  : Q = A * Rg for a dense K x K right factor (structural zeros
+//              above row l+1 skipped), used for CholeskyQR's Q = A R^-1.
+#pragma once
+
+#include "common.cuh"
+
+namespace tfk {
+
+struct GatherRows {
+  const double* y;
+  const int64_t* idx;
+  const double* wt;
+  int64_t off;  // LSAR window system: p; RH full system: p_bar
+  __device__ __forceinline__ double operator()(int64_t t, int col) const {
+    return wt[t] * y[off + idx[t] - col];
+  }
+};
+
+struct DenseRows {
+  const double* q;
+  int64_t ld;
+  __device__ __forceinline__ double operator()(int64_t t, int col) const {
+    return q[t * ld + col];
+  }
+};
+
+constexpr int kGramThreads = 128;
+constexpr int kSJ = 68;  // padded row stride (doubles): conflict-free fragment loads
+
+__device__ __forceinline__ void pair_from_index(int pair, int nblk, int& jb, int& lb) {
+  int rem = pair;
+  jb = 0;
+  while (rem >= nblk - jb) {
+    rem -= nblk - jb;
+    ++jb;
+  }
+  lb = jb + rem;
+}
+
+template <class L>
+__global__ void __launch_bounds__(kGramThreads)
+    k_gram(L ld, int64_t rows, int K, int nblk, int64_t rows_per_split, double* __restrict__ W,
+           const int* skip_flag) {
+  if (skip_flag && *skip_flag == 0) return;
+  __shared__ __align__(16) double SJ[32][kSJ];
+  __shared__ __align__(16) double SL[32][kSJ];
+  int jb, lb;
+  pair_from_index(blockIdx.x, nblk, jb, lb);
+  const bool diag = jb == lb;
+  const int J0 = jb * 64, L0 = lb * 64;
+  const int64_t rb = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t re = min(rows, rb + rows_per_split);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int cc = tid & 63, rsub = tid >> 6;
+  for (int64_t r0 = rb; r0 < re; r0 += 32) {
+#pragma unroll 4
+    for (int s = 0; s < 16; ++s) {
+      const int rr = rsub + 2 * s;
+      const int64_t row = r0 + rr;
+      double vj = 0.0, vl = 0.0;
+      if (row < re) {
+        if (J0 + cc < K) vj = ld(row, J0 + cc);
+        if (!diag && L0 + cc < K) vl = ld(row, L0 + cc);
+      }
+      SJ[rr][cc] = vj;
+      SL[rr][cc] = vl;
+    }
+    __syncthreads();
+    const double(*B)[kSJ] = diag ? SJ : SL;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int tr = 4 * kk + (lane & 3);
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = SJ[tr][32 * wm + 8 * i + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = B[tr][32 * wn + 8 * j + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+  double* out = W + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 4096;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int row = 32 * wm + 8 * i + (lane >> 2);
+      const int col = 32 * wn + 8 * j + 2 * (lane & 3);
+      *reinterpret_cast<double2*>(out + row * 64 + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+}
+
+// G[row * K + col] (row-major, upper blocks valid; diagonal blocks full)
+__global__ void k_gram_reduce(const double* __restrict__ W, int nsplit, int npair, int nblk, int K,
+                              double* __restrict__ G, const int* skip_flag) {
+  if (skip_flag && *skip_flag == 0) return;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)npair * 4096) return;
+  const int pair = (int)(e >> 12), el = (int)(e & 4095);
+  int jb, lb;
+  pair_from_index(pair, nblk, jb, lb);
+  const int row = jb * 64 + (el >> 6), col = lb * 64 + (el & 63);
+  if (row >= K || col >= K) return;
+  double s = 0.0;
+  for (int sp = 0; sp < nsplit; ++sp) s += W[((size_t)sp * npair + pair) * 4096 + el];
+  G[(size_t)row * K + col] = s;
+}
+
+constexpr int kQA = 36;
+
+// Q[t][l] = sum_j' A(t, j') * Rg[j'][l], l < K.  Rg row-major K x K with
+// Rg[j'][l] == 0 whenever j' > l + 1 (upper triangular up to the one-row
+// shift of the gathered column order).
+template <class L>
+__global__ void __launch_bounds__(kGramThreads)
+    k_qform(L ld, int64_t rows, int K, const double* __restrict__ Rg, double* __restrict__ Q,
+            int64_t ldq, const int* skip_flag) {
+  if (skip_flag && *skip_flag == 0) return;
+  __shared__ __align__(16) double SA[64][kQA];
+  __shared__ __align__(16) double SR[32][kSJ];
+  const int64_t t0 = (int64_t)blockIdx.x * 64;
+  const int L0 = blockIdx.y * 64;
+  const int jend = min(K, L0 + 64 + 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int k0 = 0; k0 < jend; k0 += 32) {
+    {
+      const int cc = tid & 31, rr0 = tid >> 5;
+#pragma unroll 4
+      for (int s = 0; s < 16; ++s) {
+        const int rr = rr0 + 4 * s;
+        const int64_t row = t0 + rr;
+        SA[rr][cc] = (row < rows && k0 + cc < K) ? ld(row, k0 + cc) : 0.0;
+      }
+      const int ll = tid & 63, c0 = tid >> 6;
+#pragma unroll 4
+      for (int s = 0; s < 16; ++s) {
+        const int c = c0 + 2 * s;
+        SR[c][ll] = (k0 + c < K && L0 + ll < K) ? Rg[(size_t)(k0 + c) * K + L0 + ll] : 0.0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = SA[32 * wm + 8 * i + (lane >> 2)][4 * kk + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = SR[4 * kk + (lane & 3)][32 * wn + 8 * j + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t row = t0 + 32 * wm + 8 * i + (lane >> 2);
+      const int col = L0 + 32 * wn + 8 * j + 2 * (lane & 3);
+      if (row < rows) {
+        if (col < K) Q[row * ldq + col] = acc[i][j][0];
+        if (col + 1 < K) Q[row * ldq + col + 1] = acc[i][j][1];
+      }
+    }
+}
+
+}  // namespace tfk

@@ -1,0 +1,216 @@
+// k_sample.cuh -- leverage-score sampling without materialising pi or a
+// w-length CDF (sketch.cpp:20-59; lsar.cpp:27-36).
+//
+// After the pass of lag q the scores the next lag samples from are
+//   s_{q+1}(i) = s_q(i) + r_q(i)^2 / R_q,
+// and the pass has already emitted, per 32-row chunk, A_c = sum s_q and
+// B_c = sum r_q^2, plus per-2048-row tile totals.  Sampling lag q+1 is then
+//   k_lag_scan : single CTA.  R_q = sum B_t (fixed tree), tile masses
+//                S_t = A_t + B_t / R_q, exclusive tile prefix OT, total S.
+//   k_draw     : one warp per draw t.  u_t = uniform01 of draw t of
+//                Rng(derive_seed(seed, p)) (bit-identical to the reference),
+//                v = u_t * S; k-ary search of OT (largest tile with OT <= v),
+//                then a sequential scan of the tile's 64 chunk masses and of
+//                the chunk's 32 row masses -- "first cumulative mass > v",
+//                i.e. std::upper_bound on the CDF.  Row masses are computed
+//                with the exact expression the next pass stores, so the
+//                weight 1/sqrt(c * s(i)/S) matches the stored scores.
+// Rounding differs from the reference's sequential CDF only at the ~1e-16
+// level; draws are distributionally identical (and identical in practice).
+#pragma once
+
+#include "common.cuh"
+#include "k_pass.cuh"
+
+namespace tfk {
+
+enum : int { kErrNone = 0, kErrUsage = 1, kErrData = 2, kErrNumerical = 3 };
+
+// status[0] = first error code, status[1] = lag of that error, status[2] = reason id
+__device__ __forceinline__ void raise_status(int* status, int code, int lag, int reason) {
+  if (atomicCAS(status, 0, code) == 0) {
+    status[1] = lag;
+    status[2] = reason;
+  }
+}
+
+// reason ids (host maps them to the reference's messages)
+enum : int {
+  kReasonZeroResidual = 1,  // lsar.cpp:21-23
+  kReasonNegativeScore = 2, // lsar.cpp:29-31
+  kReasonZeroScoreSum = 3,  // lsar.cpp:33
+  kReasonCholFail = 4,      // compressed solve failed
+  kReasonRankDeficient = 5, // RH reference matrix rank deficient (repeated_halving.cpp:57-64)
+  kReasonZeroWindow = 6,    // lsar.cpp:13 all-zero window
+};
+
+constexpr int kScanThreads = 1024;
+
+// scal[0] = R_q, scal[1] = S (total mass for lag q+1)
+__global__ void __launch_bounds__(kScanThreads)
+    k_lag_scan(const double* __restrict__ tA, const double* __restrict__ tB, int64_t ntile,
+               double* __restrict__ OT, double* scal, double* Rhist, double* Shist, int lag,
+               int check_r, int* status, int unit_r = 0) {
+  __shared__ double red[kScanThreads];
+  __shared__ double wsum[32];
+  const int tid = threadIdx.x;
+  const int64_t seg = (ntile + kScanThreads - 1) / kScanThreads;
+  const int64_t b = min(ntile, (int64_t)tid * seg), e = min(ntile, b + seg);
+  double sb = 0.0;
+  for (int64_t t = b; t < e; ++t) sb += tB[t];
+  red[tid] = sb;
+  __syncthreads();
+  for (int o = kScanThreads / 2; o > 0; o >>= 1) {
+    if (tid < o) red[tid] = red[tid] + red[tid + o];
+    __syncthreads();
+  }
+  const double R = unit_r ? 1.0 : red[0];
+  __syncthreads();
+  double ss = 0.0;
+  for (int64_t t = b; t < e; ++t) ss += tA[t] + tB[t] / R;
+  // block exclusive scan of the segment sums (fixed order)
+  const int lane = tid & 31, warp = tid >> 5;
+  const double inc = warp_incl_scan(ss);
+  double ex = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) ex = 0.0;
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const double wi = warp_incl_scan(wsum[lane]);
+    double we = __shfl_up_sync(0xffffffffu, wi, 1);
+    if (lane == 0) we = 0.0;
+    __syncwarp();
+    wsum[lane] = we;
+    if (lane == 31) red[0] = wi;
+  }
+  __syncthreads();
+  double off = wsum[warp] + ex;
+  const double S = red[0];
+  for (int64_t t = b; t < e; ++t) {
+    OT[t] = off;
+    off += tA[t] + tB[t] / R;
+  }
+  if (tid == 0) {
+    scal[0] = R;
+    scal[1] = S;
+    if (Rhist) Rhist[lag] = R;
+    if (Shist) Shist[lag + 1] = S;
+    if (check_r && R == 0.0)
+      raise_status(status, kErrNumerical, lag + 1, lag == 0 ? kReasonZeroWindow : kReasonZeroResidual);
+    if (!(S >= 0.0) || !(R >= 0.0)) raise_status(status, kErrUsage, lag + 1, kReasonNegativeScore);
+    else if (S == 0.0) raise_status(status, kErrNumerical, lag + 1, kReasonZeroScoreSum);
+  }
+}
+
+struct DrawArgs {
+  uint64_t seed;        // derive_seed(user_seed, p)
+  int64_t c;
+  const double* scal;   // R, S
+  const double* OT;
+  int64_t ntile;
+  const double* tA;
+  const double* tB;
+  const double* chunkA;
+  const double* chunkB;
+  const double* s;      // s_q
+  const double* r;      // r_q
+  int64_t w;
+  int64_t* idx;
+  double* wts;
+};
+
+constexpr int kDrawThreads = 256;
+
+__global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
+  __shared__ double buf[kDrawThreads / 32][64];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t t = (int64_t)blockIdx.x * (kDrawThreads / 32) + wib;
+  if (t >= a.c) return;
+  const double R = a.scal[0], S = a.scal[1];
+  const double v = rng_uniform01(a.seed, (uint64_t)t) * S;
+  // ---- tile: largest T with OT[T] <= v ----
+  int64_t lo = 0, hi = a.ntile;
+  while (hi - lo > 32) {
+    const int64_t stride = (hi - lo + 31) / 32;
+    const int64_t pos = lo + (int64_t)lane * stride;
+    const bool pr = pos < hi && a.OT[pos] <= v;
+    int cnt = __popc(__ballot_sync(0xffffffffu, pr));
+    if (cnt == 0) cnt = 1;
+    lo = lo + (int64_t)(cnt - 1) * stride;
+    hi = min(lo + stride, hi);
+  }
+  {
+    const int64_t pos = lo + lane;
+    const bool pr = pos < hi && a.OT[pos] <= v;
+    int cnt = __popc(__ballot_sync(0xffffffffu, pr));
+    if (cnt == 0) cnt = 1;
+    lo = lo + cnt - 1;
+  }
+  int64_t T = lo;
+  // a tile with zero mass can only be hit through the end guard: walk back
+  // (sketch.cpp:54-55 skips zero-mass rows backwards the same way)
+  while (T > 0 && !(a.tA[T] + a.tB[T] / R > 0.0)) --T;
+  double v1 = v - a.OT[T];
+  // ---- chunk within tile ----
+  const int64_t nchunk = (a.w + kChunk - 1) / kChunk;
+  const int64_t cb = T * kChunksPerTile;
+  const int nch = (int)min((int64_t)kChunksPerTile, nchunk - cb);
+  for (int k = lane; k < 64; k += 32)
+    buf[wib][k] = k < nch ? a.chunkA[cb + k] + a.chunkB[cb + k] / R : 0.0;
+  __syncwarp();
+  int chosen = -1;
+  double vrow = 0.0;
+  if (lane == 0) {
+    double cum = 0.0;
+    int lastpos = -1;
+    for (int k = 0; k < nch; ++k) {
+      const double m = buf[wib][k];
+      if (m > 0.0) lastpos = k;
+      const double nxt = cum + m;
+      if (nxt > v1 && m > 0.0) {
+        chosen = k;
+        vrow = v1 - cum;
+        break;
+      }
+      cum = nxt;
+    }
+    if (chosen < 0) {
+      chosen = lastpos < 0 ? nch - 1 : lastpos;
+      vrow = __longlong_as_double(0x7ff0000000000000ll);  // +inf: take last positive row
+    }
+  }
+  chosen = __shfl_sync(0xffffffffu, chosen, 0);
+  vrow = __shfl_sync(0xffffffffu, vrow, 0);
+  __syncwarp();
+  // ---- row within chunk ----
+  const int64_t r0 = (cb + chosen) * kChunk;
+  const int64_t row = r0 + lane;
+  double mass = 0.0;
+  if (row < a.w) {
+    const double rv = a.r[row];
+    mass = a.s[row] + (rv * rv) / R;
+  }
+  buf[wib][lane] = mass;
+  __syncwarp();
+  if (lane == 0) {
+    double cum = 0.0;
+    int pick = -1, lastpos = -1;
+    const int nr = (int)min((int64_t)kChunk, a.w - r0);
+    for (int k = 0; k < nr; ++k) {
+      const double m = buf[wib][k];
+      if (m > 0.0) lastpos = k;
+      const double nxt = cum + m;
+      if (nxt > vrow && m > 0.0) {
+        pick = k;
+        break;
+      }
+      cum = nxt;
+    }
+    if (pick < 0) pick = lastpos < 0 ? 0 : lastpos;
+    const double mp = buf[wib][pick];
+    a.idx[t] = r0 + pick;
+    a.wts[t] = 1.0 / sqrt((double)a.c * (mp / S));
+  }
+}
+
+}  // namespace tfk

@@ -1,0 +1,260 @@
+"""GPU parity of the LSAR hot path against the oracle (through the C ABI).
+
+Bars (BASELINE.json north_star): sampled rows / indices bit-exact in
+deterministic-index mode; residuals bit-exact given the same phi (same fma
+tap order); scores, residuals, phi and PACF within rel 1e-9; identical p*;
+RNG mode identical draws in practice and equal in distribution.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9  # relative fp64 tolerance of the north star
+
+
+@pytest.fixture(scope="module")
+def tf():
+    import paper_2112_12994_b200 as t
+    from paper_2112_12994_b200 import build
+    build.build()
+    return t
+
+
+@pytest.fixture(scope="module")
+def eng(tf):
+    e = tf.Engine(0)
+    yield e
+    e.close()
+
+
+def c1_like(n, seed=5, q=20):
+    from paper_2112_12994_b200 import gen
+    roots = gen.ar_roots(q, 1.2, 3.0, seed)
+    return gen.simulate_roots(roots, n, seed)
+
+
+def relerr(a, b):
+    a = np.asarray(a, float); b = np.asarray(b, float)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+# ------------------------------------------------------------------ residuals
+@pytest.mark.parametrize("n,p", [(5, 2), (6, 5), (3000, 1), (3000, 7), (3000, 8), (3000, 9),
+                                 (5000, 16), (4097, 33), (70000, 100), (9000, 250), (2049, 3)])
+def test_residuals_bit_exact(orc, eng, n, p):
+    y = c1_like(n, seed=n + p)
+    rng = np.random.default_rng(p)
+    phi = rng.standard_normal(p) / p
+    r_gpu = eng.residuals(y, n, p, phi)
+    r_ref = orc.residuals(y, n, p, phi)
+    assert r_gpu.shape == r_ref.shape
+    assert np.array_equal(r_gpu, r_ref)
+
+
+def test_residual_known_answers(eng):
+    y = [1.0, 2.0, 3.0, 4.0, 5.0]  # test_toeplitz.cpp:154-162
+    assert eng.residuals(y, 5, 2, [0.0, 0.0]).tolist() == [-3, -4, -5]
+    assert eng.residuals(y, 5, 2, [1.0, 0.0]).tolist() == [-1, -1, -1]
+
+
+def test_residual_errors(tf, eng):
+    with pytest.raises(tf.UsageError):
+        eng.residuals([1.0, 2.0, 3.0], 3, 2, [1.0])
+    with pytest.raises(tf.DataError):
+        eng.residuals([1.0, 2.0], 2, 2, [1.0, 1.0])
+
+
+# ------------------------------------------------------------------ gather
+def test_apply_sample_bit_exact(orc, eng, tf):
+    y = c1_like(20000, seed=3)
+    p = 37
+    rng = np.random.default_rng(1)
+    idx = rng.integers(0, y.size - p, size=3001)
+    w = rng.uniform(0.1, 3.0, size=idx.size)
+    a, b = eng.apply_sample(y, y.size, p, idx, w)
+    a_ref, b_ref = orc.apply_sample(y, y.size, p, idx, w)
+    assert np.array_equal(a, a_ref) and np.array_equal(b, b_ref)
+    # test_sketch.cpp:176-214 known answers and width restriction
+    a, b = eng.apply_sample([1, 2, 3, 4, 5], 5, 2, [1], [0.7])
+    assert np.allclose(a, [[2.1, 1.4]]) and np.allclose(b, [2.8])
+    a, b = eng.apply_sample([1, 2, 3, 4, 5], 5, 2, [1], [0.7], width=1)
+    assert a.shape == (1, 1) and a[0, 0] == 0.7 * 3.0
+    with pytest.raises(tf.UsageError):
+        eng.apply_sample([1, 2, 3, 4, 5], 5, 2, [3], [1.0])
+
+
+# ------------------------------------------------------------------ sampling
+def test_sample_rows_known_answers(eng, tf):
+    # test_sketch.cpp:128-156
+    n, c = 16, 8
+    idx, w = eng.sample_rows(np.full(n, 1.0 / n), c, 5)
+    assert np.allclose(w, math.sqrt(n / c), rtol=1e-15)
+    point = np.zeros(n); point[3] = 1.0
+    idx2, w2 = eng.sample_rows(point, 5, 6)
+    assert (idx2 == 3).all() and np.allclose(w2, 1 / math.sqrt(5), rtol=1e-15)
+    idx3, _ = eng.sample_rows(np.full(n, 1.0 / n), c, 5)
+    assert (idx3 == idx).all()
+    with pytest.raises(tf.DataError):
+        eng.sample_rows(np.array([0.5, -0.1]), 3, 1)
+    with pytest.raises(tf.UsageError):
+        eng.sample_rows(np.full(n, 1.0 / n), 0, 1)
+
+
+@pytest.mark.parametrize("n,c", [(16, 8), (5000, 2000), (100_003, 20_000), (2048 * 3 + 17, 5000)])
+def test_sample_rows_matches_oracle_draws(orc, eng, n, c):
+    rng = np.random.default_rng(n)
+    s = rng.exponential(size=n) ** 2
+    s[rng.integers(0, n, size=n // 10)] = 0.0  # zero-mass rows
+    pi = s / s.sum()
+    idx, w = eng.sample_rows(s, c, 1234)
+    idx_r, w_r = orc.sample_rows(pi, c, 1234)
+    agree = np.mean(idx == idx_r)
+    assert agree >= 0.999, agree
+    same = idx == idx_r
+    assert np.allclose(w[same], w_r[same], rtol=1e-12)
+    assert (s[idx] > 0).all()
+
+
+# ------------------------------------------------------------------ solve
+@pytest.mark.parametrize("p", [1, 2, 5, 31, 32, 33, 63, 64, 65, 100, 129])
+def test_solve_sampled_matches_oracle(orc, eng, p):
+    y = c1_like(60000, seed=p)
+    rng = np.random.default_rng(p)
+    c = max(4 * p, 600)
+    idx = rng.integers(0, y.size - p, size=c)
+    w = rng.uniform(0.5, 2.0, size=c)
+    phi, method = eng.solve_sampled(y, y.size, p, idx, w)
+    a, b = orc.apply_sample(y, y.size, p, idx, w)
+    ref, m, _ = orc.solve_exact(a, b)
+    assert m == 0 and method in (0, 2)
+    assert relerr(phi, ref) < TOL
+
+
+def test_solve_sampled_ill_conditioned_uses_shift(orc, eng):
+    # AR(50)-like series from the C2 generator: cond(X) ~ 1e7 breaks plain CholeskyQR
+    from paper_2112_12994_b200 import gen
+    y, _, _, _ = gen.make_config_series("C2", n=200000)
+    p = 60
+    rng = np.random.default_rng(9)
+    idx = rng.integers(0, y.size - p, size=5000)
+    w = np.ones(idx.size)
+    phi, method = eng.solve_sampled(y, y.size, p, idx, w)
+    a, b = orc.apply_sample(y, y.size, p, idx, w)
+    ref, _, _ = orc.solve_exact(a, b)
+    # residual optimality is the well-posed comparison at cond ~1e7
+    r_gpu = np.linalg.norm(a @ phi - b)
+    r_ref = np.linalg.norm(a @ ref - b)
+    assert r_gpu <= r_ref * (1 + 1e-9)
+    assert relerr(phi, ref) < 1e-5
+
+
+# ------------------------------------------------------------------ sweeps
+@pytest.mark.parametrize("n,q,p_bar,c", [(20000, 20, 30, 2000), (6000, 2, 8, 500),
+                                         (50000, 10, 64, 3000), (9000, 5, 40, 40)])
+def test_lsar_fixed_index_parity(orc, tf, eng, n, q, p_bar, c):
+    y = c1_like(n, seed=q + n, q=q)
+    ref = orc.lsar_fit(y, p_bar, c, 77)
+    fit = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, 77, engine=eng, fixed_idx=ref.idx,
+                      fixed_w=ref.w, want_diag=True)
+    d = fit.diag
+    assert np.array_equal(d["idx"], ref.idx)  # sampled indices bit-exact
+    assert relerr(fit.pacf.taus, ref.taus) < TOL
+    for p in range(p_bar):
+        assert relerr(fit.per_lag_coefficients[p], ref.coefs[p]) < TOL
+    assert relerr(d["scores"], ref.scores) < TOL
+    assert relerr(d["resid"], ref.resid) < TOL
+    assert relerr(d["rnorm2"], ref.rnorm2) < TOL
+    assert relerr(d["ssum"], ref.ssum) < TOL
+    assert fit.p_star == ref.p_star
+    assert abs(d["scores"].sum() - p_bar) < 1e-8  # telescoping (acceptance crit. 5)
+
+
+def test_lsar_rng_mode_matches_oracle_draws(orc, tf, eng):
+    y = c1_like(30000, seed=8)
+    p_bar, c = 25, 2500
+    ref = orc.lsar_fit(y, p_bar, c, 4242)
+    fit = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, 4242, engine=eng, want_diag=True)
+    # lag 1 samples from the same closed-form scores: draws agree
+    assert np.mean(fit.diag["idx"][0] == ref.idx[0]) >= 0.999
+    if np.array_equal(fit.diag["idx"], ref.idx):
+        assert relerr(fit.pacf.taus, ref.taus) < TOL
+        assert fit.p_star == ref.p_star
+
+
+def test_lsar_deterministic_and_seed_sensitive(tf, eng):
+    # test_lsar.cpp:171-197 (AR(2) partial recovery, replay determinism)
+    from oracle import oracle as orc
+    y = orc.simulate_ar([1.2, -0.36], 6000, 231)
+    s = tf.TimeSeries(y)
+    f = tf.lsar_fit(s, 8, 500, 77, engine=eng)
+    assert abs(f.pacf.taus[1] + 0.36) < 0.2 and f.p_star >= 2
+    assert f.coefficients.size == f.p_star
+    assert [c.size for c in f.per_lag_coefficients] == list(range(1, 9))
+    g = tf.lsar_fit(s, 8, 500, 77, engine=eng)
+    assert g.pacf.taus == f.pacf.taus and np.array_equal(g.coefficients, f.coefficients)
+    h = tf.lsar_fit(s, 8, 500, 78, engine=eng)
+    assert h.pacf.taus != f.pacf.taus
+    assert all(t > 0 for t in f.per_lag_seconds)
+
+
+def test_lsar_distribution_over_seeds(orc, tf, eng):
+    """RNG mode: per-lag tau estimates agree with the oracle's in distribution."""
+    y = c1_like(20000, seed=21, q=6)
+    p_bar, c = 10, 400
+    s = tf.TimeSeries(y)
+    g = np.array([tf.lsar_fit(s, p_bar, c, 1000 + k, engine=eng).pacf.taus for k in range(24)])
+    r = np.array([orc.lsar_fit(y, p_bar, c, 5000 + k).taus for k in range(24)])
+    se = np.sqrt(g.var(0) / 24 + r.var(0) / 24) + 1e-12
+    z = np.abs(g.mean(0) - r.mean(0)) / se
+    assert (z < 4.5).all(), z
+
+
+def test_lsar_errors(orc, tf, eng):
+    # test_lsar.cpp:160-169, 199-205
+    geo = tf.TimeSeries(0.5 ** np.arange(60))
+    with pytest.raises(tf.NumericalError):
+        tf.lsar_fit(geo, 3, 20, 1, engine=eng)
+    y = tf.TimeSeries(orc.simulate_ar(orc.random_stationary_ar(1, 241), 50, 242))
+    with pytest.raises(tf.UsageError):
+        tf.lsar_fit(y, 10, 5, 1, engine=eng)
+    with pytest.raises(tf.DataError):
+        tf.lsar_fit(y, 49, 100, 1, engine=eng)
+    with pytest.raises(tf.UsageError):
+        tf.lsar_fit(y, 0, 100, 1, engine=eng)
+    with pytest.raises(tf.NumericalError):
+        tf.lsar_fit(tf.TimeSeries(np.zeros(100)), 3, 20, 1, engine=eng)
+
+
+def test_run_fit_report(tf, eng):
+    from oracle import oracle as orc
+    y = tf.TimeSeries(orc.simulate_ar([0.6], 3000, 91))
+    r = tf.run_fit(y, "lsar", 4, 300, 5, with_timing=False, engine=eng)
+    assert r.per_lag_seconds == [0.0] * 4 and r.cumulative_seconds == [0.0] * 4
+    r2 = tf.run_fit(y, "lsar", 4, 300, 5, with_timing=False, engine=eng)
+    assert tf.report_to_json(r) == tf.report_to_json(r2)  # --no-timing byte stability
+
+
+# ------------------------------------------------------------------ full-size properties
+@pytest.mark.slow
+def test_lsar_c2_full_size_properties(orc, tf, eng):
+    """BASELINE C2 size (n=1e7, p_bar=200, c=1e4): size-independent properties --
+    scores telescope to p, residuals of the returned phi recomputed on CPU
+    (bit-exact per window), ||r||^2 consistent."""
+    from paper_2112_12994_b200 import gen
+    y, _, p_bar, _ = gen.make_config_series("C2")
+    c = 10_000
+    fit = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, 99, engine=eng, want_diag=True)
+    d = fit.diag
+    w = y.size - p_bar
+    assert abs(d["scores"].sum() - p_bar) < 1e-6 * p_bar
+    assert (d["scores"] >= 0).all()
+    phi = fit.per_lag_coefficients[-1]
+    for i0 in (0, w // 3, w - 5000):
+        seg = y[i0:i0 + 5000 + p_bar]
+        r = orc.residuals(seg, seg.size, p_bar, phi)
+        assert np.array_equal(r, d["resid"][i0:i0 + 5000])
+    assert relerr(d["rnorm2"][-1], float(np.dot(d["resid"], d["resid"]))) < 1e-10
+    assert (d["idx"] >= 0).all() and (d["idx"] < w).all()
