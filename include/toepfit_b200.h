@@ -68,6 +68,8 @@ typedef struct {
   double* scores_out;       /* [n - p_bar] scores of the last lag */
   double* resid_out;        /* [n - p_bar] residuals of the last lag */
   int* method_out;          /* [p_bar] 0 CholeskyQR2, 2 shifted CholeskyQR3 */
+  double* phase_seconds;    /* [p_bar][3] device time of sampling, solve, fused pass */
+  int64_t* launches_out;    /* kernel launches issued by the sweep */
 } tf_lsar_diag;
 
 typedef struct {
@@ -123,6 +125,9 @@ tf_status tf_solve_sampled(tf_context* ctx, const double* y, int64_t n_used, int
                            int* method_out);
 
 int tf_select_order(const double* taus, int p_bar, double bound);
+/* Diagnostics: measured fp64 FMA throughput of this device (TFLOP/s) from a
+ * DFMA microbenchmark, the denominator of the fp64 roofline. */
+tf_status tf_probe_fp64_peak(tf_context* ctx, double* tflops);
 uint64_t tf_derive_seed(uint64_t seed, uint64_t tag);
 
 #ifdef __cplusplus

@@ -31,7 +31,8 @@ class TfRhCfg(C.Structure):
 class TfLsarDiag(C.Structure):
     _fields_ = [("fixed_idx", _i64p), ("fixed_w", _f64p), ("idx_out", _i64p), ("w_out", _f64p),
                 ("rnorm2_out", _f64p), ("ssum_out", _f64p), ("scores_out", _f64p),
-                ("resid_out", _f64p), ("method_out", _i32p)]
+                ("resid_out", _f64p), ("method_out", _i32p), ("phase_seconds", _f64p),
+                ("launches_out", _i64p)]
 
 
 class TfRhDiag(C.Structure):
@@ -44,6 +45,7 @@ EXPORTS = [
     "tf_version", "tf_create", "tf_destroy", "tf_last_error", "tf_upload_series",
     "tf_upload_series_device", "tf_lsar_sweep", "tf_rh_sweep", "tf_residuals", "tf_sample_rows",
     "tf_apply_sample", "tf_solve_sampled", "tf_select_order", "tf_derive_seed",
+    "tf_probe_fp64_peak",
 ]
 
 _lib = None
@@ -79,6 +81,7 @@ def lib():
     L.tf_select_order.restype = C.c_int
     L.tf_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
     L.tf_derive_seed.restype = C.c_uint64
+    L.tf_probe_fp64_peak.argtypes = [C.c_void_p, _f64p]
     for name in EXPORTS:
         if not hasattr(L, name):
             raise RuntimeError(f"{LIB_PATH} does not export {name}")

@@ -179,7 +179,8 @@ class Engine:
             w = max(int(n) - pb, 1)
             diag = dict(idx=np.zeros((pb, c), np.int64), w=np.zeros((pb, c)), rnorm2=np.zeros(pb),
                         ssum=np.zeros(pb), scores=np.zeros(w), resid=np.zeros(w),
-                        method=np.zeros(pb, np.int32))
+                        method=np.zeros(pb, np.int32), phases=np.zeros((pb, 3)),
+                        launches=np.zeros(1, np.int64))
             d.idx_out = ptr(diag["idx"], _abi._i64p)
             d.w_out = ptr(diag["w"])
             d.rnorm2_out = ptr(diag["rnorm2"])
@@ -187,6 +188,8 @@ class Engine:
             d.scores_out = ptr(diag["scores"])
             d.resid_out = ptr(diag["resid"])
             d.method_out = ptr(diag["method"], _abi._i32p)
+            d.phase_seconds = ptr(diag["phases"])
+            d.launches_out = ptr(diag["launches"], _abi._i64p)
         self._check(_abi.lib().tf_lsar_sweep(self._ctx, int(p_bar), int(c), C.c_uint64(seed),
                                              C.byref(d), ptr(taus), ptr(coefs), ptr(secs),
                                              C.byref(pstar)))
@@ -230,6 +233,11 @@ class Engine:
         if diag is not None:
             diag["depth"] = depth.value
         return taus, coefs, secs, up.value, pstar.value, diag
+
+    def probe_fp64_peak(self) -> float:
+        v = C.c_double(0)
+        self._check(_abi.lib().tf_probe_fp64_peak(self._ctx, C.byref(v)))
+        return v.value
 
     # ------------------------------------------------------------ single ops
     def residuals(self, y, n_used: int, p: int, phi) -> np.ndarray:

@@ -14,6 +14,7 @@
 
 #include "engine.h"
 #include "k_chol.cuh"
+#include "k_cholinv.cuh"
 #include "k_gram.cuh"
 #include "k_pass.cuh"
 #include "k_sample.cuh"
@@ -27,6 +28,8 @@ static void cuda_check(cudaError_t e, const char* what) {
 }
 #define CK(x) cuda_check((x), #x)
 #define LAUNCH_CHECK(name) cuda_check(cudaGetLastError(), name)
+static thread_local int64_t g_launches = 0;
+#define COUNT_LAUNCH() (++g_launches)
 
 template <class T>
 void DBuf<T>::need(size_t count) {
@@ -107,23 +110,13 @@ static void launch_trinv(const double* Rrow, int K, int perm, double* out, const
     default: launch_trinv_s<32>(Rrow, K, perm, out, gate, st); break;
   }
   LAUNCH_CHECK("k_trinv");
-}
-
-template <int S>
-static void launch_phi_s(const PhiArgs& a, cudaStream_t st) {
-  k_phi<S><<<1, kPhiThreads, sizeof(double) * 3 * a.K, st>>>(a);
+  COUNT_LAUNCH();
 }
 
 static void launch_phi(const PhiArgs& a, cudaStream_t st) {
-  switch (trinv_slots(a.K)) {
-    case 1: launch_phi_s<1>(a, st); break;
-    case 2: launch_phi_s<2>(a, st); break;
-    case 4: launch_phi_s<4>(a, st); break;
-    case 8: launch_phi_s<8>(a, st); break;
-    case 16: launch_phi_s<16>(a, st); break;
-    default: launch_phi_s<32>(a, st); break;
-  }
+  k_phi<<<1, kPhiThreads, sizeof(double) * 2 * a.K, st>>>(a);
   LAUNCH_CHECK("k_phi");
+  COUNT_LAUNCH();
 }
 
 struct GramPlan {
@@ -137,7 +130,7 @@ static GramPlan gram_plan(int64_t rows, int K, int sm_count) {
   g.npair = g.nblk * (g.nblk + 1) / 2;
   const int64_t target = 2LL * sm_count;
   int64_t ns = (target + g.npair - 1) / g.npair;
-  ns = std::max<int64_t>(1, std::min<int64_t>(ns, (rows + 63) / 64));
+  ns = std::max<int64_t>(1, std::min<int64_t>(ns, (rows + 255) / 256));  // >= 8 k-blocks per CTA
   int64_t rps = (rows + ns - 1) / ns;
   rps = (rps + 31) / 32 * 32;
   g.rps = std::max<int64_t>(rps, 32);
@@ -151,12 +144,10 @@ static void gram(tf_context* ctx, const L& ld, int64_t rows, int K, double* G, c
   const GramPlan g = gram_plan(rows, K, ctx->sm_count);
   ctx->sb.W.need((size_t)g.nsplit * g.npair * 4096);
   dim3 grid(g.npair, g.nsplit);
-  k_gram<L><<<grid, kGramThreads, 0, ctx->stream>>>(ld, rows, K, g.nblk, g.rps, ctx->sb.W.get(), gate);
+  k_gram<L><<<grid, kGramThreads, 0, ctx->stream>>>(ld, rows, K, g.nblk, g.rps, ctx->sb.W.get(), G,
+                                                    ctx->sb.tickets.get(), gate);
   LAUNCH_CHECK("k_gram");
-  const int64_t tot = (int64_t)g.npair * 4096;
-  k_gram_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, ctx->stream>>>(ctx->sb.W.get(), g.nsplit, g.npair,
-                                                                       g.nblk, K, G, gate);
-  LAUNCH_CHECK("k_gram_reduce");
+  COUNT_LAUNCH();
 }
 
 template <class L>
@@ -165,6 +156,7 @@ static void qform(tf_context* ctx, const L& ld, int64_t rows, int K, const doubl
   dim3 grid((unsigned)((rows + 63) / 64), (unsigned)((K + 63) / 64));
   k_qform<L><<<grid, kGramThreads, 0, ctx->stream>>>(ld, rows, K, Rg, Q, K, gate);
   LAUNCH_CHECK("k_qform");
+  COUNT_LAUNCH();
 }
 
 static void chol(tf_context* ctx, const double* G, int K, int perm, int iter, int64_t rows,
@@ -190,6 +182,7 @@ static void chol(tf_context* ctx, const double* G, int K, int perm, int iter, in
   }
   k_chol<<<1, kCholThreads, smem, ctx->stream>>>(a);
   LAUNCH_CHECK("k_chol");
+  COUNT_LAUNCH();
 }
 
 // Size every solve buffer for the largest system of a sweep up front so that
@@ -204,6 +197,7 @@ static void reserve_solve(tf_context* ctx, int64_t c, int Kmax) {
   b.R3row.need(tri);
   b.Rg1.need(KK);
   b.Rinv2.need(KK);
+  b.Rinv3.need(KK);
   b.Q1.need((size_t)c * Kmax);
   b.Q2.need((size_t)c * Kmax);
   b.flags.need(4);
@@ -213,7 +207,43 @@ static void reserve_solve(tf_context* ctx, int64_t c, int Kmax) {
     wmax = std::max(wmax, (size_t)g.nsplit * g.npair * 4096);
   }
   b.W.need(wmax);
+  if (b.tickets.n < 4096) {
+    b.tickets.need(4096);
+    CK(cudaMemset(b.tickets.get(), 0, 4096 * sizeof(int)));
+  }
   if (!chol_fits_smem(Kmax)) b.ws.need(tri);
+}
+
+// One CholeskyQR iteration's small factorization: G -> Rinv (dense).
+static void factor_inverse(tf_context* ctx, const double* G, int K, int perm, int iter, int64_t rows,
+                           double* Rinv, int lag, int* status) {
+  if (K <= kCholinvMaxK) {
+    CholinvArgs a;
+    a.G = G;
+    a.K = K;
+    a.perm_in = perm;
+    a.perm_out = perm;
+    a.iter = iter;
+    a.nrows = rows;
+    a.Rinv = Rinv;
+    a.flags = ctx->sb.flags.get();
+    a.status = status;
+    a.lag = lag;
+    const size_t smem = cholinv_smem_bytes(K);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+      CK(cudaFuncSetAttribute(k_cholinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    k_cholinv<<<1, kCholinvThreads, smem, ctx->stream>>>(a);
+    LAUNCH_CHECK("k_cholinv");
+    COUNT_LAUNCH();
+  } else {
+    // large-K path: packed factorization in global memory + warp-per-column inverse
+    chol(ctx, G, K, perm, iter, rows, ctx->sb.R1row.get(), lag, status);
+    launch_trinv(ctx->sb.R1row.get(), K, perm, Rinv, iter == 3 ? ctx->sb.flags.get() : nullptr,
+                 ctx->stream);
+  }
 }
 
 template <class L>
@@ -223,10 +253,9 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
   int* shifted = b.flags.get();
   PhiArgs pa;
   pa.K = K;
-  pa.R2row = b.R2row.get();
-  pa.R3row = b.R3row.get();
   pa.Rg1 = b.Rg1.get();
   pa.Rinv2 = b.Rinv2.get();
+  pa.Rinv3 = b.Rinv3.get();
   pa.flags = b.flags.get();
   pa.phi = o.phi;
   pa.coefs = o.coefs;
@@ -238,23 +267,22 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
     gram(ctx, ld, c, K, b.G.get(), nullptr);
     k_solve_k2<<<1, 1, 0, ctx->stream>>>(b.G.get(), pa);
     LAUNCH_CHECK("k_solve_k2");
+    COUNT_LAUNCH();
     return;
   }
-  // iteration 1: G1 = A^T A (gathered), R1, Rinv1 (rows permuted to gathered order)
+  // iteration 1: G1 = A^T A (gathered order), Rinv_1 with rows in gathered order
   gram(ctx, ld, c, K, b.G.get(), nullptr);
-  chol(ctx, b.G.get(), K, 1, 1, c, b.R1row.get(), o.lag, o.status);
-  launch_trinv(b.R1row.get(), K, 1, b.Rg1.get(), nullptr, ctx->stream);
+  factor_inverse(ctx, b.G.get(), K, 1, 1, c, b.Rg1.get(), o.lag, o.status);
   qform(ctx, ld, c, K, b.Rg1.get(), b.Q1.get(), nullptr);
   // iteration 2: G2 = Q1^T Q1
   DenseRows q1{b.Q1.get(), K};
   gram(ctx, q1, c, K, b.G.get(), nullptr);
-  chol(ctx, b.G.get(), K, 0, 2, c, b.R2row.get(), o.lag, o.status);
+  factor_inverse(ctx, b.G.get(), K, 0, 2, c, b.Rinv2.get(), o.lag, o.status);
   // iteration 3 (only when iteration 1 needed the shift)
-  launch_trinv(b.R2row.get(), K, 0, b.Rinv2.get(), shifted, ctx->stream);
   qform(ctx, q1, c, K, b.Rinv2.get(), b.Q2.get(), shifted);
   DenseRows q2{b.Q2.get(), K};
   gram(ctx, q2, c, K, b.G.get(), shifted);
-  chol(ctx, b.G.get(), K, 0, 3, c, b.R3row.get(), o.lag, o.status);
+  factor_inverse(ctx, b.G.get(), K, 0, 3, c, b.Rinv3.get(), o.lag, o.status);
   launch_phi(pa, ctx->stream);
 }
 
@@ -281,6 +309,7 @@ static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, co
   }
   k_lsar_pass<<<(unsigned)ntile, kPassThreads, smem, ctx->stream>>>(a);
   LAUNCH_CHECK("k_lsar_pass");
+  COUNT_LAUNCH();
 }
 
 static void launch_scan(tf_context* ctx, int64_t ntile, int lag, int check_r, int unit_r = 0) {
@@ -289,6 +318,7 @@ static void launch_scan(tf_context* ctx, int64_t ntile, int lag, int check_r, in
                                                   ctx->Shist.get(), lag, check_r, ctx->status.get(),
                                                   unit_r);
   LAUNCH_CHECK("k_lag_scan");
+  COUNT_LAUNCH();
 }
 
 static void launch_draw(tf_context* ctx, uint64_t seed, int64_t c, int64_t w, int64_t* idx,
@@ -311,6 +341,7 @@ static void launch_draw(tf_context* ctx, uint64_t seed, int64_t c, int64_t w, in
   const int per = kDrawThreads / 32;
   k_draw<<<(unsigned)((c + per - 1) / per), kDrawThreads, 0, ctx->stream>>>(a);
   LAUNCH_CHECK("k_draw");
+  COUNT_LAUNCH();
 }
 
 static void alloc_state(tf_context* ctx, int p_bar, int64_t c, int64_t w) {
@@ -380,6 +411,13 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
   }
   reserve_solve(ctx, c, p_bar + 1);
   ensure_events(ctx, p_bar + 1);
+  const bool phases = d && d->phase_seconds;
+  while (phases && ctx->pev.size() < 2 * (size_t)p_bar) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ctx->pev.push_back(e);
+  }
+  const int64_t launches0 = g_launches;
   CK(cudaEventRecord(ctx->events[0], st));
   // lag-0 pass: r_0 = -y[0..w), s_0 = 0  ->  s_1 = y^2 / sum y^2 (lsar.cpp:11-15)
   launch_pass(ctx, 0, w, ctx->phi.get(), ctx->scal.get());
@@ -400,6 +438,7 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
       CK(cudaMemcpyAsync(ctx->w_hist.get() + (size_t)(p - 1) * c, wts, c * sizeof(double),
                          cudaMemcpyDeviceToDevice, st));
     }
+    if (phases) CK(cudaEventRecord(ctx->pev[2 * (p - 1)], st));
     SolveOut o;
     o.phi = ctx->phi.get();
     o.coefs = ctx->coefs.get();
@@ -410,10 +449,12 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
     o.status = ctx->status.get();
     GatherRows ld{ctx->y.get(), idx, wts, (int64_t)p};
     solve_rows(ctx, ld, c, p + 1, o);
+    if (phases) CK(cudaEventRecord(ctx->pev[2 * (p - 1) + 1], st));
     // residuals of the lag-p window fit + score update s_p = s_{p-1} + r_{p-1}^2/R_{p-1}
     launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());
     CK(cudaEventRecord(ctx->events[p], st));
   }
+  const int64_t launches = g_launches - launches0;
   if (d && d->rnorm2_out) launch_scan(ctx, ntile, p_bar, 0);  // R_{p_bar} for the diagnostics
   CK(cudaStreamSynchronize(st));
   int sth[3];
@@ -444,6 +485,17 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
     if (d->scores_out) CK(cudaMemcpy(d->scores_out, ctx->s.get(), sizeof(double) * w, cudaMemcpyDeviceToHost));
     if (d->resid_out) CK(cudaMemcpy(d->resid_out, ctx->r.get(), sizeof(double) * w, cudaMemcpyDeviceToHost));
     if (d->method_out) CK(cudaMemcpy(d->method_out, ctx->method.get(), sizeof(int) * p_bar, cudaMemcpyDeviceToHost));
+    if (d->launches_out) *d->launches_out = launches;
+    if (phases)
+      for (int p = 1; p <= p_bar; ++p) {
+        float a = 0.f, b = 0.f, cc = 0.f;
+        CK(cudaEventElapsedTime(&a, ctx->events[p - 1], ctx->pev[2 * (p - 1)]));
+        CK(cudaEventElapsedTime(&b, ctx->pev[2 * (p - 1)], ctx->pev[2 * (p - 1) + 1]));
+        CK(cudaEventElapsedTime(&cc, ctx->pev[2 * (p - 1) + 1], ctx->events[p]));
+        d->phase_seconds[3 * (p - 1) + 0] = a * 1e-3;
+        d->phase_seconds[3 * (p - 1) + 1] = b * 1e-3;
+        d->phase_seconds[3 * (p - 1) + 2] = cc * 1e-3;
+      }
   }
 }
 
@@ -547,6 +599,7 @@ static void sample_op(tf_context* ctx, const double* scores, int64_t n, int64_t 
                                                                ctx->chunkA.get(), ctx->chunkB.get(),
                                                                ctx->tileA.get(), ctx->tileB.get());
   LAUNCH_CHECK("k_partials");
+  COUNT_LAUNCH();
   launch_scan(ctx, ntile, 0, 0, /*unit_r=*/1);  // no residual term: mass = s + 0 / 1
   launch_draw(ctx, seed, c, n, ctx->idx.get(), ctx->wts.get());
   CK(cudaMemcpyAsync(idx_out, ctx->idx.get(), c * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
@@ -586,6 +639,7 @@ static void apply_sample_op(tf_context* ctx, const double* y, int64_t n_used, in
   dim3 blk(32, 8);
   k_materialize<<<(unsigned)((c + 7) / 8), blk, 0, ctx->stream>>>(ld, c, width, A.get(), B.get());
   LAUNCH_CHECK("k_materialize");
+  COUNT_LAUNCH();
   CK(cudaMemcpyAsync(a_out, A.get(), sizeof(double) * c * width, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(b_out, B.get(), sizeof(double) * c, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -618,6 +672,42 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
                      const tf_rh_diag* d, double* taus, double* coefs, double* lag_seconds,
                      double* upfront_seconds, int* p_star) {
   throw TfError{TF_USAGE, "rh sweep not built yet"};
+}
+
+__global__ void __launch_bounds__(256) k_dfma_probe(double* out, int iters, double seed) {
+  double a0 = seed + threadIdx.x, a1 = a0 * 0.5, a2 = a0 * 0.25, a3 = a0 * 0.125;
+  double a4 = a0 + 1, a5 = a1 + 1, a6 = a2 + 1, a7 = a3 + 1;
+  const double m = 0.999999999, c = 1e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+      a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+    }
+  }
+  const double r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+  if (r == 12345.678) out[threadIdx.x] = r;
+}
+
+static double probe_fp64(tf_context* ctx) {
+  DBuf<double> out;
+  out.need(256);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const int blocks = ctx->sm_count * 8, iters = 4096;
+  k_dfma_probe<<<blocks, 256, 0, ctx->stream>>>(out.get(), 64, 1.0);  // warm-up
+  CK(cudaEventRecord(e0, ctx->stream));
+  k_dfma_probe<<<blocks, 256, 0, ctx->stream>>>(out.get(), iters, 1.0);
+  CK(cudaEventRecord(e1, ctx->stream));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  out.release();
+  const double flops = 2.0 * 8 * 16 * (double)iters * 256 * blocks;
+  return flops / (ms * 1e-3) / 1e12;
 }
 
 }  // namespace tfe
@@ -679,7 +769,7 @@ void tf_destroy(tf_context* ctx) {
   ctx->method.release();
   tfe::SolveBufs& b = ctx->sb;
   b.W.release(); b.G.release(); b.R1row.release(); b.R2row.release(); b.R3row.release();
-  b.Rg1.release(); b.Rinv2.release(); b.Q1.release(); b.Q2.release(); b.ws.release(); b.flags.release();
+  b.Rg1.release(); b.Rinv2.release(); b.Rinv3.release(); b.Q1.release(); b.Q2.release(); b.ws.release(); b.flags.release(); b.tickets.release();
   ctx->rh_scores.release(); ctx->rh_approx.release(); ctx->rh_approx2.release(); ctx->rh_M.release();
   ctx->rh_G.release(); ctx->rh_lvl.release(); ctx->rh_tmp.release(); ctx->rh_picked.release();
   ctx->rh_keys.release(); ctx->rh_keys2.release(); ctx->rh_cub.release();
@@ -757,5 +847,13 @@ int tf_select_order(const double* taus, int p_bar, double bound) {
 }
 
 uint64_t tf_derive_seed(uint64_t seed, uint64_t tag) { return tfk::derive_seed(seed, tag); }
+
+tf_status tf_probe_fp64_peak(tf_context* ctx, double* tflops) {
+  if (!ctx || !tflops) return TF_USAGE;
+  return guarded(ctx, [&] {
+    cudaSetDevice(ctx->device);
+    *tflops = tfe::probe_fp64(ctx);
+  });
+}
 
 }  // extern "C"

@@ -27,8 +27,8 @@ struct DBuf {
 };
 
 struct SolveBufs {
-  DBuf<double> W, G, R1row, R2row, R3row, Rg1, Rinv2, Q1, Q2, ws;
-  DBuf<int> flags;
+  DBuf<double> W, G, R1row, R2row, R3row, Rg1, Rinv2, Rinv3, Q1, Q2, ws;
+  DBuf<int> flags, tickets;
 };
 
 }  // namespace tfe
@@ -53,4 +53,6 @@ struct tf_context {
   tfe::DBuf<uint64_t> rh_keys, rh_keys2;
   tfe::DBuf<unsigned char> rh_cub;
   std::vector<cudaEvent_t> events;
+  std::vector<cudaEvent_t> pev;  // phase events (2 per lag)
+  int64_t launches = 0;
 };

@@ -63,6 +63,12 @@ __global__ void __launch_bounds__(kCholThreads) k_chol(CholArgs a) {
   double* Dv = a.use_smem ? smem + tri : smem;
   double shift = 0.0;
   int shifted = 0;
+  double trace = 0.0;
+  for (int i = 0; i < K; ++i) {
+    const int gi = a.perm ? gperm(i, K) : i;
+    trace += a.G[(size_t)gi * K + gi];
+  }
+  const double pivot_floor = 4.930380657631324e-32 * trace;
   for (int attempt = 0; attempt < 2; ++attempt) {
     for (int j = warp; j < K; j += 32)
       for (int i = lane; i <= j; i += 32) {
@@ -80,7 +86,8 @@ __global__ void __launch_bounds__(kCholThreads) k_chol(CholArgs a) {
         for (int i = 0; i < m; ++i) {
           double d = 0.0;
           if (lane == i) {
-            const double g = A[pcol(b0 + i, b0 + i)];
+            double g = A[pcol(b0 + i, b0 + i)];
+            if (b0 + i == K - 1 && !(g > pivot_floor)) g = pivot_floor;  // see k_cholinv.cuh
             if (!(g > 0.0) || !isfinite(g)) s_bad = 1;
             d = sqrt(fmax(g, 0.0));
             A[pcol(b0 + i, b0 + i)] = d;
@@ -145,12 +152,7 @@ __global__ void __launch_bounds__(kCholThreads) k_chol(CholArgs a) {
     if (!s_bad) break;
     if (a.iter == 1 && !shifted) {
       // shifted CholeskyQR restart (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020)
-      double tr = 0.0;
-      for (int i = 0; i < K; ++i) {
-        const int gi = a.perm ? gperm(i, K) : i;
-        tr += a.G[(size_t)gi * K + gi];
-      }
-      shift = 11.0 * ((double)a.nrows * K + (double)K * (K + 1)) * 2.220446049250313e-16 * tr;
+      shift = 11.0 * ((double)a.nrows * K + (double)K * (K + 1)) * 2.220446049250313e-16 * trace;
       shifted = 1;
       __syncthreads();
       continue;
@@ -210,10 +212,9 @@ __global__ void __launch_bounds__(kTrinvWarps * 32)
 // ---------------------------------------------------------------------------
 struct PhiArgs {
   int K;                 // p + 1
-  const double* R2row;   // packed row-major R of iteration 2
-  const double* R3row;   // packed row-major R of iteration 3 (used when shifted)
   const double* Rg1;     // dense Rinv_1, rows in gathered order
-  const double* Rinv2;   // dense Rinv_2 (aug order), valid when shifted
+  const double* Rinv2;   // dense Rinv_2 (aug order)
+  const double* Rinv3;   // dense Rinv_3 (aug order), valid when shifted
   const int* flags;
   double* phi;           // out: length p
   double* coefs;         // packed coefficient array (nullable)
@@ -225,49 +226,22 @@ struct PhiArgs {
 
 constexpr int kPhiThreads = 1024;
 
-template <int SLOTS>
+// phi = R_A^-1 z for R = R_n ... R_1 (see file header)
 __global__ void __launch_bounds__(kPhiThreads) k_phi(PhiArgs a) {
-  extern __shared__ double sm[];  // x[K], v[K], u[K]
+  extern __shared__ double sm[];  // v[K], u[K]
   const int K = a.K, p = K - 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* x = sm;
-  double* v = sm + K;
-  double* u = sm + 2 * K;
+  double* v = sm;
+  double* u = sm + K;
   if (a.flags[1]) {
     for (int q = tid; q < p; q += kPhiThreads) a.phi[q] = __longlong_as_double(0x7ff8000000000000ll);
     return;
   }
   const int shifted = a.flags[0];
-  const double* Rn = shifted ? a.R3row : a.R2row;
-  // x = Rinv_n[:, p] by one warp
-  if (warp == 0) {
-    double xs[SLOTS];
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) xs[s] = 0.0;
-    for (int r = p; r >= 0; --r) {
-      const double* Rr = Rn + prow_off(r, K) - r;
-      double part = 0.0;
-#pragma unroll
-      for (int s = 0; s < SLOTS; ++s) {
-        const int q = lane + 32 * s;
-        if (q > r && q <= p) part = fma(Rr[q], xs[s], part);
-      }
-      const double sum = warp_sum(part);
-      const double xr = ((r == p ? 1.0 : 0.0) - sum) / Rr[r];
-#pragma unroll
-      for (int s = 0; s < SLOTS; ++s)
-        if (lane + 32 * s == r) xs[s] = xr;
-    }
-#pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      const int q = lane + 32 * s;
-      if (q < K) x[q] = xs[s];
-    }
-  }
+  const double* Rn = shifted ? a.Rinv3 : a.Rinv2;
+  const double xp = Rn[(size_t)p * K + p];
+  for (int q = tid; q < p; q += kPhiThreads) v[q] = -Rn[(size_t)q * K + p] / xp;
   __syncthreads();
-  for (int q = tid; q < p; q += kPhiThreads) v[q] = -x[q] / x[p];
-  __syncthreads();
-  // v_i = (Rinv_i[:p,:p] v - Rinv_i[:p,p]) / Rinv_i[p,p], i = n-1 .. 1
   for (int it = shifted ? 2 : 1; it >= 1; --it) {
     for (int q = warp; q < p; q += kPhiThreads / 32) {
       const double* row = it == 1 ? a.Rg1 + (size_t)gperm(q, K) * K : a.Rinv2 + (size_t)q * K;

@@ -12,8 +12,8 @@
 //
 //   k_gram   : split-K partial Gram tiles (64x64 upper block pairs) from rows
 //              [split * rps, (split+1) * rps); 4 warps, 32x32 per warp,
-//              16 DMMA per k4-step.  Deterministic: partials are reduced in
-//              a fixed order by k_gram_reduce.
+//              16 DMMA per k4-step.  Deterministic: the last CTA of a tile
+//              pair reduces the split partials in split order.
 //   k_qform  : Q = A * Rg for a dense K x K right factor (structural zeros
 //              above row l+1 skipped), used for CholeskyQR's Q = A R^-1.
 #pragma once
@@ -53,10 +53,13 @@ __device__ __forceinline__ void pair_from_index(int pair, int nblk, int& jb, int
   lb = jb + rem;
 }
 
+// Split-K partial tiles go to W; the last CTA of each tile pair (arrival
+// counted with an atomic ticket) sums the partials in split order and writes
+// G -- deterministic, and no separate reduction launch.
 template <class L>
 __global__ void __launch_bounds__(kGramThreads)
     k_gram(L ld, int64_t rows, int K, int nblk, int64_t rows_per_split, double* __restrict__ W,
-           const int* skip_flag) {
+           double* __restrict__ G, int* __restrict__ tickets, const int* skip_flag) {
   if (skip_flag && *skip_flag == 0) return;
   __shared__ __align__(16) double SJ[32][kSJ];
   __shared__ __align__(16) double SL[32][kSJ];
@@ -114,22 +117,41 @@ __global__ void __launch_bounds__(kGramThreads)
       const int col = 32 * wn + 8 * j + 2 * (lane & 3);
       *reinterpret_cast<double2*>(out + row * 64 + col) = make_double2(acc[i][j][0], acc[i][j][1]);
     }
-}
-
-// G[row * K + col] (row-major, upper blocks valid; diagonal blocks full)
-__global__ void k_gram_reduce(const double* __restrict__ W, int nsplit, int npair, int nblk, int K,
-                              double* __restrict__ G, const int* skip_flag) {
-  if (skip_flag && *skip_flag == 0) return;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)npair * 4096) return;
-  const int pair = (int)(e >> 12), el = (int)(e & 4095);
-  int jb, lb;
-  pair_from_index(pair, nblk, jb, lb);
-  const int row = jb * 64 + (el >> 6), col = lb * 64 + (el & 63);
-  if (row >= K || col >= K) return;
-  double s = 0.0;
-  for (int sp = 0; sp < nsplit; ++sp) s += W[((size_t)sp * npair + pair) * 4096 + el];
-  G[(size_t)row * K + col] = s;
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const int prev = atomicAdd(tickets + blockIdx.x, 1);
+    s_last = prev == (int)gridDim.y - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int nsplit = gridDim.y;
+  // valid elements only; partials summed in split order, 8 elements in flight per thread
+  const double* wp = W + (size_t)blockIdx.x * 4096;
+  const size_t sstride = (size_t)gridDim.x * 4096;
+  const int nr = min(64, K - J0), nc = min(64, K - L0);
+  const int nvalid = nr * nc;
+  for (int e0 = tid; e0 < nvalid; e0 += 8 * kGramThreads) {
+    double s[8];
+    int el[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * kGramThreads;
+      s[u] = 0.0;
+      el[u] = e < nvalid ? (e / nc) * 64 + (e % nc) : -1;
+    }
+    for (int sp = 0; sp < nsplit; ++sp) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (el[u] >= 0) s[u] += __ldcg(wp + sp * sstride + el[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (el[u] >= 0) G[(size_t)(J0 + (el[u] >> 6)) * K + L0 + (el[u] & 63)] = s[u];
+  }
+  if (tid == 0) tickets[blockIdx.x] = 0;
 }
 
 constexpr int kQA = 36;

@@ -119,7 +119,7 @@ def test_sample_rows_matches_oracle_draws(orc, eng, n, c):
 
 
 # ------------------------------------------------------------------ solve
-@pytest.mark.parametrize("p", [1, 2, 5, 31, 32, 33, 63, 64, 65, 100, 129])
+@pytest.mark.parametrize("p", [1, 2, 5, 31, 32, 33, 63, 64, 65, 100, 129, 200, 216, 217, 230, 300])
 def test_solve_sampled_matches_oracle(orc, eng, p):
     y = c1_like(60000, seed=p)
     rng = np.random.default_rng(p)

@@ -1,0 +1,44 @@
+// Standalone timing harness for k_cholinv (development tool).
+#define CI_TIMING 1
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <cmath>
+__device__ long long g_ci_clk[256];
+#define CI_STAMP(k) do { if (threadIdx.x == 0) g_ci_clk[(k)] = clock64(); } while (0)
+#include "../paper_2112_12994_b200/csrc/k_cholinv.cuh"
+using namespace tfk;
+int main(int argc, char** argv) {
+  int K = argc > 1 ? atoi(argv[1]) : 201;
+  std::vector<double> A((size_t)400 * K), G((size_t)K * K, 0.0);
+  srand(1);
+  for (auto& v : A) v = (rand() / (double)RAND_MAX) - 0.5;
+  for (int i = 0; i < K; ++i) for (int j = 0; j < K; ++j) { double s = 0; for (int t = 0; t < 400; ++t) s += A[t*K+i]*A[t*K+j]; G[i*K+j] = s; }
+  double *dG, *dR; int *flags, *status;
+  cudaMalloc(&dG, sizeof(double)*K*K); cudaMalloc(&dR, sizeof(double)*K*K);
+  cudaMalloc(&flags, 16); cudaMalloc(&status, 16); cudaMemset(flags, 0, 16); cudaMemset(status, 0, 16);
+  cudaMemcpy(dG, G.data(), sizeof(double)*K*K, cudaMemcpyHostToDevice);
+  CholinvArgs a; a.G = dG; a.K = K; a.perm_in = 0; a.perm_out = 0; a.iter = 2; a.nrows = 400; a.Rinv = dR; a.flags = flags; a.status = status; a.lag = 1;
+  size_t smem = cholinv_smem_bytes(K);
+  cudaFuncSetAttribute(k_cholinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    k_cholinv<<<1, kCholinvThreads, smem>>>(a);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    long long clk[256]; cudaMemcpyFromSymbol(clk, g_ci_clk, sizeof(clk));
+    printf("K=%d rep %d: %.1f us  err=%s\n", K, rep, ms*1e3, cudaGetErrorString(cudaGetLastError()));
+    if (rep == 4) { for (int k = 1; k < 64; ++k) if (clk[k]) printf("  stamp %2d: +%lld cycles\n", k, clk[k]-clk[0]); }
+  }
+  // check: R^-1 * R^-T = G^-1 -> verify G * Rinv * Rinv^T = I
+  std::vector<double> R(K*K); cudaMemcpy(R.data(), dR, sizeof(double)*K*K, cudaMemcpyDeviceToHost);
+  double maxerr = 0;
+  for (int i = 0; i < K; i += 37) for (int j = 0; j < K; j += 41) {
+    // (Rinv^T G Rinv)(i,j) should be delta
+    double s = 0; for (int u = 0; u < K; ++u) { double t = 0; for (int v = 0; v < K; ++v) t += G[u*K+v]*R[v*K+j]; s += R[u*K+i]*t; }
+    maxerr = fmax(maxerr, fabs(s - (i==j)));
+  }
+  printf("orthogonality check max err %.3e\n", maxerr);
+  return 0;
+}
