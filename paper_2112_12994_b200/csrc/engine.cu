@@ -13,11 +13,11 @@
 #include <vector>
 
 #include "engine.h"
-#include "k_chol.cuh"
 #include "k_cholinv.cuh"
 #include "k_gram.cuh"
 #include "k_pass.cuh"
 #include "k_sample.cuh"
+#include "k_tpu.cuh"
 
 using namespace tfk;
 
@@ -87,38 +87,6 @@ struct SolveOut {
   int* status;
 };
 
-static int trinv_slots(int K) {
-  const int s = (K + 31) / 32;
-  return s <= 1 ? 1 : s <= 2 ? 2 : s <= 4 ? 4 : s <= 8 ? 8 : s <= 16 ? 16 : 32;
-}
-
-template <int S>
-static void launch_trinv_s(const double* Rrow, int K, int perm, double* out, const int* gate,
-                           cudaStream_t st) {
-  const int grid = (K + kTrinvWarps - 1) / kTrinvWarps;
-  k_trinv<S><<<grid, kTrinvWarps * 32, 0, st>>>(Rrow, K, perm, out, gate);
-}
-
-static void launch_trinv(const double* Rrow, int K, int perm, double* out, const int* gate,
-                         cudaStream_t st) {
-  switch (trinv_slots(K)) {
-    case 1: launch_trinv_s<1>(Rrow, K, perm, out, gate, st); break;
-    case 2: launch_trinv_s<2>(Rrow, K, perm, out, gate, st); break;
-    case 4: launch_trinv_s<4>(Rrow, K, perm, out, gate, st); break;
-    case 8: launch_trinv_s<8>(Rrow, K, perm, out, gate, st); break;
-    case 16: launch_trinv_s<16>(Rrow, K, perm, out, gate, st); break;
-    default: launch_trinv_s<32>(Rrow, K, perm, out, gate, st); break;
-  }
-  LAUNCH_CHECK("k_trinv");
-  COUNT_LAUNCH();
-}
-
-static void launch_phi(const PhiArgs& a, cudaStream_t st) {
-  k_phi<<<1, kPhiThreads, sizeof(double) * 2 * a.K, st>>>(a);
-  LAUNCH_CHECK("k_phi");
-  COUNT_LAUNCH();
-}
-
 struct GramPlan {
   int nblk, npair, nsplit;
   int64_t rps;
@@ -139,10 +107,10 @@ static GramPlan gram_plan(int64_t rows, int K, int sm_count) {
   return g;
 }
 
+// G (TPU) = A^T A over `rows` rows
 template <class L>
 static void gram(tf_context* ctx, const L& ld, int64_t rows, int K, double* G, const int* gate) {
   const GramPlan g = gram_plan(rows, K, ctx->sm_count);
-  ctx->sb.W.need((size_t)g.nsplit * g.npair * 4096);
   dim3 grid(g.npair, g.nsplit);
   k_gram<L><<<grid, kGramThreads, 0, ctx->stream>>>(ld, rows, K, g.nblk, g.rps, ctx->sb.W.get(), G,
                                                     ctx->sb.tickets.get(), gate);
@@ -150,57 +118,70 @@ static void gram(tf_context* ctx, const L& ld, int64_t rows, int K, double* G, c
   COUNT_LAUNCH();
 }
 
+// Q = A B, B upper-triangular TPU
 template <class L>
-static void qform(tf_context* ctx, const L& ld, int64_t rows, int K, const double* Rg, double* Q,
+static void qform(tf_context* ctx, const L& ld, int64_t rows, int K, const double* B, double* Q,
                   const int* gate) {
   dim3 grid((unsigned)((rows + 63) / 64), (unsigned)((K + 63) / 64));
-  k_qform<L><<<grid, kGramThreads, 0, ctx->stream>>>(ld, rows, K, Rg, Q, K, gate);
+  k_qform<L><<<grid, kGramThreads, 0, ctx->stream>>>(ld, rows, K, B, Q, K, gate);
   LAUNCH_CHECK("k_qform");
   COUNT_LAUNCH();
 }
 
-static void chol(tf_context* ctx, const double* G, int K, int perm, int iter, int64_t rows,
-                 double* Rrow, int lag, int* status) {
-  CholArgs a;
+static void cholinv(tf_context* ctx, const double* G, int K, int pass, int64_t rows, double* Rinv,
+                    const int* gate, int lag, int* status) {
+  CholinvArgs a;
   a.G = G;
   a.K = K;
-  a.perm = perm;
-  a.iter = iter;
+  a.pass = pass;
   a.nrows = rows;
-  a.use_smem = chol_fits_smem(K) ? 1 : 0;
-  size_t smem = a.use_smem ? chol_smem_bytes(K) : sizeof(double) * (32 * 33 + 8);
-  if (!a.use_smem) ctx->sb.ws.need((size_t)K * (K + 1) / 2);
-  a.ws = ctx->sb.ws.get();
-  a.Rrow = Rrow;
+  a.Rinv = Rinv;
+  a.use_smem = cholinv_in_smem(K) ? 1 : 0;
   a.flags = ctx->sb.flags.get();
+  a.gate = gate;
+  a.scratch = ctx->sb.scratch.get();
   a.status = status;
   a.lag = lag;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CK(cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmemLimit));
-    attr_set = true;
+  const size_t smem = a.use_smem ? cholinv_smem_bytes(K) : 0;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    CK(cudaFuncSetAttribute(k_cholinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
   }
-  k_chol<<<1, kCholThreads, smem, ctx->stream>>>(a);
-  LAUNCH_CHECK("k_chol");
+  k_cholinv<<<1, kCholinvThreads, smem, ctx->stream>>>(a);
+  LAUNCH_CHECK("k_cholinv");
   COUNT_LAUNCH();
 }
+
+static void trmm(tf_context* ctx, const double* A, const double* B, double* C, int K, const int* gate) {
+  const int items = trmm_items(K);
+  k_trmm_tpu<<<(unsigned)((items + kTrmmWarps - 1) / kTrmmWarps), kTrmmWarps * 32, 0, ctx->stream>>>(
+      A, B, C, K, gate);
+  LAUNCH_CHECK("k_trmm_tpu");
+  COUNT_LAUNCH();
+}
+
+static unsigned tpu_grid(int K) { return (unsigned)std::min<int64_t>(1024, (tpu_size(K) + 255) / 256); }
 
 // Size every solve buffer for the largest system of a sweep up front so that
 // no cudaMalloc/cudaFree (which synchronise) happens between lags.
 static void reserve_solve(tf_context* ctx, int64_t c, int Kmax) {
   SolveBufs& b = ctx->sb;
-  const size_t KK = (size_t)Kmax * Kmax;
-  const size_t tri = (size_t)Kmax * (Kmax + 1) / 2;
-  b.G.need(KK);
-  b.R1row.need(tri);
-  b.R2row.need(tri);
-  b.R3row.need(tri);
-  b.Rg1.need(KK);
-  b.Rinv2.need(KK);
-  b.Rinv3.need(KK);
+  const size_t tsz = (size_t)tpu_size(std::max(Kmax, 2));
+  b.G.need(tsz);
+  b.RA.need(tsz);
+  b.RB.need(tsz);
+  b.RC.need(tsz);
+  b.SA.need(tsz);
+  b.SB.need(tsz);
+  b.SC.need(tsz);
+  b.T.need(tsz);
+  b.S0.need(tsz);
+  b.S1.need(tsz);
   b.Q1.need((size_t)c * Kmax);
   b.Q2.need((size_t)c * Kmax);
   b.flags.need(4);
+  b.scratch.need((size_t)((Kmax + 31) / 32 + 1) * 32 * kTLD);
   size_t wmax = 0;
   for (int K = 2; K <= Kmax; ++K) {
     const GramPlan g = gram_plan(c, K, ctx->sm_count);
@@ -211,82 +192,69 @@ static void reserve_solve(tf_context* ctx, int64_t c, int Kmax) {
     b.tickets.need(4096);
     CK(cudaMemset(b.tickets.get(), 0, 4096 * sizeof(int)));
   }
-  if (!chol_fits_smem(Kmax)) b.ws.need(tri);
 }
 
-// One CholeskyQR iteration's small factorization: G -> Rinv (dense).
-static void factor_inverse(tf_context* ctx, const double* G, int K, int perm, int iter, int64_t rows,
-                           double* Rinv, int lag, int* status) {
-  if (K <= kCholinvMaxK) {
-    CholinvArgs a;
-    a.G = G;
-    a.K = K;
-    a.perm_in = perm;
-    a.perm_out = perm;
-    a.iter = iter;
-    a.nrows = rows;
-    a.Rinv = Rinv;
-    a.flags = ctx->sb.flags.get();
-    a.status = status;
-    a.lag = lag;
-    const size_t smem = cholinv_smem_bytes(K);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-      CK(cudaFuncSetAttribute(k_cholinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
-    }
-    k_cholinv<<<1, kCholinvThreads, smem, ctx->stream>>>(a);
-    LAUNCH_CHECK("k_cholinv");
-    COUNT_LAUNCH();
-  } else {
-    // large-K path: packed factorization in global memory + warp-per-column inverse
-    chol(ctx, G, K, perm, iter, rows, ctx->sb.R1row.get(), lag, status);
-    launch_trinv(ctx->sb.R1row.get(), K, perm, Rinv, iter == 3 ? ctx->sb.flags.get() : nullptr,
-                 ctx->stream);
-  }
-}
-
+// Preconditioned CholeskyQR solve of one sampled system (forward column
+// order, K = p + 1 columns, target last).  `Sprev` (TPU, K - 1) is the
+// previous lag's inverse factor (nullptr -> identity preconditioner);
+// `Snext` receives this lag's S = R^-1 for the next lag.
 template <class L>
-static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const SolveOut& o) {
+static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const SolveOut& o,
+                       const double* Sprev, const double* phi_prev, double* Snext) {
   SolveBufs& b = ctx->sb;
   reserve_solve(ctx, c, K);
-  int* shifted = b.flags.get();
-  PhiArgs pa;
+  int* fl = b.flags.get();
+  cudaStream_t st = ctx->stream;
+  PhiSArgs pa;
   pa.K = K;
-  pa.Rg1 = b.Rg1.get();
-  pa.Rinv2 = b.Rinv2.get();
-  pa.Rinv3 = b.Rinv3.get();
-  pa.flags = b.flags.get();
+  pa.SA = b.SA.get();
+  pa.SB = b.SB.get();
+  pa.SC = b.SC.get();
+  pa.flags = fl;
   pa.phi = o.phi;
   pa.coefs = o.coefs;
   pa.coef_off = o.coef_off;
   pa.taus = o.taus;
   pa.method = o.method;
   pa.lag = o.lag;
+  pa.S_final = Snext;
   if (K == 2) {
     gram(ctx, ld, c, K, b.G.get(), nullptr);
-    k_solve_k2<<<1, 1, 0, ctx->stream>>>(b.G.get(), pa);
+    k_solve_k2<<<1, 1, 0, st>>>(b.G.get(), pa);
     LAUNCH_CHECK("k_solve_k2");
     COUNT_LAUNCH();
     return;
   }
-  // iteration 1: G1 = A^T A (gathered order), Rinv_1 with rows in gathered order
-  gram(ctx, ld, c, K, b.G.get(), nullptr);
-  factor_inverse(ctx, b.G.get(), K, 1, 1, c, b.Rg1.get(), o.lag, o.status);
-  qform(ctx, ld, c, K, b.Rg1.get(), b.Q1.get(), nullptr);
-  // iteration 2: G2 = Q1^T Q1
+  if (Sprev && phi_prev)
+    k_precond<<<tpu_grid(K), 256, 0, st>>>(Sprev, phi_prev, ctx->scal.get(), b.T.get(), K);
+  else
+    k_tpu_identity<<<tpu_grid(K), 256, 0, st>>>(b.T.get(), K);
+  LAUNCH_CHECK("k_precond");
+  COUNT_LAUNCH();
+  // pass A on Q1 = A T
+  qform(ctx, ld, c, K, b.T.get(), b.Q1.get(), nullptr);
   DenseRows q1{b.Q1.get(), K};
   gram(ctx, q1, c, K, b.G.get(), nullptr);
-  factor_inverse(ctx, b.G.get(), K, 0, 2, c, b.Rinv2.get(), o.lag, o.status);
-  // iteration 3 (only when iteration 1 needed the shift)
-  qform(ctx, q1, c, K, b.Rinv2.get(), b.Q2.get(), shifted);
+  cholinv(ctx, b.G.get(), K, 0, c, b.RA.get(), nullptr, o.lag, o.status);
+  trmm(ctx, b.T.get(), b.RA.get(), b.SA.get(), K, nullptr);
+  // pass B (gated: Q1 not orthonormal enough, or pass A shifted)
+  qform(ctx, q1, c, K, b.RA.get(), b.Q2.get(), fl + 2);
   DenseRows q2{b.Q2.get(), K};
-  gram(ctx, q2, c, K, b.G.get(), shifted);
-  factor_inverse(ctx, b.G.get(), K, 0, 3, c, b.Rinv3.get(), o.lag, o.status);
-  launch_phi(pa, ctx->stream);
+  gram(ctx, q2, c, K, b.G.get(), fl + 2);
+  cholinv(ctx, b.G.get(), K, 1, c, b.RB.get(), fl + 2, o.lag, o.status);
+  trmm(ctx, b.SA.get(), b.RB.get(), b.SB.get(), K, fl + 2);
+  // pass C (gated: pass A needed the shift)
+  qform(ctx, q2, c, K, b.RB.get(), b.Q1.get(), fl + 0);
+  gram(ctx, q1, c, K, b.G.get(), fl + 0);
+  cholinv(ctx, b.G.get(), K, 2, c, b.RC.get(), fl + 0, o.lag, o.status);
+  trmm(ctx, b.SB.get(), b.RC.get(), b.SC.get(), K, fl + 0);
+  k_phi_S<<<1, 256, 0, st>>>(pa);
+  LAUNCH_CHECK("k_phi_S");
+  COUNT_LAUNCH();
 }
 
 // ---------------------------------------------------------------------------
+
 static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev) {
   PassArgs a;
   a.y = ctx->y.get();
@@ -447,8 +415,10 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
     o.method = ctx->method.get();
     o.lag = p;
     o.status = ctx->status.get();
-    GatherRows ld{ctx->y.get(), idx, wts, (int64_t)p};
-    solve_rows(ctx, ld, c, p + 1, o);
+    FwdRows ld{ctx->y.get(), idx, wts, 0};
+    double* Snext = (p & 1) ? ctx->sb.S1.get() : ctx->sb.S0.get();
+    const double* Sprev = (p & 1) ? ctx->sb.S0.get() : ctx->sb.S1.get();
+    solve_rows(ctx, ld, c, p + 1, o, p >= 2 ? Sprev : nullptr, p >= 2 ? ctx->phi.get() : nullptr, Snext);
     if (phases) CK(cudaEventRecord(ctx->pev[2 * (p - 1) + 1], st));
     // residuals of the lag-p window fit + score update s_p = s_{p-1} + r_{p-1}^2/R_{p-1}
     launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());
@@ -541,14 +511,14 @@ __global__ void k_set_unit(double* scal) {
   scal[0] = 1.0;
 }
 
-__global__ void k_materialize(GatherRows ld, int64_t c, int width, double* a, double* b) {
+// apply_sample (sketch.cpp:61-79) through the same forward-order row loader
+// the solve uses: lag column j of row t is column p - 1 - j, the target p.
+__global__ void k_materialize(FwdRows ld, int64_t c, int p, int width, double* a, double* b) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
   if (t >= c) return;
   for (int j = threadIdx.x; j <= width; j += blockDim.x) {
-    // gathered column 0 is the target, column j' >= 1 is lag column j' - 1
-    const double v = ld(t, j);
-    if (j == 0) b[t] = v;
-    else a[t * width + (j - 1)] = v;
+    if (j == width) b[t] = ld(t, p);
+    else a[t * width + j] = ld(t, p - 1 - j);
   }
 }
 
@@ -635,9 +605,9 @@ static void apply_sample_op(tf_context* ctx, const double* y, int64_t n_used, in
   B.need(c);
   CK(cudaMemcpyAsync(ctx->idx.get(), idx, c * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->wts.get(), w, c * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-  GatherRows ld{ctx->y.get(), ctx->idx.get(), ctx->wts.get(), (int64_t)p};
+  FwdRows ld{ctx->y.get(), ctx->idx.get(), ctx->wts.get(), 0};
   dim3 blk(32, 8);
-  k_materialize<<<(unsigned)((c + 7) / 8), blk, 0, ctx->stream>>>(ld, c, width, A.get(), B.get());
+  k_materialize<<<(unsigned)((c + 7) / 8), blk, 0, ctx->stream>>>(ld, c, p, width, A.get(), B.get());
   LAUNCH_CHECK("k_materialize");
   COUNT_LAUNCH();
   CK(cudaMemcpyAsync(a_out, A.get(), sizeof(double) * c * width, cudaMemcpyDeviceToHost, ctx->stream));
@@ -656,8 +626,8 @@ static void solve_sampled_op(tf_context* ctx, const double* y, int64_t n_used, i
   CK(cudaMemcpyAsync(ctx->idx.get(), idx, c * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->wts.get(), w, c * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   SolveOut o{ctx->phi.get(), nullptr, 0, nullptr, ctx->method.get(), 1, ctx->status.get()};
-  GatherRows ld{ctx->y.get(), ctx->idx.get(), ctx->wts.get(), (int64_t)p};
-  solve_rows(ctx, ld, c, p + 1, o);
+  FwdRows ld{ctx->y.get(), ctx->idx.get(), ctx->wts.get(), 0};
+  solve_rows(ctx, ld, c, p + 1, o, nullptr, nullptr, nullptr);
   CK(cudaMemcpyAsync(phi_out, ctx->phi.get(), p * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   int m = 0;
   CK(cudaMemcpyAsync(&m, ctx->method.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -768,8 +738,9 @@ void tf_destroy(tf_context* ctx) {
   ctx->wts.release(); ctx->fw.release(); ctx->w_hist.release(); ctx->status.release();
   ctx->method.release();
   tfe::SolveBufs& b = ctx->sb;
-  b.W.release(); b.G.release(); b.R1row.release(); b.R2row.release(); b.R3row.release();
-  b.Rg1.release(); b.Rinv2.release(); b.Rinv3.release(); b.Q1.release(); b.Q2.release(); b.ws.release(); b.flags.release(); b.tickets.release();
+  b.W.release(); b.G.release(); b.RA.release(); b.RB.release(); b.RC.release(); b.SA.release();
+  b.SB.release(); b.SC.release(); b.T.release(); b.S0.release(); b.S1.release(); b.Q1.release();
+  b.Q2.release(); b.flags.release(); b.tickets.release(); b.scratch.release();
   ctx->rh_scores.release(); ctx->rh_approx.release(); ctx->rh_approx2.release(); ctx->rh_M.release();
   ctx->rh_G.release(); ctx->rh_lvl.release(); ctx->rh_tmp.release(); ctx->rh_picked.release();
   ctx->rh_keys.release(); ctx->rh_keys2.release(); ctx->rh_cub.release();

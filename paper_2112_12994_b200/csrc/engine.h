@@ -27,7 +27,7 @@ struct DBuf {
 };
 
 struct SolveBufs {
-  DBuf<double> W, G, R1row, R2row, R3row, Rg1, Rinv2, Rinv3, Q1, Q2, ws;
+  DBuf<double> W, G, RA, RB, RC, SA, SB, SC, T, S0, S1, Q1, Q2, scratch;
   DBuf<int> flags, tickets;
 };
 

@@ -4,33 +4,23 @@
 // apply_sample, sketch.cpp:61-79).
 //
 // The sampled, weighted rows are never materialised as a separate matrix:
-// row t of the augmented system in "gathered" column order is
-//   a_t[j'] = w_t * y[off + i_t - j'],  j' = 0..K-1   (K = p + 1)
-// i.e. a contiguous, reversed slice of the series (j' = 0 is the target
-// column, j' >= 1 the lag columns) -- the gather is fused into the tile
+// row t of the augmented system in forward column order (k_tpu.cuh) is
+//   a_t[a] = w_t * y[off + i_t + a],  a = 0..K-1   (K = p + 1, target last)
+// a contiguous slice of the series -- the gather is fused into the tile
 // loads (apply_sample's product w * y is formed exactly as the reference).
 //
 //   k_gram   : split-K partial Gram tiles (64x64 upper block pairs) from rows
 //              [split * rps, (split+1) * rps); 4 warps, 32x32 per warp,
 //              16 DMMA per k4-step.  Deterministic: the last CTA of a tile
 //              pair reduces the split partials in split order.
-//   k_qform  : Q = A * Rg for a dense K x K right factor (structural zeros
-//              above row l+1 skipped), used for CholeskyQR's Q = A R^-1.
+//   k_qform  : Q = A * B for an upper-triangular TPU right factor B
+//              (CholeskyQR's Q = A R^-1 and the preconditioned Q1 = A T).
 #pragma once
 
 #include "common.cuh"
+#include "k_tpu.cuh"
 
 namespace tfk {
-
-struct GatherRows {
-  const double* y;
-  const int64_t* idx;
-  const double* wt;
-  int64_t off;  // LSAR window system: p; RH full system: p_bar
-  __device__ __forceinline__ double operator()(int64_t t, int col) const {
-    return wt[t] * y[off + idx[t] - col];
-  }
-};
 
 struct DenseRows {
   const double* q;
@@ -149,26 +139,29 @@ __global__ void __launch_bounds__(kGramThreads)
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      if (el[u] >= 0) G[(size_t)(J0 + (el[u] >> 6)) * K + L0 + (el[u] & 63)] = s[u];
+      if (el[u] >= 0) {
+        const int row = J0 + (el[u] >> 6), col = L0 + (el[u] & 63);
+        if (row <= col || (row >> 5) == (col >> 5)) G[tpu_idx(K, row, col)] = s[u];  // TPU output
+      }
   }
   if (tid == 0) tickets[blockIdx.x] = 0;
 }
 
 constexpr int kQA = 36;
 
-// Q[t][l] = sum_j' A(t, j') * Rg[j'][l], l < K.  Rg row-major K x K with
-// Rg[j'][l] == 0 whenever j' > l + 1 (upper triangular up to the one-row
-// shift of the gathered column order).
+// Q[t][l] = sum_{a <= l} A(t, a) * B(a, l), l < K, for an upper-triangular
+// TPU right factor B (CholeskyQR's Q = A R^-1, or A T with the carried
+// preconditioner).
 template <class L>
 __global__ void __launch_bounds__(kGramThreads)
-    k_qform(L ld, int64_t rows, int K, const double* __restrict__ Rg, double* __restrict__ Q,
+    k_qform(L ld, int64_t rows, int K, const double* __restrict__ B, double* __restrict__ Q,
             int64_t ldq, const int* skip_flag) {
   if (skip_flag && *skip_flag == 0) return;
   __shared__ __align__(16) double SA[64][kQA];
   __shared__ __align__(16) double SR[32][kSJ];
   const int64_t t0 = (int64_t)blockIdx.x * 64;
   const int L0 = blockIdx.y * 64;
-  const int jend = min(K, L0 + 64 + 1);
+  const int jend = min(K, L0 + 64);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;
   double acc[4][4][2];
@@ -189,7 +182,8 @@ __global__ void __launch_bounds__(kGramThreads)
 #pragma unroll 4
       for (int s = 0; s < 16; ++s) {
         const int c = c0 + 2 * s;
-        SR[c][ll] = (k0 + c < K && L0 + ll < K) ? Rg[(size_t)(k0 + c) * K + L0 + ll] : 0.0;
+        const int r = k0 + c, cl = L0 + ll;
+        SR[c][ll] = (r < K && cl < K && r <= cl) ? B[tpu_idx(K, r, cl)] : 0.0;
       }
     }
     __syncthreads();

@@ -14,12 +14,15 @@ int main(int argc, char** argv) {
   srand(1);
   for (auto& v : A) v = (rand() / (double)RAND_MAX) - 0.5;
   for (int i = 0; i < K; ++i) for (int j = 0; j < K; ++j) { double s = 0; for (int t = 0; t < 400; ++t) s += A[t*K+i]*A[t*K+j]; G[i*K+j] = s; }
-  double *dG, *dR; int *flags, *status;
-  cudaMalloc(&dG, sizeof(double)*K*K); cudaMalloc(&dR, sizeof(double)*K*K);
+  const int64_t tsz = tpu_size(K);
+  std::vector<double> Gt(tsz, 0.0);
+  for (int i = 0; i < K; ++i) for (int j = i; j < K; ++j) Gt[tpu_idx(K, i, j)] = G[i*K+j];
+  double *dG, *dR, *scr; int *flags, *status;
+  cudaMalloc(&dG, sizeof(double)*tsz); cudaMalloc(&dR, sizeof(double)*tsz); cudaMalloc(&scr, sizeof(double)*40000);
   cudaMalloc(&flags, 16); cudaMalloc(&status, 16); cudaMemset(flags, 0, 16); cudaMemset(status, 0, 16);
-  cudaMemcpy(dG, G.data(), sizeof(double)*K*K, cudaMemcpyHostToDevice);
-  CholinvArgs a; a.G = dG; a.K = K; a.perm_in = 0; a.perm_out = 0; a.iter = 2; a.nrows = 400; a.Rinv = dR; a.flags = flags; a.status = status; a.lag = 1;
-  size_t smem = cholinv_smem_bytes(K);
+  cudaMemcpy(dG, Gt.data(), sizeof(double)*tsz, cudaMemcpyHostToDevice);
+  CholinvArgs a; a.G = dG; a.K = K; a.pass = 0; a.nrows = 400; a.Rinv = dR; a.use_smem = cholinv_in_smem(K); a.flags = flags; a.gate = nullptr; a.scratch = scr; a.status = status; a.lag = 1;
+  size_t smem = a.use_smem ? cholinv_smem_bytes(K) : 0;
   cudaFuncSetAttribute(k_cholinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int rep = 0; rep < 5; ++rep) {
@@ -32,11 +35,12 @@ int main(int argc, char** argv) {
     if (rep == 4) { for (int k = 1; k < 64; ++k) if (clk[k]) printf("  stamp %2d: +%lld cycles\n", k, clk[k]-clk[0]); }
   }
   // check: R^-1 * R^-T = G^-1 -> verify G * Rinv * Rinv^T = I
-  std::vector<double> R(K*K); cudaMemcpy(R.data(), dR, sizeof(double)*K*K, cudaMemcpyDeviceToHost);
+  std::vector<double> Rt(tsz), R(K*K, 0.0); cudaMemcpy(Rt.data(), dR, sizeof(double)*tsz, cudaMemcpyDeviceToHost);
+  for (int i = 0; i < K; ++i) for (int j = i; j < K; ++j) R[i*K+j] = Rt[tpu_idx(K, i, j)];
   double maxerr = 0;
   for (int i = 0; i < K; i += 37) for (int j = 0; j < K; j += 41) {
     // (Rinv^T G Rinv)(i,j) should be delta
-    double s = 0; for (int u = 0; u < K; ++u) { double t = 0; for (int v = 0; v < K; ++v) t += G[u*K+v]*R[v*K+j]; s += R[u*K+i]*t; }
+    double s = 0; for (int u = 0; u < K; ++u) { double t = 0; for (int v = 0; v < K; ++v) t += G[u*K+v]*R[v*K+j]; s += R[u*K+i]*t; }  // Rinv^T G Rinv
     maxerr = fmax(maxerr, fabs(s - (i==j)));
   }
   printf("orthogonality check max err %.3e\n", maxerr);

@@ -4,33 +4,66 @@
 #include "../paper_2112_12994_b200/csrc/common.cuh"
 using namespace tfk;
 constexpr int LD = 36;
-template <int I> struct F { static __device__ __forceinline__ void run(double (&d)[32], int lane, bool& bad) {
-    const double piv = __shfl_sync(0xffffffffu, d[I], I);
-    bad |= !(piv > 0.0);
-    const double inv = fast_rsqrt(piv);
-    if (lane == I) d[I] = piv * inv; else if (lane > I) d[I] *= inv;
-#pragma unroll
-    for (int r = I + 1; r < 32; ++r) { const double rir = __shfl_sync(0xffffffffu, d[I], r); if (lane >= r) d[r] = fma(-rir, d[I], d[r]); }
-    F<I + 1>::run(d, lane, bad); } };
-template <> struct F<32> { static __device__ __forceinline__ void run(double (&)[32], int, bool&) {} };
-template <int I> struct V { static __device__ __forceinline__ void run(double (&d)[32], int lane) {
-    double acc = (lane == I) ? 1.0 : 0.0;
-#pragma unroll
-    for (int q = I + 1; q < 32; ++q) { const double riq = __shfl_sync(0xffffffffu, d[I], q); if (lane >= q) acc = fma(-riq, d[q], acc); }
-    const double rinv = fast_rcp(__shfl_sync(0xffffffffu, d[I], I));
-    d[I] = lane >= I ? acc * rinv : 0.0;
-    V<I - 1>::run(d, lane); } };
-template <> struct V<-1> { static __device__ __forceinline__ void run(double (&)[32], int) {} };
+#define kTLD LD
 __device__ __noinline__ bool diag_reg(double* dt) {
+  const int m = 32, last = -1; const double floor = 0.0;
   const int lane = threadIdx.x & 31;
+  double* col = dt + lane * kTLD;
   double d[32];
 #pragma unroll
-  for (int r = 0; r < 32; ++r) d[r] = r <= lane ? dt[lane * LD + r] : 0.0;
+  for (int k = 0; k < 32; ++k) d[k] = (lane < m && k <= lane) ? col[k] : 0.0;
   bool bad = false;
-  F<0>::run(d, lane, bad);
-  V<31>::run(d, lane);
+  long long t0 = clock64();
+  for (int i = 0; i < m; ++i) {
+    double piv = __shfl_sync(0xffffffffu, d[0], i);
+    if (i == last && !(piv > floor)) piv = floor;
+    bad |= !(piv > 0.0) || !isfinite(piv);
+    const double inv = fast_rsqrt(piv);
+    const double ri = lane == i ? piv * inv : (lane > i ? d[0] * inv : 0.0);
+    if (lane >= i && lane < m) col[i] = ri;
 #pragma unroll
-  for (int r = 0; r < 32; ++r) dt[lane * LD + r] = r <= lane ? d[r] : 0.0;
+    for (int k = 1; k < 32; ++k) {
+      const double rik = __shfl_sync(0xffffffffu, ri, (i + k) & 31);
+      if (lane >= i + k) d[k] = fma(-rik, ri, d[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 31; ++k) d[k] = d[k + 1];
+    d[31] = 0.0;
+  }
+  __syncwarp();
+  long long t1 = clock64();
+  double xw[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) xw[k] = 0.0;
+  for (int i = m - 1; i >= 0; --i) {
+    double a0 = (lane == i) ? 1.0 : 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 31; k += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = i + 1 + k + u;
+        if (k + u < 31 && q < m) {
+          const double rq = dt[q * kTLD + i];
+          const double t = xw[k + u];
+          if (u == 0) a0 = fma(-rq, t, a0);
+          else if (u == 1) a1 = fma(-rq, t, a1);
+          else if (u == 2) a2 = fma(-rq, t, a2);
+          else a3 = fma(-rq, t, a3);
+        }
+      }
+    }
+    const double rinv = fast_rcp(dt[i * kTLD + i]);
+    const double xi = lane >= i ? ((a0 + a1) + (a2 + a3)) * rinv : 0.0;
+    __syncwarp();
+    if (lane >= i && lane < m) col[i] = xi;
+#pragma unroll
+    for (int k = 31; k > 0; --k) xw[k] = xw[k - 1];
+    xw[0] = xi;
+    __syncwarp();
+  }
+  long long t2 = clock64();
+  if (lane < m) for (int r = lane + 1; r < 32; ++r) col[r] = 0.0;
+  if (lane == 0) printf("  factor %lld cycles, inverse %lld cycles\n", t1 - t0, t2 - t1);
   return __any_sync(0xffffffffu, bad);
 }
 __global__ void k(double* g, double* out, long long* cyc, int reps) {
@@ -54,7 +87,7 @@ int main() {
   double *dg, *dx; long long* dc; cudaMalloc(&dg, 8192); cudaMalloc(&dx, 8192); cudaMalloc(&dc, 64);
   cudaMemcpy(dg, G, 8192, cudaMemcpyHostToDevice);
   k<<<1, 32>>>(dg, dx, dc, 1);
-  k<<<1, 32>>>(dg, dx, dc, 20);
+  k<<<1, 32>>>(dg, dx, dc, 3);
   long long c; cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost); cudaMemcpy(X, dx, 8192, cudaMemcpyDeviceToHost);
   // check X = R^-1:  X^T G X = I  (X(r,c) stored at X[r*32+c])
   double err = 0;
