@@ -128,36 +128,49 @@ static void qform(tf_context* ctx, const L& ld, int64_t rows, int K, const doubl
   COUNT_LAUNCH();
 }
 
-static void cholinv(tf_context* ctx, const double* G, int K, int pass, int64_t rows, double* Rinv,
-                    const int* gate, int lag, int* status) {
+static void cholinv(tf_context* ctx, const double* G, int K, int pass, int64_t rows, double* RD,
+                    const int* gate, int lag, int* status, int force_b = 0) {
   CholinvArgs a;
   a.G = G;
   a.K = K;
   a.pass = pass;
   a.nrows = rows;
-  a.Rinv = Rinv;
+  a.RD = RD;
   a.use_smem = cholinv_in_smem(K) ? 1 : 0;
   a.flags = ctx->sb.flags.get();
   a.gate = gate;
-  a.scratch = ctx->sb.scratch.get();
+  a.force_b = force_b;
   a.status = status;
   a.lag = lag;
   const size_t smem = a.use_smem ? cholinv_smem_bytes(K) : 0;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
+  static size_t attr = 0;  // static + dynamic must fit the opt-in limit, so always opt in
+  if (smem > attr) {
     CK(cudaFuncSetAttribute(k_cholinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
   k_cholinv<<<1, kCholinvThreads, smem, ctx->stream>>>(a);
-  LAUNCH_CHECK("k_cholinv");
+  {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+      throw TfError{TF_CUDA, "k_cholinv (K=" + std::to_string(K) + ", smem=" + std::to_string(smem) +
+                                 "): " + cudaGetErrorString(e)};
+  }
   COUNT_LAUNCH();
 }
 
-static void trmm(tf_context* ctx, const double* A, const double* B, double* C, int K, const int* gate) {
-  const int items = trmm_items(K);
-  k_trmm_tpu<<<(unsigned)((items + kTrmmWarps - 1) / kTrmmWarps), kTrmmWarps * 32, 0, ctx->stream>>>(
-      A, B, C, K, gate);
-  LAUNCH_CHECK("k_trmm_tpu");
+// X = B R^-1 (R in RD format); TPU: B, X upper-triangular K x K; else dense rows x K.
+template <bool TPU>
+static void trsm_right(tf_context* ctx, const double* B, const double* RD, double* X, int64_t rows,
+                       int K, const int* gate) {
+  const size_t smem = trsm_smem_bytes(K);
+  static size_t attr = 0;
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(k_trsm_right<TPU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const unsigned grid = TPU ? (unsigned)((K + 31) / 32) : (unsigned)((rows + 31) / 32);
+  k_trsm_right<TPU><<<grid, kTrsmThreads, smem, ctx->stream>>>(B, RD, X, rows, K, K, gate);
+  LAUNCH_CHECK("k_trsm_right");
   COUNT_LAUNCH();
 }
 
@@ -181,7 +194,6 @@ static void reserve_solve(tf_context* ctx, int64_t c, int Kmax) {
   b.Q1.need((size_t)c * Kmax);
   b.Q2.need((size_t)c * Kmax);
   b.flags.need(4);
-  b.scratch.need((size_t)((Kmax + 31) / 32 + 1) * 32 * kTLD);
   size_t wmax = 0;
   for (int K = 2; K <= Kmax; ++K) {
     const GramPlan g = gram_plan(c, K, ctx->sm_count);
@@ -235,19 +247,20 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
   qform(ctx, ld, c, K, b.T.get(), b.Q1.get(), nullptr);
   DenseRows q1{b.Q1.get(), K};
   gram(ctx, q1, c, K, b.G.get(), nullptr);
-  cholinv(ctx, b.G.get(), K, 0, c, b.RA.get(), nullptr, o.lag, o.status);
-  trmm(ctx, b.T.get(), b.RA.get(), b.SA.get(), K, nullptr);
+  cholinv(ctx, b.G.get(), K, 0, c, b.RA.get(), nullptr, o.lag, o.status,
+          (Sprev && phi_prev) ? 0 : 1);
+  trsm_right<true>(ctx, b.T.get(), b.RA.get(), b.SA.get(), K, K, nullptr);
   // pass B (gated: Q1 not orthonormal enough, or pass A shifted)
-  qform(ctx, q1, c, K, b.RA.get(), b.Q2.get(), fl + 2);
+  trsm_right<false>(ctx, b.Q1.get(), b.RA.get(), b.Q2.get(), c, K, fl + 2);
   DenseRows q2{b.Q2.get(), K};
   gram(ctx, q2, c, K, b.G.get(), fl + 2);
   cholinv(ctx, b.G.get(), K, 1, c, b.RB.get(), fl + 2, o.lag, o.status);
-  trmm(ctx, b.SA.get(), b.RB.get(), b.SB.get(), K, fl + 2);
+  trsm_right<true>(ctx, b.SA.get(), b.RB.get(), b.SB.get(), K, K, fl + 2);
   // pass C (gated: pass A needed the shift)
-  qform(ctx, q2, c, K, b.RB.get(), b.Q1.get(), fl + 0);
+  trsm_right<false>(ctx, b.Q2.get(), b.RB.get(), b.Q1.get(), c, K, fl + 0);
   gram(ctx, q1, c, K, b.G.get(), fl + 0);
   cholinv(ctx, b.G.get(), K, 2, c, b.RC.get(), fl + 0, o.lag, o.status);
-  trmm(ctx, b.SB.get(), b.RC.get(), b.SC.get(), K, fl + 0);
+  trsm_right<true>(ctx, b.SB.get(), b.RC.get(), b.SC.get(), K, K, fl + 0);
   k_phi_S<<<1, 256, 0, st>>>(pa);
   LAUNCH_CHECK("k_phi_S");
   COUNT_LAUNCH();
@@ -271,7 +284,7 @@ static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, co
   const int64_t ntile = (w + kPassTile - 1) / kPassTile;
   const size_t smem = pass_smem_bytes(q);
   static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
+  if (smem > attr) {
     CK(cudaFuncSetAttribute(k_lsar_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
@@ -740,7 +753,7 @@ void tf_destroy(tf_context* ctx) {
   tfe::SolveBufs& b = ctx->sb;
   b.W.release(); b.G.release(); b.RA.release(); b.RB.release(); b.RC.release(); b.SA.release();
   b.SB.release(); b.SC.release(); b.T.release(); b.S0.release(); b.S1.release(); b.Q1.release();
-  b.Q2.release(); b.flags.release(); b.tickets.release(); b.scratch.release();
+  b.Q2.release(); b.flags.release(); b.tickets.release();
   ctx->rh_scores.release(); ctx->rh_approx.release(); ctx->rh_approx2.release(); ctx->rh_M.release();
   ctx->rh_G.release(); ctx->rh_lvl.release(); ctx->rh_tmp.release(); ctx->rh_picked.release();
   ctx->rh_keys.release(); ctx->rh_keys2.release(); ctx->rh_cub.release();

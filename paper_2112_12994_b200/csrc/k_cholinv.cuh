@@ -1,28 +1,27 @@
-// k_cholinv.cuh -- fused Cholesky factorization + triangular inverse of one
-// K x K Gram matrix in a single CTA: G = R^T R (upper R), Rinv = R^-1.
+// k_cholinv.cuh -- blocked Cholesky factorization G = R^T R of one K x K Gram
+// matrix in a single CTA (the small dense core of each CholeskyQR pass that
+// replaces Eigen's ColPivHouseholderQR, toeplitz.cpp:57-71).
 //
-// This is the small dense core of each CholeskyQR pass that replaces Eigen's
-// ColPivHouseholderQR (toeplitz.cpp:57-71) on the sampled system.  Input and
-// output are tile-packed upper matrices (k_tpu.cuh); for K <= kCholinvMaxK
-// the whole matrix lives in shared memory (207 KB at K = 201), moved in and
-// out with cp.async.bulk (TMA engine); larger K work in place in global
-// memory (L2-resident).
+// Output "RD" format (tile-packed upper, k_tpu.cuh): off-diagonal tiles hold
+// R, diagonal tiles hold Dinv_J = R_JJ^-1.  No explicit R^-1 is formed:
+// consumers apply R^-1 from the right by blocked substitution
+// (k_trsm_right), which parallelises over row blocks across CTAs.
 //
-// Blocked right-looking Cholesky, block 32, with look-ahead:
-//   * warp 0 updates the next diagonal tile first, then factors and inverts
-//     it in registers (lane l owns column l; fully unrolled, __noinline__ so
-//     the ~3k-instruction body is fetched once) while warps 1..7 apply the
-//     rest of the trailing update;
-//   * panel:    R(b, J)  = Dinv_b^T G(b, J)            (DMMA m8n8k4 f64)
-//   * trailing: G(I, J) -= R(b, I)^T R(b, J)           (DMMA)
-// In-place blocked inverse, row blocks bottom-up:
-//   W(I, L)    = -Dinv_I R(I, L)                        (DMMA)
-//   Rinv(I, J) = sum_{L=I+1..J} W(I, L) Rinv(L, J)       (DMMA)
-// Breakdown handling: a non-positive pivot in pass A restarts with the
-// shift 11 (cK + K(K+1)) eps tr(G) (shifted CholeskyQR) and flags the two
-// extra passes; the target (last) pivot is clamped instead (c == p case).
-// Pass A also estimates cond(R) <= ||R||_F ||R^-1||_F and requests pass B
-// when it exceeds 16 K (CholeskyQR loses orthogonality as cond^2 eps).
+// For K <= kCholinvMaxK the whole matrix lives in shared memory (207 KB at
+// K = 201), moved with cp.async.bulk (TMA engine); larger K work in place on
+// a global (L2-resident) copy.  Blocked right-looking, 32-column panels, with
+// look-ahead:
+//   1. warp 0 factors AND inverts the next diagonal tile (ci_diag32: 8 x 8
+//      register blocks + DMMA), overlapped with warps 1..7 finishing the
+//      trailing update of the current panel,
+//   2. panel row R(b, J) = Dinv_b^T G(b, J)        (DMMA m8n8k4 f64),
+//   3. trailing update G(I, J) -= R(b, I)^T R(b, J) (DMMA).
+// Breakdown: a non-positive pivot in pass A restarts with the shift
+// 11 (cK + K(K+1)) eps tr(G) (shifted CholeskyQR) and flags two extra passes;
+// the target (last) pivot is clamped instead (vanishing residual, c == p).
+// Pass A also requests pass B when a lower bound of ||R||_F ||R^-1||_F
+// exceeds 8 K (CholeskyQR loses orthogonality as cond^2 eps), and always for
+// an unpreconditioned system (identity T: first lag, standalone solves).
 #pragma once
 
 #ifndef CI_STAMP
@@ -35,8 +34,8 @@
 
 namespace tfk {
 
-constexpr int kCholinvMaxK = 211;     // tpu_size(K) * 8 B <= 227 KB - static smem
-constexpr int kCholinvThreads = 256;  // 8 warps: warp 0 diagonal chain, 1..7 bulk updates
+constexpr int kCholinvMaxK = 203;     // tpu_size(K) * 8 B + 13 KB static <= 227 KB
+constexpr int kCholinvThreads = 256;  // 8 warps
 constexpr int kCI_W = kCholinvThreads / 32;
 
 __host__ inline size_t cholinv_smem_bytes(int K) { return (size_t)tpu_size(K) * sizeof(double); }
@@ -47,11 +46,11 @@ struct CholinvArgs {
   int K;
   int pass;          // 0 = A (may shift, estimates cond), 1 = B, 2 = C
   int64_t nrows;     // rows of the tall matrix (shift formula)
-  double* Rinv;      // TPU output; also the working copy when !use_smem
+  double* RD;        // TPU output (RD format); also the working copy when !use_smem
   int use_smem;
   int* flags;        // [0] shifted, [1] failed, [2] need pass B
   const int* gate;   // run only if *gate != 0 (nullable)
-  double* scratch;   // global scratch, (K/32) * 32 * 36 doubles (large K only)
+  int force_b;       // pass A: always request pass B (unpreconditioned system)
   int* status;
   int lag;
 };
@@ -82,7 +81,7 @@ __device__ __forceinline__ void ci_zero(double (&acc)[4][2][2]) {
     for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 }
 
-// store (MODE 0), subtract (1) or store negated (2) a 32 x 16 accumulator
+// store (MODE 0) or subtract (1) a 32 x 16 accumulator into a tile of width w
 template <int MODE>
 __device__ __forceinline__ void ci_put(double* t, int w, int n0, const double (&acc)[4][2][2]) {
   const int lane = threadIdx.x & 31;
@@ -96,82 +95,9 @@ __device__ __forceinline__ void ci_put(double* t, int w, int n0, const double (&
         if (c < w) {
           double* q = t + c * kTLD + r;
           if (MODE == 0) *q = acc[i][j][e];
-          else if (MODE == 1) *q -= acc[i][j][e];
-          else *q = -acc[i][j][e];
+          else *q -= acc[i][j][e];
         }
       }
-}
-
-// ---- 32 x 32 diagonal block: factor, then invert in place (one warp) ----
-// Lane l owns column l.  A "rotating" register window keeps the row being
-// eliminated at d[0] (the window shifts by one row per step), so every step
-// is the same compact, fully unrolled body with only compile-time register
-// indices: a fully unrolled 32-step version is ~7k instructions, which does
-// not stay in the instruction cache between calls.  It is inlined at a single
-// call site in uniform control flow so the shuffles compile to plain SHFL
-// (a non-inlined callee gets divergence-safe collective sequences, ~10x
-// slower).  Finalized rows go to the
-// tile in shared memory; the inverse reads row i of R from there (broadcast)
-// and keeps the already-computed rows of its column of R^-1 in a window too.
-__device__ __forceinline__ bool ci_diag(double* dt, int m, int last, double floor) {
-  const int lane = threadIdx.x & 31;
-  double* col = dt + lane * kTLD;  // column `lane` (column-major tile)
-  double d[32];                    // d[k] = current entry of row (i + k) of my column
-#pragma unroll
-  for (int k = 0; k < 32; ++k) d[k] = (lane < m && k <= lane) ? col[k] : 0.0;
-  bool bad = false;
-  for (int i = 0; i < m; ++i) {
-    double piv = __shfl_sync(0xffffffffu, d[0], i);
-    if (i == last && !(piv > floor)) piv = floor;  // vanishing residual (c == p)
-    bad |= !(piv > 0.0) || !isfinite(piv);
-    const double inv = fast_rsqrt(piv);
-    const double ri = lane == i ? piv * inv : (lane > i ? d[0] * inv : 0.0);  // R(i, lane)
-    if (lane >= i && lane < m) col[i] = ri;
-#pragma unroll
-    for (int k = 1; k < 32; ++k) {
-      const double rik = __shfl_sync(0xffffffffu, ri, (i + k) & 31);  // R(i, i + k)
-      if (lane >= i + k) d[k] = fma(-rik, ri, d[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < 31; ++k) d[k] = d[k + 1];
-    d[31] = 0.0;
-  }
-  __syncwarp();
-  // inverse, rows bottom-up: x(i,l) = (delta_il - sum_{q>i} R(i,q) x(q,l)) / R(i,i);
-  // xw[k] = x(i + 1 + k, lane) (zero beyond the column), row i of R read
-  // from the tile (broadcast) before row i is overwritten by row i of R^-1
-  double xw[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) xw[k] = 0.0;
-  for (int i = m - 1; i >= 0; --i) {
-    double a0 = (lane == i) ? 1.0 : 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll
-    for (int k = 0; k < 31; k += 4) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int q = i + 1 + k + u;
-        if (k + u < 31 && q < m) {
-          const double rq = dt[q * kTLD + i];  // R(i, q), same address for all lanes
-          const double t = xw[k + u];
-          if (u == 0) a0 = fma(-rq, t, a0);
-          else if (u == 1) a1 = fma(-rq, t, a1);
-          else if (u == 2) a2 = fma(-rq, t, a2);
-          else a3 = fma(-rq, t, a3);
-        }
-      }
-    }
-    const double rinv = fast_rcp(dt[i * kTLD + i]);
-    const double xi = lane >= i ? ((a0 + a1) + (a2 + a3)) * rinv : 0.0;
-    __syncwarp();
-    if (lane >= i && lane < m) col[i] = xi;
-#pragma unroll
-    for (int k = 31; k > 0; --k) xw[k] = xw[k - 1];
-    xw[0] = xi;
-    __syncwarp();
-  }
-  if (lane < m)
-    for (int r = lane + 1; r < 32; ++r) col[r] = 0.0;  // strictly lower part
-  return __any_sync(0xffffffffu, bad);
 }
 
 struct CITiles {
@@ -179,6 +105,173 @@ struct CITiles {
   int K;
   __device__ __forceinline__ double* tile(int I, int J) const { return base + tpu_tile(K, I, J); }
 };
+
+// ---- 32 x 32 diagonal tile: factor + invert with ONE warp, recursively in
+//      8 x 8 blocks.  The 8 x 8 diagonal blocks are factored and inverted in
+//      registers (lanes 0..7, width-8 shuffles, 8-step chains); every other
+//      block operation is an 8 x 8 x 8 product = 2 DMMA m8n8k4.  The serial
+//      chain is 4 x (8 + 8) pivots instead of 32 + 32, and the warp issues
+//      ~2k instructions instead of ~10k.
+template <int I>
+struct F8 {
+  static __device__ __forceinline__ void run(double (&d)[8], int lane, bool& bad, int last,
+                                             double floor) {
+    double piv = __shfl_sync(0xffu, d[I], I, 8);
+    if (I == last && !(piv > floor)) piv = floor;  // vanishing residual (c == p)
+    bad |= !(piv > 0.0) || !isfinite(piv);
+    const double inv = fast_rsqrt(piv);
+    if (lane == I) d[I] = piv * inv;
+    else if (lane > I) d[I] *= inv;
+#pragma unroll
+    for (int r = I + 1; r < 8; ++r) {
+      const double rir = __shfl_sync(0xffu, d[I], r, 8);
+      if (lane >= r) d[r] = fma(-rir, d[I], d[r]);
+    }
+    F8<I + 1>::run(d, lane, bad, last, floor);
+  }
+};
+template <>
+struct F8<8> {
+  static __device__ __forceinline__ void run(double (&)[8], int, bool&, int, double) {}
+};
+template <int I>
+struct V8 {  // x = R^-1 in place, rows bottom-up (row I of R dead once row I of X is known)
+  static __device__ __forceinline__ void run(double (&d)[8], int lane) {
+    double acc = (lane == I) ? 1.0 : 0.0;
+#pragma unroll
+    for (int q = I + 1; q < 8; ++q) {
+      const double riq = __shfl_sync(0xffu, d[I], q, 8);
+      if (lane >= q) acc = fma(-riq, d[q], acc);
+    }
+    const double rinv = fast_rcp(__shfl_sync(0xffu, d[I], I, 8));
+    d[I] = lane >= I ? acc * rinv : 0.0;
+    V8<I - 1>::run(d, lane);
+  }
+};
+template <>
+struct V8<-1> {
+  static __device__ __forceinline__ void run(double (&)[8], int) {}
+};
+
+// 8x8x8 product into a C fragment: acc += sum_k A(m, k) B(k, n)
+template <class FA, class FB>
+__device__ __forceinline__ void mma8(double& c0, double& c1, FA fa, FB fb) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int k = 4 * h + (lane & 3);
+    dmma_8x8x4(c0, c1, fa(lane >> 2, k), fb(k, lane >> 2));
+  }
+}
+
+// S: 32 x 32 scratch (column-major, leading dimension kTLD) holding the tile,
+// DI: 4 x 64 scratch for the 8 x 8 diagonal inverses, TS: 4 x 64 scratch.
+// On exit S holds Dinv of the (identity-padded) tile.  Returns bad pivot.
+__device__ __forceinline__ bool ci_diag32(double* S, double* DI, double* TS, int last,
+                                          double floor) {
+  const int lane = threadIdx.x & 31;
+  const int fr = lane >> 2, fc = 2 * (lane & 3);  // C fragment (row, col pair)
+  auto at = [&](int bi, int bj, int r, int c) -> double& { return S[(8 * bj + c) * kTLD + 8 * bi + r]; };
+  bool bad = false;
+  for (int k = 0; k < 4; ++k) {
+    // (a) factor + invert the 8 x 8 diagonal block in registers
+    if (lane < 8) {
+      double d[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) d[r] = r <= lane ? at(k, k, r, lane) : 0.0;
+      const int lb = (last >= 8 * k && last < 8 * k + 8) ? last - 8 * k : -1;
+      F8<0>::run(d, lane, bad, lb, floor);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) at(k, k, r, lane) = r <= lane ? d[r] : 0.0;
+      V8<7>::run(d, lane);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) DI[k * 64 + lane * 8 + r] = r <= lane ? d[r] : 0.0;  // column lane
+    }
+    __syncwarp();
+    // (b) block row k: S_kj = Dinv_kk^T S_kj, j > k
+    double t[3][2];
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj) {
+      const int j = k + 1 + jj;
+      t[jj][0] = t[jj][1] = 0.0;
+      if (j < 4)
+        mma8(t[jj][0], t[jj][1], [&](int m, int kk) { return DI[k * 64 + m * 8 + kk]; },
+             [&](int kk, int n) { return at(k, j, kk, n); });
+    }
+    __syncwarp();
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj) {
+      const int j = k + 1 + jj;
+      if (j < 4) {
+        at(k, j, fr, fc) = t[jj][0];
+        at(k, j, fr, fc + 1) = t[jj][1];
+      }
+    }
+    __syncwarp();
+    // (c) trailing update S_ij -= S_ki^T S_kj, k < i <= j
+    for (int i = k + 1; i < 4; ++i)
+      for (int j = i; j < 4; ++j) {
+        double c0 = at(i, j, fr, fc), c1 = at(i, j, fr, fc + 1);
+        mma8(c0, c1, [&](int m, int kk) { return -at(k, i, kk, m); }, [&](int kk, int n) { return at(k, j, kk, n); });
+        at(i, j, fr, fc) = c0;
+        at(i, j, fr, fc + 1) = c1;
+      }
+    __syncwarp();
+  }
+  // inverse from the blocks, block rows bottom-up:
+  //   X_ij = -Dinv_ii sum_{k=i+1..j} R_ik X_kj   (X_jj = Dinv_jj)
+  for (int i = 2; i >= 0; --i) {
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj) {
+      const int j = i + 1 + jj;
+      if (j < 4) {
+        double c0 = 0.0, c1 = 0.0;
+        for (int k = i + 1; k <= j; ++k)
+          mma8(c0, c1, [&](int m, int kk) { return at(i, k, m, kk); },
+               [&](int kk, int n) { return k == j ? DI[j * 64 + n * 8 + kk] : at(k, j, kk, n); });
+        TS[jj * 64 + fr * 8 + fc] = c0;  // row-major 8 x 8
+        TS[jj * 64 + fr * 8 + fc + 1] = c1;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj) {
+      const int j = i + 1 + jj;
+      if (j < 4) {
+        double c0 = 0.0, c1 = 0.0;
+        mma8(c0, c1, [&](int m, int kk) { return -DI[i * 64 + kk * 8 + m]; },
+             [&](int kk, int n) { return TS[jj * 64 + kk * 8 + n]; });
+        at(i, j, fr, fc) = c0;
+        at(i, j, fr, fc + 1) = c1;
+      }
+    }
+    __syncwarp();
+  }
+  for (int e = lane; e < 4 * 64; e += 32) {  // diagonal blocks <- Dinv_kk
+    const int k = e >> 6, c = (e >> 3) & 7, r = e & 7;
+    at(k, k, r, c) = DI[e];
+  }
+  __syncwarp();
+  return __any_sync(0xffffffffu, bad);
+}
+
+// Factor + invert diagonal tile (b, b) (width m) through the scratch S.
+__device__ __forceinline__ bool ci_diag_tile(double* tile, int m, int last, double floor,
+                                             double* S, double* DI, double* TS) {
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < 32 * 32; e += 32) {
+    const int c = e >> 5, r = e & 31;
+    S[c * kTLD + r] = c < m ? (r <= c ? tile[c * kTLD + r] : 0.0) : (r == c ? 1.0 : 0.0);
+  }
+  __syncwarp();
+  const bool bad = ci_diag32(S, DI, TS, last, floor);
+  for (int e = lane; e < 32 * m; e += 32) {
+    const int c = e >> 5, r = e & 31;
+    tile[c * kTLD + r] = r <= c ? S[c * kTLD + r] : 0.0;
+  }
+  __syncwarp();
+  return bad;
+}
 
 __device__ __forceinline__ void ci_syrk_item(const CITiles& T, int b, int I, int J, int n0) {
   const int K = T.K;
@@ -192,10 +285,12 @@ __device__ __forceinline__ void ci_syrk_item(const CITiles& T, int b, int I, int
   ci_put<1>(T.tile(I, J), wJ, n0, acc);
 }
 
-__global__ void __launch_bounds__(kCholinvThreads) k_cholinv(CholinvArgs a) {
+__global__ void __maxnreg__(255) k_cholinv(CholinvArgs a) {
   extern __shared__ __align__(128) double smem[];
   __shared__ int s_bad;
   __shared__ double s_red[kCI_W];
+  __shared__ __align__(16) double s_S[32 * kTLD];  // diagonal-tile scratch (identity padded)
+  __shared__ double s_DI[4 * 64], s_TS[4 * 64];
   __shared__ __align__(8) uint64_t s_bar;
   const int K = a.K;
   if (a.gate && *a.gate == 0) return;
@@ -205,7 +300,7 @@ __global__ void __launch_bounds__(kCholinvThreads) k_cholinv(CholinvArgs a) {
   const int64_t tsz = tpu_size(K);
   CITiles T;
   T.K = K;
-  T.base = a.use_smem ? smem : a.Rinv;
+  T.base = a.use_smem ? smem : a.RD;
   CI_STAMP(0);
 
   double shift = 0.0;
@@ -214,8 +309,7 @@ __global__ void __launch_bounds__(kCholinvThreads) k_cholinv(CholinvArgs a) {
   if (a.use_smem && tid == 0) mbar_init(&s_bar, 1);
   for (int attempt = 0; attempt < 2; ++attempt) {
     if (a.use_smem) {
-      // ---- bulk copy of the TPU image into shared memory (phase = attempt) ----
-      if (tid == 0) {
+      if (tid == 0) {  // bulk copy of the TPU image (mbarrier phase = attempt)
         const uint32_t bytes = (uint32_t)(tsz * sizeof(double));
         mbar_expect_tx(&s_bar, bytes);
         const uint32_t chunk = 32768;
@@ -226,13 +320,10 @@ __global__ void __launch_bounds__(kCholinvThreads) k_cholinv(CholinvArgs a) {
       __syncthreads();
       mbar_wait(&s_bar, (uint32_t)attempt);
     } else {
-      // large K: work on a global (L2-resident) copy
-      for (int64_t e = tid; e < tsz; e += kCholinvThreads) a.Rinv[e] = a.G[e];
-      __threadfence_block();
+      for (int64_t e = tid; e < tsz; e += kCholinvThreads) a.RD[e] = a.G[e];
     }
     __syncthreads();
-    // trace (shift, pivot floor, cond estimate) in a fixed order
-    if (warp == 0) {
+    if (warp == 0) {  // trace (shift, pivot floor, cond estimate), fixed order
       double t = 0.0;
       for (int i = lane; i < K; i += 32) t += T.base[tpu_idx(K, i, i)];
       t = warp_sum(t);
@@ -248,14 +339,13 @@ __global__ void __launch_bounds__(kCholinvThreads) k_cholinv(CholinvArgs a) {
     const double pivot_floor = 4.930380657631324e-32 * tr;  // eps^2 tr(G)
     __syncthreads();
     CI_STAMP(1);
-    // Iteration b = -1 only factors the first diagonal tile; iteration b
-    // applies panel b and, with look-ahead, factors diagonal tile b + 1 (warp
-    // 0) while warps 1..7 finish the trailing update of panel b.
+    // Iteration b = -1 only factors diagonal tile 0; iteration b applies
+    // panel b and, with look-ahead, warp 0 updates + factors diagonal tile
+    // b + 1 while warps 1..7 finish the trailing update of panel b.
     for (int b = -1; b < nb && !s_bad; ++b) {
       if (b >= 0) {
-        const double* Db = T.tile(b, b);
-        // ---- panel: R(b, J) = Dinv_b^T G(b, J), J > b.  Items (J, column half)
-        //      read and write disjoint columns, so each is updated in place. ----
+        const double* Db = T.tile(b, b);  // Dinv_b
+        // panel: R(b, J) = Dinv_b^T G(b, J); items (J, column half) are column-disjoint
         const int nitems = (nb - 1 - b) * 2;
         for (int it = warp; it < nitems; it += kCI_W) {
           const int J = b + 1 + (it >> 1), n0 = 16 * (it & 1);
@@ -270,7 +360,7 @@ __global__ void __launch_bounds__(kCholinvThreads) k_cholinv(CholinvArgs a) {
           ci_put<0>(tj, wJ, n0, acc);
         }
         __syncthreads();
-        CI_STAMP(4 + 2 * b);
+        CI_STAMP(4 + 3 * b);
       }
       if (b + 1 >= nb) break;
       const int nx = b + 1;
@@ -280,15 +370,18 @@ __global__ void __launch_bounds__(kCholinvThreads) k_cholinv(CholinvArgs a) {
           if (tpu_w(nx, K) > 16) ci_syrk_item(T, b, nx, nx, 16);
           __syncwarp();
         }
-        const bool bad = ci_diag(T.tile(nx, nx), tpu_w(nx, K), nx == nb - 1 ? tpu_w(nx, K) - 1 : -1,
-                                 pivot_floor);
+        const int mx = tpu_w(nx, K);
+        if (nx == 1) CI_STAMP(60);
+        const bool bad = ci_diag_tile(T.tile(nx, nx), mx, nx == nb - 1 ? mx - 1 : -1, pivot_floor,
+                                      s_S, s_DI, s_TS);
+        if (nx == 1) CI_STAMP(61);
         if (bad && lane == 0) s_bad = 1;
       } else if (b >= 0) {
         int it = 0;
         for (int J = b + 1; J < nb; ++J) {
           const int wJ = tpu_w(J, K);
           for (int I = b + 1; I <= J; ++I) {
-            if (I == b + 1 && J == b + 1) continue;
+            if (I == nx && J == nx) continue;
             for (int h = 0; h < 2; ++h) {
               const int n0 = 16 * h;
               if (n0 >= wJ) continue;
@@ -299,7 +392,7 @@ __global__ void __launch_bounds__(kCholinvThreads) k_cholinv(CholinvArgs a) {
         }
       }
       __syncthreads();
-      if (b >= 0) CI_STAMP(5 + 2 * b);
+      if (b >= 0) CI_STAMP(5 + 3 * b);
     }
     if (!s_bad) break;
     if (a.pass == 0 && !shifted) {
@@ -315,85 +408,17 @@ __global__ void __launch_bounds__(kCholinvThreads) k_cholinv(CholinvArgs a) {
     return;
   }
   CI_STAMP(40);
-
-  // ---- in-place inverse, row blocks bottom-up ----
-  for (int I = nb - 2; I >= 0; --I) {
-    const int nitems = (nb - 1 - I) * 2;
-    const double* Di = T.tile(I, I);
-    // W(I, J) = -Dinv_I R(I, J): column-disjoint items, in place
-    for (int it = warp; it < nitems; it += kCI_W) {
-      const int J = I + 1 + (it >> 1), n0 = 16 * (it & 1);
-      const int wJ = tpu_w(J, K);
-      if (n0 >= wJ) continue;
-      double* tj = T.tile(I, J);
-      double acc[4][2][2];
-      ci_zero(acc);
-      ci_mma(acc, n0, [&](int mm, int k) { return Di[k * kTLD + mm]; },
-             [&](int k, int n) { return n < wJ ? tj[n * kTLD + k] : 0.0; });
-      __syncwarp();
-      ci_put<2>(tj, wJ, n0, acc);
-    }
-    __syncthreads();
-    // Rinv(I, J) = sum_{L=I+1..J} W(I, L) Rinv(L, J): reads all of row I, so
-    // every item is computed before any is written (registers, <= 2 per warp,
-    // or the global scratch row for large K)
-    auto item_rinv = [&](int it, double (&acc)[4][2][2]) {
-      const int J = I + 1 + (it >> 1), n0 = 16 * (it & 1);
-      const int wJ = tpu_w(J, K);
-      ci_zero(acc);
-      for (int L = I + 1; L <= J; ++L) {
-        const int wL = tpu_w(L, K);
-        const double* w = T.tile(I, L);
-        const double* rl = T.tile(L, J);
-        ci_mma(acc, n0, [&](int mm, int k) { return k < wL ? w[k * kTLD + mm] : 0.0; },
-               [&](int k, int n) { return n < wJ ? rl[n * kTLD + k] : 0.0; });
-      }
-    };
-    if (nitems <= 2 * kCI_W) {
-      double acc[2][4][2][2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int it = warp + h * kCI_W;
-        if (it < nitems && 16 * (it & 1) < tpu_w(I + 1 + (it >> 1), K)) item_rinv(it, acc[h]);
-      }
-      __syncthreads();
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int it = warp + h * kCI_W;
-        const int J = I + 1 + (it >> 1), n0 = 16 * (it & 1);
-        if (it < nitems && n0 < tpu_w(J, K)) ci_put<0>(T.tile(I, J), tpu_w(J, K), n0, acc[h]);
-      }
-    } else {
-      for (int it = warp; it < nitems; it += kCI_W) {
-        const int J = I + 1 + (it >> 1), n0 = 16 * (it & 1);
-        if (n0 >= tpu_w(J, K)) continue;
-        double acc[4][2][2];
-        item_rinv(it, acc);
-        ci_put<0>(a.scratch + (size_t)(J - I - 1) * 32 * kTLD, tpu_w(J, K), n0, acc);
-      }
-      __syncthreads();
-      for (int it = warp; it < nitems; it += kCI_W) {
-        const int J = I + 1 + (it >> 1), n0 = 16 * (it & 1);
-        const int wJ = tpu_w(J, K);
-        if (n0 >= wJ) continue;
-        const double* src = a.scratch + (size_t)(J - I - 1) * 32 * kTLD;
-        double* dst = T.tile(I, J);
-        for (int e = lane; e < 16 * 32; e += 32) {
-          const int c = n0 + (e >> 5), r = e & 31;
-          if (c < wJ) dst[c * kTLD + r] = src[c * kTLD + r];
-        }
-      }
-    }
-    __syncthreads();
-  }
   CI_STAMP(41);
-
-  // ---- cond(R) estimate (pass A): ||R||_F^2 = tr(G) + K shift; ||Rinv||_F^2 ----
+  // ---- pass A: cond lower bound ||R||_F^2 = tr(G) + K shift, ||R^-1||_F^2 >= sum ||Dinv_J||_F^2 ----
   if (a.pass == 0) {
     double ss = 0.0;
-    for (int64_t e = tid; e < tsz; e += kCholinvThreads) {
-      const double v = T.base[e];
-      ss = fma(v, v, ss);
+    for (int J = warp; J < nb; J += kCI_W) {
+      const double* dt = T.tile(J, J);
+      const int w = tpu_w(J, K);
+      for (int e = lane; e < 32 * w; e += 32) {
+        const double v = dt[(e >> 5) * kTLD + (e & 31)];
+        ss = fma(v, v, ss);
+      }
     }
     ss = warp_sum(ss);
     if (lane == 0) s_red[warp] = ss;
@@ -401,13 +426,13 @@ __global__ void __launch_bounds__(kCholinvThreads) k_cholinv(CholinvArgs a) {
     if (tid == 0) {
       double t = 0.0;
       for (int w = 0; w < kCI_W; ++w) t += s_red[w];
-      const double cond_f = sqrt((tr + K * shift) * t);
+      const double cond_lb = sqrt((tr + K * shift) * t);
       a.flags[0] = shifted;
       a.flags[1] = 0;
-      a.flags[2] = (shifted || !(cond_f <= 16.0 * K)) ? 1 : 0;
+      a.flags[2] = (a.force_b || shifted || !(cond_lb <= 8.0 * K)) ? 1 : 0;
     }
   }
-  // ---- write Rinv (TPU) ----
+  // ---- write RD (TPU) ----
   if (a.use_smem) {
     fence_proxy_async_smem();
     __syncthreads();
@@ -415,12 +440,101 @@ __global__ void __launch_bounds__(kCholinvThreads) k_cholinv(CholinvArgs a) {
       const uint32_t bytes = (uint32_t)(tsz * sizeof(double));
       const uint32_t chunk = 32768;
       for (uint32_t off = 0; off < bytes; off += chunk)
-        bulk_s2g(reinterpret_cast<char*>(a.Rinv) + off, reinterpret_cast<const char*>(smem) + off,
+        bulk_s2g(reinterpret_cast<char*>(a.RD) + off, reinterpret_cast<const char*>(smem) + off,
                  min(chunk, bytes - off));
       bulk_commit_wait_all();
     }
   }
   CI_STAMP(42);
 }
+
+// ---------------------------------------------------------------------------
+// X = B R^-1 for R in RD format, by blocked right substitution over tile
+// columns: X(:, J) = (B(:, J) - sum_{L<J} X(:, L) R(L, J)) Dinv_J.
+// One CTA per 32-row block of B (row blocks are independent); 2 warps
+// (column halves); the CTA's row block of X stays in shared memory.
+//   dense mode: B, X row-major [rows][ld]           (Q2 = Q1 R_A^-1)
+//   tpu mode:   B, X upper-triangular TPU (K x K)   (S = T R_A^-1)
+constexpr int kTrsmThreads = 64;
+
+template <bool TPU>
+__global__ void __launch_bounds__(kTrsmThreads)
+    k_trsm_right(const double* __restrict__ B, const double* __restrict__ RD, double* __restrict__ X,
+                 int64_t rows, int K, int64_t ld, const int* gate) {
+  if (gate && *gate == 0) return;
+  extern __shared__ __align__(16) double xs[];  // tile columns of this row block, [nb][32 cols][kTLD]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nb = (K + 31) / 32;
+  const int I = blockIdx.x;  // row block
+  const int64_t r0 = (int64_t)I * 32;
+  const int jstart = TPU ? I : 0;
+  const int n0 = 16 * warp;
+  for (int J = jstart; J < nb; ++J) {
+    const int wJ = tpu_w(J, K);
+    double acc[4][2][2];
+    ci_zero(acc);
+    double* xj = xs + (size_t)J * 32 * kTLD;
+    if (n0 < wJ) {
+      for (int L = jstart; L < J; ++L) {
+        const int wL = tpu_w(L, K);
+        const double* rl = RD + tpu_tile(K, L, J);
+        const double* xl = xs + (size_t)L * 32 * kTLD;
+        ci_mma(acc, n0, [&](int mm, int k) { return k < wL ? xl[k * kTLD + mm] : 0.0; },
+               [&](int k, int n) { return n < wJ ? __ldg(rl + n * kTLD + k) : 0.0; });
+      }
+      // Y(:, J) = B(:, J) - acc, staged in xs
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = 8 * i + (lane >> 2), c = n0 + 8 * j + 2 * (lane & 3) + e;
+            if (c < wJ) {
+              double bv = 0.0;
+              if (TPU) {
+                const int gr = 32 * I + r, gc = 32 * J + c;
+                if (gr < K && gr <= gc) bv = B[tpu_idx(K, gr, gc)];
+              } else if (r0 + r < rows) {
+                bv = B[(r0 + r) * ld + 32 * J + c];
+              }
+              xj[c * kTLD + r] = bv - acc[i][j][e];
+            }
+          }
+    }
+    __syncthreads();
+    // X(:, J) = Y(:, J) Dinv_J
+    if (n0 < wJ) {
+      const double* dj = RD + tpu_tile(K, J, J);
+      ci_zero(acc);
+      ci_mma(acc, n0, [&](int mm, int k) { return k < wJ ? xj[k * kTLD + mm] : 0.0; },
+             [&](int k, int n) { return n < wJ ? __ldg(dj + n * kTLD + k) : 0.0; });
+    }
+    __syncthreads();
+    if (n0 < wJ) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = 8 * i + (lane >> 2), c = n0 + 8 * j + 2 * (lane & 3) + e;
+            if (c < wJ) {
+              xj[c * kTLD + r] = acc[i][j][e];
+              if (TPU) {
+                const int gr = 32 * I + r, gc = 32 * J + c;
+                if (gr < K && (gr <= gc || (gr >> 5) == (gc >> 5)))
+                  X[tpu_idx(K, gr, gc)] = gr <= gc ? acc[i][j][e] : 0.0;
+              } else if (r0 + r < rows) {
+                X[(r0 + r) * ld + 32 * J + c] = acc[i][j][e];
+              }
+            }
+          }
+    }
+    __syncthreads();
+  }
+}
+
+inline size_t trsm_smem_bytes(int K) { return (size_t)((K + 31) / 32) * 32 * kTLD * sizeof(double); }
 
 }  // namespace tfk

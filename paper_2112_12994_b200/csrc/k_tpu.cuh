@@ -58,81 +58,6 @@ struct FwdRows {
 };
 
 // ---------------------------------------------------------------------------
-// C = A B for upper-triangular TPU matrices (K x K); one warp per 32 x 16
-// half tile of C, DMMA m8n8k4.  C(I, J) = sum_{L=I..J} A(I, L) B(L, J).
-constexpr int kTrmmWarps = 8;
-
-__global__ void __launch_bounds__(kTrmmWarps * 32)
-    k_trmm_tpu(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
-               int K, const int* gate) {
-  if (gate && *gate == 0) return;
-  const int nb = (K + 31) / 32;
-  const int lane = threadIdx.x & 31;
-  const int item = blockIdx.x * kTrmmWarps + (threadIdx.x >> 5);
-  // items: (I, J, half) for I <= J
-  int it = item, I = 0, J = 0, h = 0;
-  {
-    int found = 0;
-    for (int jj = 0; jj < nb && !found; ++jj)
-      for (int ii = 0; ii <= jj && !found; ++ii) {
-        if (it < 2) {
-          I = ii;
-          J = jj;
-          h = it;
-          found = 1;
-        } else {
-          it -= 2;
-        }
-      }
-    if (!found) return;
-  }
-  const int wJ = tpu_w(J, K);
-  const int n0 = 16 * h;
-  if (n0 >= wJ) return;
-  double acc[4][2][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  for (int L = I; L <= J; ++L) {
-    const int wL = tpu_w(L, K);
-    const double* a = A + tpu_tile(K, I, L);
-    const double* b = B + tpu_tile(K, L, J);
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const int k = 4 * kk + (lane & 3);
-      double af[4], bf[2];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = k < wL ? a[k * kTLD + 8 * i + (lane >> 2)] : 0.0;
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int n = n0 + 8 * j + (lane >> 2);
-        bf[j] = n < wJ ? b[n * kTLD + k] : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
-  }
-  double* c = C + tpu_tile(K, I, J);
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int r = 8 * i + (lane >> 2), cc = n0 + 8 * j + 2 * (lane & 3) + e;
-        if (cc < wJ) c[cc * kTLD + r] = (I == J && r > cc) ? 0.0 : acc[i][j][e];
-      }
-}
-
-inline int trmm_items(int K) {
-  const int nb = (K + 31) / 32;
-  return nb * (nb + 1);  // (I <= J) tiles x 2 halves
-}
-
-// ---------------------------------------------------------------------------
 // Solve-state flags (per context): [0] shifted (pass A broke down),
 // [1] failed, [2] need pass B, [3] unused.
 struct SolveFlags {

