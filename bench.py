@@ -117,44 +117,111 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- CPU port
-def cpu_sweep_estimate(y, p_bar, sweeps, budget_s=25.0):
-    """Single-threaded oracle port timed on a lag sample and extrapolated.
+def cpu_sweep_estimate(y, p_bar, sweeps, n_pass=1_000_000, c_cap=5_000, rh_rows=60_000):
+    """Single-threaded oracle port timed on a bounded sample, extrapolated per part.
 
-    LSAR: t(p) = a + b p + g p^2 fitted to timed lag bodies (lsar.cpp:70-98 at
-    lag p on the full series) and summed over p = 1..p_bar.  RH: per-lag cost
-    is the LSAR solve part (sampling + gather + QR) plus an upfront term timed
-    on a 1/10 prefix of the series and scaled by rows (labelled extrapolated).
+    A lag body of the reference splits into parts with known size scaling:
+      * O(w) + O(w p): leverage update + distribution + c draws (lsar.cpp:83-93,
+        sketch.cpp:20-59) and the per-tap residual (toeplitz.cpp:84-98) -- timed
+        on a prefix of n_pass rows at p in {1, p_bar/2, p_bar}, fitted a + b p and
+        scaled by w / w';
+      * O(c p^2): sampled gather + CPQR solve (sketch.cpp:61-79,
+        toeplitz.cpp:57-71) -- timed on c' = min(c, c_cap) rows at p in
+        {p_bar/4, p_bar/2, p_bar}, fitted as a quadratic in p and scaled by c / c'.
+    LSAR = sum over p of all parts; RH = the upfront phase (repeated_halving.cpp:
+    126-189, timed on two prefixes, linear in rows) + per lag one sampling
+    draw from the fixed distribution and the solve part (repeated_halving.cpp:
+    205-231).  Returns (total seconds, per-sweep detail, description).
     """
     from oracle import oracle as orc
     orc.lib()
-    lags = [1, 25, 50, 100, 150]
-    lags = [p for p in lags if p <= p_bar]
+    n = y.size
+    w = n - p_bar
+    yp = np.ascontiguousarray(y[: min(n, n_pass + p_bar)])
+    wp = yp.size - p_bar
+    rng = np.random.default_rng(7)
+    pp = np.arange(1, p_bar + 1, dtype=float)
+    # O(w p) residual, per row
+    P1 = sorted({1, max(1, p_bar // 2), p_bar})
+    t_res = []
+    for p in P1:
+        phi = rng.standard_normal(p) * 0.01
+        t0 = time.perf_counter()
+        orc.residuals(yp[p_bar - p:], wp + p, p, phi)
+        t_res.append(time.perf_counter() - t0)
+    cr = np.polyfit(np.array(P1, float), np.array(t_res), 1) if len(P1) > 1 else [0.0, t_res[0]]
+    res_sweep = float(np.sum(np.maximum(np.polyval(cr, pp), 0.0))) * (w / wp)
+    # O(w) leverage update + distribution (+ draws, per c)
+    s0 = orc.init_leverage_p1(yp[:wp])
+    r0 = rng.standard_normal(wp)
+    t0 = time.perf_counter()
+    s1 = orc.leverage_update(s0, r0)
+    dist = orc.leverage_to_distribution(s1)
+    t_upd = (time.perf_counter() - t0) * (w / wp)
+    solve_fit, samp, solve_fit_cp = {}, {}, {}
+    P2 = sorted({max(1, p_bar // 4), max(1, p_bar // 2), p_bar})
+    for c in sorted({c for _, c in sweeps}):
+        t0 = time.perf_counter()
+        orc.sample_rows(dist, c, 11)
+        samp[c] = (time.perf_counter() - t0) * (w / wp)
+        cp = min(c, c_cap)
+        if cp in solve_fit_cp:
+            solve_fit[c] = solve_fit_cp[cp] * (c / cp)
+            continue
+        ts = []
+        for p in P2:
+            idx = rng.integers(0, wp - 1, cp)
+            wt = np.ones(cp)
+            t0 = time.perf_counter()
+            a, b = orc.apply_sample(yp, wp + p, p, idx, wt)
+            orc.solve_exact(a, b)
+            ts.append(time.perf_counter() - t0)
+        deg = min(2, len(P2) - 1)
+        cs_ = np.polyfit(np.array(P2, float), np.array(ts), deg)
+        solve_fit_cp[cp] = float(np.sum(np.maximum(np.polyval(cs_, pp), 0.0)))
+        solve_fit[c] = solve_fit_cp[cp] * (c / cp)
+    # RH upfront (halving + upward sampling + final unsketched scores) at c' = c_cap:
+    # linear in rows from two prefixes; for c > c' add the extra CPQR of the c x k
+    # level matrices (the solve part at p_bar scaled by c) once per level.
+    k = p_bar + 1
+
+    def depth(c, m):
+        base = max(c, 10 * k * int(np.ceil(np.log(k + 1.0))))
+        d = 0
+        while m > base:
+            m //= 2
+            d += 1
+        return d
+
+    up = None
+    if any(m_ == "rh" for m_, _ in sweeps):
+        cu = min(c_cap, min(c for m_, c in sweeps if m_ == "rh"))
+        r1, r2 = rh_rows // 2, rh_rows
+        t1 = orc.rh_time_upfront(np.ascontiguousarray(y[: r1 + p_bar]), p_bar, cu, 7)
+        t2 = orc.rh_time_upfront(np.ascontiguousarray(y[: r2 + p_bar]), p_bar, cu, 7)
+        slope = (t2 - t1) / (r2 - r1)
+        up = {"c0": cu, "t0": t1 + slope * (w - r1)}
+    qr_pbar = {}
+    for c in solve_fit:
+        # single-lag CPQR at p = p_bar for c rows (for the RH level-factor correction)
+        qr_pbar[c] = solve_fit[c] / max(1.0, float(np.sum((pp / p_bar) ** 2)))
     total = 0.0
     detail = []
-    t_start = time.time()
     for method, c in sweeps:
-        ts = []
-        for p in lags:
-            ts.append(orc.lsar_time_one_lag(y, p_bar, c, p, 7))
-        P = np.array(lags, float)
-        A = np.stack([np.ones_like(P), P, P * P], 1)
-        coef, *_ = np.linalg.lstsq(A, np.array(ts), rcond=None)
-        pp = np.arange(1, p_bar + 1, dtype=float)
-        est = float(np.sum(np.maximum(coef[0] + coef[1] * pp + coef[2] * pp * pp, 0.0)))
-        if method == "rh":
-            m = y.size - p_bar
-            sub = y[: max(m // 10, 20 * p_bar)]
-            t0 = time.time()
-            f = orc.rh_fit(sub, p_bar, c, 7)
-            up = f.upfront_seconds * (y.size / sub.size)
-            # RH lag bodies skip the O(w) residual pass: keep the p^2 (solve) part only
-            est = float(np.sum(np.maximum(coef[0] * 0.5 + coef[2] * pp * pp, 0.0))) + up
-            del t0
+        if method == "lsar":
+            est = res_sweep + p_bar * (t_upd + samp[c]) + solve_fit[c]
+        else:
+            upc = up["t0"]
+            if c > up["c0"]:
+                upc += depth(c, w) * max(0.0, qr_pbar[c] - qr_pbar[c] * up["c0"] / c)
+            est = upc + p_bar * samp[c] + solve_fit[c]
         total += est
         detail.append({"method": method, "c": c, "sweep_s": est})
-        if time.time() - t_start > budget_s * 4:
-            break
-    return total, detail, lags
+    desc = (f"oracle port, 1 thread, bounded sample extrapolated per part: residual pass and "
+            f"leverage/draws on a {wp}-row prefix at p in {P1} (scaled by rows), gather+CPQR on "
+            f"min(c,{c_cap}) rows at p in {P2} (scaled by c), RH upfront at c={c_cap} on "
+            f"{rh_rows // 2}/{rh_rows}-row prefixes (linear in rows; + level CPQR for larger c)")
+    return total, detail, desc
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -313,13 +380,10 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        est, detail, lags = cpu_sweep_estimate(y, p_bar, sweeps)
+        t0 = time.time()
+        est, detail, desc = cpu_sweep_estimate(y, p_bar, sweeps)
         cpu = {"value": ro_step / est, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": (f"oracle port (single thread, like the reference), lag bodies timed at "
-                          f"p in {lags} on the full series per sweep, t(p)=a+bp+gp^2 summed over "
-                          f"p=1..{p_bar}; RH upfront timed on a 1/10 prefix scaled by rows "
-                          f"(extrapolated)"),
-               "sweeps": detail}
+               "sample": f"{desc}; wall {time.time() - t0:.1f}s", "sweeps": detail}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -351,12 +415,13 @@ def run_reference(args):
     sweeps = sweeps_for(cs, True)
     ro_step = p_bar * (n - p_bar) * len(sweeps)
     # each step: the bounded lag sample of every sweep (oracle port, 1 thread)
-    for _ in range(max(0, min(args.warmup, 1))):
-        cpu_sweep_estimate(y[: max(n // 100, 10 * p_bar)], p_bar, sweeps[:1])
+    for _ in range(args.warmup):  # small warm-up (page-in, library load)
+        cpu_sweep_estimate(y[: 20 * p_bar + 4000], p_bar, sweeps[:1], n_pass=10_000, c_cap=2 * p_bar,
+                           rh_rows=4000)
     ests = []
     t0 = time.time()
-    for _ in range(max(1, min(args.steps, 2))):
-        est, detail, lags = cpu_sweep_estimate(y, p_bar, sweeps)
+    for _ in range(max(1, args.steps)):
+        est, detail, desc = cpu_sweep_estimate(y, p_bar, sweeps)
         ests.append(est)
     wall = time.time() - t0
     est = float(np.median(ests))
@@ -370,8 +435,8 @@ def run_reference(args):
                    "sweeps": [f"{m}:s={c}" for m, c in sweeps], "rows_orders_per_step": ro_step},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
                          "sample": (f"oracle port of the reference (Eigen absent, reference not "
-                                    f"buildable), single thread; lag bodies at p in {lags}, "
-                                    f"extrapolated per sweep; wall {wall:.1f}s"),
+                                    f"buildable); {desc}; median of {len(ests)} steps, "
+                                    f"wall {wall:.1f}s"),
                          "sweeps": detail},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

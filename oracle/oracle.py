@@ -74,6 +74,8 @@ def lib():
         L.orc_default_base_threshold.argtypes = [C.c_int64, C.c_int64]
         L.orc_default_gaussian_rows.restype = C.c_int64
         L.orc_default_gaussian_rows.argtypes = [C.c_int64]
+        L.orc_rh_time_upfront.restype = C.c_double
+        L.orc_rh_time_upfront.argtypes = [_f64p, C.c_int64, C.c_int, C.c_int64, C.c_uint64]
         L.orc_lsar_time_one_lag.restype = C.c_double
         L.orc_lsar_time_one_lag.argtypes = [_f64p, C.c_int64, C.c_int, C.c_int64, C.c_int, C.c_uint64]
         L.orc_select_order.argtypes = [_f64p, C.c_int, C.c_double]
@@ -269,6 +271,11 @@ def lsar_fit(y, p_bar: int, c: int, seed: int, fixed_idx=None, fixed_w=None,
 def lsar_time_one_lag(y, p_bar: int, c: int, p: int, seed: int = 1) -> float:
     y = f64(y)
     return float(lib().orc_lsar_time_one_lag(_p(y), y.size, p_bar, c, p, seed))
+
+
+def rh_time_upfront(y, p_bar: int, c: int, seed: int = 1) -> float:
+    y = f64(y)
+    return float(lib().orc_rh_time_upfront(_p(y), y.size, p_bar, c, seed))
 
 
 def rh_defaults(m: int, k: int, c: int, seed: int) -> RhCfg:

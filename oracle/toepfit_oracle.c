@@ -838,9 +838,10 @@ static void aug_row(const double* y, int p, int64_t i, double* out) {
   out[p] = y[p + i];
 }
 
-int orc_rh_fit(const double* y, int64_t n, int p_bar, int64_t c, const orc_rh_cfg* cfg_in,
-               uint64_t seed, orc_rh_diag* diag, double* taus, double* coefs_packed,
-               double* lag_seconds, double* upfront_seconds, int* p_star) {
+static int rh_fit_impl(const double* y, int64_t n, int p_bar, int64_t c, const orc_rh_cfg* cfg_in,
+                       uint64_t seed, orc_rh_diag* diag, double* taus, double* coefs_packed,
+                       double* lag_seconds, double* upfront_seconds, int* p_star,
+                       int upfront_only) {
   /* repeated_halving.cpp:191-232 */
   if (p_bar < 1) return fail(ORC_USAGE, "maximum lag must be at least 1");
   if (n <= (int64_t)p_bar + 1) return fail(ORC_DATA, "series too short for maximum lag %d", p_bar);
@@ -959,7 +960,7 @@ int orc_rh_fit(const double* y, int64_t n, int p_bar, int64_t c, const orc_rh_cf
     st = orc_leverage_to_distribution(scores, m, dist);
   }
   if (upfront_seconds) *upfront_seconds = now_seconds() - t0;
-  if (!st) {
+  if (!st && !upfront_only) {
     int64_t* idx = XMALLOC(int64_t, c);
     double* wt = XMALLOC(double, c);
     double* a = XMALLOC(double, c * (int64_t)p_bar);
@@ -993,6 +994,21 @@ int orc_rh_fit(const double* y, int64_t n, int p_bar, int64_t c, const orc_rh_cf
   free(scores);
   free(row); free(z); free(sidx); free(sw);
   return st;
+}
+
+int orc_rh_fit(const double* y, int64_t n, int p_bar, int64_t c, const orc_rh_cfg* cfg_in,
+               uint64_t seed, orc_rh_diag* diag, double* taus, double* coefs_packed,
+               double* lag_seconds, double* upfront_seconds, int* p_star) {
+  return rh_fit_impl(y, n, p_bar, c, cfg_in, seed, diag, taus, coefs_packed, lag_seconds,
+                     upfront_seconds, p_star, 0);
+}
+
+/* bench timing helper: the RH upfront phase alone (halving, upward sampling,
+ * final scores and distribution), default configuration. */
+double orc_rh_time_upfront(const double* y, int64_t n, int p_bar, int64_t c, uint64_t seed) {
+  double up = -1.0;
+  if (rh_fit_impl(y, n, p_bar, c, NULL, seed, NULL, NULL, NULL, NULL, &up, NULL, 1)) return -1.0;
+  return up;
 }
 
 /* ======================================================================
