@@ -82,6 +82,9 @@ typedef struct {
   int* depth_out;
   int64_t* idx_out;             /* [p_bar][c] */
   double* w_out;
+  int64_t* levels_out;          /* concatenated halving index sets, levels 1..depth */
+  int64_t* up_idx_out;          /* [depth][sample_count] upward-pass positions */
+  double* up_w_out;             /* [depth][sample_count] upward-pass weights */
 } tf_rh_diag;
 
 const char* tf_version(void);

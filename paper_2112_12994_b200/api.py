@@ -112,6 +112,14 @@ class RHConfig:
             raise UsageError("need at least one sketch row")
 
 
+def rh_level_sizes(m: int, base_threshold: int) -> list:
+    """Halving level sizes m, m/2, ... while above the base (repeated_halving.cpp:130-145)."""
+    sizes = [int(m)]
+    while sizes[-1] > base_threshold:
+        sizes.append(sizes[-1] // 2)
+    return sizes
+
+
 def derive_seed(seed: int, tag: int) -> int:
     return int(_abi.lib().tf_derive_seed(C.c_uint64(seed), C.c_uint64(tag)))
 
@@ -218,11 +226,21 @@ class Engine:
         depth = C.c_int(0)
         if want_diag:
             m = max(int(n) - pb, 1)
-            diag = dict(scores=np.zeros(m), idx=np.zeros((pb, c), np.int64), w=np.zeros((pb, c)))
+            ecfg = cfg if cfg is not None else RHConfig.defaults(m, pb + 1, c, derive_seed(seed, 0x5C07E5))
+            sizes = rh_level_sizes(m, ecfg.base_threshold)
+            sc = max(int(ecfg.sample_count), 1)
+            dep = len(sizes) - 1
+            diag = dict(scores=np.zeros(m), idx=np.zeros((pb, c), np.int64), w=np.zeros((pb, c)),
+                        levels_flat=np.zeros(max(sum(sizes[1:]), 1), np.int64),
+                        up_idx=np.zeros((max(dep, 1), sc), np.int64), up_w=np.zeros((max(dep, 1), sc)),
+                        level_sizes=sizes)
             d.scores_out = ptr(diag["scores"])
             d.idx_out = ptr(diag["idx"], _abi._i64p)
             d.w_out = ptr(diag["w"])
             d.depth_out = C.pointer(depth)
+            d.levels_out = ptr(diag["levels_flat"], _abi._i64p)
+            d.up_idx_out = ptr(diag["up_idx"], _abi._i64p)
+            d.up_w_out = ptr(diag["up_w"])
         ccfg = None
         if cfg is not None:
             ccfg = _abi.TfRhCfg(cfg.base_threshold, cfg.sample_count, cfg.gaussian_rows, cfg.seed)
@@ -232,6 +250,13 @@ class Engine:
                                            ptr(secs), C.byref(up), C.byref(pstar)))
         if diag is not None:
             diag["depth"] = depth.value
+            sizes, off, levels = diag["level_sizes"], 0, []
+            for l in range(1, len(sizes)):
+                levels.append(diag["levels_flat"][off:off + sizes[l]])
+                off += sizes[l]
+            diag["levels"] = levels
+            diag["up_idx"] = diag["up_idx"][:depth.value]
+            diag["up_w"] = diag["up_w"][:depth.value]
         return taus, coefs, secs, up.value, pstar.value, diag
 
     def probe_fp64_peak(self) -> float:

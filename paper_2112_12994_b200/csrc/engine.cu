@@ -16,6 +16,7 @@
 #include "k_cholinv.cuh"
 #include "k_gram.cuh"
 #include "k_pass.cuh"
+#include "k_rh.cuh"
 #include "k_sample.cuh"
 #include "k_tpu.cuh"
 
@@ -54,6 +55,7 @@ template struct DBuf<int64_t>;
 template struct DBuf<int>;
 template struct DBuf<uint64_t>;
 template struct DBuf<unsigned char>;
+template struct DBuf<long long>;
 
 static const char* reason_text(int reason) {
   switch (reason) {
@@ -63,6 +65,7 @@ static const char* reason_text(int reason) {
     case kReasonCholFail: return "compressed least-squares factorization failed";
     case kReasonRankDeficient: return "reference matrix is rank deficient";
     case kReasonZeroWindow: return "all-zero window; leverage undefined";
+    case kReasonSketchStream: return "gaussian sketch stream exhausted";
     default: return "numerical failure";
   }
 }
@@ -176,6 +179,21 @@ static void trsm_right(tf_context* ctx, const double* B, const double* RD, doubl
 
 static unsigned tpu_grid(int K) { return (unsigned)std::min<int64_t>(1024, (tpu_size(K) + 255) / 256); }
 
+// split-K workspace for every Gram up to K columns over `rows` rows
+static void reserve_gram(tf_context* ctx, int64_t rows, int Kmax) {
+  SolveBufs& b = ctx->sb;
+  size_t wmax = 0;
+  for (int K = 2; K <= Kmax; ++K) {
+    const GramPlan g = gram_plan(rows, K, ctx->sm_count);
+    wmax = std::max(wmax, (size_t)g.nsplit * g.npair * 4096);
+  }
+  b.W.need(wmax);
+  if (b.tickets.n < 4096) {
+    b.tickets.need(4096);
+    CK(cudaMemset(b.tickets.get(), 0, 4096 * sizeof(int)));
+  }
+}
+
 // Size every solve buffer for the largest system of a sweep up front so that
 // no cudaMalloc/cudaFree (which synchronise) happens between lags.
 static void reserve_solve(tf_context* ctx, int64_t c, int Kmax) {
@@ -194,25 +212,21 @@ static void reserve_solve(tf_context* ctx, int64_t c, int Kmax) {
   b.Q1.need((size_t)c * Kmax);
   b.Q2.need((size_t)c * Kmax);
   b.flags.need(4);
-  size_t wmax = 0;
-  for (int K = 2; K <= Kmax; ++K) {
-    const GramPlan g = gram_plan(c, K, ctx->sm_count);
-    wmax = std::max(wmax, (size_t)g.nsplit * g.npair * 4096);
-  }
-  b.W.need(wmax);
-  if (b.tickets.n < 4096) {
-    b.tickets.need(4096);
-    CK(cudaMemset(b.tickets.get(), 0, 4096 * sizeof(int)));
-  }
+  reserve_gram(ctx, c, Kmax);
 }
 
 // Preconditioned CholeskyQR solve of one sampled system (forward column
 // order, K = p + 1 columns, target last).  `Sprev` (TPU, K - 1) is the
 // previous lag's inverse factor (nullptr -> identity preconditioner);
 // `Snext` receives this lag's S = R^-1 for the next lag.
+// rev = 1: target-first column order (RH lags, RevRows); `rscal` points at the
+// squared residual norm that scales the carried preconditioner (LSAR: the
+// window's R_{p-1} = scal[0]; RH: the previous lag's sampled estimate), and
+// `rest_out` receives this lag's estimate (rev only).
 template <class L>
 static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const SolveOut& o,
-                       const double* Sprev, const double* phi_prev, double* Snext) {
+                       const double* Sprev, const double* phi_prev, double* Snext, int rev = 0,
+                       const double* rscal = nullptr, double* rest_out = nullptr) {
   SolveBufs& b = ctx->sb;
   reserve_solve(ctx, c, K);
   int* fl = b.flags.get();
@@ -230,6 +244,8 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
   pa.method = o.method;
   pa.lag = o.lag;
   pa.S_final = Snext;
+  pa.rev = rev;
+  pa.rest_out = rest_out;
   if (K == 2) {
     gram(ctx, ld, c, K, b.G.get(), nullptr);
     k_solve_k2<<<1, 1, 0, st>>>(b.G.get(), pa);
@@ -238,7 +254,8 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
     return;
   }
   if (Sprev && phi_prev)
-    k_precond<<<tpu_grid(K), 256, 0, st>>>(Sprev, phi_prev, ctx->scal.get(), b.T.get(), K);
+    k_precond<<<tpu_grid(K), 256, 0, st>>>(Sprev, phi_prev, rscal ? rscal : ctx->scal.get(),
+                                           b.T.get(), K);
   else
     k_tpu_identity<<<tpu_grid(K), 256, 0, st>>>(b.T.get(), K);
   LAUNCH_CHECK("k_precond");
@@ -496,7 +513,7 @@ __global__ void k_partials(const double* s, const double* r, int64_t w, double* 
     double sv = 0.0, rv = 0.0;
     if (row < rows) {
       sv = s[i0 + row];
-      rv = r[i0 + row];
+      rv = r ? r[i0 + row] : 0.0;
     }
     const double cA = warp_sum(sv), cB = warp_sum(rv * rv);
     const int crow = kPassThreads * u + kChunk * warp;
@@ -651,10 +668,360 @@ static void solve_sampled_op(tf_context* ctx, const double* y, int64_t n_used, i
   if (method_out) *method_out = m;
 }
 
-static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg, uint64_t seed,
+// ---------------------------------------------------------------------------
+// Repeated Halving (repeated_halving.cpp:126-232)
+
+static unsigned grid_for(int64_t n, const tf_context* ctx) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sm_count * 16));
+}
+
+// exclusive scan of int32 `in` (n) and f(i, excl, value) for every element
+template <class F>
+static void scan_apply(tf_context* ctx, const int* in, int64_t n, F f) {
+  const int64_t nt = (n + kScanTileN - 1) / kScanTileN;
+  ctx->rh_tsum.need(nt + 2);
+  long long* ts = ctx->rh_tsum.get();
+  k_scan_tile_sums<<<(unsigned)nt, kRhThreads, 0, ctx->stream>>>(in, n, ts);
+  k_scan_top<<<1, 1024, 0, ctx->stream>>>(ts, nt, ts + nt + 1);
+  k_scan_apply<F><<<(unsigned)nt, kRhThreads, 0, ctx->stream>>>(in, n, ts, f);
+  LAUNCH_CHECK("scan_apply");
+  g_launches += 3;
+}
+
+// one halving level: next = sorted first half of the partial shuffle of cur
+// (cur == nullptr: the identity level 0)
+static void rh_halve(tf_context* ctx, uint64_t seed, const int64_t* cur, int64_t size, int64_t* next) {
+  const int64_t half = size / 2;
+  cudaStream_t st = ctx->stream;
+  int* J = ctx->rh_J.get();
+  int* cnt = ctx->rh_cnt.get();
+  int* fill = ctx->rh_fill.get();
+  int* pick = ctx->rh_pick.get();
+  int* rej = ctx->rh_flag.get();
+  CK(cudaMemsetAsync(cnt, 0, size * sizeof(int), st));
+  CK(cudaMemsetAsync(fill, 0, size * sizeof(int), st));
+  CK(cudaMemsetAsync(pick, 0, size * sizeof(int), st));
+  CK(cudaMemsetAsync(rej, 0, sizeof(int), st));
+  k_halve_draw<<<grid_for(half, ctx), 256, 0, st>>>(seed, size, half, J, rej);
+  k_halve_draw_serial<<<1, 32, 0, st>>>(seed, size, half, J, rej);
+  k_halve_count<<<grid_for(half, ctx), 256, 0, st>>>(J, half, cnt);
+  LAUNCH_CHECK("k_halve_draw");
+  g_launches += 3;
+  scan_apply(ctx, cnt, size, StartF{ctx->rh_start.get()});
+  k_halve_scatter<<<grid_for(half, ctx), 256, 0, st>>>(J, half, ctx->rh_start.get(), fill, ctx->rh_bk.get());
+  k_halve_bucket_sort<<<grid_for(size, ctx), 256, 0, st>>>(cnt, ctx->rh_start.get(), size, ctx->rh_bk.get());
+  k_halve_resolve<<<grid_for(half, ctx), 256, 0, st>>>(J, half, cnt, ctx->rh_start.get(), ctx->rh_bk.get(), pick);
+  LAUNCH_CHECK("k_halve_resolve");
+  g_launches += 3;
+  scan_apply(ctx, pick, size, CompactF{cur, next});
+}
+
+// S (TPU, K) = R^-1 of the CholeskyQR of the approximation rows (forward order)
+static void rh_factor(tf_context* ctx, const FwdRows& ld, int64_t rows, int K, double* S) {
+  SolveOut o{ctx->rh_phis.get(), nullptr, 0, nullptr, nullptr, 0, ctx->status.get()};
+  solve_rows(ctx, ld, rows, K, o, nullptr, nullptr, S);
+}
+
+static void launch_draw_on(tf_context* ctx, const double* scores, int64_t w, uint64_t seed,
+                           int64_t c, int64_t* idx, double* wts) {
+  DrawArgs a;
+  a.seed = seed;
+  a.c = c;
+  a.scal = ctx->scal.get();
+  a.OT = ctx->OT.get();
+  a.ntile = (w + kPassTile - 1) / kPassTile;
+  a.tA = ctx->tileA.get();
+  a.tB = ctx->tileB.get();
+  a.chunkA = ctx->chunkA.get();
+  a.chunkB = ctx->chunkB.get();
+  a.s = scores;
+  a.r = nullptr;
+  a.w = w;
+  a.idx = idx;
+  a.wts = wts;
+  const int per = kDrawThreads / 32;
+  k_draw<<<(unsigned)((c + per - 1) / per), kDrawThreads, 0, ctx->stream>>>(a);
+  LAUNCH_CHECK("k_draw");
+  COUNT_LAUNCH();
+}
+
+// distribution state (chunk/tile partials, tile prefix, total) of plain scores
+static void score_distribution(tf_context* ctx, const double* scores, int64_t w) {
+  const int64_t ntile = (w + kPassTile - 1) / kPassTile;
+  k_partials<<<(unsigned)ntile, kPassThreads, 0, ctx->stream>>>(scores, nullptr, w, ctx->chunkA.get(),
+                                                               ctx->chunkB.get(), ctx->tileA.get(),
+                                                               ctx->tileB.get());
+  LAUNCH_CHECK("k_partials");
+  COUNT_LAUNCH();
+  launch_scan(ctx, ntile, 0, 0, /*unit_r=*/1);
+}
+
+static int64_t rh_default_base(int64_t c, int64_t k) {  // repeated_halving.hpp:67-70
+  const int64_t logk = (int64_t)std::ceil(std::log((double)k + 1.0));
+  return std::max<int64_t>(c, 10 * k * logk);
+}
+
+static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg_in, uint64_t seed,
                      const tf_rh_diag* d, double* taus, double* coefs, double* lag_seconds,
                      double* upfront_seconds, int* p_star) {
-  throw TfError{TF_USAGE, "rh sweep not built yet"};
+  // rh_fit argument checks (repeated_halving.cpp:191-200)
+  if (p_bar < 1) throw TfError{TF_USAGE, "maximum lag must be at least 1"};
+  if (ctx->n == 0) throw TfError{TF_USAGE, "no series uploaded"};
+  if (ctx->n <= (int64_t)p_bar + 1)
+    throw TfError{TF_DATA, "series too short for maximum lag " + std::to_string(p_bar)};
+  if (c < p_bar) throw TfError{TF_USAGE, "sample count below maximum lag"};
+  const int64_t m = ctx->n - p_bar;
+  const int K = p_bar + 1;
+  tf_rh_cfg cfg;
+  if (cfg_in) {
+    cfg = *cfg_in;
+  } else {  // RHConfig::defaults (repeated_halving.cpp:33-41)
+    cfg.sample_count = c;
+    cfg.base_threshold = rh_default_base(c, K);
+    cfg.gaussian_rows = (int64_t)std::ceil(8.0 * std::log((double)std::max<int64_t>(m, 2)));
+    cfg.seed = derive_seed(seed, 0x5c07e5ull);
+  }
+  // RHConfig::validate (repeated_halving.cpp:43-47)
+  if (cfg.sample_count < 1) throw TfError{TF_USAGE, "sample count must be positive"};
+  if (cfg.base_threshold < cfg.sample_count) throw TfError{TF_USAGE, "base threshold below sample count"};
+  if (cfg.gaussian_rows < 1) throw TfError{TF_USAGE, "need at least one sketch row"};
+  if (m >= (int64_t)INT32_MAX) throw TfError{TF_USAGE, "series too long for the halving index width"};
+  const int64_t sc = cfg.sample_count;
+  const int g = (int)cfg.gaussian_rows;
+  // level sizes are deterministic: size_{l+1} = size_l / 2 while size_l > base
+  std::vector<int64_t> lsz{m}, loff{0, 0};
+  while (lsz.back() > cfg.base_threshold) {
+    lsz.push_back(lsz.back() / 2);
+    loff.push_back(loff.back() + lsz.back());
+  }
+  const int depth = (int)lsz.size() - 1;
+  // levker_init row checks (repeated_halving.cpp:53-56)
+  const int64_t base_rows = lsz[depth];
+  if (base_rows < K || (depth > 0 && sc < K))
+    throw TfError{TF_NUMERICAL, "reference matrix has too few rows"};
+  const bool fixed = d && d->fixed_idx && d->fixed_w;
+  const bool fixed_lv = d && d->fixed_levels;
+  const bool fixed_up = d && d->fixed_up_idx && d->fixed_up_w;
+  cudaStream_t st = ctx->stream;
+  alloc_state(ctx, p_bar, c, m);
+  // buffers
+  const int64_t lvl_total = loff.back();
+  ctx->rh_lvl.need(std::max<int64_t>(lvl_total, 1));
+  if (depth > 0) {
+    ctx->rh_J.need(m / 2 + 1);
+    ctx->rh_bk.need(m / 2 + 1);
+    ctx->rh_cnt.need(m);
+    ctx->rh_start.need(m);
+    ctx->rh_fill.need(m);
+    ctx->rh_pick.need(m);
+  }
+  ctx->rh_flag.need(4);
+  const int64_t arows_max = std::max(base_rows, sc);
+  ctx->rh_aidx.need(std::max(arows_max, depth == 0 ? m : 0));
+  ctx->rh_aw.need(std::max(arows_max, depth == 0 ? m : 0));
+  ctx->rh_ones.need(std::max(arows_max, depth == 0 ? m : 0));
+  ctx->rh_sidx.need(sc);
+  ctx->rh_sw.need(sc);
+  ctx->rh_scores.need(m);
+  ctx->rh_S.need(tpu_size(K));
+  ctx->rh_phis.need(K + 1);
+  ctx->rh_rest.need(2);
+  const int Kp = g + K;
+  const int64_t max_norm = (int64_t)g * arows_max;
+  if (depth > 0) {
+    ctx->rh_norm.need(max_norm);
+    ctx->rh_ok.need((max_norm / 2 + 1) * 135 / 100 + 4096);
+    ctx->rh_Gp.need(tpu_size(Kp));
+    ctx->rh_H0.need((size_t)g * K);
+    ctx->rh_W.need((size_t)g * K);
+    reserve_gram(ctx, arows_max, Kp);
+  }
+  reserve_solve(ctx, std::max(arows_max, std::max(c, depth == 0 ? m : 0)), K);
+  ctx->rh_tsum.need((std::max(m, ((max_norm / 2 + 1) * 135 / 100 + 4096)) + kScanTileN - 1) / kScanTileN + 3);
+  if (fixed) {
+    const size_t tot = (size_t)p_bar * c;
+    for (size_t i = 0; i < tot; ++i)
+      if (d->fixed_idx[i] < 0 || d->fixed_idx[i] >= m) throw TfError{TF_USAGE, "sample index out of range"};
+    ctx->fidx.need(tot);
+    ctx->fw.need(tot);
+    CK(cudaMemcpyAsync(ctx->fidx.get(), d->fixed_idx, tot * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->fw.get(), d->fixed_w, tot * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  if (fixed_lv && lvl_total > 0) {
+    for (int64_t i = 0; i < lvl_total; ++i)
+      if (d->fixed_levels[i] < 0 || d->fixed_levels[i] >= m) throw TfError{TF_USAGE, "level index out of range"};
+    CK(cudaMemcpyAsync(ctx->rh_lvl.get(), d->fixed_levels, lvl_total * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  }
+  if (fixed_up && depth > 0) {
+    const size_t tot = (size_t)depth * sc;
+    ctx->rh_fup.need(tot);
+    ctx->rh_fupw.need(tot);
+    CK(cudaMemcpyAsync(ctx->rh_fup.get(), d->fixed_up_idx, tot * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->rh_fupw.get(), d->fixed_up_w, tot * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  const bool want_up = d && (d->up_idx_out || d->up_w_out) && depth > 0;
+  if (want_up) {
+    ctx->rh_fup.need((size_t)depth * sc);
+    ctx->rh_fupw.need((size_t)depth * sc);
+  }
+  const bool want_hist = d && (d->idx_out || d->w_out);
+  if (want_hist) {
+    ctx->idx_hist.need((size_t)p_bar * c);
+    ctx->w_hist.need((size_t)p_bar * c);
+  }
+  ensure_events(ctx, p_bar + 2);
+  const int64_t launches0 = g_launches;
+  CK(cudaEventRecord(ctx->events[0], st));
+  const double* y = ctx->y.get();
+  k_fill<<<grid_for(arows_max, ctx), 256, 0, st>>>(ctx->rh_ones.get(), std::max(arows_max, depth == 0 ? m : 0), 1.0);
+  COUNT_LAUNCH();
+  // ---- halving (repeated_halving.cpp:126-145) ----
+  auto level_ptr = [&](int l) -> int64_t* { return l == 0 ? nullptr : ctx->rh_lvl.get() + loff[l]; };
+  if (!fixed_lv)
+    for (int l = 1; l <= depth; ++l)
+      rh_halve(ctx, derive_seed(cfg.seed, 0x10000ull + (uint64_t)l), level_ptr(l - 1), lsz[l - 1], level_ptr(l));
+  // ---- base approximation: unweighted rows of the last level ----
+  int64_t arows = base_rows;
+  const int64_t* aidx;
+  if (depth == 0) {
+    k_iota<<<grid_for(m, ctx), 256, 0, st>>>(ctx->rh_aidx.get(), m);
+    COUNT_LAUNCH();
+    aidx = ctx->rh_aidx.get();
+  } else {
+    aidx = level_ptr(depth);
+  }
+  const double* aw = ctx->rh_ones.get();
+  // ---- upward pass (repeated_halving.cpp:146-180) ----
+  for (int i = depth - 1; i >= 0; --i) {
+    FwdRows B{y, aidx, aw, 0};
+    rh_factor(ctx, B, arows, K, ctx->rh_S.get());
+    // Gaussian sketch rows (g x arows), then GB = N^T B through the Gram of [N | B]
+    const uint64_t gseed = derive_seed(cfg.seed, 0x20000ull + (uint64_t)i);
+    const int64_t count = (int64_t)g * arows;
+    const int64_t attempts = (count / 2 + 1) * 135 / 100 + 4096;
+    k_polar_flags<<<grid_for(attempts, ctx), 256, 0, st>>>(gseed, attempts, ctx->rh_ok.get());
+    COUNT_LAUNCH();
+    scan_apply(ctx, ctx->rh_ok.get(), attempts, PolarF{gseed, count, ctx->rh_norm.get()});
+    k_check_normals<<<1, 1, 0, st>>>(ctx->rh_tsum.get() + ((attempts + kScanTileN - 1) / kScanTileN) + 1,
+                                     (count + 1) / 2, ctx->status.get());
+    COUNT_LAUNCH();
+    ConcatRows cr{ctx->rh_norm.get(), g, B};
+    gram(ctx, cr, arows, Kp, ctx->rh_Gp.get(), nullptr);
+    k_rh_h0<<<grid_for((int64_t)g * K, ctx), 256, 0, st>>>(ctx->rh_Gp.get(), Kp, g, ctx->rh_S.get(), K,
+                                                          ctx->rh_H0.get());
+    k_rh_w<<<grid_for((int64_t)g * K, ctx), 256, 0, st>>>(ctx->rh_H0.get(), ctx->rh_S.get(), K, g,
+                                                         ctx->rh_W.get());
+    g_launches += 2;
+    // sketched scores of every row of level i
+    const int64_t len = lsz[i];
+    WinRows rows_i{y, level_ptr(i)};
+    k_rowsq<WinRows, DenseW, false><<<(unsigned)((len + 63) / 64), kGramThreads, 0, st>>>(
+        rows_i, len, K, DenseW{ctx->rh_W.get(), g}, g, ctx->rh_scores.get());
+    LAUNCH_CHECK("k_rowsq");
+    COUNT_LAUNCH();
+    const int64_t* sidx = ctx->rh_sidx.get();
+    const double* sw = ctx->rh_sw.get();
+    if (fixed_up) {
+      sidx = ctx->rh_fup.get() + (size_t)i * sc;
+      sw = ctx->rh_fupw.get() + (size_t)i * sc;
+    } else {
+      score_distribution(ctx, ctx->rh_scores.get(), len);
+      launch_draw_on(ctx, ctx->rh_scores.get(), len, derive_seed(cfg.seed, 0x30000ull + (uint64_t)i), sc,
+                     ctx->rh_sidx.get(), ctx->rh_sw.get());
+    }
+    if (want_up && !fixed_up) {
+      CK(cudaMemcpyAsync(ctx->rh_fup.get() + (size_t)i * sc, sidx, sc * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(ctx->rh_fupw.get() + (size_t)i * sc, sw, sc * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    k_rh_compose<<<grid_for(sc, ctx), 256, 0, st>>>(sidx, sw, level_ptr(i), sc, ctx->rh_aidx.get(),
+                                                   ctx->rh_aw.get());
+    COUNT_LAUNCH();
+    aidx = ctx->rh_aidx.get();
+    aw = ctx->rh_aw.get();
+    arows = sc;
+  }
+  // ---- final unsketched scores over all m rows (repeated_halving.cpp:182-189) ----
+  {
+    FwdRows B{y, aidx, aw, 0};
+    rh_factor(ctx, B, arows, K, ctx->rh_S.get());
+    k_rowsq<WinRows, TpuW, true><<<(unsigned)((m + 63) / 64), kGramThreads, 0, st>>>(
+        WinRows{y, nullptr}, m, K, TpuW{ctx->rh_S.get(), K}, K, ctx->rh_scores.get());
+    LAUNCH_CHECK("k_rowsq");
+    COUNT_LAUNCH();
+    score_distribution(ctx, ctx->rh_scores.get(), m);
+  }
+  CK(cudaEventRecord(ctx->events[1], st));
+  // ---- per-lag solves from the fixed distribution (repeated_halving.cpp:205-231) ----
+  for (int p = 1; p <= p_bar; ++p) {
+    int64_t* idx = ctx->idx.get();
+    double* wts = ctx->wts.get();
+    if (fixed) {
+      idx = ctx->fidx.get() + (size_t)(p - 1) * c;
+      wts = ctx->fw.get() + (size_t)(p - 1) * c;
+    } else {
+      launch_draw_on(ctx, ctx->rh_scores.get(), m, derive_seed(seed, (uint64_t)p), c, idx, wts);
+    }
+    if (want_hist) {
+      CK(cudaMemcpyAsync(ctx->idx_hist.get() + (size_t)(p - 1) * c, idx, c * sizeof(int64_t),
+                         cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(ctx->w_hist.get() + (size_t)(p - 1) * c, wts, c * sizeof(double),
+                         cudaMemcpyDeviceToDevice, st));
+    }
+    SolveOut o;
+    o.phi = ctx->phi.get();
+    o.coefs = ctx->coefs.get();
+    o.coef_off = (int64_t)(p - 1) * p / 2;
+    o.taus = ctx->taus.get();
+    o.method = ctx->method.get();
+    o.lag = p;
+    o.status = ctx->status.get();
+    RevRows ld{y, idx, wts, p_bar};
+    double* Snext = (p & 1) ? ctx->sb.S1.get() : ctx->sb.S0.get();
+    const double* Sprev = (p & 1) ? ctx->sb.S0.get() : ctx->sb.S1.get();
+    solve_rows(ctx, ld, c, p + 1, o, p >= 2 ? Sprev : nullptr, p >= 2 ? ctx->phi.get() : nullptr, Snext,
+               /*rev=*/1, ctx->rh_rest.get(), ctx->rh_rest.get());
+    CK(cudaEventRecord(ctx->events[p + 1], st));
+  }
+  const int64_t launches = g_launches - launches0;
+  (void)launches;
+  CK(cudaStreamSynchronize(st));
+  int sth[3];
+  CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  if (sth[0] != 0 && sth[1] == 0 && sth[2] == kReasonCholFail)
+    throw TfError{TF_NUMERICAL, "reference matrix is rank deficient"};
+  raise_from_status(sth);
+  std::vector<double> t(p_bar);
+  CK(cudaMemcpy(t.data(), ctx->taus.get(), p_bar * sizeof(double), cudaMemcpyDeviceToHost));
+  if (taus) std::memcpy(taus, t.data(), p_bar * sizeof(double));
+  if (coefs)
+    CK(cudaMemcpy(coefs, ctx->coefs.get(), sizeof(double) * (size_t)p_bar * (p_bar + 1) / 2,
+                  cudaMemcpyDeviceToHost));
+  if (upfront_seconds) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->events[0], ctx->events[1]));
+    *upfront_seconds = ms * 1e-3;
+  }
+  if (lag_seconds)
+    for (int p = 1; p <= p_bar; ++p) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ctx->events[p], ctx->events[p + 1]));
+      lag_seconds[p - 1] = ms * 1e-3;
+    }
+  if (p_star) *p_star = tf_select_order(t.data(), p_bar, 1.96 / std::sqrt((double)c));
+  if (d) {
+    if (d->scores_out) CK(cudaMemcpy(d->scores_out, ctx->rh_scores.get(), sizeof(double) * m, cudaMemcpyDeviceToHost));
+    if (d->depth_out) *d->depth_out = depth;
+    if (d->levels_out && lvl_total > 0)
+      CK(cudaMemcpy(d->levels_out, ctx->rh_lvl.get(), sizeof(int64_t) * lvl_total, cudaMemcpyDeviceToHost));
+    if (want_up && d->up_idx_out)
+      CK(cudaMemcpy(d->up_idx_out, ctx->rh_fup.get(), sizeof(int64_t) * depth * sc, cudaMemcpyDeviceToHost));
+    if (want_up && d->up_w_out)
+      CK(cudaMemcpy(d->up_w_out, ctx->rh_fupw.get(), sizeof(double) * depth * sc, cudaMemcpyDeviceToHost));
+    if (d->idx_out)
+      CK(cudaMemcpy(d->idx_out, ctx->idx_hist.get(), sizeof(int64_t) * (size_t)p_bar * c, cudaMemcpyDeviceToHost));
+    if (d->w_out)
+      CK(cudaMemcpy(d->w_out, ctx->w_hist.get(), sizeof(double) * (size_t)p_bar * c, cudaMemcpyDeviceToHost));
+  }
 }
 
 __global__ void __launch_bounds__(256) k_dfma_probe(double* out, int iters, double seed) {
@@ -754,9 +1121,13 @@ void tf_destroy(tf_context* ctx) {
   b.W.release(); b.G.release(); b.RA.release(); b.RB.release(); b.RC.release(); b.SA.release();
   b.SB.release(); b.SC.release(); b.T.release(); b.S0.release(); b.S1.release(); b.Q1.release();
   b.Q2.release(); b.flags.release(); b.tickets.release();
-  ctx->rh_scores.release(); ctx->rh_approx.release(); ctx->rh_approx2.release(); ctx->rh_M.release();
-  ctx->rh_G.release(); ctx->rh_lvl.release(); ctx->rh_tmp.release(); ctx->rh_picked.release();
-  ctx->rh_keys.release(); ctx->rh_keys2.release(); ctx->rh_cub.release();
+  ctx->rh_J.release(); ctx->rh_cnt.release(); ctx->rh_start.release(); ctx->rh_fill.release();
+  ctx->rh_bk.release(); ctx->rh_pick.release(); ctx->rh_ok.release(); ctx->rh_flag.release();
+  ctx->rh_tsum.release(); ctx->rh_lvl.release(); ctx->rh_aidx.release(); ctx->rh_sidx.release();
+  ctx->rh_fup.release(); ctx->rh_scores.release(); ctx->rh_aw.release(); ctx->rh_sw.release();
+  ctx->rh_fupw.release(); ctx->rh_ones.release(); ctx->rh_norm.release(); ctx->rh_Gp.release();
+  ctx->rh_H0.release(); ctx->rh_W.release(); ctx->rh_S.release(); ctx->rh_phis.release();
+  ctx->rh_rest.release();
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

@@ -48,10 +48,11 @@ struct tf_context {
   tfe::DBuf<int> status, method;
   tfe::SolveBufs sb;
   // RH state
-  tfe::DBuf<double> rh_scores, rh_approx, rh_approx2, rh_M, rh_G;
-  tfe::DBuf<int64_t> rh_lvl, rh_tmp, rh_picked;
-  tfe::DBuf<uint64_t> rh_keys, rh_keys2;
-  tfe::DBuf<unsigned char> rh_cub;
+  tfe::DBuf<int> rh_J, rh_cnt, rh_start, rh_fill, rh_bk, rh_pick, rh_ok, rh_flag;
+  tfe::DBuf<long long> rh_tsum;
+  tfe::DBuf<int64_t> rh_lvl, rh_aidx, rh_sidx, rh_fup;
+  tfe::DBuf<double> rh_scores, rh_aw, rh_sw, rh_fupw, rh_ones, rh_norm, rh_Gp, rh_H0, rh_W, rh_S,
+      rh_phis, rh_rest;
   std::vector<cudaEvent_t> events;
   std::vector<cudaEvent_t> pev;  // phase events (2 per lag)
   int64_t launches = 0;

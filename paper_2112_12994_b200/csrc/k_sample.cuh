@@ -42,6 +42,7 @@ enum : int {
   kReasonCholFail = 4,      // compressed solve failed
   kReasonRankDeficient = 5, // RH reference matrix rank deficient (repeated_halving.cpp:57-64)
   kReasonZeroWindow = 6,    // lsar.cpp:13 all-zero window
+  kReasonSketchStream = 7,  // polar normal stream shorter than the sketch (never in practice)
 };
 
 constexpr int kScanThreads = 1024;
@@ -113,7 +114,7 @@ struct DrawArgs {
   const double* chunkA;
   const double* chunkB;
   const double* s;      // s_q
-  const double* r;      // r_q
+  const double* r;      // r_q (nullable: plain scores, r = 0)
   int64_t w;
   int64_t* idx;
   double* wts;
@@ -187,8 +188,12 @@ __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
   const int64_t row = r0 + lane;
   double mass = 0.0;
   if (row < a.w) {
-    const double rv = a.r[row];
-    mass = a.s[row] + (rv * rv) / R;
+    if (a.r) {
+      const double rv = a.r[row];
+      mass = a.s[row] + (rv * rv) / R;
+    } else {
+      mass = a.s[row] + 0.0 / R;  // same expression as the partials (r = 0)
+    }
   }
   buf[wib][lane] = mass;
   __syncwarp();

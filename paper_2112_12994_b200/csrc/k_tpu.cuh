@@ -46,6 +46,20 @@ __device__ __forceinline__ double tpu_get(const double* M, int K, int r, int c) 
   return (r <= c) ? M[tpu_idx(K, r, c)] : 0.0;
 }
 
+// Row loader of the reversed (target-first) weighted system of RH lag p on the
+// p_bar-wide rows: a_t[a] = w_t y[base + i_t - a], a = 0..p (base = p_bar;
+// column 0 is the target y[p_bar + i], column a >= 1 is lag a; sketch.cpp:61-79
+// with width p).  Lag p - 1 is the leading p columns of lag p.
+struct RevRows {
+  const double* y;
+  const int64_t* idx;
+  const double* wt;
+  int64_t base;
+  __device__ __forceinline__ double operator()(int64_t t, int col) const {
+    return wt[t] * y[base + idx[t] - col];
+  }
+};
+
 // Row loader of the forward-ordered, weighted sampled system.
 struct FwdRows {
   const double* y;
@@ -80,6 +94,8 @@ struct PhiSArgs {
   int* method;        // nullable
   int lag;            // 1-based
   double* S_final;    // nullable: copy of the final S (TPU) for the next lag's preconditioner
+  int rev;            // column order: 0 forward (target last), 1 reversed (target first)
+  double* rest_out;   // rev: 1 / ||S[0, :]||^2 (squared sampled residual norm) for the next lag
 };
 
 __global__ void k_phi_S(PhiSArgs a) {
@@ -90,6 +106,44 @@ __global__ void k_phi_S(PhiSArgs a) {
     return;
   }
   const double* S = fl[0] ? a.SC : (fl[2] ? a.SB : a.SA);
+  if (a.rev) {
+    // target first: v = S s0 / ||s0||^2 (s0 = row 0 of S) minimises ||A v|| with
+    // v[0] = 1, so phi[j] = -v[1 + j] (natural order: column 1 + j is lag j + 1)
+    __shared__ double red[32];
+    double part = 0.0;
+    for (int l = threadIdx.x; l < K; l += blockDim.x) {
+      const double s0 = S[tpu_idx(K, 0, l)];
+      part = fma(s0, s0, part);
+    }
+    part = warp_sum(part);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double x = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+      x = warp_sum(x);
+      if (threadIdx.x == 0) red[0] = x;
+    }
+    __syncthreads();
+    const double nrm2 = red[0];
+    for (int q = threadIdx.x; q < p; q += blockDim.x) {
+      const int j = q + 1;
+      double acc = 0.0;
+      for (int l = j; l < K; ++l) acc = fma(S[tpu_idx(K, j, l)], S[tpu_idx(K, 0, l)], acc);
+      const double v = -acc / nrm2;
+      a.phi[q] = v;
+      if (a.coefs) a.coefs[a.coef_off + q] = v;
+      if (a.taus && q == p - 1) a.taus[a.lag - 1] = v;
+    }
+    if (a.S_final) {
+      const int64_t n = tpu_size(K);
+      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) a.S_final[e] = S[e];
+    }
+    if (threadIdx.x == 0) {
+      if (a.rest_out) a.rest_out[0] = 1.0 / nrm2;
+      if (a.method) a.method[a.lag - 1] = fl[0] ? 3 : (fl[2] ? 2 : 1);
+    }
+    return;
+  }
   const double spp = S[tpu_idx(K, p, p)];
   for (int q = threadIdx.x; q < p; q += blockDim.x) {
     const double v = -S[tpu_idx(K, p - 1 - q, p)] / spp;  // phi[q] = phi_fwd[p-1-q]
@@ -161,7 +215,7 @@ __global__ void k_tpu_identity(double* __restrict__ T, int K) {
 // column 0 = y[i], column 1 = target y[i+1]).
 __global__ void k_solve_k2(const double* G, PhiSArgs a) {
   const double g00 = G[tpu_idx(2, 0, 0)], g01 = G[tpu_idx(2, 0, 1)], g11 = G[tpu_idx(2, 1, 1)];
-  const double phi = g01 / g00;
+  const double phi = a.rev ? g01 / g11 : g01 / g00;  // rev: column 0 is the target
   a.phi[0] = phi;
   if (a.coefs) a.coefs[a.coef_off] = phi;
   if (a.taus) a.taus[a.lag - 1] = phi;
@@ -176,6 +230,10 @@ __global__ void k_solve_k2(const double* G, PhiSArgs a) {
     a.S_final[tpu_idx(2, 0, 1)] = -r01 / (r00 * r11);
     a.S_final[tpu_idx(2, 1, 1)] = 1.0 / r11;
     a.S_final[tpu_idx(2, 1, 0)] = 0.0;
+    if (a.rev && a.rest_out) {
+      const double s00 = 1.0 / r00, s01 = -r01 / (r00 * r11);
+      a.rest_out[0] = 1.0 / (s00 * s00 + s01 * s01);
+    }
   }
 }
 
