@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--n", type=int, default=None, help="override series length (debug)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--profile-step", action="store_true",
+                    help="wrap one extra step in cudaProfilerStart/Stop (ncu --profile-from-start off)")
     return ap.parse_args()
 
 
@@ -294,6 +296,13 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         T = float(t.item())
     value = world * args.steps * ro_step / T
+
+    if args.profile_step:
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        one_step(7000)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
 
     # ---- instrumented step: phases, launches, roofline of the fused pass ----
     _, diags, launches = one_step(5000, want_diag=True)

@@ -85,6 +85,7 @@ typedef struct {
   int64_t* levels_out;          /* concatenated halving index sets, levels 1..depth */
   int64_t* up_idx_out;          /* [depth][sample_count] upward-pass positions */
   double* up_w_out;             /* [depth][sample_count] upward-pass weights */
+  int64_t* launches_out;        /* kernel launches issued by the sweep */
 } tf_rh_diag;
 
 const char* tf_version(void);

@@ -39,7 +39,8 @@ class TfRhDiag(C.Structure):
     _fields_ = [("fixed_idx", _i64p), ("fixed_w", _f64p), ("fixed_levels", _i64p),
                 ("fixed_up_idx", _i64p), ("fixed_up_w", _f64p), ("scores_out", _f64p),
                 ("depth_out", _i32p), ("idx_out", _i64p), ("w_out", _f64p),
-                ("levels_out", _i64p), ("up_idx_out", _i64p), ("up_w_out", _f64p)]
+                ("levels_out", _i64p), ("up_idx_out", _i64p), ("up_w_out", _f64p),
+                ("launches_out", _i64p)]
 
 
 EXPORTS = [

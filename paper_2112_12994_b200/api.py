@@ -241,6 +241,8 @@ class Engine:
             d.levels_out = ptr(diag["levels_flat"], _abi._i64p)
             d.up_idx_out = ptr(diag["up_idx"], _abi._i64p)
             d.up_w_out = ptr(diag["up_w"])
+            diag["launches"] = np.zeros(1, np.int64)
+            d.launches_out = ptr(diag["launches"], _abi._i64p)
         ccfg = None
         if cfg is not None:
             ccfg = _abi.TfRhCfg(cfg.base_threshold, cfg.sample_count, cfg.gaussian_rows, cfg.seed)

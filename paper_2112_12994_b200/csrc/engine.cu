@@ -983,7 +983,6 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
     CK(cudaEventRecord(ctx->events[p + 1], st));
   }
   const int64_t launches = g_launches - launches0;
-  (void)launches;
   CK(cudaStreamSynchronize(st));
   int sth[3];
   CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
@@ -1011,6 +1010,7 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
   if (d) {
     if (d->scores_out) CK(cudaMemcpy(d->scores_out, ctx->rh_scores.get(), sizeof(double) * m, cudaMemcpyDeviceToHost));
     if (d->depth_out) *d->depth_out = depth;
+    if (d->launches_out) *d->launches_out = launches;
     if (d->levels_out && lvl_total > 0)
       CK(cudaMemcpy(d->levels_out, ctx->rh_lvl.get(), sizeof(int64_t) * lvl_total, cudaMemcpyDeviceToHost));
     if (want_up && d->up_idx_out)
