@@ -95,13 +95,18 @@ struct GramPlan {
   int64_t rps;
 };
 
+// leading dimension of the dense tall matrices (Q1, Q2, materialised rows):
+// even, so every row starts 16-byte aligned for cp.async
+static inline int64_t ldq_of(int K) { return (K + 1) & ~1; }
+
+// split-K plan: ~4 CTAs per SM (two resident, 104 KB smem each), >= 2 slabs per split
 static GramPlan gram_plan(int64_t rows, int K, int sm_count) {
   GramPlan g;
   g.nblk = (K + 63) / 64;
   g.npair = g.nblk * (g.nblk + 1) / 2;
-  const int64_t target = 2LL * sm_count;
+  const int64_t target = 4LL * sm_count;
   int64_t ns = (target + g.npair - 1) / g.npair;
-  ns = std::max<int64_t>(1, std::min<int64_t>(ns, (rows + 255) / 256));  // >= 8 k-blocks per CTA
+  ns = std::max<int64_t>(1, std::min<int64_t>(ns, (rows + 63) / 64));
   int64_t rps = (rows + ns - 1) / ns;
   rps = (rps + 31) / 32 * 32;
   g.rps = std::max<int64_t>(rps, 32);
@@ -110,15 +115,35 @@ static GramPlan gram_plan(int64_t rows, int K, int sm_count) {
   return g;
 }
 
-// G (TPU) = A^T A over `rows` rows
+// G (TPU) = Q^T Q for a dense row-major Q (ld even): pipelined DMMA tiles +
+// ordered split reduction
+static void gram_dense(tf_context* ctx, const double* Q, int64_t ld, int64_t rows, int K, double* G,
+                       const int* gate) {
+  const GramPlan g = gram_plan(rows, K, ctx->sm_count);
+  const size_t smem = gram2_smem_bytes();
+  static size_t attr = 0;
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(k_gram_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  dim3 grid(g.npair, g.nsplit);
+  k_gram_dense<<<grid, kGramThreads, smem, ctx->stream>>>(Q, ld, rows, K, g.nblk, g.rps, ctx->sb.W.get(), gate);
+  LAUNCH_CHECK("k_gram_dense");
+  k_gram_reduce<<<g.npair * 128, 256, 0, ctx->stream>>>(ctx->sb.W.get(), g.npair, g.nsplit, g.nblk, K, G, gate);
+  LAUNCH_CHECK("k_gram_reduce");
+  g_launches += 2;
+}
+
+// G (TPU) = A^T A for loader rows: materialise densely, then gram_dense
 template <class L>
 static void gram(tf_context* ctx, const L& ld, int64_t rows, int K, double* G, const int* gate) {
-  const GramPlan g = gram_plan(rows, K, ctx->sm_count);
-  dim3 grid(g.npair, g.nsplit);
-  k_gram<L><<<grid, kGramThreads, 0, ctx->stream>>>(ld, rows, K, g.nblk, g.rps, ctx->sb.W.get(), G,
-                                                    ctx->sb.tickets.get(), gate);
-  LAUNCH_CHECK("k_gram");
+  const int64_t lq = ldq_of(K);
+  ctx->sb.M.need((size_t)rows * lq);
+  dim3 blk(32, 8);
+  k_rows_dense<L><<<(unsigned)((rows + 7) / 8), blk, 0, ctx->stream>>>(ld, rows, K, ctx->sb.M.get(), lq);
+  LAUNCH_CHECK("k_rows_dense");
   COUNT_LAUNCH();
+  gram_dense(ctx, ctx->sb.M.get(), lq, rows, K, G, gate);
 }
 
 // Q = A B, B upper-triangular TPU
@@ -126,7 +151,12 @@ template <class L>
 static void qform(tf_context* ctx, const L& ld, int64_t rows, int K, const double* B, double* Q,
                   const int* gate) {
   dim3 grid((unsigned)((rows + 63) / 64), (unsigned)((K + 63) / 64));
-  k_qform<L><<<grid, kGramThreads, 0, ctx->stream>>>(ld, rows, K, B, Q, K, gate);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_qform<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQformSmem));
+    attr = true;
+  }
+  k_qform<L><<<grid, kGramThreads, kQformSmem, ctx->stream>>>(ld, rows, K, B, Q, ldq_of(K), gate);
   LAUNCH_CHECK("k_qform");
   COUNT_LAUNCH();
 }
@@ -143,6 +173,7 @@ static void cholinv(tf_context* ctx, const double* G, int K, int pass, int64_t r
   a.flags = ctx->sb.flags.get();
   a.gate = gate;
   a.force_b = force_b;
+  a.invert = 1;
   a.status = status;
   a.lag = lag;
   const size_t smem = a.use_smem ? cholinv_smem_bytes(K) : 0;
@@ -161,6 +192,15 @@ static void cholinv(tf_context* ctx, const double* G, int K, int pass, int64_t r
   COUNT_LAUNCH();
 }
 
+// X = A Rinv (and X2 = X when non-null) for upper-triangular TPU operands
+static void trmm_tpu(tf_context* ctx, const double* A, const double* Rinv, double* X, double* X2, int K,
+                     const int* gate) {
+  const int nb = (K + 31) / 32;
+  k_trmm_tpu<<<nb * (nb + 1) / 2, 64, 0, ctx->stream>>>(A, Rinv, X, X2, K, gate);
+  LAUNCH_CHECK("k_trmm_tpu");
+  COUNT_LAUNCH();
+}
+
 // X = B R^-1 (R in RD format); TPU: B, X upper-triangular K x K; else dense rows x K.
 template <bool TPU>
 static void trsm_right(tf_context* ctx, const double* B, const double* RD, double* X, int64_t rows,
@@ -172,7 +212,7 @@ static void trsm_right(tf_context* ctx, const double* B, const double* RD, doubl
     attr = smem;
   }
   const unsigned grid = TPU ? (unsigned)((K + 31) / 32) : (unsigned)((rows + 31) / 32);
-  k_trsm_right<TPU><<<grid, kTrsmThreads, smem, ctx->stream>>>(B, RD, X, rows, K, K, gate);
+  k_trsm_right<TPU><<<grid, kTrsmThreads, smem, ctx->stream>>>(B, RD, X, rows, K, TPU ? K : ldq_of(K), gate);
   LAUNCH_CHECK("k_trsm_right");
   COUNT_LAUNCH();
 }
@@ -209,8 +249,8 @@ static void reserve_solve(tf_context* ctx, int64_t c, int Kmax) {
   b.T.need(tsz);
   b.S0.need(tsz);
   b.S1.need(tsz);
-  b.Q1.need((size_t)c * Kmax);
-  b.Q2.need((size_t)c * Kmax);
+  b.Q1.need((size_t)c * ldq_of(Kmax));
+  b.Q2.need((size_t)c * ldq_of(Kmax));
   b.flags.need(4);
   reserve_gram(ctx, c, Kmax);
 }
@@ -243,7 +283,7 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
   pa.taus = o.taus;
   pa.method = o.method;
   pa.lag = o.lag;
-  pa.S_final = Snext;
+  pa.S_final = Snext ? Snext : b.S0.get();
   pa.rev = rev;
   pa.rest_out = rest_out;
   if (K == 2) {
@@ -260,24 +300,25 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
     k_tpu_identity<<<tpu_grid(K), 256, 0, st>>>(b.T.get(), K);
   LAUNCH_CHECK("k_precond");
   COUNT_LAUNCH();
-  // pass A on Q1 = A T
+  double* Sfin = pa.S_final;
+  // pass A on Q1 = A T; the Cholesky kernel returns R_A^-1, S_A = T R_A^-1
+  const int64_t lq = ldq_of(K);
   qform(ctx, ld, c, K, b.T.get(), b.Q1.get(), nullptr);
-  DenseRows q1{b.Q1.get(), K};
-  gram(ctx, q1, c, K, b.G.get(), nullptr);
+  gram_dense(ctx, b.Q1.get(), lq, c, K, b.G.get(), nullptr);
   cholinv(ctx, b.G.get(), K, 0, c, b.RA.get(), nullptr, o.lag, o.status,
           (Sprev && phi_prev) ? 0 : 1);
-  trsm_right<true>(ctx, b.T.get(), b.RA.get(), b.SA.get(), K, K, nullptr);
-  // pass B (gated: Q1 not orthonormal enough, or pass A shifted)
-  trsm_right<false>(ctx, b.Q1.get(), b.RA.get(), b.Q2.get(), c, K, fl + 2);
-  DenseRows q2{b.Q2.get(), K};
-  gram(ctx, q2, c, K, b.G.get(), fl + 2);
+  trmm_tpu(ctx, b.T.get(), b.RA.get(), b.SA.get(), Sfin, K, nullptr);
+  // pass B (gated: Q1 not orthonormal enough, or pass A shifted): Q2 = Q1 R_A^-1
+  DenseRows q1{b.Q1.get(), lq}, q2{b.Q2.get(), lq};
+  qform(ctx, q1, c, K, b.RA.get(), b.Q2.get(), fl + 2);
+  gram_dense(ctx, b.Q2.get(), lq, c, K, b.G.get(), fl + 2);
   cholinv(ctx, b.G.get(), K, 1, c, b.RB.get(), fl + 2, o.lag, o.status);
-  trsm_right<true>(ctx, b.SA.get(), b.RB.get(), b.SB.get(), K, K, fl + 2);
-  // pass C (gated: pass A needed the shift)
-  trsm_right<false>(ctx, b.Q2.get(), b.RB.get(), b.Q1.get(), c, K, fl + 0);
-  gram(ctx, q1, c, K, b.G.get(), fl + 0);
+  trmm_tpu(ctx, b.SA.get(), b.RB.get(), b.SB.get(), Sfin, K, fl + 2);
+  // pass C (gated: pass A needed the shift): Q1 = Q2 R_B^-1
+  qform(ctx, q2, c, K, b.RB.get(), b.Q1.get(), fl + 0);
+  gram_dense(ctx, b.Q1.get(), lq, c, K, b.G.get(), fl + 0);
   cholinv(ctx, b.G.get(), K, 2, c, b.RC.get(), fl + 0, o.lag, o.status);
-  trsm_right<true>(ctx, b.SB.get(), b.RC.get(), b.SC.get(), K, K, fl + 0);
+  trmm_tpu(ctx, b.SB.get(), b.RC.get(), b.SC.get(), Sfin, K, fl + 0);
   k_phi_S<<<1, 256, 0, st>>>(pa);
   LAUNCH_CHECK("k_phi_S");
   COUNT_LAUNCH();
@@ -756,6 +797,15 @@ static void score_distribution(tf_context* ctx, const double* scores, int64_t w)
   launch_scan(ctx, ntile, 0, 0, /*unit_r=*/1);
 }
 
+template <class L, class WL, bool UPPER>
+static void rowsq_attr() {
+  static bool done = false;
+  if (!done) {
+    CK(cudaFuncSetAttribute(k_rowsq<L, WL, UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowsqSmem));
+    done = true;
+  }
+}
+
 static int64_t rh_default_base(int64_t c, int64_t k) {  // repeated_halving.hpp:67-70
   const int64_t logk = (int64_t)std::ceil(std::log((double)k + 1.0));
   return std::max<int64_t>(c, 10 * k * logk);
@@ -915,7 +965,8 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
     // sketched scores of every row of level i
     const int64_t len = lsz[i];
     WinRows rows_i{y, level_ptr(i)};
-    k_rowsq<WinRows, DenseW, false><<<(unsigned)((len + 63) / 64), kGramThreads, 0, st>>>(
+    rowsq_attr<WinRows, DenseW, false>();
+    k_rowsq<WinRows, DenseW, false><<<(unsigned)((len + 63) / 64), kGramThreads, kRowsqSmem, st>>>(
         rows_i, len, K, DenseW{ctx->rh_W.get(), g}, g, ctx->rh_scores.get());
     LAUNCH_CHECK("k_rowsq");
     COUNT_LAUNCH();
@@ -944,7 +995,8 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
   {
     FwdRows B{y, aidx, aw, 0};
     rh_factor(ctx, B, arows, K, ctx->rh_S.get());
-    k_rowsq<WinRows, TpuW, true><<<(unsigned)((m + 63) / 64), kGramThreads, 0, st>>>(
+    rowsq_attr<WinRows, TpuW, true>();
+    k_rowsq<WinRows, TpuW, true><<<(unsigned)((m + 63) / 64), kGramThreads, kRowsqSmem, st>>>(
         WinRows{y, nullptr}, m, K, TpuW{ctx->rh_S.get(), K}, K, ctx->rh_scores.get());
     LAUNCH_CHECK("k_rowsq");
     COUNT_LAUNCH();
@@ -1120,7 +1172,7 @@ void tf_destroy(tf_context* ctx) {
   tfe::SolveBufs& b = ctx->sb;
   b.W.release(); b.G.release(); b.RA.release(); b.RB.release(); b.RC.release(); b.SA.release();
   b.SB.release(); b.SC.release(); b.T.release(); b.S0.release(); b.S1.release(); b.Q1.release();
-  b.Q2.release(); b.flags.release(); b.tickets.release();
+  b.Q2.release(); b.M.release(); b.flags.release(); b.tickets.release();
   ctx->rh_J.release(); ctx->rh_cnt.release(); ctx->rh_start.release(); ctx->rh_fill.release();
   ctx->rh_bk.release(); ctx->rh_pick.release(); ctx->rh_ok.release(); ctx->rh_flag.release();
   ctx->rh_tsum.release(); ctx->rh_lvl.release(); ctx->rh_aidx.release(); ctx->rh_sidx.release();

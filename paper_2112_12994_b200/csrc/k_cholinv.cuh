@@ -51,6 +51,7 @@ struct CholinvArgs {
   int* flags;        // [0] shifted, [1] failed, [2] need pass B
   const int* gate;   // run only if *gate != 0 (nullable)
   int force_b;       // pass A: always request pass B (unpreconditioned system)
+  int invert;        // output R^-1 (TPU) instead of the RD factor
   int* status;
   int lag;
 };
@@ -432,7 +433,57 @@ __global__ void __maxnreg__(255) k_cholinv(CholinvArgs a) {
       a.flags[2] = (a.force_b || shifted || !(cond_lb <= 8.0 * K)) ? 1 : 0;
     }
   }
-  // ---- write RD (TPU) ----
+  // ---- R^-1 in place, block rows bottom-up:
+  //      Rinv(I, J) = -Dinv_I sum_{L = I+1..J} R(I, L) Rinv(L, J),  Rinv(J, J) = Dinv_J.
+  //      Items (J, column half) run in rounds of 8 with J descending, so a
+  //      round only reads R(I, L <= J) tiles that no earlier round overwrote;
+  //      products land in registers before the barrier, the writes follow it.
+  if (a.invert) {
+    for (int I = nb - 2; I >= 0; --I) {
+      const int nitems = 2 * (nb - 1 - I);
+      for (int r0 = 0; r0 < nitems; r0 += kCI_W) {
+        const int it = r0 + warp;
+        int J = 0, n0 = 0, wJ = 0;
+        bool act = false;
+        double acc[4][2][2];
+        ci_zero(acc);
+        if (it < nitems) {
+          J = nb - 1 - (it >> 1);
+          n0 = 16 * (it & 1);
+          wJ = tpu_w(J, K);
+          act = n0 < wJ;
+        }
+        if (act) {
+          for (int L = I + 1; L <= J; ++L) {
+            const double* rIL = T.tile(I, L);
+            const double* vLJ = T.tile(L, J);
+            const int wL = tpu_w(L, K);
+            ci_mma(acc, n0, [&](int mm, int k) { return k < wL ? rIL[k * kTLD + mm] : 0.0; },
+                   [&](int k, int n) { return (n < wJ && k < wL) ? vLJ[n * kTLD + k] : 0.0; });
+          }
+        }
+        __syncthreads();
+        if (act) {
+          double* tIJ = T.tile(I, J);
+          ci_put<0>(tIJ, wJ, n0, acc);
+          __syncwarp();
+          const double* dI = T.tile(I, I);
+          double acc2[4][2][2];
+          ci_zero(acc2);
+          ci_mma(acc2, n0, [&](int mm, int k) { return dI[k * kTLD + mm]; },
+                 [&](int k, int n) { return n < wJ ? tIJ[n * kTLD + k] : 0.0; });
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) acc2[i][j][0] = -acc2[i][j][0], acc2[i][j][1] = -acc2[i][j][1];
+          ci_put<0>(tIJ, wJ, n0, acc2);
+        }
+        __syncthreads();
+      }
+    }
+  }
+  // ---- write RD / R^-1 (TPU) ----
   if (a.use_smem) {
     fence_proxy_async_smem();
     __syncthreads();
@@ -446,6 +497,38 @@ __global__ void __maxnreg__(255) k_cholinv(CholinvArgs a) {
     }
   }
   CI_STAMP(42);
+}
+
+// ---------------------------------------------------------------------------
+// X = A Rinv for upper-triangular TPU A and Rinv (S = T R_A^-1, S_B = S_A R_B^-1):
+// one CTA per output tile (I <= J), one warp per column half;
+// X(I, J) = sum_{L = I..J} A(I, L) Rinv(L, J).  X2 (nullable) gets a copy.
+__global__ void __launch_bounds__(64)
+    k_trmm_tpu(const double* __restrict__ A, const double* __restrict__ Rinv, double* __restrict__ X,
+               double* __restrict__ X2, int K, const int* gate) {
+  if (gate && *gate == 0) return;
+  const int nb = (K + 31) / 32;
+  int rem = blockIdx.x, I = 0;
+  while (rem >= nb - I) {
+    rem -= nb - I;
+    ++I;
+  }
+  const int J = I + rem;
+  const int warp = threadIdx.x >> 5;
+  const int n0 = 16 * warp;
+  const int wJ = tpu_w(J, K);
+  if (n0 >= wJ) return;
+  double acc[4][2][2];
+  ci_zero(acc);
+  for (int L = I; L <= J; ++L) {
+    const double* aIL = A + tpu_tile(K, I, L);
+    const double* rLJ = Rinv + tpu_tile(K, L, J);
+    const int wL = tpu_w(L, K);
+    ci_mma(acc, n0, [&](int mm, int k) { return k < wL ? __ldg(aIL + k * kTLD + mm) : 0.0; },
+           [&](int k, int n) { return (n < wJ && k < wL) ? __ldg(rLJ + n * kTLD + k) : 0.0; });
+  }
+  ci_put<0>(X + tpu_tile(K, I, J), wJ, n0, acc);
+  if (X2) ci_put<0>(X2 + tpu_tile(K, I, J), wJ, n0, acc);
 }
 
 // ---------------------------------------------------------------------------

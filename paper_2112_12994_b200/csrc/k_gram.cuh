@@ -147,57 +147,220 @@ __global__ void __launch_bounds__(kGramThreads)
   if (tid == 0) tickets[blockIdx.x] = 0;
 }
 
-constexpr int kQA = 36;
 
-// Q[t][l] = sum_{a <= l} A(t, a) * B(a, l), l < K, for an upper-triangular
-// TPU right factor B (CholeskyQR's Q = A R^-1, or A T with the carried
-// preconditioner).
-template <class L>
+// ---------------------------------------------------------------------------
+// Dense Gram, pipelined: G = Q^T Q for a dense row-major Q (ld even, so rows
+// are 16-byte aligned).  Each CTA owns one 64 x 64 upper tile pair and a
+// contiguous row range; 32-row slabs of the two 64-column blocks stream into
+// shared memory with cp.async (LDGSTS, 16 B, zero-fill past the last row) in
+// a 3-stage ring, so global latency overlaps the DMMA work of earlier slabs.
+// Partial tiles go to W[split][pair][64 x 64]; k_gram_reduce sums them in
+// split order (deterministic) with many CTAs.
+constexpr int kG2Stages = 3;
+constexpr int kG2Ld = 68;  // padded smem row (doubles): 544 B, 16-byte aligned, conflict-free fragments
+
+__host__ __device__ inline size_t gram2_smem_bytes() {
+  return (size_t)kG2Stages * 2 * 32 * kG2Ld * sizeof(double);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __global__ void __launch_bounds__(kGramThreads)
-    k_qform(L ld, int64_t rows, int K, const double* __restrict__ B, double* __restrict__ Q,
-            int64_t ldq, const int* skip_flag) {
+    k_gram_dense(const double* __restrict__ Q, int64_t ld, int64_t rows, int K, int nblk,
+                 int64_t rows_per_split, double* __restrict__ W, const int* skip_flag) {
   if (skip_flag && *skip_flag == 0) return;
-  __shared__ __align__(16) double SA[64][kQA];
-  __shared__ __align__(16) double SR[32][kSJ];
-  const int64_t t0 = (int64_t)blockIdx.x * 64;
-  const int L0 = blockIdx.y * 64;
-  const int jend = min(K, L0 + 64);
+  extern __shared__ __align__(16) double g2s[];
+  int jb, lb;
+  pair_from_index(blockIdx.x, nblk, jb, lb);
+  const bool diag = jb == lb;
+  const int J0 = jb * 64, L0 = lb * 64;
+  const int64_t rb = (int64_t)blockIdx.y * rows_per_split;
+  const int64_t re = min(rows, rb + rows_per_split);
+  const int nslab = (int)((re - rb + 31) / 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;
+  // 16-byte chunk assignment: 32 rows x 32 chunks per operand, 8 per thread
+  auto issue = [&](int slab) {
+    double* sj = g2s + (size_t)(slab % kG2Stages) * 2 * 32 * kG2Ld;
+    double* sl = sj + 32 * kG2Ld;
+    const int64_t r0 = rb + (int64_t)slab * 32;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int ch = tid + kGramThreads * u;  // 0..1023
+      const int rr = ch >> 5, cc = (ch & 31) * 2;
+      const int64_t row = r0 + rr;
+      const bool rok = row < re;
+      {
+        const int col = J0 + cc;
+        const int nb = (rok && col < K) ? 16 : 0;
+        cp_async16(sj + rr * kG2Ld + cc, Q + (nb ? row * ld + col : 0), nb);
+      }
+      if (!diag) {
+        const int col = L0 + cc;
+        const int nb = (rok && col < K) ? 16 : 0;
+        cp_async16(sl + rr * kG2Ld + cc, Q + (nb ? row * ld + col : 0), nb);
+      }
+    }
+  };
+  // warp-uniform work trimming: 8-wide fragments past column K, and the strictly
+  // lower 32 x 32 quadrant of a diagonal pair, are never multiplied (their
+  // outputs are not stored)
+  const int ni = min(4, max(0, (K - (J0 + 32 * wm) + 7) / 8));
+  const int nj = min(4, max(0, (K - (L0 + 32 * wn) + 7) / 8));
+  const bool wskip = (diag && wm > wn) || ni == 0 || nj == 0;
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  for (int k0 = 0; k0 < jend; k0 += 32) {
-    {
-      const int cc = tid & 31, rr0 = tid >> 5;
-#pragma unroll 4
-      for (int s = 0; s < 16; ++s) {
-        const int rr = rr0 + 4 * s;
-        const int64_t row = t0 + rr;
-        SA[rr][cc] = (row < rows && k0 + cc < K) ? ld(row, k0 + cc) : 0.0;
-      }
-      const int ll = tid & 63, c0 = tid >> 6;
-#pragma unroll 4
-      for (int s = 0; s < 16; ++s) {
-        const int c = c0 + 2 * s;
-        const int r = k0 + c, cl = L0 + ll;
-        SR[c][ll] = (r < K && cl < K && r <= cl) ? B[tpu_idx(K, r, cl)] : 0.0;
+#pragma unroll
+  for (int s = 0; s < kG2Stages - 1; ++s) {
+    if (s < nslab) issue(s);
+    cp_async_commit();
+  }
+  for (int s = 0; s < nslab; ++s) {
+    cp_async_wait<kG2Stages - 2>();
+    __syncthreads();
+    // refill the stage consumed in the previous iteration
+    if (s + kG2Stages - 1 < nslab) issue(s + kG2Stages - 1);
+    cp_async_commit();
+    const double* SJ = g2s + (size_t)(s % kG2Stages) * 2 * 32 * kG2Ld;
+    const double* SL = diag ? SJ : SJ + 32 * kG2Ld;
+    if (!wskip) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int tr = 4 * kk + (lane & 3);
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = SJ[tr * kG2Ld + 32 * wm + 8 * i + (lane >> 2)];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = SL[tr * kG2Ld + 32 * wn + 8 * j + (lane >> 2)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (i < ni && j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
       }
     }
+  }
+  cp_async_wait<0>();
+  double* out = W + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 4096;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int row = 32 * wm + 8 * i + (lane >> 2);
+      const int col = 32 * wn + 8 * j + 2 * (lane & 3);
+      *reinterpret_cast<double2*>(out + row * 64 + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+}
+
+// dense copy of loader rows (row-major, leading dimension ld >= K, even)
+template <class L>
+__global__ void k_rows_dense(L ld, int64_t rows, int K, double* __restrict__ out, int64_t ldo) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+  if (t >= rows) return;
+  for (int j = threadIdx.x; j < K; j += blockDim.x) out[t * ldo + j] = ld(t, j);
+}
+
+// G (TPU) = sum over splits of W[split][pair] in split order.  Block: 8 warps,
+// 32 consecutive tile elements of one pair; warp w sums splits w, w + 8, ...;
+// the 8 warp partials are then added in warp order.
+__global__ void __launch_bounds__(256)
+    k_gram_reduce(const double* __restrict__ W, int npair, int nsplit, int nblk, int K,
+                  double* __restrict__ G, const int* skip_flag) {
+  if (skip_flag && *skip_flag == 0) return;
+  __shared__ double part[8][33];
+  const int pair = blockIdx.x / 128, grp = blockIdx.x % 128;
+  int jb, lb;
+  pair_from_index(pair, nblk, jb, lb);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = grp * 32 + lane;          // element of the 64 x 64 tile (row-major)
+  const int row = jb * 64 + (e >> 6), col = lb * 64 + (e & 63);
+  const bool rowok = jb * 64 + ((grp * 32) >> 6) < K;  // whole group shares one tile row
+  if (!rowok) return;
+  const size_t sstride = (size_t)npair * 4096;
+  const double* wp = W + (size_t)pair * 4096 + e;
+  double s0 = 0.0, s1 = 0.0;
+  int sp = warp;
+  for (; sp + 8 < nsplit; sp += 16) {
+    s0 += __ldcg(wp + (size_t)sp * sstride);
+    s1 += __ldcg(wp + (size_t)(sp + 8) * sstride);
+  }
+  if (sp < nsplit) s0 += __ldcg(wp + (size_t)sp * sstride);
+  part[warp][lane] = s0 + s1;
+  __syncthreads();
+  if (warp == 0) {
+    double t = part[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) t += part[w][lane];
+    if (row < K && col < K && (row <= col || (row >> 5) == (col >> 5))) G[tpu_idx(K, row, col)] = t;
+  }
+}
+
+constexpr int kQA = 36;
+
+constexpr size_t kQformSmem = (64 * kQA + 32 * kSJ) * sizeof(double);
+
+// Q[t][l] = sum_{a <= l} A(t, a) * B(a, l), l < K, for an upper-triangular
+// TPU right factor B (CholeskyQR's Q = A R^-1, or A T with the carried
+// preconditioner).  8-wide output fragments past column K are skipped.
+template <class L>
+__global__ void __launch_bounds__(kGramThreads)
+    k_qform(L ld, int64_t rows, int K, const double* __restrict__ B, double* __restrict__ Q,
+            int64_t ldq, const int* skip_flag) {
+  if (skip_flag && *skip_flag == 0) return;
+  extern __shared__ __align__(16) double qf_smem[];
+  double(*SA)[64][kQA] = reinterpret_cast<double(*)[64][kQA]>(qf_smem);
+  double(*SR)[32][kSJ] = reinterpret_cast<double(*)[32][kSJ]>(qf_smem + 64 * kQA);
+  const int64_t t0 = (int64_t)blockIdx.x * 64;
+  const int L0 = blockIdx.y * 64;
+  const int jend = min(K, L0 + 64);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int nj = min(4, max(0, (K - (L0 + 32 * wn) + 7) / 8));
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int cc = tid & 31, rr0 = tid >> 5;
+  const int ll = tid & 63, c0 = tid >> 6;
+  for (int k0 = 0; k0 < jend; k0 += 32) {
+#pragma unroll 4
+    for (int s = 0; s < 16; ++s) {
+      const int64_t row = t0 + rr0 + 4 * s;
+      SA[0][rr0 + 4 * s][cc] = (row < rows && k0 + cc < K) ? ld(row, k0 + cc) : 0.0;
+    }
+#pragma unroll 4
+    for (int s = 0; s < 16; ++s) {
+      const int r = k0 + c0 + 2 * s, cl = L0 + ll;
+      SR[0][c0 + 2 * s][ll] = (r < K && cl < K && r <= cl) ? B[tpu_idx(K, r, cl)] : 0.0;
+    }
     __syncthreads();
+    if (nj > 0) {
 #pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      double af[4], bf[4];
+      for (int kk = 0; kk < 8; ++kk) {
+        double af[4], bf[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = SA[32 * wm + 8 * i + (lane >> 2)][4 * kk + (lane & 3)];
+        for (int i = 0; i < 4; ++i) af[i] = SA[0][32 * wm + 8 * i + (lane >> 2)][4 * kk + (lane & 3)];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = SR[4 * kk + (lane & 3)][32 * wn + 8 * j + (lane >> 2)];
+        for (int j = 0; j < 4; ++j) bf[j] = SR[0][4 * kk + (lane & 3)][32 * wn + 8 * j + (lane >> 2)];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int j = 0; j < 4; ++j)
+            if (j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
     }
     __syncthreads();
   }

@@ -49,7 +49,7 @@ inline size_t pass_smem_bytes(int q) {
   return sizeof(double) * (size_t)(phi_n + ys_sk + rn_sk);
 }
 
-__global__ void __launch_bounds__(kPassThreads) k_lsar_pass(PassArgs a) {
+__global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass(PassArgs a) {
   extern __shared__ double sm[];
   const int q = a.q;
   const int tid = threadIdx.x;
@@ -68,18 +68,6 @@ __global__ void __launch_bounds__(kPassThreads) k_lsar_pass(PassArgs a) {
   for (int x = tid; x < ys_n; x += kPassThreads)
     ys[skew16(x)] = x < need ? __ldg(a.y + i0 + x) : 0.0;
 
-  // coalesced loads of the previous state (row = tid + 128 u)
-  double so[kPassR], ro[kPassR];
-#pragma unroll
-  for (int u = 0; u < kPassR; ++u) {
-    const int row = tid + kPassThreads * u;
-    so[u] = 0.0;
-    ro[u] = 0.0;
-    if (q > 0 && row < rows) {
-      so[u] = a.s[i0 + row];
-      ro[u] = a.r[i0 + row];
-    }
-  }
   __syncthreads();
 
   // ---- FIR: thread owns rows o = 16 tid + u ----
@@ -113,6 +101,19 @@ __global__ void __launch_bounds__(kPassThreads) k_lsar_pass(PassArgs a) {
   __syncthreads();
 
   // ---- update + chunk partials (coalesced: warp covers one 32-row chunk per u) ----
+  // previous state loaded only now: keeps the FIR's register footprint small
+  // (more resident CTAs hide this latency)
+  double so[kPassR], ro[kPassR];
+#pragma unroll
+  for (int u = 0; u < kPassR; ++u) {
+    const int row = tid + kPassThreads * u;
+    so[u] = 0.0;
+    ro[u] = 0.0;
+    if (q > 0 && row < rows) {
+      so[u] = a.s[i0 + row];
+      ro[u] = a.r[i0 + row];
+    }
+  }
   const double Rp = q > 0 ? *a.Rprev : 1.0;
   const int warp = tid >> 5, lane = tid & 31;
   double tA = 0.0, tB = 0.0;

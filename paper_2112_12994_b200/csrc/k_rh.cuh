@@ -328,17 +328,25 @@ struct TpuW {
   }
 };
 
+constexpr size_t kRowsqSmem = (64 * kQA + 32 * kSJ) * sizeof(double);
+
+// out[t] = || x_t W ||^2 over column tiles of W (K x N); 8-wide fragments
+// past column N are skipped (warp-uniform).
 template <class L, class WL, bool UPPER>
 __global__ void __launch_bounds__(kGramThreads)
     k_rowsq(L ld, int64_t rows, int K, WL wl, int N, double* __restrict__ out) {
-  __shared__ __align__(16) double SA[64][kQA];
-  __shared__ __align__(16) double SW[32][kSJ];
+  extern __shared__ __align__(16) double rq_smem[];
+  double(*SA)[64][kQA] = reinterpret_cast<double(*)[64][kQA]>(rq_smem);
+  double(*SW)[32][kSJ] = reinterpret_cast<double(*)[32][kSJ]>(rq_smem + 64 * kQA);
   __shared__ double red[2][64];
   const int64_t t0 = (int64_t)blockIdx.x * 64;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;
+  const int cc = tid & 31, rr0 = tid >> 5;
+  const int ll = tid & 63, c0 = tid >> 6;
   double rs[4] = {0.0, 0.0, 0.0, 0.0};
   for (int N0 = 0; N0 < N; N0 += 64) {
+    const int nj = min(4, max(0, (N - (N0 + 32 * wn) + 7) / 8));
     double acc[4][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -346,33 +354,31 @@ __global__ void __launch_bounds__(kGramThreads)
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const int kend = UPPER ? min(K, N0 + 64) : K;
     for (int k0 = 0; k0 < kend; k0 += 32) {
-      {
-        const int cc = tid & 31, rr0 = tid >> 5;
 #pragma unroll 4
-        for (int s = 0; s < 16; ++s) {
-          const int rr = rr0 + 4 * s;
-          const int64_t row = t0 + rr;
-          SA[rr][cc] = (row < rows && k0 + cc < K) ? ld(row, k0 + cc) : 0.0;
-        }
-        const int ll = tid & 63, c0 = tid >> 6;
+      for (int s = 0; s < 16; ++s) {
+        const int64_t row = t0 + rr0 + 4 * s;
+        SA[0][rr0 + 4 * s][cc] = (row < rows && k0 + cc < K) ? ld(row, k0 + cc) : 0.0;
+      }
 #pragma unroll 4
-        for (int s = 0; s < 16; ++s) {
-          const int c = c0 + 2 * s;
-          SW[c][ll] = (k0 + c < K && N0 + ll < N) ? wl(k0 + c, N0 + ll) : 0.0;
-        }
+      for (int s = 0; s < 16; ++s) {
+        const int c = k0 + c0 + 2 * s;
+        SW[0][c0 + 2 * s][ll] = (c < K && N0 + ll < N) ? wl(c, N0 + ll) : 0.0;
       }
       __syncthreads();
+      if (nj > 0) {
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        double af[4], bf[4];
+        for (int kk = 0; kk < 8; ++kk) {
+          double af[4], bf[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = SA[32 * wm + 8 * i + (lane >> 2)][4 * kk + (lane & 3)];
+          for (int i = 0; i < 4; ++i) af[i] = SA[0][32 * wm + 8 * i + (lane >> 2)][4 * kk + (lane & 3)];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = SW[4 * kk + (lane & 3)][32 * wn + 8 * j + (lane >> 2)];
+          for (int j = 0; j < 4; ++j) bf[j] = SW[0][4 * kk + (lane & 3)][32 * wn + 8 * j + (lane >> 2)];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            for (int j = 0; j < 4; ++j)
+              if (j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
       }
       __syncthreads();
     }

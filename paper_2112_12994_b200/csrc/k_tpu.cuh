@@ -93,7 +93,7 @@ struct PhiSArgs {
   double* taus;       // nullable
   int* method;        // nullable
   int lag;            // 1-based
-  double* S_final;    // nullable: copy of the final S (TPU) for the next lag's preconditioner
+  double* S_final;    // the final S (TPU): written by the last pass, read here and by the next lag
   int rev;            // column order: 0 forward (target last), 1 reversed (target first)
   double* rest_out;   // rev: 1 / ||S[0, :]||^2 (squared sampled residual norm) for the next lag
 };
@@ -105,7 +105,7 @@ __global__ void k_phi_S(PhiSArgs a) {
     for (int q = threadIdx.x; q < p; q += blockDim.x) a.phi[q] = __longlong_as_double(0x7ff8000000000000ll);
     return;
   }
-  const double* S = fl[0] ? a.SC : (fl[2] ? a.SB : a.SA);
+  const double* S = a.S_final;  // the last S formed (every pass writes its S there too)
   if (a.rev) {
     // target first: v = S s0 / ||s0||^2 (s0 = row 0 of S) minimises ||A v|| with
     // v[0] = 1, so phi[j] = -v[1 + j] (natural order: column 1 + j is lag j + 1)
@@ -134,10 +134,6 @@ __global__ void k_phi_S(PhiSArgs a) {
       if (a.coefs) a.coefs[a.coef_off + q] = v;
       if (a.taus && q == p - 1) a.taus[a.lag - 1] = v;
     }
-    if (a.S_final) {
-      const int64_t n = tpu_size(K);
-      for (int64_t e = threadIdx.x; e < n; e += blockDim.x) a.S_final[e] = S[e];
-    }
     if (threadIdx.x == 0) {
       if (a.rest_out) a.rest_out[0] = 1.0 / nrm2;
       if (a.method) a.method[a.lag - 1] = fl[0] ? 3 : (fl[2] ? 2 : 1);
@@ -149,10 +145,6 @@ __global__ void k_phi_S(PhiSArgs a) {
     const double v = -S[tpu_idx(K, p - 1 - q, p)] / spp;  // phi[q] = phi_fwd[p-1-q]
     a.phi[q] = v;
     if (a.coefs) a.coefs[a.coef_off + q] = v;
-  }
-  if (a.S_final) {
-    const int64_t n = tpu_size(K);
-    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) a.S_final[e] = S[e];
   }
   if (threadIdx.x == 0) {
     if (a.taus) a.taus[a.lag - 1] = -S[tpu_idx(K, 0, p)] / spp;

@@ -1,0 +1,126 @@
+// gram_bench.cu -- microbenchmark of the split-K DMMA Gram kernels on dense Q.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2112_12994_b200/csrc gram_bench.cu -o gram_bench
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "k_gram.cuh"
+
+using namespace tfk;
+
+#define CK(x)                                                                         \
+  do {                                                                                \
+    cudaError_t e = (x);                                                              \
+    if (e != cudaSuccess) {                                                           \
+      printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+      exit(1);                                                                        \
+    }                                                                                 \
+  } while (0)
+
+struct Plan {
+  int nblk, npair, nsplit;
+  int64_t rps;
+};
+static Plan plan(int64_t rows, int K, int sms, int per_sm, int bw) {
+  Plan g;
+  g.nblk = (K + bw - 1) / bw;
+  g.npair = g.nblk * (g.nblk + 1) / 2;
+  const int64_t target = (int64_t)per_sm * sms;
+  int64_t ns = (target + g.npair - 1) / g.npair;
+  ns = std::max<int64_t>(1, std::min<int64_t>(ns, (rows + 255) / 256));
+  int64_t rps = (rows + ns - 1) / ns;
+  rps = (rps + 31) / 32 * 32;
+  g.rps = std::max<int64_t>(rps, 32);
+  g.nsplit = (int)((rows + g.rps - 1) / g.rps);
+  return g;
+}
+
+int main() {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int64_t cmax = 100000;
+  const int Kmax = 512;
+  double* Q;
+  CK(cudaMalloc(&Q, sizeof(double) * cmax * (Kmax + 4)));
+  std::vector<double> h((size_t)cmax * (Kmax + 4));
+  for (size_t i = 0; i < h.size(); ++i) h[i] = std::sin(0.37 * (double)i) * 0.5;
+  CK(cudaMemcpy(Q, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+  double *W, *G;
+  int* tickets;
+  CK(cudaMalloc(&W, sizeof(double) * 64 * 1024 * 1024));
+  CK(cudaMalloc(&G, sizeof(double) * 1024 * 1024));
+  CK(cudaMalloc(&tickets, sizeof(int) * 4096));
+  CK(cudaMemset(tickets, 0, sizeof(int) * 4096));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  printf("%8s %5s %7s %7s %10s %9s\n", "c", "K", "nsplit", "npair", "us", "TF/s(alg)");
+  for (int64_t c : {10000LL, 100000LL}) {
+    for (int K : {17, 33, 64, 100, 128, 160, 201, 301}) {
+      for (int per_sm : {2, 6}) {
+        Plan g = plan(c, K, sms, per_sm, 64);
+        DenseRows ld{Q, K};
+        dim3 grid(g.npair, g.nsplit);
+        for (int it = 0; it < 3; ++it)
+          k_gram<DenseRows><<<grid, kGramThreads>>>(ld, c, K, g.nblk, g.rps, W, G, tickets, nullptr);
+        CK(cudaEventRecord(e0));
+        const int reps = 20;
+        for (int it = 0; it < reps; ++it)
+          k_gram<DenseRows><<<grid, kGramThreads>>>(ld, c, K, g.nblk, g.rps, W, G, tickets, nullptr);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        const double us = ms * 1e3 / reps;
+        const double flop = (double)c * K * (K + 1);  // upper half, 2 flop per FMA
+        printf("%8lld %5d %7d %7d %10.1f %9.2f  (old, per_sm %d)\n", (long long)c, K, g.nsplit, g.npair, us,
+               flop / (us * 1e-6) / 1e12, per_sm);
+      }
+      for (int per_sm : {2, 4, 8}) {
+        Plan g = plan(c, K, sms, per_sm, 64);
+        const int64_t ldq = (K + 1) / 2 * 2;
+        dim3 grid(g.npair, g.nsplit);
+        const size_t sm2 = gram2_smem_bytes();
+        CK(cudaFuncSetAttribute(k_gram_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+        auto run = [&]() {
+          k_gram_dense<<<grid, kGramThreads, sm2>>>(Q, ldq, c, K, g.nblk, g.rps, W, nullptr);
+          k_gram_reduce<<<g.npair * 128, 256>>>(W, g.npair, g.nsplit, g.nblk, K, G, nullptr);
+        };
+        for (int it = 0; it < 3; ++it) run();
+        CK(cudaEventRecord(e0));
+        const int reps = 20;
+        for (int it = 0; it < reps; ++it) run();
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        const double us = ms * 1e3 / reps;
+        const double flop = (double)c * K * (K + 1);
+        printf("%8lld %5d %7d %7d %10.1f %9.2f  (new, per_sm %d)\n", (long long)c, K, g.nsplit, g.npair, us,
+               flop / (us * 1e-6) / 1e12, per_sm);
+        // correctness vs old kernel on the same Q (ld even): compare G
+        if (per_sm == 4) {
+          std::vector<double> g1(tpu_size(K)), g2(tpu_size(K));
+          CK(cudaMemcpy(g2.data(), G, sizeof(double) * g2.size(), cudaMemcpyDeviceToHost));
+          Plan g0 = plan(c, K, sms, 2, 64);
+          DenseRows ld{Q, ldq};
+          k_gram<DenseRows><<<dim3(g0.npair, g0.nsplit), kGramThreads>>>(ld, c, K, g0.nblk, g0.rps, W, G, tickets, nullptr);
+          CK(cudaMemcpy(g1.data(), G, sizeof(double) * g1.size(), cudaMemcpyDeviceToHost));
+          double md = 0, mx = 0;
+          for (int r = 0; r < K; ++r)
+            for (int cc = r; cc < K; ++cc) {
+              const int64_t ix = tpu_idx(K, r, cc);
+              md = std::max(md, std::fabs(g1[ix] - g2[ix]));
+              mx = std::max(mx, std::fabs(g1[ix]));
+            }
+          printf("          check: max|dG|/max|G| = %.3e\n", md / mx);
+        }
+      }
+    }
+  }
+  CK(cudaGetLastError());
+  return 0;
+}
