@@ -162,7 +162,7 @@ static void qform(tf_context* ctx, const L& ld, int64_t rows, int K, const doubl
 }
 
 static void cholinv(tf_context* ctx, const double* G, int K, int pass, int64_t rows, double* RD,
-                    const int* gate, int lag, int* status, int force_b = 0) {
+                    const int* gate, int lag, int* status, int force_b = 0, int invert = 0) {
   CholinvArgs a;
   a.G = G;
   a.K = K;
@@ -173,7 +173,7 @@ static void cholinv(tf_context* ctx, const double* G, int K, int pass, int64_t r
   a.flags = ctx->sb.flags.get();
   a.gate = gate;
   a.force_b = force_b;
-  a.invert = 1;
+  a.invert = invert;
   a.status = status;
   a.lag = lag;
   const size_t smem = a.use_smem ? cholinv_smem_bytes(K) : 0;
@@ -244,6 +244,7 @@ static void reserve_solve(tf_context* ctx, int64_t c, int Kmax) {
   b.RB.need(tsz);
   b.RC.need(tsz);
   b.SA.need(tsz);
+  b.RI.need(tsz);
   b.SB.need(tsz);
   b.SC.need(tsz);
   b.T.need(tsz);
@@ -266,7 +267,7 @@ static void reserve_solve(tf_context* ctx, int64_t c, int Kmax) {
 template <class L>
 static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const SolveOut& o,
                        const double* Sprev, const double* phi_prev, double* Snext, int rev = 0,
-                       const double* rscal = nullptr, double* rest_out = nullptr) {
+                       const double* rscal = nullptr, double* rest_out = nullptr, bool exact = false) {
   SolveBufs& b = ctx->sb;
   reserve_solve(ctx, c, K);
   int* fl = b.flags.get();
@@ -301,26 +302,75 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
   LAUNCH_CHECK("k_precond");
   COUNT_LAUNCH();
   double* Sfin = pa.S_final;
-  // pass A on Q1 = A T; the Cholesky kernel returns R_A^-1, S_A = T R_A^-1
   const int64_t lq = ldq_of(K);
+  const int forceb = (Sprev && phi_prev) ? 0 : 1;
+  if (exact) {
+    // exact S (RH generalized leverage): the Cholesky kernel returns R^-1 and
+    // S = T R_A^-1 [R_B^-1 [R_C^-1]] is formed by triangular products
+    qform(ctx, ld, c, K, b.T.get(), b.Q1.get(), nullptr);
+    gram_dense(ctx, b.Q1.get(), lq, c, K, b.G.get(), nullptr);
+    cholinv(ctx, b.G.get(), K, 0, c, b.RA.get(), nullptr, o.lag, o.status, forceb, 1);
+    trmm_tpu(ctx, b.T.get(), b.RA.get(), b.SA.get(), Sfin, K, nullptr);
+    DenseRows q1{b.Q1.get(), lq}, q2{b.Q2.get(), lq};
+    qform(ctx, q1, c, K, b.RA.get(), b.Q2.get(), fl + 2);
+    gram_dense(ctx, b.Q2.get(), lq, c, K, b.G.get(), fl + 2);
+    cholinv(ctx, b.G.get(), K, 1, c, b.RB.get(), fl + 2, o.lag, o.status, 0, 1);
+    trmm_tpu(ctx, b.SA.get(), b.RB.get(), b.SB.get(), Sfin, K, fl + 2);
+    qform(ctx, q2, c, K, b.RB.get(), b.Q1.get(), fl + 0);
+    gram_dense(ctx, b.Q1.get(), lq, c, K, b.G.get(), fl + 0);
+    cholinv(ctx, b.G.get(), K, 2, c, b.RC.get(), fl + 0, o.lag, o.status, 0, 1);
+    trmm_tpu(ctx, b.SB.get(), b.RC.get(), b.SC.get(), Sfin, K, fl + 0);
+    k_phi_S<<<1, 256, 0, st>>>(pa);
+    LAUNCH_CHECK("k_phi_S");
+    COUNT_LAUNCH();
+    return;
+  }
+  // fast path (sweep lags, standalone solves): factors only; phi by O(K^2)
+  // substitutions; the next lag's preconditioner S ~ T R^-1 to first order
   qform(ctx, ld, c, K, b.T.get(), b.Q1.get(), nullptr);
   gram_dense(ctx, b.Q1.get(), lq, c, K, b.G.get(), nullptr);
-  cholinv(ctx, b.G.get(), K, 0, c, b.RA.get(), nullptr, o.lag, o.status,
-          (Sprev && phi_prev) ? 0 : 1);
-  trmm_tpu(ctx, b.T.get(), b.RA.get(), b.SA.get(), Sfin, K, nullptr);
-  // pass B (gated: Q1 not orthonormal enough, or pass A shifted): Q2 = Q1 R_A^-1
-  DenseRows q1{b.Q1.get(), lq}, q2{b.Q2.get(), lq};
-  qform(ctx, q1, c, K, b.RA.get(), b.Q2.get(), fl + 2);
+  cholinv(ctx, b.G.get(), K, 0, c, b.RA.get(), nullptr, o.lag, o.status, forceb, 0);
+  const unsigned npair = (unsigned)(((K + 31) / 32) * ((K + 31) / 32 + 1) / 2);
+  if (Snext) {
+    k_rinv_first_order<<<npair, 64, 0, st>>>(b.RA.get(), b.RI.get(), K, nullptr);
+    COUNT_LAUNCH();
+    trmm_tpu(ctx, b.T.get(), b.RI.get(), b.SA.get(), Snext, K, nullptr);
+  }
+  // pass B (gated): Q2 = Q1 R_A^-1 by blocked substitution
+  trsm_right<false>(ctx, b.Q1.get(), b.RA.get(), b.Q2.get(), c, K, fl + 2);
   gram_dense(ctx, b.Q2.get(), lq, c, K, b.G.get(), fl + 2);
   cholinv(ctx, b.G.get(), K, 1, c, b.RB.get(), fl + 2, o.lag, o.status);
-  trmm_tpu(ctx, b.SA.get(), b.RB.get(), b.SB.get(), Sfin, K, fl + 2);
-  // pass C (gated: pass A needed the shift): Q1 = Q2 R_B^-1
-  qform(ctx, q2, c, K, b.RB.get(), b.Q1.get(), fl + 0);
+  if (Snext) {
+    k_rinv_first_order<<<npair, 64, 0, st>>>(b.RB.get(), b.RI.get(), K, fl + 2);
+    COUNT_LAUNCH();
+    trmm_tpu(ctx, b.SA.get(), b.RI.get(), b.SB.get(), Snext, K, fl + 2);
+  }
+  // pass C (gated: pass A shifted): Q1 = Q2 R_B^-1
+  trsm_right<false>(ctx, b.Q2.get(), b.RB.get(), b.Q1.get(), c, K, fl + 0);
   gram_dense(ctx, b.Q1.get(), lq, c, K, b.G.get(), fl + 0);
   cholinv(ctx, b.G.get(), K, 2, c, b.RC.get(), fl + 0, o.lag, o.status);
-  trmm_tpu(ctx, b.SB.get(), b.RC.get(), b.SC.get(), Sfin, K, fl + 0);
-  k_phi_S<<<1, 256, 0, st>>>(pa);
-  LAUNCH_CHECK("k_phi_S");
+  if (Snext) {
+    k_rinv_first_order<<<npair, 64, 0, st>>>(b.RC.get(), b.RI.get(), K, fl + 0);
+    COUNT_LAUNCH();
+    trmm_tpu(ctx, b.SB.get(), b.RI.get(), b.SC.get(), Snext, K, fl + 0);
+  }
+  PhiSolveArgs ps;
+  ps.K = K;
+  ps.T = b.T.get();
+  ps.RA = b.RA.get();
+  ps.RB = b.RB.get();
+  ps.RC = b.RC.get();
+  ps.flags = fl;
+  ps.rev = rev;
+  ps.phi = o.phi;
+  ps.coefs = o.coefs;
+  ps.coef_off = o.coef_off;
+  ps.taus = o.taus;
+  ps.method = o.method;
+  ps.lag = o.lag;
+  ps.rest_out = rest_out;
+  k_phi_solve<<<1, kPhiThreads, (size_t)(2 * K + 32) * sizeof(double), st>>>(ps);
+  LAUNCH_CHECK("k_phi_solve");
   COUNT_LAUNCH();
 }
 
@@ -760,7 +810,7 @@ static void rh_halve(tf_context* ctx, uint64_t seed, const int64_t* cur, int64_t
 // S (TPU, K) = R^-1 of the CholeskyQR of the approximation rows (forward order)
 static void rh_factor(tf_context* ctx, const FwdRows& ld, int64_t rows, int K, double* S) {
   SolveOut o{ctx->rh_phis.get(), nullptr, 0, nullptr, nullptr, 0, ctx->status.get()};
-  solve_rows(ctx, ld, rows, K, o, nullptr, nullptr, S);
+  solve_rows(ctx, ld, rows, K, o, nullptr, nullptr, S, 0, nullptr, nullptr, /*exact=*/true);
 }
 
 static void launch_draw_on(tf_context* ctx, const double* scores, int64_t w, uint64_t seed,
@@ -1172,7 +1222,7 @@ void tf_destroy(tf_context* ctx) {
   tfe::SolveBufs& b = ctx->sb;
   b.W.release(); b.G.release(); b.RA.release(); b.RB.release(); b.RC.release(); b.SA.release();
   b.SB.release(); b.SC.release(); b.T.release(); b.S0.release(); b.S1.release(); b.Q1.release();
-  b.Q2.release(); b.M.release(); b.flags.release(); b.tickets.release();
+  b.Q2.release(); b.M.release(); b.RI.release(); b.flags.release(); b.tickets.release();
   ctx->rh_J.release(); ctx->rh_cnt.release(); ctx->rh_start.release(); ctx->rh_fill.release();
   ctx->rh_bk.release(); ctx->rh_pick.release(); ctx->rh_ok.release(); ctx->rh_flag.release();
   ctx->rh_tsum.release(); ctx->rh_lvl.release(); ctx->rh_aidx.release(); ctx->rh_sidx.release();

@@ -621,3 +621,205 @@ __global__ void __launch_bounds__(kTrsmThreads)
 inline size_t trsm_smem_bytes(int K) { return (size_t)((K + 31) / 32) * 32 * kTLD * sizeof(double); }
 
 }  // namespace tfk
+
+namespace tfk {
+
+// ---------------------------------------------------------------------------
+// phi straight from the Cholesky factors (RD format) -- O(K^2) per pass, no
+// explicit inverse:  S = T R_A^-1 [R_B^-1 [R_C^-1]] is never formed.
+//   forward order (target last):  s = S e_last;  phi_fwd = -s[:p] / s[p]
+//   reversed order (target first): s0 = S^T e_0, v = S s0 / ||s0||^2,
+//                                   phi[j] = -v[1 + j]; rest = 1 / ||s0||^2
+// One CTA; 8 threads per row (column) of a 32-block, shuffle-reduced dots.
+struct PhiSolveArgs {
+  int K;
+  const double* T;    // TPU preconditioner
+  const double* RA;   // RD factors
+  const double* RB;
+  const double* RC;
+  const int* flags;   // [0] shifted (pass C ran), [1] failed, [2] pass B ran
+  int rev;
+  double* phi;
+  double* coefs;
+  int64_t coef_off;
+  double* taus;
+  int* method;
+  int lag;
+  double* rest_out;
+};
+
+constexpr int kPhiThreads = 256;
+
+__device__ __forceinline__ double oct_sum(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  return v;
+}
+
+// x <- R^-1 x (back substitution, R in RD format)
+__device__ void rd_solve_col(const double* R, int K, double* x, double* tmp) {
+  const int nb = (K + 31) / 32;
+  const int r = threadIdx.x >> 3, sub = threadIdx.x & 7;
+  for (int J = nb - 1; J >= 0; --J) {
+    const int wJ = tpu_w(J, K);
+    double part = 0.0;
+    if (r < wJ)
+      for (int c = 32 * (J + 1) + sub; c < K; c += 8)
+        part = fma(R[tpu_tile(K, J, c >> 5) + (c & 31) * kTLD + r], x[c], part);
+    part = oct_sum(part);
+    if (sub == 0 && r < 32) tmp[r] = r < wJ ? x[32 * J + r] - part : 0.0;
+    __syncthreads();
+    const double* D = R + tpu_tile(K, J, J);
+    double q = 0.0;
+    if (r < wJ)
+      for (int c = r + sub; c < wJ; c += 8) q = fma(D[c * kTLD + r], tmp[c], q);
+    q = oct_sum(q);
+    if (sub == 0 && r < wJ) x[32 * J + r] = q;
+    __syncthreads();
+  }
+}
+
+// y <- y R^-1 (row vector, forward substitution, R in RD format)
+__device__ void rd_solve_row(const double* R, int K, double* y, double* tmp) {
+  const int nb = (K + 31) / 32;
+  const int c = threadIdx.x >> 3, sub = threadIdx.x & 7;
+  for (int J = 0; J < nb; ++J) {
+    const int wJ = tpu_w(J, K);
+    double part = 0.0;
+    if (c < wJ)
+      for (int rr = sub; rr < 32 * J; rr += 8)
+        part = fma(y[rr], R[tpu_tile(K, rr >> 5, J) + c * kTLD + (rr & 31)], part);
+    part = oct_sum(part);
+    if (sub == 0 && c < 32) tmp[c] = c < wJ ? y[32 * J + c] - part : 0.0;
+    __syncthreads();
+    const double* D = R + tpu_tile(K, J, J);
+    double q = 0.0;
+    if (c < wJ)
+      for (int rr = sub; rr <= c; rr += 8) q = fma(tmp[rr], D[c * kTLD + rr], q);
+    q = oct_sum(q);
+    if (sub == 0 && c < wJ) y[32 * J + c] = q;
+    __syncthreads();
+  }
+}
+
+// s <- T x (upper TPU)
+__device__ void tpu_matvec(const double* T, int K, const double* x, double* s) {
+  for (int r = threadIdx.x; r < K; r += blockDim.x) {
+    double acc = 0.0;
+    for (int c = r; c < K; ++c) acc = fma(T[tpu_idx(K, r, c)], x[c], acc);
+    s[r] = acc;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPhiThreads) k_phi_solve(PhiSolveArgs a) {
+  extern __shared__ double ps[];
+  const int K = a.K, p = K - 1;
+  const int* fl = a.flags;
+  double* x = ps;
+  double* s = ps + K;
+  double* tmp = ps + 2 * K;
+  __shared__ double red[kPhiThreads / 32];
+  if (fl[1]) {
+    for (int q = threadIdx.x; q < p; q += blockDim.x) a.phi[q] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  const bool hasB = fl[2] != 0, hasC = fl[0] != 0;
+  if (!a.rev) {
+    for (int i = threadIdx.x; i < K; i += blockDim.x) x[i] = i == p ? 1.0 : 0.0;
+    __syncthreads();
+    if (hasC) rd_solve_col(a.RC, K, x, tmp);
+    if (hasB) rd_solve_col(a.RB, K, x, tmp);
+    rd_solve_col(a.RA, K, x, tmp);
+    tpu_matvec(a.T, K, x, s);
+    const double spp = s[p];
+    for (int q = threadIdx.x; q < p; q += blockDim.x) {
+      const double v = -s[p - 1 - q] / spp;
+      a.phi[q] = v;
+      if (a.coefs) a.coefs[a.coef_off + q] = v;
+    }
+    if (threadIdx.x == 0) {
+      if (a.taus) a.taus[a.lag - 1] = -s[0] / spp;
+      if (a.method) a.method[a.lag - 1] = hasC ? 3 : (hasB ? 2 : 1);
+    }
+    return;
+  }
+  // reversed: s0 = e_0^T T R_A^-1 R_B^-1 R_C^-1
+  for (int i = threadIdx.x; i < K; i += blockDim.x) x[i] = a.T[tpu_idx(K, 0, i)];
+  __syncthreads();
+  rd_solve_row(a.RA, K, x, tmp);
+  if (hasB) rd_solve_row(a.RB, K, x, tmp);
+  if (hasC) rd_solve_row(a.RC, K, x, tmp);
+  double part = 0.0;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) part = fma(x[i], x[i], part);
+  part = warp_sum(part);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  double nrm2 = 0.0;
+  for (int w = 0; w < kPhiThreads / 32; ++w) nrm2 += red[w];
+  // v = T R_A^-1 R_B^-1 R_C^-1 s0
+  if (hasC) rd_solve_col(a.RC, K, x, tmp);
+  if (hasB) rd_solve_col(a.RB, K, x, tmp);
+  rd_solve_col(a.RA, K, x, tmp);
+  tpu_matvec(a.T, K, x, s);
+  for (int q = threadIdx.x; q < p; q += blockDim.x) {
+    const double v = -s[1 + q] / nrm2;
+    a.phi[q] = v;
+    if (a.coefs) a.coefs[a.coef_off + q] = v;
+    if (a.taus && q == p - 1) a.taus[a.lag - 1] = v;
+  }
+  if (threadIdx.x == 0) {
+    if (a.rest_out) a.rest_out[0] = 1.0 / nrm2;
+    if (a.method) a.method[a.lag - 1] = hasC ? 3 : (hasB ? 2 : 1);
+  }
+}
+
+// First-order inverse of an RD factor, for the NEXT lag's preconditioner only:
+// Rinv(J, J) = Dinv_J, Rinv(I, J) ~ -Dinv_I R(I, J) Dinv_J (I < J); the
+// neglected terms are O(||Dinv R_off||^2), small because the preconditioned
+// Gram is close to the identity.  One CTA per tile pair, one warp per column half.
+__global__ void __launch_bounds__(64)
+    k_rinv_first_order(const double* __restrict__ RD, double* __restrict__ Ri, int K, const int* gate) {
+  if (gate && *gate == 0) return;
+  __shared__ double tmp[32 * kTLD];
+  const int nb = (K + 31) / 32;
+  int rem = blockIdx.x, I = 0;
+  while (rem >= nb - I) {
+    rem -= nb - I;
+    ++I;
+  }
+  const int J = I + rem;
+  const int warp = threadIdx.x >> 5;
+  const int n0 = 16 * warp;
+  const int wJ = tpu_w(J, K), wI = tpu_w(I, K);
+  const double* dJ = RD + tpu_tile(K, J, J);
+  double* out = Ri + tpu_tile(K, I, J);
+  if (I == J) {
+    for (int e = threadIdx.x; e < 32 * wJ; e += 64) {
+      const int c = e >> 5, r = e & 31;
+      out[c * kTLD + r] = dJ[c * kTLD + r];
+    }
+    return;
+  }
+  const double* rIJ = RD + tpu_tile(K, I, J);
+  const double* dI = RD + tpu_tile(K, I, I);
+  double acc[4][2][2];
+  ci_zero(acc);
+  if (n0 < wJ)  // tmp = R(I, J) Dinv_J
+    ci_mma(acc, n0, [&](int mm, int k) { return k < wJ ? rIJ[k * kTLD + mm] : 0.0; },
+           [&](int k, int n) { return (n < wJ && k < wJ) ? dJ[n * kTLD + k] : 0.0; });
+  if (n0 < wJ) ci_put<0>(tmp, wJ, n0, acc);
+  __syncthreads();
+  ci_zero(acc);
+  if (n0 < wJ)
+    ci_mma(acc, n0, [&](int mm, int k) { return k < wI ? dI[k * kTLD + mm] : 0.0; },
+           [&](int k, int n) { return n < wJ ? tmp[n * kTLD + k] : 0.0; });
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = -acc[i][j][0], acc[i][j][1] = -acc[i][j][1];
+  if (n0 < wJ) ci_put<0>(out, wJ, n0, acc);
+}
+
+}  // namespace tfk
