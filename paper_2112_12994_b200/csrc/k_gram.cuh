@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kGramThreads)
 
   const int cc = tid & 63, rsub = tid >> 6;
   for (int64_t r0 = rb; r0 < re; r0 += 32) {
-#pragma unroll 4
+#pragma unroll
     for (int s = 0; s < 16; ++s) {
       const int rr = rsub + 2 * s;
       const int64_t row = r0 + rr;
@@ -336,12 +336,12 @@ __global__ void __launch_bounds__(kGramThreads)
   const int cc = tid & 31, rr0 = tid >> 5;
   const int ll = tid & 63, c0 = tid >> 6;
   for (int k0 = 0; k0 < jend; k0 += 32) {
-#pragma unroll 4
+#pragma unroll
     for (int s = 0; s < 16; ++s) {
       const int64_t row = t0 + rr0 + 4 * s;
       SA[0][rr0 + 4 * s][cc] = (row < rows && k0 + cc < K) ? ld(row, k0 + cc) : 0.0;
     }
-#pragma unroll 4
+#pragma unroll
     for (int s = 0; s < 16; ++s) {
       const int r = k0 + c0 + 2 * s, cl = L0 + ll;
       SR[0][c0 + 2 * s][ll] = (r < K && cl < K && r <= cl) ? B[tpu_idx(K, r, cl)] : 0.0;

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kRhThreads)
   __shared__ long long tot;
   const int64_t base = (int64_t)blockIdx.x * kScanTileN;
   long long acc = 0;
-#pragma unroll 4
+#pragma unroll
   for (int u = 0; u < kScanPer; ++u) {
     const int64_t i = base + (int64_t)u * kRhThreads + threadIdx.x;
     if (i < n) acc += in[i];
@@ -354,12 +354,12 @@ __global__ void __launch_bounds__(kGramThreads)
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const int kend = UPPER ? min(K, N0 + 64) : K;
     for (int k0 = 0; k0 < kend; k0 += 32) {
-#pragma unroll 4
+#pragma unroll
       for (int s = 0; s < 16; ++s) {
         const int64_t row = t0 + rr0 + 4 * s;
         SA[0][rr0 + 4 * s][cc] = (row < rows && k0 + cc < K) ? ld(row, k0 + cc) : 0.0;
       }
-#pragma unroll 4
+#pragma unroll
       for (int s = 0; s < 16; ++s) {
         const int c = k0 + c0 + 2 * s;
         SW[0][c0 + 2 * s][ll] = (c < K && N0 + ll < N) ? wl(c, N0 + ll) : 0.0;
