@@ -1,0 +1,234 @@
+// toepfit_b200.hpp -- header-only C++17 host API over the C ABI
+// (include/toepfit_b200.h), mirroring the reference's fit surface in
+// namespace toepfit (proj/include/toepfit):
+//
+//   TimeSeries                series.hpp:16-31 (shared immutable storage)
+//   UsageError / DataError /  errors.hpp:12-29 (thrown from the C-ABI status)
+//     NumericalError
+//   PACFResult, PacfMethod    toeplitz.hpp:64-68
+//   FitResult                 lsar.hpp:28-35 (std::vector instead of Eigen::VectorXd)
+//   RHConfig                  repeated_halving.hpp:56-65 (defaults / validate)
+//   lsar_fit                  lsar.hpp:89
+//   rh_fit (5- and 4-arg)     repeated_halving.hpp:97-99
+//   select_order              toeplitz.hpp:100
+//
+// One device context per host thread (created lazily on device 0, or bound
+// with toepfit::gpu::use_device); the reference is single-threaded and
+// distinct fits may run concurrently on distinct threads.
+// Nothing here computes on the CPU: without a CUDA device every call throws
+// toepfit::gpu::CudaError.
+#ifndef TOEPFIT_B200_HPP
+#define TOEPFIT_B200_HPP
+
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "toepfit_b200.h"
+
+namespace toepfit {
+
+class UsageError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class DataError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class NumericalError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+namespace gpu {
+class CudaError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+}  // namespace gpu
+
+class TimeSeries {
+ public:
+  explicit TimeSeries(std::vector<double> values, std::string label = "")
+      : values_(std::make_shared<const std::vector<double>>(std::move(values))), label_(std::move(label)) {
+    if (values_->empty()) throw DataError("series must contain at least one value");
+    for (std::size_t i = 0; i < values_->size(); ++i)
+      if (!std::isfinite((*values_)[i]))
+        throw DataError("series value at position " + std::to_string(i) + " is not finite");
+  }
+  const std::vector<double>& values() const { return *values_; }
+  std::size_t size() const { return values_->size(); }
+  const std::string& label() const { return label_; }
+  std::shared_ptr<const std::vector<double>> storage() const { return values_; }
+
+ private:
+  std::shared_ptr<const std::vector<double>> values_;
+  std::string label_;
+};
+
+enum class PacfMethod { exact, lsar, rh, srht };
+
+struct PACFResult {
+  std::vector<double> taus;
+  double bound = 0.0;
+  PacfMethod method = PacfMethod::exact;
+};
+
+struct FitResult {
+  int p_star = 0;
+  std::vector<double> coefficients;
+  PACFResult pacf;
+  std::vector<double> per_lag_seconds;
+  std::vector<std::vector<double>> per_lag_coefficients;
+  double upfront_seconds = 0.0;
+};
+
+struct RHConfig {
+  std::int64_t base_threshold = 0;
+  std::int64_t sample_count = 0;
+  std::int64_t gaussian_rows = 0;
+  std::uint64_t seed = 0;
+
+  static RHConfig defaults(std::int64_t n, std::int64_t k, std::int64_t c, std::uint64_t seed) {
+    RHConfig r;
+    const std::int64_t logk = (std::int64_t)std::ceil(std::log((double)k + 1.0));
+    r.base_threshold = c > 10 * k * logk ? c : 10 * k * logk;
+    r.sample_count = c;
+    r.gaussian_rows = (std::int64_t)std::ceil(8.0 * std::log((double)(n > 2 ? n : 2)));
+    r.seed = seed;
+    return r;
+  }
+  void validate() const {
+    if (sample_count < 1) throw UsageError("sample count must be positive");
+    if (base_threshold < sample_count) throw UsageError("base threshold below sample count");
+    if (gaussian_rows < 1) throw UsageError("need at least one sketch row");
+  }
+};
+
+namespace gpu {
+
+inline void raise(tf_status st, const tf_context* ctx) {
+  const std::string msg = ctx ? tf_last_error(ctx) : std::string("no CUDA device");
+  switch (st) {
+    case TF_OK: return;
+    case TF_USAGE: throw UsageError(msg);
+    case TF_DATA: throw DataError(msg);
+    case TF_NUMERICAL: throw NumericalError(msg);
+    default: throw CudaError(msg);
+  }
+}
+
+// per-thread device context with the last uploaded series cached by identity
+struct Context {
+  tf_context* ctx = nullptr;
+  int device = 0;
+  const std::vector<double>* cached = nullptr;
+  std::shared_ptr<const std::vector<double>> keep;
+  ~Context() {
+    if (ctx) tf_destroy(ctx);
+  }
+  tf_context* get() {
+    if (!ctx) {
+      tf_opts o{device, 0};
+      const tf_status st = tf_create(&o, &ctx);
+      if (st != TF_OK) {
+        ctx = nullptr;
+        raise(st == TF_USAGE ? TF_USAGE : TF_CUDA, nullptr);
+      }
+    }
+    return ctx;
+  }
+  void upload(const TimeSeries& s) {
+    tf_context* c = get();
+    if (cached == &s.values() && keep == s.storage()) return;
+    raise(tf_upload_series(c, s.values().data(), (int64_t)s.size()), c);
+    cached = &s.values();
+    keep = s.storage();
+  }
+};
+
+inline Context& context() {
+  thread_local Context c;
+  return c;
+}
+
+inline void use_device(int device) {
+  Context& c = context();
+  if (c.ctx && c.device != device) {
+    tf_destroy(c.ctx);
+    c.ctx = nullptr;
+    c.cached = nullptr;
+    c.keep.reset();
+  }
+  c.device = device;
+}
+
+inline FitResult finish(PacfMethod m, int p_bar, std::int64_t c, const std::vector<double>& taus,
+                        const std::vector<double>& packed, std::vector<double> secs, int p_star,
+                        double upfront) {
+  FitResult f;
+  f.pacf.taus = taus;
+  f.pacf.bound = 1.96 / std::sqrt((double)c);
+  f.pacf.method = m;
+  f.per_lag_seconds = std::move(secs);
+  f.p_star = p_star;
+  f.upfront_seconds = upfront;
+  std::size_t off = 0;
+  for (int p = 1; p <= p_bar; ++p) {
+    f.per_lag_coefficients.emplace_back(packed.begin() + off, packed.begin() + off + p);
+    off += p;
+  }
+  if (p_star > 0) f.coefficients = f.per_lag_coefficients[p_star - 1];
+  return f;
+}
+
+}  // namespace gpu
+
+inline FitResult lsar_fit(const TimeSeries& series, int p_bar, std::int64_t c, std::uint64_t seed) {
+  gpu::Context& g = gpu::context();
+  tf_context* ctx = g.get();
+  g.upload(series);
+  const int pb = p_bar > 0 ? p_bar : 1;
+  std::vector<double> taus(pb), packed((std::size_t)pb * (pb + 1) / 2), secs(pb);
+  int p_star = 0;
+  gpu::raise(tf_lsar_sweep(ctx, p_bar, c, seed, nullptr, taus.data(), packed.data(), secs.data(), &p_star),
+             ctx);
+  return gpu::finish(PacfMethod::lsar, p_bar, c, taus, packed, std::move(secs), p_star, 0.0);
+}
+
+inline FitResult rh_fit(const TimeSeries& series, int p_bar, std::int64_t c, const RHConfig* config,
+                        std::uint64_t seed) {
+  gpu::Context& g = gpu::context();
+  tf_context* ctx = g.get();
+  g.upload(series);
+  tf_rh_cfg cfg{};
+  if (config) {
+    config->validate();
+    cfg = tf_rh_cfg{config->base_threshold, config->sample_count, config->gaussian_rows, config->seed};
+  }
+  const int pb = p_bar > 0 ? p_bar : 1;
+  std::vector<double> taus(pb), packed((std::size_t)pb * (pb + 1) / 2), secs(pb);
+  double upfront = 0.0;
+  int p_star = 0;
+  gpu::raise(tf_rh_sweep(ctx, p_bar, c, config ? &cfg : nullptr, seed, nullptr, taus.data(), packed.data(),
+                         secs.data(), &upfront, &p_star),
+             ctx);
+  return gpu::finish(PacfMethod::rh, p_bar, c, taus, packed, std::move(secs), p_star, upfront);
+}
+
+inline FitResult rh_fit(const TimeSeries& series, int p_bar, std::int64_t c, std::uint64_t seed) {
+  return rh_fit(series, p_bar, c, nullptr, seed);
+}
+
+inline int select_order(const PACFResult& pacf) {
+  return tf_select_order(pacf.taus.data(), (int)pacf.taus.size(), pacf.bound);
+}
+
+}  // namespace toepfit
+
+#endif  // TOEPFIT_B200_HPP

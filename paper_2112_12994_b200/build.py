@@ -31,5 +31,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+ROOT = os.path.dirname(HERE)
+CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_cpp_api.cpp")
+CPP_TEST_OUT = os.path.join(ROOT, "build", "test_cpp_api")
+
+
+def build_cpp_api_test(force: bool = False) -> str:
+    """C++ host-API program (include/toepfit_b200.hpp) linked against the library."""
+    lib = build()
+    deps = [CPP_TEST_SRC, os.path.join(ROOT, "include", "toepfit_b200.hpp"), lib]
+    if force or not os.path.exists(CPP_TEST_OUT) or any(
+            os.path.getmtime(d) > os.path.getmtime(CPP_TEST_OUT) for d in deps):
+        os.makedirs(os.path.dirname(CPP_TEST_OUT), exist_ok=True)
+        subprocess.check_call(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), CPP_TEST_SRC,
+                               "-L", HERE, "-ltoepfit_b200",
+                               "-Wl,-rpath,$ORIGIN/../paper_2112_12994_b200", "-o", CPP_TEST_OUT])
+    return CPP_TEST_OUT
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
