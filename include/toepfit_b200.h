@@ -132,6 +132,30 @@ int tf_select_order(const double* taus, int p_bar, double bound);
 /* Diagnostics: measured fp64 FMA throughput of this device (TFLOP/s) from a
  * DFMA microbenchmark, the denominator of the fp64 roofline. */
 tf_status tf_probe_fp64_peak(tf_context* ctx, double* tflops);
+
+/* ---- row-sharded LSAR steps (one process per GPU) ----
+ * The caller owns the collectives (paper_2112_12994_b200/shard.py).  A shard
+ * uploads y[row0 .. row0 + w_local + p_bar) with tf_upload_series; its window
+ * rows are the global rows row0 .. row0 + w_local.  Per lag p the only
+ * cross-rank data are this shard's (sum s, sum r^2) (allgather) and, per
+ * CholeskyQR pass, the K x K Gram (allreduce sum, tile-packed layout of
+ * tf_tpu_size(K) doubles).  Same recursion as tf_lsar_sweep (lsar.cpp:70-98). */
+tf_status tf_shard_open(tf_context* ctx, int p_bar, int64_t c, int64_t w_local);
+/* fused pass at lag q (phi: q host values, NULL for q = 0) with the global
+ * R_{q-1}; out2 = (sum s_q, sum r_q^2) over this shard's rows */
+tf_status tf_shard_pass(tf_context* ctx, int q, const double* phi, double r_prev, double* out2);
+/* draws t of Rng(seed_p) whose global CDF position u_t * s_total falls in this
+ * shard's segment [offset, offset + mass) are resolved here (sketch.cpp:20-59);
+ * k_out = local draw count (kept in draw order) */
+tf_status tf_shard_sample(tf_context* ctx, uint64_t seed_p, double s_total, double offset, double r_glob,
+                          int is_last, int64_t* k_out);
+/* local Gram of the sampled rows, CholeskyQR pass 0 (Q1 = A T_p), 1 or 2 */
+tf_status tf_shard_gram(tf_context* ctx, int p, int pass, double r_prev, double* G_out);
+/* Cholesky of the reduced Gram; flags3 = (shifted, failed, need pass B) */
+tf_status tf_shard_factor(tf_context* ctx, int p, int pass, const double* G, int64_t c_total, int* flags3);
+/* phi_p (p host values) and tau_p; forms the next lag's preconditioner */
+tf_status tf_shard_finish(tf_context* ctx, int p, double* phi_out, double* tau_out);
+int64_t tf_tpu_size(int K);
 uint64_t tf_derive_seed(uint64_t seed, uint64_t tag);
 
 #ifdef __cplusplus

@@ -47,7 +47,8 @@ EXPORTS = [
     "tf_version", "tf_create", "tf_destroy", "tf_last_error", "tf_upload_series",
     "tf_upload_series_device", "tf_lsar_sweep", "tf_rh_sweep", "tf_residuals", "tf_sample_rows",
     "tf_apply_sample", "tf_solve_sampled", "tf_select_order", "tf_derive_seed",
-    "tf_probe_fp64_peak",
+    "tf_probe_fp64_peak", "tf_shard_open", "tf_shard_pass", "tf_shard_sample", "tf_shard_gram",
+    "tf_shard_factor", "tf_shard_finish", "tf_tpu_size",
 ]
 
 _lib = None
@@ -84,6 +85,15 @@ def lib():
     L.tf_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
     L.tf_derive_seed.restype = C.c_uint64
     L.tf_probe_fp64_peak.argtypes = [C.c_void_p, _f64p]
+    L.tf_shard_open.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64]
+    L.tf_shard_pass.argtypes = [C.c_void_p, C.c_int, _f64p, C.c_double, _f64p]
+    L.tf_shard_sample.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_int,
+                                  C.POINTER(C.c_int64)]
+    L.tf_shard_gram.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, _f64p]
+    L.tf_shard_factor.argtypes = [C.c_void_p, C.c_int, C.c_int, _f64p, C.c_int64, _i32p]
+    L.tf_shard_finish.argtypes = [C.c_void_p, C.c_int, _f64p, _f64p]
+    L.tf_tpu_size.argtypes = [C.c_int]
+    L.tf_tpu_size.restype = C.c_int64
     for name in EXPORTS:
         if not hasattr(L, name):
             raise RuntimeError(f"{LIB_PATH} does not export {name}")

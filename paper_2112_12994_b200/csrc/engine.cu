@@ -401,11 +401,12 @@ static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, co
   COUNT_LAUNCH();
 }
 
-static void launch_scan(tf_context* ctx, int64_t ntile, int lag, int check_r, int unit_r = 0) {
+static void launch_scan(tf_context* ctx, int64_t ntile, int lag, int check_r, int unit_r = 0,
+                        const double* r_fixed = nullptr) {
   k_lag_scan<<<1, kScanThreads, 0, ctx->stream>>>(ctx->tileA.get(), ctx->tileB.get(), ntile,
                                                   ctx->OT.get(), ctx->scal.get(), ctx->Rhist.get(),
                                                   ctx->Shist.get(), lag, check_r, ctx->status.get(),
-                                                  unit_r);
+                                                  unit_r, r_fixed);
   LAUNCH_CHECK("k_lag_scan");
   COUNT_LAUNCH();
 }
@@ -413,6 +414,8 @@ static void launch_scan(tf_context* ctx, int64_t ntile, int lag, int check_r, in
 static void launch_draw(tf_context* ctx, uint64_t seed, int64_t c, int64_t w, int64_t* idx,
                         double* wts) {
   DrawArgs a;
+  a.shard = 0;
+  a.accept = nullptr;
   a.seed = seed;
   a.c = c;
   a.scal = ctx->scal.get();
@@ -816,6 +819,8 @@ static void rh_factor(tf_context* ctx, const FwdRows& ld, int64_t rows, int K, d
 static void launch_draw_on(tf_context* ctx, const double* scores, int64_t w, uint64_t seed,
                            int64_t c, int64_t* idx, double* wts) {
   DrawArgs a;
+  a.shard = 0;
+  a.accept = nullptr;
   a.seed = seed;
   a.c = c;
   a.scal = ctx->scal.get();
@@ -1126,6 +1131,246 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
   }
 }
 
+// ---------------------------------------------------------------------------
+// Row-sharded LSAR steps.  The caller (paper_2112_12994_b200/
+// shard.py) owns the collectives: per lag an allgather of this shard's
+// (sum s, sum r^2) and, per CholeskyQR pass, an allreduce of the K x K Gram.
+// The shard's series slice is y[row0 .. row0 + w_local + p_bar) (uploaded with
+// tf_upload_series); its window rows are the global rows row0 .. row0 + w_local.
+
+__global__ void k_sum_tiles(const double* tA, const double* tB, int64_t ntile, double* out) {
+  __shared__ double ra[1024], rb[1024];
+  const int tid = threadIdx.x;
+  const int64_t seg = (ntile + 1023) / 1024;
+  const int64_t b = min(ntile, (int64_t)tid * seg), e = min(ntile, b + seg);
+  double sa = 0.0, sb = 0.0;
+  for (int64_t t = b; t < e; ++t) {
+    sa += tA[t];
+    sb += tB[t];
+  }
+  ra[tid] = sa;
+  rb[tid] = sb;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (tid < o) {
+      ra[tid] = ra[tid] + ra[tid + o];
+      rb[tid] = rb[tid] + rb[tid + o];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    out[0] = ra[0];
+    out[1] = rb[0];
+  }
+}
+
+struct CompactDrawF {
+  const int64_t* idx;
+  const double* wts;
+  int64_t* oidx;
+  double* ow;
+  __device__ void operator()(int64_t t, long long excl, int v) const {
+    if (v) {
+      oidx[excl] = idx[t];
+      ow[excl] = wts[t];
+    }
+  }
+};
+
+static void shard_check(const tf_context* ctx) {
+  if (ctx->sh_pbar < 1) throw TfError{TF_USAGE, "shard session not open"};
+}
+
+static void shard_open(tf_context* ctx, int p_bar, int64_t c, int64_t w_local) {
+  if (p_bar < 1) throw TfError{TF_USAGE, "maximum lag must be at least 1"};
+  if (c < p_bar) throw TfError{TF_USAGE, "sample count below maximum lag"};
+  if (w_local < 1 || ctx->n < w_local + p_bar)
+    throw TfError{TF_DATA, "shard slice shorter than its rows plus the p_bar halo"};
+  ctx->sh_pbar = p_bar;
+  ctx->sh_c = c;
+  ctx->sh_w = w_local;
+  ctx->sh_k = 0;
+  alloc_state(ctx, p_bar, c, w_local);
+  reserve_solve(ctx, c, p_bar + 1);
+  ctx->sh_buf.need(8);
+  ctx->sh_idx.need(c);
+  ctx->sh_wts.need(c);
+  ctx->rh_ok.need(c);
+}
+
+static void shard_pass(tf_context* ctx, int q, const double* phi, double r_prev, double out[2]) {
+  shard_check(ctx);
+  cudaStream_t st = ctx->stream;
+  double* dev = ctx->sh_buf.get();
+  if (q > 0) {
+    CK(cudaMemcpyAsync(ctx->phi.get(), phi, q * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dev + 2, &r_prev, sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  launch_pass(ctx, q, ctx->sh_w, ctx->phi.get(), dev + 2);
+  const int64_t ntile = (ctx->sh_w + kPassTile - 1) / kPassTile;
+  k_sum_tiles<<<1, 1024, 0, st>>>(ctx->tileA.get(), ctx->tileB.get(), ntile, dev);
+  COUNT_LAUNCH();
+  CK(cudaMemcpyAsync(out, dev, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+static int64_t shard_sample(tf_context* ctx, uint64_t seed, double s_total, double offset, double r_glob,
+                            int is_last) {
+  shard_check(ctx);
+  cudaStream_t st = ctx->stream;
+  const int64_t w = ctx->sh_w, c = ctx->sh_c;
+  const int64_t ntile = (w + kPassTile - 1) / kPassTile;
+  double* dev = ctx->sh_buf.get();
+  CK(cudaMemcpyAsync(dev + 3, &r_glob, sizeof(double), cudaMemcpyHostToDevice, st));
+  launch_scan(ctx, ntile, 0, 0, 0, dev + 3);  // local tile prefix, mass with the global R
+  DrawArgs a;
+  a.seed = seed;
+  a.c = c;
+  a.scal = ctx->scal.get();
+  a.OT = ctx->OT.get();
+  a.ntile = ntile;
+  a.tA = ctx->tileA.get();
+  a.tB = ctx->tileB.get();
+  a.chunkA = ctx->chunkA.get();
+  a.chunkB = ctx->chunkB.get();
+  a.s = ctx->s.get();
+  a.r = ctx->r.get();
+  a.w = w;
+  a.idx = ctx->idx.get();
+  a.wts = ctx->wts.get();
+  a.shard = 1;
+  a.s_total = s_total;
+  a.offset = offset;
+  a.is_last = is_last;
+  a.accept = ctx->rh_ok.get();
+  const int per = kDrawThreads / 32;
+  k_draw<<<(unsigned)((c + per - 1) / per), kDrawThreads, 0, st>>>(a);
+  LAUNCH_CHECK("k_draw");
+  COUNT_LAUNCH();
+  // draw-order compaction of the accepted draws (deterministic local order)
+  scan_apply(ctx, ctx->rh_ok.get(), c, CompactDrawF{ctx->idx.get(), ctx->wts.get(), ctx->sh_idx.get(), ctx->sh_wts.get()});
+  const int64_t nt = (c + kScanTileN - 1) / kScanTileN;
+  long long k = 0;
+  CK(cudaMemcpyAsync(&k, ctx->rh_tsum.get() + nt + 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  ctx->sh_k = k;
+  return k;
+}
+
+// local Gram of this shard's sampled rows at lag p for CholeskyQR pass `pass`
+static void shard_gram(tf_context* ctx, int p, int pass, double r_prev, double* G_out) {
+  shard_check(ctx);
+  SolveBufs& b = ctx->sb;
+  cudaStream_t st = ctx->stream;
+  const int K = p + 1;
+  const int64_t k = ctx->sh_k, lq = ldq_of(K);
+  const int64_t tsz = tpu_size(K);
+  if (k == 0) {
+    CK(cudaMemsetAsync(b.G.get(), 0, tsz * sizeof(double), st));
+  } else if (K == 2) {
+    FwdRows ld{ctx->y.get(), ctx->sh_idx.get(), ctx->sh_wts.get(), 0};
+    gram(ctx, ld, k, K, b.G.get(), nullptr);
+  } else if (pass == 0) {
+    FwdRows ld{ctx->y.get(), ctx->sh_idx.get(), ctx->sh_wts.get(), 0};
+    double* dev = ctx->sh_buf.get();
+    CK(cudaMemcpyAsync(dev + 4, &r_prev, sizeof(double), cudaMemcpyHostToDevice, st));
+    const double* Sprev = (p & 1) ? b.S0.get() : b.S1.get();
+    k_precond<<<tpu_grid(K), 256, 0, st>>>(Sprev, ctx->phi.get(), dev + 4, b.T.get(), K);
+    COUNT_LAUNCH();
+    qform(ctx, ld, k, K, b.T.get(), b.Q1.get(), nullptr);
+    gram_dense(ctx, b.Q1.get(), lq, k, K, b.G.get(), nullptr);
+  } else if (pass == 1) {
+    trsm_right<false>(ctx, b.Q1.get(), b.RA.get(), b.Q2.get(), k, K, nullptr);
+    gram_dense(ctx, b.Q2.get(), lq, k, K, b.G.get(), nullptr);
+  } else {
+    trsm_right<false>(ctx, b.Q2.get(), b.RB.get(), b.Q1.get(), k, K, nullptr);
+    gram_dense(ctx, b.Q1.get(), lq, k, K, b.G.get(), nullptr);
+  }
+  CK(cudaMemcpyAsync(G_out, b.G.get(), tsz * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+// Cholesky of the reduced Gram (identical on every rank)
+static void shard_factor(tf_context* ctx, int p, int pass, const double* G, int64_t c_total, int flags_out[3]) {
+  shard_check(ctx);
+  SolveBufs& b = ctx->sb;
+  cudaStream_t st = ctx->stream;
+  const int K = p + 1;
+  CK(cudaMemcpyAsync(b.G.get(), G, tpu_size(K) * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (K == 2) {
+    CK(cudaMemsetAsync(b.flags.get(), 0, 4 * sizeof(int), st));
+  } else {
+    double* RD = pass == 0 ? b.RA.get() : pass == 1 ? b.RB.get() : b.RC.get();
+    cholinv(ctx, b.G.get(), K, pass, c_total, RD, nullptr, p, ctx->status.get(), 0, 0);
+  }
+  int fl[4];
+  CK(cudaMemcpyAsync(fl, b.flags.get(), 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int sth[3];
+  CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  raise_from_status(sth);
+  flags_out[0] = fl[0];
+  flags_out[1] = fl[1];
+  flags_out[2] = fl[2];
+}
+
+// phi_p from the factors; the next lag's preconditioner is formed on device
+static void shard_finish(tf_context* ctx, int p, double* phi_out, double* tau_out) {
+  shard_check(ctx);
+  SolveBufs& b = ctx->sb;
+  cudaStream_t st = ctx->stream;
+  const int K = p + 1;
+  int* fl = b.flags.get();
+  double* Snext = (p & 1) ? b.S1.get() : b.S0.get();
+  if (K == 2) {
+    PhiSArgs pa;
+    pa.K = 2;
+    pa.SA = pa.SB = pa.SC = nullptr;
+    pa.flags = fl;
+    pa.phi = ctx->phi.get();
+    pa.coefs = nullptr;
+    pa.coef_off = 0;
+    pa.taus = ctx->taus.get();
+    pa.method = ctx->method.get();
+    pa.lag = 1;
+    pa.S_final = Snext;
+    pa.rev = 0;
+    pa.rest_out = nullptr;
+    k_solve_k2<<<1, 1, 0, st>>>(b.G.get(), pa);
+    COUNT_LAUNCH();
+  } else {
+    const unsigned npair = (unsigned)(((K + 31) / 32) * ((K + 31) / 32 + 1) / 2);
+    k_rinv_first_order<<<npair, 64, 0, st>>>(b.RA.get(), b.RI.get(), K, nullptr);
+    trmm_tpu(ctx, b.T.get(), b.RI.get(), b.SA.get(), Snext, K, nullptr);
+    k_rinv_first_order<<<npair, 64, 0, st>>>(b.RB.get(), b.RI.get(), K, fl + 2);
+    trmm_tpu(ctx, b.SA.get(), b.RI.get(), b.SB.get(), Snext, K, fl + 2);
+    k_rinv_first_order<<<npair, 64, 0, st>>>(b.RC.get(), b.RI.get(), K, fl + 0);
+    trmm_tpu(ctx, b.SB.get(), b.RI.get(), b.SC.get(), Snext, K, fl + 0);
+    g_launches += 3;
+    PhiSolveArgs ps;
+    ps.K = K;
+    ps.T = b.T.get();
+    ps.RA = b.RA.get();
+    ps.RB = b.RB.get();
+    ps.RC = b.RC.get();
+    ps.flags = fl;
+    ps.rev = 0;
+    ps.phi = ctx->phi.get();
+    ps.coefs = nullptr;
+    ps.coef_off = 0;
+    ps.taus = ctx->taus.get();
+    ps.method = ctx->method.get();
+    ps.lag = p;
+    ps.rest_out = nullptr;
+    k_phi_solve<<<1, kPhiThreads, (size_t)(2 * K + 32) * sizeof(double), st>>>(ps);
+    LAUNCH_CHECK("k_phi_solve");
+    COUNT_LAUNCH();
+  }
+  CK(cudaMemcpyAsync(phi_out, ctx->phi.get(), p * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(tau_out, ctx->taus.get() + (p - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+
 __global__ void __launch_bounds__(256) k_dfma_probe(double* out, int iters, double seed) {
   double a0 = seed + threadIdx.x, a1 = a0 * 0.5, a2 = a0 * 0.25, a3 = a0 * 0.125;
   double a4 = a0 + 1, a5 = a1 + 1, a6 = a2 + 1, a7 = a3 + 1;
@@ -1304,6 +1549,39 @@ int tf_select_order(const double* taus, int p_bar, double bound) {
 }
 
 uint64_t tf_derive_seed(uint64_t seed, uint64_t tag) { return tfk::derive_seed(seed, tag); }
+
+tf_status tf_shard_open(tf_context* ctx, int p_bar, int64_t c, int64_t w_local) {
+  if (!ctx) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::shard_open(ctx, p_bar, c, w_local); });
+}
+
+tf_status tf_shard_pass(tf_context* ctx, int q, const double* phi, double r_prev, double* out2) {
+  if (!ctx || !out2 || (q > 0 && !phi)) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::shard_pass(ctx, q, phi, r_prev, out2); });
+}
+
+tf_status tf_shard_sample(tf_context* ctx, uint64_t seed_p, double s_total, double offset, double r_glob,
+                          int is_last, int64_t* k_out) {
+  if (!ctx || !k_out) return TF_USAGE;
+  return guarded(ctx, [&] { *k_out = tfe::shard_sample(ctx, seed_p, s_total, offset, r_glob, is_last); });
+}
+
+tf_status tf_shard_gram(tf_context* ctx, int p, int pass, double r_prev, double* G_out) {
+  if (!ctx || !G_out) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::shard_gram(ctx, p, pass, r_prev, G_out); });
+}
+
+tf_status tf_shard_factor(tf_context* ctx, int p, int pass, const double* G, int64_t c_total, int* flags3) {
+  if (!ctx || !G || !flags3) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::shard_factor(ctx, p, pass, G, c_total, flags3); });
+}
+
+tf_status tf_shard_finish(tf_context* ctx, int p, double* phi_out, double* tau_out) {
+  if (!ctx || !phi_out || !tau_out) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::shard_finish(ctx, p, phi_out, tau_out); });
+}
+
+int64_t tf_tpu_size(int K) { return K < 1 ? 0 : tfk::tpu_size(K); }
 
 tf_status tf_probe_fp64_peak(tf_context* ctx, double* tflops) {
   if (!ctx || !tflops) return TF_USAGE;

@@ -53,6 +53,11 @@ struct tf_context {
   tfe::DBuf<int64_t> rh_lvl, rh_aidx, rh_sidx, rh_fup;
   tfe::DBuf<double> rh_scores, rh_aw, rh_sw, rh_fupw, rh_ones, rh_norm, rh_Gp, rh_H0, rh_W, rh_S,
       rh_phis, rh_rest;
+  // row-sharded LSAR session (tf_shard_*)
+  int sh_pbar = 0;
+  int64_t sh_c = 0, sh_w = 0, sh_k = 0;
+  tfe::DBuf<double> sh_buf, sh_wts;
+  tfe::DBuf<int64_t> sh_idx;
   std::vector<cudaEvent_t> events;
   std::vector<cudaEvent_t> pev;  // phase events (2 per lag)
   int64_t launches = 0;

@@ -51,7 +51,7 @@ constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads)
     k_lag_scan(const double* __restrict__ tA, const double* __restrict__ tB, int64_t ntile,
                double* __restrict__ OT, double* scal, double* Rhist, double* Shist, int lag,
-               int check_r, int* status, int unit_r = 0) {
+               int check_r, int* status, int unit_r = 0, const double* r_fixed = nullptr) {
   __shared__ double red[kScanThreads];
   __shared__ double wsum[32];
   const int tid = threadIdx.x;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kScanThreads)
     if (tid < o) red[tid] = red[tid] + red[tid + o];
     __syncthreads();
   }
-  const double R = unit_r ? 1.0 : red[0];
+  const double R = r_fixed ? *r_fixed : (unit_r ? 1.0 : red[0]);
   __syncthreads();
   double ss = 0.0;
   for (int64_t t = b; t < e; ++t) ss += tA[t] + tB[t] / R;
@@ -118,6 +118,13 @@ struct DrawArgs {
   int64_t w;
   int64_t* idx;
   double* wts;
+  // row-sharded mode: this shard holds the global CDF segment
+  // [offset, offset + S); draws outside it are skipped (accept[t] = 0)
+  int shard;
+  double s_total;
+  double offset;
+  int is_last;
+  int* accept;
 };
 
 constexpr int kDrawThreads = 256;
@@ -128,7 +135,13 @@ __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
   const int64_t t = (int64_t)blockIdx.x * (kDrawThreads / 32) + wib;
   if (t >= a.c) return;
   const double R = a.scal[0], S = a.scal[1];
-  const double v = rng_uniform01(a.seed, (uint64_t)t) * S;
+  double v = rng_uniform01(a.seed, (uint64_t)t) * (a.shard ? a.s_total : S);
+  if (a.shard) {
+    v -= a.offset;
+    const bool mine = v >= 0.0 && (v < S || a.is_last);
+    if (lane == 0) a.accept[t] = mine ? 1 : 0;
+    if (!mine) return;
+  }
   // ---- tile: largest T with OT[T] <= v ----
   int64_t lo = 0, hi = a.ntile;
   while (hi - lo > 32) {
@@ -214,7 +227,7 @@ __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
     if (pick < 0) pick = lastpos < 0 ? 0 : lastpos;
     const double mp = buf[wib][pick];
     a.idx[t] = r0 + pick;
-    a.wts[t] = 1.0 / sqrt((double)a.c * (mp / S));
+    a.wts[t] = 1.0 / sqrt((double)a.c * (mp / (a.shard ? a.s_total : S)));
   }
 }
 

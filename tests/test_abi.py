@@ -25,7 +25,7 @@ def abi():
 
 def declared_functions():
     text = open(HEADER).read()
-    pat = r"^\s*(?:const\s+char\s*\*|tf_status|void|int|uint64_t)\s+(tf_[a-z0-9_]+)\s*\("
+    pat = r"^\s*(?:const\s+char\s*\*|tf_status|void|int|int64_t|uint64_t)\s+(tf_[a-z0-9_]+)\s*\("
     return sorted(set(re.findall(pat, text, flags=re.M)))
 
 

@@ -1,0 +1,96 @@
+"""Row-sharded LSAR orchestration (paper_2112_12994_b200/shard.py): world
+size 2 over gloo on CPU (numpy stand-in for the device steps) must resolve
+exactly the single-shard draws and give the same fit; on a GPU, world size 1
+through tf_shard_* must match tf_lsar_sweep."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _series(n=3000, seed=3):
+    from paper_2112_12994_b200 import gen
+    return gen.simulate_roots(gen.ar_roots(5, 1.3, 3.0, seed), n, seed)
+
+
+def _worker(rank, world, port, y, p_bar, c, seed, q):
+    import torch.distributed as dist
+    from paper_2112_12994_b200 import shard
+    from shard_numpy import NumpyShard
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        fit = shard.lsar_fit_sharded(y, p_bar, c, seed, comm=shard.TorchComm(), backend=NumpyShard())
+        q.put((rank, fit.taus, fit.p_star, fit.local_draws, fit.row0, fit.rows))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_rows_partition():
+    from paper_2112_12994_b200.shard import shard_rows
+    for w, world in [(10, 3), (997, 8), (8, 8)]:
+        blocks = [shard_rows(w, world, r) for r in range(world)]
+        assert blocks[0][0] == 0 and sum(b for _, b in blocks) == w
+        assert all(blocks[r][0] + blocks[r][1] == blocks[r + 1][0] for r in range(world - 1))
+        assert max(b for _, b in blocks) - min(b for _, b in blocks) <= 1
+
+
+def test_sharded_gloo_world2_matches_single():
+    import multiprocessing as mp
+    from paper_2112_12994_b200 import shard
+    from shard_numpy import NumpyShard
+    y, p_bar, c, seed = _series(), 6, 300, 17
+    single = shard.lsar_fit_sharded(y, p_bar, c, seed, backend=NumpyShard())
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, y, p_bar, c, seed, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    (r0, t0, ps0, d0, row0a, rows0), (r1, t1, ps1, d1, row0b, rows1) = res
+    assert row0a == 0 and row0b == rows0 and rows0 + rows1 == y.size - p_bar
+    # every draw resolved by exactly one shard
+    assert [a + b for a, b in zip(d0, d1)] == [c] * p_bar
+    assert np.allclose(t0, t1, rtol=0, atol=0)  # identical on both ranks
+    assert np.max(np.abs(t0 - single.taus) / np.maximum(np.abs(single.taus), 1e-3)) < 1e-9
+    assert ps0 == ps1 == single.p_star
+
+
+def test_sharded_numpy_matches_oracle_fixed_draws():
+    # the numpy stand-in is faithful: same draws as the oracle's LSAR for one shard
+    from oracle import oracle as orc
+    from paper_2112_12994_b200 import shard
+    from shard_numpy import NumpyShard
+    y, p_bar, c, seed = _series(2500, 9), 5, 250, 4
+    ref = orc.lsar_fit(y, p_bar, c, seed)
+    fit = shard.lsar_fit_sharded(y, p_bar, c, seed, backend=NumpyShard())
+    assert np.max(np.abs(fit.taus - ref.taus) / np.maximum(np.abs(ref.taus), 1e-3)) < 1e-8
+    assert fit.p_star == ref.p_star
+
+
+@pytest.mark.gpu
+def test_sharded_gpu_world1_matches_sweep():
+    import paper_2112_12994_b200 as tf
+    from paper_2112_12994_b200 import shard
+    y = _series(40000, 6)
+    p_bar, c, seed = 24, 2000, 5
+    eng = tf.Engine(0)
+    ref = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, seed, engine=eng)
+    fit = shard.lsar_fit_sharded(y, p_bar, c, seed, backend=shard.GpuShard(engine=eng))
+    rel = np.max(np.abs(fit.taus - np.array(ref.pacf.taus)) / np.maximum(np.abs(ref.pacf.taus), 1e-3))
+    assert rel < 1e-9
+    assert fit.p_star == ref.p_star
+    assert fit.local_draws == [c] * p_bar
+    eng.close()
