@@ -861,6 +861,34 @@ static void rowsq_attr() {
   }
 }
 
+// scores of every window row t in [0, rows): out[t] = ||x_t W||^2 (Hankel tiles)
+template <class WL, bool UPPER>
+static void rowsq_all_rows(tf_context* ctx, int64_t rows, int K, const WL& wl, int N, double* out) {
+  const int ntiles = (N + 63) / 64;
+  if (ntiles > 8) throw TfError{TF_USAGE, "row-score tiles > 8"};
+  const size_t smem = rowsq_hankel_smem(K);
+  static size_t attr = 0;
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(k_rowsq_hankel<WL, UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rowsq_hankel<WL, UPPER>, kHkThreads, smem));
+  // equal CTA share per column tile, one wave (a narrow tile's blocks are not
+  // proportionally cheaper: loads and barriers dominate them)
+  const int per_tile = std::max(1, per_sm * ctx->sm_count / ntiles);
+  HkPlan plan;
+  plan.ntiles = ntiles;
+  for (int j = 0; j <= ntiles; ++j) plan.first[j] = j * per_tile;
+  ctx->rh_part.need((size_t)ntiles * rows);
+  k_rowsq_hankel<WL, UPPER><<<plan.first[ntiles], kHkThreads, smem, ctx->stream>>>(
+      ctx->y.get(), ctx->n, rows, K, wl, N, plan, ctx->rh_part.get());
+  LAUNCH_CHECK("k_rowsq_hankel");
+  k_rowsq_combine<<<grid_for(rows, ctx), 256, 0, ctx->stream>>>(ctx->rh_part.get(), rows, ntiles, out);
+  LAUNCH_CHECK("k_rowsq_combine");
+  g_launches += 2;
+}
+
 static int64_t rh_default_base(int64_t c, int64_t k) {  // repeated_halving.hpp:67-70
   const int64_t logk = (int64_t)std::ceil(std::log((double)k + 1.0));
   return std::max<int64_t>(c, 10 * k * logk);
@@ -1019,12 +1047,16 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
     g_launches += 2;
     // sketched scores of every row of level i
     const int64_t len = lsz[i];
-    WinRows rows_i{y, level_ptr(i)};
-    rowsq_attr<WinRows, DenseW, false>();
-    k_rowsq<WinRows, DenseW, false><<<(unsigned)((len + 63) / 64), kGramThreads, kRowsqSmem, st>>>(
-        rows_i, len, K, DenseW{ctx->rh_W.get(), g}, g, ctx->rh_scores.get());
-    LAUNCH_CHECK("k_rowsq");
-    COUNT_LAUNCH();
+    if (i == 0 && rowsq_hankel_smem(K) <= 200 * 1024) {
+      rowsq_all_rows<DenseW, false>(ctx, len, K, DenseW{ctx->rh_W.get(), g}, g, ctx->rh_scores.get());
+    } else {
+      WinRows rows_i{y, level_ptr(i)};
+      rowsq_attr<WinRows, DenseW, false>();
+      k_rowsq<WinRows, DenseW, false><<<(unsigned)((len + 63) / 64), kGramThreads, kRowsqSmem, st>>>(
+          rows_i, len, K, DenseW{ctx->rh_W.get(), g}, g, ctx->rh_scores.get());
+      LAUNCH_CHECK("k_rowsq");
+      COUNT_LAUNCH();
+    }
     const int64_t* sidx = ctx->rh_sidx.get();
     const double* sw = ctx->rh_sw.get();
     if (fixed_up) {
@@ -1050,11 +1082,15 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
   {
     FwdRows B{y, aidx, aw, 0};
     rh_factor(ctx, B, arows, K, ctx->rh_S.get());
-    rowsq_attr<WinRows, TpuW, true>();
-    k_rowsq<WinRows, TpuW, true><<<(unsigned)((m + 63) / 64), kGramThreads, kRowsqSmem, st>>>(
-        WinRows{y, nullptr}, m, K, TpuW{ctx->rh_S.get(), K}, K, ctx->rh_scores.get());
-    LAUNCH_CHECK("k_rowsq");
-    COUNT_LAUNCH();
+    if (rowsq_hankel_smem(K) <= 200 * 1024) {
+      rowsq_all_rows<TpuW, true>(ctx, m, K, TpuW{ctx->rh_S.get(), K}, K, ctx->rh_scores.get());
+    } else {
+      rowsq_attr<WinRows, TpuW, true>();
+      k_rowsq<WinRows, TpuW, true><<<(unsigned)((m + 63) / 64), kGramThreads, kRowsqSmem, st>>>(
+          WinRows{y, nullptr}, m, K, TpuW{ctx->rh_S.get(), K}, K, ctx->rh_scores.get());
+      LAUNCH_CHECK("k_rowsq");
+      COUNT_LAUNCH();
+    }
     score_distribution(ctx, ctx->rh_scores.get(), m);
   }
   CK(cudaEventRecord(ctx->events[1], st));
@@ -1474,7 +1510,7 @@ void tf_destroy(tf_context* ctx) {
   ctx->rh_fup.release(); ctx->rh_scores.release(); ctx->rh_aw.release(); ctx->rh_sw.release();
   ctx->rh_fupw.release(); ctx->rh_ones.release(); ctx->rh_norm.release(); ctx->rh_Gp.release();
   ctx->rh_H0.release(); ctx->rh_W.release(); ctx->rh_S.release(); ctx->rh_phis.release();
-  ctx->rh_rest.release();
+  ctx->rh_rest.release(); ctx->rh_part.release();
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

@@ -52,7 +52,7 @@ struct tf_context {
   tfe::DBuf<long long> rh_tsum;
   tfe::DBuf<int64_t> rh_lvl, rh_aidx, rh_sidx, rh_fup;
   tfe::DBuf<double> rh_scores, rh_aw, rh_sw, rh_fupw, rh_ones, rh_norm, rh_Gp, rh_H0, rh_W, rh_S,
-      rh_phis, rh_rest;
+      rh_phis, rh_rest, rh_part;
   // row-sharded LSAR session (tf_shard_*)
   int sh_pbar = 0;
   int64_t sh_c = 0, sh_w = 0, sh_k = 0;

@@ -397,6 +397,123 @@ __global__ void __launch_bounds__(kGramThreads)
   if (tid < 64 && t0 + tid < rows) out[t0 + tid] = red[0][tid] + red[1][tid];
 }
 
+// Row scores over CONSECUTIVE windows x_t = y[t .. t + K) (level 0 and the
+// final unsketched pass, i.e. every row of the window): the 64-row A tile of a
+// row block is the Hankel matrix of the 64 + K series values it spans, so a
+// block costs one short vector load instead of 64 x K gathered values.
+// Persistent CTAs, one per (column tile of W, SM): the CTA keeps its K x 64
+// slice of W resident in shared memory and streams row blocks, prefetching the
+// next block's series segment with cp.async while DMMA runs.  Per-tile partial
+// sums of squares go to part[tile][row]; k_rowsq_combine adds them in order.
+constexpr int kHkLd = 68;       // W slice row stride (doubles)
+constexpr int kHkRows = 128;    // rows per block (8 warps: 4 row x 2 column warp tiles)
+constexpr int kHkThreads = 256;
+
+__host__ __device__ inline int hk_kpad(int K) { return (K + 3) & ~3; }
+__host__ inline size_t rowsq_hankel_smem(int K) {
+  return ((size_t)hk_kpad(K) * kHkLd + 2 * (size_t)(kHkRows + hk_kpad(K) + 8)) * sizeof(double);
+}
+
+// CTAs per column tile are proportional to the tile's DMMA work (narrow last
+// tiles and the triangular final pass would otherwise leave SMs idle)
+struct HkPlan {
+  int ntiles;
+  int first[9];  // CTA range of tile j: [first[j], first[j + 1])
+};
+
+template <class WL, bool UPPER>
+__global__ void __launch_bounds__(kHkThreads)
+    k_rowsq_hankel(const double* __restrict__ y, int64_t n, int64_t rows, int K, WL wl, int N, HkPlan plan,
+                   double* __restrict__ part) {
+  extern __shared__ __align__(16) double hk[];
+  __shared__ double red[2][kHkRows];
+  const int kp = hk_kpad(K);
+  const int seg = kHkRows + kp + 8;
+  double* Wt = hk;
+  double* yb = hk + (size_t)kp * kHkLd;
+  int tile = 0;
+  while (tile + 1 < plan.ntiles && (int)blockIdx.x >= plan.first[tile + 1]) ++tile;
+  const int cta = blockIdx.x - plan.first[tile], nct = plan.first[tile + 1] - plan.first[tile];
+  const int N0 = tile * 64;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;
+  const int nj = min(4, max(0, (N - (N0 + 32 * wn) + 7) / 8));
+  const int kend = UPPER ? min(kp, hk_kpad(min(K, N0 + 64))) : kp;
+  for (int e = tid; e < kp * 64; e += kHkThreads) {
+    const int k = e >> 6, c = e & 63;
+    Wt[k * kHkLd + c] = (k < K && N0 + c < N) ? wl(k, N0 + c) : 0.0;
+  }
+  const int64_t nblk = (rows + kHkRows - 1) / kHkRows;
+  auto fetch = [&](int64_t b, double* dst) {
+    const int64_t t0 = b * kHkRows;
+    for (int x = tid; x < seg; x += kHkThreads) {
+      const int64_t gi = t0 + x;
+      const bool ok = gi < n;
+      const unsigned d = (unsigned)__cvta_generic_to_shared(dst + x);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(y + (ok ? gi : 0)),
+                   "r"(ok ? 8 : 0)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int buf = 0;
+  if (cta < nblk) fetch(cta, yb);
+  for (int64_t b = cta; b < nblk; b += nct) {
+    const int64_t bn = b + nct;
+    if (bn < nblk) fetch(bn, yb + (buf ^ 1) * seg);
+    if (bn < nblk) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    const double* ys = yb + buf * seg;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    if (nj > 0) {
+      const int rbase = 32 * wm + (lane >> 2) + (lane & 3);
+#pragma unroll 4
+      for (int k = 0; k < kend; k += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = ys[rbase + 8 * i + k];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = Wt[(k + (lane & 3)) * kHkLd + 32 * wn + 8 * j + (lane >> 2)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+    }
+    if ((lane & 3) == 0 || true) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v = fma(acc[i][j][0], acc[i][j][0], fma(acc[i][j][1], acc[i][j][1], v));
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if ((lane & 3) == 0) red[wn][32 * wm + 8 * i + (lane >> 2)] = v;
+      }
+    }
+    __syncthreads();
+    const int64_t t0 = b * kHkRows;
+    if (tid < kHkRows && t0 + tid < rows) part[(size_t)tile * rows + t0 + tid] = red[0][tid] + red[1][tid];
+    buf ^= 1;
+  }
+}
+
+__global__ void k_rowsq_combine(const double* __restrict__ part, int64_t rows, int ntiles,
+                                double* __restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < rows;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < ntiles; ++j) s += part[(size_t)j * rows + t];
+    out[t] = s;
+  }
+}
+
 // next approximation rows: idx = cur[sidx] (cur nullable -> identity), weights = sw
 __global__ void k_rh_compose(const int64_t* __restrict__ sidx, const double* __restrict__ sw,
                              const int64_t* __restrict__ cur, int64_t sc, int64_t* __restrict__ aidx,
