@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--n", type=int, default=None, help="override series length (debug)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--sequential", action="store_true",
+                    help="run the step's sweeps one after another instead of concurrently")
     ap.add_argument("--profile-step", action="store_true",
                     help="wrap one extra step in cudaProfilerStart/Stop (ncu --profile-from-start off)")
     return ap.parse_args()
@@ -259,19 +261,46 @@ def run_ours(args):
     ro_step = ro_sweep * len(sweeps)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MiB > L2
 
-    def one_step(seed0, want_diag=False):
-        dev = 0.0
-        launches = 0
-        diags = []
-        for k, (method, c) in enumerate(sweeps):
-            if method == "lsar":
-                fit = tf.lsar_fit(series, p_bar, c, seed0 + k, engine=eng, want_diag=want_diag)
-            else:
-                fit = tf.rh_fit(series, p_bar, c, None, seed0 + k, engine=eng, want_diag=want_diag)
-            dev += sum(fit.per_lag_seconds) + fit.upfront_seconds
-            if want_diag and fit.diag is not None:
-                diags.append((method, c, fit.diag))
-                launches += int(fit.diag.get("launches", [0])[0]) if "launches" in fit.diag else 0
+    # one context (device buffers + stream) per sweep: the four sweeps of a step
+    # are independent fits and run concurrently, each on its own
+    # stream; the step's device time is the span from the earliest sweep start
+    # to the latest sweep end (CUDA events, tf_sweep_span)
+    engs = [eng] + [tf.Engine(local) for _ in sweeps[1:]]
+    for e in engs:
+        e.upload(series)
+
+    def run_sweep(k, seed0, want_diag, fits, ser):
+        method, c = sweeps[k]
+        if method == "lsar":
+            fits[k] = tf.lsar_fit(ser, p_bar, c, seed0 + k, engine=engs[k], want_diag=want_diag)
+        else:
+            fits[k] = tf.rh_fit(ser, p_bar, c, None, seed0 + k, engine=engs[k], want_diag=want_diag)
+
+    def one_step(seed0, want_diag=False, concurrent=not args.sequential, ser=None):
+        ser = ser or series
+        fits = [None] * len(sweeps)
+        if concurrent:
+            th = [threading.Thread(target=run_sweep, args=(k, seed0, want_diag, fits, ser))
+                  for k in range(len(sweeps))]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+        else:
+            for k in range(len(sweeps)):
+                run_sweep(k, seed0, want_diag, fits, ser)
+        if any(f is None for f in fits):
+            raise RuntimeError("a sweep failed")
+        spans = [e.sweep_span(engs[0]) for e in engs]
+        if concurrent:
+            dev = (max(b for _, b in spans) - min(a for a, _ in spans)) * 1e-3
+        else:
+            dev = sum(b - a for a, b in spans) * 1e-3
+        diags, launches = [], 0
+        for k, f in enumerate(fits):
+            if want_diag and f.diag is not None:
+                diags.append((sweeps[k][0], sweeps[k][1], f.diag))
+                launches += int(f.diag["launches"][0]) if "launches" in f.diag else 0
         return dev, diags, launches
 
     for w in range(args.warmup):
@@ -304,8 +333,9 @@ def run_ours(args):
         torch.cuda.synchronize()
         torch.cuda.profiler.stop()
 
-    # ---- instrumented step: phases, launches, roofline of the fused pass ----
-    _, diags, launches = one_step(5000, want_diag=True)
+    # ---- instrumented step (sweeps one after another, so per-kernel event
+    #      times are the kernels' own): phases, launches, roofline of the pass ----
+    _, diags, launches = one_step(5000, want_diag=True, concurrent=False)
     fp64_peak = eng.probe_fp64_peak()
     peaks = {}
     try:
@@ -365,19 +395,15 @@ def run_ours(args):
 
     # ---- e2e: public API with host buffers, H2D upload + sweeps + D2H inside the timer ----
     e2e_steps = max(1, min(args.steps, 3))
-    h2d = 8 * n
-    d2h = 0
+    pinned = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    pinned[:] = y
+    h2d = 8 * n * len(engs)  # every context uploads the series from the pinned host buffer
+    d2h = 8 * len(sweeps) * (p_bar + p_bar * (p_bar + 1) // 2 + p_bar)  # taus, coefs, lag times
+    torch.cuda.synchronize()
     t0 = time.time()
     for s in range(e2e_steps):
-        fresh = tf.TimeSeries(y)          # host buffer; Engine.upload re-copies it (H2D)
-        eng.upload(fresh)
-        for k, (method, c) in enumerate(sweeps):
-            if method == "lsar":
-                fit = tf.lsar_fit(fresh, p_bar, c, 7000 + k, engine=eng)
-            else:
-                fit = tf.rh_fit(fresh, p_bar, c, None, 7000 + k, engine=eng)
-            if s == 0:
-                d2h += 8 * (p_bar + p_bar * (p_bar + 1) // 2 + p_bar)  # taus, coefs, lag times
+        fresh = tf.TimeSeries(pinned, copy=False)  # pinned host buffer; each context uploads it (H2D)
+        one_step(7000 + 10 * s, ser=fresh)
     torch.cuda.synchronize()
     t_e2e = (time.time() - t0) / e2e_steps
     if dist:
@@ -401,7 +427,12 @@ def run_ours(args):
         "config": {"workload": WORKLOAD, "n": n, "p_max": p_bar, "sweeps": [f"{m}:s={c}" for m, c in sweeps],
                    "rows_orders_per_step": ro_step, "parallelism": f"replicas x{world}",
                    "l2": "flushed between steps (256 MiB write); series 80 MB + 2 x 80 MB state > L2",
-                   "timing": "device time: CUDA events on the engine stream around each lag body"},
+                   "timing": ("device time: CUDA events (span from the earliest sweep start to the latest "
+                              "sweep end; the four sweeps run concurrently, one context and stream each)"
+                              if not args.sequential else
+                              "device time: CUDA events around each sweep, sweeps one after another"),
+                   "roofline_timing": "k_lsar_pass per-launch CUDA events in an instrumented step "
+                                      "with the sweeps run one after another"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(launches) * args.steps if launches else None,
         "clocks": clk.summary(), "wall_s_timed_region": wall,

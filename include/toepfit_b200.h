@@ -156,6 +156,11 @@ tf_status tf_shard_factor(tf_context* ctx, int p, int pass, const double* G, int
 /* phi_p (p host values) and tau_p; forms the next lag's preconditioner */
 tf_status tf_shard_finish(tf_context* ctx, int p, double* phi_out, double* tau_out);
 int64_t tf_tpu_size(int K);
+
+/* Device-time span of ctx's last sweep relative to the start of ref's last
+ * sweep (ms, CUDA events): for timing concurrent sweeps on several contexts
+ * (independent fits may run concurrently). */
+tf_status tf_sweep_span(const tf_context* ref, const tf_context* ctx, double* start_ms, double* end_ms);
 uint64_t tf_derive_seed(uint64_t seed, uint64_t tag);
 
 #ifdef __cplusplus

@@ -51,8 +51,10 @@ EXIT_CODES = {UsageError: 2, DataError: 3, NumericalError: 4}  # errors.hpp:8-9
 class TimeSeries:
     """Immutable fp64 series; validated non-empty and finite (series.cpp:23-32)."""
 
-    def __init__(self, values, label: str = ""):
-        v = np.array(values, dtype=np.float64, copy=True).ravel()
+    def __init__(self, values, label: str = "", copy: bool = True):
+        # copy=False keeps a read-only view of a contiguous fp64 array (e.g. a
+        # pinned host buffer) instead of the owning copy the reference makes
+        v = np.array(values, dtype=np.float64, copy=copy).ravel()
         if v.size == 0:
             raise DataError("series must contain at least one value")
         bad = np.flatnonzero(~np.isfinite(v))
@@ -260,6 +262,13 @@ class Engine:
             diag["up_idx"] = diag["up_idx"][:depth.value]
             diag["up_w"] = diag["up_w"][:depth.value]
         return taus, coefs, secs, up.value, pstar.value, diag
+
+    def sweep_span(self, ref: "Engine"):
+        """(start_ms, end_ms) of this engine's last sweep relative to the start
+        of ref's last sweep (device events)."""
+        a, b = C.c_double(0), C.c_double(0)
+        self._check(_abi.lib().tf_sweep_span(ref._ctx, self._ctx, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def probe_fp64_peak(self) -> float:
         v = C.c_double(0)

@@ -469,6 +469,11 @@ static void ensure_events(tf_context* ctx, size_t n) {
   }
 }
 
+static void ensure_span_events(tf_context* ctx) {
+  if (!ctx->ev_begin) CK(cudaEventCreate(&ctx->ev_begin));
+  if (!ctx->ev_end) CK(cudaEventCreate(&ctx->ev_end));
+}
+
 static void check_lsar_args(const tf_context* ctx, int p_bar, int64_t c) {
   // LsarDriver ctor (lsar.cpp:55-64)
   if (p_bar < 1) throw TfError{TF_USAGE, "maximum lag must be at least 1"};
@@ -510,6 +515,8 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
     ctx->pev.push_back(e);
   }
   const int64_t launches0 = g_launches;
+  ensure_span_events(ctx);
+  CK(cudaEventRecord(ctx->ev_begin, st));
   CK(cudaEventRecord(ctx->events[0], st));
   // lag-0 pass: r_0 = -y[0..w), s_0 = 0  ->  s_1 = y^2 / sum y^2 (lsar.cpp:11-15)
   launch_pass(ctx, 0, w, ctx->phi.get(), ctx->scal.get());
@@ -548,6 +555,7 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
     launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());
     CK(cudaEventRecord(ctx->events[p], st));
   }
+  CK(cudaEventRecord(ctx->ev_end, st));
   const int64_t launches = g_launches - launches0;
   if (d && d->rnorm2_out) launch_scan(ctx, ntile, p_bar, 0);  // R_{p_bar} for the diagnostics
   CK(cudaStreamSynchronize(st));
@@ -1004,6 +1012,8 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
   }
   ensure_events(ctx, p_bar + 2);
   const int64_t launches0 = g_launches;
+  ensure_span_events(ctx);
+  CK(cudaEventRecord(ctx->ev_begin, st));
   CK(cudaEventRecord(ctx->events[0], st));
   const double* y = ctx->y.get();
   k_fill<<<grid_for(arows_max, ctx), 256, 0, st>>>(ctx->rh_ones.get(), std::max(arows_max, depth == 0 ? m : 0), 1.0);
@@ -1125,6 +1135,7 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
                /*rev=*/1, ctx->rh_rest.get(), ctx->rh_rest.get());
     CK(cudaEventRecord(ctx->events[p + 1], st));
   }
+  CK(cudaEventRecord(ctx->ev_end, st));
   const int64_t launches = g_launches - launches0;
   CK(cudaStreamSynchronize(st));
   int sth[3];
@@ -1494,6 +1505,8 @@ void tf_destroy(tf_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (auto e : ctx->events) cudaEventDestroy(e);
+  if (ctx->ev_begin) cudaEventDestroy(ctx->ev_begin);
+  if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
   ctx->y.release(); ctx->s.release(); ctx->r.release(); ctx->chunkA.release(); ctx->chunkB.release();
   ctx->tileA.release(); ctx->tileB.release(); ctx->OT.release(); ctx->scal.release();
   ctx->Rhist.release(); ctx->Shist.release(); ctx->phi.release(); ctx->coefs.release();
@@ -1585,6 +1598,16 @@ int tf_select_order(const double* taus, int p_bar, double bound) {
 }
 
 uint64_t tf_derive_seed(uint64_t seed, uint64_t tag) { return tfk::derive_seed(seed, tag); }
+
+tf_status tf_sweep_span(const tf_context* ref, const tf_context* ctx, double* start_ms, double* end_ms) {
+  if (!ref || !ctx || !start_ms || !end_ms || !ref->ev_begin || !ctx->ev_begin || !ctx->ev_end) return TF_USAGE;
+  float a = 0.f, b = 0.f;
+  if (cudaEventElapsedTime(&a, ref->ev_begin, ctx->ev_begin) != cudaSuccess) return TF_CUDA;
+  if (cudaEventElapsedTime(&b, ref->ev_begin, ctx->ev_end) != cudaSuccess) return TF_CUDA;
+  *start_ms = a;
+  *end_ms = b;
+  return TF_OK;
+}
 
 tf_status tf_shard_open(tf_context* ctx, int p_bar, int64_t c, int64_t w_local) {
   if (!ctx) return TF_USAGE;

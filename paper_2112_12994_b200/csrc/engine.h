@@ -58,6 +58,7 @@ struct tf_context {
   int64_t sh_c = 0, sh_w = 0, sh_k = 0;
   tfe::DBuf<double> sh_buf, sh_wts;
   tfe::DBuf<int64_t> sh_idx;
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;  // span of the last sweep
   std::vector<cudaEvent_t> events;
   std::vector<cudaEvent_t> pev;  // phase events (2 per lag)
   int64_t launches = 0;

@@ -22,7 +22,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&dG, sizeof(double)*tsz); cudaMalloc(&dR, sizeof(double)*tsz); cudaMalloc(&scr, sizeof(double)*40000);
   cudaMalloc(&flags, 16); cudaMalloc(&status, 16); cudaMemset(flags, 0, 16); cudaMemset(status, 0, 16);
   cudaMemcpy(dG, Gt.data(), sizeof(double)*tsz, cudaMemcpyHostToDevice);
-  CholinvArgs a; a.G = dG; a.K = K; a.pass = 0; a.nrows = 400; a.RD = dR; a.use_smem = cholinv_in_smem(K); a.flags = flags; a.gate = nullptr; a.status = status; a.lag = 1;
+  CholinvArgs a; a.G = dG; a.K = K; a.pass = 0; a.nrows = 400; a.RD = dR; a.use_smem = cholinv_in_smem(K); a.flags = flags; a.gate = nullptr; a.status = status; a.lag = 1; a.force_b = 0; a.invert = argc > 2 ? atoi(argv[2]) : 0;
   size_t smem = a.use_smem ? cholinv_smem_bytes(K) : 0;
   cudaFuncSetAttribute(k_cholinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
