@@ -376,7 +376,10 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
 
 // ---------------------------------------------------------------------------
 
-static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev) {
+constexpr int kPassMmaMinQ = 16;  // tensor-core FIR from this lag on (sweep passes)
+
+static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev,
+                        bool exact_order = false) {
   PassArgs a;
   a.y = ctx->y.get();
   a.w = w;
@@ -390,6 +393,18 @@ static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, co
   a.tileA = ctx->tileA.get();
   a.tileB = ctx->tileB.get();
   const int64_t ntile = (w + kPassTile - 1) / kPassTile;
+  if (!exact_order && q >= kPassMmaMinQ) {
+    const size_t smem = pass_mma_smem_bytes(q);
+    static size_t attr = 0;
+    if (smem > attr) {
+      CK(cudaFuncSetAttribute(k_lsar_pass_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    k_lsar_pass_mma<<<(unsigned)ntile, kPassThreads, smem, ctx->stream>>>(a);
+    LAUNCH_CHECK("k_lsar_pass_mma");
+    COUNT_LAUNCH();
+    return;
+  }
   const size_t smem = pass_smem_bytes(q);
   static size_t attr = 0;
   if (smem > attr) {
@@ -682,7 +697,7 @@ static void residuals_op(tf_context* ctx, const double* y, int64_t n_used, int p
   CK(cudaMemsetAsync(ctx->r.get(), 0, w * sizeof(double), ctx->stream));
   CK(cudaMemcpyAsync(ctx->phi.get(), phi, p * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   k_set_unit<<<1, 1, 0, ctx->stream>>>(ctx->scal.get());
-  launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());
+  launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get(), /*exact_order=*/true);  // toeplitz.cpp:87-98 tap order
   CK(cudaMemcpyAsync(r_out, ctx->r.get(), w * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
 }

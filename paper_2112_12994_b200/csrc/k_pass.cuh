@@ -150,4 +150,138 @@ __global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass(PassArgs a) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Tensor-core variant of the fused pass for larger lags (fp64 DMMA m8n8k4).
+// The FIR over a tile is a polyphase GEMM: with rows i = 8a + b,
+//   r[8a + b] = sum_k Y[a][k] Phi[k][b],   Y[a][k] = y[i0 + 8a + k]  (Hankel, stride 8)
+//   Phi[k][b] = phi[q-1+b-k] for 0 <= q-1+b-k < q,  -1 for k = q + b  (the target),  0 else
+// so M = 256 (a), N = 8 (b), K = q + 8 per 2048-row tile; every warp owns 8
+// m8 tiles (64 a-rows = 512 outputs), tile u holding a-rows 8 g + u.  Then the
+// A fragment of tile u at k-step s equals that of tile u + 1 at step s - 2, so
+// the 8 tiles walk one shared register window (one new fragment per step).  The y tile
+// uses a padded layout (x + 4 floor(x / 64): lanes 8 g + t read x = 64 g + t)
+// that makes the fragment reads bank-conflict free; Phi fragments are tabulated once per CTA.
+// Summation order differs from the reference's tap loop (rounding ~1e-16);
+// the exact-order FMA kernel above serves tf_residuals and small lags.
+__host__ __device__ __forceinline__ int skew12(int x) { return x + 4 * (x >> 6); }
+
+inline int pass_mma_kd(int q) { return (q + 8 + 3) & ~3; }
+inline size_t pass_mma_smem_bytes(int q) {
+  const int kd = pass_mma_kd(q);
+  const int ys_n = kPassTile + kd + 8;
+  const int ys_sk = skew12(ys_n) + 8;
+  const int rn_sk = kPassTile + (kPassTile >> 4) + 2;
+  return sizeof(double) * (size_t)(kd * 8 + ys_sk + rn_sk);
+}
+
+__global__ void __launch_bounds__(kPassThreads, 3) k_lsar_pass_mma(PassArgs a) {
+  extern __shared__ double sm[];
+  const int q = a.q;
+  const int kd = (q + 8 + 3) & ~3;
+  const int ys_n = kPassTile + kd + 8;
+  double* phiF = sm;                       // [kd / 4][32]: B fragment of k-step s for each lane
+  double* ys = sm + kd * 8;
+  double* rn = ys + skew12(ys_n) + 8;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = (int64_t)blockIdx.x * kPassTile;
+  const int rows = (int)min((int64_t)kPassTile, a.w - i0);
+  const int need = rows + q;
+  for (int x = tid; x < ys_n; x += kPassThreads) ys[skew12(x)] = x < need ? __ldg(a.y + i0 + x) : 0.0;
+  for (int e = tid; e < kd * 8; e += kPassThreads) {
+    const int sstep = e >> 5, ln = e & 31;
+    const int k = 4 * sstep + (ln & 3), b = ln >> 2;
+    const int j = q - 1 + b - k;
+    phiF[e] = (j >= 0 && j < q) ? __ldg(a.phi + j) : (k == q + b ? -1.0 : 0.0);
+  }
+  __syncthreads();
+  // ---- FIR on DMMA: warp tiles a in [64 warp, 64 warp + 64) ----
+  const int g = lane >> 2, t = lane & 3;
+  const int abase = 64 * warp;
+  double c0[8], c1[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) c0[u] = c1[u] = 0.0;
+  // m8 tile u holds a-rows abase + 8 g + u (g = lane / 4), so its A fragment at
+  // k-step s is f[s + 2u] with f[m] = Y[abase + 8 g][4 m + t]
+  const int xbase = 8 * (abase + 8 * g) + t;
+  double fe[8], fo[8];  // windows for even / odd steps: fe[u] = f[s + 2u] (s even)
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    fe[u] = ys[skew12(xbase + 8 * u)];      // f[2u]     (step 0)
+    fo[u] = ys[skew12(xbase + 8 * u + 4)];  // f[2u + 1] (step 1)
+  }
+  const int nsteps = kd >> 2;
+  for (int sstep = 0; sstep < nsteps; sstep += 2) {
+    const double be = phiF[sstep * 32 + lane];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dmma_8x8x4(c0[u], c1[u], fe[u], be);
+    if (sstep + 1 < nsteps) {
+      const double bo = phiF[(sstep + 1) * 32 + lane];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dmma_8x8x4(c0[u], c1[u], fo[u], bo);
+    }
+    // advance both windows by one tile: f[s + 2 + 2u] = old window[u + 1]
+#pragma unroll
+    for (int u = 0; u < 7; ++u) {
+      fe[u] = fe[u + 1];
+      fo[u] = fo[u + 1];
+    }
+    const int xn = xbase + 8 * 8 + 8 * (sstep >> 1);  // f[sstep + 2 + 14] = Y[.][4 (sstep + 16) + t]
+    fe[7] = ys[skew12(xn)];
+    fo[7] = ys[skew12(xn + 4)];
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int r = 8 * (abase + 8 * g + u) + 2 * t;
+    rn[skew16(r)] = c0[u];
+    rn[skew16(r + 1)] = c1[u];
+  }
+  __syncthreads();
+  // ---- update + chunk partials (identical to k_lsar_pass) ----
+  double so[kPassR], ro[kPassR];
+#pragma unroll
+  for (int u = 0; u < kPassR; ++u) {
+    const int row = tid + kPassThreads * u;
+    so[u] = 0.0;
+    ro[u] = 0.0;
+    if (row < rows) {
+      so[u] = a.s[i0 + row];
+      ro[u] = a.r[i0 + row];
+    }
+  }
+  const double Rp = *a.Rprev;
+  double tA = 0.0, tB = 0.0;
+#pragma unroll
+  for (int u = 0; u < kPassR; ++u) {
+    const int row = tid + kPassThreads * u;
+    double snew = 0.0, rnew = 0.0;
+    if (row < rows) {
+      rnew = rn[skew16(row)];
+      snew = so[u] + (ro[u] * ro[u]) / Rp;
+      a.s[i0 + row] = snew;
+      a.r[i0 + row] = rnew;
+    }
+    const double cA = warp_sum(snew);
+    const double cB = warp_sum(rnew * rnew);
+    const int crow = kPassThreads * u + kChunk * warp;
+    if (lane == 0 && crow < rows) {
+      const int64_t cidx = (i0 + crow) / kChunk;
+      a.chunkA[cidx] = cA;
+      a.chunkB[cidx] = cB;
+    }
+    tA += cA;
+    tB += cB;
+  }
+  __shared__ double wA[kPassThreads / 32], wB[kPassThreads / 32];
+  if (lane == 0) {
+    wA[warp] = tA;
+    wB[warp] = tB;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    a.tileA[blockIdx.x] = ((wA[0] + wA[1]) + wA[2]) + wA[3];
+    a.tileB[blockIdx.x] = ((wB[0] + wB[1]) + wB[2]) + wB[3];
+  }
+}
+
 }  // namespace tfk
