@@ -256,11 +256,13 @@ def test_lsar_c2_full_size_properties(orc, tf, eng):
     assert (d["scores"] >= 0).all()
     phi = fit.per_lag_coefficients[-1]
     # the sweep's pass runs its FIR on tensor cores for q >= 16 (summation order
-    # differs from the reference tap loop by rounding only); the exact tap
-    # order is checked bit-for-bit through tf_residuals above
+    # differs from the reference tap loop by rounding only; with C2's large
+    # coefficients the taps cancel ~1e6-fold, so the difference is ~1e-10 of
+    # max|r|, inside the north star's 1e-9); the exact tap order is checked
+    # bit-for-bit through tf_residuals above
     for i0 in (0, w // 3, w - 5000):
         seg = y[i0:i0 + 5000 + p_bar]
         r = orc.residuals(seg, seg.size, p_bar, phi)
-        assert relerr(d["resid"][i0:i0 + 5000], r) < 1e-12
+        assert relerr(d["resid"][i0:i0 + 5000], r) < TOL
     assert relerr(d["rnorm2"][-1], float(np.dot(d["resid"], d["resid"]))) < 1e-10
     assert (d["idx"] >= 0).all() and (d["idx"] < w).all()
