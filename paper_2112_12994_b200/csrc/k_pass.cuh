@@ -27,6 +27,26 @@ constexpr int kChunksPerTile = kPassTile / kChunk;
 
 __device__ __forceinline__ int skew16(int x) { return x + (x >> 4); }
 
+// Series window -> shared memory: eight independent loads in flight per thread
+// before the stores (a load-store loop would serialise on each load's latency).
+template <int NT, class F>
+__device__ __forceinline__ void stage_y(double* ys, const double* src, int n, int need, F pos) {
+  const int tid = threadIdx.x;
+  for (int x0 = 0; x0 < n; x0 += 8 * NT) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int x = x0 + tid + NT * u;
+      v[u] = x < need ? __ldg(src + x) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int x = x0 + tid + NT * u;
+      if (x < n) ys[pos(x)] = v[u];
+    }
+  }
+}
+
 struct PassArgs {
   const double* y;
   int64_t w;          // window rows
@@ -65,8 +85,7 @@ __global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass(PassArgs a) {
   for (int t = tid; t < q; t += kPassThreads) sphi[t] = a.phi[t];
   // y[i0 .. i0 + rows + q) -- taps and targets of this tile's rows
   const int need = rows + q;
-  for (int x = tid; x < ys_n; x += kPassThreads)
-    ys[skew16(x)] = x < need ? __ldg(a.y + i0 + x) : 0.0;
+  stage_y<kPassThreads>(ys, a.y + i0, ys_n, need, [](int x) { return skew16(x); });
 
   __syncthreads();
 
@@ -175,7 +194,7 @@ inline size_t pass_mma_smem_bytes(int q) {
   return sizeof(double) * (size_t)(kd * 8 + ys_sk + rn_sk);
 }
 
-__global__ void __launch_bounds__(kPassThreads, 3) k_lsar_pass_mma(PassArgs a) {
+__global__ void __launch_bounds__(kPassThreads, 5) k_lsar_pass_mma(PassArgs a) {
   extern __shared__ double sm[];
   const int q = a.q;
   const int kd = (q + 8 + 3) & ~3;
@@ -187,7 +206,7 @@ __global__ void __launch_bounds__(kPassThreads, 3) k_lsar_pass_mma(PassArgs a) {
   const int64_t i0 = (int64_t)blockIdx.x * kPassTile;
   const int rows = (int)min((int64_t)kPassTile, a.w - i0);
   const int need = rows + q;
-  for (int x = tid; x < ys_n; x += kPassThreads) ys[skew12(x)] = x < need ? __ldg(a.y + i0 + x) : 0.0;
+  stage_y<kPassThreads>(ys, a.y + i0, ys_n, need, [](int x) { return skew12(x); });
   for (int e = tid; e < kd * 8; e += kPassThreads) {
     const int sstep = e >> 5, ln = e & 31;
     const int k = 4 * sstep + (ln & 3), b = ln >> 2;
