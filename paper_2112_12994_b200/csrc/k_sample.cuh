@@ -130,7 +130,6 @@ struct DrawArgs {
 constexpr int kDrawThreads = 256;
 
 __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
-  __shared__ double buf[kDrawThreads / 32][64];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t t = (int64_t)blockIdx.x * (kDrawThreads / 32) + wib;
   if (t >= a.c) return;
@@ -165,38 +164,38 @@ __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
   // (sketch.cpp:54-55 skips zero-mass rows backwards the same way)
   while (T > 0 && !(a.tA[T] + a.tB[T] / R > 0.0)) --T;
   double v1 = v - a.OT[T];
-  // ---- chunk within tile ----
+  // ---- chunk within tile, then row within chunk: warp-parallel CDF search.
+  //      Inclusive warp scans of the masses (fixed tree order); the pick is
+  //      the first position whose cumulative mass exceeds v with positive
+  //      mass (sketch.cpp:45-55 upper_bound + zero-mass skip); past the end,
+  //      the last positive entry (end guard).
   const int64_t nchunk = (a.w + kChunk - 1) / kChunk;
   const int64_t cb = T * kChunksPerTile;
   const int nch = (int)min((int64_t)kChunksPerTile, nchunk - cb);
-  for (int k = lane; k < 64; k += 32)
-    buf[wib][k] = k < nch ? a.chunkA[cb + k] + a.chunkB[cb + k] / R : 0.0;
-  __syncwarp();
   int chosen = -1;
   double vrow = 0.0;
-  if (lane == 0) {
-    double cum = 0.0;
+  {
+    double base = 0.0;
     int lastpos = -1;
-    for (int k = 0; k < nch; ++k) {
-      const double m = buf[wib][k];
-      if (m > 0.0) lastpos = k;
-      const double nxt = cum + m;
-      if (nxt > v1 && m > 0.0) {
-        chosen = k;
-        vrow = v1 - cum;
-        break;
+    for (int h = 0; h < 2 && chosen < 0; ++h) {
+      const int k = 32 * h + lane;
+      const double m = k < nch ? a.chunkA[cb + k] + a.chunkB[cb + k] / R : 0.0;
+      const double inc = base + warp_incl_scan(m);
+      const unsigned hit = __ballot_sync(0xffffffffu, inc > v1 && m > 0.0);
+      const unsigned pos = __ballot_sync(0xffffffffu, m > 0.0);
+      if (pos) lastpos = 32 * h + 31 - __clz(pos);
+      if (hit) {
+        const int src = __ffs(hit) - 1;
+        chosen = 32 * h + src;
+        vrow = v1 - __shfl_sync(0xffffffffu, inc - m, src);
       }
-      cum = nxt;
+      base = __shfl_sync(0xffffffffu, inc, 31);
     }
     if (chosen < 0) {
       chosen = lastpos < 0 ? nch - 1 : lastpos;
       vrow = __longlong_as_double(0x7ff0000000000000ll);  // +inf: take last positive row
     }
   }
-  chosen = __shfl_sync(0xffffffffu, chosen, 0);
-  vrow = __shfl_sync(0xffffffffu, vrow, 0);
-  __syncwarp();
-  // ---- row within chunk ----
   const int64_t r0 = (cb + chosen) * kChunk;
   const int64_t row = r0 + lane;
   double mass = 0.0;
@@ -208,24 +207,12 @@ __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
       mass = a.s[row] + 0.0 / R;  // same expression as the partials (r = 0)
     }
   }
-  buf[wib][lane] = mass;
-  __syncwarp();
+  const double incr = warp_incl_scan(mass);
+  const unsigned hitr = __ballot_sync(0xffffffffu, incr > vrow && mass > 0.0);
+  const unsigned posr = __ballot_sync(0xffffffffu, mass > 0.0);
+  const int pick = hitr ? __ffs(hitr) - 1 : (posr ? 31 - __clz(posr) : 0);
+  const double mp = __shfl_sync(0xffffffffu, mass, pick);
   if (lane == 0) {
-    double cum = 0.0;
-    int pick = -1, lastpos = -1;
-    const int nr = (int)min((int64_t)kChunk, a.w - r0);
-    for (int k = 0; k < nr; ++k) {
-      const double m = buf[wib][k];
-      if (m > 0.0) lastpos = k;
-      const double nxt = cum + m;
-      if (nxt > vrow && m > 0.0) {
-        pick = k;
-        break;
-      }
-      cum = nxt;
-    }
-    if (pick < 0) pick = lastpos < 0 ? 0 : lastpos;
-    const double mp = buf[wib][pick];
     a.idx[t] = r0 + pick;
     a.wts[t] = 1.0 / sqrt((double)a.c * (mp / (a.shard ? a.s_total : S)));
   }
