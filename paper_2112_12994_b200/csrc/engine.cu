@@ -146,18 +146,26 @@ static void gram(tf_context* ctx, const L& ld, int64_t rows, int K, double* G, c
   gram_dense(ctx, ctx->sb.M.get(), lq, rows, K, G, gate);
 }
 
-// Q = A B, B upper-triangular TPU
+// Q = A B, B upper-triangular TPU (window-row kernel: row pointers and
+// weights staged per CTA, 2-stage cp.async ring; tools/qform_bench.cu)
+static WinFwd to_win(const FwdRows& l) { return WinFwd{l.y, l.idx, l.wt, l.off}; }
+static WinRev to_win(const RevRows& l) { return WinRev{l.y, l.idx, l.wt, l.base}; }
+static WinDense to_win(const DenseRows& l) { return WinDense{l.q, l.ld}; }
+
 template <class L>
 static void qform(tf_context* ctx, const L& ld, int64_t rows, int K, const double* B, double* Q,
                   const int* gate) {
-  dim3 grid((unsigned)((rows + 63) / 64), (unsigned)((K + 63) / 64));
+  using Wt = decltype(to_win(ld));
+  constexpr size_t smem = qform_pipe_smem<2>();
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(k_qform<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQformSmem));
+    CK(cudaFuncSetAttribute(k_qform_pipe<Wt, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  k_qform<L><<<grid, kGramThreads, kQformSmem, ctx->stream>>>(ld, rows, K, B, Q, ldq_of(K), gate);
-  LAUNCH_CHECK("k_qform");
+  dim3 grid((unsigned)((rows + 63) / 64), (unsigned)((K + 63) / 64));
+  k_qform_pipe<Wt, 2, false><<<grid, kGramThreads, smem, ctx->stream>>>(to_win(ld), rows, K, B, Q, ldq_of(K),
+                                                                       gate);
+  LAUNCH_CHECK("k_qform_pipe");
   COUNT_LAUNCH();
 }
 

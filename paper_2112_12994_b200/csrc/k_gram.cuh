@@ -377,4 +377,263 @@ __global__ void __launch_bounds__(kGramThreads)
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Window-row operands for k_qform: A(t, k) = weight(t) * row(t)[dir * k].
+// The row pointers and weights of a CTA's 64 rows are read once into shared
+// memory, so each 32-column chunk costs one global load per element (not the
+// idx -> y dependent pair), and the weights scale the accumulator rows at the
+// end instead of every loaded element.
+struct WinFwd {  // w_t y[off + idx_t + k]
+  const double* y;
+  const int64_t* idx;
+  const double* wt;
+  int64_t off;
+  __device__ __forceinline__ const double* row(int64_t t) const { return y + off + idx[t]; }
+  static constexpr int dir = 1;
+  __device__ __forceinline__ double weight(int64_t t) const { return wt[t]; }
+};
+struct WinRev {  // w_t y[base + idx_t - k]
+  const double* y;
+  const int64_t* idx;
+  const double* wt;
+  int64_t base;
+  __device__ __forceinline__ const double* row(int64_t t) const { return y + base + idx[t]; }
+  static constexpr int dir = -1;
+  __device__ __forceinline__ double weight(int64_t t) const { return wt[t]; }
+};
+struct WinDense {  // q[t * ld + k]
+  const double* q;
+  int64_t ld;
+  __device__ __forceinline__ const double* row(int64_t t) const { return q + t * ld; }
+  static constexpr int dir = 1;
+  __device__ __forceinline__ double weight(int64_t) const { return 1.0; }
+};
+
+template <class W>
+__global__ void __launch_bounds__(kGramThreads)
+    k_qform_win(W win, int64_t rows, int K, const double* __restrict__ B, double* __restrict__ Q,
+                int64_t ldq, const int* skip_flag) {
+  if (skip_flag && *skip_flag == 0) return;
+  __shared__ __align__(16) double SA[64][kQA];
+  __shared__ __align__(16) double SR[32][kSJ];
+  __shared__ const double* rp[64];
+  __shared__ double rw[64];
+  const int64_t t0 = (int64_t)blockIdx.x * 64;
+  const int L0 = blockIdx.y * 64;
+  const int jend = min(K, L0 + 64);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int nj = min(4, max(0, (K - (L0 + 32 * wn) + 7) / 8));
+  if (tid < 64) {
+    const int64_t t = t0 + tid;
+    rp[tid] = t < rows ? win.row(t) : nullptr;
+    rw[tid] = t < rows ? win.weight(t) : 0.0;
+  }
+  __syncthreads();
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int cc = tid & 31, rr0 = tid >> 5;
+  const int ll = tid & 63, c0 = tid >> 6;
+  for (int k0 = 0; k0 < jend; k0 += 32) {
+    const int kc = k0 + cc;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int rr = rr0 + 4 * s;
+      const double* p = rp[rr];
+      SA[rr][cc] = (p && kc < K) ? __ldg(p + W::dir * kc) : 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int c = c0 + 2 * s;
+      const int r = k0 + c, cl = L0 + ll;
+      SR[c][ll] = (r < K && cl < K && r <= cl) ? B[tpu_idx(K, r, cl)] : 0.0;
+    }
+    __syncthreads();
+    if (nj > 0) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = SA[32 * wm + 8 * i + (lane >> 2)][4 * kk + (lane & 3)];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = SR[4 * kk + (lane & 3)][32 * wn + 8 * j + (lane >> 2)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = 32 * wm + 8 * i + (lane >> 2);
+    const int64_t row = t0 + r;
+    if (row >= rows) continue;
+    const double wr = rw[r];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = L0 + 32 * wn + 8 * j + 2 * (lane & 3);
+      if (col < K) Q[row * ldq + col] = wr * acc[i][j][0];
+      if (col + 1 < K) Q[row * ldq + col + 1] = wr * acc[i][j][1];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined window-row Q = A B: A chunks gathered with 8-byte cp.async (or
+// 16-byte when the operand is a dense even-ld matrix), B's TPU tiles copied
+// as stored ([n][k], LD 36, conflict-free fragment reads) with 16-byte
+// cp.async; STAGES-deep ring, one barrier per 32-wide k chunk; the row
+// weights scale the accumulator rows at the end.
+template <int STAGES>
+__host__ __device__ constexpr size_t qform_pipe_smem() {
+  return (size_t)STAGES * (64 * kQA + 2 * 32 * kTLD) * sizeof(double);
+}
+
+template <class W, int STAGES, bool DENSE16>
+__global__ void __launch_bounds__(kGramThreads)
+    k_qform_pipe(W win, int64_t rows, int K, const double* __restrict__ B, double* __restrict__ Q,
+                 int64_t ldq, const int* skip_flag) {
+  if (skip_flag && *skip_flag == 0) return;
+  extern __shared__ __align__(16) double qps[];
+  __shared__ const double* rp[64];
+  __shared__ double rw[64];
+  constexpr int SA_N = 64 * kQA, SB_N = 2 * 32 * kTLD;
+  const int64_t t0 = (int64_t)blockIdx.x * 64;
+  const int L0 = blockIdx.y * 64;
+  const int jend = min(K, L0 + 64);
+  const int nchunk = (jend + 31) / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int nj = min(4, max(0, (K - (L0 + 32 * wn) + 7) / 8));
+  const int JB = L0 >> 5, nbj = (K + 31) / 32;
+  if (tid < 64) {
+    const int64_t t = t0 + tid;
+    rp[tid] = t < rows ? win.row(t) : nullptr;
+    rw[tid] = t < rows ? win.weight(t) : 0.0;
+  }
+  __syncthreads();
+  auto issue = [&](int ch) {
+    double* sa = qps + (size_t)(ch % STAGES) * (SA_N + SB_N);
+    double* sb = sa + SA_N;
+    const int k0 = ch * 32;
+    if (DENSE16) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = tid + kGramThreads * u;  // 1024 16-byte chunks
+        const int r = e >> 4, c = 2 * (e & 15);
+        const double* p = rp[r];
+        const bool ok = p && k0 + c < K;
+        const unsigned d = (unsigned)__cvta_generic_to_shared(sa + r * kQA + c);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(ok ? p + k0 + c : B),
+                     "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int e = tid + kGramThreads * u;
+        const int r = e >> 5, c = e & 31;
+        const double* p = rp[r];
+        const bool ok = p && k0 + c < K;
+        const unsigned d = (unsigned)__cvta_generic_to_shared(sa + r * kQA + c);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d),
+                     "l"(ok ? p + W::dir * (k0 + c) : B), "r"(ok ? 8 : 0)
+                     : "memory");
+      }
+    }
+    const int I = k0 >> 5;
+#pragma unroll
+    for (int u = 0; u < 9; ++u) {
+      const int e = tid + kGramThreads * u;
+      if (e < 2 * 32 * 18) {
+        const int sub = e / (32 * 18), rem = e % (32 * 18);
+        const int n = rem / 18, kc = rem % 18;
+        const int J = JB + sub;
+        const bool tok = J < nbj && I <= J;
+        const bool ok = tok && n < tpu_w(J, K);
+        const double* src = ok ? B + tpu_tile(K, I, J) + (int64_t)n * kTLD + 2 * kc : B;
+        const unsigned d = (unsigned)__cvta_generic_to_shared(sb + sub * 32 * kTLD + n * kTLD + 2 * kc);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < nchunk) issue(st);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int ch = 0; ch < nchunk; ++ch) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 2) : "memory");
+    __syncthreads();
+    if (ch + STAGES - 1 < nchunk) issue(ch + STAGES - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const double* sa = qps + (size_t)(ch % STAGES) * (SA_N + SB_N);
+    const double* sb = sa + SA_N + wn * 32 * kTLD;
+    if (nj > 0) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = sa[(32 * wm + 8 * i + (lane >> 2)) * kQA + 4 * kk + (lane & 3)];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = sb[(8 * j + (lane >> 2)) * kTLD + 4 * kk + (lane & 3)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = 32 * wm + 8 * i + (lane >> 2);
+    const int64_t row = t0 + r;
+    if (row >= rows) continue;
+    const double wr = rw[r];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = L0 + 32 * wn + 8 * j + 2 * (lane & 3);
+      if (col < K) Q[row * ldq + col] = wr * acc[i][j][0];
+      if (col + 1 < K) Q[row * ldq + col + 1] = wr * acc[i][j][1];
+    }
+  }
+}
+
+// dense A rows (weights folded) for the 16-byte pipelined path
+template <class W>
+__global__ void k_gather_rows(W win, int64_t rows, int K, double* __restrict__ out, int64_t ldo) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+  if (t >= rows) return;
+  const double* p = win.row(t);
+  const double w = win.weight(t);
+  double v[8];
+  for (int j0 = 0; j0 < K; j0 += 8 * 32) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + threadIdx.x + 32 * u;
+      v[u] = j < K ? w * p[W::dir * j] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + threadIdx.x + 32 * u;
+      if (j < ldo) out[t * ldo + j] = v[u];
+    }
+  }
+}
+
 }  // namespace tfk
