@@ -123,11 +123,11 @@ static void gram_dense(tf_context* ctx, const double* Q, int64_t ld, int64_t row
   const size_t smem = gram2_smem_bytes();
   static size_t attr = 0;
   if (smem > attr) {
-    CK(cudaFuncSetAttribute(k_gram_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_gram_dense_t<kG2Stages>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
   dim3 grid(g.npair, g.nsplit);
-  k_gram_dense<<<grid, kGramThreads, smem, ctx->stream>>>(Q, ld, rows, K, g.nblk, g.rps, ctx->sb.W.get(), gate);
+  k_gram_dense_t<kG2Stages><<<grid, kGramThreads, smem, ctx->stream>>>(Q, ld, rows, K, g.nblk, g.rps, ctx->sb.W.get(), gate);
   LAUNCH_CHECK("k_gram_dense");
   k_gram_reduce<<<g.npair * 128, 256, 0, ctx->stream>>>(ctx->sb.W.get(), g.npair, g.nsplit, g.nblk, K, G, gate);
   LAUNCH_CHECK("k_gram_reduce");

@@ -153,14 +153,15 @@ __global__ void __launch_bounds__(kGramThreads)
 // are 16-byte aligned).  Each CTA owns one 64 x 64 upper tile pair and a
 // contiguous row range; 32-row slabs of the two 64-column blocks stream into
 // shared memory with cp.async (LDGSTS, 16 B, zero-fill past the last row) in
-// a 3-stage ring, so global latency overlaps the DMMA work of earlier slabs.
+// a 2-stage ring (3 CTAs per SM; 2 stages beat 3 by 2-7 % in
+// tools/gram_bench.cu), so global latency overlaps the DMMA work.
 // Partial tiles go to W[split][pair][64 x 64]; k_gram_reduce sums them in
 // split order (deterministic) with many CTAs.
-constexpr int kG2Stages = 3;
+constexpr int kG2Stages = 2;
 constexpr int kG2Ld = 68;  // padded smem row (doubles): 544 B, 16-byte aligned, conflict-free fragments
 
-__host__ __device__ inline size_t gram2_smem_bytes() {
-  return (size_t)kG2Stages * 2 * 32 * kG2Ld * sizeof(double);
+__host__ __device__ inline size_t gram2_smem_bytes(int stages = kG2Stages) {
+  return (size_t)stages * 2 * 32 * kG2Ld * sizeof(double);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -174,8 +175,9 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+template <int ST>
 __global__ void __launch_bounds__(kGramThreads)
-    k_gram_dense(const double* __restrict__ Q, int64_t ld, int64_t rows, int K, int nblk,
+    k_gram_dense_t(const double* __restrict__ Q, int64_t ld, int64_t rows, int K, int nblk,
                  int64_t rows_per_split, double* __restrict__ W, const int* skip_flag) {
   if (skip_flag && *skip_flag == 0) return;
   extern __shared__ __align__(16) double g2s[];
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(kGramThreads)
   const int wm = warp & 1, wn = warp >> 1;
   // 16-byte chunk assignment: 32 rows x 32 chunks per operand, 8 per thread
   auto issue = [&](int slab) {
-    double* sj = g2s + (size_t)(slab % kG2Stages) * 2 * 32 * kG2Ld;
+    double* sj = g2s + (size_t)(slab % ST) * 2 * 32 * kG2Ld;
     double* sl = sj + 32 * kG2Ld;
     const int64_t r0 = rb + (int64_t)slab * 32;
 #pragma unroll
@@ -223,17 +225,17 @@ __global__ void __launch_bounds__(kGramThreads)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
-  for (int s = 0; s < kG2Stages - 1; ++s) {
+  for (int s = 0; s < ST - 1; ++s) {
     if (s < nslab) issue(s);
     cp_async_commit();
   }
   for (int s = 0; s < nslab; ++s) {
-    cp_async_wait<kG2Stages - 2>();
+    cp_async_wait<ST - 2>();
     __syncthreads();
     // refill the stage consumed in the previous iteration
-    if (s + kG2Stages - 1 < nslab) issue(s + kG2Stages - 1);
+    if (s + ST - 1 < nslab) issue(s + ST - 1);
     cp_async_commit();
-    const double* SJ = g2s + (size_t)(s % kG2Stages) * 2 * 32 * kG2Ld;
+    const double* SJ = g2s + (size_t)(s % ST) * 2 * 32 * kG2Ld;
     const double* SL = diag ? SJ : SJ + 32 * kG2Ld;
     if (!wskip) {
 #pragma unroll

@@ -79,14 +79,18 @@ int main() {
         printf("%8lld %5d %7d %7d %10.1f %9.2f  (old, per_sm %d)\n", (long long)c, K, g.nsplit, g.npair, us,
                flop / (us * 1e-6) / 1e12, per_sm);
       }
-      for (int per_sm : {2, 4, 8}) {
+      for (int variant = 0; variant < 4; ++variant) {
+        const int per_sm = variant < 2 ? 4 : 6;
+        const int stages = (variant % 2) ? 2 : 3;
         Plan g = plan(c, K, sms, per_sm, 64);
         const int64_t ldq = (K + 1) / 2 * 2;
         dim3 grid(g.npair, g.nsplit);
-        const size_t sm2 = gram2_smem_bytes();
-        CK(cudaFuncSetAttribute(k_gram_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+        const size_t sm2 = gram2_smem_bytes(stages);
+        CK(cudaFuncSetAttribute(k_gram_dense_t<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram2_smem_bytes(3)));
+        CK(cudaFuncSetAttribute(k_gram_dense_t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram2_smem_bytes(2)));
         auto run = [&]() {
-          k_gram_dense<<<grid, kGramThreads, sm2>>>(Q, ldq, c, K, g.nblk, g.rps, W, nullptr);
+          if (stages == 3) k_gram_dense_t<3><<<grid, kGramThreads, sm2>>>(Q, ldq, c, K, g.nblk, g.rps, W, nullptr);
+          else k_gram_dense_t<2><<<grid, kGramThreads, sm2>>>(Q, ldq, c, K, g.nblk, g.rps, W, nullptr);
           k_gram_reduce<<<g.npair * 128, 256>>>(W, g.npair, g.nsplit, g.nblk, K, G, nullptr);
         };
         for (int it = 0; it < 3; ++it) run();
@@ -99,10 +103,11 @@ int main() {
         CK(cudaEventElapsedTime(&ms, e0, e1));
         const double us = ms * 1e3 / reps;
         const double flop = (double)c * K * (K + 1);
-        printf("%8lld %5d %7d %7d %10.1f %9.2f  (new, per_sm %d)\n", (long long)c, K, g.nsplit, g.npair, us,
-               flop / (us * 1e-6) / 1e12, per_sm);
-        // correctness vs old kernel on the same Q (ld even): compare G
-        if (per_sm == 4) {
+        printf("%8lld %5d %7d %7d %10.1f %9.2f  (stages %d, per_sm %d)\n", (long long)c, K, g.nsplit, g.npair, us,
+               flop / (us * 1e-6) / 1e12, stages, per_sm);
+        const bool check = false;
+        if (check) {
+
           std::vector<double> g1(tpu_size(K)), g2(tpu_size(K));
           CK(cudaMemcpy(g2.data(), G, sizeof(double) * g2.size(), cudaMemcpyDeviceToHost));
           Plan g0 = plan(c, K, sms, 2, 64);
