@@ -12,6 +12,7 @@
  *   tf_apply_sample    <- apply_sample(sys, sample, width, A_S, b_S)          sketch.hpp:53-54, sketch.cpp:61-79
  *   tf_solve_sampled   <- solve_compressed(apply_sample(...))                 sketch.hpp:63-64, sketch.cpp:96-101
  *   tf_select_order    <- int select_order(const PACFResult&)                 toeplitz.hpp:100, toeplitz.cpp:133-138
+ *   tf_exact_sweep     <- exact per-lag OLS fit (run_fit "exact")              bench.cpp:27-48
  *
  * Conventions (mirroring the reference): indices are 0-based int64, series
  * and coefficients are fp64; errors never cross the ABI as exceptions --
@@ -111,6 +112,12 @@ tf_status tf_lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed,
 tf_status tf_rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg, uint64_t seed,
                       const tf_rh_diag* diag, double* taus, double* coefs_packed,
                       double* lag_seconds, double* upfront_seconds, int* p_star);
+
+/* Exact per-lag OLS on the full series (bench.cpp:27-48, the reference's
+ * "exact" method): lag h uses all n - h rows.  Outputs as tf_lsar_sweep;
+ * p_star uses the bound 1.96 / sqrt(n - p_bar). */
+tf_status tf_exact_sweep(tf_context* ctx, int p_bar, double* taus, double* coefs_packed, double* lag_seconds,
+                         int* p_star);
 
 /* ---- single operations on host buffers (tests, integration) ---- */
 tf_status tf_residuals(tf_context* ctx, const double* y, int64_t n_used, int p, const double* phi,

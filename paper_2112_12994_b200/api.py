@@ -263,6 +263,16 @@ class Engine:
             diag["up_w"] = diag["up_w"][:depth.value]
         return taus, coefs, secs, up.value, pstar.value, diag
 
+    def exact_sweep(self, p_bar: int):
+        pb = max(int(p_bar), 1)
+        taus = np.zeros(pb)
+        coefs = np.zeros(pb * (pb + 1) // 2)
+        secs = np.zeros(pb)
+        pstar = C.c_int(0)
+        self._check(_abi.lib().tf_exact_sweep(self._ctx, int(p_bar), ptr(taus), ptr(coefs), ptr(secs),
+                                              C.byref(pstar)))
+        return taus, coefs, secs, pstar.value
+
     def sweep_span(self, ref: "Engine"):
         """(start_ms, end_ms) of this engine's last sweep relative to the start
         of ref's last sweep (device events)."""
@@ -372,6 +382,16 @@ def rh_fit(series: TimeSeries, p_bar: int, c: int, config: RHConfig | None = Non
     return _finish("rh", taus, coefs, secs, pstar, p_bar, c, up, diag)
 
 
+def exact_fit(series: TimeSeries, p_bar: int, *, engine: Engine | None = None) -> FitResult:
+    """Exact per-lag OLS on the full series (bench.cpp:27-48) on the GPU."""
+    eng = engine or default_engine()
+    eng.upload(series)
+    taus, coefs, secs, pstar = eng.exact_sweep(p_bar)
+    fit = _finish("exact", taus, coefs, secs, pstar, p_bar, 1, 0.0, None)
+    fit.pacf.bound = 1.96 / math.sqrt(float(series.size() - p_bar))
+    return fit
+
+
 def select_order(pacf: PACFResult) -> int:
     t = np.ascontiguousarray(pacf.taus, dtype=np.float64)
     return int(_abi.lib().tf_select_order(ptr(t), t.size, float(pacf.bound)))
@@ -396,11 +416,13 @@ class RunReport:
 def run_fit(series: TimeSeries, method: str, p_bar: int, c: int, seed: int,
             with_timing: bool = True, engine: Engine | None = None) -> RunReport:
     """bench.cpp:107-124 restricted to the GPU methods (lsar, rh)."""
-    if method in ("exact", "srht"):
-        raise UsageError(f"method '{method}' is outside the B200 hot path (lsar | rh)")
-    if c < 1:
+    if method == "srht":
+        raise UsageError(f"method '{method}' is outside the B200 hot path (lsar | rh | exact)")
+    if method != "exact" and c < 1:
         raise UsageError(f"method '{method}' needs a sample count")
-    if method == "lsar":
+    if method == "exact":
+        fit = exact_fit(series, p_bar, engine=engine)
+    elif method == "lsar":
         fit = lsar_fit(series, p_bar, c, seed, engine=engine)
     elif method == "rh":
         fit = rh_fit(series, p_bar, c, None, seed, engine=engine)

@@ -1441,6 +1441,68 @@ static void shard_finish(tf_context* ctx, int p, double* phi_out, double* tau_ou
   CK(cudaStreamSynchronize(st));
 }
 
+// ---------------------------------------------------------------------------
+// Exact per-lag OLS on the full series (bench.cpp:27-48):
+// lag h uses every row i = 0..n-h-1 (forward order y[i .. i + h], target
+// last), solved by the same preconditioned CholeskyQR as the sampled systems;
+// lag h - 1's factor preconditions lag h (its rows are a superset).
+
+static void exact_sweep(tf_context* ctx, int p_bar, double* taus, double* coefs, double* lag_seconds,
+                        int* p_star) {
+  if (p_bar < 1) throw TfError{TF_USAGE, "maximum lag must be at least 1"};
+  if (ctx->n == 0) throw TfError{TF_USAGE, "no series uploaded"};
+  const int64_t n = ctx->n;
+  if (n <= (int64_t)p_bar + 1) throw TfError{TF_DATA, "series too short for maximum lag " + std::to_string(p_bar)};
+  const int64_t rows_max = n - 1;
+  cudaStream_t st = ctx->stream;
+  alloc_state(ctx, p_bar, 1, 1);
+  ctx->rh_aidx.need(rows_max);
+  ctx->rh_ones.need(rows_max);
+  k_iota<<<grid_for(rows_max, ctx), 256, 0, st>>>(ctx->rh_aidx.get(), rows_max);
+  k_fill<<<grid_for(rows_max, ctx), 256, 0, st>>>(ctx->rh_ones.get(), rows_max, 1.0);
+  g_launches += 2;
+  reserve_solve(ctx, rows_max, p_bar + 1);
+  ctx->rh_rest.need(2);
+  ensure_events(ctx, p_bar + 1);
+  ensure_span_events(ctx);
+  CK(cudaEventRecord(ctx->ev_begin, st));
+  CK(cudaEventRecord(ctx->events[0], st));
+  for (int h = 1; h <= p_bar; ++h) {
+    const int64_t m = n - h;
+    SolveOut o;
+    o.phi = ctx->phi.get();
+    o.coefs = ctx->coefs.get();
+    o.coef_off = (int64_t)(h - 1) * h / 2;
+    o.taus = ctx->taus.get();
+    o.method = ctx->method.get();
+    o.lag = h;
+    o.status = ctx->status.get();
+    FwdRows ld{ctx->y.get(), ctx->rh_aidx.get(), ctx->rh_ones.get(), 0};
+    double* Snext = (h & 1) ? ctx->sb.S1.get() : ctx->sb.S0.get();
+    const double* Sprev = (h & 1) ? ctx->sb.S0.get() : ctx->sb.S1.get();
+    solve_rows(ctx, ld, m, h + 1, o, h >= 2 ? Sprev : nullptr, h >= 2 ? ctx->phi.get() : nullptr, Snext, 0,
+               ctx->rh_rest.get(), ctx->rh_rest.get());
+    CK(cudaEventRecord(ctx->events[h], st));
+  }
+  CK(cudaEventRecord(ctx->ev_end, st));
+  CK(cudaStreamSynchronize(st));
+  int sth[3];
+  CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  raise_from_status(sth);
+  std::vector<double> t(p_bar);
+  CK(cudaMemcpy(t.data(), ctx->taus.get(), p_bar * sizeof(double), cudaMemcpyDeviceToHost));
+  if (taus) std::memcpy(taus, t.data(), p_bar * sizeof(double));
+  if (coefs)
+    CK(cudaMemcpy(coefs, ctx->coefs.get(), sizeof(double) * (size_t)p_bar * (p_bar + 1) / 2, cudaMemcpyDeviceToHost));
+  if (lag_seconds)
+    for (int h = 1; h <= p_bar; ++h) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ctx->events[h - 1], ctx->events[h]));
+      lag_seconds[h - 1] = ms * 1e-3;
+    }
+  if (p_star) *p_star = tf_select_order(t.data(), p_bar, 1.96 / std::sqrt((double)(n - p_bar)));
+}
+
 __global__ void __launch_bounds__(256) k_dfma_probe(double* out, int iters, double seed) {
   double a0 = seed + threadIdx.x, a1 = a0 * 0.5, a2 = a0 * 0.25, a3 = a0 * 0.125;
   double a4 = a0 + 1, a5 = a1 + 1, a6 = a2 + 1, a7 = a3 + 1;
@@ -1621,6 +1683,12 @@ int tf_select_order(const double* taus, int p_bar, double bound) {
 }
 
 uint64_t tf_derive_seed(uint64_t seed, uint64_t tag) { return tfk::derive_seed(seed, tag); }
+
+tf_status tf_exact_sweep(tf_context* ctx, int p_bar, double* taus, double* coefs_packed, double* lag_seconds,
+                         int* p_star) {
+  if (!ctx) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::exact_sweep(ctx, p_bar, taus, coefs_packed, lag_seconds, p_star); });
+}
 
 tf_status tf_sweep_span(const tf_context* ref, const tf_context* ctx, double* start_ms, double* end_ms) {
   if (!ref || !ctx || !start_ms || !end_ms || !ref->ev_begin || !ctx->ev_begin || !ctx->ev_end) return TF_USAGE;

@@ -742,6 +742,7 @@ __global__ void __launch_bounds__(kPhiThreads) k_phi_solve(PhiSolveArgs a) {
     if (threadIdx.x == 0) {
       if (a.taus) a.taus[a.lag - 1] = -s[0] / spp;
       if (a.method) a.method[a.lag - 1] = hasC ? 3 : (hasB ? 2 : 1);
+      if (a.rest_out) a.rest_out[0] = 1.0 / (spp * spp);  // ||r||^2 of this system
     }
     return;
   }

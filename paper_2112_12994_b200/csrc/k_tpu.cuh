@@ -225,6 +225,8 @@ __global__ void k_solve_k2(const double* G, PhiSArgs a) {
     if (a.rev && a.rest_out) {
       const double s00 = 1.0 / r00, s01 = -r01 / (r00 * r11);
       a.rest_out[0] = 1.0 / (s00 * s00 + s01 * s01);
+    } else if (a.rest_out) {
+      a.rest_out[0] = piv;  // forward order: ||r||^2 = g11 - g01^2 / g00
     }
   }
 }

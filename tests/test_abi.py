@@ -89,8 +89,10 @@ def test_host_mirror_validation():
     bad = tf.RHConfig(base_threshold=10, sample_count=20, gaussian_rows=3)
     with pytest.raises(tf.UsageError):
         bad.validate()
+    with pytest.raises(tf.UsageError):  # outside the GPU path, rejected before any device work
+        tf.run_fit(tf.TimeSeries([1.0, 2.0, 3.0]), "srht", 1, 10, 0)
     with pytest.raises(tf.UsageError):
-        tf.run_fit(tf.TimeSeries([1.0, 2.0, 3.0]), "exact", 1, 0, 0)
+        tf.run_fit(tf.TimeSeries([1.0, 2.0, 3.0]), "lsar", 1, 0, 0)
 
 
 def test_report_json_schema():
