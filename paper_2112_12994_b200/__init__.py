@@ -5,7 +5,7 @@ libtoepfit_b200.so (hand-written sm_100a kernels); see DESIGN.md.
 """
 from .api import (CudaError, DataError, Engine, FitResult, NumericalError, PACFResult, RHConfig,  # noqa: F401
                   RunReport, TimeSeries, UsageError, default_engine, derive_seed, lsar_fit,
-                  report_to_json, rh_fit, run_fit, select_order, exact_fit)
+                  report_to_json, rh_fit, run_fit, select_order, exact_fit, fit_many)
 
 __all__ = ["TimeSeries", "FitResult", "PACFResult", "RHConfig", "RunReport", "Engine",
            "UsageError", "DataError", "NumericalError", "CudaError", "lsar_fit", "rh_fit",

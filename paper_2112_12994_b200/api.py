@@ -392,6 +392,55 @@ def exact_fit(series: TimeSeries, p_bar: int, *, engine: Engine | None = None) -
     return fit
 
 
+def fit_many(series_list, method: str, p_bar: int, c: int, seeds, *, workers: int = 8,
+             device: int = 0, config: RHConfig | None = None) -> list:
+    """Independent fits (many series, or many seeds over one series -- the
+    reference's run_compare / run_sweep loops, bench.cpp:183-188, 221-228, and
+    the BASELINE C5 batch) run concurrently: `workers` contexts, one CUDA
+    stream each, fed from a shared queue (independent fits may run
+    concurrently).  Returns FitResults in input order."""
+    import threading
+    items = list(zip(series_list, seeds))
+    out = [None] * len(items)
+    errors = []
+    lock = threading.Lock()
+    nxt = [0]
+
+    def work():
+        eng = Engine(device)
+        try:
+            while True:
+                with lock:
+                    k = nxt[0]
+                    nxt[0] += 1
+                if k >= len(items) or errors:
+                    return
+                ser, seed = items[k]
+                if not isinstance(ser, TimeSeries):
+                    ser = TimeSeries(ser)
+                if method == "lsar":
+                    out[k] = lsar_fit(ser, p_bar, c, seed, engine=eng)
+                elif method == "rh":
+                    out[k] = rh_fit(ser, p_bar, c, config, seed, engine=eng)
+                elif method == "exact":
+                    out[k] = exact_fit(ser, p_bar, engine=eng)
+                else:
+                    raise UsageError(f"unknown method '{method}'")
+        except Exception as e:  # noqa: BLE001 -- re-raised in the caller
+            errors.append(e)
+        finally:
+            eng.close()
+
+    th = [threading.Thread(target=work) for _ in range(max(1, min(workers, len(items))))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errors:
+        raise errors[0]
+    return out
+
+
 def select_order(pacf: PACFResult) -> int:
     t = np.ascontiguousarray(pacf.taus, dtype=np.float64)
     return int(_abi.lib().tf_select_order(ptr(t), t.size, float(pacf.bound)))

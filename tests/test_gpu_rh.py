@@ -129,3 +129,17 @@ def test_rh_errors(tf, eng):
         tf.rh_fit(tf.TimeSeries(y[:5]), 4, 100, None, 1, engine=eng)
     with pytest.raises(tf.NumericalError):  # approximation rows < k
         tf.rh_fit(tf.TimeSeries(y), 20, 25, tf.RHConfig(30, 10, 8, 1), 1, engine=eng)
+
+
+def test_fit_many_matches_sequential(tf, eng):
+    # concurrent contexts give exactly the sequential results (same kernels, same seeds)
+    ys = [c1_like(8000 + 500 * k, seed=40 + k, q=4) for k in range(6)]
+    seeds = [3 + k for k in range(6)]
+    many = tf.fit_many(ys, "lsar", 10, 300, seeds, workers=3)
+    for y, s, f in zip(ys, seeds, many):
+        ref = tf.lsar_fit(tf.TimeSeries(y), 10, 300, s, engine=eng)
+        assert f.pacf.taus == ref.pacf.taus and f.p_star == ref.p_star
+    rh = tf.fit_many(ys[:3], "rh", 8, 300, seeds[:3], workers=3)
+    for y, s, f in zip(ys[:3], seeds[:3], rh):
+        ref = tf.rh_fit(tf.TimeSeries(y), 8, 300, None, s, engine=eng)
+        assert f.pacf.taus == ref.pacf.taus
