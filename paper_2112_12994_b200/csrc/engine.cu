@@ -169,8 +169,55 @@ static void qform(tf_context* ctx, const L& ld, int64_t rows, int K, const doubl
   COUNT_LAUNCH();
 }
 
+// blocked multi-launch Cholesky for K > kCholinvMaxK (RD output, no inverse)
+static void cholinv_big(tf_context* ctx, const double* G, int K, int pass, int64_t rows, double* RD,
+                        const int* gate, int lag, int* status, int force_b) {
+  ctx->sh_buf.need(16);
+  ctx->rh_flag.need(8);
+  BigChol a;
+  a.G = G;
+  a.RD = RD;
+  a.K = K;
+  a.nrows = rows;
+  a.pass = pass;
+  a.force_b = force_b;
+  a.flags = ctx->sb.flags.get();
+  a.work = ctx->rh_flag.get() + 4;
+  a.tr = ctx->sh_buf.get() + 8;
+  a.gate = gate;
+  a.status = status;
+  a.lag = lag;
+  cudaStream_t st = ctx->stream;
+  const int nb = (K + 31) / 32;
+  const unsigned cgrid = (unsigned)std::min<int64_t>(148, (tpu_size(K) + 255) / 256);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    k_bchol_arm<<<1, 32, 0, st>>>(a, attempt);
+    k_bchol_copy<<<cgrid, 256, 0, st>>>(a);
+    k_bchol_shift<<<1, 256, 0, st>>>(a);
+    g_launches += 3;
+    for (int b = 0; b < nb; ++b) {
+      k_bchol_diag<<<1, 32, 0, st>>>(a, b);
+      ++g_launches;
+      if (b + 1 < nb) {
+        const int nt = nb - 1 - b;
+        k_bchol_panel<<<nt, 64, 0, st>>>(a, b);
+        k_bchol_syrk<<<nt * (nt + 1) / 2, 64, 0, st>>>(a, b);
+        g_launches += 2;
+      }
+    }
+    if (pass != 0) break;  // only pass A retries with a shift
+  }
+  k_bchol_finish<<<1, 256, 0, st>>>(a);
+  LAUNCH_CHECK("k_bchol");
+  COUNT_LAUNCH();
+}
+
 static void cholinv(tf_context* ctx, const double* G, int K, int pass, int64_t rows, double* RD,
                     const int* gate, int lag, int* status, int force_b = 0, int invert = 0) {
+  if (!cholinv_in_smem(K) && !invert) {
+    cholinv_big(ctx, G, K, pass, rows, RD, gate, lag, status, force_b);
+    return;
+  }
   CholinvArgs a;
   a.G = G;
   a.K = K;

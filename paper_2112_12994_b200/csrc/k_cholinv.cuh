@@ -824,3 +824,163 @@ __global__ void __launch_bounds__(64)
 }
 
 }  // namespace tfk
+
+namespace tfk {
+
+// ---------------------------------------------------------------------------
+// Cholesky for K > kCholinvMaxK (the TPU matrix no longer fits one SM's
+// shared memory): the same blocked right-looking factorization as k_cholinv,
+// one launch per phase of every block step -- the diagonal tile on one CTA,
+// the panel and the trailing update spread over many CTAs (2 warps each, one
+// per column half) -- on the L2-resident working copy.  Same RD output,
+// shift-and-retry on breakdown (pass A), cond gate and flags as k_cholinv.
+struct BigChol {
+  const double* G;
+  double* RD;
+  int K;
+  int64_t nrows;
+  int pass;
+  int force_b;
+  int* flags;     // solve flags: [0] shifted, [1] failed, [2] need pass B
+  int* work;      // [0] bad pivot, [1] attempt armed, [2] shifted
+  double* tr;     // trace of G
+  const int* gate;
+  int* status;
+  int lag;
+};
+
+__device__ __forceinline__ bool bchol_skip(const BigChol& a) {
+  if (a.gate && *a.gate == 0) return true;
+  if (a.pass > 0 && a.flags[1] != 0) return true;
+  return false;
+}
+
+__global__ void k_bchol_arm(BigChol a, int attempt) {
+  if (bchol_skip(a) || threadIdx.x != 0) return;
+  if (attempt == 0) {
+    double t = 0.0;
+    for (int i = 0; i < a.K; ++i) t += a.G[tpu_idx(a.K, i, i)];
+    a.tr[0] = t;
+    a.work[0] = 0;
+    a.work[1] = 1;
+    a.work[2] = 0;
+    return;
+  }
+  // second attempt only for pass A after a breakdown (shifted CholeskyQR3)
+  const int again = a.work[0] != 0 && a.pass == 0;
+  if (a.work[0] != 0 && a.pass != 0) {
+    a.flags[1] = 1;
+    raise_status(a.status, kErrNumerical, a.lag, kReasonCholFail);
+  }
+  a.work[1] = again;
+  if (again) {
+    a.work[0] = 0;
+    a.work[2] = 1;
+  }
+}
+
+__global__ void k_bchol_copy(BigChol a) {
+  if (bchol_skip(a) || a.work[1] == 0) return;
+  const int64_t n = tpu_size(a.K);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    a.RD[e] = a.G[e];
+}
+
+// shifted retry: RD(i, i) += shift (after the copy kernel)
+__global__ void k_bchol_shift(BigChol a) {
+  if (bchol_skip(a) || a.work[1] == 0 || a.work[2] == 0) return;
+  const double shift = 11.0 * ((double)a.nrows * a.K + (double)a.K * (a.K + 1)) * 2.220446049250313e-16 * a.tr[0];
+  for (int i = threadIdx.x; i < a.K; i += blockDim.x) a.RD[tpu_idx(a.K, i, i)] += shift;
+}
+
+__global__ void __launch_bounds__(32) k_bchol_diag(BigChol a, int b) {
+  if (bchol_skip(a) || a.work[1] == 0 || a.work[0] != 0) return;
+  __shared__ __align__(16) double s_S[32 * kTLD];
+  __shared__ double s_DI[4 * 64], s_TS[4 * 64];
+  const int K = a.K, nb = (K + 31) / 32;
+  const int m = tpu_w(b, K);
+  const double floor = 4.930380657631324e-32 * a.tr[0];
+  const bool bad = ci_diag_tile(a.RD + tpu_tile(K, b, b), m, b == nb - 1 ? m - 1 : -1, floor, s_S, s_DI, s_TS);
+  if (bad && threadIdx.x == 0) a.work[0] = 1;
+}
+
+// R(b, J) = Dinv_b^T G(b, J), J > b: CTA per J, warp per column half
+__global__ void __launch_bounds__(64) k_bchol_panel(BigChol a, int b) {
+  if (bchol_skip(a) || a.work[1] == 0 || a.work[0] != 0) return;
+  const int K = a.K;
+  const int J = b + 1 + blockIdx.x;
+  const int n0 = 16 * (threadIdx.x >> 5);
+  const int wJ = tpu_w(J, K);
+  if (n0 >= wJ) return;
+  CITiles T;
+  T.base = a.RD;
+  T.K = K;
+  const double* Db = T.tile(b, b);
+  double* tj = T.tile(b, J);
+  double acc[4][2][2];
+  ci_zero(acc);
+  ci_mma(acc, n0, [&](int mm, int k) { return Db[mm * kTLD + k]; },
+         [&](int k, int n) { return n < wJ ? tj[n * kTLD + k] : 0.0; });
+  __syncwarp();
+  ci_put<0>(tj, wJ, n0, acc);
+}
+
+// G(I, J) -= R(b, I)^T R(b, J) for b < I <= J: CTA per tile pair, warp per column half
+__global__ void __launch_bounds__(64) k_bchol_syrk(BigChol a, int b) {
+  if (bchol_skip(a) || a.work[1] == 0 || a.work[0] != 0) return;
+  const int K = a.K, nb = (K + 31) / 32;
+  const int nt = nb - 1 - b;  // trailing tile count
+  int rem = blockIdx.x, I = 0;
+  while (rem >= nt - I) {
+    rem -= nt - I;
+    ++I;
+  }
+  const int J = I + rem;
+  const int n0 = 16 * (threadIdx.x >> 5);
+  if (n0 >= tpu_w(b + 1 + J, K)) return;
+  CITiles T;
+  T.base = a.RD;
+  T.K = K;
+  ci_syrk_item(T, b, b + 1 + I, b + 1 + J, n0);
+}
+
+// cond lower bound and the pass flags (as k_cholinv's epilogue)
+__global__ void __launch_bounds__(256) k_bchol_finish(BigChol a) {
+  if (bchol_skip(a)) return;
+  __shared__ double red[8];
+  const int K = a.K, nb = (K + 31) / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (a.work[0] != 0) {  // still broken after the retry (or pass B/C breakdown)
+    if (threadIdx.x == 0) {
+      a.flags[1] = 1;
+      raise_status(a.status, kErrNumerical, a.lag, kReasonCholFail);
+    }
+    return;
+  }
+  if (a.pass != 0) return;
+  double ss = 0.0;
+  for (int J = warp; J < nb; J += 8) {
+    const double* dt = a.RD + tpu_tile(K, J, J);
+    const int w = tpu_w(J, K);
+    for (int e = lane; e < 32 * w; e += 32) {
+      const double v = dt[(e >> 5) * kTLD + (e & 31)];
+      ss = fma(v, v, ss);
+    }
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) red[warp] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    const int shifted = a.work[2];
+    const double shift =
+        shifted ? 11.0 * ((double)a.nrows * K + (double)K * (K + 1)) * 2.220446049250313e-16 * a.tr[0] : 0.0;
+    const double cond_lb = sqrt((a.tr[0] + K * shift) * t);
+    a.flags[0] = shifted;
+    a.flags[1] = 0;
+    a.flags[2] = (a.force_b || shifted || !(cond_lb <= 8.0 * K)) ? 1 : 0;
+  }
+}
+
+}  // namespace tfk
