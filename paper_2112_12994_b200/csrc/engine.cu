@@ -283,10 +283,6 @@ static void reserve_gram(tf_context* ctx, int64_t rows, int Kmax) {
     wmax = std::max(wmax, (size_t)g.nsplit * g.npair * 4096);
   }
   b.W.need(wmax);
-  if (b.tickets.n < 4096) {
-    b.tickets.need(4096);
-    CK(cudaMemset(b.tickets.get(), 0, 4096 * sizeof(int)));
-  }
 }
 
 // Size every solve buffer for the largest system of a sweep up front so that
@@ -1648,7 +1644,7 @@ void tf_destroy(tf_context* ctx) {
   tfe::SolveBufs& b = ctx->sb;
   b.W.release(); b.G.release(); b.RA.release(); b.RB.release(); b.RC.release(); b.SA.release();
   b.SB.release(); b.SC.release(); b.T.release(); b.S0.release(); b.S1.release(); b.Q1.release();
-  b.Q2.release(); b.M.release(); b.RI.release(); b.flags.release(); b.tickets.release();
+  b.Q2.release(); b.M.release(); b.RI.release(); b.flags.release();
   ctx->rh_J.release(); ctx->rh_cnt.release(); ctx->rh_start.release(); ctx->rh_fill.release();
   ctx->rh_bk.release(); ctx->rh_pick.release(); ctx->rh_ok.release(); ctx->rh_flag.release();
   ctx->rh_tsum.release(); ctx->rh_lvl.release(); ctx->rh_aidx.release(); ctx->rh_sidx.release();

@@ -28,7 +28,7 @@ struct DBuf {
 
 struct SolveBufs {
   DBuf<double> W, G, RA, RB, RC, SA, SB, SC, T, S0, S1, Q1, Q2, M, RI;
-  DBuf<int> flags, tickets;
+  DBuf<int> flags;
 };
 
 }  // namespace tfe

@@ -60,25 +60,6 @@ int main() {
   printf("%8s %5s %7s %7s %10s %9s\n", "c", "K", "nsplit", "npair", "us", "TF/s(alg)");
   for (int64_t c : {10000LL, 100000LL}) {
     for (int K : {17, 33, 64, 100, 128, 160, 201, 301}) {
-      for (int per_sm : {2, 6}) {
-        Plan g = plan(c, K, sms, per_sm, 64);
-        DenseRows ld{Q, K};
-        dim3 grid(g.npair, g.nsplit);
-        for (int it = 0; it < 3; ++it)
-          k_gram<DenseRows><<<grid, kGramThreads>>>(ld, c, K, g.nblk, g.rps, W, G, tickets, nullptr);
-        CK(cudaEventRecord(e0));
-        const int reps = 20;
-        for (int it = 0; it < reps; ++it)
-          k_gram<DenseRows><<<grid, kGramThreads>>>(ld, c, K, g.nblk, g.rps, W, G, tickets, nullptr);
-        CK(cudaEventRecord(e1));
-        CK(cudaEventSynchronize(e1));
-        float ms;
-        CK(cudaEventElapsedTime(&ms, e0, e1));
-        const double us = ms * 1e3 / reps;
-        const double flop = (double)c * K * (K + 1);  // upper half, 2 flop per FMA
-        printf("%8lld %5d %7d %7d %10.1f %9.2f  (old, per_sm %d)\n", (long long)c, K, g.nsplit, g.npair, us,
-               flop / (us * 1e-6) / 1e12, per_sm);
-      }
       for (int variant = 0; variant < 4; ++variant) {
         const int per_sm = variant < 2 ? 4 : 6;
         const int stages = (variant % 2) ? 2 : 3;
@@ -105,24 +86,6 @@ int main() {
         const double flop = (double)c * K * (K + 1);
         printf("%8lld %5d %7d %7d %10.1f %9.2f  (stages %d, per_sm %d)\n", (long long)c, K, g.nsplit, g.npair, us,
                flop / (us * 1e-6) / 1e12, stages, per_sm);
-        const bool check = false;
-        if (check) {
-
-          std::vector<double> g1(tpu_size(K)), g2(tpu_size(K));
-          CK(cudaMemcpy(g2.data(), G, sizeof(double) * g2.size(), cudaMemcpyDeviceToHost));
-          Plan g0 = plan(c, K, sms, 2, 64);
-          DenseRows ld{Q, ldq};
-          k_gram<DenseRows><<<dim3(g0.npair, g0.nsplit), kGramThreads>>>(ld, c, K, g0.nblk, g0.rps, W, G, tickets, nullptr);
-          CK(cudaMemcpy(g1.data(), G, sizeof(double) * g1.size(), cudaMemcpyDeviceToHost));
-          double md = 0, mx = 0;
-          for (int r = 0; r < K; ++r)
-            for (int cc = r; cc < K; ++cc) {
-              const int64_t ix = tpu_idx(K, r, cc);
-              md = std::max(md, std::fabs(g1[ix] - g2[ix]));
-              mx = std::max(mx, std::fabs(g1[ix]));
-            }
-          printf("          check: max|dG|/max|G| = %.3e\n", md / mx);
-        }
       }
     }
   }

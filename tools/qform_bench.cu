@@ -38,7 +38,6 @@ int main() {
     for (int K : {65, 129, 201}) {
       const int64_t ldq = (K + 1) & ~1;
       dim3 grid((unsigned)((c + 63) / 64), (unsigned)((K + 63) / 64));
-      FwdRows fr{y, idx, wt, 0};
       WinFwd wf{y, idx, wt, 0};
       auto timeit = [&](auto launch, const char* name) {
         for (int i = 0; i < 3; ++i) launch();
@@ -52,8 +51,6 @@ int main() {
         fma *= c;
         printf("c=%6lld K=%3d %-14s %8.1f us  %6.2f TFLOP/s (padded)\n", (long long)c, K, name, us, 2 * fma / (us * 1e-6) / 1e12);
       };
-      timeit([&] { k_qform<FwdRows><<<grid, kGramThreads, kQformSmem>>>(fr, c, K, T, Q, ldq, nullptr); }, "k_qform");
-      timeit([&] { k_qform_win<WinFwd><<<grid, kGramThreads>>>(wf, c, K, T, Q, ldq, nullptr); }, "k_qform_win");
       {
         static bool once = false;
         if (!once) {
