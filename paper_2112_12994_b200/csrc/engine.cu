@@ -5,8 +5,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -32,9 +34,12 @@ static void cuda_check(cudaError_t e, const char* what) {
 static thread_local int64_t g_launches = 0;
 #define COUNT_LAUNCH() (++g_launches)
 
+std::atomic<uint64_t> g_alloc_gen{0};  // bumped by every device (re)allocation
+
 template <class T>
 void DBuf<T>::need(size_t count) {
   if (count <= n && p) return;
+  g_alloc_gen.fetch_add(1);
   if (p) cudaFree(p);
   p = nullptr;
   n = 0;
@@ -478,11 +483,13 @@ static void launch_scan(tf_context* ctx, int64_t ntile, int lag, int check_r, in
 }
 
 static void launch_draw(tf_context* ctx, uint64_t seed, int64_t c, int64_t w, int64_t* idx,
-                        double* wts) {
+                        double* wts, const uint64_t* seed_ptr = nullptr) {
   DrawArgs a;
   a.shard = 0;
   a.accept = nullptr;
+  a.seed_ptr = nullptr;
   a.seed = seed;
+  a.seed_ptr = seed_ptr;
   a.c = c;
   a.scal = ctx->scal.get();
   a.OT = ctx->OT.get();
@@ -580,50 +587,113 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
     CK(cudaEventCreate(&e));
     ctx->pev.push_back(e);
   }
-  const int64_t launches0 = g_launches;
   ensure_span_events(ctx);
-  CK(cudaEventRecord(ctx->ev_begin, st));
-  CK(cudaEventRecord(ctx->events[0], st));
-  // lag-0 pass: r_0 = -y[0..w), s_0 = 0  ->  s_1 = y^2 / sum y^2 (lsar.cpp:11-15)
-  launch_pass(ctx, 0, w, ctx->phi.get(), ctx->scal.get());
-  for (int p = 1; p <= p_bar; ++p) {
-    const int q = p - 1;
-    launch_scan(ctx, ntile, q, 1);
-    int64_t* idx = ctx->idx.get();
-    double* wts = ctx->wts.get();
-    if (fixed) {
-      idx = ctx->fidx.get() + (size_t)(p - 1) * c;
-      wts = ctx->fw.get() + (size_t)(p - 1) * c;
-    } else {
-      launch_draw(ctx, derive_seed(seed, (uint64_t)p), c, w, idx, wts);
-    }
-    if (want_hist) {
-      CK(cudaMemcpyAsync(ctx->idx_hist.get() + (size_t)(p - 1) * c, idx, c * sizeof(int64_t),
-                         cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(ctx->w_hist.get() + (size_t)(p - 1) * c, wts, c * sizeof(double),
-                         cudaMemcpyDeviceToDevice, st));
-    }
-    if (phases) CK(cudaEventRecord(ctx->pev[2 * (p - 1)], st));
-    SolveOut o;
-    o.phi = ctx->phi.get();
-    o.coefs = ctx->coefs.get();
-    o.coef_off = (int64_t)(p - 1) * p / 2;
-    o.taus = ctx->taus.get();
-    o.method = ctx->method.get();
-    o.lag = p;
-    o.status = ctx->status.get();
-    FwdRows ld{ctx->y.get(), idx, wts, 0};
-    double* Snext = (p & 1) ? ctx->sb.S1.get() : ctx->sb.S0.get();
-    const double* Sprev = (p & 1) ? ctx->sb.S0.get() : ctx->sb.S1.get();
-    solve_rows(ctx, ld, c, p + 1, o, p >= 2 ? Sprev : nullptr, p >= 2 ? ctx->phi.get() : nullptr, Snext);
-    if (phases) CK(cudaEventRecord(ctx->pev[2 * (p - 1) + 1], st));
-    // residuals of the lag-p window fit + score update s_p = s_{p-1} + r_{p-1}^2/R_{p-1}
-    launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());
-    CK(cudaEventRecord(ctx->events[p], st));
+  // per-lag draw seeds live in device memory, so a captured graph of the sweep
+  // replays for any seed
+  ctx->seedtab.need(p_bar + 1);
+  {
+    std::vector<uint64_t> seeds(p_bar + 1);
+    for (int p = 0; p <= p_bar; ++p) seeds[p] = derive_seed(seed, (uint64_t)p);
+    CK(cudaMemcpyAsync(ctx->seedtab.get(), seeds.data(), (p_bar + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // the host vector goes out of scope
   }
-  CK(cudaEventRecord(ctx->ev_end, st));
-  const int64_t launches = g_launches - launches0;
-  if (d && d->rnorm2_out) launch_scan(ctx, ntile, p_bar, 0);  // R_{p_bar} for the diagnostics
+  ctx->sb.M.need((size_t)c * ldq_of(2));  // the p = 1 Gram's dense staging (no allocation inside the loop)
+  const int rn2 = d && d->rnorm2_out;
+  bool capturing = false;
+  // timing events: plain records when eager, external event nodes when captured
+  auto rec = [&](cudaEvent_t e) {
+    if (capturing) CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else CK(cudaEventRecord(e, st));
+  };
+  auto record = [&]() {
+    rec(ctx->ev_begin);
+    rec(ctx->events[0]);
+    // lag-0 pass: r_0 = -y[0..w), s_0 = 0  ->  s_1 = y^2 / sum y^2 (lsar.cpp:11-15)
+    launch_pass(ctx, 0, w, ctx->phi.get(), ctx->scal.get());
+    for (int p = 1; p <= p_bar; ++p) {
+      const int q = p - 1;
+      launch_scan(ctx, ntile, q, 1);
+      int64_t* idx = ctx->idx.get();
+      double* wts = ctx->wts.get();
+      if (fixed) {
+        idx = ctx->fidx.get() + (size_t)(p - 1) * c;
+        wts = ctx->fw.get() + (size_t)(p - 1) * c;
+      } else {
+        launch_draw(ctx, 0, c, w, idx, wts, ctx->seedtab.get() + p);
+      }
+      if (want_hist) {
+        CK(cudaMemcpyAsync(ctx->idx_hist.get() + (size_t)(p - 1) * c, idx, c * sizeof(int64_t),
+                           cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(ctx->w_hist.get() + (size_t)(p - 1) * c, wts, c * sizeof(double),
+                           cudaMemcpyDeviceToDevice, st));
+      }
+      if (phases) rec(ctx->pev[2 * (p - 1)]);
+      SolveOut o;
+      o.phi = ctx->phi.get();
+      o.coefs = ctx->coefs.get();
+      o.coef_off = (int64_t)(p - 1) * p / 2;
+      o.taus = ctx->taus.get();
+      o.method = ctx->method.get();
+      o.lag = p;
+      o.status = ctx->status.get();
+      FwdRows ld{ctx->y.get(), idx, wts, 0};
+      double* Snext = (p & 1) ? ctx->sb.S1.get() : ctx->sb.S0.get();
+      const double* Sprev = (p & 1) ? ctx->sb.S0.get() : ctx->sb.S1.get();
+      solve_rows(ctx, ld, c, p + 1, o, p >= 2 ? Sprev : nullptr, p >= 2 ? ctx->phi.get() : nullptr, Snext);
+      if (phases) rec(ctx->pev[2 * (p - 1) + 1]);
+      // residuals of the lag-p window fit + score update s_p = s_{p-1} + r_{p-1}^2/R_{p-1}
+      launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());
+      rec(ctx->events[p]);
+    }
+    rec(ctx->ev_end);
+    if (rn2) launch_scan(ctx, ntile, p_bar, 0);  // R_{p_bar} for the diagnostics
+  };
+  // The lag loop's launch sequence depends only on (w, c, p_bar, mode) and on
+  // the buffers: the first sweep of a shape runs eagerly, the second is
+  // captured into a CUDA graph, later ones replay it (one launch per sweep).
+  GraphCache& gc = ctx->lsar_graph;
+  const int mode = (fixed ? 1 : 0) | (want_hist ? 2 : 0) | (phases ? 4 : 0) | (rn2 ? 8 : 0);
+  const bool same = gc.w == w && gc.c == c && gc.p_bar == p_bar && gc.mode == mode &&
+                    gc.gen == g_alloc_gen.load();
+  int64_t launches = 0;
+  if (same && gc.exec) {
+    CK(cudaGraphLaunch(gc.exec, st));
+    launches = gc.launches;
+  } else if (same && gc.seen && !ctx->no_graphs) {
+    const int64_t l0 = g_launches;
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    capturing = true;
+    try {
+      record();
+    } catch (...) {
+      capturing = false;
+      cudaStreamEndCapture(st, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    capturing = false;
+    CK(cudaStreamEndCapture(st, &graph));
+    CK(cudaGraphInstantiate(&gc.exec, graph, 0));
+    cudaGraphDestroy(graph);
+    gc.launches = g_launches - l0;
+    launches = gc.launches;
+    CK(cudaGraphLaunch(gc.exec, st));
+  } else {
+    if (gc.exec) {
+      cudaGraphExecDestroy(gc.exec);
+      gc.exec = nullptr;
+    }
+    const int64_t l0 = g_launches;
+    record();
+    launches = g_launches - l0;
+    gc.w = w;
+    gc.c = c;
+    gc.p_bar = p_bar;
+    gc.mode = mode;
+    gc.seen = 1;
+    gc.gen = g_alloc_gen.load();
+  }
   CK(cudaStreamSynchronize(st));
   int sth[3];
   CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
@@ -895,6 +965,7 @@ static void launch_draw_on(tf_context* ctx, const double* scores, int64_t w, uin
   DrawArgs a;
   a.shard = 0;
   a.accept = nullptr;
+  a.seed_ptr = nullptr;
   a.seed = seed;
   a.c = c;
   a.scal = ctx->scal.get();
@@ -1351,6 +1422,7 @@ static int64_t shard_sample(tf_context* ctx, uint64_t seed, double s_total, doub
   a.w = w;
   a.idx = ctx->idx.get();
   a.wts = ctx->wts.get();
+  a.seed_ptr = nullptr;
   a.shard = 1;
   a.s_total = s_total;
   a.offset = offset;
@@ -1620,6 +1692,10 @@ tf_status tf_create(const tf_opts* opts, tf_context** out) {
   if (!ctx) return TF_CUDA;
   ctx->device = dev;
   cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  {
+    const char* v = std::getenv("TF_NO_GRAPHS");  // debugging: launch every sweep eagerly
+    ctx->no_graphs = v && v[0] == '1';
+  }
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
     return TF_CUDA;
@@ -1634,6 +1710,7 @@ void tf_destroy(tf_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (auto e : ctx->events) cudaEventDestroy(e);
   if (ctx->ev_begin) cudaEventDestroy(ctx->ev_begin);
+  if (ctx->lsar_graph.exec) cudaGraphExecDestroy(ctx->lsar_graph.exec);
   if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
   ctx->y.release(); ctx->s.release(); ctx->r.release(); ctx->chunkA.release(); ctx->chunkB.release();
   ctx->tileA.release(); ctx->tileB.release(); ctx->OT.release(); ctx->scal.release();
@@ -1651,7 +1728,7 @@ void tf_destroy(tf_context* ctx) {
   ctx->rh_fup.release(); ctx->rh_scores.release(); ctx->rh_aw.release(); ctx->rh_sw.release();
   ctx->rh_fupw.release(); ctx->rh_ones.release(); ctx->rh_norm.release(); ctx->rh_Gp.release();
   ctx->rh_H0.release(); ctx->rh_W.release(); ctx->rh_S.release(); ctx->rh_phis.release();
-  ctx->rh_rest.release(); ctx->rh_part.release();
+  ctx->rh_rest.release(); ctx->rh_part.release(); ctx->seedtab.release();
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

@@ -26,6 +26,14 @@ struct DBuf {
   T* get() const { return p; }
 };
 
+// captured launch sequence of a sweep shape (see lsar_sweep)
+struct GraphCache {
+  cudaGraphExec_t exec = nullptr;
+  uint64_t gen = 0;
+  int64_t w = 0, c = 0, launches = 0;
+  int p_bar = 0, mode = 0, seen = 0;
+};
+
 struct SolveBufs {
   DBuf<double> W, G, RA, RB, RC, SA, SB, SC, T, S0, S1, Q1, Q2, M, RI;
   DBuf<int> flags;
@@ -59,6 +67,9 @@ struct tf_context {
   tfe::DBuf<double> sh_buf, sh_wts;
   tfe::DBuf<int64_t> sh_idx;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;  // span of the last sweep
+  tfe::GraphCache lsar_graph;
+  tfe::DBuf<uint64_t> seedtab;
+  bool no_graphs = false;
   std::vector<cudaEvent_t> events;
   std::vector<cudaEvent_t> pev;  // phase events (2 per lag)
   int64_t launches = 0;

@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(kScanThreads)
 
 struct DrawArgs {
   uint64_t seed;        // derive_seed(user_seed, p)
+  const uint64_t* seed_ptr;  // nullable: read the seed from device memory (graph replays)
   int64_t c;
   const double* scal;   // R, S
   const double* OT;
@@ -134,7 +135,8 @@ __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
   const int64_t t = (int64_t)blockIdx.x * (kDrawThreads / 32) + wib;
   if (t >= a.c) return;
   const double R = a.scal[0], S = a.scal[1];
-  double v = rng_uniform01(a.seed, (uint64_t)t) * (a.shard ? a.s_total : S);
+  const uint64_t seed = a.seed_ptr ? *a.seed_ptr : a.seed;
+  double v = rng_uniform01(seed, (uint64_t)t) * (a.shard ? a.s_total : S);
   if (a.shard) {
     v -= a.offset;
     const bool mine = v >= 0.0 && (v < S || a.is_last);
