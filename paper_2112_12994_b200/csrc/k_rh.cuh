@@ -409,9 +409,9 @@ constexpr int kHkLd = 68;       // W slice row stride (doubles)
 constexpr int kHkRows = 128;    // rows per block (8 warps: 4 row x 2 column warp tiles)
 constexpr int kHkThreads = 256;
 
-__host__ __device__ inline int hk_kpad(int K) { return (K + 3) & ~3; }
+__host__ __device__ inline int hk_kpad(int K) { return (K + 7) & ~7; }  // k runs in steps of 8
 __host__ inline size_t rowsq_hankel_smem(int K) {
-  return ((size_t)hk_kpad(K) * kHkLd + 2 * (size_t)(kHkRows + hk_kpad(K) + 8)) * sizeof(double);
+  return ((size_t)hk_kpad(K) * kHkLd + 2 * (size_t)(kHkRows + hk_kpad(K) + 48)) * sizeof(double);
 }
 
 // CTAs per column tile are proportional to the tile's DMMA work (narrow last
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kHkThreads)
   extern __shared__ __align__(16) double hk[];
   __shared__ double red[2][kHkRows];
   const int kp = hk_kpad(K);
-  const int seg = kHkRows + kp + 8;
+  const int seg = kHkRows + kp + 48;
   double* Wt = hk;
   double* yb = hk + (size_t)kp * kHkLd;
   int tile = 0;
@@ -471,19 +471,42 @@ __global__ void __launch_bounds__(kHkThreads)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     if (nj > 0) {
+      // Hankel A fragments: row 8 i + r at column k equals row 8 (i + 1) + r at
+      // column k - 8, so two register windows (k = 0 and k = 4 mod 8) advance
+      // with one new shared-memory load each per 8 columns
       const int rbase = 32 * wm + (lane >> 2) + (lane & 3);
-#pragma unroll 4
-      for (int k = 0; k < kend; k += 4) {
-        double af[4], bf[4];
+      double ae[4], ao[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = ys[rbase + 8 * i + k];
+      for (int i = 0; i < 4; ++i) {
+        ae[i] = ys[rbase + 8 * i];
+        ao[i] = ys[rbase + 8 * i + 4];
+      }
+#pragma unroll 2
+      for (int k = 0; k < kend; k += 8) {
+        double bf[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) bf[j] = Wt[(k + (lane & 3)) * kHkLd + 32 * wn + 8 * j + (lane >> 2)];
+        const double ae_n = ys[rbase + k + 32];
+        const double ao_n = ys[rbase + k + 36];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            if (j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            if (j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], ae[i], bf[j]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = Wt[(k + 4 + (lane & 3)) * kHkLd + 32 * wn + 8 * j + (lane >> 2)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], ao[i], bf[j]);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          ae[i] = ae[i + 1];
+          ao[i] = ao[i + 1];
+        }
+        ae[3] = ae_n;
+        ao[3] = ao_n;
       }
     }
     if ((lane & 3) == 0 || true) {
