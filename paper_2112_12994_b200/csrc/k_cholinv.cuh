@@ -703,12 +703,16 @@ __device__ void rd_solve_row(const double* R, int K, double* y, double* tmp) {
   }
 }
 
-// s <- T x (upper TPU)
+// s <- T x (upper TPU): one warp per row, lanes over columns (independent
+// loads in flight instead of a per-thread dependent row loop)
 __device__ void tpu_matvec(const double* T, int K, const double* x, double* s) {
-  for (int r = threadIdx.x; r < K; r += blockDim.x) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = warp; r < K; r += nw) {
     double acc = 0.0;
-    for (int c = r; c < K; ++c) acc = fma(T[tpu_idx(K, r, c)], x[c], acc);
-    s[r] = acc;
+#pragma unroll 4
+    for (int c = r + lane; c < K; c += 32) acc = fma(__ldg(T + tpu_idx(K, r, c)), x[c], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) s[r] = acc;
   }
   __syncthreads();
 }
