@@ -55,11 +55,9 @@ def parse():
     return ap.parse_args()
 
 
-def sweeps_for(cs, have_rh=True):
-    out = [("lsar", c) for c in cs]
-    if have_rh:
-        out += [("rh", c) for c in cs]
-    return out
+def sweeps_for(cs):
+    """The C2 step: LSAR and Repeated Halving side by side at every sample size."""
+    return [("lsar", c) for c in cs] + [("rh", c) for c in cs]
 
 
 # --------------------------------------------------------------------------- clocks
@@ -248,15 +246,7 @@ def run_ours(args):
     eng = tf.Engine(local)
     series = tf.TimeSeries(y)
     eng.upload(series)
-    have_rh = True
-    try:
-        eng.rh_sweep(4, 40, None, 1) if False else None
-        probe = tf.TimeSeries(y[:20000])
-        tf.rh_fit(probe, 4, 40, None, 1, engine=eng)
-    except Exception:
-        have_rh = False
-    eng.upload(series)
-    sweeps = sweeps_for(cs, have_rh)
+    sweeps = sweeps_for(cs)
     ro_sweep = p_bar * (n - p_bar)
     ro_step = ro_sweep * len(sweeps)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")  # 256 MiB > L2
@@ -461,7 +451,7 @@ def run_reference(args):
     from paper_2112_12994_b200 import gen
     y, _, p_bar, cs = gen.make_config_series(args.config, seed=SEED, n=args.n)
     n = y.size
-    sweeps = sweeps_for(cs, True)
+    sweeps = sweeps_for(cs)
     ro_step = p_bar * (n - p_bar) * len(sweeps)
     # each step: the four sweeps are independent fits; the reference is
     # single-threaded, so with all host cores it runs them side by side, one
