@@ -556,6 +556,58 @@ static void check_lsar_args(const tf_context* ctx, int p_bar, int64_t c) {
   if (c < p_bar) throw TfError{TF_USAGE, "sample count below maximum lag"};
 }
 
+// Run a fixed launch sequence through a CUDA graph: the first call for a
+// shape runs eagerly, the second is captured (thread-local capture mode, so
+// concurrent contexts on other host threads are unaffected), later calls
+// replay the instantiated graph.  `capturing` tells the recorder to emit
+// external event nodes for its timing events.  Returns the launch count.
+template <class F>
+static int64_t run_graphed(tf_context* ctx, GraphCache& gc, int64_t w, int64_t c, int p_bar, int mode,
+                           bool& capturing, F&& record) {
+  cudaStream_t st = ctx->stream;
+  const bool same = gc.w == w && gc.c == c && gc.p_bar == p_bar && gc.mode == mode &&
+                    gc.gen == g_alloc_gen.load();
+  if (same && gc.exec) {
+    CK(cudaGraphLaunch(gc.exec, st));
+    g_launches += gc.launches;  // the replayed kernels count like launched ones
+    return gc.launches;
+  }
+  if (same && gc.seen && !ctx->no_graphs) {
+    const int64_t l0 = g_launches;
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    capturing = true;
+    try {
+      record();
+    } catch (...) {
+      capturing = false;
+      cudaStreamEndCapture(st, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    capturing = false;
+    CK(cudaStreamEndCapture(st, &graph));
+    CK(cudaGraphInstantiate(&gc.exec, graph, 0));
+    cudaGraphDestroy(graph);
+    gc.launches = g_launches - l0;
+    CK(cudaGraphLaunch(gc.exec, st));
+    return gc.launches;
+  }
+  if (gc.exec) {
+    cudaGraphExecDestroy(gc.exec);
+    gc.exec = nullptr;
+  }
+  const int64_t l0 = g_launches;
+  record();
+  gc.w = w;
+  gc.c = c;
+  gc.p_bar = p_bar;
+  gc.mode = mode;
+  gc.seen = 1;
+  gc.gen = g_alloc_gen.load();
+  return g_launches - l0;
+}
+
 static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, const tf_lsar_diag* d,
                        double* taus, double* coefs, double* lag_seconds, int* p_star) {
   check_lsar_args(ctx, p_bar, c);
@@ -649,51 +701,9 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
     if (rn2) launch_scan(ctx, ntile, p_bar, 0);  // R_{p_bar} for the diagnostics
   };
   // The lag loop's launch sequence depends only on (w, c, p_bar, mode) and on
-  // the buffers: the first sweep of a shape runs eagerly, the second is
-  // captured into a CUDA graph, later ones replay it (one launch per sweep).
-  GraphCache& gc = ctx->lsar_graph;
+  // the buffers: graph capture/replay (run_graphed).
   const int mode = (fixed ? 1 : 0) | (want_hist ? 2 : 0) | (phases ? 4 : 0) | (rn2 ? 8 : 0);
-  const bool same = gc.w == w && gc.c == c && gc.p_bar == p_bar && gc.mode == mode &&
-                    gc.gen == g_alloc_gen.load();
-  int64_t launches = 0;
-  if (same && gc.exec) {
-    CK(cudaGraphLaunch(gc.exec, st));
-    launches = gc.launches;
-  } else if (same && gc.seen && !ctx->no_graphs) {
-    const int64_t l0 = g_launches;
-    cudaGraph_t graph = nullptr;
-    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    capturing = true;
-    try {
-      record();
-    } catch (...) {
-      capturing = false;
-      cudaStreamEndCapture(st, &graph);
-      if (graph) cudaGraphDestroy(graph);
-      throw;
-    }
-    capturing = false;
-    CK(cudaStreamEndCapture(st, &graph));
-    CK(cudaGraphInstantiate(&gc.exec, graph, 0));
-    cudaGraphDestroy(graph);
-    gc.launches = g_launches - l0;
-    launches = gc.launches;
-    CK(cudaGraphLaunch(gc.exec, st));
-  } else {
-    if (gc.exec) {
-      cudaGraphExecDestroy(gc.exec);
-      gc.exec = nullptr;
-    }
-    const int64_t l0 = g_launches;
-    record();
-    launches = g_launches - l0;
-    gc.w = w;
-    gc.c = c;
-    gc.p_bar = p_bar;
-    gc.mode = mode;
-    gc.seen = 1;
-    gc.gen = g_alloc_gen.load();
-  }
+  const int64_t launches = run_graphed(ctx, ctx->lsar_graph, w, c, p_bar, mode, capturing, record);
   CK(cudaStreamSynchronize(st));
   int sth[3];
   CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
@@ -961,11 +971,11 @@ static void rh_factor(tf_context* ctx, const FwdRows& ld, int64_t rows, int K, d
 }
 
 static void launch_draw_on(tf_context* ctx, const double* scores, int64_t w, uint64_t seed,
-                           int64_t c, int64_t* idx, double* wts) {
+                           int64_t c, int64_t* idx, double* wts, const uint64_t* seed_ptr = nullptr) {
   DrawArgs a;
   a.shard = 0;
   a.accept = nullptr;
-  a.seed_ptr = nullptr;
+  a.seed_ptr = seed_ptr;
   a.seed = seed;
   a.c = c;
   a.scal = ctx->scal.get();
@@ -1240,39 +1250,58 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
     }
     score_distribution(ctx, ctx->rh_scores.get(), m);
   }
-  CK(cudaEventRecord(ctx->events[1], st));
   // ---- per-lag solves from the fixed distribution (repeated_halving.cpp:205-231) ----
-  for (int p = 1; p <= p_bar; ++p) {
-    int64_t* idx = ctx->idx.get();
-    double* wts = ctx->wts.get();
-    if (fixed) {
-      idx = ctx->fidx.get() + (size_t)(p - 1) * c;
-      wts = ctx->fw.get() + (size_t)(p - 1) * c;
-    } else {
-      launch_draw_on(ctx, ctx->rh_scores.get(), m, derive_seed(seed, (uint64_t)p), c, idx, wts);
-    }
-    if (want_hist) {
-      CK(cudaMemcpyAsync(ctx->idx_hist.get() + (size_t)(p - 1) * c, idx, c * sizeof(int64_t),
-                         cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(ctx->w_hist.get() + (size_t)(p - 1) * c, wts, c * sizeof(double),
-                         cudaMemcpyDeviceToDevice, st));
-    }
-    SolveOut o;
-    o.phi = ctx->phi.get();
-    o.coefs = ctx->coefs.get();
-    o.coef_off = (int64_t)(p - 1) * p / 2;
-    o.taus = ctx->taus.get();
-    o.method = ctx->method.get();
-    o.lag = p;
-    o.status = ctx->status.get();
-    RevRows ld{y, idx, wts, p_bar};
-    double* Snext = (p & 1) ? ctx->sb.S1.get() : ctx->sb.S0.get();
-    const double* Sprev = (p & 1) ? ctx->sb.S0.get() : ctx->sb.S1.get();
-    solve_rows(ctx, ld, c, p + 1, o, p >= 2 ? Sprev : nullptr, p >= 2 ? ctx->phi.get() : nullptr, Snext,
-               /*rev=*/1, ctx->rh_rest.get(), ctx->rh_rest.get());
-    CK(cudaEventRecord(ctx->events[p + 1], st));
+  //      (a fixed launch sequence per shape: captured into a CUDA graph and
+  //      replayed, per-lag seeds from a device table)
+  ctx->seedtab.need(p_bar + 1);
+  {
+    std::vector<uint64_t> seeds(p_bar + 1);
+    for (int p = 0; p <= p_bar; ++p) seeds[p] = derive_seed(seed, (uint64_t)p);
+    CK(cudaMemcpyAsync(ctx->seedtab.get(), seeds.data(), (p_bar + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
   }
-  CK(cudaEventRecord(ctx->ev_end, st));
+  ctx->sb.M.need((size_t)c * ldq_of(2));
+  bool capturing = false;
+  auto rec = [&](cudaEvent_t e) {
+    if (capturing) CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else CK(cudaEventRecord(e, st));
+  };
+  auto record_lags = [&]() {
+    rec(ctx->events[1]);
+    for (int p = 1; p <= p_bar; ++p) {
+      int64_t* idx = ctx->idx.get();
+      double* wts = ctx->wts.get();
+      if (fixed) {
+        idx = ctx->fidx.get() + (size_t)(p - 1) * c;
+        wts = ctx->fw.get() + (size_t)(p - 1) * c;
+      } else {
+        launch_draw_on(ctx, ctx->rh_scores.get(), m, 0, c, idx, wts, ctx->seedtab.get() + p);
+      }
+      if (want_hist) {
+        CK(cudaMemcpyAsync(ctx->idx_hist.get() + (size_t)(p - 1) * c, idx, c * sizeof(int64_t),
+                           cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(ctx->w_hist.get() + (size_t)(p - 1) * c, wts, c * sizeof(double),
+                           cudaMemcpyDeviceToDevice, st));
+      }
+      SolveOut o;
+      o.phi = ctx->phi.get();
+      o.coefs = ctx->coefs.get();
+      o.coef_off = (int64_t)(p - 1) * p / 2;
+      o.taus = ctx->taus.get();
+      o.method = ctx->method.get();
+      o.lag = p;
+      o.status = ctx->status.get();
+      RevRows ld{y, idx, wts, p_bar};
+      double* Snext = (p & 1) ? ctx->sb.S1.get() : ctx->sb.S0.get();
+      const double* Sprev = (p & 1) ? ctx->sb.S0.get() : ctx->sb.S1.get();
+      solve_rows(ctx, ld, c, p + 1, o, p >= 2 ? Sprev : nullptr, p >= 2 ? ctx->phi.get() : nullptr, Snext,
+                 /*rev=*/1, ctx->rh_rest.get(), ctx->rh_rest.get());
+      rec(ctx->events[p + 1]);
+    }
+    rec(ctx->ev_end);
+  };
+  const int lag_mode = (fixed ? 1 : 0) | (want_hist ? 2 : 0);
+  run_graphed(ctx, ctx->rh_graph, m, c, p_bar, lag_mode, capturing, record_lags);
   const int64_t launches = g_launches - launches0;
   CK(cudaStreamSynchronize(st));
   int sth[3];
@@ -1711,6 +1740,7 @@ void tf_destroy(tf_context* ctx) {
   for (auto e : ctx->events) cudaEventDestroy(e);
   if (ctx->ev_begin) cudaEventDestroy(ctx->ev_begin);
   if (ctx->lsar_graph.exec) cudaGraphExecDestroy(ctx->lsar_graph.exec);
+  if (ctx->rh_graph.exec) cudaGraphExecDestroy(ctx->rh_graph.exec);
   if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
   ctx->y.release(); ctx->s.release(); ctx->r.release(); ctx->chunkA.release(); ctx->chunkB.release();
   ctx->tileA.release(); ctx->tileB.release(); ctx->OT.release(); ctx->scal.release();

@@ -67,7 +67,7 @@ struct tf_context {
   tfe::DBuf<double> sh_buf, sh_wts;
   tfe::DBuf<int64_t> sh_idx;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;  // span of the last sweep
-  tfe::GraphCache lsar_graph;
+  tfe::GraphCache lsar_graph, rh_graph;
   tfe::DBuf<uint64_t> seedtab;
   bool no_graphs = false;
   std::vector<cudaEvent_t> events;
