@@ -97,6 +97,15 @@ const char* tf_last_error(const tf_context* ctx);
 /* Series resident in HBM for the following sweeps.  Validates non-empty and
  * finite values (DataError, series.cpp:23-32). */
 tf_status tf_upload_series(tf_context* ctx, const double* y, int64_t n);
+/* Synthetic AR series generated on the device into the context (the BASELINE
+ * root-based cascade generator: x_t = x_{t-1} / r_k + in_t per real root r_k,
+ * counter-RNG innovations, innovations 0 = N(0,1), 1 = Student-t(3)/sqrt(3);
+ * the first burn_in samples are dropped).  Replaces host generation +
+ * upload for large configs. */
+tf_status tf_generate_series(tf_context* ctx, const double* roots, int q, int64_t n, uint64_t seed,
+                             int innovations, int64_t burn_in);
+/* Copy the first n values of the resident series to the host. */
+tf_status tf_download_series(tf_context* ctx, double* out, int64_t n);
 /* Same, from a device pointer already in HBM (no host copy). */
 tf_status tf_upload_series_device(tf_context* ctx, const double* d_y, int64_t n);
 

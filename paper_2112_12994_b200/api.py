@@ -263,6 +263,20 @@ class Engine:
             diag["up_w"] = diag["up_w"][:depth.value]
         return taus, coefs, secs, up.value, pstar.value, diag
 
+    def generate_series(self, roots, n: int, seed: int, innovations: str = "normal", burn_in: int = 1000):
+        """Synthetic AR series generated on the device and kept resident (the
+        sweeps then run on it without a host copy)."""
+        r = np.ascontiguousarray(roots, dtype=np.float64)
+        self._check(_abi.lib().tf_generate_series(self._ctx, ptr(r), int(r.size), int(n), C.c_uint64(seed),
+                                                  1 if innovations == "t3" else 0, int(burn_in)))
+        self._series_id = ("device", int(n))
+        return int(n)
+
+    def download_series(self, n: int) -> np.ndarray:
+        out = np.empty(int(n))
+        self._check(_abi.lib().tf_download_series(self._ctx, ptr(out), int(n)))
+        return out
+
     def exact_sweep(self, p_bar: int):
         pb = max(int(p_bar), 1)
         taus = np.zeros(pb)

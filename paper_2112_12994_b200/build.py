@@ -9,7 +9,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["csrc/engine.cu"]
 HEADERS = ["csrc/common.cuh", "csrc/k_pass.cuh", "csrc/k_sample.cuh", "csrc/k_gram.cuh",
-           "csrc/k_cholinv.cuh", "csrc/k_tpu.cuh", "csrc/k_rh.cuh", "csrc/engine.h", "../include/toepfit_b200.h"]
+           "csrc/k_cholinv.cuh", "csrc/k_tpu.cuh", "csrc/k_rh.cuh", "csrc/k_gen.cuh", "csrc/engine.h", "../include/toepfit_b200.h"]
 OUT = os.path.join(HERE, "libtoepfit_b200.so")
 
 

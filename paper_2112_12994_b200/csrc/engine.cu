@@ -16,6 +16,7 @@
 
 #include "engine.h"
 #include "k_cholinv.cuh"
+#include "k_gen.cuh"
 #include "k_gram.cuh"
 #include "k_pass.cuh"
 #include "k_rh.cuh"
@@ -1647,6 +1648,48 @@ static void exact_sweep(tf_context* ctx, int p_bar, double* taus, double* coefs,
   if (p_star) *p_star = tf_select_order(t.data(), p_bar, 1.96 / std::sqrt((double)(n - p_bar)));
 }
 
+// ---------------------------------------------------------------------------
+// On-device synthetic series: cascade of first-order AR
+// sections over counter-RNG innovations, written straight into the context's
+// series buffer (the generator the BASELINE configs describe; bench inputs of
+// C4 size never cross PCIe).
+static void generate_series(tf_context* ctx, const double* roots, int q, int64_t n, uint64_t seed,
+                            int innovations, int64_t burn_in) {
+  if (n < 1 || q < 0 || burn_in < 0) throw TfError{TF_USAGE, "invalid generator arguments"};
+  for (int k = 0; k < q; ++k)
+    if (!(std::fabs(roots[k]) > 1.0)) throw TfError{TF_USAGE, "AR roots must lie outside the unit circle"};
+  cudaStream_t st = ctx->stream;
+  const int64_t total = n + burn_in;
+  DBuf<double> x;
+  x.need(total);
+  k_gen_innovations<<<grid_for(total / 2 + 1, ctx), 256, 0, st>>>(seed, total, innovations == 1 ? 1 : 0, x.get());
+  LAUNCH_CHECK("k_gen_innovations");
+  const int64_t nblk = (total + kGenBlock - 1) / kGenBlock;
+  DBuf<double> bend;
+  bend.need(nblk);
+  for (int k = 0; k < q; ++k) {
+    const double a = 1.0 / roots[k];
+    double aB = 1.0;
+    for (int u = 0; u < kGenBlock; ++u) aB *= a;
+    k_ar_scan_local<<<(unsigned)nblk, kGenThreads, 0, st>>>(x.get(), total, a, bend.get());
+    k_ar_scan_blocks<<<1, 1024, 0, st>>>(bend.get(), nblk, aB);
+    k_ar_scan_apply<<<(unsigned)nblk, kGenThreads, 0, st>>>(x.get(), total, a, bend.get());
+    LAUNCH_CHECK("k_ar_scan");
+  }
+  ctx->y.need(n + 64);
+  CK(cudaMemcpyAsync(ctx->y.get(), x.get() + burn_in, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemsetAsync(ctx->y.get() + n, 0, 64 * sizeof(double), st));
+  CK(cudaStreamSynchronize(st));
+  x.release();
+  bend.release();
+  ctx->n = n;
+}
+
+static void download_series(tf_context* ctx, double* out, int64_t n) {
+  CK(cudaMemcpyAsync(out, ctx->y.get(), n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+}
+
 __global__ void __launch_bounds__(256) k_dfma_probe(double* out, int iters, double seed) {
   double a0 = seed + threadIdx.x, a1 = a0 * 0.5, a2 = a0 * 0.25, a3 = a0 * 0.125;
   double a4 = a0 + 1, a5 = a1 + 1, a6 = a2 + 1, a7 = a3 + 1;
@@ -1838,6 +1881,17 @@ tf_status tf_exact_sweep(tf_context* ctx, int p_bar, double* taus, double* coefs
                          int* p_star) {
   if (!ctx) return TF_USAGE;
   return guarded(ctx, [&] { tfe::exact_sweep(ctx, p_bar, taus, coefs_packed, lag_seconds, p_star); });
+}
+
+tf_status tf_download_series(tf_context* ctx, double* out, int64_t n) {
+  if (!ctx || !out || n < 0 || n > ctx->n) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::download_series(ctx, out, n); });
+}
+
+tf_status tf_generate_series(tf_context* ctx, const double* roots, int q, int64_t n, uint64_t seed,
+                             int innovations, int64_t burn_in) {
+  if (!ctx || (q > 0 && !roots)) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::generate_series(ctx, roots, q, n, seed, innovations, burn_in); });
 }
 
 tf_status tf_sweep_span(const tf_context* ref, const tf_context* ctx, double* start_ms, double* end_ms) {
