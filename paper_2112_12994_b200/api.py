@@ -185,7 +185,13 @@ class Engine:
             keep += [fi, fw]
             d.fixed_idx = ptr(fi, _abi._i64p)
             d.fixed_w = ptr(fw)
-        if want_diag:
+        if want_diag == "light":  # phases / methods / launches only (no per-row dumps)
+            diag = dict(method=np.zeros(pb, np.int32), phases=np.zeros((pb, 3)),
+                        launches=np.zeros(1, np.int64))
+            d.method_out = ptr(diag["method"], _abi._i32p)
+            d.phase_seconds = ptr(diag["phases"])
+            d.launches_out = ptr(diag["launches"], _abi._i64p)
+        elif want_diag:
             w = max(int(n) - pb, 1)
             diag = dict(idx=np.zeros((pb, c), np.int64), w=np.zeros((pb, c)), rnorm2=np.zeros(pb),
                         ssum=np.zeros(pb), scores=np.zeros(w), resid=np.zeros(w),
