@@ -429,6 +429,20 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
   k_phi_solve<<<1, kPhiThreads, (size_t)(2 * K + 32) * sizeof(double), st>>>(ps);
   LAUNCH_CHECK("k_phi_solve");
   COUNT_LAUNCH();
+  // rank-deficient / breakdown systems: the reference's minimum-norm answer
+  // (gated on the shift flag inside the kernel; small systems only)
+  if (c * (int64_t)(K - 1) <= kMinNormCap && K - 1 <= 64 && c <= 4096) {
+    const size_t smem = sizeof(double) * ((size_t)c * (K - 1) + c + 2 * (size_t)(K - 1) * (K - 1));
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+      CK(cudaFuncSetAttribute(k_minnorm<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = smem;
+    }
+    k_minnorm<L><<<1, kMinNormThreads, smem, st>>>(ld, c, K, rev, fl, o.phi, o.coefs, o.coef_off, o.taus,
+                                                   o.method, o.lag, o.status);
+    LAUNCH_CHECK("k_minnorm");
+    COUNT_LAUNCH();
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -116,10 +116,16 @@ struct CITiles {
 template <int I>
 struct F8 {
   static __device__ __forceinline__ void run(double (&d)[8], int lane, bool& bad, int last,
-                                             double floor) {
+                                             double floor, double badfloor) {
     double piv = __shfl_sync(0xffu, d[I], I, 8);
-    if (I == last && !(piv > floor)) piv = floor;  // vanishing residual (c == p)
-    bad |= !(piv > 0.0) || !isfinite(piv);
+    if (I == last) {
+      if (!(piv > floor)) piv = floor;  // vanishing residual (c == p)
+      bad |= !isfinite(piv);
+    } else if (I < last) {
+      // numerically rank deficient: the pivot of a singular Gram is O(eps tr G),
+      // so anything below max(c, K) eps tr(G) is a breakdown (shift / min-norm)
+      bad |= !(piv > badfloor) || !isfinite(piv);
+    }  // I > last: identity padding of the final tile (pivot 1, never checked)
     const double inv = fast_rsqrt(piv);
     if (lane == I) d[I] = piv * inv;
     else if (lane > I) d[I] *= inv;
@@ -128,12 +134,12 @@ struct F8 {
       const double rir = __shfl_sync(0xffu, d[I], r, 8);
       if (lane >= r) d[r] = fma(-rir, d[I], d[r]);
     }
-    F8<I + 1>::run(d, lane, bad, last, floor);
+    F8<I + 1>::run(d, lane, bad, last, floor, badfloor);
   }
 };
 template <>
 struct F8<8> {
-  static __device__ __forceinline__ void run(double (&)[8], int, bool&, int, double) {}
+  static __device__ __forceinline__ void run(double (&)[8], int, bool&, int, double, double) {}
 };
 template <int I>
 struct V8 {  // x = R^-1 in place, rows bottom-up (row I of R dead once row I of X is known)
@@ -169,7 +175,7 @@ __device__ __forceinline__ void mma8(double& c0, double& c1, FA fa, FB fb) {
 // DI: 4 x 64 scratch for the 8 x 8 diagonal inverses, TS: 4 x 64 scratch.
 // On exit S holds Dinv of the (identity-padded) tile.  Returns bad pivot.
 __device__ __forceinline__ bool ci_diag32(double* S, double* DI, double* TS, int last,
-                                          double floor) {
+                                          double floor, double badfloor) {
   const int lane = threadIdx.x & 31;
   const int fr = lane >> 2, fc = 2 * (lane & 3);  // C fragment (row, col pair)
   auto at = [&](int bi, int bj, int r, int c) -> double& { return S[(8 * bj + c) * kTLD + 8 * bi + r]; };
@@ -180,8 +186,9 @@ __device__ __forceinline__ bool ci_diag32(double* S, double* DI, double* TS, int
       double d[8];
 #pragma unroll
       for (int r = 0; r < 8; ++r) d[r] = r <= lane ? at(k, k, r, lane) : 0.0;
-      const int lb = (last >= 8 * k && last < 8 * k + 8) ? last - 8 * k : -1;
-      F8<0>::run(d, lane, bad, lb, floor);
+      // target column index relative to this 8-block; no target in the tile -> +inf
+      const int lb = last >= 0 ? last - 8 * k : (1 << 20);
+      F8<0>::run(d, lane, bad, lb, floor, badfloor);
 #pragma unroll
       for (int r = 0; r < 8; ++r) at(k, k, r, lane) = r <= lane ? d[r] : 0.0;
       V8<7>::run(d, lane);
@@ -257,7 +264,7 @@ __device__ __forceinline__ bool ci_diag32(double* S, double* DI, double* TS, int
 }
 
 // Factor + invert diagonal tile (b, b) (width m) through the scratch S.
-__device__ __forceinline__ bool ci_diag_tile(double* tile, int m, int last, double floor,
+__device__ __forceinline__ bool ci_diag_tile(double* tile, int m, int last, double floor, double badfloor,
                                              double* S, double* DI, double* TS) {
   const int lane = threadIdx.x & 31;
   for (int e = lane; e < 32 * 32; e += 32) {
@@ -265,7 +272,7 @@ __device__ __forceinline__ bool ci_diag_tile(double* tile, int m, int last, doub
     S[c * kTLD + r] = c < m ? (r <= c ? tile[c * kTLD + r] : 0.0) : (r == c ? 1.0 : 0.0);
   }
   __syncwarp();
-  const bool bad = ci_diag32(S, DI, TS, last, floor);
+  const bool bad = ci_diag32(S, DI, TS, last, floor, badfloor);
   for (int e = lane; e < 32 * m; e += 32) {
     const int c = e >> 5, r = e & 31;
     tile[c * kTLD + r] = r <= c ? S[c * kTLD + r] : 0.0;
@@ -338,6 +345,7 @@ __global__ void __maxnreg__(255) k_cholinv(CholinvArgs a) {
     if (attempt > 0)
       for (int i = tid; i < K; i += kCholinvThreads) T.base[tpu_idx(K, i, i)] += shift;
     const double pivot_floor = 4.930380657631324e-32 * tr;  // eps^2 tr(G)
+    const double bad_floor = (double)max(a.nrows, (int64_t)K) * 2.220446049250313e-16 * tr;
     __syncthreads();
     CI_STAMP(1);
     // Iteration b = -1 only factors diagonal tile 0; iteration b applies
@@ -373,7 +381,7 @@ __global__ void __maxnreg__(255) k_cholinv(CholinvArgs a) {
         }
         const int mx = tpu_w(nx, K);
         if (nx == 1) CI_STAMP(60);
-        const bool bad = ci_diag_tile(T.tile(nx, nx), mx, nx == nb - 1 ? mx - 1 : -1, pivot_floor,
+        const bool bad = ci_diag_tile(T.tile(nx, nx), mx, nx == nb - 1 ? mx - 1 : -1, pivot_floor, bad_floor,
                                       s_S, s_DI, s_TS);
         if (nx == 1) CI_STAMP(61);
         if (bad && lane == 0) s_bad = 1;
@@ -904,7 +912,9 @@ __global__ void __launch_bounds__(32) k_bchol_diag(BigChol a, int b) {
   const int K = a.K, nb = (K + 31) / 32;
   const int m = tpu_w(b, K);
   const double floor = 4.930380657631324e-32 * a.tr[0];
-  const bool bad = ci_diag_tile(a.RD + tpu_tile(K, b, b), m, b == nb - 1 ? m - 1 : -1, floor, s_S, s_DI, s_TS);
+  const double badfloor = (double)max(a.nrows, (int64_t)K) * 2.220446049250313e-16 * a.tr[0];
+  const bool bad =
+      ci_diag_tile(a.RD + tpu_tile(K, b, b), m, b == nb - 1 ? m - 1 : -1, floor, badfloor, s_S, s_DI, s_TS);
   if (bad && threadIdx.x == 0) a.work[0] = 1;
 }
 
@@ -984,6 +994,170 @@ __global__ void __launch_bounds__(256) k_bchol_finish(BigChol a) {
     a.flags[0] = shifted;
     a.flags[1] = 0;
     a.flags[2] = (a.force_b || shifted || !(cond_lb <= 8.0 * K)) ? 1 : 0;
+  }
+}
+
+}  // namespace tfk
+
+namespace tfk {
+
+// ---------------------------------------------------------------------------
+// Minimum-norm fallback (toeplitz.cpp:72-83 BDCSVD branch): when pass A had
+// to shift (a breakdown: the sampled system is rank deficient or nearly so),
+// recompute phi as the reference does -- unpivoted Householder QR of the
+// c x p system, one-sided Jacobi SVD of R, singular values kept above
+// max(c, p) eps s_max, x = sum V_i (R_i^T Q^T b) / s_i^2.  One CTA, the system
+// in shared memory (c p <= kMinNormCap); larger degenerate systems keep the
+// shifted CholeskyQR3 result (method 3).
+constexpr int kMinNormCap = 20000;  // doubles of the c x p system held in shared memory
+constexpr int kMinNormThreads = 256;
+
+template <class L>
+__global__ void __launch_bounds__(kMinNormThreads)
+    k_minnorm(L ld, int64_t c, int K, int rev, int* flags, double* phi, double* coefs, int64_t coef_off,
+              double* taus, int* method, int lag, int* status) {
+  if (flags[0] == 0) return;  // pass A factored without a breakdown
+  const int p = K - 1;
+  if (c * (int64_t)p > kMinNormCap || p > 64 || c > 4096) return;
+  extern __shared__ double mn[];
+  const int rows = (int)c;
+  double* M = mn;                     // rows x p, column-major: lag j + 1 in column j
+  double* bvec = M + (size_t)rows * p;  // rows
+  double* R = bvec + rows;            // p x p (column-major)
+  double* V = R + p * p;              // p x p
+  __shared__ double red[kMinNormThreads / 32];
+  __shared__ double s_beta, s_tau;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kMinNormThreads / 32;
+  for (int e = tid; e < rows * p; e += kMinNormThreads) {
+    const int j = e / rows, t = e % rows;
+    M[e] = ld(t, rev ? 1 + j : p - 1 - j);
+  }
+  for (int t = tid; t < rows; t += kMinNormThreads) bvec[t] = ld(t, rev ? 0 : p);
+  __syncthreads();
+  // Householder QR (LAPACK-style reflectors, as the oracle's restatement)
+  const int ksteps = min(rows, p);
+  for (int k = 0; k < ksteps; ++k) {
+    double* xk = M + (size_t)k * rows + k;
+    const int len = rows - k;
+    double part = 0.0;
+    for (int i = 1 + tid; i < len; i += kMinNormThreads) part = fma(xk[i], xk[i], part);
+    part = warp_sum(part);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    if (tid == 0) {
+      double tail = 0.0;
+      for (int w = 0; w < nw; ++w) tail += red[w];
+      const double c0 = xk[0];
+      double tau, beta;
+      if (tail <= 2.2250738585072014e-308) {
+        tau = 0.0;
+        beta = c0;
+      } else {
+        beta = sqrt(c0 * c0 + tail);
+        if (c0 >= 0.0) beta = -beta;
+        tau = (beta - c0) / beta;
+      }
+      s_beta = beta;
+      s_tau = tau;
+    }
+    __syncthreads();
+    const double beta = s_beta, tau = s_tau;
+    const double d = xk[0] - beta;
+    if (tau != 0.0)
+      for (int i = 1 + tid; i < len; i += kMinNormThreads) xk[i] /= d;
+    else
+      for (int i = 1 + tid; i < len; i += kMinNormThreads) xk[i] = 0.0;
+    __syncthreads();
+    if (tid == 0) xk[0] = beta;
+    // apply H = I - tau v v^T (v = [1, xk[1..]]) to columns k+1.. and b: one warp per column
+    for (int j = k + 1 + warp; j <= p; j += nw) {
+      double* cj = j < p ? M + (size_t)j * rows + k : bvec + k;
+      double dot = 0.0;
+      for (int i = 1 + lane; i < len; i += 32) dot = fma(xk[i], cj[i], dot);
+      dot = warp_sum(dot) + cj[0];
+      const double f = tau * dot;
+      if (lane == 0) cj[0] -= f;
+      for (int i = 1 + lane; i < len; i += 32) cj[i] = fma(-f, xk[i], cj[i]);
+    }
+    __syncthreads();
+  }
+  // R (upper, p x p; rows >= p here since c >= p_bar >= p) and V = I
+  for (int e = tid; e < p * p; e += kMinNormThreads) {
+    const int j = e / p, i = e % p;
+    R[e] = i <= j ? M[(size_t)j * rows + i] : 0.0;
+    V[e] = i == j ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  // one-sided Jacobi on the columns of R, cyclic pair order, one warp (the
+  // degenerate path is rare; p <= 64)
+  const double eps = 2.220446049250313e-16;
+  if (warp == 0) {
+    for (int sweep = 0; sweep < 60; ++sweep) {
+      bool rotated = false;
+      for (int i = 0; i < p - 1; ++i) {
+        for (int j = i + 1; j < p; ++j) {
+          double a = 0.0, b = 0.0, g = 0.0;
+          for (int r = lane; r < p; r += 32) {
+            const double ri = R[i * p + r], rj = R[j * p + r];
+            a = fma(ri, ri, a);
+            b = fma(rj, rj, b);
+            g = fma(ri, rj, g);
+          }
+          a = warp_sum(a);
+          b = warp_sum(b);
+          g = warp_sum(g);
+          if (g != 0.0 && fabs(g) > eps * sqrt(a * b)) {
+            const double zeta = (b - a) / (2.0 * g);
+            const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+            for (int r = lane; r < p; r += 32) {
+              const double ri = R[i * p + r], rj = R[j * p + r];
+              R[i * p + r] = cs * ri - sn * rj;
+              R[j * p + r] = sn * ri + cs * rj;
+              const double vi = V[i * p + r], vj = V[j * p + r];
+              V[i * p + r] = cs * vi - sn * vj;
+              V[j * p + r] = sn * vi + cs * vj;
+            }
+            rotated = true;
+          }
+          __syncwarp();
+        }
+      }
+      if (!rotated) break;
+    }
+  }
+  __syncthreads();
+  // x = sum_i V_i (R_i^T qb) / s_i^2 over s_i >= s_max max(c, p) eps
+  double* qb = bvec;  // Q^T b: first p entries
+  __shared__ double sv[64], coef[64];
+  if (tid < p) {
+    double s2 = 0.0, dq = 0.0;
+    for (int r = 0; r < p; ++r) {
+      s2 = fma(R[tid * p + r], R[tid * p + r], s2);
+      dq = fma(R[tid * p + r], qb[r], dq);
+    }
+    sv[tid] = sqrt(s2);
+    coef[tid] = s2 > 0.0 ? dq / s2 : 0.0;
+  }
+  __syncthreads();
+  double smax = 0.0;
+  for (int i = 0; i < p; ++i) smax = fmax(smax, sv[i]);
+  double pre = smax * (double)max((int64_t)p, c) * eps;
+  if (pre < 2.2250738585072014e-308) pre = 2.2250738585072014e-308;
+  if (tid < p) {
+    double x = 0.0;
+    for (int i = 0; i < p; ++i)
+      if (sv[i] >= pre) x = fma(coef[i], V[i * p + tid], x);
+    phi[tid] = x;
+    if (coefs) coefs[coef_off + tid] = x;
+    if (taus && tid == p - 1) taus[lag - 1] = x;
+  }
+  if (tid == 0) {
+    if (method) method[lag - 1] = 4;  // minimum-norm SVD path
+    // a pass B / C breakdown of this lag is answered by the minimum-norm solve
+    if (flags[1] != 0 && status[0] == kErrNumerical && status[1] == lag && status[2] == kReasonCholFail)
+      status[0] = 0;
+    flags[1] = 0;
   }
 }
 

@@ -266,3 +266,37 @@ def test_lsar_c2_full_size_properties(orc, tf, eng):
         assert relerr(d["resid"][i0:i0 + 5000], r) < TOL
     assert relerr(d["rnorm2"][-1], float(np.dot(d["resid"], d["resid"]))) < 1e-10
     assert (d["idx"] >= 0).all() and (d["idx"] < w).all()
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("n,p_bar,c", [(5, 1, 3), (6, 2, 2), (40, 1, 500), (300, 12, 12), (2050, 3, 4000)])
+def test_lsar_edge_shapes_match_oracle(orc, tf, eng, n, p_bar, c):
+    # smallest windows, p_bar = 1, c = p_bar, c larger than the window (draws
+    # repeat rows), a window that ends one row past a 2048-row tile
+    y = orc.simulate_ar(orc.random_stationary_ar(2, n + p_bar), n, 7 + n)
+    ref = orc.lsar_fit(y, p_bar, c, 5)
+    fit = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, 5, engine=eng, fixed_idx=ref.idx, fixed_w=ref.w)
+    assert relerr(fit.pacf.taus, ref.taus) < 1e-8
+    assert fit.p_star == ref.p_star
+
+
+def test_rh_edge_shapes_match_oracle(orc, tf, eng):
+    for n, p_bar, c in [(30, 1, 5), (500, 2, 40), (5000, 1, 200)]:
+        y = orc.simulate_ar(orc.random_stationary_ar(2, n), n, 3 + n)
+        ref = orc.rh_fit(y, p_bar, c, 9, want_levels=True)
+        flat = np.concatenate(ref.levels) if ref.levels else np.zeros(0, np.int64)
+        fit = tf.rh_fit(tf.TimeSeries(y), p_bar, c, None, 9, engine=eng, want_diag=True,
+                        fixed=dict(idx=ref.idx, w=ref.w, levels=flat, up_idx=ref.up_idx, up_w=ref.up_w))
+        assert relerr(fit.pacf.taus, ref.taus) < 1e-8
+        assert relerr(fit.diag["scores"], ref.scores) < 1e-8
+
+
+def test_exact_edge_and_errors(orc, tf, eng):
+    y = orc.simulate_ar(orc.random_stationary_ar(2, 1), 50, 11)
+    ref = orc.exact_fit(y, 1)
+    fit = tf.exact_fit(tf.TimeSeries(y), 1, engine=eng)
+    assert relerr(fit.pacf.taus, ref.taus) < 1e-9
+    with pytest.raises(tf.DataError):
+        tf.exact_fit(tf.TimeSeries(y[:3]), 2, engine=eng)
+    with pytest.raises(tf.UsageError):
+        tf.exact_fit(tf.TimeSeries(y), 0, engine=eng)
