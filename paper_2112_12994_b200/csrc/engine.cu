@@ -451,7 +451,7 @@ constexpr int kPassMmaMinQ = 16;  // tensor-core FIR from this lag on (sweep pas
 
 static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev,
                         bool exact_order = false) {
-  PassArgs a;
+  PassArgs a{};
   a.y = ctx->y.get();
   a.w = w;
   a.q = q;
@@ -463,16 +463,17 @@ static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, co
   a.chunkB = ctx->chunkB.get();
   a.tileA = ctx->tileA.get();
   a.tileB = ctx->tileB.get();
+  a.ylen = ctx->n + 64;
   const int64_t ntile = (w + kPassTile - 1) / kPassTile;
   if (!exact_order && q >= kPassMmaMinQ) {
-    const size_t smem = pass_mma_smem_bytes(q);
+    const size_t smem = PassTmaLayout(q).bytes();
     static size_t attr = 0;
     if (smem > attr) {
-      CK(cudaFuncSetAttribute(k_lsar_pass_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CK(cudaFuncSetAttribute(k_lsar_pass_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr = smem;
     }
-    k_lsar_pass_mma<<<(unsigned)ntile, kPassThreads, smem, ctx->stream>>>(a);
-    LAUNCH_CHECK("k_lsar_pass_mma");
+    k_lsar_pass_tma<<<(unsigned)ntile, kPassThreads, smem, ctx->stream>>>(a);
+    LAUNCH_CHECK("k_lsar_pass_tma");
     COUNT_LAUNCH();
     return;
   }

@@ -5,14 +5,16 @@
 //   r_q(i) = -y[q+i] + sum_{j=0}^{q-1} phi_q[j] * y[q-1-j+i]
 //            (toeplitz.cpp:87-98: tap order j = 0..q-1 starting from -y, one
 //             fma per tap -- bit-identical to the oracle's residuals())
-//   per 32-row chunk:  A_c = sum s_q,  B_c = sum r_q^2   (fixed-order warp tree)
-//   per 2048-row tile: A_t, B_t (fixed-order sum of its chunks)
+//   per 32-row chunk:  A_c = sum s_q,  B_c = sum r_q^2   (fixed order)
+//   per 2048-row tile: A_t, B_t (fixed-order tree of its chunks)
 // The lag-q design matrix is never stored: each CTA stages the 2048 + q
 // series values its rows touch (q-sample halo) in shared memory.
 //
-// Layout: y tile in smem with one pad double every 16 (skew) so that the
-// register-blocked FIR (16 consecutive outputs per thread, 23-value sliding
-// window per 8 taps) reads are bank-conflict free.
+// k_lsar_pass (q < 16, and tf_residuals at any q): CUDA-core FIR in the
+// reference's tap order; y tile in smem with one pad double every 16 (skew)
+// so that the register-blocked FIR (16 consecutive outputs per thread,
+// 23-value sliding window per 8 taps) reads are bank-conflict free.
+// k_lsar_pass_tma (q >= 16): tensor-core FIR + TMA bulk loads (below).
 #pragma once
 
 #include "common.cuh"
@@ -59,7 +61,19 @@ struct PassArgs {
   double* chunkB;
   double* tileA;
   double* tileB;
+  int dbg;           // development switches (tools/pass_bench.cu): bit 2 skips the FIR, bit 3 the state traffic
+  int64_t ylen;      // readable doubles at y (series + zero pad)
+  unsigned long long* stamps;  // development: per-CTA phase timestamps (nullptr in the product)
 };
+
+#define STAMP(i)                                                                        \
+  do {                                                                                  \
+    if (a.stamps && threadIdx.x == 0) {                                                 \
+      unsigned long long t_;                                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+      a.stamps[8 * (size_t)blockIdx.x + (i)] = t_;                                      \
+    }                                                                                   \
+  } while (0)
 
 inline size_t pass_smem_bytes(int q) {
   const int phi_n = ((q + 1) & ~1) + 2;
@@ -67,6 +81,48 @@ inline size_t pass_smem_bytes(int q) {
   const int ys_sk = ys_n + (ys_n >> 4) + 2;
   const int rn_sk = kPassTile + (kPassTile >> 4) + 2;
   return sizeof(double) * (size_t)(phi_n + ys_sk + rn_sk);
+}
+
+// chunk (32 rows) and tile partial sums of s_q and r_q^2 from the tile's s_q, r_q
+// in shared memory (r_q optionally in the skew16 layout): one thread per chunk, sequential over its rows from a
+// rotated start (the rotation makes the strided reads conflict free); the
+// tile sums are a fixed tree over the 64 chunk sums.  Deterministic; no
+// per-row warp reductions.
+template <bool RSKEW>
+__device__ __forceinline__ void pass_partials(const PassArgs& a, const double* ss, const double* rs, int rows,
+                                              int64_t i0, int64_t tile) {
+  __shared__ double red[2][kChunksPerTile];
+  const int tid = threadIdx.x;
+  if (tid < kChunksPerTile) {
+    const int c0 = kChunk * tid;
+    const int nr = min(kChunk, rows - c0);
+    double A = 0.0, B = 0.0;
+#pragma unroll 8
+    for (int k = 0; k < kChunk; ++k) {
+      const int j = (k + tid) & (kChunk - 1);
+      if (j < nr) {
+        const double rv = rs[RSKEW ? skew16(c0 + j) : c0 + j];
+        A += ss[c0 + j];
+        B = fma(rv, rv, B);
+      }
+    }
+    if (nr > 0) {
+      const int64_t cidx = i0 / kChunk + tid;
+      a.chunkA[cidx] = A;
+      a.chunkB[cidx] = B;
+    }
+    red[0][tid] = A;
+    red[1][tid] = B;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const double TA = warp_sum(red[0][tid] + red[0][tid + 32]);
+    const double TB = warp_sum(red[1][tid] + red[1][tid + 32]);
+    if (tid == 0) {
+      a.tileA[tile] = TA;
+      a.tileB[tile] = TB;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass(PassArgs a) {
@@ -119,7 +175,7 @@ __global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass(PassArgs a) {
   for (int u = 0; u < kPassR; ++u) rn[skew16(ob + u)] = acc[u];
   __syncthreads();
 
-  // ---- update + chunk partials (coalesced: warp covers one 32-row chunk per u) ----
+  // ---- update (coalesced), then chunk / tile partials from shared memory ----
   // previous state loaded only now: keeps the FIR's register footprint small
   // (more resident CTAs hide this latency)
   double so[kPassR], ro[kPassR];
@@ -134,173 +190,183 @@ __global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass(PassArgs a) {
     }
   }
   const double Rp = q > 0 ? *a.Rprev : 1.0;
-  const int warp = tid >> 5, lane = tid & 31;
-  double tA = 0.0, tB = 0.0;
+  double* snew_s = ys;  // series tile is dead after the FIR barrier
 #pragma unroll
   for (int u = 0; u < kPassR; ++u) {
     const int row = tid + kPassThreads * u;
-    double snew = 0.0, rnew = 0.0;
     if (row < rows) {
-      rnew = rn[skew16(row)];
-      snew = q > 0 ? so[u] + (ro[u] * ro[u]) / Rp : 0.0;
+      const double rnew = rn[skew16(row)];
+      const double snew = q > 0 ? so[u] + (ro[u] * ro[u]) / Rp : 0.0;
       a.s[i0 + row] = snew;
       a.r[i0 + row] = rnew;
+      snew_s[row] = snew;
     }
-    const double cA = warp_sum(snew);
-    const double cB = warp_sum(rnew * rnew);
-    const int crow = kPassThreads * u + kChunk * warp;  // chunk's first row in tile
-    if (lane == 0 && crow < rows) {
-      const int64_t cidx = (i0 + crow) / kChunk;
-      a.chunkA[cidx] = cA;
-      a.chunkB[cidx] = cB;
-    }
-    tA += cA;
-    tB += cB;
-  }
-  __shared__ double wA[kPassThreads / 32], wB[kPassThreads / 32];
-  if (lane == 0) {
-    wA[warp] = tA;
-    wB[warp] = tB;
   }
   __syncthreads();
-  if (tid == 0) {
-    a.tileA[blockIdx.x] = ((wA[0] + wA[1]) + wA[2]) + wA[3];
-    a.tileB[blockIdx.x] = ((wB[0] + wB[1]) + wB[2]) + wB[3];
-  }
+  pass_partials<true>(a, snew_s, rn, rows, i0, blockIdx.x);
 }
-
 
 // ---------------------------------------------------------------------------
-// Tensor-core variant of the fused pass for larger lags (fp64 DMMA m8n8k4).
-// The FIR over a tile is a polyphase GEMM: with rows i = 8a + b,
+// k_lsar_pass_tma: the pass for q >= 16, FIR on the fp64 tensor cores (DMMA
+// m8n8k4) with every load asynchronous.
+//
+// FIR as a polyphase GEMM: with tile rows i = 8a + b,
 //   r[8a + b] = sum_k Y[a][k] Phi[k][b],   Y[a][k] = y[i0 + 8a + k]  (Hankel, stride 8)
-//   Phi[k][b] = phi[q-1+b-k] for 0 <= q-1+b-k < q,  -1 for k = q + b  (the target),  0 else
+//   Phi[k][b] = phi[q-1+b-k] for 0 <= q-1+b-k < q,  -1 for k = q + b (the target),  0 else
 // so M = 256 (a), N = 8 (b), K = q + 8 per 2048-row tile; every warp owns 8
-// m8 tiles (64 a-rows = 512 outputs), tile u holding a-rows 8 g + u.  Then the
-// A fragment of tile u at k-step s equals that of tile u + 1 at step s - 2, so
-// the 8 tiles walk one shared register window (one new fragment per step).  The y tile
-// uses a padded layout (x + 4 floor(x / 64): lanes 8 g + t read x = 64 g + t)
-// that makes the fragment reads bank-conflict free; Phi fragments are tabulated once per CTA.
-// Summation order differs from the reference's tap loop (rounding ~1e-16);
-// the exact-order FMA kernel above serves tf_residuals and small lags.
+// m8 tiles (64 a-rows = 512 outputs), tile u holding a-rows 8 g + u.  The A
+// fragment of tile u at k-step s equals that of tile u + 1 at step s - 2, so
+// the 8 tiles walk one shared register window (one new fragment per step).
+// The series tile uses the skew12 layout (x + 4 floor(x / 64): lanes 8 g + t
+// read x = 64 g + t), which makes the fragment reads bank-conflict free; the
+// B fragments come from a compact table phiP[j + kPhiOff] (11 distinct
+// addresses per warp load, broadcast).  Summation order differs from the
+// reference's tap loop (rounding ~1e-16); k_lsar_pass keeps the exact order.
+//
+// Memory: at CTA entry one warp issues TMA bulk copies (cp.async.bulk +
+// mbarrier) of the series tile (64-double segments into the skew12 layout)
+// and of the tile's previous state s_{q-1}, r_{q-1}; the FIR waits only for
+// the series and the state lands while it runs.  r_q goes to a skew16 buffer
+// aliasing the dead series tile; the update and the chunk partials then run
+// out of shared memory (pass_partials), with coalesced stores of s_q, r_q.
 __host__ __device__ __forceinline__ int skew12(int x) { return x + 4 * (x >> 6); }
 
-inline int pass_mma_kd(int q) { return (q + 8 + 3) & ~3; }
-inline size_t pass_mma_smem_bytes(int q) {
-  const int kd = pass_mma_kd(q);
-  const int ys_n = kPassTile + kd + 8;
-  const int ys_sk = skew12(ys_n) + 8;
-  const int rn_sk = kPassTile + (kPassTile >> 4) + 2;
-  return sizeof(double) * (size_t)(kd * 8 + ys_sk + rn_sk);
-}
-
-__global__ void __launch_bounds__(kPassThreads, 5) k_lsar_pass_mma(PassArgs a) {
-  extern __shared__ double sm[];
-  const int q = a.q;
-  const int kd = (q + 8 + 3) & ~3;
-  const int ys_n = kPassTile + kd + 8;
-  double* phiF = sm;                       // [kd / 4][32]: B fragment of k-step s for each lane
-  double* ys = sm + kd * 8;
-  double* rn = ys + skew12(ys_n) + 8;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t i0 = (int64_t)blockIdx.x * kPassTile;
-  const int rows = (int)min((int64_t)kPassTile, a.w - i0);
-  const int need = rows + q;
-  stage_y<kPassThreads>(ys, a.y + i0, ys_n, need, [](int x) { return skew12(x); });
-  for (int e = tid; e < kd * 8; e += kPassThreads) {
-    const int sstep = e >> 5, ln = e & 31;
-    const int k = 4 * sstep + (ln & 3), b = ln >> 2;
-    const int j = q - 1 + b - k;
-    phiF[e] = (j >= 0 && j < q) ? __ldg(a.phi + j) : (k == q + b ? -1.0 : 0.0);
+struct PassTmaLayout {
+  int kd, ys_n, ys_sk, phi_n;
+  __host__ __device__ explicit PassTmaLayout(int q)
+      : kd((q + 8 + 3) & ~3), ys_n(kPassTile + ((q + 8 + 3) & ~3) + 8) {
+    const int rn_sk = kPassTile + (kPassTile >> 4) + 2;
+    ys_sk = max(skew12(ys_n) + 8, rn_sk);
+    ys_sk = (ys_sk + 1) & ~1;
+    phi_n = (q + 25) & ~1;
   }
-  __syncthreads();
-  // ---- FIR on DMMA: warp tiles a in [64 warp, 64 warp + 64) ----
+  // doubles: [2 mbarriers][s: 2048][r: 2048][ys / rn: ys_sk][phi: phi_n]
+  __host__ __device__ size_t bytes() const { return sizeof(double) * (size_t)(2 + 2 * kPassTile + ys_sk + phi_n); }
+};
+constexpr int kPhiOff = 16;
+
+// DMMA FIR of one 2048-row tile (the polyphase GEMM above):
+// ys = series tile (skew12), pb = phiP + kPhiOff + q - 1 + g - t, result r_q
+// written to rn (skew16) AFTER a barrier (rn may alias ys)
+__device__ __forceinline__ void pass_fir_dmma(const double* ys, const double* pb, int nsteps, double* rn) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int abase = 64 * warp;
   double c0[8], c1[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) c0[u] = c1[u] = 0.0;
-  // m8 tile u holds a-rows abase + 8 g + u (g = lane / 4), so its A fragment at
-  // k-step s is f[s + 2u] with f[m] = Y[abase + 8 g][4 m + t]
   const int xbase = 8 * (abase + 8 * g) + t;
-  double fe[8], fo[8];  // windows for even / odd steps: fe[u] = f[s + 2u] (s even)
+  double fe[8], fo[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    fe[u] = ys[skew12(xbase + 8 * u)];      // f[2u]     (step 0)
-    fo[u] = ys[skew12(xbase + 8 * u + 4)];  // f[2u + 1] (step 1)
+    fe[u] = ys[skew12(xbase + 8 * u)];
+    fo[u] = ys[skew12(xbase + 8 * u + 4)];
   }
-  const int nsteps = kd >> 2;
   for (int sstep = 0; sstep < nsteps; sstep += 2) {
-    const double be = phiF[sstep * 32 + lane];
+    const double be = pb[-4 * sstep];
 #pragma unroll
     for (int u = 0; u < 8; ++u) dmma_8x8x4(c0[u], c1[u], fe[u], be);
     if (sstep + 1 < nsteps) {
-      const double bo = phiF[(sstep + 1) * 32 + lane];
+      const double bo = pb[-4 * sstep - 4];
 #pragma unroll
       for (int u = 0; u < 8; ++u) dmma_8x8x4(c0[u], c1[u], fo[u], bo);
     }
-    // advance both windows by one tile: f[s + 2 + 2u] = old window[u + 1]
 #pragma unroll
     for (int u = 0; u < 7; ++u) {
       fe[u] = fe[u + 1];
       fo[u] = fo[u + 1];
     }
-    const int xn = xbase + 8 * 8 + 8 * (sstep >> 1);  // f[sstep + 2 + 14] = Y[.][4 (sstep + 16) + t]
+    const int xn = xbase + 8 * 8 + 8 * (sstep >> 1);
     fe[7] = ys[skew12(xn)];
     fo[7] = ys[skew12(xn + 4)];
   }
+  __syncthreads();  // series tile dead: r_q may go to its space
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
     const int r = 8 * (abase + 8 * g + u) + 2 * t;
     rn[skew16(r)] = c0[u];
     rn[skew16(r + 1)] = c1[u];
   }
+}
+
+__global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass_tma(PassArgs a) {
+  extern __shared__ __align__(128) double sm[];
+  const int q = a.q;
+  const PassTmaLayout L(q);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
+  double* ss = sm + 2;
+  double* rr = ss + kPassTile;
+  double* ys = rr + kPassTile;
+  double* rn = ys;  // after the FIR
+  double* phiP = ys + L.ys_sk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = (int64_t)blockIdx.x * kPassTile;
+  const int rows = (int)min((int64_t)kPassTile, a.w - i0);
+  // series values readable from y + i0 (the buffer carries a zero pad), even count
+  const int ycopy = (int)min((int64_t)L.ys_n, a.ylen - i0) & ~1;
+  const int rcopy = (a.dbg & 8) ? 0 : rows & ~1;
+  STAMP(0);
+  const double invR = 1.0 / *a.Rprev;  // issued early: off the post-FIR critical path
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      mbar_expect_tx(&bars[0], (uint32_t)ycopy * 8u);
+      mbar_expect_tx(&bars[1], (uint32_t)rcopy * 16u);
+    }
+    __syncwarp();
+    const int nseg = (ycopy + 63) >> 6;
+    for (int k = lane; k < nseg; k += 32) {
+      const int len = min(64, ycopy - 64 * k);
+      bulk_g2s(ys + skew12(64 * k), a.y + i0 + 64 * k, (uint32_t)len * 8u, &bars[0]);
+    }
+    if (lane == 0 && rcopy > 0) {
+      bulk_g2s(ss, a.s + i0, (uint32_t)rcopy * 8u, &bars[1]);
+      bulk_g2s(rr, a.r + i0, (uint32_t)rcopy * 8u, &bars[1]);
+    }
+  }
+  // generic-proxy fills of what the copies do not cover (disjoint addresses)
+  for (int x = ycopy + tid; x < L.ys_n; x += kPassThreads) ys[skew12(x)] = 0.0;
+  if (tid == 0 && rows > rcopy && !(a.dbg & 8)) {
+    ss[rcopy] = a.s[i0 + rcopy];
+    rr[rcopy] = a.r[i0 + rcopy];
+  }
+  for (int m = tid; m < L.phi_n; m += kPassThreads) {
+    const int j = m - kPhiOff;
+    phiP[m] = (j >= 0 && j < q) ? __ldg(a.phi + j) : (j == -1 ? -1.0 : 0.0);
+  }
   __syncthreads();
-  // ---- update + chunk partials (identical to k_lsar_pass) ----
-  double so[kPassR], ro[kPassR];
-#pragma unroll
+  STAMP(1);
+  mbar_wait(&bars[0], 0);
+  STAMP(2);
+  // ---- FIR on DMMA (B fragment from the compact table) ----
+  // B(s, lane) = Phi[k = 4 s + t][b = g] = tap j = q - 1 + g - 4 s - t
+  const double* pb = phiP + kPhiOff + q - 1 + (lane >> 2) - (lane & 3);
+  pass_fir_dmma(ys, pb, (a.dbg & 4) ? 0 : L.kd >> 2, rn);
+  STAMP(3);
+  __syncthreads();
+  mbar_wait(&bars[1], 0);
+  STAMP(4);
+  // ---- update: coalesced over rows, new state stored from registers ----
+#pragma unroll 4
   for (int u = 0; u < kPassR; ++u) {
     const int row = tid + kPassThreads * u;
-    so[u] = 0.0;
-    ro[u] = 0.0;
     if (row < rows) {
-      so[u] = a.s[i0 + row];
-      ro[u] = a.r[i0 + row];
+      const double rnew = rn[skew16(row)];
+      const double ro = rr[row];
+      const double snew = fma(ro * ro, invR, ss[row]);
+      if (!(a.dbg & 8)) {
+        a.s[i0 + row] = snew;
+        a.r[i0 + row] = rnew;
+      }
+      ss[row] = snew;
+      rr[row] = rnew;
     }
-  }
-  const double Rp = *a.Rprev;
-  double tA = 0.0, tB = 0.0;
-#pragma unroll
-  for (int u = 0; u < kPassR; ++u) {
-    const int row = tid + kPassThreads * u;
-    double snew = 0.0, rnew = 0.0;
-    if (row < rows) {
-      rnew = rn[skew16(row)];
-      snew = so[u] + (ro[u] * ro[u]) / Rp;
-      a.s[i0 + row] = snew;
-      a.r[i0 + row] = rnew;
-    }
-    const double cA = warp_sum(snew);
-    const double cB = warp_sum(rnew * rnew);
-    const int crow = kPassThreads * u + kChunk * warp;
-    if (lane == 0 && crow < rows) {
-      const int64_t cidx = (i0 + crow) / kChunk;
-      a.chunkA[cidx] = cA;
-      a.chunkB[cidx] = cB;
-    }
-    tA += cA;
-    tB += cB;
-  }
-  __shared__ double wA[kPassThreads / 32], wB[kPassThreads / 32];
-  if (lane == 0) {
-    wA[warp] = tA;
-    wB[warp] = tB;
   }
   __syncthreads();
-  if (tid == 0) {
-    a.tileA[blockIdx.x] = ((wA[0] + wA[1]) + wA[2]) + wA[3];
-    a.tileB[blockIdx.x] = ((wB[0] + wB[1]) + wB[2]) + wB[3];
-  }
+  STAMP(5);
+  pass_partials<false>(a, ss, rr, rows, i0, blockIdx.x);
+  STAMP(6);
 }
 
 }  // namespace tfk
