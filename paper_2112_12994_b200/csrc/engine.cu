@@ -13,6 +13,8 @@
 #include <new>
 #include <string>
 #include <vector>
+#include <mutex>
+#include <map>
 
 #include "engine.h"
 #include "k_cholinv.cuh"
@@ -447,7 +449,7 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
 
 // ---------------------------------------------------------------------------
 
-constexpr int kPassMmaMinQ = 16;  // tensor-core FIR from this lag on (sweep passes)
+constexpr int kPassPstMinQ = 1;  // sweeps: tensor-core persistent pass for every lag q >= 1
 
 static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev,
                         bool exact_order = false) {
@@ -465,15 +467,29 @@ static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, co
   a.tileB = ctx->tileB.get();
   a.ylen = ctx->n + 64;
   const int64_t ntile = (w + kPassTile - 1) / kPassTile;
-  if (!exact_order && q >= kPassMmaMinQ) {
-    const size_t smem = PassTmaLayout(q).bytes();
+  if (!exact_order && q >= kPassPstMinQ) {
+    const size_t smem = PassLayout(q).bytes();
+    static std::mutex mu;  // contexts launch from several host threads
     static size_t attr = 0;
-    if (smem > attr) {
-      CK(cudaFuncSetAttribute(k_lsar_pass_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
+    static std::map<size_t, int> occ_of;
+    int occ;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (smem > attr) {
+        CK(cudaFuncSetAttribute(k_lsar_pass_pst, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = smem;
+      }
+      auto it = occ_of.find(smem);
+      if (it == occ_of.end()) {
+        int o = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_lsar_pass_pst, kPassThreads, smem));
+        it = occ_of.emplace(smem, o).first;
+      }
+      occ = it->second;
     }
-    k_lsar_pass_tma<<<(unsigned)ntile, kPassThreads, smem, ctx->stream>>>(a);
-    LAUNCH_CHECK("k_lsar_pass_tma");
+    const int64_t grid = std::min<int64_t>(ntile, (int64_t)std::max(occ, 1) * ctx->sm_count);
+    k_lsar_pass_pst<<<(unsigned)grid, kPassThreads, smem, ctx->stream>>>(a);
+    LAUNCH_CHECK("k_lsar_pass_pst");
     COUNT_LAUNCH();
     return;
   }

@@ -14,7 +14,8 @@
 // reference's tap order; y tile in smem with one pad double every 16 (skew)
 // so that the register-blocked FIR (16 consecutive outputs per thread,
 // 23-value sliding window per 8 taps) reads are bank-conflict free.
-// k_lsar_pass_tma (q >= 16): tensor-core FIR + TMA bulk loads (below).
+// k_lsar_pass_pst (q >= 1 in the sweeps): tensor-core FIR, TMA bulk loads,
+// persistent CTAs (below).
 #pragma once
 
 #include "common.cuh"
@@ -63,17 +64,8 @@ struct PassArgs {
   double* tileB;
   int dbg;           // development switches (tools/pass_bench.cu): bit 2 skips the FIR, bit 3 the state traffic
   int64_t ylen;      // readable doubles at y (series + zero pad)
-  unsigned long long* stamps;  // development: per-CTA phase timestamps (nullptr in the product)
 };
 
-#define STAMP(i)                                                                        \
-  do {                                                                                  \
-    if (a.stamps && threadIdx.x == 0) {                                                 \
-      unsigned long long t_;                                                            \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
-      a.stamps[8 * (size_t)blockIdx.x + (i)] = t_;                                      \
-    }                                                                                   \
-  } while (0)
 
 inline size_t pass_smem_bytes(int q) {
   const int phi_n = ((q + 1) & ~1) + 2;
@@ -207,8 +199,8 @@ __global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass(PassArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_lsar_pass_tma: the pass for q >= 16, FIR on the fp64 tensor cores (DMMA
-// m8n8k4) with every load asynchronous.
+// k_lsar_pass_pst: the pass for q >= 1 in the sweeps, FIR on the fp64 tensor
+// cores (DMMA m8n8k4), TMA bulk loads, persistent CTAs.
 //
 // FIR as a polyphase GEMM: with tile rows i = 8a + b,
 //   r[8a + b] = sum_k Y[a][k] Phi[k][b],   Y[a][k] = y[i0 + 8a + k]  (Hankel, stride 8)
@@ -223,36 +215,33 @@ __global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass(PassArgs a) {
 // addresses per warp load, broadcast).  Summation order differs from the
 // reference's tap loop (rounding ~1e-16); k_lsar_pass keeps the exact order.
 //
-// Memory: at CTA entry one warp issues TMA bulk copies (cp.async.bulk +
-// mbarrier) of the series tile (64-double segments into the skew12 layout)
-// and of the tile's previous state s_{q-1}, r_{q-1}; the FIR waits only for
-// the series and the state lands while it runs.  r_q goes to a skew16 buffer
-// aliasing the dead series tile; the update and the chunk partials then run
-// out of shared memory (pass_partials), with coalesced stores of s_q, r_q.
 __host__ __device__ __forceinline__ int skew12(int x) { return x + 4 * (x >> 6); }
 
-struct PassTmaLayout {
-  int kd, ys_n, ys_sk, phi_n;
-  __host__ __device__ explicit PassTmaLayout(int q)
-      : kd((q + 8 + 3) & ~3), ys_n(kPassTile + ((q + 8 + 3) & ~3) + 8) {
-    const int rn_sk = kPassTile + (kPassTile >> 4) + 2;
-    ys_sk = max(skew12(ys_n) + 8, rn_sk);
-    ys_sk = (ys_sk + 1) & ~1;
+// shared memory of k_lsar_pass_pst, in doubles:
+//   [4: mbarriers][s tile: 2048][r tile: 2048][series tile: ys_sk (skew12)][phiP: phi_n]
+struct PassLayout {
+  int kd;     // GEMM depth: q + 8 rounded up to a k-step of 4
+  int ys_n;   // series values staged per tile (2048 + kd + 8 halo)
+  int ys_sk;  // their skew12 footprint (even, for 16-byte alignment)
+  int phi_n;  // compact B table
+  __host__ __device__ explicit PassLayout(int q) {
+    kd = (q + 8 + 3) & ~3;
+    ys_n = kPassTile + kd + 8;
+    ys_sk = (skew12(ys_n) + 8 + 1) & ~1;
     phi_n = (q + 25) & ~1;
   }
-  // doubles: [2 mbarriers][s: 2048][r: 2048][ys / rn: ys_sk][phi: phi_n]
-  __host__ __device__ size_t bytes() const { return sizeof(double) * (size_t)(2 + 2 * kPassTile + ys_sk + phi_n); }
+  __host__ __device__ size_t bytes() const { return sizeof(double) * (size_t)(4 + 2 * kPassTile + ys_sk + phi_n); }
 };
 constexpr int kPhiOff = 16;
 
-// DMMA FIR of one 2048-row tile (the polyphase GEMM above):
-// ys = series tile (skew12), pb = phiP + kPhiOff + q - 1 + g - t, result r_q
-// written to rn (skew16) AFTER a barrier (rn may alias ys)
-__device__ __forceinline__ void pass_fir_dmma(const double* ys, const double* pb, int nsteps, double* rn) {
+// DMMA FIR of one 2048-row tile (the polyphase GEMM above): ys = series tile
+// (skew12), pb = phiP + kPhiOff + q - 1 + g - t; on return c0[u] / c1[u] hold
+// r_q of tile rows 8 (64 warp + 8 g + u) + 2 t (+ 1)
+__device__ __forceinline__ void pass_fir_acc(const double* ys, const double* pb, int nsteps, double (&c0)[8],
+                                             double (&c1)[8]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int abase = 64 * warp;
-  double c0[8], c1[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) c0[u] = c1[u] = 0.0;
   const int xbase = 8 * (abase + 8 * g) + t;
@@ -280,93 +269,160 @@ __device__ __forceinline__ void pass_fir_dmma(const double* ys, const double* pb
     fe[7] = ys[skew12(xn)];
     fo[7] = ys[skew12(xn + 4)];
   }
-  __syncthreads();  // series tile dead: r_q may go to its space
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int r = 8 * (abase + 8 * g + u) + 2 * t;
-    rn[skew16(r)] = c0[u];
-    rn[skew16(r + 1)] = c1[u];
+}
+
+// ---------------------------------------------------------------------------
+// Persistent CTAs (grid = resident CTAs), each walking tiles blockIdx.x,
+// + gridDim.x, ...  Loads are TMA bulk copies (cp.async.bulk + mbarrier): the
+// series tile as 64-double segments into the skew12 layout, the previous
+// state s_{q-1}, r_{q-1} as two contiguous copies.  The update works straight
+// from the FIR accumulators, so the series buffer is free as soon as the FIR
+// ends: the next tile's series copy is issued then and lands during this
+// tile's update, and the next tile's state copy is issued after the update
+// and lands during the next FIR.  Chunk sums: each lane folds its 8 values of
+// a chunk (rows 8 a + 2 t + e), then two shuffles over t; tile sums: shuffles
+// over g, fixed-order sum over the warps.  Deterministic.
+__device__ __forceinline__ void pst_issue_y(const PassArgs& a, int64_t i0, double* ys, const PassLayout& L,
+                                            uint64_t* bar) {  // warp 0
+  const int lane = threadIdx.x & 31;
+  const int ycopy = (int)min((int64_t)L.ys_n, a.ylen - i0) & ~1;
+  if (lane == 0) {
+    fence_proxy_async_smem();
+    mbar_expect_tx(bar, (uint32_t)ycopy * 8u);
+  }
+  __syncwarp();
+  const int nseg = (ycopy + 63) >> 6;
+  for (int k = lane; k < nseg; k += 32) {
+    const int len = min(64, ycopy - 64 * k);
+    bulk_g2s(ys + skew12(64 * k), a.y + i0 + 64 * k, (uint32_t)len * 8u, bar);
+  }
+}
+__device__ __forceinline__ void pst_fill_y(const PassArgs& a, int64_t i0, double* ys, const PassLayout& L) {
+  const int ycopy = (int)min((int64_t)L.ys_n, a.ylen - i0) & ~1;
+  for (int x = ycopy + threadIdx.x; x < L.ys_n; x += kPassThreads) ys[skew12(x)] = 0.0;
+}
+__device__ __forceinline__ void pst_issue_state(const PassArgs& a, int64_t i0, int rows, double* ss, double* rr,
+                                                uint64_t* bar) {  // one thread
+  const int rcopy = (a.dbg & 8) ? 0 : rows & ~1;
+  fence_proxy_async_smem();
+  mbar_expect_tx(bar, (uint32_t)rcopy * 16u);
+  if (rcopy > 0) {
+    bulk_g2s(ss, a.s + i0, (uint32_t)rcopy * 8u, bar);
+    bulk_g2s(rr, a.r + i0, (uint32_t)rcopy * 8u, bar);
+  }
+  if (rows > rcopy && !(a.dbg & 8)) {  // odd last row: generic load (address not covered by the copy)
+    ss[rcopy] = a.s[i0 + rcopy];
+    rr[rcopy] = a.r[i0 + rcopy];
   }
 }
 
-__global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass_tma(PassArgs a) {
+__global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass_pst(PassArgs a) {
   extern __shared__ __align__(128) double sm[];
+  __shared__ double red[2][kPassThreads / 32];
   const int q = a.q;
-  const PassTmaLayout L(q);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
-  double* ss = sm + 2;
+  const PassLayout L(q);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);  // [0]: series, [1]: state
+  double* ss = sm + 4;
   double* rr = ss + kPassTile;
   double* ys = rr + kPassTile;
-  double* rn = ys;  // after the FIR
   double* phiP = ys + L.ys_sk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t i0 = (int64_t)blockIdx.x * kPassTile;
-  const int rows = (int)min((int64_t)kPassTile, a.w - i0);
-  // series values readable from y + i0 (the buffer carries a zero pad), even count
-  const int ycopy = (int)min((int64_t)L.ys_n, a.ylen - i0) & ~1;
-  const int rcopy = (a.dbg & 8) ? 0 : rows & ~1;
-  STAMP(0);
-  const double invR = 1.0 / *a.Rprev;  // issued early: off the post-FIR critical path
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_init(&bars[0], 1);
-      mbar_init(&bars[1], 1);
-      mbar_expect_tx(&bars[0], (uint32_t)ycopy * 8u);
-      mbar_expect_tx(&bars[1], (uint32_t)rcopy * 16u);
-    }
-    __syncwarp();
-    const int nseg = (ycopy + 63) >> 6;
-    for (int k = lane; k < nseg; k += 32) {
-      const int len = min(64, ycopy - 64 * k);
-      bulk_g2s(ys + skew12(64 * k), a.y + i0 + 64 * k, (uint32_t)len * 8u, &bars[0]);
-    }
-    if (lane == 0 && rcopy > 0) {
-      bulk_g2s(ss, a.s + i0, (uint32_t)rcopy * 8u, &bars[1]);
-      bulk_g2s(rr, a.r + i0, (uint32_t)rcopy * 8u, &bars[1]);
-    }
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t ntile = (a.w + kPassTile - 1) / kPassTile;
+  int64_t tile = blockIdx.x;
+  const double invR = 1.0 / *a.Rprev;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
   }
-  // generic-proxy fills of what the copies do not cover (disjoint addresses)
-  for (int x = ycopy + tid; x < L.ys_n; x += kPassThreads) ys[skew12(x)] = 0.0;
-  if (tid == 0 && rows > rcopy && !(a.dbg & 8)) {
-    ss[rcopy] = a.s[i0 + rcopy];
-    rr[rcopy] = a.r[i0 + rcopy];
+  __syncthreads();
+  {
+    const int64_t i0 = tile * kPassTile;
+    if (warp == 0) pst_issue_y(a, i0, ys, L, &bars[0]);
+    if (tid == 32) pst_issue_state(a, i0, (int)min((int64_t)kPassTile, a.w - i0), ss, rr, &bars[1]);
+    pst_fill_y(a, i0, ys, L);
   }
   for (int m = tid; m < L.phi_n; m += kPassThreads) {
     const int j = m - kPhiOff;
     phiP[m] = (j >= 0 && j < q) ? __ldg(a.phi + j) : (j == -1 ? -1.0 : 0.0);
   }
   __syncthreads();
-  STAMP(1);
-  mbar_wait(&bars[0], 0);
-  STAMP(2);
-  // ---- FIR on DMMA (B fragment from the compact table) ----
-  // B(s, lane) = Phi[k = 4 s + t][b = g] = tap j = q - 1 + g - 4 s - t
-  const double* pb = phiP + kPhiOff + q - 1 + (lane >> 2) - (lane & 3);
-  pass_fir_dmma(ys, pb, (a.dbg & 4) ? 0 : L.kd >> 2, rn);
-  STAMP(3);
-  __syncthreads();
-  mbar_wait(&bars[1], 0);
-  STAMP(4);
-  // ---- update: coalesced over rows, new state stored from registers ----
-#pragma unroll 4
-  for (int u = 0; u < kPassR; ++u) {
-    const int row = tid + kPassThreads * u;
-    if (row < rows) {
-      const double rnew = rn[skew16(row)];
-      const double ro = rr[row];
-      const double snew = fma(ro * ro, invR, ss[row]);
-      if (!(a.dbg & 8)) {
-        a.s[i0 + row] = snew;
-        a.r[i0 + row] = rnew;
-      }
-      ss[row] = snew;
-      rr[row] = rnew;
+  const double* pb = phiP + kPhiOff + q - 1 + g - t;
+  const int nsteps = (a.dbg & 4) ? 0 : L.kd >> 2;
+  for (int k = 0; tile < ntile; ++k, tile += gridDim.x) {
+    const int64_t i0 = tile * kPassTile;
+    const int rows = (int)min((int64_t)kPassTile, a.w - i0);
+    const int64_t next = tile + gridDim.x;
+    mbar_wait(&bars[0], (uint32_t)k & 1u);
+    double c0[8], c1[8];
+    pass_fir_acc(ys, pb, nsteps, c0, c1);
+    __syncthreads();  // series tile consumed
+    if (next < ntile) {
+      if (warp == 0) pst_issue_y(a, next * kPassTile, ys, L, &bars[0]);
+      pst_fill_y(a, next * kPassTile, ys, L);
     }
+    mbar_wait(&bars[1], (uint32_t)k & 1u);
+    // ---- update from the accumulators; chunk h of this lane = rows of u in [4h, 4h + 4) ----
+    double A[2] = {0.0, 0.0}, B[2] = {0.0, 0.0};
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int row = 8 * (64 * warp + 8 * g + u) + 2 * t;
+      if (row < rows) {
+        const double2 so = *reinterpret_cast<const double2*>(ss + row);
+        const double2 ro = *reinterpret_cast<const double2*>(rr + row);
+        const double s0 = fma(ro.x * ro.x, invR, so.x);
+        const double s1 = fma(ro.y * ro.y, invR, so.y);
+        const int h = u >> 2;
+        A[h] += s0;
+        B[h] = fma(c0[u], c0[u], B[h]);
+        if (row + 1 < rows) {
+          A[h] += s1;
+          B[h] = fma(c1[u], c1[u], B[h]);
+          if (!(a.dbg & 8)) {
+            *reinterpret_cast<double2*>(a.s + i0 + row) = make_double2(s0, s1);
+            *reinterpret_cast<double2*>(a.r + i0 + row) = make_double2(c0[u], c1[u]);
+          }
+        } else if (!(a.dbg & 8)) {
+          a.s[i0 + row] = s0;
+          a.r[i0 + row] = c0[u];
+        }
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      A[h] += __shfl_xor_sync(0xffffffffu, A[h], 1);
+      A[h] += __shfl_xor_sync(0xffffffffu, A[h], 2);
+      B[h] += __shfl_xor_sync(0xffffffffu, B[h], 1);
+      B[h] += __shfl_xor_sync(0xffffffffu, B[h], 2);
+    }
+    if (t == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 16 * warp + 2 * g + h;  // chunk of the tile
+        if (kChunk * c < rows) {
+          a.chunkA[i0 / kChunk + c] = A[h];
+          a.chunkB[i0 / kChunk + c] = B[h];
+        }
+      }
+    }
+    double TA = A[0] + A[1], TB = B[0] + B[1];
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      TA += __shfl_xor_sync(0xffffffffu, TA, o);
+      TB += __shfl_xor_sync(0xffffffffu, TB, o);
+    }
+    if (lane == 0) {
+      red[0][warp] = TA;
+      red[1][warp] = TB;
+    }
+    __syncthreads();  // state tile consumed; red complete
+    if (tid == 0) {
+      a.tileA[tile] = ((red[0][0] + red[0][1]) + red[0][2]) + red[0][3];
+      a.tileB[tile] = ((red[1][0] + red[1][1]) + red[1][2]) + red[1][3];
+    }
+    if (tid == 32 && next < ntile)
+      pst_issue_state(a, next * kPassTile, (int)min((int64_t)kPassTile, a.w - next * kPassTile), ss, rr, &bars[1]);
   }
-  __syncthreads();
-  STAMP(5);
-  pass_partials<false>(a, ss, rr, rows, i0, blockIdx.x);
-  STAMP(6);
 }
 
 }  // namespace tfk

@@ -1,8 +1,7 @@
 // pass_bench.cu -- the fused LSAR pass kernels in isolation (development helper).
-// Times k_lsar_pass and k_lsar_pass_tma over w = 1e7 rows at several lags,
-// the latter also with its debug switches (dbg bit 2: no FIR, bit 3: no state
-// traffic) to split the cost into memory and FIR parts, plus per-CTA phase
-// timestamps (%globaltimer).
+// Times k_lsar_pass_pst over w = 1e7 rows at several lags, also with its
+// debug switches (dbg bit 2: no FIR, bit 3: no state traffic) to split the
+// cost into memory and FIR parts, and k_lsar_pass (exact tap order) at q < 16.
 // build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -I paper_2112_12994_b200/csrc tools/pass_bench.cu -o gpurun_out/pass_bench
 #include <cuda_runtime.h>
 #include <cstdio>
@@ -54,49 +53,55 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     return ms * 1e3 / reps;
   };
-  for (int q : {1, 8, 15}) {  // CUDA-core pass (exact tap order)
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  for (int q : {1, 8, 15, 16, 50, 100, 200, 500}) {
     a.q = q;
     a.dbg = 0;
-    const size_t sm0 = pass_smem_bytes(q);
-    CK(cudaFuncSetAttribute(k_lsar_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm0));
-    const double t = timeit([&] { k_lsar_pass<<<(unsigned)ntile, kPassThreads, sm0>>>(a); });
-    CK(cudaGetLastError());
-    printf("q=%3d k_lsar_pass %7.1f us  %.0f GB/s (40 B/row moved)\n", q, t, 40.0 * w / t / 1e3);
-  }
-  for (int q : {16, 50, 100, 200, 500}) {
-    a.q = q;
-    const size_t sm2 = PassTmaLayout(q).bytes();
-    CK(cudaFuncSetAttribute(k_lsar_pass_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
-    int o2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_lsar_pass_tma, kPassThreads, sm2);
-    double t_tma[4];
+    const double fl = 2.0 * (q + 1) * w;
+    const double t_mem = 40.0 * w / 6537e3, t_fir = fl / 36.4e6;  // us at the measured copy / DFMA peaks
+    double t_core = 0;
+    if (q < 16) {  // CUDA-core pass (exact tap order)
+      const size_t sm0 = pass_smem_bytes(q);
+      CK(cudaFuncSetAttribute(k_lsar_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm0));
+      t_core = timeit([&] { k_lsar_pass<<<(unsigned)ntile, kPassThreads, sm0>>>(a); });
+    }
+    const size_t smp = PassLayout(q).bytes();
+    CK(cudaFuncSetAttribute(k_lsar_pass_pst, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lsar_pass_pst, kPassThreads, smp);
+    const unsigned grid = (unsigned)std::min<int64_t>(ntile, (int64_t)occ * nsm);
+    double tp[4];
     for (int m = 0; m < 4; ++m) {
       a.dbg = 4 * m;
-      t_tma[m] = timeit([&] { k_lsar_pass_tma<<<(unsigned)ntile, kPassThreads, sm2>>>(a); });
+      tp[m] = timeit([&] { k_lsar_pass_pst<<<grid, kPassThreads, smp>>>(a); });
     }
     a.dbg = 0;
     CK(cudaGetLastError());
-    const double fl = 2.0 * (q + 1) * w;
-    const double t_mem = 40.0 * w / 6537e3, t_fir = fl / 36.4e6;  // us at the measured copy / DFMA peaks
-    printf("q=%3d occ %d | tma full %7.1f  noFIR %7.1f  noState %7.1f  neither %7.1f us | "
-           "roofline max(mem %.1f, fp64 %.1f) -> %.0f%%\n",
-           q, o2, t_tma[0], t_tma[1], t_tma[2], t_tma[3], t_mem, t_fir, 100.0 * std::max(t_mem, t_fir) / t_tma[0]);
-    {  // phase timestamps (one extra run)
-      unsigned long long* st;
-      CK(cudaMalloc(&st, sizeof(unsigned long long) * 8 * ntile));
-      CK(cudaMemset(st, 0, sizeof(unsigned long long) * 8 * ntile));
-      a.stamps = st;
-      k_lsar_pass_tma<<<(unsigned)ntile, kPassThreads, sm2>>>(a);
-      CK(cudaDeviceSynchronize());
-      a.stamps = nullptr;
-      std::vector<unsigned long long> hs(8 * ntile);
-      CK(cudaMemcpy(hs.data(), st, sizeof(unsigned long long) * 8 * ntile, cudaMemcpyDeviceToHost));
-      cudaFree(st);
-      double acc[7] = {0};
-      for (int64_t b = 0; b < ntile; ++b)
-        for (int i = 1; i < 7; ++i) acc[i] += (double)(hs[8 * b + i] - hs[8 * b + i - 1]);
-      printf("      phases (ns/CTA): issue+fill %.0f  ywait %.0f  fir %.0f  swait %.0f  update %.0f  partials %.0f\n",
-             acc[1] / ntile, acc[2] / ntile, acc[3] / ntile, acc[4] / ntile, acc[5] / ntile, acc[6] / ntile);
+    printf("q=%3d pst occ %d | full %7.1f  noFIR %7.1f  noState %7.1f  neither %7.1f us | roofline max(mem %.1f, "
+           "fp64 %.1f) -> %.0f%%",
+           q, occ, tp[0], tp[1], tp[2], tp[3], t_mem, t_fir, 100.0 * std::max(t_mem, t_fir) / tp[0]);
+    if (q < 16) printf(" | k_lsar_pass %.1f us", t_core);
+    printf("\n");
+    if (q < 16) {  // agreement with the exact-order kernel
+      std::vector<double> s1(w), r1(w), s2(w), r2(w);
+      const size_t sm0 = pass_smem_bytes(q);
+      CK(cudaMemcpy(s, hy.data(), sizeof(double) * w, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(r, hy.data() + 1, sizeof(double) * w, cudaMemcpyHostToDevice));
+      k_lsar_pass<<<(unsigned)ntile, kPassThreads, sm0>>>(a);
+      CK(cudaMemcpy(s1.data(), s, sizeof(double) * w, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(r1.data(), r, sizeof(double) * w, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(s, hy.data(), sizeof(double) * w, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(r, hy.data() + 1, sizeof(double) * w, cudaMemcpyHostToDevice));
+      k_lsar_pass_pst<<<grid, kPassThreads, smp>>>(a);
+      CK(cudaMemcpy(s2.data(), s, sizeof(double) * w, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(r2.data(), r, sizeof(double) * w, cudaMemcpyDeviceToHost));
+      double ds = 0, dr = 0;
+      for (int64_t i = 0; i < w; ++i) {
+        ds = std::max(ds, std::abs(s1[i] - s2[i]) / std::max(std::abs(s1[i]), 1e-300));
+        dr = std::max(dr, std::abs(r1[i] - r2[i]) / (std::abs(r1[i]) + 1e-3));
+      }
+      printf("      pst vs exact-order: s max rel %.2e, r max rel %.2e\n", ds, dr);
     }
   }
   return 0;
