@@ -37,6 +37,21 @@ static void cuda_check(cudaError_t e, const char* what) {
 static thread_local int64_t g_launches = 0;
 #define COUNT_LAUNCH() (++g_launches)
 
+// Opt a kernel in to `bytes` of dynamic shared memory (monotone per kernel).
+// Always, not only above 48 KB: static + dynamic can cross the default limit
+// below it.  Serialised: contexts launch from several host threads.
+static void smem_optin(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> have;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& h = have[func];
+  if (bytes > h) {
+    const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) throw TfError{TF_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e)};
+    h = bytes;
+  }
+}
+
 std::atomic<uint64_t> g_alloc_gen{0};  // bumped by every device (re)allocation
 
 template <class T>
@@ -129,11 +144,7 @@ static void gram_dense(tf_context* ctx, const double* Q, int64_t ld, int64_t row
                        const int* gate) {
   const GramPlan g = gram_plan(rows, K, ctx->sm_count);
   const size_t smem = gram2_smem_bytes();
-  static size_t attr = 0;
-  if (smem > attr) {
-    CK(cudaFuncSetAttribute(k_gram_dense_t<kG2Stages>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  smem_optin((const void*)k_gram_dense_t<kG2Stages>, smem);
   dim3 grid(g.npair, g.nsplit);
   k_gram_dense_t<kG2Stages><<<grid, kGramThreads, smem, ctx->stream>>>(Q, ld, rows, K, g.nblk, g.rps, ctx->sb.W.get(), gate);
   LAUNCH_CHECK("k_gram_dense");
@@ -165,11 +176,7 @@ static void qform(tf_context* ctx, const L& ld, int64_t rows, int K, const doubl
                   const int* gate) {
   using Wt = decltype(to_win(ld));
   constexpr size_t smem = qform_pipe_smem<2>();
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_qform_pipe<Wt, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  smem_optin((const void*)k_qform_pipe<Wt, 2, false>, smem);
   dim3 grid((unsigned)((rows + 63) / 64), (unsigned)((K + 63) / 64));
   k_qform_pipe<Wt, 2, false><<<grid, kGramThreads, smem, ctx->stream>>>(to_win(ld), rows, K, B, Q, ldq_of(K),
                                                                        gate);
@@ -240,11 +247,7 @@ static void cholinv(tf_context* ctx, const double* G, int K, int pass, int64_t r
   a.status = status;
   a.lag = lag;
   const size_t smem = a.use_smem ? cholinv_smem_bytes(K) : 0;
-  static size_t attr = 0;  // static + dynamic must fit the opt-in limit, so always opt in
-  if (smem > attr) {
-    CK(cudaFuncSetAttribute(k_cholinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  smem_optin((const void*)k_cholinv, smem);
   k_cholinv<<<1, kCholinvThreads, smem, ctx->stream>>>(a);
   {
     const cudaError_t e = cudaGetLastError();
@@ -269,11 +272,7 @@ template <bool TPU>
 static void trsm_right(tf_context* ctx, const double* B, const double* RD, double* X, int64_t rows,
                        int K, const int* gate) {
   const size_t smem = trsm_smem_bytes(K);
-  static size_t attr = 0;
-  if (smem > attr) {
-    CK(cudaFuncSetAttribute(k_trsm_right<TPU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  smem_optin((const void*)k_trsm_right<TPU>, smem);
   const unsigned grid = TPU ? (unsigned)((K + 31) / 32) : (unsigned)((rows + 31) / 32);
   k_trsm_right<TPU><<<grid, kTrsmThreads, smem, ctx->stream>>>(B, RD, X, rows, K, TPU ? K : ldq_of(K), gate);
   LAUNCH_CHECK("k_trsm_right");
@@ -435,11 +434,7 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
   // (gated on the shift flag inside the kernel; small systems only)
   if (c * (int64_t)(K - 1) <= kMinNormCap && K - 1 <= 64 && c <= 4096) {
     const size_t smem = sizeof(double) * ((size_t)c * (K - 1) + c + 2 * (size_t)(K - 1) * (K - 1));
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-      CK(cudaFuncSetAttribute(k_minnorm<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = smem;
-    }
+    smem_optin((const void*)k_minnorm<L>, smem);
     k_minnorm<L><<<1, kMinNormThreads, smem, st>>>(ld, c, K, rev, fl, o.phi, o.coefs, o.coef_off, o.taus,
                                                    o.method, o.lag, o.status);
     LAUNCH_CHECK("k_minnorm");
@@ -469,16 +464,12 @@ static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, co
   const int64_t ntile = (w + kPassTile - 1) / kPassTile;
   if (!exact_order && q >= kPassPstMinQ) {
     const size_t smem = PassLayout(q).bytes();
+    smem_optin((const void*)k_lsar_pass_pst, smem);
     static std::mutex mu;  // contexts launch from several host threads
-    static size_t attr = 0;
     static std::map<size_t, int> occ_of;
     int occ;
     {
       std::lock_guard<std::mutex> lk(mu);
-      if (smem > attr) {
-        CK(cudaFuncSetAttribute(k_lsar_pass_pst, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = smem;
-      }
       auto it = occ_of.find(smem);
       if (it == occ_of.end()) {
         int o = 0;
@@ -494,11 +485,7 @@ static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, co
     return;
   }
   const size_t smem = pass_smem_bytes(q);
-  static size_t attr = 0;
-  if (smem > attr) {
-    CK(cudaFuncSetAttribute(k_lsar_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  smem_optin((const void*)k_lsar_pass, smem);
   k_lsar_pass<<<(unsigned)ntile, kPassThreads, smem, ctx->stream>>>(a);
   LAUNCH_CHECK("k_lsar_pass");
   COUNT_LAUNCH();
@@ -1041,11 +1028,7 @@ static void score_distribution(tf_context* ctx, const double* scores, int64_t w)
 
 template <class L, class WL, bool UPPER>
 static void rowsq_attr() {
-  static bool done = false;
-  if (!done) {
-    CK(cudaFuncSetAttribute(k_rowsq<L, WL, UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowsqSmem));
-    done = true;
-  }
+  smem_optin((const void*)k_rowsq<L, WL, UPPER>, kRowsqSmem);
 }
 
 // scores of every window row t in [0, rows): out[t] = ||x_t W||^2 (Hankel tiles)
@@ -1054,19 +1037,32 @@ static void rowsq_all_rows(tf_context* ctx, int64_t rows, int K, const WL& wl, i
   const int ntiles = (N + 63) / 64;
   if (ntiles > 8) throw TfError{TF_USAGE, "row-score tiles > 8"};
   const size_t smem = rowsq_hankel_smem(K);
-  static size_t attr = 0;
-  if (smem > attr) {
-    CK(cudaFuncSetAttribute(k_rowsq_hankel<WL, UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  smem_optin((const void*)k_rowsq_hankel<WL, UPPER>, smem);
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rowsq_hankel<WL, UPPER>, kHkThreads, smem));
-  // equal CTA share per column tile, one wave (a narrow tile's blocks are not
-  // proportionally cheaper: loads and barriers dominate them)
-  const int per_tile = std::max(1, per_sm * ctx->sm_count / ntiles);
+  // one wave of CTAs split over the column tiles in proportion to each tile's
+  // cost: (k-steps it runs) x (8-column fragments it holds + F), F = 16
+  // (measured: a block's loads, barriers and epilogue cost about as much as
+  // two full column tiles of DMMA) -- narrow last tiles and the triangular
+  // final pass (tile j only needs k < 64 (j + 1)) get somewhat fewer CTAs
+  const int total = std::max(ntiles, per_sm * ctx->sm_count);
+  double wsum = 0.0, wj[9];
+  for (int j = 0; j < ntiles; ++j) {
+    const int kend = UPPER ? std::min(hk_kpad(K), hk_kpad(std::min(K, 64 * (j + 1)))) : hk_kpad(K);
+    const int frags = std::min(8, (N - 64 * j + 7) / 8);
+    static const double fo = [] { const char* v = std::getenv("TF_HK_F"); return v ? std::atof(v) : 16.0; }();
+    wj[j] = (double)kend * (frags + fo);
+    wsum += wj[j];
+  }
   HkPlan plan;
   plan.ntiles = ntiles;
-  for (int j = 0; j <= ntiles; ++j) plan.first[j] = j * per_tile;
+  plan.first[0] = 0;
+  double acc = 0.0;
+  for (int j = 0; j < ntiles; ++j) {
+    acc += wj[j];
+    const int want = (int)std::lround(acc / wsum * total);
+    plan.first[j + 1] = std::max(plan.first[j] + 1, std::min(want, total - (ntiles - 1 - j)));
+  }
   ctx->rh_part.need((size_t)ntiles * rows);
   k_rowsq_hankel<WL, UPPER><<<plan.first[ntiles], kHkThreads, smem, ctx->stream>>>(
       ctx->y.get(), ctx->n, rows, K, wl, N, plan, ctx->rh_part.get());

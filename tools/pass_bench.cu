@@ -12,7 +12,8 @@
 #include "k_pass.cuh"
 using namespace tfk;
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s line %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
-int main() {
+int main(int argc, char** argv) {
+  const int only_q = argc > 1 ? atoi(argv[1]) : -1;  // profile mode: one launch of the pst kernel at this lag
   const int64_t w = 10000000, n = w + 600;
   std::vector<double> hy(n + 64);
   std::mt19937_64 g(1);
@@ -55,6 +56,18 @@ int main() {
   };
   int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  if (only_q >= 0) {
+    a.q = only_q;
+    const size_t smp = PassLayout(only_q).bytes();
+    CK(cudaFuncSetAttribute(k_lsar_pass_pst, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lsar_pass_pst, kPassThreads, smp);
+    const unsigned grid = (unsigned)std::min<int64_t>(ntile, (int64_t)occ * nsm);
+    k_lsar_pass_pst<<<grid, kPassThreads, smp>>>(a);
+    CK(cudaDeviceSynchronize());
+    printf("one launch at q=%d done\n", only_q);
+    return 0;
+  }
   for (int q : {1, 8, 15, 16, 50, 100, 200, 500}) {
     a.q = q;
     a.dbg = 0;
