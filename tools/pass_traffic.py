@@ -15,7 +15,7 @@ res = {"kernel": d.get("Kernel Name", "").split("(")[0], "lag": q, "n": n, "p_ba
        "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch_avg": rd + wr,
        "algorithmic_bytes_per_launch": 24.0 * w, "moved_bytes_model": 40.0 * w,
        "duration_s_under_ncu": num("gpu__time_duration.sum"),
-       "note": "one ncu --set full capture (clock-control none); algorithmic = 24 B/row (y, s in, s out); "
+       "note": "one ncu --set full capture of the launch at this lag inside a C2 LSAR sweep (clock-control none); algorithmic = 24 B/row (y, s in, s out); "
                "the kernel also reads and writes r (40 B/row moved)"}
 json.dump(res, open("profiles/ncu_pass_traffic.json", "w"), indent=1)
 print(json.dumps(res))
