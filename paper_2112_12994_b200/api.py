@@ -74,6 +74,47 @@ class TimeSeries:
         return self.size()
 
 
+def load_series_bin(path: str, *, pinned: bool = False) -> TimeSeries:
+    """Read the reference's flat binary series (series.cpp:273-284, format
+    series.hpp:93: uint64 little-endian count, then count f64 little-endian
+    values), with its DataError messages.  pinned=True reads straight into
+    page-locked host memory (a copy-free TimeSeries for a fast upload)."""
+    try:
+        f = open(path, "rb")
+    except OSError:
+        raise DataError("cannot open " + path) from None
+    with f:
+        head = f.read(8)
+        if len(head) < 8:
+            raise DataError(path + ": truncated header")
+        count = int(np.frombuffer(head, dtype="<u8")[0])
+        if pinned:
+            import torch
+            buf = torch.empty(count, dtype=torch.float64, pin_memory=True)
+            arr = buf.numpy()
+            got = f.readinto(memoryview(arr).cast("B")) if count else 0
+            if got != 8 * count:
+                raise DataError(path + ": truncated payload")
+            ts = TimeSeries(arr, copy=False)
+            ts._pinned = buf  # keep the page-locked buffer alive with the series
+            return ts
+        vals = np.fromfile(f, dtype="<f8", count=count)
+        if vals.size != count:
+            raise DataError(path + ": truncated payload")
+    return TimeSeries(vals, copy=False)
+
+
+def save_series_bin(series: TimeSeries, path: str) -> None:
+    """Write the flat binary format (series.cpp:262-271)."""
+    v = np.ascontiguousarray(series.values(), dtype="<f8")
+    try:
+        with open(path, "wb") as f:
+            f.write(np.array([v.size], dtype="<u8").tobytes())
+            v.tofile(f)
+    except OSError:
+        raise DataError("cannot write " + path) from None
+
+
 @dataclass
 class PACFResult:
     taus: list
