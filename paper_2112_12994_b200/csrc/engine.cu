@@ -496,7 +496,7 @@ static void launch_scan(tf_context* ctx, int64_t ntile, int lag, int check_r, in
   k_lag_scan<<<1, kScanThreads, 0, ctx->stream>>>(ctx->tileA.get(), ctx->tileB.get(), ntile,
                                                   ctx->OT.get(), ctx->scal.get(), ctx->Rhist.get(),
                                                   ctx->Shist.get(), lag, check_r, ctx->status.get(),
-                                                  unit_r, r_fixed);
+                                                  unit_r, r_fixed, ctx->guide.get());
   LAUNCH_CHECK("k_lag_scan");
   COUNT_LAUNCH();
 }
@@ -512,6 +512,7 @@ static void launch_draw(tf_context* ctx, uint64_t seed, int64_t c, int64_t w, in
   a.c = c;
   a.scal = ctx->scal.get();
   a.OT = ctx->OT.get();
+  a.guide = ctx->guide.get();
   a.ntile = (w + kPassTile - 1) / kPassTile;
   a.tA = ctx->tileA.get();
   a.tB = ctx->tileB.get();
@@ -522,7 +523,7 @@ static void launch_draw(tf_context* ctx, uint64_t seed, int64_t c, int64_t w, in
   a.w = w;
   a.idx = idx;
   a.wts = wts;
-  const int per = kDrawThreads / 32;
+  const int per = kDrawPerCta;
   k_draw<<<(unsigned)((c + per - 1) / per), kDrawThreads, 0, ctx->stream>>>(a);
   LAUNCH_CHECK("k_draw");
   COUNT_LAUNCH();
@@ -538,6 +539,7 @@ static void alloc_state(tf_context* ctx, int p_bar, int64_t c, int64_t w) {
   ctx->tileA.need(ntile);
   ctx->tileB.need(ntile);
   ctx->OT.need(ntile);
+  ctx->guide.need(guide_buckets(ntile) + 1);
   ctx->scal.need(4);
   ctx->Rhist.need(p_bar + 2);
   ctx->Shist.need(p_bar + 2);
@@ -999,6 +1001,7 @@ static void launch_draw_on(tf_context* ctx, const double* scores, int64_t w, uin
   a.c = c;
   a.scal = ctx->scal.get();
   a.OT = ctx->OT.get();
+  a.guide = ctx->guide.get();
   a.ntile = (w + kPassTile - 1) / kPassTile;
   a.tA = ctx->tileA.get();
   a.tB = ctx->tileB.get();
@@ -1009,7 +1012,7 @@ static void launch_draw_on(tf_context* ctx, const double* scores, int64_t w, uin
   a.w = w;
   a.idx = idx;
   a.wts = wts;
-  const int per = kDrawThreads / 32;
+  const int per = kDrawPerCta;
   k_draw<<<(unsigned)((c + per - 1) / per), kDrawThreads, 0, ctx->stream>>>(a);
   LAUNCH_CHECK("k_draw");
   COUNT_LAUNCH();
@@ -1469,6 +1472,7 @@ static int64_t shard_sample(tf_context* ctx, uint64_t seed, double s_total, doub
   a.c = c;
   a.scal = ctx->scal.get();
   a.OT = ctx->OT.get();
+  a.guide = ctx->guide.get();
   a.ntile = ntile;
   a.tA = ctx->tileA.get();
   a.tB = ctx->tileB.get();
@@ -1485,7 +1489,7 @@ static int64_t shard_sample(tf_context* ctx, uint64_t seed, double s_total, doub
   a.offset = offset;
   a.is_last = is_last;
   a.accept = ctx->rh_ok.get();
-  const int per = kDrawThreads / 32;
+  const int per = kDrawPerCta;
   k_draw<<<(unsigned)((c + per - 1) / per), kDrawThreads, 0, st>>>(a);
   LAUNCH_CHECK("k_draw");
   COUNT_LAUNCH();
@@ -1813,7 +1817,7 @@ void tf_destroy(tf_context* ctx) {
   if (ctx->rh_graph.exec) cudaGraphExecDestroy(ctx->rh_graph.exec);
   if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
   ctx->y.release(); ctx->s.release(); ctx->r.release(); ctx->chunkA.release(); ctx->chunkB.release();
-  ctx->tileA.release(); ctx->tileB.release(); ctx->OT.release(); ctx->scal.release();
+  ctx->tileA.release(); ctx->tileB.release(); ctx->OT.release(); ctx->guide.release(); ctx->scal.release();
   ctx->Rhist.release(); ctx->Shist.release(); ctx->phi.release(); ctx->coefs.release();
   ctx->taus.release(); ctx->idx.release(); ctx->fidx.release(); ctx->idx_hist.release();
   ctx->wts.release(); ctx->fw.release(); ctx->w_hist.release(); ctx->status.release();

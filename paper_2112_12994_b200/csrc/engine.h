@@ -51,6 +51,7 @@ struct tf_context {
   int64_t n = 0;
   // LSAR state
   tfe::DBuf<double> s, r, chunkA, chunkB, tileA, tileB, OT, scal, Rhist, Shist, phi, coefs, taus;
+  tfe::DBuf<int> guide;  // draw guide table (k_lag_scan)
   tfe::DBuf<int64_t> idx, fidx, idx_hist;
   tfe::DBuf<double> wts, fw, w_hist;
   tfe::DBuf<int> status, method;

@@ -7,10 +7,13 @@
 // B_c = sum r_q^2, plus per-2048-row tile totals.  Sampling lag q+1 is then
 //   k_lag_scan : single CTA.  R_q = sum B_t (fixed tree), tile masses
 //                S_t = A_t + B_t / R_q, exclusive tile prefix OT, total S.
-//   k_draw     : one warp per draw t.  u_t = uniform01 of draw t of
+//                It also fills a guide table: the first tile of each of G
+//                equal buckets of [0, S).
+//   k_draw     : one group of 8 lanes per draw t (4 draws per warp).  u_t = uniform01 of draw t of
 //                Rng(derive_seed(seed, p)) (bit-identical to the reference),
-//                v = u_t * S; k-ary search of OT (largest tile with OT <= v),
-//                then a sequential scan of the tile's 64 chunk masses and of
+//                v = u_t * S; the guide table brackets the tile (largest
+//                tile with OT <= v; usually one 32-wide probe), then
+//                warp scans of the tile's 64 chunk masses and of
 //                the chunk's 32 row masses -- "first cumulative mass > v",
 //                i.e. std::upper_bound on the CDF.  Row masses are computed
 //                with the exact expression the next pass stores, so the
@@ -48,10 +51,23 @@ enum : int {
 constexpr int kScanThreads = 1024;
 
 // scal[0] = R_q, scal[1] = S (total mass for lag q+1)
+// Guide table for the draws' tile search (inverse transform with a guide
+// table): G equal buckets of [0, S), bucket(x) = min(G - 1, (int)(x * (G / S))),
+// first[b] = smallest tile T with bucket(OT[T]) >= b (first[G] = ntile).
+// bucket() is monotone, so a draw v in bucket b has its tile in
+// [max(0, first[b] - 1), first[b + 1]) -- exact, no tolerance.
+constexpr int kGuideMax = 8192;
+__host__ __device__ inline int guide_buckets(int64_t ntile) { return (int)min(ntile, (int64_t)kGuideMax); }
+__device__ __forceinline__ int guide_bucket(double x, double gscale, int G) {
+  const double f = x * gscale;
+  return f >= (double)(G - 1) ? G - 1 : (f > 0.0 ? (int)f : 0);
+}
+
 __global__ void __launch_bounds__(kScanThreads)
     k_lag_scan(const double* __restrict__ tA, const double* __restrict__ tB, int64_t ntile,
                double* __restrict__ OT, double* scal, double* Rhist, double* Shist, int lag,
-               int check_r, int* status, int unit_r = 0, const double* r_fixed = nullptr) {
+               int check_r, int* status, int unit_r = 0, const double* r_fixed = nullptr,
+               int* __restrict__ guide = nullptr) {
   __shared__ double red[kScanThreads];
   __shared__ double wsum[32];
   const int tid = threadIdx.x;
@@ -91,6 +107,25 @@ __global__ void __launch_bounds__(kScanThreads)
     OT[t] = off;
     off += tA[t] + tB[t] / R;
   }
+  if (guide) {
+    // each thread scatters the bucket starts of its own tiles: tile t is the
+    // first tile of buckets (bucket(OT[t-1]), bucket(OT[t])]
+    __shared__ int last_b[kScanThreads];
+    const int G = guide_buckets(ntile);
+    const double gscale = S > 0.0 ? (double)G / S : 0.0;
+    last_b[tid] = e > b ? guide_bucket(OT[e - 1], gscale, G) : -2;
+    __syncthreads();
+    if (e > b) {
+      int bprev = tid > 0 ? last_b[tid - 1] : -1;
+      for (int64_t t = b; t < e; ++t) {
+        const int bt = guide_bucket(OT[t], gscale, G);
+        for (int k = bprev + 1; k <= bt; ++k) guide[k] = (int)t;
+        bprev = bt;
+      }
+      if (e == ntile)
+        for (int k = bprev + 1; k <= G; ++k) guide[k] = (int)ntile;
+    }
+  }
   if (tid == 0) {
     scal[0] = R;
     scal[1] = S;
@@ -109,6 +144,7 @@ struct DrawArgs {
   int64_t c;
   const double* scal;   // R, S
   const double* OT;
+  const int* guide;     // k_lag_scan's guide table (nullable: full k-ary search)
   int64_t ntile;
   const double* tA;
   const double* tB;
@@ -129,92 +165,173 @@ struct DrawArgs {
 };
 
 constexpr int kDrawThreads = 256;
+constexpr int kDrawL = 8;                    // lanes per draw
+constexpr int kDrawPerWarp = 32 / kDrawL;    // draws in flight per warp
+constexpr int kDrawPerCta = kDrawThreads / kDrawL;
+
+// lane-group primitives (groups of kDrawL lanes; every lane of a group takes
+// the same path, so the group mask is exact)
+struct DrawGroup {
+  unsigned mask;
+  int sl;  // lane within the group
+  __device__ __forceinline__ DrawGroup() {
+    const int lane = threadIdx.x & 31;
+    sl = lane % kDrawL;
+    mask = ((1u << kDrawL) - 1u) << (lane - sl);
+  }
+  __device__ __forceinline__ unsigned ballot(bool p) const {
+    return (__ballot_sync(mask, p) & mask) >> ((threadIdx.x & 31) - sl);
+  }
+  __device__ __forceinline__ double bcast(double x, int src) const { return __shfl_sync(mask, x, src, kDrawL); }
+  __device__ __forceinline__ int bcast(int x, int src) const { return __shfl_sync(mask, x, src, kDrawL); }
+  __device__ __forceinline__ double incl_scan(double x) const {  // fixed order
+#pragma unroll
+    for (int o = 1; o < kDrawL; o <<= 1) {
+      const double y = __shfl_up_sync(mask, x, o, kDrawL);
+      if (sl >= o) x += y;
+    }
+    return x;
+  }
+};
+
+// First entry (in order) whose cumulative mass exceeds v with positive mass,
+// over NPL consecutive entries per lane (lane sl holds entries NPL sl ..):
+// returns the entry index or -1, the mass before it in *before, and the last
+// positive entry in *lastpos (-1 if none).  Cumulative sums: per-lane
+// sequential prefix + group scan of the lane totals (fixed order).
+template <int NPL>
+__device__ __forceinline__ int group_pick(const DrawGroup& g, const double (&m)[NPL], double v, double* before,
+                                          int* lastpos) {
+  double loc[NPL];
+  double acc = 0.0;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    acc += m[j];
+    loc[j] = acc;
+  }
+  const double excl = g.incl_scan(acc) - acc;
+  int jh = -1, jp = -1;
+#pragma unroll
+  for (int j = NPL - 1; j >= 0; --j) {
+    if (m[j] > 0.0) {
+      if (excl + loc[j] > v) jh = j;
+      if (jp < 0) jp = j;
+    }
+  }
+  const unsigned hit = g.ballot(jh >= 0), pos = g.ballot(jp >= 0);
+  *lastpos = pos ? NPL * (31 - __clz(pos)) + g.bcast(jp, 31 - __clz(pos)) : -1;
+  if (!hit) return -1;
+  const int src = __ffs(hit) - 1;
+  const int j = g.bcast(jh, src);
+  double b = 0.0;
+#pragma unroll
+  for (int k = 0; k < NPL; ++k)
+    if (k == jh) b = excl + loc[k] - m[k];
+  *before = g.bcast(b, src);
+  return NPL * src + j;
+}
 
 __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t t = (int64_t)blockIdx.x * (kDrawThreads / 32) + wib;
-  if (t >= a.c) return;
+  const DrawGroup g;
+  const int64_t t = (int64_t)blockIdx.x * kDrawPerCta + (threadIdx.x / kDrawL);
+  if (t >= a.c) return;  // group-uniform
   const double R = a.scal[0], S = a.scal[1];
+  const double invR = 1.0 / R;
   const uint64_t seed = a.seed_ptr ? *a.seed_ptr : a.seed;
   double v = rng_uniform01(seed, (uint64_t)t) * (a.shard ? a.s_total : S);
   if (a.shard) {
     v -= a.offset;
     const bool mine = v >= 0.0 && (v < S || a.is_last);
-    if (lane == 0) a.accept[t] = mine ? 1 : 0;
+    if (g.sl == 0) a.accept[t] = mine ? 1 : 0;
     if (!mine) return;
   }
-  // ---- tile: largest T with OT[T] <= v ----
+  // ---- tile: largest T with OT[T] <= v (the guide table brackets it) ----
   int64_t lo = 0, hi = a.ntile;
-  while (hi - lo > 32) {
-    const int64_t stride = (hi - lo + 31) / 32;
-    const int64_t pos = lo + (int64_t)lane * stride;
-    const bool pr = pos < hi && a.OT[pos] <= v;
-    int cnt = __popc(__ballot_sync(0xffffffffu, pr));
+  if (a.guide) {
+    const int G = guide_buckets(a.ntile);
+    const int gb = guide_bucket(v, S > 0.0 ? (double)G / S : 0.0, G);
+    lo = max(0, a.guide[gb] - 1);
+    hi = max(lo + 1, (int64_t)a.guide[gb + 1]);
+  }
+  while (hi - lo > kDrawL) {  // k-ary narrowing (OT nondecreasing: the predicate is a prefix)
+    const int64_t stride = (hi - lo + kDrawL - 1) / kDrawL;
+    const int64_t pos = lo + (int64_t)g.sl * stride;
+    int cnt = __popc(g.ballot(pos < hi && a.OT[pos] <= v));
     if (cnt == 0) cnt = 1;
     lo = lo + (int64_t)(cnt - 1) * stride;
     hi = min(lo + stride, hi);
   }
+  double ot_lo;
   {
-    const int64_t pos = lo + lane;
-    const bool pr = pos < hi && a.OT[pos] <= v;
-    int cnt = __popc(__ballot_sync(0xffffffffu, pr));
+    const int64_t pos = lo + g.sl;
+    const double ot = pos < hi ? a.OT[pos] : 0.0;
+    int cnt = __popc(g.ballot(pos < hi && ot <= v));
     if (cnt == 0) cnt = 1;
+    ot_lo = g.bcast(ot, cnt - 1);
     lo = lo + cnt - 1;
   }
   int64_t T = lo;
-  // a tile with zero mass can only be hit through the end guard: walk back
-  // (sketch.cpp:54-55 skips zero-mass rows backwards the same way)
-  while (T > 0 && !(a.tA[T] + a.tB[T] / R > 0.0)) --T;
-  double v1 = v - a.OT[T];
-  // ---- chunk within tile, then row within chunk: warp-parallel CDF search.
-  //      Inclusive warp scans of the masses (fixed tree order); the pick is
-  //      the first position whose cumulative mass exceeds v with positive
-  //      mass (sketch.cpp:45-55 upper_bound + zero-mass skip); past the end,
-  //      the last positive entry (end guard).
+  double v1 = v - ot_lo;
+  // ---- chunk within the tile, then row within the chunk: upper_bound with
+  //      the zero-mass skip (sketch.cpp:45-55); past the end, the last
+  //      positive entry (end guard).  A tile with zero mass can only be
+  //      reached through the end guard (the last tiles): walk back to the
+  //      last tile with positive mass and take its last positive entry.
+  constexpr int CPL = kChunksPerTile / kDrawL;  // chunks per lane
   const int64_t nchunk = (a.w + kChunk - 1) / kChunk;
-  const int64_t cb = T * kChunksPerTile;
-  const int nch = (int)min((int64_t)kChunksPerTile, nchunk - cb);
-  int chosen = -1;
-  double vrow = 0.0;
-  {
-    double base = 0.0;
-    int lastpos = -1;
-    for (int h = 0; h < 2 && chosen < 0; ++h) {
-      const int k = 32 * h + lane;
-      const double m = k < nch ? a.chunkA[cb + k] + a.chunkB[cb + k] / R : 0.0;
-      const double inc = base + warp_incl_scan(m);
-      const unsigned hit = __ballot_sync(0xffffffffu, inc > v1 && m > 0.0);
-      const unsigned pos = __ballot_sync(0xffffffffu, m > 0.0);
-      if (pos) lastpos = 32 * h + 31 - __clz(pos);
-      if (hit) {
-        const int src = __ffs(hit) - 1;
-        chosen = 32 * h + src;
-        vrow = v1 - __shfl_sync(0xffffffffu, inc - m, src);
-      }
-      base = __shfl_sync(0xffffffffu, inc, 31);
+  int64_t cb;
+  int chosen;
+  double vrow;
+  for (;;) {
+    cb = T * kChunksPerTile;
+    const int nch = (int)min((int64_t)kChunksPerTile, nchunk - cb);
+    double m[CPL];
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int k = CPL * g.sl + j;
+      m[j] = k < nch ? fma(a.chunkB[cb + k], invR, a.chunkA[cb + k]) : 0.0;
     }
-    if (chosen < 0) {
+    double before = 0.0;
+    int lastpos;
+    chosen = group_pick<CPL>(g, m, v1, &before, &lastpos);
+    if (chosen >= 0) {
+      vrow = v1 - before;
+      break;
+    }
+    if (lastpos >= 0 || T == 0) {
       chosen = lastpos < 0 ? nch - 1 : lastpos;
-      vrow = __longlong_as_double(0x7ff0000000000000ll);  // +inf: take last positive row
+      vrow = __longlong_as_double(0x7ff0000000000000ll);  // +inf: take the last positive row
+      break;
     }
+    --T;  // zero-mass tile (end guard): walk back
+    v1 = __longlong_as_double(0x7ff0000000000000ll);
   }
+  constexpr int RPL = kChunk / kDrawL;  // rows per lane
   const int64_t r0 = (cb + chosen) * kChunk;
-  const int64_t row = r0 + lane;
-  double mass = 0.0;
-  if (row < a.w) {
-    if (a.r) {
-      const double rv = a.r[row];
-      mass = a.s[row] + (rv * rv) / R;
-    } else {
-      mass = a.s[row] + 0.0 / R;  // same expression as the partials (r = 0)
+  double mass[RPL];
+#pragma unroll
+  for (int j = 0; j < RPL; ++j) {
+    const int64_t row = r0 + RPL * g.sl + j;
+    mass[j] = 0.0;
+    if (row < a.w) {
+      if (a.r) {
+        const double rv = a.r[row];
+        mass[j] = fma(rv * rv, invR, a.s[row]);  // exactly the s_{q+1} the next pass stores
+      } else {
+        mass[j] = a.s[row];
+      }
     }
   }
-  const double incr = warp_incl_scan(mass);
-  const unsigned hitr = __ballot_sync(0xffffffffu, incr > vrow && mass > 0.0);
-  const unsigned posr = __ballot_sync(0xffffffffu, mass > 0.0);
-  const int pick = hitr ? __ffs(hitr) - 1 : (posr ? 31 - __clz(posr) : 0);
-  const double mp = __shfl_sync(0xffffffffu, mass, pick);
-  if (lane == 0) {
+  double before = 0.0;
+  int lastr;
+  int pick = group_pick<RPL>(g, mass, vrow, &before, &lastr);
+  if (pick < 0) pick = lastr >= 0 ? lastr : 0;
+  double mp = 0.0;
+#pragma unroll
+  for (int j = 0; j < RPL; ++j)
+    if (RPL * g.sl + j == pick) mp = mass[j];
+  mp = g.bcast(mp, pick / RPL);
+  if (g.sl == 0) {
     a.idx[t] = r0 + pick;
     a.wts[t] = 1.0 / sqrt((double)a.c * (mp / (a.shard ? a.s_total : S)));
   }

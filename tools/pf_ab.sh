@@ -1,1 +1,2 @@
-for f in 1 4 16 1000; do echo "== F=$f"; TF_HK_F=$f python tools/dbg_rh.py 2>&1 | grep "depth=-"; done
+python tools/phase_profile.py C2 100000 2>&1 | grep -E "p=|total|sample"
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -3
