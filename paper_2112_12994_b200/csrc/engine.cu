@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 #include <mutex>
+#include <numeric>
 #include <map>
 
 #include "engine.h"

@@ -94,3 +94,25 @@ def test_sharded_gpu_world1_matches_sweep():
     assert fit.p_star == ref.p_star
     assert fit.local_draws == [c] * p_bar
     eng.close()
+
+
+@pytest.mark.gpu
+def test_sharded_gpu_nccl_world1_matches_sweep():
+    # the NCCL collective path (TorchComm on device tensors) end to end; only
+    # one GPU is available to this build, so world size 1
+    import torch.distributed as dist
+    import paper_2112_12994_b200 as tf
+    from paper_2112_12994_b200 import shard
+    y = _series(30000, 8)
+    p_bar, c, seed = 16, 1500, 3
+    eng = tf.Engine(0)
+    ref = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, seed, engine=eng)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1)
+    try:
+        comm = shard.TorchComm()
+        fit = shard.lsar_fit_sharded(y, p_bar, c, seed, comm=comm, backend=shard.GpuShard(engine=eng))
+    finally:
+        dist.destroy_process_group()
+    rel = np.max(np.abs(fit.taus - np.array(ref.pacf.taus)) / np.maximum(np.abs(ref.pacf.taus), 1e-3))
+    assert rel < 1e-9 and fit.p_star == ref.p_star
+    eng.close()
