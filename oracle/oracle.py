@@ -346,6 +346,40 @@ def exact_fit(y, p_bar: int) -> Fit:
                bound=1.96 / np.sqrt(y.size - p_bar))
 
 
+# ---------------------------------------------------------------- SRHT (sketch.cpp:103-239)
+def hadamard_apply(x) -> np.ndarray:
+    v = f64(x).copy()
+    _check(lib().orc_hadamard_apply(_p(v), C.c_int64(v.size)))
+    return v
+
+
+def srht_sample_count(n: int, d: int, epsilon: float):
+    fv = C.c_double(0.0); c = C.c_int64(0); capped = C.c_int(0)
+    _check(lib().orc_srht_sample_count(C.c_int64(n), C.c_int64(d), C.c_double(epsilon), C.byref(fv),
+                                       C.byref(c), C.byref(capped)))
+    return fv.value, c.value, bool(capped.value)
+
+
+def srht_solve(a, b, c: int, seed: int):
+    """a: rows x cols; returns (x, sampled a (c x cols), sampled b)."""
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    b = f64(b)
+    rows, cols = a.shape
+    x = np.zeros(cols); sa = np.zeros((c, cols), order="F"); sb = np.zeros(c)
+    _check(lib().orc_srht_solve(_p(a.ravel(order="F")), C.c_int64(rows), C.c_int64(cols), _p(b), C.c_int64(c),
+                                C.c_uint64(seed), _p(x), _p(sa.ravel(order="F")), _p(sb)))
+    return x, sa, sb
+
+
+def srht_fit(y, p_bar: int, c: int, seed: int) -> Fit:
+    y = f64(y)
+    taus = np.zeros(max(p_bar, 1)); coefs = np.zeros(max(p_bar, 1) * (max(p_bar, 1) + 1) // 2)
+    pstar = C.c_int(0)
+    _check(lib().orc_srht_fit(_p(y), C.c_int64(y.size), C.c_int(p_bar), C.c_int64(c), C.c_uint64(seed),
+                              _p(taus), _p(coefs), C.byref(pstar)))
+    return Fit(taus=taus, coefs=_unpack(coefs, p_bar), p_star=pstar.value, bound=1.96 / np.sqrt(c))
+
+
 # ---------------------------------------------------------------- generators
 def random_stationary_ar(p: int, seed: int) -> np.ndarray:
     phi = np.empty(p)

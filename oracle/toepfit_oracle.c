@@ -1037,6 +1037,158 @@ int orc_exact_fit(const double* y, int64_t n, int p_bar, double* taus, double* c
 }
 
 /* ======================================================================
+ * SRHT path: sketch.cpp:103-239, bench.cpp:50-72
+ * ==================================================================== */
+#define INV_SQRT2 0.70710678118654752440
+
+/* sketch.cpp:107-120: in place, strides 1, 2, 4, ... (n a power of two) */
+int orc_hadamard_apply(double* x, int64_t n) {
+  if (n == 0 || (n & (n - 1)) != 0) return fail(ORC_USAGE, "transform length must be a power of two");
+  for (int64_t h = 1; h < n; h <<= 1)
+    for (int64_t i = 0; i < n; i += 2 * h)
+      for (int64_t j = i; j < i + h; ++j) {
+        const double a = x[j], b = x[j + h];
+        x[j] = (a + b) * INV_SQRT2;
+        x[j + h] = (a - b) * INV_SQRT2;
+      }
+  return ORC_OK;
+}
+
+/* sketch.cpp:145-163 (PartialHadamard::recurse): largest stride first, only
+ * the halves that hold requested rows; idx sorted unique, relative to x */
+static void partial_recurse(const double* x, int64_t len, const int64_t* idx, int64_t nidx, double* out,
+                            const int64_t* outpos, double* scratch) {
+  if (nidx == 0) return;
+  if (len == 1) {
+    for (int64_t r = 0; r < nidx; ++r) out[outpos[r]] = x[0];
+    return;
+  }
+  const int64_t h = len / 2;
+  int64_t mid = 0;
+  while (mid < nidx && idx[mid] < h) ++mid;
+  double* buf = scratch;  /* this level's buffer (len / 2), deeper levels after it */
+  if (mid > 0) {
+    for (int64_t i = 0; i < h; ++i) buf[i] = (x[i] + x[i + h]) * INV_SQRT2;
+    partial_recurse(buf, h, idx, mid, out, outpos, scratch + h);
+  }
+  if (mid < nidx) {
+    for (int64_t i = 0; i < h; ++i) buf[i] = (x[i] - x[i + h]) * INV_SQRT2;
+    int64_t* shifted = XMALLOC(int64_t, nidx - mid);
+    for (int64_t r = mid; r < nidx; ++r) shifted[r - mid] = idx[r] - h;
+    partial_recurse(buf, h, shifted, nidx - mid, out, outpos + mid, scratch + h);
+    free(shifted);
+  }
+}
+
+/* sketch.cpp:165-185 */
+int orc_srht_sample_count(int64_t n, int64_t d, double epsilon, double* formula_value, int64_t* c,
+                          int* capped) {
+  if (!(n > d && d >= 1)) return fail(ORC_USAGE, "need n > d >= 1");
+  if (!(epsilon > 0.0 && epsilon < 1.0)) return fail(ORC_USAGE, "epsilon must lie in (0, 1)");
+  const double nd = (double)n * (double)d;
+  const double log_term = log(40.0 * nd);
+  const double branch1 = 48.0 * 48.0 * (double)d * log_term * log(100.0 * 100.0 * d * log_term);
+  const double branch2 = 40.0 * (double)d * log_term / epsilon;
+  *formula_value = branch1 > branch2 ? branch1 : branch2;
+  const double rounded = ceil(*formula_value);
+  if (rounded > (double)n) {
+    *c = n;
+    *capped = 1;
+  } else {
+    *c = (int64_t)rounded;
+    *capped = 0;
+  }
+  return ORC_OK;
+}
+
+static uint64_t bit_ceil_u64(uint64_t v) {
+  uint64_t n = 1;
+  while (n < v) n <<= 1;
+  return n;
+}
+
+/* sketch.cpp:187-239.  a: rows x cols, column-major.  sa / sb (optional)
+ * receive the sampled, weighted c x cols system (column-major) */
+int orc_srht_solve(const double* a, int64_t n0, int64_t d, const double* b, int64_t c, uint64_t seed,
+                   double* x, double* sa, double* sb) {
+  if (n0 < d) return fail(ORC_USAGE, "need rows >= columns");
+  if (c < d) return fail(ORC_USAGE, "sample count below column count");
+  const int64_t n = (int64_t)bit_ceil_u64((uint64_t)n0);
+  orc_rng rng;
+  orc_rng_init(&rng, seed);
+  double* sign = XMALLOC(double, n0);
+  for (int64_t i = 0; i < n0; ++i) sign[i] = (orc_rng_next(&rng) >> 63) ? 1.0 : -1.0;
+  int64_t* draws = XMALLOC(int64_t, c);
+  for (int64_t t = 0; t < c; ++t) draws[t] = (int64_t)orc_rng_below(&rng, (uint64_t)n);
+  int64_t* uniq = XMALLOC(int64_t, c);
+  for (int64_t t = 0; t < c; ++t) uniq[t] = draws[t];
+  qsort(uniq, (size_t)c, sizeof(int64_t), cmp_i64);
+  int64_t nu = 0;
+  for (int64_t t = 0; t < c; ++t)
+    if (nu == 0 || uniq[t] != uniq[nu - 1]) uniq[nu++] = uniq[t];
+  int64_t* outpos = XMALLOC(int64_t, nu);
+  for (int64_t k = 0; k < nu; ++k) outpos[k] = k;
+  double* padded = XMALLOC(double, n);
+  double* scratch = XMALLOC(double, n);
+  double* vals = XMALLOC(double, nu);
+  int64_t* posof = XMALLOC(int64_t, c);
+  for (int64_t t = 0; t < c; ++t) { /* lower_bound in uniq */
+    int64_t lo = 0, hi = nu;
+    while (lo < hi) {
+      const int64_t m = (lo + hi) / 2;
+      if (uniq[m] < draws[t]) lo = m + 1;
+      else hi = m;
+    }
+    posof[t] = lo;
+  }
+  const double w = sqrt((double)n / (double)c);
+  double* as = sa ? sa : XMALLOC(double, c * d);
+  double* bs = sb ? sb : XMALLOC(double, c);
+  for (int64_t j = 0; j <= d; ++j) {
+    const double* col = j < d ? a + j * n0 : b;
+    for (int64_t i = 0; i < n0; ++i) padded[i] = sign[i] * col[i];
+    for (int64_t i = n0; i < n; ++i) padded[i] = 0.0;
+    partial_recurse(padded, n, uniq, nu, vals, outpos, scratch);
+    double* dst = j < d ? as + j * c : bs;
+    for (int64_t t = 0; t < c; ++t) dst[t] = w * vals[posof[t]];
+  }
+  const int rc = orc_solve_exact(as, c, d, bs, x, NULL, NULL);
+  if (!sa) free(as);
+  if (!sb) free(bs);
+  free(sign); free(draws); free(uniq); free(outpos); free(padded); free(scratch); free(vals); free(posof);
+  return rc;
+}
+
+/* bench.cpp:50-72 */
+int orc_srht_fit(const double* y, int64_t n, int p_bar, int64_t c, uint64_t seed, double* taus,
+                 double* coefs_packed, int* p_star) {
+  if (p_bar < 1) return fail(ORC_USAGE, "maximum lag must be at least 1");
+  if (n <= (int64_t)p_bar + 1) return fail(ORC_DATA, "series too short for maximum lag %d", p_bar);
+  if (c < p_bar) return fail(ORC_USAGE, "sample count below maximum lag");
+  int64_t off = 0;
+  for (int h = 1; h <= p_bar; ++h) {
+    const int64_t m = n - h;
+    double* a = XMALLOC(double, m * h);
+    double* phi = XMALLOC(double, h);
+    for (int j = 0; j < h; ++j)
+      for (int64_t i = 0; i < m; ++i) a[(int64_t)j * m + i] = y[h - 1 - j + i];
+    const int rc = orc_srht_solve(a, m, h, y + h, c, orc_derive_seed(seed, (uint64_t)h), phi, NULL, NULL);
+    if (rc != ORC_OK) {
+      free(a);
+      free(phi);
+      return rc;
+    }
+    taus[h - 1] = phi[h - 1];
+    if (coefs_packed) memcpy(coefs_packed + off, phi, sizeof(double) * (size_t)h);
+    off += h;
+    free(a);
+    free(phi);
+  }
+  if (p_star) *p_star = orc_select_order(taus, p_bar, 1.96 / sqrt((double)c));
+  return ORC_OK;
+}
+
+/* ======================================================================
  * series.cpp:58-107 -- reference generators (test inputs only)
  * ==================================================================== */
 int orc_partials_to_ar(const double* partials, int p, double* phi) {
