@@ -13,6 +13,8 @@
  *   tf_solve_sampled   <- solve_compressed(apply_sample(...))                 sketch.hpp:63-64, sketch.cpp:96-101
  *   tf_select_order    <- int select_order(const PACFResult&)                 toeplitz.hpp:100, toeplitz.cpp:133-138
  *   tf_exact_sweep     <- exact per-lag OLS fit (run_fit "exact")              bench.cpp:27-48
+ *   tf_srht_sweep      <- FitResult srht_fit(series, p_bar, c, seed)          bench.cpp:50-72, sketch.cpp:187-239
+ *   tf_hadamard        <- void hadamard_apply(std::span<double>)              sketch.hpp, sketch.cpp:107-120
  *
  * Conventions (mirroring the reference): indices are 0-based int64, series
  * and coefficients are fp64; errors never cross the ABI as exceptions --
@@ -127,6 +129,17 @@ tf_status tf_rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cf
  * p_star uses the bound 1.96 / sqrt(n - p_bar). */
 tf_status tf_exact_sweep(tf_context* ctx, int p_bar, double* taus, double* coefs_packed, double* lag_seconds,
                          int* p_star);
+
+/* Subsampled randomized Hadamard transform sweep (bench.cpp:50-72 srht_fit;
+ * sketch.cpp:187-239 srht_solve per lag with seed derive_seed(seed, h)).
+ * Outputs as tf_lsar_sweep; p_star uses the bound 1.96 / sqrt(c).  Errors:
+ * TF_USAGE for p_bar < 1 or c < p_bar, TF_DATA for n <= p_bar + 1. */
+tf_status tf_srht_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, double* taus, double* coefs_packed,
+                        double* lag_seconds, int* p_star);
+
+/* In-place orthonormal Walsh-Hadamard transform of a host vector of
+ * power-of-two length (sketch.cpp:107-120; TF_USAGE otherwise). */
+tf_status tf_hadamard(tf_context* ctx, double* x, int64_t n);
 
 /* ---- single operations on host buffers (tests, integration) ---- */
 tf_status tf_residuals(tf_context* ctx, const double* y, int64_t n_used, int p, const double* phi,

@@ -225,6 +225,32 @@ inline FitResult rh_fit(const TimeSeries& series, int p_bar, std::int64_t c, std
   return rh_fit(series, p_bar, c, nullptr, seed);
 }
 
+// exact per-lag OLS (bench.cpp:27-48); bound 1.96 / sqrt(n - p_bar)
+inline FitResult exact_fit(const TimeSeries& series, int p_bar) {
+  gpu::Context& g = gpu::context();
+  tf_context* ctx = g.get();
+  g.upload(series);
+  const int pb = p_bar > 0 ? p_bar : 1;
+  std::vector<double> taus(pb), packed((std::size_t)pb * (pb + 1) / 2), secs(pb);
+  int p_star = 0;
+  gpu::raise(tf_exact_sweep(ctx, p_bar, taus.data(), packed.data(), secs.data(), &p_star), ctx);
+  FitResult f = gpu::finish(PacfMethod::exact, p_bar, 1, taus, packed, std::move(secs), p_star, 0.0);
+  f.pacf.bound = 1.96 / std::sqrt((double)series.size() - p_bar);
+  return f;
+}
+
+// subsampled randomized Hadamard transform fit (bench.cpp:50-72)
+inline FitResult srht_fit(const TimeSeries& series, int p_bar, std::int64_t c, std::uint64_t seed) {
+  gpu::Context& g = gpu::context();
+  tf_context* ctx = g.get();
+  g.upload(series);
+  const int pb = p_bar > 0 ? p_bar : 1;
+  std::vector<double> taus(pb), packed((std::size_t)pb * (pb + 1) / 2), secs(pb);
+  int p_star = 0;
+  gpu::raise(tf_srht_sweep(ctx, p_bar, c, seed, taus.data(), packed.data(), secs.data(), &p_star), ctx);
+  return gpu::finish(PacfMethod::srht, p_bar, c, taus, packed, std::move(secs), p_star, 0.0);
+}
+
 inline int select_order(const PACFResult& pacf) {
   return tf_select_order(pacf.taus.data(), (int)pacf.taus.size(), pacf.bound);
 }

@@ -6,9 +6,11 @@ libtoepfit_b200.so (hand-written sm_100a kernels); see DESIGN.md.
 from .api import (CudaError, DataError, Engine, FitResult, NumericalError, PACFResult, RHConfig,  # noqa: F401
                   RunReport, TimeSeries, UsageError, default_engine, derive_seed, lsar_fit,
                   report_to_json, rh_fit, run_fit, select_order, exact_fit, fit_many,
-                  load_series_bin, save_series_bin)
+                  load_series_bin, save_series_bin, srht_fit, hadamard_apply,
+                  srht_sample_count, SrhtCount)
 
 __all__ = ["TimeSeries", "FitResult", "PACFResult", "RHConfig", "RunReport", "Engine",
            "UsageError", "DataError", "NumericalError", "CudaError", "lsar_fit", "rh_fit",
            "run_fit", "report_to_json", "select_order", "derive_seed", "default_engine",
-           "exact_fit", "fit_many", "load_series_bin", "save_series_bin"]
+           "exact_fit", "fit_many", "load_series_bin", "save_series_bin", "srht_fit",
+           "hadamard_apply", "srht_sample_count", "SrhtCount"]

@@ -48,7 +48,7 @@ EXPORTS = [
     "tf_upload_series_device", "tf_lsar_sweep", "tf_rh_sweep", "tf_residuals", "tf_sample_rows",
     "tf_apply_sample", "tf_solve_sampled", "tf_select_order", "tf_derive_seed",
     "tf_probe_fp64_peak", "tf_shard_open", "tf_shard_pass", "tf_shard_sample", "tf_shard_gram",
-    "tf_shard_factor", "tf_shard_finish", "tf_tpu_size", "tf_sweep_span", "tf_exact_sweep", "tf_generate_series", "tf_download_series",
+    "tf_shard_factor", "tf_shard_finish", "tf_tpu_size", "tf_sweep_span", "tf_exact_sweep", "tf_srht_sweep", "tf_hadamard", "tf_generate_series", "tf_download_series",
 ]
 
 _lib = None
@@ -94,6 +94,8 @@ def lib():
     L.tf_shard_finish.argtypes = [C.c_void_p, C.c_int, _f64p, _f64p]
     L.tf_sweep_span.argtypes = [C.c_void_p, C.c_void_p, _f64p, _f64p]
     L.tf_exact_sweep.argtypes = [C.c_void_p, C.c_int, _f64p, _f64p, _f64p, _i32p]
+    L.tf_srht_sweep.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_uint64, _f64p, _f64p, _f64p, _i32p]
+    L.tf_hadamard.argtypes = [C.c_void_p, _f64p, C.c_int64]
     L.tf_download_series.argtypes = [C.c_void_p, _f64p, C.c_int64]
     L.tf_generate_series.argtypes = [C.c_void_p, _f64p, C.c_int, C.c_int64, C.c_uint64, C.c_int, C.c_int64]
     L.tf_tpu_size.argtypes = [C.c_int]

@@ -334,6 +334,21 @@ class Engine:
                                               C.byref(pstar)))
         return taus, coefs, secs, pstar.value
 
+    def srht_sweep(self, p_bar: int, c: int, seed: int):
+        pb = max(int(p_bar), 1)
+        taus = np.zeros(pb)
+        coefs = np.zeros(pb * (pb + 1) // 2)
+        secs = np.zeros(pb)
+        pstar = C.c_int(0)
+        self._check(_abi.lib().tf_srht_sweep(self._ctx, int(p_bar), int(c), int(seed) & (2**64 - 1), ptr(taus),
+                                             ptr(coefs), ptr(secs), C.byref(pstar)))
+        return taus, coefs, secs, pstar.value
+
+    def hadamard(self, x) -> np.ndarray:
+        v = np.array(x, dtype=np.float64).ravel()
+        self._check(_abi.lib().tf_hadamard(self._ctx, ptr(v), v.size))
+        return v
+
     def sweep_span(self, ref: "Engine"):
         """(start_ms, end_ms) of this engine's last sweep relative to the start
         of ref's last sweep (device events)."""
@@ -453,6 +468,48 @@ def exact_fit(series: TimeSeries, p_bar: int, *, engine: Engine | None = None) -
     return fit
 
 
+def srht_fit(series: TimeSeries, p_bar: int, c: int, seed: int, *, engine: Engine | None = None) -> FitResult:
+    """Subsampled randomized Hadamard transform fit (bench.cpp:50-72): lag h
+    solves the SRHT sketch (sketch.cpp:187-239, seed derive_seed(seed, h)) of
+    its n - h row system on the GPU."""
+    eng = engine or default_engine()
+    eng.upload(series)
+    taus, coefs, secs, pstar = eng.srht_sweep(p_bar, c, seed)
+    fit = _finish("srht", taus, coefs, secs, pstar, p_bar, c, 0.0, None)
+    fit.pacf.bound = 1.96 / math.sqrt(float(c))
+    return fit
+
+
+def hadamard_apply(x, *, engine: Engine | None = None) -> np.ndarray:
+    """Orthonormal Walsh-Hadamard transform (sketch.cpp:107-120) on the GPU;
+    UsageError unless the length is a power of two."""
+    return (engine or default_engine()).hadamard(x)
+
+
+@dataclass
+class SrhtCount:
+    c: int
+    formula_value: float
+    capped: bool
+
+
+def srht_sample_count(n: int, d: int, epsilon: float) -> SrhtCount:
+    """sketch.cpp:165-185 (host arithmetic)."""
+    if not (n > d >= 1):
+        raise UsageError("need n > d >= 1")
+    if not (0.0 < epsilon < 1.0):
+        raise UsageError("epsilon must lie in (0, 1)")
+    nd = float(n) * float(d)
+    log_term = math.log(40.0 * nd)
+    branch1 = 48.0 * 48.0 * float(d) * log_term * math.log(100.0 * 100.0 * d * log_term)
+    branch2 = 40.0 * float(d) * log_term / epsilon
+    fv = max(branch1, branch2)
+    rounded = math.ceil(fv)
+    if rounded > n:
+        return SrhtCount(int(n), fv, True)
+    return SrhtCount(int(rounded), fv, False)
+
+
 def fit_many(series_list, method: str, p_bar: int, c: int, seeds, *, workers: int = 8,
              device: int = 0, config: RHConfig | None = None) -> list:
     """Independent fits (many series, or many seeds over one series -- the
@@ -525,9 +582,7 @@ class RunReport:
 
 def run_fit(series: TimeSeries, method: str, p_bar: int, c: int, seed: int,
             with_timing: bool = True, engine: Engine | None = None) -> RunReport:
-    """bench.cpp:107-124 restricted to the GPU methods (lsar, rh)."""
-    if method == "srht":
-        raise UsageError(f"method '{method}' is outside the B200 hot path (lsar | rh | exact)")
+    """bench.cpp:107-124: exact | lsar | rh | srht, all on the GPU."""
     if method != "exact" and c < 1:
         raise UsageError(f"method '{method}' needs a sample count")
     if method == "exact":
@@ -536,6 +591,8 @@ def run_fit(series: TimeSeries, method: str, p_bar: int, c: int, seed: int,
         fit = lsar_fit(series, p_bar, c, seed, engine=engine)
     elif method == "rh":
         fit = rh_fit(series, p_bar, c, None, seed, engine=engine)
+    elif method == "srht":
+        fit = srht_fit(series, p_bar, c, seed, engine=engine)
     else:
         raise UsageError(f"unknown method '{method}'")
     if not with_timing:  # bench.cpp:76-79

@@ -24,6 +24,7 @@
 #include "k_pass.cuh"
 #include "k_rh.cuh"
 #include "k_sample.cuh"
+#include "k_srht.cuh"
 #include "k_tpu.cuh"
 
 using namespace tfk;
@@ -1681,6 +1682,178 @@ static void exact_sweep(tf_context* ctx, int p_bar, double* taus, double* coefs,
 }
 
 // ---------------------------------------------------------------------------
+// SRHT sweep (bench.cpp:50-72 srht_fit, sketch.cpp:187-239
+// srht_solve): per lag h the signed, zero-padded columns y[i + a] (forward
+// order, a = h the target) go through the Walsh-Hadamard transform on the
+// device (k_fwht_pass, largest stride first: bit-identical to the reference's
+// pruned transform), the c rows below(N) are gathered with weight sqrt(N / c)
+// into a dense c x (h + 1) system, and the compressed solve is the LSAR one
+// (preconditioned CholeskyQR; lag h - 1's factor preconditions lag h: both
+// sketches approximate the same Gram).
+static std::vector<std::pair<int, int>> fwht_passes(int m) {
+  std::vector<std::pair<int, int>> ps;
+  int rem = m;
+  while (rem > kFwhtMaxFirst) {
+    ps.push_back({rem - kFwhtMaxLevels, rem});
+    rem -= kFwhtMaxLevels;
+  }
+  if (rem > 0) ps.push_back({0, rem});
+  return ps;
+}
+
+static void fwht_columns(tf_context* ctx, double* X, int64_t N, int nb, const double* y, int64_t n0, int a0,
+                         uint64_t seed) {
+  int m = 0;
+  while (((int64_t)1 << m) < N) ++m;
+  const auto ps = fwht_passes(m);
+  for (size_t k = 0; k < ps.size(); ++k) {
+    FwhtArgs a;
+    a.X = X;
+    a.N = N;
+    a.l0 = ps[k].first;
+    a.l1 = ps[k].second;
+    a.y = k == 0 ? y : nullptr;
+    a.n0 = n0;
+    a.a0 = a0;
+    a.seed = seed;
+    const int LW = a.l0 >= 4 ? 16 : (1 << a.l0);
+    const int M = 1 << (a.l1 - a.l0);
+    const size_t smem = sizeof(double) * (size_t)M * LW;
+    smem_optin((const void*)k_fwht_pass, smem);
+    dim3 grid((unsigned)(N / ((int64_t)M * LW)), (unsigned)nb);
+    k_fwht_pass<<<grid, kFwhtThreads, smem, ctx->stream>>>(a);
+    LAUNCH_CHECK("k_fwht_pass");
+    COUNT_LAUNCH();
+  }
+}
+
+static int64_t bit_ceil64(int64_t v) {
+  int64_t n = 1;
+  while (n < v) n <<= 1;
+  return n;
+}
+
+// host below(N) draws (rng.hpp:59-66) for a lag whose device draws hit a rejection
+static void srht_host_draws(uint64_t seed, int64_t n0, int64_t N, int64_t c, std::vector<int64_t>& out) {
+  const uint64_t limit = 0ull - (uint64_t)N;
+  uint64_t t = (uint64_t)n0;
+  out.resize(c);
+  for (int64_t k = 0; k < c; ++k) {
+    uint64_t x;
+    do x = rng_draw(seed, t++);
+    while (x >= limit);
+    out[k] = (int64_t)(x & (uint64_t)(N - 1));
+  }
+}
+
+static void srht_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, double* taus, double* coefs,
+                       double* lag_seconds, int* p_star) {
+  // srht_fit argument checks (bench.cpp:50-56)
+  if (p_bar < 1) throw TfError{TF_USAGE, "maximum lag must be at least 1"};
+  if (ctx->n == 0) throw TfError{TF_USAGE, "no series uploaded"};
+  const int64_t n = ctx->n;
+  if (n <= (int64_t)p_bar + 1) throw TfError{TF_DATA, "series too short for maximum lag " + std::to_string(p_bar)};
+  if (c < p_bar) throw TfError{TF_USAGE, "sample count below maximum lag"};
+  cudaStream_t st = ctx->stream;
+  const int Kmax = p_bar + 1;
+  const int64_t Nmax = bit_ceil64(n - 1);
+  alloc_state(ctx, p_bar, 1, 1);
+  reserve_solve(ctx, c, Kmax);
+  const int64_t ldD = ldq_of(Kmax);
+  ctx->srht_D.need((size_t)c * ldD);
+  ctx->srht_draws.need(c);
+  ctx->srht_reject.need(p_bar + 1);
+  // transform batch: as many columns as fit in ~512 MB
+  const int nbmax = (int)std::max<int64_t>(1, std::min<int64_t>(Kmax, ((int64_t)512 << 20) / (Nmax * 8)));
+  ctx->srht_X.need((size_t)nbmax * Nmax);
+  ctx->rh_rest.need(2);
+  ensure_events(ctx, p_bar + 1);
+  ensure_span_events(ctx);
+  std::vector<int> host_lag(p_bar + 1, 0);  // lags whose device draws hit a rejection
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    CK(cudaMemsetAsync(ctx->status.get(), 0, 3 * sizeof(int), st));
+    CK(cudaMemsetAsync(ctx->srht_reject.get(), 0, sizeof(int) * (p_bar + 1), st));
+    CK(cudaEventRecord(ctx->ev_begin, st));
+    CK(cudaEventRecord(ctx->events[0], st));
+    for (int h = 1; h <= p_bar; ++h) {
+      const int64_t n0 = n - h;
+      const int64_t N = bit_ceil64(n0);
+      const uint64_t sh = derive_seed(seed, (uint64_t)h);
+      const int K = h + 1;
+      if (host_lag[h]) {
+        std::vector<int64_t> dr;
+        srht_host_draws(sh, n0, N, c, dr);
+        CK(cudaMemcpyAsync(ctx->srht_draws.get(), dr.data(), sizeof(int64_t) * c, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+      } else {
+        k_srht_draws<<<grid_for(c, ctx), 256, 0, st>>>(sh, n0, N, c, ctx->srht_draws.get(),
+                                                       ctx->srht_reject.get() + h);
+        LAUNCH_CHECK("k_srht_draws");
+        COUNT_LAUNCH();
+      }
+      const double w = std::sqrt((double)N / (double)c);
+      for (int a0 = 0; a0 < K; a0 += nbmax) {
+        const int nb = std::min(nbmax, K - a0);
+        fwht_columns(ctx, ctx->srht_X.get(), N, nb, ctx->y.get(), n0, a0, sh);
+        k_srht_gather<<<grid_for(c * nb, ctx), 256, 0, st>>>(ctx->srht_X.get(), N, nb, ctx->srht_draws.get(), c, w,
+                                                            ctx->srht_D.get(), ldD, a0);
+        LAUNCH_CHECK("k_srht_gather");
+        COUNT_LAUNCH();
+      }
+      SolveOut o;
+      o.phi = ctx->phi.get();
+      o.coefs = ctx->coefs.get();
+      o.coef_off = (int64_t)(h - 1) * h / 2;
+      o.taus = ctx->taus.get();
+      o.method = ctx->method.get();
+      o.lag = h;
+      o.status = ctx->status.get();
+      DenseRows ld{ctx->srht_D.get(), ldD};
+      double* Snext = (h & 1) ? ctx->sb.S1.get() : ctx->sb.S0.get();
+      const double* Sprev = (h & 1) ? ctx->sb.S0.get() : ctx->sb.S1.get();
+      solve_rows(ctx, ld, c, K, o, h >= 2 ? Sprev : nullptr, h >= 2 ? ctx->phi.get() : nullptr, Snext, 0,
+                 ctx->rh_rest.get(), ctx->rh_rest.get());
+      CK(cudaEventRecord(ctx->events[h], st));
+    }
+    CK(cudaEventRecord(ctx->ev_end, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int> rj(p_bar + 1);
+    CK(cudaMemcpy(rj.data(), ctx->srht_reject.get(), sizeof(int) * (p_bar + 1), cudaMemcpyDeviceToHost));
+    bool again = false;
+    for (int h = 1; h <= p_bar; ++h)
+      if (rj[h] && !host_lag[h]) host_lag[h] = 1, again = true;  // below() rejected (p ~ N / 2^64): redo exactly
+    if (!again) break;
+  }
+  int sth[3];
+  CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  raise_from_status(sth);
+  std::vector<double> t(p_bar);
+  CK(cudaMemcpy(t.data(), ctx->taus.get(), p_bar * sizeof(double), cudaMemcpyDeviceToHost));
+  if (taus) std::memcpy(taus, t.data(), p_bar * sizeof(double));
+  if (coefs)
+    CK(cudaMemcpy(coefs, ctx->coefs.get(), sizeof(double) * (size_t)p_bar * (p_bar + 1) / 2, cudaMemcpyDeviceToHost));
+  if (lag_seconds)
+    for (int h = 1; h <= p_bar; ++h) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ctx->events[h - 1], ctx->events[h]));
+      lag_seconds[h - 1] = ms * 1e-3;
+    }
+  if (p_star) *p_star = tf_select_order(t.data(), p_bar, 1.96 / std::sqrt((double)c));
+}
+
+// orthonormal Walsh-Hadamard transform of a host vector (sketch.cpp:107-120;
+// level order largest stride first, as the pruned transform)
+static void hadamard_host(tf_context* ctx, double* x, int64_t n) {
+  if (n < 1 || (n & (n - 1)) != 0) throw TfError{TF_USAGE, "transform length must be a power of two"};
+  cudaStream_t st = ctx->stream;
+  ctx->srht_X.need(n);
+  CK(cudaMemcpyAsync(ctx->srht_X.get(), x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  fwht_columns(ctx, ctx->srht_X.get(), n, 1, nullptr, 0, 0, 0);
+  CK(cudaMemcpyAsync(x, ctx->srht_X.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+// ---------------------------------------------------------------------------
 // On-device synthetic series: cascade of first-order AR
 // sections over counter-RNG innovations, written straight into the context's
 // series buffer (the generator the BASELINE configs describe; bench inputs of
@@ -1817,6 +1990,7 @@ void tf_destroy(tf_context* ctx) {
   if (ctx->lsar_graph.exec) cudaGraphExecDestroy(ctx->lsar_graph.exec);
   if (ctx->rh_graph.exec) cudaGraphExecDestroy(ctx->rh_graph.exec);
   if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
+  ctx->srht_X.release(); ctx->srht_D.release(); ctx->srht_draws.release(); ctx->srht_reject.release();
   ctx->y.release(); ctx->s.release(); ctx->r.release(); ctx->chunkA.release(); ctx->chunkB.release();
   ctx->tileA.release(); ctx->tileB.release(); ctx->OT.release(); ctx->guide.release(); ctx->scal.release();
   ctx->Rhist.release(); ctx->Shist.release(); ctx->phi.release(); ctx->coefs.release();
@@ -1913,6 +2087,17 @@ tf_status tf_exact_sweep(tf_context* ctx, int p_bar, double* taus, double* coefs
                          int* p_star) {
   if (!ctx) return TF_USAGE;
   return guarded(ctx, [&] { tfe::exact_sweep(ctx, p_bar, taus, coefs_packed, lag_seconds, p_star); });
+}
+
+tf_status tf_srht_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, double* taus, double* coefs_packed,
+                        double* lag_seconds, int* p_star) {
+  if (!ctx) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::srht_sweep(ctx, p_bar, c, seed, taus, coefs_packed, lag_seconds, p_star); });
+}
+
+tf_status tf_hadamard(tf_context* ctx, double* x, int64_t n) {
+  if (!ctx || !x) return TF_USAGE;
+  return guarded(ctx, [&] { tfe::hadamard_host(ctx, x, n); });
 }
 
 tf_status tf_download_series(tf_context* ctx, double* out, int64_t n) {

@@ -52,6 +52,9 @@ struct tf_context {
   // LSAR state
   tfe::DBuf<double> s, r, chunkA, chunkB, tileA, tileB, OT, scal, Rhist, Shist, phi, coefs, taus;
   tfe::DBuf<int> guide;  // draw guide table (k_lag_scan)
+  tfe::DBuf<double> srht_X, srht_D;  // SRHT: transform batch, sampled dense system
+  tfe::DBuf<int64_t> srht_draws;
+  tfe::DBuf<int> srht_reject;
   tfe::DBuf<int64_t> idx, fidx, idx_hist;
   tfe::DBuf<double> wts, fw, w_hist;
   tfe::DBuf<int> status, method;

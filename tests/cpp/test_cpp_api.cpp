@@ -35,6 +35,8 @@ int main(int argc, char** argv) {
   std::printf("{\n");
   print_fit("lsar", toepfit::lsar_fit(series, p_bar, c, seed), true);
   print_fit("rh", toepfit::rh_fit(series, p_bar, c, seed), true);
+  print_fit("srht", toepfit::srht_fit(series, p_bar, c, seed), true);
+  print_fit("exact", toepfit::exact_fit(series, p_bar), true);
   // error mapping (errors.hpp:12-29 types)
   int usage = 0, data = 0, numerical = 0;
   try {

@@ -89,8 +89,18 @@ def test_host_mirror_validation():
     bad = tf.RHConfig(base_threshold=10, sample_count=20, gaussian_rows=3)
     with pytest.raises(tf.UsageError):
         bad.validate()
-    with pytest.raises(tf.UsageError):  # outside the GPU path, rejected before any device work
-        tf.run_fit(tf.TimeSeries([1.0, 2.0, 3.0]), "srht", 1, 10, 0)
+    with pytest.raises(tf.UsageError):  # argument errors come before any device work
+        tf.run_fit(tf.TimeSeries([1.0, 2.0, 3.0]), "srht", 1, 0, 0)
+    with pytest.raises(tf.UsageError):
+        tf.run_fit(tf.TimeSeries([1.0, 2.0, 3.0]), "nope", 1, 10, 0)
+    # sample count formula: the reference's frozen regression value (test_sketch.cpp:112-125)
+    sc = tf.srht_sample_count(1 << 20, 10, 0.5)
+    assert abs(sc.formula_value - 6633578.924774391) <= 1e-12 * 6633578.924774391
+    assert sc.capped and sc.c == 1 << 20
+    assert tf.srht_sample_count(1 << 20, 10, 0.9).formula_value <= sc.formula_value
+    for args in ((5, 5, 0.5), (10, 0, 0.5), (100, 5, 0.0), (100, 5, 1.0)):
+        with pytest.raises(tf.UsageError):
+            tf.srht_sample_count(*args)
     with pytest.raises(tf.UsageError):
         tf.run_fit(tf.TimeSeries([1.0, 2.0, 3.0]), "lsar", 1, 0, 0)
 

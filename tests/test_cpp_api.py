@@ -33,5 +33,9 @@ def test_cpp_api_matches_python(tmp_path):
     assert res["lsar"]["taus"] == a.pacf.taus and res["lsar"]["p_star"] == a.p_star
     assert res["rh"]["taus"] == b.pacf.taus and res["rh"]["p_star"] == b.p_star
     assert res["lsar"]["select"] == a.p_star
+    sr = tf.srht_fit(s, 16, 900, 11, engine=eng)
+    ex = tf.exact_fit(s, 16, engine=eng)
+    assert res["srht"]["taus"] == sr.pacf.taus and res["srht"]["p_star"] == sr.p_star
+    assert res["exact"]["taus"] == ex.pacf.taus and res["exact"]["p_star"] == ex.p_star
     assert res["errors"] == {"usage": 1, "data": 1, "numerical": 1}
     eng.close()
