@@ -1690,12 +1690,15 @@ static void exact_sweep(tf_context* ctx, int p_bar, double* taus, double* coefs,
 // into a dense c x (h + 1) system, and the compressed solve is the LSAR one
 // (preconditioned CholeskyQR; lag h - 1's factor preconditions lag h: both
 // sketches approximate the same Gram).
+// level ranges from the top (largest strides first): 8-level passes while
+// at least 12 levels remain (so a strided pass has 16 low offsets), then the
+// remainder in one pass
 static std::vector<std::pair<int, int>> fwht_passes(int m) {
   std::vector<std::pair<int, int>> ps;
   int rem = m;
-  while (rem > kFwhtMaxFirst) {
-    ps.push_back({rem - kFwhtMaxLevels, rem});
-    rem -= kFwhtMaxLevels;
+  while (rem >= kFwhtLevels + 4) {
+    ps.push_back({rem - kFwhtLevels, rem});
+    rem -= kFwhtLevels;
   }
   if (rem > 0) ps.push_back({0, rem});
   return ps;
@@ -1716,8 +1719,12 @@ static void fwht_columns(tf_context* ctx, double* X, int64_t N, int nb, const do
     a.n0 = n0;
     a.a0 = a0;
     a.seed = seed;
-    const int LW = a.l0 >= 4 ? 16 : (1 << a.l0);
-    const int M = 1 << (a.l1 - a.l0);
+    const int L = a.l1 - a.l0;
+    const int M = 1 << L;
+    int LW;  // lanes per CTA (as k_fwht_pass derives them)
+    if (L == 8 && (a.l0 == 0 || a.l0 >= 4) && N >= 4096) LW = 16;
+    else if (a.l0 == 0) LW = (int)std::min<int64_t>(std::max(1, 4096 / M), N / M);
+    else LW = a.l0 >= 4 ? 16 : (1 << a.l0);
     const size_t smem = sizeof(double) * (size_t)M * LW;
     smem_optin((const void*)k_fwht_pass, smem);
     dim3 grid((unsigned)(N / ((int64_t)M * LW)), (unsigned)nb);
