@@ -7,10 +7,13 @@ from .api import (CudaError, DataError, Engine, FitResult, NumericalError, PACFR
                   RunReport, TimeSeries, UsageError, default_engine, derive_seed, lsar_fit,
                   report_to_json, rh_fit, run_fit, select_order, exact_fit, fit_many,
                   load_series_bin, save_series_bin, srht_fit, hadamard_apply,
-                  srht_sample_count, SrhtCount)
+                  srht_sample_count, SrhtCount, run_compare, run_sweep, compare_to_json,
+                  CompareReport, MethodComparison, SweepRow, relative_error_pct, trimmed_mean)
 
 __all__ = ["TimeSeries", "FitResult", "PACFResult", "RHConfig", "RunReport", "Engine",
            "UsageError", "DataError", "NumericalError", "CudaError", "lsar_fit", "rh_fit",
            "run_fit", "report_to_json", "select_order", "derive_seed", "default_engine",
            "exact_fit", "fit_many", "load_series_bin", "save_series_bin", "srht_fit",
-           "hadamard_apply", "srht_sample_count", "SrhtCount"]
+           "hadamard_apply", "srht_sample_count", "SrhtCount", "run_compare", "run_sweep",
+           "compare_to_json", "CompareReport", "MethodComparison", "SweepRow", "relative_error_pct",
+           "trimmed_mean"]

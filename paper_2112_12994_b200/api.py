@@ -542,6 +542,8 @@ def fit_many(series_list, method: str, p_bar: int, c: int, seeds, *, workers: in
                     out[k] = rh_fit(ser, p_bar, c, config, seed, engine=eng)
                 elif method == "exact":
                     out[k] = exact_fit(ser, p_bar, engine=eng)
+                elif method == "srht":
+                    out[k] = srht_fit(ser, p_bar, c, seed, engine=eng)
                 else:
                     raise UsageError(f"unknown method '{method}'")
         except Exception as e:  # noqa: BLE001 -- re-raised in the caller
@@ -616,3 +618,149 @@ def report_to_json(r: RunReport) -> str:
          "pacf": {"method": r.pacf.method, "bound": r.pacf.bound, "taus": r.pacf.taus},
          "p_star": r.p_star, "coefficients": r.coefficients}
     return json.dumps(j, indent=2, sort_keys=True) + "\n"  # nlohmann objects are key-sorted
+
+
+# ---------------------------------------------------------------------------
+# Comparison drivers (bench.cpp:126-243): the callers that run many seeds of
+# lsar / rh against one exact fit.  The repetitions are independent fits and
+# run concurrently on the device (fit_many: one context and stream each).
+def relative_error_pct(estimate, reference) -> float:
+    """toeplitz.cpp:140-146."""
+    e = np.asarray(estimate, dtype=np.float64)
+    r = np.asarray(reference, dtype=np.float64)
+    if e.size != r.size:
+        raise UsageError("length mismatch")
+    ref_norm = float(np.linalg.norm(r))
+    if ref_norm == 0.0:
+        raise NumericalError("reference coefficients have zero norm")
+    return 100.0 * float(np.linalg.norm(e - r)) / ref_norm
+
+
+def trimmed_mean(values, trim_fraction: float) -> float:
+    """bench.cpp:126-139."""
+    v = sorted(float(x) for x in values)
+    if not v:
+        raise UsageError("trimmed mean of an empty sample")
+    if not (0.0 <= trim_fraction < 0.5):
+        raise UsageError("trim fraction must lie in [0, 0.5)")
+    drop = int(math.floor(trim_fraction * len(v)))
+    kept = v[drop:len(v) - drop]
+    acc = 0.0
+    for x in kept:  # sequential, as std::accumulate
+        acc += x
+    return acc / len(kept)
+
+
+@dataclass
+class MethodComparison:
+    method: str
+    trimmed_error_pct: list
+    mean_lag_seconds: list
+    mean_upfront_seconds: float
+    p_stars: list
+
+
+@dataclass
+class CompareReport:
+    n: int
+    p_bar: int
+    c: int
+    repetitions: int
+    trim_fraction: float
+    seed: int
+    timing_recorded: bool
+    exact_p_star: int
+    exact_lag_seconds: list
+    exact_taus: list
+    lsar: MethodComparison
+    rh: MethodComparison
+
+
+@dataclass
+class SweepRow:
+    method: str
+    c: int
+    max_lag_seconds: float
+    max_error_pct: float
+
+
+def _strip_timing(f: FitResult) -> None:
+    f.per_lag_seconds = [0.0] * len(f.per_lag_seconds)
+    f.upfront_seconds = 0.0
+
+
+def _summarize(method: str, exact: FitResult, runs: list, trim_fraction: float) -> MethodComparison:
+    """bench.cpp:143-168."""
+    p_bar = len(exact.per_lag_coefficients)
+    reps = len(runs)
+    err, secs = [], []
+    for h in range(p_bar):
+        errs = [relative_error_pct(r.per_lag_coefficients[h], exact.per_lag_coefficients[h]) for r in runs]
+        acc = 0.0
+        for r in runs:
+            acc += r.per_lag_seconds[h]
+        secs.append(acc / reps)
+        err.append(trimmed_mean(errs, trim_fraction))
+    up = 0.0
+    for r in runs:
+        up += r.upfront_seconds
+    return MethodComparison(method, err, secs, up / reps, [r.p_star for r in runs])
+
+
+def run_compare(series: TimeSeries, p_bar: int, c: int, reps: int, trim_fraction: float, seed: int,
+                with_timing: bool = True, *, workers: int = 8) -> CompareReport:
+    """bench.cpp:172-212: one exact fit, `reps` LSAR and RH fits with seeds
+    derive_seed(seed, 0x1000 + r) / derive_seed(seed, 0x2000 + r)."""
+    if reps < 1:
+        raise UsageError("need at least one repetition")
+    if not (0.0 <= trim_fraction < 0.5):
+        raise UsageError("trim fraction must lie in [0, 0.5)")
+    exact = exact_fit(series, p_bar)
+    lsar_runs = fit_many([series] * reps, "lsar", p_bar, c, [derive_seed(seed, 0x1000 + r) for r in range(reps)],
+                         workers=workers)
+    rh_runs = fit_many([series] * reps, "rh", p_bar, c, [derive_seed(seed, 0x2000 + r) for r in range(reps)],
+                       workers=workers)
+    if not with_timing:
+        for f in [exact] + lsar_runs + rh_runs:
+            _strip_timing(f)
+    return CompareReport(n=series.size(), p_bar=p_bar, c=c, repetitions=reps, trim_fraction=trim_fraction,
+                         seed=seed, timing_recorded=with_timing, exact_p_star=exact.p_star,
+                         exact_lag_seconds=list(exact.per_lag_seconds), exact_taus=list(exact.pacf.taus),
+                         lsar=_summarize("lsar", exact, lsar_runs, trim_fraction),
+                         rh=_summarize("rh", exact, rh_runs, trim_fraction))
+
+
+def run_sweep(series: TimeSeries, c_list, p_bar: int, reps: int, trim_fraction: float, seed: int,
+              with_timing: bool = True, *, workers: int = 8) -> list:
+    """bench.cpp:214-243: per c, `reps` LSAR and RH fits against one exact
+    fit (seeds derive_seed(seed, (ci << 20) + 0x10000 / 0x20000 + r)); rows
+    carry the max-over-lags mean lag time and trimmed error."""
+    c_list = list(c_list)
+    if not c_list:
+        raise UsageError("empty c list")
+    exact = exact_fit(series, p_bar)
+    rows = []
+    for ci, c in enumerate(c_list):
+        for method in ("lsar", "rh"):
+            tag = 0x10000 if method == "lsar" else 0x20000
+            seeds = [derive_seed(seed, (ci << 20) + tag + r) for r in range(reps)]
+            runs = fit_many([series] * reps, method, p_bar, c, seeds, workers=workers)
+            if not with_timing:
+                for f in runs:
+                    _strip_timing(f)
+            sm = _summarize(method, exact, runs, trim_fraction)
+            rows.append(SweepRow(method, int(c), max(sm.mean_lag_seconds), max(sm.trimmed_error_pct)))
+    return rows
+
+
+def compare_to_json(r: CompareReport) -> str:
+    """bench.cpp:286-303 (nlohmann objects: keys sorted, dump(2))."""
+    def mc(m: MethodComparison):
+        return {"method": m.method, "trimmed_error_pct": m.trimmed_error_pct, "mean_lag_seconds": m.mean_lag_seconds,
+                "mean_upfront_seconds": m.mean_upfront_seconds, "p_stars": m.p_stars}
+    j = {"n": r.n, "p_bar": r.p_bar, "c": r.c, "repetitions": r.repetitions, "trim_fraction": r.trim_fraction,
+         "seed": r.seed, "timing_recorded": r.timing_recorded,
+         "exact": {"p_star": r.exact_p_star, "per_lag_seconds": r.exact_lag_seconds, "taus": r.exact_taus},
+         "lsar": mc(r.lsar), "rh": mc(r.rh)}
+    return json.dumps(j, indent=2, sort_keys=True) + "\n"
+
