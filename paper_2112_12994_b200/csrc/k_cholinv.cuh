@@ -107,175 +107,101 @@ struct CITiles {
   __device__ __forceinline__ double* tile(int I, int J) const { return base + tpu_tile(K, I, J); }
 };
 
-// ---- 32 x 32 diagonal tile: factor + invert with ONE warp, recursively in
-//      8 x 8 blocks.  The 8 x 8 diagonal blocks are factored and inverted in
-//      registers (lanes 0..7, width-8 shuffles, 8-step chains); every other
-//      block operation is an 8 x 8 x 8 product = 2 DMMA m8n8k4.  The serial
-//      chain is 4 x (8 + 8) pivots instead of 32 + 32, and the warp issues
-//      ~2k instructions instead of ~10k.
-template <int I>
-struct F8 {
-  static __device__ __forceinline__ void run(double (&d)[8], int lane, bool& bad, int last,
+// Lane-per-column factor + inverse of a 32 x 32 diagonal tile (one warp):
+// lane j keeps column j of the tile in registers.  Step k: the pivot comes
+// from lane k, every lane scales its entry of row k (R(k, j)), row k goes to
+// shared memory (its slot in S, column-major (k, j)), and each lane folds
+// R(k, i) R(k, j) into its rows i in (k, j] -- broadcast reads, no shuffles
+// per element.  Then lane j back-substitutes column j of R^-1 from the rows
+// in S and the stored 1/R(i, i).  Pivot rules as F8: the target column
+// `last` is clamped to `floor`, earlier columns break down at `badfloor`,
+// columns past `last` are identity padding.  On exit S holds R^-1 (upper).
+// Compile-time loops (template recursion) keep v[] in registers, and every
+// lane runs the same instruction stream (entries below a lane's diagonal are
+// computed and ignored) -- lane-dependent branches would serialise the warp.
+template <int K, int I>
+struct LUpd {  // v[i] -= R(K, i) R(K, lane), i > K
+  static __device__ __forceinline__ void run(double (&v)[32], const double* S, double rkj) {
+    v[I] = fma(-S[I * kTLD + K], rkj, v[I]);
+    LUpd<K, I + 1>::run(v, S, rkj);
+  }
+};
+template <int K>
+struct LUpd<K, 32> {
+  static __device__ __forceinline__ void run(double (&)[32], const double*, double) {}
+};
+template <int K>
+struct LFac {
+  static __device__ __forceinline__ void run(double (&v)[32], double* S, double* invd, int lane, bool& bad, int last,
                                              double floor, double badfloor) {
-    double piv = __shfl_sync(0xffu, d[I], I, 8);
-    if (I == last) {
+    double piv = __shfl_sync(0xffffffffu, v[K], K);
+    if (K == last) {
       if (!(piv > floor)) piv = floor;  // vanishing residual (c == p)
       bad |= !isfinite(piv);
-    } else if (I < last) {
-      // numerically rank deficient: the pivot of a singular Gram is O(eps tr G),
-      // so anything below max(c, K) eps tr(G) is a breakdown (shift / min-norm)
+    } else if (last < 0 || K < last) {
       bad |= !(piv > badfloor) || !isfinite(piv);
-    }  // I > last: identity padding of the final tile (pivot 1, never checked)
-    const double inv = fast_rsqrt(piv);
-    if (lane == I) d[I] = piv * inv;
-    else if (lane > I) d[I] *= inv;
-#pragma unroll
-    for (int r = I + 1; r < 8; ++r) {
-      const double rir = __shfl_sync(0xffu, d[I], r, 8);
-      if (lane >= r) d[r] = fma(-rir, d[I], d[r]);
     }
-    F8<I + 1>::run(d, lane, bad, last, floor, badfloor);
+    const double inv = fast_rsqrt(piv);
+    v[K] = lane == K ? piv * inv : v[K] * inv;  // R(K, lane) (lanes < K: ignored)
+    if (lane == K) invd[K] = inv;
+    if (lane >= K) S[lane * kTLD + K] = v[K];   // row K of R
+    __syncwarp();
+    LUpd<K, K + 1>::run(v, S, v[K]);
+    LFac<K + 1>::run(v, S, invd, lane, bad, last, floor, badfloor);
   }
 };
 template <>
-struct F8<8> {
-  static __device__ __forceinline__ void run(double (&)[8], int, bool&, int, double, double) {}
+struct LFac<32> {
+  static __device__ __forceinline__ void run(double (&)[32], double*, double*, int, bool&, int, double, double) {}
+};
+template <int I, int L>
+struct LDot {  // a += R(I, l) x_l, l >= L (x_l = 0 past the lane's diagonal)
+  static __device__ __forceinline__ void run(const double (&v)[32], const double* S, double& a0, double& a1) {
+    a0 = fma(S[L * kTLD + I], v[L], a0);
+    if (L + 1 < 32) a1 = fma(S[(L + 1 < 32 ? L + 1 : L) * kTLD + I], v[L + 1 < 32 ? L + 1 : L], a1);
+    LDot<I, (L + 2 < 32 ? L + 2 : 32)>::run(v, S, a0, a1);
+  }
 };
 template <int I>
-struct V8 {  // x = R^-1 in place, rows bottom-up (row I of R dead once row I of X is known)
-  static __device__ __forceinline__ void run(double (&d)[8], int lane) {
-    double acc = (lane == I) ? 1.0 : 0.0;
-#pragma unroll
-    for (int q = I + 1; q < 8; ++q) {
-      const double riq = __shfl_sync(0xffu, d[I], q, 8);
-      if (lane >= q) acc = fma(-riq, d[q], acc);
-    }
-    const double rinv = fast_rcp(__shfl_sync(0xffu, d[I], I, 8));
-    d[I] = lane >= I ? acc * rinv : 0.0;
-    V8<I - 1>::run(d, lane);
+struct LDot<I, 32> {
+  static __device__ __forceinline__ void run(const double (&)[32], const double*, double&, double&) {}
+};
+template <int I>
+struct LInv {  // rows I, I-1, ..., 0 of column lane of R^-1
+  static __device__ __forceinline__ void run(double (&v)[32], const double* S, const double* invd, int lane) {
+    double a0 = 0.0, a1 = 0.0;
+    LDot<I, I + 1>::run(v, S, a0, a1);
+    const double d = invd[I];
+    v[I] = I == lane ? d : (I < lane ? -(a0 + a1) * d : 0.0);
+    LInv<I - 1>::run(v, S, invd, lane);
   }
 };
 template <>
-struct V8<-1> {
-  static __device__ __forceinline__ void run(double (&)[8], int) {}
+struct LInv<-1> {
+  static __device__ __forceinline__ void run(double (&)[32], const double*, const double*, int) {}
 };
 
-// 8x8x8 product into a C fragment: acc += sum_k A(m, k) B(k, n)
-template <class FA, class FB>
-__device__ __forceinline__ void mma8(double& c0, double& c1, FA fa, FB fb) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int k = 4 * h + (lane & 3);
-    dmma_8x8x4(c0, c1, fa(lane >> 2, k), fb(k, lane >> 2));
-  }
-}
-
-// S: 32 x 32 scratch (column-major, leading dimension kTLD) holding the tile,
-// DI: 4 x 64 scratch for the 8 x 8 diagonal inverses, TS: 4 x 64 scratch.
-// On exit S holds Dinv of the (identity-padded) tile.  Returns bad pivot.
-__device__ __forceinline__ bool ci_diag32(double* S, double* DI, double* TS, int last,
-                                          double floor, double badfloor) {
-  const int lane = threadIdx.x & 31;
-  const int fr = lane >> 2, fc = 2 * (lane & 3);  // C fragment (row, col pair)
-  auto at = [&](int bi, int bj, int r, int c) -> double& { return S[(8 * bj + c) * kTLD + 8 * bi + r]; };
-  bool bad = false;
-  for (int k = 0; k < 4; ++k) {
-    // (a) factor + invert the 8 x 8 diagonal block in registers
-    if (lane < 8) {
-      double d[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) d[r] = r <= lane ? at(k, k, r, lane) : 0.0;
-      // target column index relative to this 8-block; no target in the tile -> +inf
-      const int lb = last >= 0 ? last - 8 * k : (1 << 20);
-      F8<0>::run(d, lane, bad, lb, floor, badfloor);
-#pragma unroll
-      for (int r = 0; r < 8; ++r) at(k, k, r, lane) = r <= lane ? d[r] : 0.0;
-      V8<7>::run(d, lane);
-#pragma unroll
-      for (int r = 0; r < 8; ++r) DI[k * 64 + lane * 8 + r] = r <= lane ? d[r] : 0.0;  // column lane
-    }
-    __syncwarp();
-    // (b) block row k: S_kj = Dinv_kk^T S_kj, j > k
-    double t[3][2];
-#pragma unroll
-    for (int jj = 0; jj < 3; ++jj) {
-      const int j = k + 1 + jj;
-      t[jj][0] = t[jj][1] = 0.0;
-      if (j < 4)
-        mma8(t[jj][0], t[jj][1], [&](int m, int kk) { return DI[k * 64 + m * 8 + kk]; },
-             [&](int kk, int n) { return at(k, j, kk, n); });
-    }
-    __syncwarp();
-#pragma unroll
-    for (int jj = 0; jj < 3; ++jj) {
-      const int j = k + 1 + jj;
-      if (j < 4) {
-        at(k, j, fr, fc) = t[jj][0];
-        at(k, j, fr, fc + 1) = t[jj][1];
-      }
-    }
-    __syncwarp();
-    // (c) trailing update S_ij -= S_ki^T S_kj, k < i <= j
-    for (int i = k + 1; i < 4; ++i)
-      for (int j = i; j < 4; ++j) {
-        double c0 = at(i, j, fr, fc), c1 = at(i, j, fr, fc + 1);
-        mma8(c0, c1, [&](int m, int kk) { return -at(k, i, kk, m); }, [&](int kk, int n) { return at(k, j, kk, n); });
-        at(i, j, fr, fc) = c0;
-        at(i, j, fr, fc + 1) = c1;
-      }
-    __syncwarp();
-  }
-  // inverse from the blocks, block rows bottom-up:
-  //   X_ij = -Dinv_ii sum_{k=i+1..j} R_ik X_kj   (X_jj = Dinv_jj)
-  for (int i = 2; i >= 0; --i) {
-#pragma unroll
-    for (int jj = 0; jj < 3; ++jj) {
-      const int j = i + 1 + jj;
-      if (j < 4) {
-        double c0 = 0.0, c1 = 0.0;
-        for (int k = i + 1; k <= j; ++k)
-          mma8(c0, c1, [&](int m, int kk) { return at(i, k, m, kk); },
-               [&](int kk, int n) { return k == j ? DI[j * 64 + n * 8 + kk] : at(k, j, kk, n); });
-        TS[jj * 64 + fr * 8 + fc] = c0;  // row-major 8 x 8
-        TS[jj * 64 + fr * 8 + fc + 1] = c1;
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int jj = 0; jj < 3; ++jj) {
-      const int j = i + 1 + jj;
-      if (j < 4) {
-        double c0 = 0.0, c1 = 0.0;
-        mma8(c0, c1, [&](int m, int kk) { return -DI[i * 64 + kk * 8 + m]; },
-             [&](int kk, int n) { return TS[jj * 64 + kk * 8 + n]; });
-        at(i, j, fr, fc) = c0;
-        at(i, j, fr, fc + 1) = c1;
-      }
-    }
-    __syncwarp();
-  }
-  for (int e = lane; e < 4 * 64; e += 32) {  // diagonal blocks <- Dinv_kk
-    const int k = e >> 6, c = (e >> 3) & 7, r = e & 7;
-    at(k, k, r, c) = DI[e];
-  }
-  __syncwarp();
-  return __any_sync(0xffffffffu, bad);
-}
-
-// Factor + invert diagonal tile (b, b) (width m) through the scratch S.
+// tile: the m-column diagonal tile (column-major upper, LD kTLD; columns past
+// m are identity padding), factored and replaced by Dinv = R^-1.  S (32 x
+// kTLD scratch) receives the rows of R, invd the reciprocal pivots.
 __device__ __forceinline__ bool ci_diag_tile(double* tile, int m, int last, double floor, double badfloor,
-                                             double* S, double* DI, double* TS) {
+                                             double* S, double* invd, double* /*unused*/) {
   const int lane = threadIdx.x & 31;
-  for (int e = lane; e < 32 * 32; e += 32) {
-    const int c = e >> 5, r = e & 31;
-    S[c * kTLD + r] = c < m ? (r <= c ? tile[c * kTLD + r] : 0.0) : (r == c ? 1.0 : 0.0);
-  }
+  double v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    v[i] = lane < m ? (i <= lane ? tile[lane * kTLD + i] : 0.0) : (i == lane ? 1.0 : 0.0);
   __syncwarp();
-  const bool bad = ci_diag32(S, DI, TS, last, floor, badfloor);
-  for (int e = lane; e < 32 * m; e += 32) {
-    const int c = e >> 5, r = e & 31;
-    tile[c * kTLD + r] = r <= c ? S[c * kTLD + r] : 0.0;
+  bool bad = false;
+  LFac<0>::run(v, S, invd, lane, bad, last, floor, badfloor);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i > lane) v[i] = 0.0;  // below the diagonal of column lane
+  LInv<31>::run(v, S, invd, lane);
+  if (lane < m) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) tile[lane * kTLD + i] = i <= lane ? v[i] : 0.0;
   }
   __syncwarp();
   return bad;
@@ -665,25 +591,40 @@ __device__ __forceinline__ double oct_sum(double v) {
   return v;
 }
 
-// x <- R^-1 x (back substitution, R in RD format)
+// x <- R^-1 x (back substitution, R in RD format), right-looking: once block
+// J is final (x_J = Dinv_J x_J, one warp), every warp subtracts R(I, J) x_J
+// from a block I < J -- the tile loads of a step are independent (one memory
+// round trip per block instead of one per column group)
 __device__ void rd_solve_col(const double* R, int K, double* x, double* tmp) {
+  (void)tmp;
   const int nb = (K + 31) / 32;
-  const int r = threadIdx.x >> 3, sub = threadIdx.x & 7;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int J = nb - 1; J >= 0; --J) {
     const int wJ = tpu_w(J, K);
-    double part = 0.0;
-    if (r < wJ)
-      for (int c = 32 * (J + 1) + sub; c < K; c += 8)
-        part = fma(R[tpu_tile(K, J, c >> 5) + (c & 31) * kTLD + r], x[c], part);
-    part = oct_sum(part);
-    if (sub == 0 && r < 32) tmp[r] = r < wJ ? x[32 * J + r] - part : 0.0;
+    if (warp == 0) {
+      const double* D = R + tpu_tile(K, J, J);
+      double q0 = 0.0, q1 = 0.0;
+      if (lane < wJ) {
+#pragma unroll 8
+        for (int c = lane; c < wJ; c += 2) {
+          q0 = fma(D[c * kTLD + lane], x[32 * J + c], q0);
+          if (c + 1 < wJ) q1 = fma(D[(c + 1) * kTLD + lane], x[32 * J + c + 1], q1);
+        }
+      }
+      __syncwarp();
+      if (lane < wJ) x[32 * J + lane] = q0 + q1;
+    }
     __syncthreads();
-    const double* D = R + tpu_tile(K, J, J);
-    double q = 0.0;
-    if (r < wJ)
-      for (int c = r + sub; c < wJ; c += 8) q = fma(D[c * kTLD + r], tmp[c], q);
-    q = oct_sum(q);
-    if (sub == 0 && r < wJ) x[32 * J + r] = q;
+    for (int I = warp; I < J; I += nw) {  // blocks above J are full (32 rows)
+      const double* Rt = R + tpu_tile(K, I, J);
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll 8
+      for (int c = 0; c < wJ; c += 2) {
+        a0 = fma(Rt[c * kTLD + lane], x[32 * J + c], a0);
+        if (c + 1 < wJ) a1 = fma(Rt[(c + 1) * kTLD + lane], x[32 * J + c + 1], a1);
+      }
+      x[32 * I + lane] -= a0 + a1;
+    }
     __syncthreads();
   }
 }
@@ -711,16 +652,25 @@ __device__ void rd_solve_row(const double* R, int K, double* y, double* tmp) {
   }
 }
 
-// s <- T x (upper TPU): one warp per row, lanes over columns (independent
-// loads in flight instead of a per-thread dependent row loop)
+// s <- T x (upper TPU): a warp per 32-row block I, lane = row, summing the
+// tiles T(I, J), J >= I, in order -- coalesced tile columns, loads independent
+// across the whole row block
 __device__ void tpu_matvec(const double* T, int K, const double* x, double* s) {
+  const int nb = (K + 31) / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int r = warp; r < K; r += nw) {
-    double acc = 0.0;
-#pragma unroll 4
-    for (int c = r + lane; c < K; c += 32) acc = fma(__ldg(T + tpu_idx(K, r, c)), x[c], acc);
-    acc = warp_sum(acc);
-    if (lane == 0) s[r] = acc;
+  for (int I = warp; I < nb; I += nw) {
+    const int wI = tpu_w(I, K);
+    double a0 = 0.0, a1 = 0.0;
+    for (int J = I; J < nb; ++J) {
+      const int wJ = tpu_w(J, K);
+      const double* Tt = T + tpu_tile(K, I, J);
+#pragma unroll 8
+      for (int c = 0; c < wJ; c += 2) {
+        if (J > I || c >= lane) a0 = fma(__ldg(Tt + c * kTLD + lane), x[32 * J + c], a0);
+        if (c + 1 < wJ && (J > I || c + 1 >= lane)) a1 = fma(__ldg(Tt + (c + 1) * kTLD + lane), x[32 * J + c + 1], a1);
+      }
+    }
+    if (lane < wI) s[32 * I + lane] = a0 + a1;
   }
   __syncthreads();
 }
