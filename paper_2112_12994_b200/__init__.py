@@ -8,7 +8,9 @@ from .api import (CudaError, DataError, Engine, FitResult, NumericalError, PACFR
                   report_to_json, rh_fit, run_fit, select_order, exact_fit, fit_many,
                   load_series_bin, save_series_bin, srht_fit, hadamard_apply,
                   srht_sample_count, SrhtCount, run_compare, run_sweep, compare_to_json,
-                  CompareReport, MethodComparison, SweepRow, relative_error_pct, trimmed_mean)
+                  CompareReport, MethodComparison, SweepRow, relative_error_pct, trimmed_mean,
+                  write_run_report, write_compare_json, write_compare_errors_csv, write_compare_timing_csv,
+                  write_sweep_csv, write_pacf_plot_csv, write_pacf_csv)
 
 __all__ = ["TimeSeries", "FitResult", "PACFResult", "RHConfig", "RunReport", "Engine",
            "UsageError", "DataError", "NumericalError", "CudaError", "lsar_fit", "rh_fit",
@@ -16,4 +18,5 @@ __all__ = ["TimeSeries", "FitResult", "PACFResult", "RHConfig", "RunReport", "En
            "exact_fit", "fit_many", "load_series_bin", "save_series_bin", "srht_fit",
            "hadamard_apply", "srht_sample_count", "SrhtCount", "run_compare", "run_sweep",
            "compare_to_json", "CompareReport", "MethodComparison", "SweepRow", "relative_error_pct",
-           "trimmed_mean"]
+           "trimmed_mean", "write_run_report", "write_compare_json", "write_compare_errors_csv",
+           "write_compare_timing_csv", "write_sweep_csv", "write_pacf_plot_csv", "write_pacf_csv"]

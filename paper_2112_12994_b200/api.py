@@ -764,3 +764,61 @@ def compare_to_json(r: CompareReport) -> str:
          "lsar": mc(r.lsar), "rh": mc(r.rh)}
     return json.dumps(j, indent=2, sort_keys=True) + "\n"
 
+
+
+# ---------------------------------------------------------------------------
+# Report writers (bench.cpp:301-363, toeplitz.cpp:148-158): same text, %.17g
+def _write_text(path: str, text: str) -> None:
+    try:
+        with open(path, "w", newline="") as f:
+            f.write(text)
+    except OSError:
+        raise DataError("cannot write " + path) from None
+
+
+def write_run_report(report: RunReport, path: str) -> None:
+    _write_text(path, report_to_json(report))
+
+
+def write_compare_json(report: CompareReport, path: str) -> None:
+    _write_text(path, compare_to_json(report))
+
+
+def write_compare_errors_csv(report: CompareReport, path: str) -> None:
+    lines = ["lag,lsar_error,rh_error\n"]
+    for h, (a, b) in enumerate(zip(report.lsar.trimmed_error_pct, report.rh.trimmed_error_pct)):
+        lines.append("%d,%.17g,%.17g\n" % (h + 1, a, b))
+    _write_text(path, "".join(lines))
+
+
+def write_compare_timing_csv(report: CompareReport, path: str) -> None:
+    lines = ["lag,exact_cum,lsar_cum,rh_cum\n"]
+    ex = ls = 0.0
+    rh = report.rh.mean_upfront_seconds
+    for h in range(len(report.exact_lag_seconds)):
+        ex += report.exact_lag_seconds[h]
+        ls += report.lsar.mean_lag_seconds[h]
+        rh += report.rh.mean_lag_seconds[h]
+        lines.append("%d,%.17g,%.17g,%.17g\n" % (h + 1, ex, ls, rh))
+    _write_text(path, "".join(lines))
+
+
+def write_sweep_csv(rows, path: str) -> None:
+    lines = ["method,c,max_seconds,max_error_pct\n"]
+    for r in rows:
+        lines.append("%s,%d,%.17g,%.17g\n" % (r.method, r.c, r.max_lag_seconds, r.max_error_pct))
+    _write_text(path, "".join(lines))
+
+
+def write_pacf_plot_csv(pacf: PACFResult, path: str) -> None:
+    lines = ["lag,tau,bound_hi,bound_lo\n"]
+    for i, t in enumerate(pacf.taus):
+        lines.append("%d,%.17g,%.17g,%.17g\n" % (i + 1, t, pacf.bound, -pacf.bound))
+    _write_text(path, "".join(lines))
+
+
+def write_pacf_csv(pacf: PACFResult, path: str) -> None:
+    lines = ["lag,tau,bound\n"]
+    for i, t in enumerate(pacf.taus):
+        lines.append("%d,%.17g,%.17g\n" % (i + 1, t, pacf.bound))
+    _write_text(path, "".join(lines))

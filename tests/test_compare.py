@@ -21,6 +21,24 @@ def test_trimmed_mean_and_relative_error_cpu():
         tf.relative_error_pct([1, 2], [0, 0])
 
 
+def test_report_writers_cpu(tmp_path):
+    import paper_2112_12994_b200 as tf
+    pacf = tf.PACFResult(taus=[0.4, -0.2, 0.05], bound=0.1, method="lsar")
+    p = tmp_path / "plot.csv"
+    tf.write_pacf_plot_csv(pacf, str(p))
+    assert p.read_text().splitlines() == ["lag,tau,bound_hi,bound_lo", "1,0.40000000000000002,0.10000000000000001,-0.10000000000000001",
+                                          "2,-0.20000000000000001,0.10000000000000001,-0.10000000000000001",
+                                          "3,0.050000000000000003,0.10000000000000001,-0.10000000000000001"]
+    tf.write_pacf_csv(pacf, str(tmp_path / "pacf.csv"))
+    assert (tmp_path / "pacf.csv").read_text().splitlines()[0] == "lag,tau,bound"
+    rows = [tf.SweepRow("lsar", 200, 0.0, 1.5), tf.SweepRow("rh", 200, 0.0, 2.5)]
+    tf.write_sweep_csv(rows, str(tmp_path / "sweep.csv"))
+    assert (tmp_path / "sweep.csv").read_text().splitlines() == ["method,c,max_seconds,max_error_pct",
+                                                                 "lsar,200,0,1.5", "rh,200,0,2.5"]
+    with pytest.raises(tf.DataError, match="cannot write"):
+        tf.write_pacf_csv(pacf, str(tmp_path / "no" / "such" / "dir.csv"))
+
+
 def _series():
     from paper_2112_12994_b200 import gen
     return gen.simulate_roots(gen.ar_roots(4, 1.3, 3.0, 8), 3000, 8)
@@ -51,6 +69,12 @@ def test_run_compare_aggregates_repetitions():
     assert j["n"] == 3000 and j["exact"]["p_star"] == rep.exact_p_star
     assert len(j["lsar"]["trimmed_error_pct"]) == 5 and len(j["rh"]["p_stars"]) == 3
     assert tf.compare_to_json(rep) == tf.compare_to_json(rep)
+    import os, tempfile
+    d = tempfile.mkdtemp()
+    tf.write_compare_errors_csv(rep, os.path.join(d, "e.csv"))
+    tf.write_compare_timing_csv(rep, os.path.join(d, "t.csv"))
+    assert open(os.path.join(d, "e.csv")).readline().strip() == "lag,lsar_error,rh_error"
+    assert open(os.path.join(d, "t.csv")).readline().strip() == "lag,exact_cum,lsar_cum,rh_cum"
     with pytest.raises(tf.UsageError):
         tf.run_compare(s, 5, 300, 0, 0.0, 1)
     with pytest.raises(tf.UsageError):
