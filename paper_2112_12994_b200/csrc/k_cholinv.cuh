@@ -108,33 +108,37 @@ struct CITiles {
 };
 
 // Lane-per-column factor + inverse of a 32 x 32 diagonal tile (one warp):
-// lane j keeps column j of the tile in registers.  Step k: the pivot comes
-// from lane k, every lane scales its entry of row k (R(k, j)), row k goes to
-// shared memory (its slot in S, column-major (k, j)), and each lane folds
-// R(k, i) R(k, j) into its rows i in (k, j] -- broadcast reads, no shuffles
-// per element.  Then lane j back-substitutes column j of R^-1 from the rows
-// in S and the stored 1/R(i, i).  Pivot rules as F8: the target column
-// `last` is clamped to `floor`, earlier columns break down at `badfloor`,
-// columns past `last` are identity padding.  On exit S holds R^-1 (upper).
-// Compile-time loops (template recursion) keep v[] in registers, and every
-// lane runs the same instruction stream (entries below a lane's diagonal are
-// computed and ignored) -- lane-dependent branches would serialise the warp.
+// lane j keeps column j of the tile in registers, and every lane keeps a
+// copy of the running diagonal d[i] = G(i, i) - sum R(k, i)^2.  Step k: every
+// lane takes the pivot from its own d[k] (no shuffle; all copies are bitwise
+// equal), scales its entry of row k (R(k, j)), row k goes to shared memory
+// (its slot in S, column-major (k, j)), and each lane folds R(k, i) R(k, j)
+// into its rows i in (k, j] and R(k, i)^2 into d[i] -- broadcast reads.  The
+// inverse is right-looking too: once x_l = R^-1(l, j) is known, every row i < l
+// accumulates R(i, l) x_l, so x_{l-1} is one multiply away.  Pivot rules:
+// the target column `last` is clamped to `floor`, earlier columns break down
+// at `badfloor`, columns past `last` are identity padding.  Compile-time
+// loops (template recursion) keep v[], d[] in registers, and every lane runs
+// the same instruction stream (entries below a lane's diagonal are computed
+// and ignored) -- lane-dependent branches would serialise the warp.
 template <int K, int I>
-struct LUpd {  // v[i] -= R(K, i) R(K, lane), i > K
-  static __device__ __forceinline__ void run(double (&v)[32], const double* S, double rkj) {
-    v[I] = fma(-S[I * kTLD + K], rkj, v[I]);
-    LUpd<K, I + 1>::run(v, S, rkj);
+struct LUpd {  // i > K: v[i] -= R(K, i) R(K, lane), d[i] -= R(K, i)^2
+  static __device__ __forceinline__ void run(double (&v)[32], double (&d)[32], const double* S, double rkj) {
+    const double r = S[I * kTLD + K];
+    v[I] = fma(-r, rkj, v[I]);
+    d[I] = fma(-r, r, d[I]);
+    LUpd<K, I + 1>::run(v, d, S, rkj);
   }
 };
 template <int K>
 struct LUpd<K, 32> {
-  static __device__ __forceinline__ void run(double (&)[32], const double*, double) {}
+  static __device__ __forceinline__ void run(double (&)[32], double (&)[32], const double*, double) {}
 };
 template <int K>
 struct LFac {
-  static __device__ __forceinline__ void run(double (&v)[32], double* S, double* invd, int lane, bool& bad, int last,
-                                             double floor, double badfloor) {
-    double piv = __shfl_sync(0xffffffffu, v[K], K);
+  static __device__ __forceinline__ void run(double (&v)[32], double (&d)[32], double* S, double* invd, int lane,
+                                             bool& bad, int last, double floor, double badfloor) {
+    double piv = d[K];
     if (K == last) {
       if (!(piv > floor)) piv = floor;  // vanishing residual (c == p)
       bad |= !isfinite(piv);
@@ -146,39 +150,40 @@ struct LFac {
     if (lane == K) invd[K] = inv;
     if (lane >= K) S[lane * kTLD + K] = v[K];   // row K of R
     __syncwarp();
-    LUpd<K, K + 1>::run(v, S, v[K]);
-    LFac<K + 1>::run(v, S, invd, lane, bad, last, floor, badfloor);
+    LUpd<K, K + 1>::run(v, d, S, v[K]);
+    LFac<K + 1>::run(v, d, S, invd, lane, bad, last, floor, badfloor);
   }
 };
 template <>
 struct LFac<32> {
-  static __device__ __forceinline__ void run(double (&)[32], double*, double*, int, bool&, int, double, double) {}
+  static __device__ __forceinline__ void run(double (&)[32], double (&)[32], double*, double*, int, bool&, int,
+                                             double, double) {}
 };
-template <int I, int L>
-struct LDot {  // a += R(I, l) x_l, l >= L (x_l = 0 past the lane's diagonal)
-  static __device__ __forceinline__ void run(const double (&v)[32], const double* S, double& a0, double& a1) {
-    a0 = fma(S[L * kTLD + I], v[L], a0);
-    if (L + 1 < 32) a1 = fma(S[(L + 1 < 32 ? L + 1 : L) * kTLD + I], v[L + 1 < 32 ? L + 1 : L], a1);
-    LDot<I, (L + 2 < 32 ? L + 2 : 32)>::run(v, S, a0, a1);
+template <int L, int I>
+struct LAcc {  // i < L: acc[i] += R(i, L) x_L
+  static __device__ __forceinline__ void run(double (&acc)[32], const double* S, double xl) {
+    acc[I] = fma(S[L * kTLD + I], xl, acc[I]);
+    LAcc<L, I - 1>::run(acc, S, xl);
   }
 };
-template <int I>
-struct LDot<I, 32> {
-  static __device__ __forceinline__ void run(const double (&)[32], const double*, double&, double&) {}
+template <int L>
+struct LAcc<L, -1> {
+  static __device__ __forceinline__ void run(double (&)[32], const double*, double) {}
 };
-template <int I>
-struct LInv {  // rows I, I-1, ..., 0 of column lane of R^-1
-  static __device__ __forceinline__ void run(double (&v)[32], const double* S, const double* invd, int lane) {
-    double a0 = 0.0, a1 = 0.0;
-    LDot<I, I + 1>::run(v, S, a0, a1);
-    const double d = invd[I];
-    v[I] = I == lane ? d : (I < lane ? -(a0 + a1) * d : 0.0);
-    LInv<I - 1>::run(v, S, invd, lane);
+template <int L>
+struct LInv {  // x_L = R^-1(L, lane), then its contributions to the rows above
+  static __device__ __forceinline__ void run(double (&v)[32], double (&acc)[32], const double* S, const double* invd,
+                                             int lane) {
+    const double dl = invd[L];
+    const double xl = L == lane ? dl : (L < lane ? -acc[L] * dl : 0.0);
+    v[L] = xl;
+    LAcc<L, L - 1>::run(acc, S, xl);
+    LInv<L - 1>::run(v, acc, S, invd, lane);
   }
 };
 template <>
 struct LInv<-1> {
-  static __device__ __forceinline__ void run(double (&)[32], const double*, const double*, int) {}
+  static __device__ __forceinline__ void run(double (&)[32], double (&)[32], const double*, const double*, int) {}
 };
 
 // tile: the m-column diagonal tile (column-major upper, LD kTLD; columns past
@@ -187,18 +192,19 @@ struct LInv<-1> {
 __device__ __forceinline__ bool ci_diag_tile(double* tile, int m, int last, double floor, double badfloor,
                                              double* S, double* invd, double* /*unused*/) {
   const int lane = threadIdx.x & 31;
-  double v[32];
+  double v[32], d[32];
 #pragma unroll
-  for (int i = 0; i < 32; ++i)
+  for (int i = 0; i < 32; ++i) {
     v[i] = lane < m ? (i <= lane ? tile[lane * kTLD + i] : 0.0) : (i == lane ? 1.0 : 0.0);
+    d[i] = i < m ? tile[i * kTLD + i] : 1.0;  // every lane: the diagonal
+  }
   __syncwarp();
   bool bad = false;
-  LFac<0>::run(v, S, invd, lane, bad, last, floor, badfloor);
+  LFac<0>::run(v, d, S, invd, lane, bad, last, floor, badfloor);
   __syncwarp();
 #pragma unroll
-  for (int i = 0; i < 32; ++i)
-    if (i > lane) v[i] = 0.0;  // below the diagonal of column lane
-  LInv<31>::run(v, S, invd, lane);
+  for (int i = 0; i < 32; ++i) d[i] = 0.0;  // reused: the inverse's row accumulators
+  LInv<31>::run(v, d, S, invd, lane);
   if (lane < m) {
 #pragma unroll
     for (int i = 0; i < 32; ++i) tile[lane * kTLD + i] = i <= lane ? v[i] : 0.0;
