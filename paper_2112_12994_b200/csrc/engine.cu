@@ -466,7 +466,7 @@ static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, co
   const int64_t ntile = (w + kPassTile - 1) / kPassTile;
   if (!exact_order && q >= kPassPstMinQ) {
     const size_t smem = PassLayout(q).bytes();
-    smem_optin((const void*)k_lsar_pass_pst, smem);
+    smem_optin((const void*)k_lsar_pass_pst<0>, smem);
     static std::mutex mu;  // contexts launch from several host threads
     static std::map<size_t, int> occ_of;
     int occ;
@@ -475,13 +475,13 @@ static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, co
       auto it = occ_of.find(smem);
       if (it == occ_of.end()) {
         int o = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_lsar_pass_pst, kPassThreads, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_lsar_pass_pst<0>, kPassThreads, smem));
         it = occ_of.emplace(smem, o).first;
       }
       occ = it->second;
     }
     const int64_t grid = std::min<int64_t>(ntile, (int64_t)std::max(occ, 1) * ctx->sm_count);
-    k_lsar_pass_pst<<<(unsigned)grid, kPassThreads, smem, ctx->stream>>>(a);
+    k_lsar_pass_pst<0><<<(unsigned)grid, kPassThreads, smem, ctx->stream>>>(a);
     LAUNCH_CHECK("k_lsar_pass_pst");
     COUNT_LAUNCH();
     return;
@@ -1055,8 +1055,7 @@ static void rowsq_all_rows(tf_context* ctx, int64_t rows, int K, const WL& wl, i
   for (int j = 0; j < ntiles; ++j) {
     const int kend = UPPER ? std::min(hk_kpad(K), hk_kpad(std::min(K, 64 * (j + 1)))) : hk_kpad(K);
     const int frags = std::min(8, (N - 64 * j + 7) / 8);
-    static const double fo = [] { const char* v = std::getenv("TF_HK_F"); return v ? std::atof(v) : 16.0; }();
-    wj[j] = (double)kend * (frags + fo);
+    wj[j] = (double)kend * (frags + 16.0);
     wsum += wj[j];
   }
   HkPlan plan;

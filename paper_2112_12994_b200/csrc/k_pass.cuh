@@ -62,7 +62,6 @@ struct PassArgs {
   double* chunkB;
   double* tileA;
   double* tileB;
-  int dbg;           // development switches (tools/pass_bench.cu): bit 2 skips the FIR, bit 3 the state traffic
   int64_t ylen;      // readable doubles at y (series + zero pad)
 };
 
@@ -301,21 +300,25 @@ __device__ __forceinline__ void pst_fill_y(const PassArgs& a, int64_t i0, double
   const int ycopy = (int)min((int64_t)L.ys_n, a.ylen - i0) & ~1;
   for (int x = ycopy + threadIdx.x; x < L.ys_n; x += kPassThreads) ys[skew12(x)] = 0.0;
 }
+template <int DBG>
 __device__ __forceinline__ void pst_issue_state(const PassArgs& a, int64_t i0, int rows, double* ss, double* rr,
                                                 uint64_t* bar) {  // one thread
-  const int rcopy = (a.dbg & 8) ? 0 : rows & ~1;
+  const int rcopy = (DBG & 8) ? 0 : rows & ~1;
   fence_proxy_async_smem();
   mbar_expect_tx(bar, (uint32_t)rcopy * 16u);
   if (rcopy > 0) {
     bulk_g2s(ss, a.s + i0, (uint32_t)rcopy * 8u, bar);
     bulk_g2s(rr, a.r + i0, (uint32_t)rcopy * 8u, bar);
   }
-  if (rows > rcopy && !(a.dbg & 8)) {  // odd last row: generic load (address not covered by the copy)
+  if (rows > rcopy && !(DBG & 8)) {  // odd last row: generic load (address not covered by the copy)
     ss[rcopy] = a.s[i0 + rcopy];
     rr[rcopy] = a.r[i0 + rcopy];
   }
 }
 
+// DBG (development, tools/pass_bench.cu; the product uses 0): bit 2 skips the
+// FIR, bit 3 the state traffic
+template <int DBG = 0>
 __global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass_pst(PassArgs a) {
   extern __shared__ __align__(128) double sm[];
   __shared__ double red[2][kPassThreads / 32];
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass_pst(PassArgs a) {
   {
     const int64_t i0 = tile * kPassTile;
     if (warp == 0) pst_issue_y(a, i0, ys, L, &bars[0]);
-    if (tid == 32) pst_issue_state(a, i0, (int)min((int64_t)kPassTile, a.w - i0), ss, rr, &bars[1]);
+    if (tid == 32) pst_issue_state<DBG>(a, i0, (int)min((int64_t)kPassTile, a.w - i0), ss, rr, &bars[1]);
     pst_fill_y(a, i0, ys, L);
   }
   for (int m = tid; m < L.phi_n; m += kPassThreads) {
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass_pst(PassArgs a) {
   }
   __syncthreads();
   const double* pb = phiP + kPhiOff + q - 1 + g - t;
-  const int nsteps = (a.dbg & 4) ? 0 : L.kd >> 2;
+  const int nsteps = (DBG & 4) ? 0 : L.kd >> 2;
   for (int k = 0; tile < ntile; ++k, tile += gridDim.x) {
     const int64_t i0 = tile * kPassTile;
     const int rows = (int)min((int64_t)kPassTile, a.w - i0);
@@ -378,11 +381,11 @@ __global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass_pst(PassArgs a) {
         if (row + 1 < rows) {
           A[h] += s1;
           B[h] = fma(c1[u], c1[u], B[h]);
-          if (!(a.dbg & 8)) {
+          if (!(DBG & 8)) {
             *reinterpret_cast<double2*>(a.s + i0 + row) = make_double2(s0, s1);
             *reinterpret_cast<double2*>(a.r + i0 + row) = make_double2(c0[u], c1[u]);
           }
-        } else if (!(a.dbg & 8)) {
+        } else if (!(DBG & 8)) {
           a.s[i0 + row] = s0;
           a.r[i0 + row] = c0[u];
         }
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass_pst(PassArgs a) {
       a.tileB[tile] = ((red[1][0] + red[1][1]) + red[1][2]) + red[1][3];
     }
     if (tid == 32 && next < ntile)
-      pst_issue_state(a, next * kPassTile, (int)min((int64_t)kPassTile, a.w - next * kPassTile), ss, rr, &bars[1]);
+      pst_issue_state<DBG>(a, next * kPassTile, (int)min((int64_t)kPassTile, a.w - next * kPassTile), ss, rr, &bars[1]);
   }
 }
 

@@ -1,6 +1,6 @@
 // pass_bench.cu -- the fused LSAR pass kernels in isolation (development helper).
 // Times k_lsar_pass_pst over w = 1e7 rows at several lags, also with its
-// debug switches (dbg bit 2: no FIR, bit 3: no state traffic) to split the
+// debug variants (template DBG bit 2: no FIR, bit 3: no state traffic) to split the
 // cost into memory and FIR parts, and k_lsar_pass (exact tap order) at q < 16.
 // build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -I paper_2112_12994_b200/csrc tools/pass_bench.cu -o gpurun_out/pass_bench
 #include <cuda_runtime.h>
@@ -59,19 +59,18 @@ int main(int argc, char** argv) {
   if (only_q >= 0) {
     a.q = only_q;
     const size_t smp = PassLayout(only_q).bytes();
-    CK(cudaFuncSetAttribute(k_lsar_pass_pst, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
+    CK(cudaFuncSetAttribute(k_lsar_pass_pst<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lsar_pass_pst, kPassThreads, smp);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lsar_pass_pst<0>, kPassThreads, smp);
     const unsigned grid = (unsigned)std::min<int64_t>(ntile, (int64_t)occ * nsm);
-    k_lsar_pass_pst<<<grid, kPassThreads, smp>>>(a);
+    k_lsar_pass_pst<0><<<grid, kPassThreads, smp>>>(a);
     CK(cudaDeviceSynchronize());
     printf("one launch at q=%d done\n", only_q);
     return 0;
   }
   for (int q : {1, 8, 15, 16, 50, 100, 200, 500}) {
     a.q = q;
-    a.dbg = 0;
-    const double fl = 2.0 * (q + 1) * w;
+      const double fl = 2.0 * (q + 1) * w;
     const double t_mem = 40.0 * w / 6537e3, t_fir = fl / 36.4e6;  // us at the measured copy / DFMA peaks
     double t_core = 0;
     if (q < 16) {  // CUDA-core pass (exact tap order)
@@ -80,16 +79,18 @@ int main(int argc, char** argv) {
       t_core = timeit([&] { k_lsar_pass<<<(unsigned)ntile, kPassThreads, sm0>>>(a); });
     }
     const size_t smp = PassLayout(q).bytes();
-    CK(cudaFuncSetAttribute(k_lsar_pass_pst, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
+    CK(cudaFuncSetAttribute(k_lsar_pass_pst<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
+    CK(cudaFuncSetAttribute(k_lsar_pass_pst<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
+    CK(cudaFuncSetAttribute(k_lsar_pass_pst<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
+    CK(cudaFuncSetAttribute(k_lsar_pass_pst<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp));
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lsar_pass_pst, kPassThreads, smp);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lsar_pass_pst<0>, kPassThreads, smp);
     const unsigned grid = (unsigned)std::min<int64_t>(ntile, (int64_t)occ * nsm);
     double tp[4];
-    for (int m = 0; m < 4; ++m) {
-      a.dbg = 4 * m;
-      tp[m] = timeit([&] { k_lsar_pass_pst<<<grid, kPassThreads, smp>>>(a); });
-    }
-    a.dbg = 0;
+    tp[0] = timeit([&] { k_lsar_pass_pst<0><<<grid, kPassThreads, smp>>>(a); });
+    tp[1] = timeit([&] { k_lsar_pass_pst<4><<<grid, kPassThreads, smp>>>(a); });
+    tp[2] = timeit([&] { k_lsar_pass_pst<8><<<grid, kPassThreads, smp>>>(a); });
+    tp[3] = timeit([&] { k_lsar_pass_pst<12><<<grid, kPassThreads, smp>>>(a); });
     CK(cudaGetLastError());
     printf("q=%3d pst occ %d | full %7.1f  noFIR %7.1f  noState %7.1f  neither %7.1f us | roofline max(mem %.1f, "
            "fp64 %.1f) -> %.0f%%",
@@ -106,7 +107,7 @@ int main(int argc, char** argv) {
       CK(cudaMemcpy(r1.data(), r, sizeof(double) * w, cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(s, hy.data(), sizeof(double) * w, cudaMemcpyHostToDevice));
       CK(cudaMemcpy(r, hy.data() + 1, sizeof(double) * w, cudaMemcpyHostToDevice));
-      k_lsar_pass_pst<<<grid, kPassThreads, smp>>>(a);
+      k_lsar_pass_pst<0><<<grid, kPassThreads, smp>>>(a);
       CK(cudaMemcpy(s2.data(), s, sizeof(double) * w, cudaMemcpyDeviceToHost));
       CK(cudaMemcpy(r2.data(), r, sizeof(double) * w, cudaMemcpyDeviceToHost));
       double ds = 0, dr = 0;
