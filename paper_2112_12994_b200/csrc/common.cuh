@@ -11,6 +11,8 @@
 // * Warp inclusive scans / reductions in a fixed order (deterministic).
 #pragma once
 
+#include <type_traits>
+
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -44,6 +46,20 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
+}
+
+// 4 x 4 DMMA block acc[i][j] += a[i] b[j].  FULL: every product (no
+// predicates).  Otherwise only i < ni, j < nj; a predicated mma.sync costs a
+// WARPSYNC + NOP + compare per DMMA, so callers branch to FULL (warp-uniformly)
+// whenever the whole block is live.
+template <bool FULL>
+__device__ __forceinline__ void dmma_4x4(double (&acc)[4][4][2], const double (&a)[4], const double (&b)[4], int ni,
+                                         int nj) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (FULL || (i < ni && j < nj)) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
 }
 
 // Division-free reciprocal / reciprocal square root: MUFU approximation plus

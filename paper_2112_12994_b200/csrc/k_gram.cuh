@@ -55,8 +55,8 @@ __device__ __forceinline__ void pair_from_index(int pair, int nblk, int& jb, int
 constexpr int kG2Stages = 2;
 constexpr int kG2Ld = 68;  // padded smem row (doubles): 544 B, 16-byte aligned, conflict-free fragments
 
-__host__ __device__ inline size_t gram2_smem_bytes(int stages = kG2Stages) {
-  return (size_t)stages * 2 * 32 * kG2Ld * sizeof(double);
+__host__ __device__ inline size_t gram2_smem_bytes(int stages = kG2Stages, int slab = 32) {
+  return (size_t)stages * 2 * slab * kG2Ld * sizeof(double);
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -70,7 +70,7 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int ST>
+template <int ST, int SLAB = 32>
 __global__ void __launch_bounds__(kGramThreads)
     k_gram_dense_t(const double* __restrict__ Q, int64_t ld, int64_t rows, int K, int nblk,
                  int64_t rows_per_split, double* __restrict__ W, const int* skip_flag) {
@@ -82,16 +82,16 @@ __global__ void __launch_bounds__(kGramThreads)
   const int J0 = jb * 64, L0 = lb * 64;
   const int64_t rb = (int64_t)blockIdx.y * rows_per_split;
   const int64_t re = min(rows, rb + rows_per_split);
-  const int nslab = (int)((re - rb + 31) / 32);
+  const int nslab = (int)((re - rb + SLAB - 1) / SLAB);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;
-  // 16-byte chunk assignment: 32 rows x 32 chunks per operand, 8 per thread
+  // 16-byte chunk assignment: SLAB rows x 32 chunks per operand, SLAB / 4 per thread
   auto issue = [&](int slab) {
-    double* sj = g2s + (size_t)(slab % ST) * 2 * 32 * kG2Ld;
-    double* sl = sj + 32 * kG2Ld;
-    const int64_t r0 = rb + (int64_t)slab * 32;
+    double* sj = g2s + (size_t)(slab % ST) * 2 * SLAB * kG2Ld;
+    double* sl = sj + SLAB * kG2Ld;
+    const int64_t r0 = rb + (int64_t)slab * SLAB;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < SLAB / 4; ++u) {
       const int ch = tid + kGramThreads * u;  // 0..1023
       const int rr = ch >> 5, cc = (ch & 31) * 2;
       const int64_t row = r0 + rr;
@@ -130,23 +130,25 @@ __global__ void __launch_bounds__(kGramThreads)
     // refill the stage consumed in the previous iteration
     if (s + ST - 1 < nslab) issue(s + ST - 1);
     cp_async_commit();
-    const double* SJ = g2s + (size_t)(s % ST) * 2 * 32 * kG2Ld;
-    const double* SL = diag ? SJ : SJ + 32 * kG2Ld;
-    if (!wskip) {
+    const double* SJ = g2s + (size_t)(s % ST) * 2 * SLAB * kG2Ld;
+    const double* SL = diag ? SJ : SJ + SLAB * kG2Ld;
+    // full 32 x 32 warp tiles take an unpredicated path: a predicated
+    // mma.sync costs a WARPSYNC + NOP + ISETP per DMMA
+    auto ksteps = [&](auto full) {
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
+      for (int kk = 0; kk < SLAB / 4; ++kk) {
         const int tr = 4 * kk + (lane & 3);
         double af[4], bf[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) af[i] = SJ[tr * kG2Ld + 32 * wm + 8 * i + (lane >> 2)];
 #pragma unroll
         for (int j = 0; j < 4; ++j) bf[j] = SL[tr * kG2Ld + 32 * wn + 8 * j + (lane >> 2)];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (i < ni && j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        dmma_4x4<decltype(full)::value>(acc, af, bf, ni, nj);
       }
+    };
+    if (!wskip) {
+      if (ni == 4 && nj == 4) ksteps(std::true_type{});
+      else ksteps(std::false_type{});
     }
   }
   cp_async_wait<0>();
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(kGramThreads)
     asm volatile("cp.async.commit_group;" ::: "memory");
     const double* sa = qps + (size_t)(ch % STAGES) * (SA_N + SB_N);
     const double* sb = sa + SA_N + wn * 32 * kTLD;
-    if (nj > 0) {
+    auto ksteps = [&](auto full) {
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         double af[4], bf[4];
@@ -343,13 +345,11 @@ __global__ void __launch_bounds__(kGramThreads)
         for (int i = 0; i < 4; ++i) af[i] = sa[(32 * wm + 8 * i + (lane >> 2)) * kQA + 4 * kk + (lane & 3)];
 #pragma unroll
         for (int j = 0; j < 4; ++j) bf[j] = sb[(8 * j + (lane >> 2)) * kTLD + 4 * kk + (lane & 3)];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        dmma_4x4<decltype(full)::value>(acc, af, bf, 4, nj);
       }
-    }
+    };
+    if (nj == 4) ksteps(std::true_type{});
+    else if (nj > 0) ksteps(std::false_type{});
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll

@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kGramThreads)
         SW[0][c0 + 2 * s][ll] = (c < K && N0 + ll < N) ? wl(c, N0 + ll) : 0.0;
       }
       __syncthreads();
-      if (nj > 0) {
+      auto ksteps = [&](auto full) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           double af[4], bf[4];
@@ -373,13 +373,11 @@ __global__ void __launch_bounds__(kGramThreads)
           for (int i = 0; i < 4; ++i) af[i] = SA[0][32 * wm + 8 * i + (lane >> 2)][4 * kk + (lane & 3)];
 #pragma unroll
           for (int j = 0; j < 4; ++j) bf[j] = SW[0][4 * kk + (lane & 3)][32 * wn + 8 * j + (lane >> 2)];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          dmma_4x4<decltype(full)::value>(acc, af, bf, 4, nj);
         }
-      }
+      };
+      if (nj == 4) ksteps(std::true_type{});
+      else if (nj > 0) ksteps(std::false_type{});
       __syncthreads();
     }
 #pragma unroll
@@ -470,10 +468,11 @@ __global__ void __launch_bounds__(kHkThreads)
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    if (nj > 0) {
-      // Hankel A fragments: row 8 i + r at column k equals row 8 (i + 1) + r at
-      // column k - 8, so two register windows (k = 0 and k = 4 mod 8) advance
-      // with one new shared-memory load each per 8 columns
+    // Hankel A fragments: row 8 i + r at column k equals row 8 (i + 1) + r at
+    // column k - 8, so two register windows (k = 0 and k = 4 mod 8) advance
+    // with one new shared-memory load each per 8 columns
+    auto ksteps = [&](auto full) {
+      constexpr bool F = decltype(full)::value;
       const int rbase = 32 * wm + (lane >> 2) + (lane & 3);
       double ae[4], ao[4];
 #pragma unroll
@@ -488,18 +487,10 @@ __global__ void __launch_bounds__(kHkThreads)
         for (int j = 0; j < 4; ++j) bf[j] = Wt[(k + (lane & 3)) * kHkLd + 32 * wn + 8 * j + (lane >> 2)];
         const double ae_n = ys[rbase + k + 32];
         const double ao_n = ys[rbase + k + 36];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], ae[i], bf[j]);
+        dmma_4x4<F>(acc, ae, bf, 4, nj);
 #pragma unroll
         for (int j = 0; j < 4; ++j) bf[j] = Wt[(k + 4 + (lane & 3)) * kHkLd + 32 * wn + 8 * j + (lane >> 2)];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], ao[i], bf[j]);
+        dmma_4x4<F>(acc, ao, bf, 4, nj);
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           ae[i] = ae[i + 1];
@@ -508,7 +499,9 @@ __global__ void __launch_bounds__(kHkThreads)
         ae[3] = ae_n;
         ao[3] = ao_n;
       }
-    }
+    };
+    if (nj == 4) ksteps(std::true_type{});
+    else if (nj > 0) ksteps(std::false_type{});
     if ((lane & 3) == 0 || true) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {

@@ -41,7 +41,7 @@ static Plan plan(int64_t rows, int K, int sms, int per_sm, int bw) {
 int main() {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  const int64_t cmax = 100000;
+  const int64_t cmax = 200000;
   const int Kmax = 512;
   double* Q;
   CK(cudaMalloc(&Q, sizeof(double) * cmax * (Kmax + 4)));
@@ -58,20 +58,29 @@ int main() {
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   printf("%8s %5s %7s %7s %10s %9s\n", "c", "K", "nsplit", "npair", "us", "TF/s(alg)");
-  for (int64_t c : {10000LL, 100000LL}) {
-    for (int K : {17, 33, 64, 100, 128, 160, 201, 301}) {
-      for (int variant = 0; variant < 4; ++variant) {
-        const int per_sm = variant < 2 ? 4 : 6;
-        const int stages = (variant % 2) ? 2 : 3;
-        Plan g = plan(c, K, sms, per_sm, 64);
+  for (int64_t c : {10000LL, 100000LL, 200000LL}) {
+    for (int K : {64, 101, 151, 201, 301, 501}) {
+      for (int variant = 0; variant < 5; ++variant) {
+        static const int vst[5] = {2, 3, 4, 3, 2}, vslab[5] = {32, 16, 16, 32, 16};
+        const int stages = vst[variant], slab = vslab[variant];
+        Plan g = plan(c, K, sms, 4, 64);
         const int64_t ldq = (K + 1) / 2 * 2;
         dim3 grid(g.npair, g.nsplit);
-        const size_t sm2 = gram2_smem_bytes(stages);
-        CK(cudaFuncSetAttribute(k_gram_dense_t<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram2_smem_bytes(3)));
-        CK(cudaFuncSetAttribute(k_gram_dense_t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram2_smem_bytes(2)));
+        const size_t sm2 = gram2_smem_bytes(stages, slab);
+        auto kern = [&]() -> void (*)(const double*, int64_t, int64_t, int, int, int64_t, double*, const int*) {
+          switch (variant) {
+            case 0: return k_gram_dense_t<2, 32>;
+            case 1: return k_gram_dense_t<3, 16>;
+            case 2: return k_gram_dense_t<4, 16>;
+            case 3: return k_gram_dense_t<3, 32>;
+            default: return k_gram_dense_t<2, 16>;
+          }
+        }();
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2));
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kGramThreads, sm2));
         auto run = [&]() {
-          if (stages == 3) k_gram_dense_t<3><<<grid, kGramThreads, sm2>>>(Q, ldq, c, K, g.nblk, g.rps, W, nullptr);
-          else k_gram_dense_t<2><<<grid, kGramThreads, sm2>>>(Q, ldq, c, K, g.nblk, g.rps, W, nullptr);
+          kern<<<grid, kGramThreads, sm2>>>(Q, ldq, c, K, g.nblk, g.rps, W, nullptr);
           k_gram_reduce<<<g.npair * 128, 256>>>(W, g.npair, g.nsplit, g.nblk, K, G, nullptr);
         };
         for (int it = 0; it < 3; ++it) run();
@@ -84,8 +93,8 @@ int main() {
         CK(cudaEventElapsedTime(&ms, e0, e1));
         const double us = ms * 1e3 / reps;
         const double flop = (double)c * K * (K + 1);
-        printf("%8lld %5d %7d %7d %10.1f %9.2f  (stages %d, per_sm %d)\n", (long long)c, K, g.nsplit, g.npair, us,
-               flop / (us * 1e-6) / 1e12, stages, per_sm);
+        printf("%8lld %5d %7d %7d %10.1f %9.2f  (stages %d, slab %d, occ %d)\n", (long long)c, K, g.nsplit, g.npair, us,
+               flop / (us * 1e-6) / 1e12, stages, slab, occ);
       }
     }
   }
