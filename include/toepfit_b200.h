@@ -5,6 +5,8 @@
  *
  *   tf_upload_series   <- TimeSeries(std::vector<double>)      series.hpp:16-31, series.cpp:23-32
  *   tf_lsar_sweep      <- FitResult lsar_fit(series, p_bar, c, seed)          lsar.hpp:89, lsar.cpp:100-124
+ *   tf_lsar_sweep_batch<- lsar_fit over many series / seeds (the run_compare / bench.cpp:183-188, 221-228
+ *                         run_sweep loops; BASELINE C5 batch)
  *   tf_rh_sweep        <- FitResult rh_fit(series, p_bar, c, cfg*, seed)      repeated_halving.hpp:97-99,
  *                                                                            repeated_halving.cpp:191-232
  *   tf_residuals       <- Eigen::VectorXd residuals(sys, phi)                 toeplitz.hpp:84-86, toeplitz.cpp:87-98
@@ -117,6 +119,21 @@ tf_status tf_upload_series_device(tf_context* ctx, const double* d_y, int64_t n)
 tf_status tf_lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed,
                         const tf_lsar_diag* diag, double* taus, double* coefs_packed,
                         double* lag_seconds, int* p_star);
+
+/* LSAR order sweeps of a BATCH of independent fits in one pass per lag:
+ * series b = y + b * y_stride (n values each; y_stride 0: one series shared
+ * by every fit, i.e. B seeds over one series), seed seeds[b], all with the
+ * same p_bar (<= 63) and c.  fixed_idx / fixed_w (nullable, [batch][p_bar][c])
+ * replace the draws (deterministic-index mode).  Outputs per fit b:
+ * taus[b * p_bar ..], coefs_packed[b * p_bar (p_bar+1)/2 ..], p_star[b],
+ * status_out[3 b ..] = {error code (0, 1 usage, 2 data, 3 numerical), lag,
+ * reason}; lag_seconds[p_bar] is the batch's device time per lag.  Each fit
+ * equals lsar_fit(series_b, p_bar, c, seeds[b]) (lsar.cpp:100-124); a fit
+ * whose sampled system breaks down is re-run through tf_lsar_sweep. */
+tf_status tf_lsar_sweep_batch(tf_context* ctx, const double* y, int64_t y_stride, int64_t batch, int64_t n,
+                              int p_bar, int64_t c, const uint64_t* seeds, const int64_t* fixed_idx,
+                              const double* fixed_w, double* taus, double* coefs_packed, double* lag_seconds,
+                              int* p_star, int* status_out);
 
 /* Repeated-Halving sweep; cfg NULL -> RHConfig::defaults(n - p_bar, p_bar + 1, c,
  * derive_seed(seed, 0x5c07e5)). */

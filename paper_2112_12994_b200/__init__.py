@@ -4,7 +4,7 @@ Host mirror of the reference toepfit API over the C ABI of
 libtoepfit_b200.so (hand-written sm_100a kernels); see DESIGN.md.
 """
 from .api import (CudaError, DataError, Engine, FitResult, NumericalError, PACFResult, RHConfig,  # noqa: F401
-                  RunReport, TimeSeries, UsageError, default_engine, derive_seed, lsar_fit,
+                  RunReport, TimeSeries, UsageError, default_engine, derive_seed, lsar_fit, lsar_fit_batch,
                   report_to_json, rh_fit, run_fit, select_order, exact_fit, fit_many,
                   load_series_bin, save_series_bin, srht_fit, hadamard_apply,
                   srht_sample_count, SrhtCount, run_compare, run_sweep, compare_to_json,
@@ -13,7 +13,7 @@ from .api import (CudaError, DataError, Engine, FitResult, NumericalError, PACFR
                   write_sweep_csv, write_pacf_plot_csv, write_pacf_csv)
 
 __all__ = ["TimeSeries", "FitResult", "PACFResult", "RHConfig", "RunReport", "Engine",
-           "UsageError", "DataError", "NumericalError", "CudaError", "lsar_fit", "rh_fit",
+           "UsageError", "DataError", "NumericalError", "CudaError", "lsar_fit", "lsar_fit_batch", "rh_fit",
            "run_fit", "report_to_json", "select_order", "derive_seed", "default_engine",
            "exact_fit", "fit_many", "load_series_bin", "save_series_bin", "srht_fit",
            "hadamard_apply", "srht_sample_count", "SrhtCount", "run_compare", "run_sweep",

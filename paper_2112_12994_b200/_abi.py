@@ -49,6 +49,7 @@ EXPORTS = [
     "tf_apply_sample", "tf_solve_sampled", "tf_select_order", "tf_derive_seed",
     "tf_probe_fp64_peak", "tf_shard_open", "tf_shard_pass", "tf_shard_sample", "tf_shard_gram",
     "tf_shard_factor", "tf_shard_finish", "tf_tpu_size", "tf_sweep_span", "tf_exact_sweep", "tf_srht_sweep", "tf_hadamard", "tf_generate_series", "tf_download_series",
+    "tf_lsar_sweep_batch",
 ]
 
 _lib = None
@@ -98,6 +99,8 @@ def lib():
     L.tf_hadamard.argtypes = [C.c_void_p, _f64p, C.c_int64]
     L.tf_download_series.argtypes = [C.c_void_p, _f64p, C.c_int64]
     L.tf_generate_series.argtypes = [C.c_void_p, _f64p, C.c_int, C.c_int64, C.c_uint64, C.c_int, C.c_int64]
+    L.tf_lsar_sweep_batch.argtypes = [C.c_void_p, _f64p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int64,
+                                      C.POINTER(C.c_uint64), _i64p, _f64p, _f64p, _f64p, _f64p, _i32p, _i32p]
     L.tf_tpu_size.argtypes = [C.c_int]
     L.tf_tpu_size.restype = C.c_int64
     for name in EXPORTS:

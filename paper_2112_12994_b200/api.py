@@ -208,6 +208,41 @@ class Engine:
         self._series_id = None
 
     # ---------------------------------------------------------------- sweeps
+    def lsar_sweep_batch(self, ys, p_bar: int, c: int, seeds, fixed_idx=None, fixed_w=None, shared=False):
+        """tf_lsar_sweep_batch: ys is a (B, n) array (or one series of n values
+        with shared=True, fitted once per seed).  Returns taus (B, p_bar),
+        packed coefficients (B, p_bar (p_bar+1)/2), per-lag batch seconds,
+        p_star (B,) and status (B, 3)."""
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+        B = int(seeds.size)
+        y = np.ascontiguousarray(ys, dtype=np.float64)
+        if shared:
+            y = y.reshape(-1)
+            n, stride = y.size, 0
+        else:
+            if y.ndim != 2 or y.shape[0] != B:
+                raise UsageError("batch series must be a (len(seeds), n) array")
+            n, stride = y.shape[1], y.shape[1]
+        pb = max(int(p_bar), 1)
+        taus = np.zeros((B, pb))
+        coefs = np.zeros((B, pb * (pb + 1) // 2))
+        secs = np.zeros(pb)
+        pstar = np.zeros(B, np.int32)
+        status = np.zeros((B, 3), np.int32)
+        fi = fw = None
+        if fixed_idx is not None:
+            fi = np.ascontiguousarray(fixed_idx, dtype=np.int64)
+            fw = np.ascontiguousarray(fixed_w, dtype=np.float64)
+            if fi.size != B * pb * c or fw.size != B * pb * c:
+                raise UsageError("fixed samples must be [batch][p_bar][c]")
+        self._series_id = None  # a re-run fit replaces the resident series
+        self._check(_abi.lib().tf_lsar_sweep_batch(
+            self._ctx, ptr(y), int(stride), B, int(n), int(p_bar), int(c),
+            seeds.ctypes.data_as(C.POINTER(C.c_uint64)),
+            ptr(fi, _abi._i64p) if fi is not None else None, ptr(fw) if fw is not None else None,
+            ptr(taus), ptr(coefs), ptr(secs), ptr(pstar, _abi._i32p), ptr(status, _abi._i32p)))
+        return taus, coefs, secs, pstar, status
+
     def lsar_sweep(self, p_bar: int, c: int, seed: int, fixed_idx=None, fixed_w=None,
                    want_diag: bool = False, n: int | None = None):
         pb = max(int(p_bar), 1)
@@ -446,6 +481,50 @@ def lsar_fit(series: TimeSeries, p_bar: int, c: int, seed: int, *, engine: Engin
     taus, coefs, secs, pstar, diag = eng.lsar_sweep(p_bar, c, seed, fixed_idx, fixed_w, want_diag,
                                                     n=series.size())
     return _finish("lsar", taus, coefs, secs, pstar, p_bar, c, 0.0, diag)
+
+
+_BATCH_REASONS = {1: "zero residual norm; sampling distribution undefined", 2: "negative leverage score",
+                  3: "zero score sum; distribution undefined", 4: "compressed least-squares factorization failed",
+                  6: "all-zero window; leverage undefined"}
+_BATCH_ERRS = {1: UsageError, 2: DataError, 3: NumericalError}
+
+
+def lsar_fit_batch(series_list, p_bar: int, c: int, seeds, *, engine: Engine | None = None,
+                   fixed_idx=None, fixed_w=None, errors: str = "raise") -> list:
+    """Many independent LSAR fits in one batched sweep (tf_lsar_sweep_batch):
+    fit b = lsar_fit(series_list[b], p_bar, c, seeds[b]) (lsar.cpp:100-124).
+    series_list: equal-length series (a list or a (B, n) array), or a single
+    TimeSeries / 1-D array fitted once per seed (the reference's multi-seed
+    run_compare / run_sweep loops, bench.cpp:183-188, 221-228).  p_bar <= 63.
+    per_lag_seconds are the batch's per-lag device times.  errors="raise"
+    raises the first failing fit's UsageError / DataError / NumericalError;
+    "return" puts the exception in that fit's slot instead."""
+    eng = engine or default_engine()
+    seeds = list(seeds)
+    if isinstance(series_list, TimeSeries) or (isinstance(series_list, np.ndarray) and series_list.ndim == 1):
+        y = series_list.values() if isinstance(series_list, TimeSeries) else series_list
+        out = eng.lsar_sweep_batch(y, p_bar, c, seeds, fixed_idx, fixed_w, shared=True)
+    elif isinstance(series_list, np.ndarray):  # (B, n): used in place
+        out = eng.lsar_sweep_batch(series_list, p_bar, c, seeds, fixed_idx, fixed_w)
+    else:
+        rows = [s.values() if isinstance(s, TimeSeries) else np.asarray(s, dtype=np.float64) for s in series_list]
+        if len({r.size for r in rows}) > 1:
+            raise UsageError("batched fits need equal-length series")
+        out = eng.lsar_sweep_batch(np.stack(rows) if rows else np.zeros((0, 0)), p_bar, c, seeds, fixed_idx,
+                                   fixed_w)
+    taus, coefs, secs, pstar, status = out
+    fits = []
+    for b in range(len(seeds)):
+        code, lag, reason = (int(v) for v in status[b])
+        if code:
+            err = _BATCH_ERRS.get(code, NumericalError)(
+                f"fit {b}: {_BATCH_REASONS.get(reason, 'numerical failure')} (lag {lag})")
+            if errors == "raise":
+                raise err
+            fits.append(err)
+            continue
+        fits.append(_finish("lsar", taus[b], coefs[b], secs, int(pstar[b]), p_bar, c))
+    return fits
 
 
 def rh_fit(series: TimeSeries, p_bar: int, c: int, config: RHConfig | None = None, seed: int = 0, *,

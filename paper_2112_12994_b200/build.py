@@ -8,8 +8,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["csrc/engine.cu"]
-HEADERS = ["csrc/common.cuh", "csrc/k_pass.cuh", "csrc/k_sample.cuh", "csrc/k_gram.cuh",
-           "csrc/k_cholinv.cuh", "csrc/k_tpu.cuh", "csrc/k_rh.cuh", "csrc/k_gen.cuh", "csrc/engine.h", "../include/toepfit_b200.h"]
+HEADERS = sorted("csrc/" + f for f in os.listdir(os.path.join(HERE, "csrc")) if f.endswith((".cuh", ".h"))) + [
+    "../include/toepfit_b200.h"]
 OUT = os.path.join(HERE, "libtoepfit_b200.so")
 
 

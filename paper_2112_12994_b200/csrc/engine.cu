@@ -18,6 +18,7 @@
 #include <map>
 
 #include "engine.h"
+#include "k_bsolve.cuh"
 #include "k_cholinv.cuh"
 #include "k_gen.cuh"
 #include "k_gram.cuh"
@@ -505,7 +506,7 @@ static void launch_scan(tf_context* ctx, int64_t ntile, int lag, int check_r, in
 
 static void launch_draw(tf_context* ctx, uint64_t seed, int64_t c, int64_t w, int64_t* idx,
                         double* wts, const uint64_t* seed_ptr = nullptr) {
-  DrawArgs a;
+  DrawArgs a{};
   a.shard = 0;
   a.accept = nullptr;
   a.seed_ptr = nullptr;
@@ -771,6 +772,206 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
 }
 
 // ---------------------------------------------------------------------------
+// Batched LSAR sweeps: B series of equal length n (or one series shared by B
+// seeds: y_stride 0), the same p_bar and c -- the BASELINE C5 batch and the
+// reference's multi-seed loops (run_compare / run_sweep, bench.cpp:183-188,
+// 221-228).  Per lag four launches cover every series (blockIdx.y / x =
+// series): the exact-tap-order pass (k_lsar_pass), the scan, the draws and
+// the one-CTA solve k_bsolve (K <= 64).  Per-series state lives at fixed
+// strides.  A series whose sampled system breaks down is flagged and re-run
+// by the caller through the single-series path (lsar_sweep).
+static constexpr int kBatchMaxPbar = kBsMaxK - 1;
+
+static void lsar_batch(tf_context* ctx, const double* y_host, int64_t y_stride, int64_t B, int64_t n, int p_bar,
+                       int64_t c, const uint64_t* seeds, const int64_t* fixed_idx, const double* fixed_w,
+                       double* taus, double* coefs, double* lag_seconds, int* status_out, int* fallback_out) {
+  if (B < 1) throw TfError{TF_USAGE, "batch must hold at least one series"};
+  if (p_bar < 1) throw TfError{TF_USAGE, "maximum lag must be at least 1"};
+  if (p_bar > kBatchMaxPbar)
+    throw TfError{TF_USAGE, "batched sweeps support p_bar <= " + std::to_string(kBatchMaxPbar)};
+  if (n <= (int64_t)p_bar + 1) throw TfError{TF_DATA, "series too short for maximum lag " + std::to_string(p_bar)};
+  if (c < p_bar) throw TfError{TF_USAGE, "sample count below maximum lag"};
+  if (y_stride != 0 && y_stride < n) throw TfError{TF_USAGE, "series stride below series length"};
+  const int64_t w = n - p_bar;
+  const int64_t ntile = (w + kPassTile - 1) / kPassTile;
+  const int64_t nchunk = ntile * kChunksPerTile;
+  const int64_t wst = ntile * kPassTile;                // state stride
+  const int64_t nseries = y_stride ? B : 1;
+  const int64_t yst = y_stride ? n + 64 : 0;            // device series stride (zero pad)
+  const int G = guide_buckets(ntile);
+  const int64_t ncoef = (int64_t)p_bar * (p_bar + 1) / 2;
+  const bool fixed = fixed_idx && fixed_w;
+  cudaStream_t st = ctx->stream;
+  // ---- buffers ----
+  ctx->bt_y.need((size_t)(nseries * (n + 64)));
+  ctx->bt_s.need((size_t)(B * wst));
+  ctx->bt_r.need((size_t)(B * wst));
+  ctx->bt_cA.need((size_t)(B * nchunk));
+  ctx->bt_cB.need((size_t)(B * nchunk));
+  ctx->bt_tA.need((size_t)(B * ntile));
+  ctx->bt_tB.need((size_t)(B * ntile));
+  ctx->bt_OT.need((size_t)(B * ntile));
+  ctx->bt_guide.need((size_t)(B * (G + 1)));
+  ctx->bt_scal.need((size_t)(4 * B));
+  ctx->bt_Rh.need((size_t)(B * (p_bar + 2)));
+  ctx->bt_Sh.need((size_t)(B * (p_bar + 2)));
+  ctx->bt_phi.need((size_t)(B * (p_bar + 1)));
+  ctx->bt_coefs.need((size_t)(B * ncoef));
+  ctx->bt_taus.need((size_t)(B * p_bar));
+  ctx->bt_method.need((size_t)(B * p_bar));
+  ctx->bt_S0.need((size_t)(B * kBsSLd * kBsSLd));
+  ctx->bt_S1.need((size_t)(B * kBsSLd * kBsSLd));
+  ctx->bt_status.need((size_t)(4 * B));
+  ctx->bt_fb.need((size_t)B);
+  ctx->bt_seed.need((size_t)((p_bar + 1) * B));
+  if (fixed) {
+    ctx->bt_fidx.need((size_t)(B * p_bar * c));
+    ctx->bt_fw.need((size_t)(B * p_bar * c));
+  } else {
+    ctx->bt_idx.need((size_t)(B * c));
+    ctx->bt_wts.need((size_t)(B * c));
+  }
+  // ---- inputs ----
+  CK(cudaMemsetAsync(ctx->bt_y.get(), 0, (size_t)(nseries * (n + 64)) * sizeof(double), st));  // zero pads
+  CK(cudaMemcpy2DAsync(ctx->bt_y.get(), (n + 64) * sizeof(double), y_host, (y_stride ? y_stride : n) * sizeof(double),
+                       n * sizeof(double), (size_t)nseries, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(ctx->bt_status.get(), 0, 4 * B * sizeof(int), st));
+  CK(cudaMemsetAsync(ctx->bt_fb.get(), 0, B * sizeof(int), st));
+  CK(cudaMemsetAsync(ctx->bt_scal.get(), 0, 4 * B * sizeof(double), st));
+  std::vector<uint64_t> sd((size_t)(p_bar + 1) * B);  // [p][b] = derive_seed(seed_b, p)
+  for (int p = 0; p <= p_bar; ++p)
+    for (int64_t b = 0; b < B; ++b) sd[(size_t)p * B + b] = derive_seed(seeds[b], (uint64_t)p);
+  CK(cudaMemcpyAsync(ctx->bt_seed.get(), sd.data(), sd.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  if (fixed) {
+    for (int64_t i = 0; i < B * p_bar * c; ++i)
+      if (fixed_idx[i] < 0 || fixed_idx[i] >= w) throw TfError{TF_USAGE, "sample index out of range"};  // sketch.cpp:69
+    CK(cudaMemcpyAsync(ctx->bt_fidx.get(), fixed_idx, B * p_bar * c * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->bt_fw.get(), fixed_w, B * p_bar * c * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  ensure_events(ctx, p_bar + 1);
+  // ---- launches ----
+  PassArgs pa{};
+  pa.y = ctx->bt_y.get();
+  pa.w = w;
+  pa.s = ctx->bt_s.get();
+  pa.r = ctx->bt_r.get();
+  pa.chunkA = ctx->bt_cA.get();
+  pa.chunkB = ctx->bt_cB.get();
+  pa.tileA = ctx->bt_tA.get();
+  pa.tileB = ctx->bt_tB.get();
+  pa.ylen = n + 64;
+  pa.bs_y = yst;
+  pa.bs_w = wst;
+  pa.bs_chunk = nchunk;
+  pa.bs_tile = ntile;
+  pa.bs_phi = p_bar + 1;
+  pa.bs_scal = 4;
+  pa.phi = ctx->bt_phi.get();
+  pa.Rprev = ctx->bt_scal.get();
+  const dim3 pgrid((unsigned)ntile, (unsigned)B);
+  auto pass = [&](int q) {
+    pa.q = q;
+    const size_t smem = pass_smem_bytes(q);
+    smem_optin((const void*)k_lsar_pass, smem);
+    k_lsar_pass<<<pgrid, kPassThreads, smem, st>>>(pa);
+    LAUNCH_CHECK("k_lsar_pass (batch)");
+    COUNT_LAUNCH();
+  };
+  const size_t bsm = bsolve_smem_bytes();
+  smem_optin((const void*)k_bsolve, bsm);
+  CK(cudaEventRecord(ctx->events[0], st));
+  pass(0);
+  for (int p = 1; p <= p_bar; ++p) {
+    const int q = p - 1;
+    k_lag_scan<<<(unsigned)B, kScanThreads, 0, st>>>(ctx->bt_tA.get(), ctx->bt_tB.get(), ntile, ctx->bt_OT.get(),
+                                                     ctx->bt_scal.get(), ctx->bt_Rh.get(), ctx->bt_Sh.get(), q, 1,
+                                                     ctx->bt_status.get(), 0, nullptr, ctx->bt_guide.get(), ntile,
+                                                     p_bar + 2);
+    LAUNCH_CHECK("k_lag_scan (batch)");
+    COUNT_LAUNCH();
+    const int64_t* idx;
+    const double* wts;
+    int64_t bs_idx;
+    if (fixed) {
+      idx = ctx->bt_fidx.get() + (size_t)(p - 1) * c;
+      wts = ctx->bt_fw.get() + (size_t)(p - 1) * c;
+      bs_idx = (int64_t)p_bar * c;
+    } else {
+      DrawArgs da{};
+      da.seed_ptr = ctx->bt_seed.get() + (size_t)p * B;
+      da.bs_seed = 1;
+      da.c = c;
+      da.scal = ctx->bt_scal.get();
+      da.OT = ctx->bt_OT.get();
+      da.guide = ctx->bt_guide.get();
+      da.ntile = ntile;
+      da.tA = ctx->bt_tA.get();
+      da.tB = ctx->bt_tB.get();
+      da.chunkA = ctx->bt_cA.get();
+      da.chunkB = ctx->bt_cB.get();
+      da.s = ctx->bt_s.get();
+      da.r = ctx->bt_r.get();
+      da.w = w;
+      da.idx = ctx->bt_idx.get();
+      da.wts = ctx->bt_wts.get();
+      da.bs_w = wst;
+      da.bs_chunk = nchunk;
+      da.bs_tile = ntile;
+      const dim3 dgrid((unsigned)((c + kDrawPerCta - 1) / kDrawPerCta), (unsigned)B);
+      k_draw<<<dgrid, kDrawThreads, 0, st>>>(da);
+      LAUNCH_CHECK("k_draw (batch)");
+      COUNT_LAUNCH();
+      idx = ctx->bt_idx.get();
+      wts = ctx->bt_wts.get();
+      bs_idx = c;
+    }
+    BSolveArgs sa{};
+    sa.y = ctx->bt_y.get();
+    sa.bs_y = yst;
+    sa.idx = idx;
+    sa.wts = wts;
+    sa.bs_idx = bs_idx;
+    sa.c = c;
+    sa.K = p + 1;
+    sa.lag = p;
+    sa.Sprev = (p & 1) ? ctx->bt_S0.get() : ctx->bt_S1.get();
+    sa.Snext = (p & 1) ? ctx->bt_S1.get() : ctx->bt_S0.get();
+    sa.phi = ctx->bt_phi.get();
+    sa.bs_phi = p_bar + 1;
+    sa.scal = ctx->bt_scal.get();
+    sa.coefs = ctx->bt_coefs.get();
+    sa.bs_coef = ncoef;
+    sa.taus = ctx->bt_taus.get();
+    sa.bs_tau = p_bar;
+    sa.method = ctx->bt_method.get();
+    sa.fallback = ctx->bt_fb.get();
+    k_bsolve<<<(unsigned)B, kBsThreads, bsm, st>>>(sa);
+    LAUNCH_CHECK("k_bsolve");
+    COUNT_LAUNCH();
+    pass(p);
+    CK(cudaEventRecord(ctx->events[p], st));
+  }
+  CK(cudaStreamSynchronize(st));
+  // ---- outputs ----
+  std::vector<int> stv((size_t)(4 * B)), fb((size_t)B);
+  CK(cudaMemcpy(stv.data(), ctx->bt_status.get(), stv.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(fb.data(), ctx->bt_fb.get(), fb.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  if (taus) CK(cudaMemcpy(taus, ctx->bt_taus.get(), (size_t)(B * p_bar) * sizeof(double), cudaMemcpyDeviceToHost));
+  if (coefs) CK(cudaMemcpy(coefs, ctx->bt_coefs.get(), (size_t)(B * ncoef) * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int64_t b = 0; b < B; ++b) {
+    if (status_out)
+      for (int k = 0; k < 3; ++k) status_out[3 * b + k] = stv[4 * b + k];
+    if (fallback_out) fallback_out[b] = fb[b];
+  }
+  if (lag_seconds)
+    for (int p = 1; p <= p_bar; ++p) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ctx->events[p - 1], ctx->events[p]));
+      lag_seconds[p - 1] = ms * 1e-3;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // single operations
 __global__ void k_partials(const double* s, const double* r, int64_t w, double* chunkA,
                            double* chunkB, double* tileA, double* tileB) {
@@ -995,7 +1196,7 @@ static void rh_factor(tf_context* ctx, const FwdRows& ld, int64_t rows, int K, d
 
 static void launch_draw_on(tf_context* ctx, const double* scores, int64_t w, uint64_t seed,
                            int64_t c, int64_t* idx, double* wts, const uint64_t* seed_ptr = nullptr) {
-  DrawArgs a;
+  DrawArgs a{};
   a.shard = 0;
   a.accept = nullptr;
   a.seed_ptr = seed_ptr;
@@ -1468,7 +1669,7 @@ static int64_t shard_sample(tf_context* ctx, uint64_t seed, double s_total, doub
   double* dev = ctx->sh_buf.get();
   CK(cudaMemcpyAsync(dev + 3, &r_glob, sizeof(double), cudaMemcpyHostToDevice, st));
   launch_scan(ctx, ntile, 0, 0, 0, dev + 3);  // local tile prefix, mass with the global R
-  DrawArgs a;
+  DrawArgs a{};
   a.seed = seed;
   a.c = c;
   a.scal = ctx->scal.get();
@@ -2014,6 +2215,12 @@ void tf_destroy(tf_context* ctx) {
   ctx->rh_fupw.release(); ctx->rh_ones.release(); ctx->rh_norm.release(); ctx->rh_Gp.release();
   ctx->rh_H0.release(); ctx->rh_W.release(); ctx->rh_S.release(); ctx->rh_phis.release();
   ctx->rh_rest.release(); ctx->rh_part.release(); ctx->seedtab.release();
+  ctx->bt_y.release(); ctx->bt_s.release(); ctx->bt_r.release(); ctx->bt_cA.release(); ctx->bt_cB.release();
+  ctx->bt_tA.release(); ctx->bt_tB.release(); ctx->bt_OT.release(); ctx->bt_scal.release(); ctx->bt_Rh.release();
+  ctx->bt_Sh.release(); ctx->bt_phi.release(); ctx->bt_coefs.release(); ctx->bt_taus.release();
+  ctx->bt_wts.release(); ctx->bt_S0.release(); ctx->bt_S1.release(); ctx->bt_fw.release(); ctx->bt_idx.release();
+  ctx->bt_fidx.release(); ctx->bt_seed.release(); ctx->bt_status.release(); ctx->bt_fb.release();
+  ctx->bt_guide.release(); ctx->bt_method.release();
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -2042,6 +2249,47 @@ tf_status tf_lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, co
   return guarded(ctx, [&] {
     cudaSetDevice(ctx->device);
     tfe::lsar_sweep(ctx, p_bar, c, seed, diag, taus, coefs_packed, lag_seconds, p_star);
+  });
+}
+
+tf_status tf_lsar_sweep_batch(tf_context* ctx, const double* y, int64_t y_stride, int64_t batch, int64_t n,
+                              int p_bar, int64_t c, const uint64_t* seeds, const int64_t* fixed_idx,
+                              const double* fixed_w, double* taus, double* coefs_packed, double* lag_seconds,
+                              int* p_star, int* status_out) {
+  if (!ctx || !y || !seeds || batch < 1) return TF_USAGE;
+  return guarded(ctx, [&] {
+    cudaSetDevice(ctx->device);
+    const int64_t ncoef = (int64_t)p_bar * (p_bar + 1) / 2;
+    std::vector<double> t((size_t)(batch * std::max(p_bar, 1))), cf((size_t)(batch * std::max<int64_t>(ncoef, 1)));
+    std::vector<int> stv((size_t)(3 * batch)), fb((size_t)batch);
+    tfe::lsar_batch(ctx, y, y_stride, batch, n, p_bar, c, seeds, fixed_idx, fixed_w, t.data(), cf.data(),
+                    lag_seconds, stv.data(), fb.data());
+    // series whose sampled system broke down: the single-series path (shifted
+    // CholeskyQR3 / minimum-norm answers, tf_lsar_sweep)
+    for (int64_t b = 0; b < batch; ++b) {
+      if (!fb[b]) continue;  // (a flagged fit's later lags ran on stale state: its status is moot)
+      stv[3 * b] = stv[3 * b + 1] = stv[3 * b + 2] = 0;
+      tfe::upload_series(ctx, y + b * y_stride, n, false);
+      tf_lsar_diag d{};
+      if (fixed_idx && fixed_w) {
+        d.fixed_idx = fixed_idx + b * p_bar * c;
+        d.fixed_w = fixed_w + b * p_bar * c;
+      }
+      try {
+        tfe::lsar_sweep(ctx, p_bar, c, seeds[b], (fixed_idx && fixed_w) ? &d : nullptr, t.data() + b * p_bar,
+                        cf.data() + b * ncoef, nullptr, nullptr);
+      } catch (const tfe::TfError& e) {
+        stv[3 * b] = e.code == TF_USAGE ? kErrUsage : e.code == TF_DATA ? kErrData : kErrNumerical;
+        stv[3 * b + 2] = kReasonCholFail;
+      }
+    }
+    for (int64_t b = 0; b < batch; ++b) {
+      if (taus) std::memcpy(taus + b * p_bar, t.data() + b * p_bar, p_bar * sizeof(double));
+      if (coefs_packed) std::memcpy(coefs_packed + b * ncoef, cf.data() + b * ncoef, ncoef * sizeof(double));
+      if (p_star) p_star[b] = stv[3 * b] ? 0 : tf_select_order(t.data() + b * p_bar, p_bar, 1.96 / std::sqrt((double)c));
+      if (status_out)
+        for (int k = 0; k < 3; ++k) status_out[3 * b + k] = stv[3 * b + k];
+    }
   });
 }
 

@@ -70,6 +70,12 @@ struct tf_context {
   int64_t sh_c = 0, sh_w = 0, sh_k = 0;
   tfe::DBuf<double> sh_buf, sh_wts;
   tfe::DBuf<int64_t> sh_idx;
+  // batched LSAR sweeps of equal-shape series (tf_lsar_sweep_batch)
+  tfe::DBuf<double> bt_y, bt_s, bt_r, bt_cA, bt_cB, bt_tA, bt_tB, bt_OT, bt_scal, bt_Rh, bt_Sh, bt_phi,
+      bt_coefs, bt_taus, bt_wts, bt_S0, bt_S1, bt_fw;
+  tfe::DBuf<int64_t> bt_idx, bt_fidx;
+  tfe::DBuf<uint64_t> bt_seed;
+  tfe::DBuf<int> bt_status, bt_fb, bt_guide, bt_method;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;  // span of the last sweep
   tfe::GraphCache lsar_graph, rh_graph;
   tfe::DBuf<uint64_t> seedtab;

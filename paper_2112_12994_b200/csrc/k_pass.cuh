@@ -63,7 +63,22 @@ struct PassArgs {
   double* tileA;
   double* tileB;
   int64_t ylen;      // readable doubles at y (series + zero pad)
+  // batched sweeps (k_lsar_pass only): series b = blockIdx.y reads / writes
+  // every array at base + b * stride (0 for a single series)
+  int64_t bs_y, bs_w, bs_chunk, bs_tile, bs_phi, bs_scal;
 };
+
+__device__ __forceinline__ void pass_batch_offset(PassArgs& a, int64_t b) {
+  a.y += b * a.bs_y;
+  a.s += b * a.bs_w;
+  a.r += b * a.bs_w;
+  a.chunkA += b * a.bs_chunk;
+  a.chunkB += b * a.bs_chunk;
+  a.tileA += b * a.bs_tile;
+  a.tileB += b * a.bs_tile;
+  a.phi += b * a.bs_phi;
+  a.Rprev += b * a.bs_scal;
+}
 
 
 inline size_t pass_smem_bytes(int q) {
@@ -118,6 +133,7 @@ __device__ __forceinline__ void pass_partials(const PassArgs& a, const double* s
 
 __global__ void __launch_bounds__(kPassThreads, 4) k_lsar_pass(PassArgs a) {
   extern __shared__ double sm[];
+  if (blockIdx.y) pass_batch_offset(a, blockIdx.y);
   const int q = a.q;
   const int tid = threadIdx.x;
   const int phi_n = ((q + 1) & ~1) + 2;

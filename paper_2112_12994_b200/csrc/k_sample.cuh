@@ -67,8 +67,19 @@ __global__ void __launch_bounds__(kScanThreads)
     k_lag_scan(const double* __restrict__ tA, const double* __restrict__ tB, int64_t ntile,
                double* __restrict__ OT, double* scal, double* Rhist, double* Shist, int lag,
                int check_r, int* status, int unit_r = 0, const double* r_fixed = nullptr,
-               int* __restrict__ guide = nullptr) {
+               int* __restrict__ guide = nullptr, int64_t bs_tile = 0, int bs_hist = 0) {
   __shared__ double red[kScanThreads];
+  if (blockIdx.x) {  // batched sweeps: series b = blockIdx.x (4 scalars, 4 status words each)
+    const int64_t b = blockIdx.x;
+    tA += b * bs_tile;
+    tB += b * bs_tile;
+    OT += b * bs_tile;
+    scal += 4 * b;
+    status += 4 * b;
+    if (Rhist) Rhist += b * bs_hist;
+    if (Shist) Shist += b * bs_hist;
+    if (guide) guide += b * (guide_buckets(ntile) + 1);
+  }
   __shared__ double wsum[32];
   const int tid = threadIdx.x;
   const int64_t seg = (ntile + kScanThreads - 1) / kScanThreads;
@@ -162,6 +173,8 @@ struct DrawArgs {
   double offset;
   int is_last;
   int* accept;
+  // batched sweeps: series b = blockIdx.y at base + b * stride
+  int64_t bs_w, bs_chunk, bs_tile, bs_seed;
 };
 
 constexpr int kDrawThreads = 256;
@@ -233,6 +246,21 @@ __device__ __forceinline__ int group_pick(const DrawGroup& g, const double (&m)[
 
 __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
   const DrawGroup g;
+  if (blockIdx.y) {
+    const int64_t b = blockIdx.y;
+    a.scal += 4 * b;
+    a.OT += b * a.bs_tile;
+    if (a.guide) a.guide += b * (guide_buckets(a.ntile) + 1);
+    a.tA += b * a.bs_tile;
+    a.tB += b * a.bs_tile;
+    a.chunkA += b * a.bs_chunk;
+    a.chunkB += b * a.bs_chunk;
+    a.s += b * a.bs_w;
+    if (a.r) a.r += b * a.bs_w;
+    a.idx += b * a.c;
+    a.wts += b * a.c;
+    if (a.seed_ptr) a.seed_ptr += b * a.bs_seed;
+  }
   const int64_t t = (int64_t)blockIdx.x * kDrawPerCta + (threadIdx.x / kDrawL);
   if (t >= a.c) return;  // group-uniform
   const double R = a.scal[0], S = a.scal[1];
