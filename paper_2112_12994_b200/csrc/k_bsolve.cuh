@@ -25,6 +25,7 @@ namespace tfk {
 
 constexpr int kBsMaxK = 64;
 constexpr int kBsLd = 66;     // shared row stride (doubles): 16-byte rows, spread banks
+constexpr int kBsALd = 65;    // gathered chunk rows: odd stride, lane-per-row reads conflict free
 constexpr int kBsCh = 32;     // rows per gathered chunk
 constexpr int kBsThreads = 256;
 constexpr int kBsSLd = 64;    // global S stride (dense K x K per series)
@@ -112,9 +113,7 @@ __global__ void __launch_bounds__(kBsThreads, 2) k_bsolve(BSolveArgs a) {
     }
     bj = bi + rem;
   }
-  // chunk A M: thread owns rows 2 ri, 2 ri + 1 and columns 4 cj .. 4 cj + 3
-  const int ri = tid >> 4, cj = tid & 15;
-  const int qk = min(K, 4 * cj + 4);  // M upper: rows k <= column
+  const int lane = tid & 31, warp = tid >> 5;
   const int nch = (int)((c + kBsCh - 1) / kBsCh);
   int passes = 0, need_b = (p == 1);
   for (int pass = 0; pass < 2; ++pass) {
@@ -136,14 +135,14 @@ __global__ void __launch_bounds__(kBsThreads, 2) k_bsolve(BSolveArgs a) {
       sW[slot][tid] = t < c ? wt[t] : 0.0;
     };
     auto issue = [&](int ch) {
-      double* dst = Ab + (ch & 1) * kBsCh * kBsLd;
+      double* dst = Ab + (ch & 1) * kBsCh * kBsALd;
       const int slot = ch % 3;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int e = tid + kBsThreads * u, r = e >> 6, k = e & 63;
         const int64_t off = sIdx[slot][r];
         const bool ok = off >= 0 && k < K;
-        const unsigned d = (unsigned)__cvta_generic_to_shared(dst + r * kBsLd + k);
+        const unsigned d = (unsigned)__cvta_generic_to_shared(dst + r * kBsALd + k);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(ok ? y + off + k : y),
                      "r"(ok ? 8 : 0)
                      : "memory");
@@ -167,31 +166,32 @@ __global__ void __launch_bounds__(kBsThreads, 2) k_bsolve(BSolveArgs a) {
         nidx = t < c ? idx[t] : -1;
         nw = t < c ? wt[t] : 0.0;
       }
-      // Q = diag(w) (Y M) for the chunk (32 x K)
-      const double* As = Ab + (ch & 1) * kBsCh * kBsLd;
-      if (4 * cj < K) {
-        double q0[4] = {0.0, 0.0, 0.0, 0.0}, q1[4] = {0.0, 0.0, 0.0, 0.0};
-        const double* a0 = As + (2 * ri) * kBsLd;
-        const double* a1 = a0 + kBsLd;
-        for (int k = 0; k < qk; ++k) {
-          const double2 m01 = *reinterpret_cast<const double2*>(Ms + k * kBsLd + 4 * cj);
-          const double2 m23 = *reinterpret_cast<const double2*>(Ms + k * kBsLd + 4 * cj + 2);
-          const double x0 = a0[k], x1 = a1[k];
-          q0[0] = fma(x0, m01.x, q0[0]);
-          q0[1] = fma(x0, m01.y, q0[1]);
-          q0[2] = fma(x0, m23.x, q0[2]);
-          q0[3] = fma(x0, m23.y, q0[3]);
-          q1[0] = fma(x1, m01.x, q1[0]);
-          q1[1] = fma(x1, m01.y, q1[1]);
-          q1[2] = fma(x1, m23.x, q1[2]);
-          q1[3] = fma(x1, m23.y, q1[3]);
+      // Q = diag(w) (Y M) for the chunk (32 x K): lane = chunk row, warp w
+      // takes column groups w and 15 - w (4 columns each; the triangular
+      // depths of the pair sum to a constant, and every lane of a warp runs
+      // the same depth -- no divergence)
+      const double* As = Ab + (ch & 1) * kBsCh * kBsALd;
+      {
+        const double* arow = As + lane * kBsALd;
+        const double wr = sW[ch % 3][lane];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cg = h ? 15 - warp : warp;
+          if (4 * cg >= K) continue;
+          const int qk = min(K, 4 * cg + 4);  // M upper: rows k <= column
+          double q[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int k = 0; k < qk; ++k) {
+            const double2 m01 = *reinterpret_cast<const double2*>(Ms + k * kBsLd + 4 * cg);
+            const double2 m23 = *reinterpret_cast<const double2*>(Ms + k * kBsLd + 4 * cg + 2);
+            const double x = arow[k];
+            q[0] = fma(x, m01.x, q[0]);
+            q[1] = fma(x, m01.y, q[1]);
+            q[2] = fma(x, m23.x, q[2]);
+            q[3] = fma(x, m23.y, q[3]);
+          }
+          *reinterpret_cast<double2*>(Qs + lane * kBsLd + 4 * cg) = make_double2(wr * q[0], wr * q[1]);
+          *reinterpret_cast<double2*>(Qs + lane * kBsLd + 4 * cg + 2) = make_double2(wr * q[2], wr * q[3]);
         }
-        const double w0 = sW[ch % 3][2 * ri], w1 = sW[ch % 3][2 * ri + 1];
-        *reinterpret_cast<double2*>(Qs + (2 * ri) * kBsLd + 4 * cj) = make_double2(w0 * q0[0], w0 * q0[1]);
-        *reinterpret_cast<double2*>(Qs + (2 * ri) * kBsLd + 4 * cj + 2) = make_double2(w0 * q0[2], w0 * q0[3]);
-        *reinterpret_cast<double2*>(Qs + (2 * ri + 1) * kBsLd + 4 * cj) = make_double2(w1 * q1[0], w1 * q1[1]);
-        *reinterpret_cast<double2*>(Qs + (2 * ri + 1) * kBsLd + 4 * cj + 2) =
-            make_double2(w1 * q1[2], w1 * q1[3]);
       }
       __syncthreads();
       if (gact) {
