@@ -496,7 +496,8 @@ def lsar_fit_batch(series_list, p_bar: int, c: int, seeds, *, engine: Engine | N
     series_list: equal-length series (a list or a (B, n) array), or a single
     TimeSeries / 1-D array fitted once per seed (the reference's multi-seed
     run_compare / run_sweep loops, bench.cpp:183-188, 221-228).  p_bar <= 63.
-    per_lag_seconds are the batch's per-lag device times.  errors="raise"
+    per_lag_seconds are the batch's per-lag device times divided by the
+    number of fits (the amortised cost of one fit).  errors="raise"
     raises the first failing fit's UsageError / DataError / NumericalError;
     "return" puts the exception in that fit's slot instead."""
     eng = engine or default_engine()
@@ -523,8 +524,17 @@ def lsar_fit_batch(series_list, p_bar: int, c: int, seeds, *, engine: Engine | N
                 raise err
             fits.append(err)
             continue
-        fits.append(_finish("lsar", taus[b], coefs[b], secs, int(pstar[b]), p_bar, c))
+        fits.append(_finish("lsar", taus[b], coefs[b], secs / len(seeds), int(pstar[b]), p_bar, c))
     return fits
+
+
+def _lsar_reps(series: TimeSeries, p_bar: int, c: int, seeds, workers: int) -> list:
+    """The LSAR repetitions of run_compare / run_sweep (many seeds over one
+    series): one batched sweep sharing the series (tf_lsar_sweep_batch,
+    y_stride 0) where the batch supports p_bar, else concurrent single fits."""
+    if 1 <= p_bar <= 63:
+        return lsar_fit_batch(series, p_bar, c, seeds)
+    return fit_many([series] * len(seeds), "lsar", p_bar, c, seeds, workers=workers)
 
 
 def rh_fit(series: TimeSeries, p_bar: int, c: int, config: RHConfig | None = None, seed: int = 0, *,
@@ -795,8 +805,7 @@ def run_compare(series: TimeSeries, p_bar: int, c: int, reps: int, trim_fraction
     if not (0.0 <= trim_fraction < 0.5):
         raise UsageError("trim fraction must lie in [0, 0.5)")
     exact = exact_fit(series, p_bar)
-    lsar_runs = fit_many([series] * reps, "lsar", p_bar, c, [derive_seed(seed, 0x1000 + r) for r in range(reps)],
-                         workers=workers)
+    lsar_runs = _lsar_reps(series, p_bar, c, [derive_seed(seed, 0x1000 + r) for r in range(reps)], workers)
     rh_runs = fit_many([series] * reps, "rh", p_bar, c, [derive_seed(seed, 0x2000 + r) for r in range(reps)],
                        workers=workers)
     if not with_timing:
@@ -823,7 +832,8 @@ def run_sweep(series: TimeSeries, c_list, p_bar: int, reps: int, trim_fraction: 
         for method in ("lsar", "rh"):
             tag = 0x10000 if method == "lsar" else 0x20000
             seeds = [derive_seed(seed, (ci << 20) + tag + r) for r in range(reps)]
-            runs = fit_many([series] * reps, method, p_bar, c, seeds, workers=workers)
+            runs = (_lsar_reps(series, p_bar, c, seeds, workers) if method == "lsar"
+                    else fit_many([series] * reps, method, p_bar, c, seeds, workers=workers))
             if not with_timing:
                 for f in runs:
                     _strip_timing(f)

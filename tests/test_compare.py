@@ -57,7 +57,7 @@ def test_run_compare_aggregates_repetitions():
     # one repetition, no trimming: that run's direct error (test_bench.cpp:136-144)
     single = tf.run_compare(s, 5, 300, 1, 0.0, 21, False)
     exact = tf.exact_fit(s, 5)
-    one = tf.lsar_fit(s, 5, 300, tf.derive_seed(21, 0x1000))
+    one = tf.lsar_fit_batch(s, 5, 300, [tf.derive_seed(21, 0x1000)])[0]  # the repetitions' batched path
     for h in range(5):
         direct = tf.relative_error_pct(one.per_lag_coefficients[h], exact.per_lag_coefficients[h])
         assert abs(single.lsar.trimmed_error_pct[h] - direct) <= 1e-12 * max(direct, 1e-300)
