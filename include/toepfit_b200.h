@@ -50,7 +50,8 @@ typedef struct tf_context tf_context;
 
 typedef struct {
   int device;    /* CUDA device ordinal */
-  int reserved;  /* must be 0 */
+  int priority;  /* stream priority: 0 = default, k > 0 = k levels above it (clamped to the
+                    device range) -- lets a latency-bound fit run ahead of concurrent ones */
 } tf_opts;
 
 /* RHConfig (repeated_halving.hpp:56-65) */

@@ -20,7 +20,7 @@ _i32p = C.POINTER(C.c_int)
 
 
 class TfOpts(C.Structure):
-    _fields_ = [("device", C.c_int), ("reserved", C.c_int)]
+    _fields_ = [("device", C.c_int), ("priority", C.c_int)]
 
 
 class TfRhCfg(C.Structure):

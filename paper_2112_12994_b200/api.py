@@ -170,10 +170,12 @@ def derive_seed(seed: int, tag: int) -> int:
 class Engine:
     """One tf_context (one CUDA device, one stream) with a resident series."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, priority: int = 0):
+        """priority: CUDA stream priority levels above the default (concurrent
+        contexts on one GPU: the higher one's kernels are scheduled first)."""
         L = _abi.lib()
         self._ctx = C.c_void_p()
-        opts = _abi.TfOpts(device=device, reserved=0)
+        opts = _abi.TfOpts(device=device, priority=int(priority))
         st = L.tf_create(C.byref(opts), C.byref(self._ctx))
         if st != _abi.TF_OK:
             raise CudaError(f"tf_create failed (status {st}); no usable CUDA device")

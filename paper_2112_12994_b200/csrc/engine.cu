@@ -1238,8 +1238,35 @@ static void rowsq_attr() {
 }
 
 // scores of every window row t in [0, rows): out[t] = ||x_t W||^2 (Hankel tiles)
+// columns of W handled by DMMA tiles: a last tile of <= kTailMax columns goes
+// to k_rowsq_tail instead (N = 129 sketch rows: 128 + 1)
+static inline int rowsq_main_cols(int N) {
+  const int rem = N % 64;
+  return (N > 64 && rem != 0 && rem <= kTailMax) ? N - rem : N;
+}
+
+template <class L, class WL>
+static void rowsq_tail(tf_context* ctx, const L& ld, int64_t rows, int K, const WL& wl, int N0, int N, double* out,
+                       int add) {
+  if (N0 >= N || rows <= 0) return;
+  const int T = N - N0;
+  const size_t smem = sizeof(double) * (size_t)K * T;
+  auto go = [&](auto kern, int rw) {
+    smem_optin((const void*)kern, smem);
+    const int64_t wblocks = (rows + 32LL * rw - 1) / (32LL * rw);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((wblocks + 7) / 8, 8LL * ctx->sm_count));
+    kern<<<grid, 256, smem, ctx->stream>>>(ld, rows, K, wl, N0, N, out, add);
+  };
+  if (T <= 2) go(k_rowsq_tail<L, WL, 2, 8>, 8);
+  else if (T <= 12) go(k_rowsq_tail<L, WL, 12, 4>, 4);
+  else go(k_rowsq_tail<L, WL, 16, 2>, 2);
+  LAUNCH_CHECK("k_rowsq_tail");
+  COUNT_LAUNCH();
+}
+
 template <class WL, bool UPPER>
-static void rowsq_all_rows(tf_context* ctx, int64_t rows, int K, const WL& wl, int N, double* out) {
+static void rowsq_all_rows(tf_context* ctx, int64_t rows, int K, const WL& wl, int Nfull, double* out) {
+  const int N = rowsq_main_cols(Nfull);
   const int ntiles = (N + 63) / 64;
   if (ntiles > 8) throw TfError{TF_USAGE, "row-score tiles > 8"};
   const size_t smem = rowsq_hankel_smem(K);
@@ -1268,11 +1295,13 @@ static void rowsq_all_rows(tf_context* ctx, int64_t rows, int K, const WL& wl, i
     const int want = (int)std::lround(acc / wsum * total);
     plan.first[j + 1] = std::max(plan.first[j] + 1, std::min(want, total - (ntiles - 1 - j)));
   }
-  ctx->rh_part.need((size_t)ntiles * rows);
+  const int nparts = ntiles + (Nfull > N ? 1 : 0);
+  ctx->rh_part.need((size_t)nparts * rows);
   k_rowsq_hankel<WL, UPPER><<<plan.first[ntiles], kHkThreads, smem, ctx->stream>>>(
       ctx->y.get(), ctx->n, rows, K, wl, N, plan, ctx->rh_part.get());
   LAUNCH_CHECK("k_rowsq_hankel");
-  k_rowsq_combine<<<grid_for(rows, ctx), 256, 0, ctx->stream>>>(ctx->rh_part.get(), rows, ntiles, out);
+  rowsq_tail(ctx, WinRows{ctx->y.get(), nullptr}, rows, K, wl, N, Nfull, ctx->rh_part.get() + (size_t)ntiles * rows, 0);
+  k_rowsq_combine<<<grid_for(rows, ctx), 256, 0, ctx->stream>>>(ctx->rh_part.get(), rows, nparts, out);
   LAUNCH_CHECK("k_rowsq_combine");
   g_launches += 2;
 }
@@ -1442,10 +1471,12 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
     } else {
       WinRows rows_i{y, level_ptr(i)};
       rowsq_attr<WinRows, DenseW, false>();
+      const int gm = rowsq_main_cols(g);
       k_rowsq<WinRows, DenseW, false><<<(unsigned)((len + 63) / 64), kGramThreads, kRowsqSmem, st>>>(
-          rows_i, len, K, DenseW{ctx->rh_W.get(), g}, g, ctx->rh_scores.get());
+          rows_i, len, K, DenseW{ctx->rh_W.get(), g}, gm, ctx->rh_scores.get());
       LAUNCH_CHECK("k_rowsq");
       COUNT_LAUNCH();
+      rowsq_tail(ctx, rows_i, len, K, DenseW{ctx->rh_W.get(), g}, gm, g, ctx->rh_scores.get(), 1);
     }
     const int64_t* sidx = ctx->rh_sidx.get();
     const double* sw = ctx->rh_sw.get();
@@ -1476,10 +1507,12 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
       rowsq_all_rows<TpuW, true>(ctx, m, K, TpuW{ctx->rh_S.get(), K}, K, ctx->rh_scores.get());
     } else {
       rowsq_attr<WinRows, TpuW, true>();
+      const int km = rowsq_main_cols(K);
       k_rowsq<WinRows, TpuW, true><<<(unsigned)((m + 63) / 64), kGramThreads, kRowsqSmem, st>>>(
-          WinRows{y, nullptr}, m, K, TpuW{ctx->rh_S.get(), K}, K, ctx->rh_scores.get());
+          WinRows{y, nullptr}, m, K, TpuW{ctx->rh_S.get(), K}, km, ctx->rh_scores.get());
       LAUNCH_CHECK("k_rowsq");
       COUNT_LAUNCH();
+      rowsq_tail(ctx, WinRows{y, nullptr}, m, K, TpuW{ctx->rh_S.get(), K}, km, K, ctx->rh_scores.get(), 1);
     }
     score_distribution(ctx, ctx->rh_scores.get(), m);
   }
@@ -2180,7 +2213,10 @@ tf_status tf_create(const tf_opts* opts, tf_context** out) {
     const char* v = std::getenv("TF_NO_GRAPHS");  // debugging: launch every sweep eagerly
     ctx->no_graphs = v && v[0] == '1';
   }
-  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  const int prio = std::max(greatest, least - std::max(0, opts ? opts->priority : 0));
+  if (cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, prio) != cudaSuccess) {
     delete ctx;
     return TF_CUDA;
   }

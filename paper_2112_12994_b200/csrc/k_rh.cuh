@@ -314,6 +314,7 @@ struct WinRows {  // unweighted forward rows y[b_t .. b_t + K); idx nullable -> 
   __device__ __forceinline__ double operator()(int64_t t, int col) const {
     return y[(idx ? idx[t] : t) + col];
   }
+  __device__ __forceinline__ const double* row(int64_t t) const { return y + (idx ? idx[t] : t); }
 };
 struct DenseW {
   const double* w;
@@ -517,6 +518,61 @@ __global__ void __launch_bounds__(kHkThreads)
     const int64_t t0 = b * kHkRows;
     if (tid < kHkRows && t0 + tid < rows) part[(size_t)tile * rows + t0 + tid] = red[0][tid] + red[1][tid];
     buf ^= 1;
+  }
+}
+
+// Narrow last column tile of W (N - N0 <= kTailMax columns, e.g. the 129th
+// sketch row g = ceil(8 ln m)): out[t] (+)= sum_j (x_t . W[:, j])^2 on the
+// CUDA cores, one row per thread (K fmas per column), W's tail columns in
+// shared memory.  A DMMA tile pass for one or a few columns would pay a whole
+// tile's loads and barriers for 1/8 of a fragment of work.
+constexpr int kTailMax = 16;
+// MT: max tail columns, RW: rows per thread (32 apart: coalesced loads; one
+// W read serves RW rows); instantiated as <2, 8>, <12, 4>, <16, 2>
+template <class L, class WL, int MT, int RW>
+__global__ void __launch_bounds__(256) k_rowsq_tail(L ld, int64_t rows, int K, WL wl, int N0, int N,
+                                                    double* __restrict__ out, int add) {
+  extern __shared__ double wtail[];  // [K][T]
+  const int T = N - N0;
+  for (int e = threadIdx.x; e < K * T; e += blockDim.x) wtail[e] = wl(e / T, N0 + e % T);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nblk = (rows + 32 * RW - 1) / (32 * RW);  // 256-row warp blocks
+  for (int64_t wb = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; wb < nblk;
+       wb += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int64_t t0 = wb * 32 * RW + lane;
+    const double* row[RW];
+#pragma unroll
+    for (int r = 0; r < RW; ++r) row[r] = ld.row(min(t0 + 32 * r, rows - 1));
+    double acc[RW][MT];
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
+#pragma unroll
+      for (int j = 0; j < MT; ++j) acc[r][j] = 0.0;
+    for (int k = 0; k < K; ++k) {
+      double x[RW];
+#pragma unroll
+      for (int r = 0; r < RW; ++r) x[r] = __ldg(row[r] + k);
+#pragma unroll
+      for (int j = 0; j < MT; ++j) {
+        if (j < T) {
+          const double wv = wtail[k * T + j];
+#pragma unroll
+          for (int r = 0; r < RW; ++r) acc[r][j] = fma(x[r], wv, acc[r][j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const int64_t t = t0 + 32 * r;
+      if (t < rows) {
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < MT; ++j)
+          if (j < T) v = fma(acc[r][j], acc[r][j], v);
+        out[t] = add ? out[t] + v : v;
+      }
+    }
   }
 }
 

@@ -71,7 +71,7 @@ def test_create_without_gpu_fails_loudly(abi):
     if torch.cuda.is_available():
         pytest.skip("GPU present")
     ctx = C.c_void_p()
-    opts = abi.TfOpts(device=0, reserved=0)
+    opts = abi.TfOpts(device=0, priority=0)
     assert abi.lib().tf_create(C.byref(opts), C.byref(ctx)) == abi.TF_CUDA
     import paper_2112_12994_b200 as tf
     with pytest.raises(tf.CudaError):
