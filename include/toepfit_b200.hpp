@@ -201,6 +201,50 @@ inline FitResult lsar_fit(const TimeSeries& series, int p_bar, std::int64_t c, s
   return gpu::finish(PacfMethod::lsar, p_bar, c, taus, packed, std::move(secs), p_star, 0.0);
 }
 
+// Many independent LSAR fits in one batched sweep (tf_lsar_sweep_batch): fit b
+// = lsar_fit(series[b], p_bar, c, seeds[b]); equal-length series, p_bar <= 63.
+// The reference's run_compare / run_sweep repetition loops (bench.cpp:183-188,
+// 221-228) pass the same series for every seed.  Throws the first failing
+// fit's exception.  per_lag_seconds: the batch's per-lag time / fits.
+inline std::vector<FitResult> lsar_fit_batch(const std::vector<TimeSeries>& series, int p_bar, std::int64_t c,
+                                             const std::vector<std::uint64_t>& seeds) {
+  if (series.size() != seeds.size() || series.empty()) throw UsageError("one seed per series, at least one fit");
+  const std::size_t n = series[0].size();
+  std::vector<double> y;
+  y.reserve(n * series.size());
+  for (const TimeSeries& s : series) {
+    if (s.size() != n) throw UsageError("batched fits need equal-length series");
+    y.insert(y.end(), s.values().begin(), s.values().end());
+  }
+  gpu::Context& g = gpu::context();
+  tf_context* ctx = g.get();
+  g.cached = nullptr;  // a re-run fit replaces the resident series
+  const std::int64_t B = (std::int64_t)series.size();
+  const int pb = p_bar > 0 ? p_bar : 1;
+  const std::size_t nc = (std::size_t)pb * (pb + 1) / 2;
+  std::vector<double> taus((std::size_t)B * pb), packed((std::size_t)B * nc), secs(pb);
+  std::vector<int> p_star((std::size_t)B), status((std::size_t)(3 * B));
+  gpu::raise(tf_lsar_sweep_batch(ctx, y.data(), (std::int64_t)n, B, (std::int64_t)n, p_bar, c, seeds.data(),
+                                 nullptr, nullptr, taus.data(), packed.data(), secs.data(), p_star.data(),
+                                 status.data()),
+             ctx);
+  for (double& s : secs) s /= (double)B;
+  std::vector<FitResult> out;
+  for (std::int64_t b = 0; b < B; ++b) {
+    if (status[3 * b]) {
+      const std::string what = "fit " + std::to_string(b) + " failed at lag " + std::to_string(status[3 * b + 1]);
+      if (status[3 * b] == 1) throw UsageError(what);
+      if (status[3 * b] == 2) throw DataError(what);
+      throw NumericalError(what);
+    }
+    out.push_back(gpu::finish(PacfMethod::lsar, p_bar, c,
+                              std::vector<double>(taus.begin() + b * pb, taus.begin() + (b + 1) * pb),
+                              std::vector<double>(packed.begin() + b * nc, packed.begin() + (b + 1) * nc), secs,
+                              p_star[b], 0.0));
+  }
+  return out;
+}
+
 inline FitResult rh_fit(const TimeSeries& series, int p_bar, std::int64_t c, const RHConfig* config,
                         std::uint64_t seed) {
   gpu::Context& g = gpu::context();

@@ -37,6 +37,11 @@ int main(int argc, char** argv) {
   print_fit("rh", toepfit::rh_fit(series, p_bar, c, seed), true);
   print_fit("srht", toepfit::srht_fit(series, p_bar, c, seed), true);
   print_fit("exact", toepfit::exact_fit(series, p_bar), true);
+  {  // batched: two seeds over the same series
+    const auto fits = toepfit::lsar_fit_batch({series, series}, p_bar, c, {seed, seed + 1});
+    print_fit("batch0", fits[0], true);
+    print_fit("batch1", fits[1], true);
+  }
   // error mapping (errors.hpp:12-29 types)
   int usage = 0, data = 0, numerical = 0;
   try {

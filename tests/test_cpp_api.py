@@ -38,4 +38,7 @@ def test_cpp_api_matches_python(tmp_path):
     assert res["srht"]["taus"] == sr.pacf.taus and res["srht"]["p_star"] == sr.p_star
     assert res["exact"]["taus"] == ex.pacf.taus and res["exact"]["p_star"] == ex.p_star
     assert res["errors"] == {"usage": 1, "data": 1, "numerical": 1}
+    bt = tf.lsar_fit_batch(s, 16, 900, [11, 12], engine=eng)
+    assert res["batch0"]["taus"] == bt[0].pacf.taus and res["batch1"]["taus"] == bt[1].pacf.taus
+    assert res["batch0"]["p_star"] == bt[0].p_star
     eng.close()
