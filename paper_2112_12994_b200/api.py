@@ -57,9 +57,8 @@ class TimeSeries:
         v = np.array(values, dtype=np.float64, copy=copy).ravel()
         if v.size == 0:
             raise DataError("series must contain at least one value")
-        bad = np.flatnonzero(~np.isfinite(v))
-        if bad.size:
-            raise DataError(f"series value at position {int(bad[0])} is not finite")
+        if not np.isfinite(v).all():
+            raise DataError(f"series value at position {int(np.flatnonzero(~np.isfinite(v))[0])} is not finite")
         v.setflags(write=False)
         self._v = v
         self.label = label
@@ -202,6 +201,7 @@ class Engine:
         if self._series_id is not None and self._series_id[0] is series:
             return
         v = series.values()
+        self._series_id = None  # a failed upload leaves no series resident
         self._check(_abi.lib().tf_upload_series(self._ctx, ptr(v), v.size))
         self._series_id = (series,)
 

@@ -82,6 +82,7 @@ template struct DBuf<int>;
 template struct DBuf<uint64_t>;
 template struct DBuf<unsigned char>;
 template struct DBuf<long long>;
+template struct DBuf<unsigned long long>;
 
 static const char* reason_text(int reason) {
   switch (reason) {
@@ -1024,19 +1025,33 @@ __global__ void k_materialize(FwdRows ld, int64_t c, int p, int width, double* a
   }
 }
 
+// first non-finite position (series.cpp:23-32 validation), on the device
+__global__ void k_first_nonfinite(const double* __restrict__ y, int64_t n, unsigned long long* first) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(y[i])) atomicMin(first, (unsigned long long)i);
+}
+
 static void upload_series(tf_context* ctx, const double* y, int64_t n, bool device_src) {
   if (n < 1 || !y) throw TfError{TF_DATA, "series must contain at least one value"};
-  if (!device_src) {
-    for (int64_t i = 0; i < n; ++i)
-      if (!std::isfinite(y[i]))
-        throw TfError{TF_DATA, "series value at position " + std::to_string(i) + " is not finite"};
-  }
   ctx->y.need(n + 64);
+  ctx->n = 0;  // no valid series until the check below passes
   if (device_src)
     CK(cudaMemcpyAsync(ctx->y.get(), y, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   else
     CK(cudaMemcpyAsync(ctx->y.get(), y, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemsetAsync(ctx->y.get() + n, 0, 64 * sizeof(double), ctx->stream));
+  if (!device_src) {  // the finiteness check runs at HBM speed after the copy (a host loop cost ~10 ms at n = 1e7)
+    ctx->fincheck.need(1);
+    CK(cudaMemsetAsync(ctx->fincheck.get(), 0xff, sizeof(unsigned long long), ctx->stream));
+    const unsigned fgrid = (unsigned)std::min<int64_t>((n + 255) / 256, 8LL * ctx->sm_count);
+    k_first_nonfinite<<<fgrid, 256, 0, ctx->stream>>>(ctx->y.get(), n, ctx->fincheck.get());
+    LAUNCH_CHECK("k_first_nonfinite");
+    unsigned long long first = 0;
+    CK(cudaMemcpyAsync(&first, ctx->fincheck.get(), sizeof(first), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (first < (unsigned long long)n)
+      throw TfError{TF_DATA, "series value at position " + std::to_string(first) + " is not finite"};
+  }
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->n = n;
 }
@@ -2256,7 +2271,7 @@ void tf_destroy(tf_context* ctx) {
   ctx->bt_Sh.release(); ctx->bt_phi.release(); ctx->bt_coefs.release(); ctx->bt_taus.release();
   ctx->bt_wts.release(); ctx->bt_S0.release(); ctx->bt_S1.release(); ctx->bt_fw.release(); ctx->bt_idx.release();
   ctx->bt_fidx.release(); ctx->bt_seed.release(); ctx->bt_status.release(); ctx->bt_fb.release();
-  ctx->bt_guide.release(); ctx->bt_method.release();
+  ctx->bt_guide.release(); ctx->bt_method.release(); ctx->fincheck.release();
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

@@ -76,6 +76,7 @@ struct tf_context {
   tfe::DBuf<int64_t> bt_idx, bt_fidx;
   tfe::DBuf<uint64_t> bt_seed;
   tfe::DBuf<int> bt_status, bt_fb, bt_guide, bt_method;
+  tfe::DBuf<unsigned long long> fincheck;  // upload validation
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;  // span of the last sweep
   tfe::GraphCache lsar_graph, rh_graph;
   tfe::DBuf<uint64_t> seedtab;

@@ -114,3 +114,21 @@ def test_batch_rank_deficient_fit_falls_back(tf, eng):
     for y, s, f in zip(ys, [5, 6, 7], fits):
         g = tf.lsar_fit(tf.TimeSeries(y), 10, 10, s, engine=eng)
         assert f.pacf.taus == g.pacf.taus
+
+
+def test_upload_rejects_non_finite_through_the_abi(tf, eng):
+    # series.cpp:23-32 through tf_upload_series itself (the host mirror's
+    # TimeSeries check bypassed): DataError with the first bad position, and
+    # no series stays resident
+    import ctypes as C
+    from paper_2112_12994_b200 import _abi
+    y = np.arange(10.0)
+    y[7] = np.inf
+    y[8] = np.nan
+    st = _abi.lib().tf_upload_series(eng._ctx, _abi.ptr(y), y.size)
+    assert st == _abi.TF_DATA
+    assert "position 7" in _abi.lib().tf_last_error(eng._ctx).decode()
+    taus = np.zeros(2)
+    st = _abi.lib().tf_lsar_sweep(eng._ctx, 2, 4, C.c_uint64(1), None, _abi.ptr(taus), None, None, None)
+    assert st == _abi.TF_USAGE  # "no series uploaded"
+    eng._series_id = None
