@@ -162,9 +162,9 @@ tf_status tf_hadamard(tf_context* ctx, double* x, int64_t n);
 /* ---- single operations on host buffers (tests, integration) ---- */
 tf_status tf_residuals(tf_context* ctx, const double* y, int64_t n_used, int p, const double* phi,
                        double* r_out);
-/* Draw c rows with probability proportional to scores[i] (scores need not be
- * normalised; sketch.cpp:20-59 with pi = scores / sum). */
-tf_status tf_sample_rows(tf_context* ctx, const double* scores, int64_t n, int64_t c, uint64_t seed,
+/* Draw c rows from the distribution pi (sketch.cpp:20-59): TF_DATA for a
+ * negative entry or |sum pi - 1| > 1e-8 (sketch.cpp:25-32), TF_USAGE for c < 1. */
+tf_status tf_sample_rows(tf_context* ctx, const double* pi, int64_t n, int64_t c, uint64_t seed,
                          int64_t* idx_out, double* w_out);
 /* A_S (c x width, row-major) and b_S of the window system (y, n_used, p). */
 tf_status tf_apply_sample(tf_context* ctx, const double* y, int64_t n_used, int p,

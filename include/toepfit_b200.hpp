@@ -146,6 +146,8 @@ struct Context {
   void upload(const TimeSeries& s) {
     tf_context* c = get();
     if (cached == &s.values() && keep == s.storage()) return;
+    cached = nullptr;  // a failed upload leaves no resident series: force the next upload
+    keep.reset();
     raise(tf_upload_series(c, s.values().data(), (int64_t)s.size()), c);
     cached = &s.values();
     keep = s.storage();

@@ -579,6 +579,9 @@ static void check_lsar_args(const tf_context* ctx, int p_bar, int64_t c) {
   if (ctx->n <= (int64_t)p_bar + 1)
     throw TfError{TF_DATA, "series too short for maximum lag " + std::to_string(p_bar)};
   if (c < p_bar) throw TfError{TF_USAGE, "sample count below maximum lag"};
+  // the fused pass stages a q-sample halo per tile in shared memory
+  if (std::max(PassLayout(p_bar).bytes(), pass_smem_bytes(p_bar)) > (size_t)ctx->smem_optin_max)
+    throw TfError{TF_USAGE, "maximum lag " + std::to_string(p_bar) + " exceeds the fused pass's shared-memory tile"};
 }
 
 // Run a fixed launch sequence through a CUDA graph: the first call for a
@@ -787,6 +790,7 @@ static void lsar_batch(tf_context* ctx, const double* y_host, int64_t y_stride, 
                        int64_t c, const uint64_t* seeds, const int64_t* fixed_idx, const double* fixed_w,
                        double* taus, double* coefs, double* lag_seconds, int* status_out, int* fallback_out) {
   if (B < 1) throw TfError{TF_USAGE, "batch must hold at least one series"};
+  if (B > 65535) throw TfError{TF_USAGE, "batch exceeds 65535 fits per call (launch grid y limit)"};
   if (p_bar < 1) throw TfError{TF_USAGE, "maximum lag must be at least 1"};
   if (p_bar > kBatchMaxPbar)
     throw TfError{TF_USAGE, "batched sweeps support p_bar <= " + std::to_string(kBatchMaxPbar)};
@@ -1033,8 +1037,8 @@ __global__ void k_first_nonfinite(const double* __restrict__ y, int64_t n, unsig
 
 static void upload_series(tf_context* ctx, const double* y, int64_t n, bool device_src) {
   if (n < 1 || !y) throw TfError{TF_DATA, "series must contain at least one value"};
+  ctx->n = 0;  // no valid series until the check below passes (also when the allocation fails)
   ctx->y.need(n + 64);
-  ctx->n = 0;  // no valid series until the check below passes
   if (device_src)
     CK(cudaMemcpyAsync(ctx->y.get(), y, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   else
@@ -1076,8 +1080,17 @@ static void sample_op(tf_context* ctx, const double* scores, int64_t n, int64_t 
                       int64_t* idx_out, double* w_out) {
   if (n < 1) throw TfError{TF_DATA, "empty distribution"};
   if (c < 1) throw TfError{TF_USAGE, "sample count must be positive"};
-  for (int64_t i = 0; i < n; ++i)
+  // sketch.cpp:25-32: entries non-negative, sequential sum within 1e-8 of 1
+  double total = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
     if (!(scores[i] >= 0.0)) throw TfError{TF_DATA, "distribution has a negative entry"};
+    total += scores[i];
+  }
+  if (std::fabs(total - 1.0) > 1e-8) {
+    char buf[96];
+    std::snprintf(buf, sizeof buf, "distribution sums to %g, not 1", total);
+    throw TfError{TF_DATA, buf};
+  }
   const int64_t ntile = (n + kPassTile - 1) / kPassTile;
   alloc_state(ctx, 1, c, n);
   CK(cudaMemcpyAsync(ctx->s.get(), scores, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
@@ -2224,6 +2237,7 @@ tf_status tf_create(const tf_opts* opts, tf_context** out) {
   if (!ctx) return TF_CUDA;
   ctx->device = dev;
   cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&ctx->smem_optin_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   {
     const char* v = std::getenv("TF_NO_GRAPHS");  // debugging: launch every sweep eagerly
     ctx->no_graphs = v && v[0] == '1';
@@ -2244,36 +2258,13 @@ void tf_destroy(tf_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (auto e : ctx->events) cudaEventDestroy(e);
+  for (auto e : ctx->pev) cudaEventDestroy(e);
   if (ctx->ev_begin) cudaEventDestroy(ctx->ev_begin);
+  if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
   if (ctx->lsar_graph.exec) cudaGraphExecDestroy(ctx->lsar_graph.exec);
   if (ctx->rh_graph.exec) cudaGraphExecDestroy(ctx->rh_graph.exec);
-  if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
-  ctx->srht_X.release(); ctx->srht_D.release(); ctx->srht_draws.release(); ctx->srht_reject.release();
-  ctx->y.release(); ctx->s.release(); ctx->r.release(); ctx->chunkA.release(); ctx->chunkB.release();
-  ctx->tileA.release(); ctx->tileB.release(); ctx->OT.release(); ctx->guide.release(); ctx->scal.release();
-  ctx->Rhist.release(); ctx->Shist.release(); ctx->phi.release(); ctx->coefs.release();
-  ctx->taus.release(); ctx->idx.release(); ctx->fidx.release(); ctx->idx_hist.release();
-  ctx->wts.release(); ctx->fw.release(); ctx->w_hist.release(); ctx->status.release();
-  ctx->method.release();
-  tfe::SolveBufs& b = ctx->sb;
-  b.W.release(); b.G.release(); b.RA.release(); b.RB.release(); b.RC.release(); b.SA.release();
-  b.SB.release(); b.SC.release(); b.T.release(); b.S0.release(); b.S1.release(); b.Q1.release();
-  b.Q2.release(); b.M.release(); b.RI.release(); b.flags.release();
-  ctx->rh_J.release(); ctx->rh_cnt.release(); ctx->rh_start.release(); ctx->rh_fill.release();
-  ctx->rh_bk.release(); ctx->rh_pick.release(); ctx->rh_ok.release(); ctx->rh_flag.release();
-  ctx->rh_tsum.release(); ctx->rh_lvl.release(); ctx->rh_aidx.release(); ctx->rh_sidx.release();
-  ctx->rh_fup.release(); ctx->rh_scores.release(); ctx->rh_aw.release(); ctx->rh_sw.release();
-  ctx->rh_fupw.release(); ctx->rh_ones.release(); ctx->rh_norm.release(); ctx->rh_Gp.release();
-  ctx->rh_H0.release(); ctx->rh_W.release(); ctx->rh_S.release(); ctx->rh_phis.release();
-  ctx->rh_rest.release(); ctx->rh_part.release(); ctx->seedtab.release();
-  ctx->bt_y.release(); ctx->bt_s.release(); ctx->bt_r.release(); ctx->bt_cA.release(); ctx->bt_cB.release();
-  ctx->bt_tA.release(); ctx->bt_tB.release(); ctx->bt_OT.release(); ctx->bt_scal.release(); ctx->bt_Rh.release();
-  ctx->bt_Sh.release(); ctx->bt_phi.release(); ctx->bt_coefs.release(); ctx->bt_taus.release();
-  ctx->bt_wts.release(); ctx->bt_S0.release(); ctx->bt_S1.release(); ctx->bt_fw.release(); ctx->bt_idx.release();
-  ctx->bt_fidx.release(); ctx->bt_seed.release(); ctx->bt_status.release(); ctx->bt_fb.release();
-  ctx->bt_guide.release(); ctx->bt_method.release(); ctx->fincheck.release();
   cudaStreamDestroy(ctx->stream);
-  delete ctx;
+  delete ctx;  // DBuf destructors free every device buffer
 }
 
 const char* tf_last_error(const tf_context* ctx) { return ctx ? ctx->err.c_str() : "null context"; }

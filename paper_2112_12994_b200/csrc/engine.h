@@ -21,6 +21,10 @@ template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }  // every buffer of a context is freed by tf_destroy's delete
   void need(size_t count);
   void release();
   T* get() const { return p; }
@@ -46,6 +50,7 @@ struct tf_context {
   cudaStream_t stream = nullptr;
   std::string err;
   int sm_count = 148;
+  int smem_optin_max = 232448;  // cudaDevAttrMaxSharedMemoryPerBlockOptin
   // series
   tfe::DBuf<double> y;
   int64_t n = 0;

@@ -101,6 +101,10 @@ def test_sample_rows_known_answers(eng, tf):
         eng.sample_rows(np.array([0.5, -0.1]), 3, 1)
     with pytest.raises(tf.UsageError):
         eng.sample_rows(np.full(n, 1.0 / n), 0, 1)
+    # sketch.cpp:25-32: the distribution must sum to 1 within 1e-8
+    with pytest.raises(tf.DataError, match="sums to"):
+        eng.sample_rows(np.full(n, 2.0 / n), c, 1)
+    eng.sample_rows(np.full(n, 1.0 / n) * (1 + 5e-9), c, 1)  # inside the tolerance
 
 
 @pytest.mark.parametrize("n,c", [(16, 8), (5000, 2000), (100_003, 20_000), (2048 * 3 + 17, 5000)])
@@ -109,7 +113,7 @@ def test_sample_rows_matches_oracle_draws(orc, eng, n, c):
     s = rng.exponential(size=n) ** 2
     s[rng.integers(0, n, size=n // 10)] = 0.0  # zero-mass rows
     pi = s / s.sum()
-    idx, w = eng.sample_rows(s, c, 1234)
+    idx, w = eng.sample_rows(pi, c, 1234)
     idx_r, w_r = orc.sample_rows(pi, c, 1234)
     agree = np.mean(idx == idx_r)
     assert agree >= 0.999, agree
