@@ -66,21 +66,24 @@ typedef struct {
  * pointers are host pointers and may be NULL. */
 typedef struct {
   const int64_t* fixed_idx; /* [p_bar][c]: replaces sampling (deterministic-index mode) */
-  const double* fixed_w;    /* [p_bar][c] */
+  const double* fixed_w;    /* [p_bar][c]; NULL with fixed_idx: each lag's own weights
+                               1/sqrt(c pi_i) from its distribution (sketch.cpp:56-57) */
   int64_t* idx_out;         /* [p_bar][c] drawn indices */
   double* w_out;            /* [p_bar][c] drawn weights */
   double* rnorm2_out;       /* [p_bar] ||r_p||^2 */
   double* ssum_out;         /* [p_bar] sum of the scores sampled at lag p */
   double* scores_out;       /* [n - p_bar] scores of the last lag */
   double* resid_out;        /* [n - p_bar] residuals of the last lag */
-  int* method_out;          /* [p_bar] 0 CholeskyQR2, 2 shifted CholeskyQR3 */
+  int* method_out;          /* [p_bar] SolveMethod of the lag (toeplitz.hpp:49-56): 0 exact_qr (CPQR
+                               rank = p), 1 exact_svd (rank < p: minimum-norm SVD answer) */
   double* phase_seconds;    /* [p_bar][3] device time of sampling, solve, fused pass */
   int64_t* launches_out;    /* kernel launches issued by the sweep */
+  int* rank_out;            /* [p_bar] CPQR rank of the sampled system (threshold max(c, p) eps) */
 } tf_lsar_diag;
 
 typedef struct {
   const int64_t* fixed_idx;     /* [p_bar][c] per-lag samples (nullable) */
-  const double* fixed_w;
+  const double* fixed_w;        /* [p_bar][c]; NULL with fixed_idx: weights from the final scores */
   const int64_t* fixed_levels;  /* concatenated halving index sets, levels 1..depth (nullable) */
   const int64_t* fixed_up_idx;  /* [depth][sample_count] upward-pass samples (nullable) */
   const double* fixed_up_w;
@@ -92,6 +95,8 @@ typedef struct {
   int64_t* up_idx_out;          /* [depth][sample_count] upward-pass positions */
   double* up_w_out;             /* [depth][sample_count] upward-pass weights */
   int64_t* launches_out;        /* kernel launches issued by the sweep */
+  int* method_out;              /* [p_bar] 0 exact_qr / 1 exact_svd (as tf_lsar_diag) */
+  int* rank_out;                /* [p_bar] CPQR rank */
 } tf_rh_diag;
 
 const char* tf_version(void);
@@ -170,7 +175,9 @@ tf_status tf_sample_rows(tf_context* ctx, const double* pi, int64_t n, int64_t c
 tf_status tf_apply_sample(tf_context* ctx, const double* y, int64_t n_used, int p,
                           const int64_t* idx, const double* w, int64_t c, int width, double* a_out,
                           double* b_out);
-/* phi = argmin || A_S phi - b_S || for the sampled window system. */
+/* phi = argmin || A_S phi - b_S || for the sampled window system
+ * (solve_compressed, sketch.cpp:96-101 -> toeplitz.cpp:57-85): method_out 0 =
+ * exact_qr (CPQR rank = p), 1 = exact_svd (minimum-norm answer). */
 tf_status tf_solve_sampled(tf_context* ctx, const double* y, int64_t n_used, int p,
                            const int64_t* idx, const double* w, int64_t c, double* phi_out,
                            int* method_out);

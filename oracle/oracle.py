@@ -268,6 +268,27 @@ def lsar_fit(y, p_bar: int, c: int, seed: int, fixed_idx=None, fixed_w=None,
                scores_all=sall, bound=1.96 / np.sqrt(c))
 
 
+def lsar_replay(y, p_bar: int, c: int, seed: int, coefs_packed) -> Fit:
+    """orc_lsar_replay: the oracle's draws of a lsar_fit run from its coefficients."""
+    y = f64(y); cf = f64(coefs_packed)
+    if cf.size != p_bar * (p_bar + 1) // 2:
+        raise OracleError(USAGE, "packed coefficients must hold p_bar (p_bar + 1) / 2 values")
+    idx = np.zeros((p_bar, c), np.int64); w = np.zeros((p_bar, c)); rn = np.zeros(p_bar); ss = np.zeros(p_bar)
+    _check(lib().orc_lsar_replay(_p(y), C.c_int64(y.size), C.c_int(p_bar), C.c_int64(c), C.c_uint64(seed),
+                                 _p(cf), _p(idx, _i64p), _p(w), _p(rn), _p(ss)))
+    return Fit(idx=idx, w=w, rnorm2=rn, ssum=ss)
+
+
+def rh_replay(y, p_bar: int, c: int, seed: int, arow_idx, arow_w) -> Fit:
+    """orc_rh_replay: final scores and per-lag draws from the final approximation rows."""
+    y = f64(y); ai = i64(arow_idx); aw = f64(arow_w)
+    m = y.size - p_bar
+    scores = np.zeros(m); idx = np.zeros((p_bar, c), np.int64); w = np.zeros((p_bar, c))
+    _check(lib().orc_rh_replay(_p(y), C.c_int64(y.size), C.c_int(p_bar), C.c_int64(c), C.c_uint64(seed),
+                               _p(ai, _i64p), _p(aw), C.c_int64(ai.size), _p(scores), _p(idx, _i64p), _p(w)))
+    return Fit(scores=scores, idx=idx, w=w)
+
+
 def lsar_time_one_lag(y, p_bar: int, c: int, p: int, seed: int = 1) -> float:
     y = f64(y)
     return float(lib().orc_lsar_time_one_lag(_p(y), y.size, p_bar, c, p, seed))

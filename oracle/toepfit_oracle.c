@@ -142,11 +142,18 @@ int orc_residuals(const double* y, int64_t n_used, int p, const double* phi, dou
   if (p < 1) return fail(ORC_USAGE, "lag order must be at least 1");
   if (n_used <= p) return fail(ORC_DATA, "series window too short for lag order");
   const int64_t m = n_used - p;
-  for (int64_t i = 0; i < m; ++i) r[i] = -y[p + i];
-  for (int j = 0; j < p; ++j) {
-    const double a = phi[j];
-    const double* src = y + (p - 1 - j);
-    for (int64_t i = 0; i < m; ++i) r[i] = fma(a, src[i], r[i]);
+  /* row blocks are independent: every r[i] sees the same fma sequence as the
+   * reference's whole-vector tap loop, whatever the thread count */
+  const int64_t blk = 4096;
+#pragma omp parallel for schedule(static)
+  for (int64_t b0 = 0; b0 < m; b0 += blk) {
+    const int64_t b1 = b0 + blk < m ? b0 + blk : m;
+    for (int64_t i = b0; i < b1; ++i) r[i] = -y[p + i];
+    for (int j = 0; j < p; ++j) {
+      const double a = phi[j];
+      const double* src = y + (p - 1 - j);
+      for (int64_t i = b0; i < b1; ++i) r[i] = fma(a, src[i], r[i]);
+    }
   }
   return ORC_OK;
 }
@@ -328,7 +335,9 @@ static void cpqr_compute(cpqr_t* f, const double* a, int64_t rows, int64_t cols)
     x[0] = beta;
     f->hc[k] = tau;
     if (fabs(beta) > f->maxpivot) f->maxpivot = fabs(beta);
-    /* applyHouseholderOnTheLeft on bottomRightCorner(rows-k, cols-k-1) */
+    /* applyHouseholderOnTheLeft on bottomRightCorner(rows-k, cols-k-1)
+     * (columns independent: thread count does not change the result) */
+#pragma omp parallel for schedule(static) if ((cols - k) * len > 65536)
     for (int64_t j = k + 1; j < cols; ++j) {
       double* cj = q + j * rows + k;
       if (len == 1) {
@@ -340,6 +349,7 @@ static void cpqr_compute(cpqr_t* f, const double* a, int64_t rows, int64_t cols)
       }
     }
     /* norm downdate */
+#pragma omp parallel for schedule(static) if ((cols - k) * len > 65536)
     for (int64_t j = k + 1; j < cols; ++j) {
       if (upd[j] != 0.0) {
         double temp = fabs(q[j * rows + k]) / upd[j];
@@ -422,33 +432,42 @@ static void cpqr_solve(const cpqr_t* f, const double* b, double* x) {
  * Eigen's BDCSVD at toeplitz.cpp:75-81; same rank rule: singular values
  * below max(rows,cols)*eps*sigma_max are dropped).
  * ==================================================================== */
-/* one-sided Jacobi on M (m x n, col-major, m >= n); V (n x n) accumulates. */
+/* one-sided Jacobi on M (m x n, col-major, m >= n); V (n x n) accumulates.
+ * Round-robin (tournament) pair order: the n/2 pairs of a round touch
+ * disjoint columns, so a round runs in parallel and the result does not
+ * depend on the thread count. */
 static void jacobi_svd(double* M, int64_t m, int64_t n, double* V, double* sigma) {
   for (int64_t i = 0; i < n * n; ++i) V[i] = 0.0;
   for (int64_t i = 0; i < n; ++i) V[i * n + i] = 1.0;
-  for (int sweep = 0; sweep < 80; ++sweep) {
+  const int64_t np2 = n + (n & 1); /* players; index n is a bye when n is odd */
+  for (int sweep = 0; sweep < 80 && n > 1; ++sweep) {
     int rotated = 0;
-    for (int64_t i = 0; i < n; ++i) {
-      for (int64_t j = i + 1; j < n; ++j) {
+    for (int64_t rd = 0; rd < np2 - 1; ++rd) {
+#pragma omp parallel for schedule(static) reduction(| : rotated) if (m * n > 40000)
+      for (int64_t t = 0; t < np2 / 2; ++t) {
+        int64_t a = (rd + t) % (np2 - 1);
+        int64_t b = t == 0 ? np2 - 1 : (rd - t + (np2 - 1)) % (np2 - 1);
+        if (a >= n || b >= n) continue;
+        const int64_t i = a < b ? a : b, j = a < b ? b : a;
         double* mi = M + i * m;
         double* mj = M + j * m;
         const double alpha = sqnorm(mi, m), beta = sqnorm(mj, m), gamma = dot(mi, mj, m);
         if (gamma == 0.0 || fabs(gamma) <= DBL_EPSILON * sqrt(alpha * beta)) continue;
         rotated = 1;
         const double zeta = (beta - alpha) / (2.0 * gamma);
-        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
         for (int64_t r = 0; r < m; ++r) {
-          const double a = mi[r], b = mj[r];
-          mi[r] = cs * a - sn * b;
-          mj[r] = sn * a + cs * b;
+          const double x = mi[r], y = mj[r];
+          mi[r] = cs * x - sn * y;
+          mj[r] = sn * x + cs * y;
         }
         double* vi = V + i * n;
         double* vj = V + j * n;
         for (int64_t r = 0; r < n; ++r) {
-          const double a = vi[r], b = vj[r];
-          vi[r] = cs * a - sn * b;
-          vj[r] = sn * a + cs * b;
+          const double x = vi[r], y = vj[r];
+          vi[r] = cs * x - sn * y;
+          vj[r] = sn * x + cs * y;
         }
       }
     }
@@ -486,6 +505,7 @@ static void minnorm_solve(const double* a, int64_t rows, int64_t cols, const dou
       }
       xk[0] = beta;
       f.hc[k] = tau;
+#pragma omp parallel for schedule(static) if ((cols - k) * len > 65536)
       for (int64_t j = k + 1; j < cols; ++j) {
         double* cj = f.qr + j * rows + k;
         if (len == 1) cj[0] *= (1.0 - tau);
@@ -592,18 +612,23 @@ int orc_gaussian_apply(int64_t g, uint64_t seed, const double* m, int64_t rows, 
                        double* out) {
   if (g < 1) return fail(ORC_USAGE, "sketch needs at least one row");
   for (int64_t i = 0; i < g * cols; ++i) out[i] = 0.0;
-  double* col = XMALLOC(double, g);
+  /* the normals in stream order (column j of G = draws j*g .. j*g+g-1), then
+   * every output column accumulates over j in order (columns in parallel) */
+  double* G = XMALLOC(double, g * rows);
   orc_rng rng;
   orc_rng_init(&rng, seed);
-  for (int64_t j = 0; j < rows; ++j) {
-    for (int64_t i = 0; i < g; ++i) col[i] = orc_rng_normal(&rng);
-    for (int64_t l = 0; l < cols; ++l) {
+  for (int64_t j = 0; j < rows; ++j)
+    for (int64_t i = 0; i < g; ++i) G[j * g + i] = orc_rng_normal(&rng);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t l = 0; l < cols; ++l) {
+    double* o = out + l * g;
+    for (int64_t j = 0; j < rows; ++j) {
       const double mv = m[l * rows + j];
-      double* o = out + l * g;
+      const double* col = G + j * g;
       for (int64_t i = 0; i < g; ++i) o[i] += col[i] * mv;
     }
   }
-  free(col);
+  free(G);
   return ORC_OK;
 }
 
@@ -691,6 +716,50 @@ int orc_lsar_fit(const double* y, int64_t n, int p_bar, int64_t c, uint64_t seed
   }
   if (!st && p_star) *p_star = orc_select_order(taus, p_bar, 1.96 / sqrt((double)c));
   free(s); free(s2); free(r); free(dist); free(a); free(b); free(idx); free(wt); free(phi);
+  return st;
+}
+
+/* lsar_fit's recursion and draws replayed from given per-lag coefficients
+ * (the solve skipped): with the coefficients orc_lsar_fit produced, every
+ * score, residual and draw is bit-identical to that run (same functions,
+ * same order).  Lets a test reproduce the oracle's samples of a BASELINE-size
+ * fit from a small fixture (the packed coefficients) in O(p_bar n) time. */
+int orc_lsar_replay(const double* y, int64_t n, int p_bar, int64_t c, uint64_t seed,
+                    const double* coefs_packed, int64_t* idx_out, double* w_out, double* rnorm2_out,
+                    double* ssum_out) {
+  if (p_bar < 1) return fail(ORC_USAGE, "maximum lag must be at least 1");
+  if (n <= (int64_t)p_bar + 1) return fail(ORC_DATA, "series too short for maximum lag %d", p_bar);
+  if (c < p_bar) return fail(ORC_USAGE, "sample count below maximum lag");
+  const int64_t w = n - p_bar;
+  double* s = XMALLOC(double, w);
+  double* s2 = XMALLOC(double, w);
+  double* r = XMALLOC(double, w);
+  double* dist = XMALLOC(double, w);
+  int st = ORC_OK;
+  int64_t off = 0;
+  for (int p = 1; p <= p_bar && !st; ++p) {
+    if (p == 1) {
+      st = orc_init_leverage_p1(y, w, s);
+    } else {
+      st = orc_leverage_update(s, r, w, s2);
+      if (!st) { double* t = s; s = s2; s2 = t; }
+    }
+    if (st) break;
+    st = orc_leverage_to_distribution(s, w, dist);
+    if (!st)
+      st = orc_sample_rows(dist, w, c, orc_derive_seed(seed, (uint64_t)p), idx_out + (int64_t)(p - 1) * c,
+                           w_out + (int64_t)(p - 1) * c);
+    if (!st) st = orc_residuals(y, w + p, p, coefs_packed + off, r);
+    off += p;
+    if (st) break;
+    if (rnorm2_out) rnorm2_out[p - 1] = seq_sqnorm(r, w);
+    if (ssum_out) {
+      double ss = 0.0;
+      for (int64_t i = 0; i < w; ++i) ss += s[i];
+      ssum_out[p - 1] = ss;
+    }
+  }
+  free(s); free(s2); free(r); free(dist);
   return st;
 }
 
@@ -901,9 +970,16 @@ static int rh_fit_impl(const double* y, int64_t n, int p_bar, int64_t c, const o
                      orc_derive_seed(cfg.seed, 0x20000u + (unsigned)i));
     if (st) break;
     double* sco = XMALLOC(double, len);
-    for (int64_t t = 0; t < len; ++t) {
-      aug_row(y, p_bar, cur[t], row);
-      sco[t] = levker_score(&L, row, z);
+#pragma omp parallel
+    {
+      double* prow = XMALLOC(double, k);
+      double* pz = XMALLOC(double, k);
+#pragma omp for schedule(static)
+      for (int64_t t = 0; t < len; ++t) {
+        aug_row(y, p_bar, cur[t], prow);
+        sco[t] = levker_score(&L, prow, pz);
+      }
+      free(prow); free(pz);
     }
     levker_free(&L);
     st = orc_leverage_to_distribution(sco, len, sco);
@@ -929,9 +1005,16 @@ static int rh_fit_impl(const double* y, int64_t n, int p_bar, int64_t c, const o
     st = levker_init(&L, approx, arows, k, 0, 0);
     if (!st) {
       scores = XMALLOC(double, m);
-      for (int64_t i = 0; i < m; ++i) {
-        aug_row(y, p_bar, i, row);
-        scores[i] = levker_score(&L, row, z);
+#pragma omp parallel
+      {
+        double* prow = XMALLOC(double, k);
+        double* pz = XMALLOC(double, k);
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < m; ++i) {
+          aug_row(y, p_bar, i, prow);
+          scores[i] = levker_score(&L, prow, pz);
+        }
+        free(prow); free(pz);
       }
       levker_free(&L);
     }
@@ -993,6 +1076,50 @@ static int rh_fit_impl(const double* y, int64_t n, int p_bar, int64_t c, const o
   free(dist);
   free(scores);
   free(row); free(z); free(sidx); free(sw);
+  return st;
+}
+
+/* The end of rh_fit replayed from its final approximation (rows arow_idx of
+ * the augmented lag-p_bar system, scaled by arow_w, in the order the upward
+ * pass gathered them): rh_leverage_scores (repeated_halving.cpp:182-189),
+ * leverage_to_distribution and the per-lag draws (:205-220).  With the
+ * level-0 upward sample of an orc_rh_fit run the scores and draws are
+ * bit-identical to that run. */
+int orc_rh_replay(const double* y, int64_t n, int p_bar, int64_t c, uint64_t seed, const int64_t* arow_idx,
+                  const double* arow_w, int64_t arows, double* scores_out, int64_t* idx_out, double* w_out) {
+  if (p_bar < 1) return fail(ORC_USAGE, "maximum lag must be at least 1");
+  if (n <= (int64_t)p_bar + 1) return fail(ORC_DATA, "series too short for maximum lag %d", p_bar);
+  const int64_t m = n - p_bar, k = p_bar + 1;
+  double* approx = XMALLOC(double, arows * k);
+  double* row = XMALLOC(double, k);
+  for (int64_t t = 0; t < arows; ++t) {
+    aug_row(y, p_bar, arow_idx[t], row);
+    for (int64_t j = 0; j < k; ++j) approx[j * arows + t] = arow_w ? row[j] * arow_w[t] : row[j];
+  }
+  levker_t L;
+  int st = levker_init(&L, approx, arows, k, 0, 0);
+  double* scores = XMALLOC(double, m);
+  if (!st) {
+#pragma omp parallel
+    {
+      double* prow = XMALLOC(double, k);
+      double* pz = XMALLOC(double, k);
+#pragma omp for schedule(static)
+      for (int64_t i = 0; i < m; ++i) {
+        aug_row(y, p_bar, i, prow);
+        scores[i] = levker_score(&L, prow, pz);
+      }
+      free(prow); free(pz);
+    }
+    levker_free(&L);
+  }
+  double* dist = XMALLOC(double, m);
+  if (!st && scores_out) memcpy(scores_out, scores, sizeof(double) * (size_t)m);
+  if (!st) st = orc_leverage_to_distribution(scores, m, dist);
+  for (int p = 1; p <= p_bar && !st; ++p)
+    st = orc_sample_rows(dist, m, c, orc_derive_seed(seed, (uint64_t)p), idx_out + (int64_t)(p - 1) * c,
+                         w_out + (int64_t)(p - 1) * c);
+  free(approx); free(row); free(scores); free(dist);
   return st;
 }
 

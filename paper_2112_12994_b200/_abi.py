@@ -32,7 +32,7 @@ class TfLsarDiag(C.Structure):
     _fields_ = [("fixed_idx", _i64p), ("fixed_w", _f64p), ("idx_out", _i64p), ("w_out", _f64p),
                 ("rnorm2_out", _f64p), ("ssum_out", _f64p), ("scores_out", _f64p),
                 ("resid_out", _f64p), ("method_out", _i32p), ("phase_seconds", _f64p),
-                ("launches_out", _i64p)]
+                ("launches_out", _i64p), ("rank_out", _i32p)]
 
 
 class TfRhDiag(C.Structure):
@@ -40,7 +40,7 @@ class TfRhDiag(C.Structure):
                 ("fixed_up_idx", _i64p), ("fixed_up_w", _f64p), ("scores_out", _f64p),
                 ("depth_out", _i32p), ("idx_out", _i64p), ("w_out", _f64p),
                 ("levels_out", _i64p), ("up_idx_out", _i64p), ("up_w_out", _f64p),
-                ("launches_out", _i64p)]
+                ("launches_out", _i64p), ("method_out", _i32p), ("rank_out", _i32p)]
 
 
 EXPORTS = [

@@ -256,25 +256,32 @@ class Engine:
         keep = []
         diag = None
         if fixed_idx is not None:
+            # fixed_w None: the weights of each lag's own distribution (k_fixed_weights)
             fi = np.ascontiguousarray(fixed_idx, dtype=np.int64)
-            fw = np.ascontiguousarray(fixed_w, dtype=np.float64)
-            if fi.size != pb * c or fw.size != pb * c:
+            if fi.size != pb * c:
                 raise UsageError("fixed samples must be [p_bar][c]")
-            keep += [fi, fw]
+            keep.append(fi)
             d.fixed_idx = ptr(fi, _abi._i64p)
-            d.fixed_w = ptr(fw)
+            if fixed_w is not None:
+                fw = np.ascontiguousarray(fixed_w, dtype=np.float64)
+                if fw.size != pb * c:
+                    raise UsageError("fixed samples must be [p_bar][c]")
+                keep.append(fw)
+                d.fixed_w = ptr(fw)
         if want_diag == "light":  # phases / methods / launches only (no per-row dumps)
-            diag = dict(method=np.zeros(pb, np.int32), phases=np.zeros((pb, 3)),
+            diag = dict(method=np.zeros(pb, np.int32), rank=np.zeros(pb, np.int32), phases=np.zeros((pb, 3)),
                         launches=np.zeros(1, np.int64))
             d.method_out = ptr(diag["method"], _abi._i32p)
+            d.rank_out = ptr(diag["rank"], _abi._i32p)
             d.phase_seconds = ptr(diag["phases"])
             d.launches_out = ptr(diag["launches"], _abi._i64p)
         elif want_diag:
             w = max(int(n) - pb, 1)
             diag = dict(idx=np.zeros((pb, c), np.int64), w=np.zeros((pb, c)), rnorm2=np.zeros(pb),
                         ssum=np.zeros(pb), scores=np.zeros(w), resid=np.zeros(w),
-                        method=np.zeros(pb, np.int32), phases=np.zeros((pb, 3)),
+                        method=np.zeros(pb, np.int32), rank=np.zeros(pb, np.int32), phases=np.zeros((pb, 3)),
                         launches=np.zeros(1, np.int64))
+            d.rank_out = ptr(diag["rank"], _abi._i32p)
             d.idx_out = ptr(diag["idx"], _abi._i64p)
             d.w_out = ptr(diag["w"])
             d.rnorm2_out = ptr(diag["rnorm2"])
@@ -329,6 +336,10 @@ class Engine:
             d.up_w_out = ptr(diag["up_w"])
             diag["launches"] = np.zeros(1, np.int64)
             d.launches_out = ptr(diag["launches"], _abi._i64p)
+            diag["method"] = np.zeros(pb, np.int32)
+            diag["rank"] = np.zeros(pb, np.int32)
+            d.method_out = ptr(diag["method"], _abi._i32p)
+            d.rank_out = ptr(diag["rank"], _abi._i32p)
         ccfg = None
         if cfg is not None:
             ccfg = _abi.TfRhCfg(cfg.base_threshold, cfg.sample_count, cfg.gaussian_rows, cfg.seed)

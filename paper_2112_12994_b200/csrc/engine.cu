@@ -20,6 +20,7 @@
 #include "engine.h"
 #include "k_bsolve.cuh"
 #include "k_cholinv.cuh"
+#include "k_exact.cuh"
 #include "k_gen.cuh"
 #include "k_gram.cuh"
 #include "k_pass.cuh"
@@ -447,6 +448,110 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
 }
 
 // ---------------------------------------------------------------------------
+// The reference's rank-revealing solve of a sampled lag system at every K
+// (toeplitz.cpp:57-85; k_exact.cuh): double-double Gram -> pivoted Cholesky
+// (= CPQR) -> phi by back-substitution, or the minimum-norm SVD answer when
+// the rank rule finds rank < p.  rev = 1: target-first column order (RH).
+constexpr int kExactMaxP = 640;  // the SVD block pair of a 16-CTA cluster fits shared memory up to here
+
+static void svd_plan(int p, int& nct, int& nblk, int& bw) {
+  nct = std::min(kSvdMaxCta, std::max(1, (p + 31) / 32));
+  nblk = 2 * nct;
+  bw = std::max(1, (p + nblk - 1) / nblk);
+}
+
+static void reserve_exact(tf_context* ctx, int64_t c, int Kmax) {
+  SolveBufs& b = ctx->sb;
+  size_t wmax = 0;
+  for (int K = 2; K <= Kmax; ++K) {
+    const GramDDPlan g = gram_dd_plan(c, K, ctx->sm_count);
+    wmax = std::max(wmax, (size_t)g.npair * g.nsplit * 8192);
+  }
+  const size_t KK = (size_t)Kmax * Kmax;
+  b.Wdd.need(wmax);
+  b.Gh.need(KK);
+  b.Gl.need(KK);
+  b.Rh.need(KK);
+  b.Rl.need(KK);
+  b.Nsv.need((size_t)Kmax * Kmax);
+  b.sig.need(Kmax);
+  b.xpart.need((size_t)2 * kSvdMaxCta * Kmax);
+  b.tolv.need(2);
+  b.perm.need(Kmax);
+  b.svdf.need(2 + kSvdMaxSweeps + 8);
+}
+
+template <class L>
+static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev, const ExactOut& o) {
+  SolveBufs& b = ctx->sb;
+  cudaStream_t st = ctx->stream;
+  const int p = K - 1;
+  if (p > kExactMaxP) throw TfError{TF_USAGE, "lag order above " + std::to_string(kExactMaxP) + " (rank-revealing solve)"};
+  const GramDDPlan g = gram_dd_plan(c, K, ctx->sm_count);
+  k_gram_dd<L><<<dim3((unsigned)g.npair, (unsigned)g.nsplit), kDDThreads, 0, st>>>(ld, c, K, g.nblk, g.rps, g.nsplit,
+                                                                                  b.Wdd.get(), nullptr);
+  LAUNCH_CHECK("k_gram_dd");
+  k_gram_dd_reduce<<<(unsigned)(((int64_t)g.npair * 4096 + 255) / 256), 256, 0, st>>>(
+      b.Wdd.get(), g.npair, g.nsplit, g.nblk, K, b.Gh.get(), b.Gl.get(), nullptr);
+  LAUNCH_CHECK("k_gram_dd_reduce");
+  PcholArgs pa{};
+  pa.Gh = b.Gh.get();
+  pa.Gl = b.Gl.get();
+  pa.K = K;
+  pa.rev = rev;
+  pa.rows = c;
+  pa.Rh = b.Rh.get();
+  pa.Rl = b.Rl.get();
+  pa.N = b.Nsv.get();
+  pa.perm = b.perm.get();
+  pa.svd = b.svdf.get();
+  pa.tol = b.tolv.get();
+  pa.o = o;
+  pa.gate = nullptr;
+  k_pchol_dd<<<1, kPcThreads, 0, st>>>(pa);
+  LAUNCH_CHECK("k_pchol_dd");
+  int nct, nblk, bw;
+  svd_plan(p, nct, nblk, bw);
+  SvdArgs sa{};
+  sa.N = b.Nsv.get();
+  sa.sig = b.sig.get();
+  sa.xpart = b.xpart.get();
+  sa.perm = b.perm.get();
+  sa.svd = b.svdf.get();
+  sa.tol = b.tolv.get();
+  sa.p = p;
+  sa.nblk = nblk;
+  sa.bw = bw;
+  sa.rev = rev;
+  sa.o = o;
+  const size_t smem = svd_smem_bytes(p, bw);
+  {
+    static std::mutex mu;
+    static bool attr = false;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!attr) {
+      CK(cudaFuncSetAttribute((const void*)k_svd_minnorm, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      attr = true;
+    }
+  }
+  smem_optin((const void*)k_svd_minnorm, smem);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)nct);
+  cfg.blockDim = dim3(kSvdThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)nct;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_svd_minnorm, sa));
+  g_launches += 4;
+}
+
+// ---------------------------------------------------------------------------
 
 constexpr int kPassPstMinQ = 1;  // sweeps: tensor-core persistent pass for every lag q >= 1
 
@@ -530,6 +635,13 @@ static void launch_draw(tf_context* ctx, uint64_t seed, int64_t c, int64_t w, in
   const int per = kDrawPerCta;
   k_draw<<<(unsigned)((c + per - 1) / per), kDrawThreads, 0, ctx->stream>>>(a);
   LAUNCH_CHECK("k_draw");
+  COUNT_LAUNCH();
+}
+
+static void launch_fixed_weights(tf_context* ctx, const int64_t* idx, int64_t c, const double* s, const double* r,
+                                 double* wts) {
+  k_fixed_weights<<<(unsigned)((c + 255) / 256), 256, 0, ctx->stream>>>(idx, c, ctx->scal.get(), s, r, wts);
+  LAUNCH_CHECK("k_fixed_weights");
   COUNT_LAUNCH();
 }
 
@@ -643,23 +755,29 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
   const int64_t ntile = (w + kPassTile - 1) / kPassTile;
   cudaStream_t st = ctx->stream;
   alloc_state(ctx, p_bar, c, w);
-  const bool fixed = d && d->fixed_idx && d->fixed_w;
+  // deterministic-index mode: reference indices, with the reference's weights
+  // or (fixed_w null) the weights of this lag's own distribution
+  const bool fixed = d && d->fixed_idx;
+  const bool fixed_wts = fixed && d->fixed_w;
   if (fixed) {
     const size_t tot = (size_t)p_bar * c;
     for (size_t i = 0; i < tot; ++i)
       if (d->fixed_idx[i] < 0 || d->fixed_idx[i] >= w)
         throw TfError{TF_USAGE, "sample index out of range"};  // sketch.cpp:69
     ctx->fidx.need(tot);
-    ctx->fw.need(tot);
     CK(cudaMemcpyAsync(ctx->fidx.get(), d->fixed_idx, tot * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(ctx->fw.get(), d->fixed_w, tot * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (fixed_wts) {
+      ctx->fw.need(tot);
+      CK(cudaMemcpyAsync(ctx->fw.get(), d->fixed_w, tot * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
   }
   const bool want_hist = d && (d->idx_out || d->w_out);
   if (want_hist) {
     ctx->idx_hist.need((size_t)p_bar * c);
     ctx->w_hist.need((size_t)p_bar * c);
   }
-  reserve_solve(ctx, c, p_bar + 1);
+  reserve_exact(ctx, c, p_bar + 1);
+  ctx->rank.need(p_bar);
   ensure_events(ctx, p_bar + 1);
   const bool phases = d && d->phase_seconds;
   while (phases && ctx->pev.size() < 2 * (size_t)p_bar) {
@@ -697,7 +815,8 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
       double* wts = ctx->wts.get();
       if (fixed) {
         idx = ctx->fidx.get() + (size_t)(p - 1) * c;
-        wts = ctx->fw.get() + (size_t)(p - 1) * c;
+        if (fixed_wts) wts = ctx->fw.get() + (size_t)(p - 1) * c;
+        else launch_fixed_weights(ctx, idx, c, ctx->s.get(), ctx->r.get(), wts);
       } else {
         launch_draw(ctx, 0, c, w, idx, wts, ctx->seedtab.get() + p);
       }
@@ -708,18 +827,10 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
                            cudaMemcpyDeviceToDevice, st));
       }
       if (phases) rec(ctx->pev[2 * (p - 1)]);
-      SolveOut o;
-      o.phi = ctx->phi.get();
-      o.coefs = ctx->coefs.get();
-      o.coef_off = (int64_t)(p - 1) * p / 2;
-      o.taus = ctx->taus.get();
-      o.method = ctx->method.get();
-      o.lag = p;
-      o.status = ctx->status.get();
-      FwdRows ld{ctx->y.get(), idx, wts, 0};
-      double* Snext = (p & 1) ? ctx->sb.S1.get() : ctx->sb.S0.get();
-      const double* Sprev = (p & 1) ? ctx->sb.S0.get() : ctx->sb.S1.get();
-      solve_rows(ctx, ld, c, p + 1, o, p >= 2 ? Sprev : nullptr, p >= 2 ? ctx->phi.get() : nullptr, Snext);
+      // rank-revealing solve of the sampled lag-p system (toeplitz.cpp:57-85)
+      ExactOut o{ctx->phi.get(), ctx->coefs.get(), (int64_t)(p - 1) * p / 2, ctx->taus.get(), ctx->method.get(),
+                 ctx->rank.get(), p};
+      solve_exact(ctx, FwdRows{ctx->y.get(), idx, wts, 0}, c, p + 1, /*rev=*/0, o);
       if (phases) rec(ctx->pev[2 * (p - 1) + 1]);
       // residuals of the lag-p window fit + score update s_p = s_{p-1} + r_{p-1}^2/R_{p-1}
       launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());
@@ -730,7 +841,7 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
   };
   // The lag loop's launch sequence depends only on (w, c, p_bar, mode) and on
   // the buffers: graph capture/replay (run_graphed).
-  const int mode = (fixed ? 1 : 0) | (want_hist ? 2 : 0) | (phases ? 4 : 0) | (rn2 ? 8 : 0);
+  const int mode = (fixed ? 1 : 0) | (want_hist ? 2 : 0) | (phases ? 4 : 0) | (rn2 ? 8 : 0) | (fixed_wts ? 16 : 0);
   const int64_t launches = run_graphed(ctx, ctx->lsar_graph, w, c, p_bar, mode, capturing, record);
   CK(cudaStreamSynchronize(st));
   int sth[3];
@@ -761,6 +872,7 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
     if (d->scores_out) CK(cudaMemcpy(d->scores_out, ctx->s.get(), sizeof(double) * w, cudaMemcpyDeviceToHost));
     if (d->resid_out) CK(cudaMemcpy(d->resid_out, ctx->r.get(), sizeof(double) * w, cudaMemcpyDeviceToHost));
     if (d->method_out) CK(cudaMemcpy(d->method_out, ctx->method.get(), sizeof(int) * p_bar, cudaMemcpyDeviceToHost));
+    if (d->rank_out) CK(cudaMemcpy(d->rank_out, ctx->rank.get(), sizeof(int) * p_bar, cudaMemcpyDeviceToHost));
     if (d->launches_out) *d->launches_out = launches;
     if (phases)
       for (int p = 1; p <= p_bar; ++p) {
@@ -1155,9 +1267,10 @@ static void solve_sampled_op(tf_context* ctx, const double* y, int64_t n_used, i
   alloc_state(ctx, p, c, 1);
   CK(cudaMemcpyAsync(ctx->idx.get(), idx, c * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(ctx->wts.get(), w, c * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-  SolveOut o{ctx->phi.get(), nullptr, 0, nullptr, ctx->method.get(), 1, ctx->status.get()};
-  FwdRows ld{ctx->y.get(), ctx->idx.get(), ctx->wts.get(), 0};
-  solve_rows(ctx, ld, c, p + 1, o, nullptr, nullptr, nullptr);
+  reserve_exact(ctx, c, p + 1);
+  ctx->rank.need(1);
+  ExactOut o{ctx->phi.get(), nullptr, 0, nullptr, ctx->method.get(), ctx->rank.get(), 1};
+  solve_exact(ctx, FwdRows{ctx->y.get(), ctx->idx.get(), ctx->wts.get(), 0}, c, p + 1, /*rev=*/0, o);
   CK(cudaMemcpyAsync(phi_out, ctx->phi.get(), p * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   int m = 0;
   CK(cudaMemcpyAsync(&m, ctx->method.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1377,7 +1490,8 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
   const int64_t base_rows = lsz[depth];
   if (base_rows < K || (depth > 0 && sc < K))
     throw TfError{TF_NUMERICAL, "reference matrix has too few rows"};
-  const bool fixed = d && d->fixed_idx && d->fixed_w;
+  const bool fixed = d && d->fixed_idx;
+  const bool fixed_wts = fixed && d->fixed_w;
   const bool fixed_lv = d && d->fixed_levels;
   const bool fixed_up = d && d->fixed_up_idx && d->fixed_up_w;
   cudaStream_t st = ctx->stream;
@@ -1421,9 +1535,11 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
     for (size_t i = 0; i < tot; ++i)
       if (d->fixed_idx[i] < 0 || d->fixed_idx[i] >= m) throw TfError{TF_USAGE, "sample index out of range"};
     ctx->fidx.need(tot);
-    ctx->fw.need(tot);
     CK(cudaMemcpyAsync(ctx->fidx.get(), d->fixed_idx, tot * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(ctx->fw.get(), d->fixed_w, tot * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (fixed_wts) {
+      ctx->fw.need(tot);
+      CK(cudaMemcpyAsync(ctx->fw.get(), d->fixed_w, tot * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
   }
   if (fixed_lv && lvl_total > 0) {
     for (int64_t i = 0; i < lvl_total; ++i)
@@ -1554,7 +1670,8 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
     CK(cudaMemcpyAsync(ctx->seedtab.get(), seeds.data(), (p_bar + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
   }
-  ctx->sb.M.need((size_t)c * ldq_of(2));
+  reserve_exact(ctx, c, K);
+  ctx->rank.need(p_bar);
   bool capturing = false;
   auto rec = [&](cudaEvent_t e) {
     if (capturing) CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
@@ -1567,7 +1684,8 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
       double* wts = ctx->wts.get();
       if (fixed) {
         idx = ctx->fidx.get() + (size_t)(p - 1) * c;
-        wts = ctx->fw.get() + (size_t)(p - 1) * c;
+        if (fixed_wts) wts = ctx->fw.get() + (size_t)(p - 1) * c;
+        else launch_fixed_weights(ctx, idx, c, ctx->rh_scores.get(), nullptr, wts);
       } else {
         launch_draw_on(ctx, ctx->rh_scores.get(), m, 0, c, idx, wts, ctx->seedtab.get() + p);
       }
@@ -1577,24 +1695,15 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
         CK(cudaMemcpyAsync(ctx->w_hist.get() + (size_t)(p - 1) * c, wts, c * sizeof(double),
                            cudaMemcpyDeviceToDevice, st));
       }
-      SolveOut o;
-      o.phi = ctx->phi.get();
-      o.coefs = ctx->coefs.get();
-      o.coef_off = (int64_t)(p - 1) * p / 2;
-      o.taus = ctx->taus.get();
-      o.method = ctx->method.get();
-      o.lag = p;
-      o.status = ctx->status.get();
-      RevRows ld{y, idx, wts, p_bar};
-      double* Snext = (p & 1) ? ctx->sb.S1.get() : ctx->sb.S0.get();
-      const double* Sprev = (p & 1) ? ctx->sb.S0.get() : ctx->sb.S1.get();
-      solve_rows(ctx, ld, c, p + 1, o, p >= 2 ? Sprev : nullptr, p >= 2 ? ctx->phi.get() : nullptr, Snext,
-                 /*rev=*/1, ctx->rh_rest.get(), ctx->rh_rest.get());
+      // apply_sample(full, s, p) + solve_compressed (repeated_halving.cpp:221-222)
+      ExactOut o{ctx->phi.get(), ctx->coefs.get(), (int64_t)(p - 1) * p / 2, ctx->taus.get(), ctx->method.get(),
+                 ctx->rank.get(), p};
+      solve_exact(ctx, RevRows{y, idx, wts, p_bar}, c, p + 1, /*rev=*/1, o);
       rec(ctx->events[p + 1]);
     }
     rec(ctx->ev_end);
   };
-  const int lag_mode = (fixed ? 1 : 0) | (want_hist ? 2 : 0);
+  const int lag_mode = (fixed ? 1 : 0) | (want_hist ? 2 : 0) | (fixed_wts ? 4 : 0);
   run_graphed(ctx, ctx->rh_graph, m, c, p_bar, lag_mode, capturing, record_lags);
   const int64_t launches = g_launches - launches0;
   CK(cudaStreamSynchronize(st));
@@ -1625,6 +1734,8 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
     if (d->scores_out) CK(cudaMemcpy(d->scores_out, ctx->rh_scores.get(), sizeof(double) * m, cudaMemcpyDeviceToHost));
     if (d->depth_out) *d->depth_out = depth;
     if (d->launches_out) *d->launches_out = launches;
+    if (d->method_out) CK(cudaMemcpy(d->method_out, ctx->method.get(), sizeof(int) * p_bar, cudaMemcpyDeviceToHost));
+    if (d->rank_out) CK(cudaMemcpy(d->rank_out, ctx->rank.get(), sizeof(int) * p_bar, cudaMemcpyDeviceToHost));
     if (d->levels_out && lvl_total > 0)
       CK(cudaMemcpy(d->levels_out, ctx->rh_lvl.get(), sizeof(int64_t) * lvl_total, cudaMemcpyDeviceToHost));
     if (want_up && d->up_idx_out)

@@ -41,6 +41,10 @@ struct GraphCache {
 struct SolveBufs {
   DBuf<double> W, G, RA, RB, RC, SA, SB, SC, T, S0, S1, Q1, Q2, M, RI;
   DBuf<int> flags;
+  // rank-revealing solve (k_exact.cuh): double-double Gram partials and
+  // planes, pivoted factor, SVD matrix / singular values / partial solutions
+  DBuf<double> Wdd, Gh, Gl, Rh, Rl, Nsv, sig, xpart, tolv;
+  DBuf<int> perm, svdf;
 };
 
 }  // namespace tfe
@@ -62,7 +66,7 @@ struct tf_context {
   tfe::DBuf<int> srht_reject;
   tfe::DBuf<int64_t> idx, fidx, idx_hist;
   tfe::DBuf<double> wts, fw, w_hist;
-  tfe::DBuf<int> status, method;
+  tfe::DBuf<int> status, method, rank;
   tfe::SolveBufs sb;
   // RH state
   tfe::DBuf<int> rh_J, rh_cnt, rh_start, rh_fill, rh_bk, rh_pick, rh_ok, rh_flag;

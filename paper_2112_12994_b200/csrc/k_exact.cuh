@@ -1,0 +1,575 @@
+// k_exact.cuh -- the reference's rank-revealing solve of one sampled lag
+// system (toeplitz.cpp:57-85: Eigen ColPivHouseholderQR with threshold
+// tol = max(rows, cols) eps, rank = #{|r_ii| > tol max|r_ii|}; full rank ->
+// qr.solve, otherwise BDCSVD's minimum-norm solution with the same threshold),
+// for every K, on the GPU:
+//
+//  1. k_gram_dd + k_gram_dd_reduce: G = A^T A of the gathered, weighted rows
+//     A = [X | b] (K = p + 1 columns) in double-double.  Each product is
+//     error-free (p = a b, e = fma(a, b, -p)) and the sums are TwoSum
+//     accumulated, so G is exact to ~1e-30 relative -- far below the CPQR
+//     threshold's square (tol^2 >= 1e-31 only for c < 2, never in practice:
+//     tol^2 = (c eps)^2 ~ 5e-24 at c = 1e4).
+//  2. k_pchol_dd: diagonally pivoted Cholesky of G in double-double.  In exact
+//     arithmetic this is the column-pivoting Householder QR of X: step k picks
+//     the column of largest remaining norm (the Schur diagonal, which is
+//     Eigen's updated column norm squared) and |r_kk|^2 is that diagonal; the
+//     target column rides along unpivoted, so its column of R is z = Q^T b.
+//     Rank by Eigen's rule; full rank -> phi by double-double back-substitution.
+//  3. k_svd_minnorm (rank-deficient systems only; one thread-block cluster):
+//     one-sided block Jacobi on N = [R'^T; z^T] (R' the pivoted p x p factor),
+//     so N J = W; then R' = J Sigma U^T with W = U Sigma and the minimum-norm
+//     solution x = sum_{s_i >= tol s_max} w_i (J^T z)_i / s_i^2 (BDCSVD's
+//     premultiplied threshold, JacobiSVD / BDCSVD _solve_impl semantics).
+//
+// Why not CholeskyQR here: the BASELINE C4 systems have cond ~ 1e16-1e21, so
+// fp64 Gram / preconditioned CholeskyQR factors cannot resolve |r_kk| near the
+// threshold (4.4e-11 |r_11| at c = 2e5); shifted CholeskyQR3 breaks down
+// (tools/rank_experiment.py).  The double-double Gram keeps the whole
+// decision exact at the cost of ~10 fp64 operations per multiply-add.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "k_gram.cuh"
+
+namespace tfk {
+
+// ---------------------------------------------------------------- double-double
+// Every operation goes through __dadd_rn / __dsub_rn / __dmul_rn: the compiler
+// may not contract them into an FMA (which would break the error-free
+// transformations -- e.g. s = h + a*b fused into fma(a, b, h) makes TwoSum's
+// error term wrong by up to eps |a b|).
+struct DD {
+  double h, l;
+};
+__device__ __forceinline__ DD dd_two_sum(double a, double b) {
+  const double s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  return {s, __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb))};
+}
+__device__ __forceinline__ DD dd_fast(double a, double b) {  // |a| >= |b|
+  const double s = __dadd_rn(a, b);
+  return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  DD s = dd_two_sum(a.h, b.h);
+  const DD t = dd_two_sum(a.l, b.l);
+  s.l = __dadd_rn(s.l, t.h);
+  s = dd_fast(s.h, s.l);
+  s.l = __dadd_rn(s.l, t.l);
+  return dd_fast(s.h, s.l);
+}
+__device__ __forceinline__ DD dd_neg(DD a) { return {-a.h, -a.l}; }
+__device__ __forceinline__ DD dd_mul(DD a, DD b) {
+  const double p = __dmul_rn(a.h, b.h);
+  double e = fma(a.h, b.h, -p);
+  e = fma(a.h, b.l, e);
+  e = fma(a.l, b.h, e);
+  return dd_fast(p, e);
+}
+__device__ __forceinline__ DD dd_div(DD a, DD b) {
+  const double q1 = __ddiv_rn(a.h, b.h);
+  DD r = dd_add(a, dd_neg(dd_mul(b, DD{q1, 0.0})));
+  const double q2 = __ddiv_rn(r.h, b.h);
+  r = dd_add(r, dd_neg(dd_mul(b, DD{q2, 0.0})));
+  const double q3 = __ddiv_rn(r.h, b.h);
+  return dd_add(dd_fast(q1, q2), DD{q3, 0.0});
+}
+__device__ __forceinline__ DD dd_sqrt(DD a) {
+  if (!(a.h > 0.0)) return {0.0, 0.0};
+  const double x = __dsqrt_rn(a.h);
+  const DD d = dd_add(a, dd_neg(dd_mul(DD{x, 0.0}, DD{x, 0.0})));
+  return dd_fast(x, __ddiv_rn(d.h, __dmul_rn(2.0, x)));
+}
+__device__ __forceinline__ bool dd_gt(DD a, DD b) { return a.h > b.h || (a.h == b.h && a.l > b.l); }
+// acc += a * b, exact product, TwoSum into (h, l)
+__device__ __forceinline__ void dd_acc(double& h, double& l, double a, double b) {
+  const double p = __dmul_rn(a, b);
+  const double e = fma(a, b, -p);
+  const double s = __dadd_rn(h, p);
+  const double bb = __dsub_rn(s, h);
+  l = __dadd_rn(l, __dadd_rn(__dadd_rn(__dsub_rn(h, __dsub_rn(s, bb)), __dsub_rn(p, bb)), e));
+  h = s;
+}
+// acc += a * b for double-double a, b (cross terms to first order)
+__device__ __forceinline__ void dd_acc2(double& h, double& l, DD a, DD b) {
+  const double p = __dmul_rn(a.h, b.h);
+  double e = fma(a.h, b.h, -p);
+  e = fma(a.h, b.l, e);
+  e = fma(a.l, b.h, e);
+  const double s = __dadd_rn(h, p);
+  const double bb = __dsub_rn(s, h);
+  l = __dadd_rn(l, __dadd_rn(__dadd_rn(__dsub_rn(h, __dsub_rn(s, bb)), __dsub_rn(p, bb)), e));
+  h = s;
+}
+__device__ __forceinline__ DD dd_shfl_xor(DD v, int m) {
+  return {__shfl_xor_sync(0xffffffffu, v.h, m), __shfl_xor_sync(0xffffffffu, v.l, m)};
+}
+__device__ __forceinline__ DD dd_warp_sum(DD v) {  // fixed butterfly order
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) v = dd_add(v, dd_shfl_xor(v, m));
+  return v;
+}
+
+// ---------------------------------------------------------------- 1. Gram
+constexpr int kDDThreads = 256;
+constexpr int kDDSlab = 16;
+
+struct GramDDPlan {
+  int nblk, npair, nsplit;
+  int64_t rps;
+};
+
+inline GramDDPlan gram_dd_plan(int64_t rows, int K, int sm_count) {
+  GramDDPlan g;
+  g.nblk = (K + 63) / 64;
+  g.npair = g.nblk * (g.nblk + 1) / 2;
+  const int64_t target = 3LL * sm_count;
+  int64_t ns = (target + g.npair - 1) / g.npair;
+  ns = std::max<int64_t>(1, std::min<int64_t>(ns, (rows + 4 * kDDSlab - 1) / (4 * kDDSlab)));
+  int64_t rps = (rows + ns - 1) / ns;
+  rps = (rps + kDDSlab - 1) / kDDSlab * kDDSlab;
+  g.rps = std::max<int64_t>(rps, kDDSlab);
+  g.nsplit = (int)((rows + g.rps - 1) / g.rps);
+  if (g.nsplit < 1) g.nsplit = 1;
+  return g;
+}
+
+// Partial double-double Gram of one 64 x 64 tile pair (I <= J) over a row
+// range; element (ty + 16 i, tx + 16 j) per thread (conflict-free shared
+// reads).  W[(pair * nsplit + split) * 8192 + {0, 4096} + e] = (hi, lo).
+template <class L>
+__global__ void __launch_bounds__(kDDThreads) k_gram_dd(L ld, int64_t rows, int K, int nblk, int64_t rps, int nsplit,
+                                                        double* __restrict__ W, const int* gate) {
+  if (gate && *gate == 0) return;
+  __shared__ double As[kDDSlab][64], Bs[kDDSlab][64];
+  int I, J;
+  pair_from_index(blockIdx.x, nblk, I, J);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t r0 = (int64_t)blockIdx.y * rps, r1 = min(rows, r0 + rps);
+  double h[4][4], l[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[i][j] = l[i][j] = 0.0;
+  double ra[4], rb[4];
+  auto load = [&](int64_t t0) {
+    const int64_t t = t0 + ty;
+    const bool ok = t < r1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int ca = 64 * I + tx + 16 * q, cb = 64 * J + tx + 16 * q;
+      ra[q] = (ok && ca < K) ? ld(t, ca) : 0.0;
+      rb[q] = (ok && cb < K) ? ld(t, cb) : 0.0;
+    }
+  };
+  if (r0 < r1) load(r0);
+  for (int64_t t0 = r0; t0 < r1; t0 += kDDSlab) {
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      As[ty][tx + 16 * q] = ra[q];
+      Bs[ty][tx + 16 * q] = rb[q];
+    }
+    __syncthreads();
+    if (t0 + kDDSlab < r1) load(t0 + kDDSlab);
+#pragma unroll 2
+    for (int r = 0; r < kDDSlab; ++r) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = As[r][ty + 16 * i];
+        b[i] = Bs[r][tx + 16 * i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dd_acc(h[i][j], l[i][j], a[i], b[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const DD s = dd_two_sum(h[i][j], l[i][j]);
+        h[i][j] = s.h;
+        l[i][j] = s.l;
+      }
+  }
+  double* out = W + ((size_t)blockIdx.x * nsplit + blockIdx.y) * 8192;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int e = (ty + 16 * i) * 64 + tx + 16 * j;
+      out[e] = h[i][j];
+      out[4096 + e] = l[i][j];
+    }
+}
+
+// split partials summed in split order (deterministic) -> full symmetric
+// K x K (row-major) hi / lo planes
+__global__ void k_gram_dd_reduce(const double* __restrict__ W, int npair, int nsplit, int nblk, int K,
+                                 double* __restrict__ Gh, double* __restrict__ Gl, const int* gate) {
+  if (gate && *gate == 0) return;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)npair * 4096) return;
+  const int pair = (int)(e >> 12), loc = (int)(e & 4095);
+  int I, J;
+  pair_from_index(pair, nblk, I, J);
+  const int row = 64 * I + (loc >> 6), col = 64 * J + (loc & 63);
+  if (row >= K || col >= K) return;
+  DD s{0.0, 0.0};
+  for (int sp = 0; sp < nsplit; ++sp) {
+    const double* w = W + ((size_t)pair * nsplit + sp) * 8192;
+    s = dd_add(s, DD{w[loc], w[4096 + loc]});
+  }
+  Gh[(int64_t)row * K + col] = s.h;
+  Gl[(int64_t)row * K + col] = s.l;
+  if (I != J) {
+    Gh[(int64_t)col * K + row] = s.h;
+    Gl[(int64_t)col * K + row] = s.l;
+  }
+}
+
+// ---------------------------------------------------------------- 2. pivoted Cholesky
+constexpr int kPcThreads = 1024;
+constexpr int kPcMaxK = 704;  // K <= kExactMaxP + 1 (static shared memory: 6 double + 1 int arrays)
+
+struct ExactOut {
+  double* phi;     // [p] reference order (lag j + 1 at index j)
+  double* coefs;   // nullable, packed
+  int64_t coef_off;
+  double* taus;    // nullable, [lag - 1] = phi[p - 1]
+  int* method;     // nullable, [lag - 1] = 0 exact_qr / 1 exact_svd (toeplitz.hpp:49-56)
+  int* rank;       // nullable, [lag - 1] = CPQR rank
+  int lag;
+};
+
+struct PcholArgs {
+  const double* Gh;
+  const double* Gl;
+  int K;
+  int rev;         // 0: forward rows (target last, column a = lag p - a); 1: target first (column a = lag a)
+  int64_t rows;    // sampled rows (tolerance max(rows, p) eps)
+  double* Rh;      // workspace K x K: Rh[col * K + i] = r_{i, pos(col)} (by original column)
+  double* Rl;
+  double* N;       // SVD input (p + 1) x p, column-major: column i = row i of R', row p = z_i
+  int* perm;       // [K] pivot position -> original column
+  int* svd;        // [0] rank deficient, [1] rank, [2..] sweep convergence flags (zeroed)
+  double* tol;     // [0] tol
+  ExactOut o;
+  const int* gate;
+};
+
+__device__ __forceinline__ int exact_phi_index(int col, int p, int rev) { return rev ? col - 1 : p - 1 - col; }
+
+__global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
+  if (a.gate && *a.gate == 0) return;
+  __shared__ int perm[kPcMaxK];
+  __shared__ double dh[kPcMaxK], dl[kPcMaxK];
+  __shared__ double ch[kPcMaxK], cl[kPcMaxK];  // pivot column: r_{i,k}, i < k (then reused for z')
+  __shared__ double rkh[kPcMaxK], rkl[kPcMaxK];
+  __shared__ double wv_h[32], wv_l[32];
+  __shared__ int wv_i[32];
+  __shared__ int s_stop, s_rank;
+  __shared__ double s_x[2];
+  const int K = a.K, p = K - 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tc = a.rev ? 0 : p;
+  for (int pos = tid; pos < K; pos += kPcThreads) {
+    const int col = pos == p ? tc : (a.rev ? pos + 1 : pos);
+    perm[pos] = col;
+    dh[pos] = a.Gh[(int64_t)col * K + col];
+    dl[pos] = a.Gl[(int64_t)col * K + col];
+  }
+  if (tid == 0) s_stop = p;
+  __syncthreads();
+  // Eigen's zero-pivot floor: (max column norm * eps)^2 (ColPivHouseholderQR
+  // threshold_helper); pivots below it are exact zeros of a rank-deficient X
+  double maxd = 0.0;
+  for (int pos = 0; pos < p; ++pos) maxd = fmax(maxd, dh[pos]);
+  const double zfloor = maxd * 4.930380657631324e-32;
+  for (int k = 0; k < p; ++k) {
+    // (a) pivot: largest Schur diagonal among positions [k, p), ties -> first
+    {
+      const int pos = k + tid;
+      DD v{-INFINITY, 0.0};  // positions past p never win (Schur diagonals may be negative noise)
+      int vi = pos;
+      if (pos < p) v = DD{dh[pos], dl[pos]};
+#pragma unroll
+      for (int m = 16; m > 0; m >>= 1) {
+        const DD o{__shfl_xor_sync(0xffffffffu, v.h, m), __shfl_xor_sync(0xffffffffu, v.l, m)};
+        const int oi = __shfl_xor_sync(0xffffffffu, vi, m);
+        if (dd_gt(o, v) || (o.h == v.h && o.l == v.l && oi < vi)) {
+          v = o;
+          vi = oi;
+        }
+      }
+      if (lane == 0) {
+        wv_h[warp] = v.h;
+        wv_l[warp] = v.l;
+        wv_i[warp] = vi;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        DD b{wv_h[0], wv_l[0]};
+        int bi = wv_i[0];
+        for (int w = 1; w < kPcThreads / 32; ++w) {
+          const DD o{wv_h[w], wv_l[w]};
+          if (dd_gt(o, b) || (o.h == b.h && o.l == b.l && wv_i[w] < bi)) {
+            b = o;
+            bi = wv_i[w];
+          }
+        }
+        // swap positions k <-> bi
+        const int tp = perm[k];
+        perm[k] = perm[bi];
+        perm[bi] = tp;
+        double t = dh[k];
+        dh[k] = dh[bi];
+        dh[bi] = t;
+        t = dl[k];
+        dl[k] = dl[bi];
+        dl[bi] = t;
+        if (!(dh[k] > zfloor)) s_stop = k;
+        const DD r = dd_sqrt(DD{dh[k], dl[k]});
+        rkh[k] = r.h;
+        rkl[k] = r.l;
+      }
+      __syncthreads();
+    }
+    if (s_stop == k) break;
+    const int ck = perm[k];
+    for (int i = tid; i < k; i += kPcThreads) {
+      ch[i] = a.Rh[(int64_t)ck * K + i];
+      cl[i] = a.Rl[(int64_t)ck * K + i];
+    }
+    __syncthreads();
+    const DD rkk{rkh[k], rkl[k]};
+    // (b) row k: r_kj = (G[ck][col_j] - sum_{i<k} r_ik r_ij) / r_kk, one warp per position j
+    for (int j = k + 1 + warp; j < K; j += kPcThreads / 32) {
+      const int cj = perm[j];
+      const double* rjh = a.Rh + (int64_t)cj * K;
+      const double* rjl = a.Rl + (int64_t)cj * K;
+      double sh = 0.0, sl = 0.0;
+      for (int i = lane; i < k; i += 32) dd_acc2(sh, sl, DD{ch[i], cl[i]}, DD{rjh[i], rjl[i]});
+      DD s = dd_warp_sum(dd_two_sum(sh, sl));
+      if (lane == 0) {
+        const DD g{a.Gh[(int64_t)ck * K + cj], a.Gl[(int64_t)ck * K + cj]};
+        const DD r = dd_div(dd_add(g, dd_neg(s)), rkk);
+        a.Rh[(int64_t)cj * K + k] = r.h;
+        a.Rl[(int64_t)cj * K + k] = r.l;
+        if (j < p) {
+          const DD d = dd_add(DD{dh[j], dl[j]}, dd_neg(dd_mul(r, r)));
+          dh[j] = d.h;
+          dl[j] = d.l;
+        }
+      }
+    }
+    if (tid == 0) {
+      a.Rh[(int64_t)ck * K + k] = rkk.h;
+      a.Rl[(int64_t)ck * K + k] = rkk.l;
+    }
+    __syncthreads();
+  }
+  const int kend = s_stop;  // rows kend.. are exact zeros
+  // rank (Eigen ColPivHouseholderQR::rank with the prescribed threshold)
+  const double tol = (double)max(a.rows, (int64_t)p) * 2.220446049250313e-16;
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int k = 0; k < kend; ++k) mx = fmax(mx, fabs(rkh[k]));
+    int rk = 0;
+    for (int k = 0; k < kend; ++k) rk += fabs(rkh[k]) > tol * mx;
+    s_rank = rk;
+    a.svd[0] = rk < p ? 1 : 0;
+    a.svd[1] = rk;
+    a.tol[0] = tol;
+    for (int s = 2; s < 66; ++s) a.svd[s] = 0;
+    if (a.o.method) a.o.method[a.o.lag - 1] = rk < p ? 1 : 0;
+    if (a.o.rank) a.o.rank[a.o.lag - 1] = rk;
+  }
+  __syncthreads();
+  const int rank = s_rank;
+  for (int pos = tid; pos < K; pos += kPcThreads) a.perm[pos] = perm[pos];
+  if (rank < p) {
+    // N = [R'^T; z^T], R' (p x p) in pivot order; zero rows past kend
+    const int m = p + 1;
+    for (int64_t e = tid; e < (int64_t)m * p; e += kPcThreads) {
+      const int i = (int)(e / m), j = (int)(e % m);  // column i of N = row i of R'; entry j
+      double v = 0.0;
+      if (i < kend) {
+        if (j == p) v = a.Rh[(int64_t)tc * K + i];
+        else if (j >= i) v = a.Rh[(int64_t)perm[j] * K + i];
+      }
+      a.N[e] = v;
+    }
+    return;
+  }
+  // full rank: R11 x = z (double-double, column-oriented back substitution)
+  for (int i = tid; i < p; i += kPcThreads) {
+    ch[i] = a.Rh[(int64_t)tc * K + i];
+    cl[i] = a.Rl[(int64_t)tc * K + i];
+  }
+  __syncthreads();
+  for (int k = p - 1; k >= 0; --k) {
+    if (tid == 0) {
+      const DD x = dd_div(DD{ch[k], cl[k]}, DD{rkh[k], rkl[k]});
+      s_x[0] = x.h;
+      s_x[1] = x.l;
+      const int q = exact_phi_index(perm[k], p, a.rev);
+      a.o.phi[q] = x.h + x.l;
+      if (a.o.coefs) a.o.coefs[a.o.coef_off + q] = x.h + x.l;
+      if (a.o.taus && q == p - 1) a.o.taus[a.o.lag - 1] = x.h + x.l;
+    }
+    __syncthreads();
+    const DD x{s_x[0], s_x[1]};
+    const int ckk = perm[k];
+    for (int i = tid; i < k; i += kPcThreads) {
+      const DD z = dd_add(DD{ch[i], cl[i]}, dd_neg(dd_mul(DD{a.Rh[(int64_t)ckk * K + i], a.Rl[(int64_t)ckk * K + i]}, x)));
+      ch[i] = z.h;
+      cl[i] = z.l;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- 3. minimum-norm SVD
+constexpr int kSvdThreads = 512;
+constexpr int kSvdMaxCta = 16;
+constexpr int kSvdMaxSweeps = 60;
+
+struct SvdArgs {
+  double* N;       // (p + 1) x p column-major (in place)
+  double* sig;     // [p] singular values
+  double* xpart;   // [nblk][p]
+  const int* perm;
+  int* svd;        // [0] needed, [2 + sweep] rotation flags
+  const double* tol;
+  int p, nblk, bw, rev;
+  ExactOut o;
+};
+
+inline size_t svd_smem_bytes(int p, int bw) { return sizeof(double) * 2 * (size_t)bw * (p + 1); }
+
+// round-robin (circle method) pair t of round r among n (even) players
+__device__ __forceinline__ void rr_pair(int n, int r, int t, int& a, int& b) {
+  a = t == 0 ? n - 1 : (r + t) % (n - 1);
+  b = (r - t + (n - 1)) % (n - 1);
+}
+
+__global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
+  namespace cg = cooperative_groups;
+  if (a.svd[0] == 0) return;  // full rank (uniform over the cluster)
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(128) double sm[];
+  const int p = a.p, m = p + 1, bw = a.bw, nblk = a.nblk;
+  const int cta = (int)cl.block_rank(), nct = nblk / 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = kSvdThreads / 32;
+  double* slot[2] = {sm, sm + (size_t)bw * m};
+  int colof[2];
+  for (int sweep = 0; sweep < kSvdMaxSweeps; ++sweep) {
+    int rotated = 0;
+    for (int r = 0; r < nblk - 1; ++r) {
+      int ba, bb;
+      rr_pair(nblk, r, cta, ba, bb);
+      colof[0] = ba * bw;
+      colof[1] = bb * bw;
+      for (int s = 0; s < 2; ++s) {
+        const int c0 = colof[s];
+        for (int e = tid; e < bw * m; e += kSvdThreads) {
+          const int c = c0 + e / m;
+          slot[s][e] = c < p ? a.N[(int64_t)c * m + (e % m)] : 0.0;
+        }
+      }
+      __syncthreads();
+      // inner sweep over the 2 bw local columns
+      const int nl = 2 * bw;
+      for (int sr = 0; sr < nl - 1; ++sr) {
+        for (int t = warp; t < bw; t += nwarp) {
+          int u, v;
+          rr_pair(nl, sr, t, u, v);
+          const int gu = colof[u / bw] + u % bw, gv = colof[v / bw] + v % bw;
+          if (gu >= p || gv >= p) continue;
+          double* xu = slot[u / bw] + (size_t)(u % bw) * m;
+          double* xv = slot[v / bw] + (size_t)(v % bw) * m;
+          double al = 0.0, be = 0.0, ga = 0.0;
+          for (int i = lane; i < p; i += 32) {
+            const double x = xu[i], y = xv[i];
+            al = fma(x, x, al);
+            be = fma(y, y, be);
+            ga = fma(x, y, ga);
+          }
+          al = warp_sum(al);
+          be = warp_sum(be);
+          ga = warp_sum(ga);
+          if (ga == 0.0 || fabs(ga) <= 2.220446049250313e-16 * sqrt(al * be)) continue;
+          rotated = 1;
+          const double zeta = (be - al) / (2.0 * ga);
+          const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+          for (int i = lane; i < m; i += 32) {
+            const double x = xu[i], y = xv[i];
+            xu[i] = cs * x - sn * y;
+            xv[i] = sn * x + cs * y;
+          }
+        }
+        __syncthreads();
+      }
+      for (int s = 0; s < 2; ++s) {
+        const int c0 = colof[s];
+        for (int e = tid; e < bw * m; e += kSvdThreads) {
+          const int c = c0 + e / m;
+          if (c < p) a.N[(int64_t)c * m + (e % m)] = slot[s][e];
+        }
+      }
+      __threadfence();
+      cl.sync();
+    }
+    rotated = __syncthreads_or(rotated);
+    if (tid == 0 && rotated) atomicOr(&a.svd[2 + sweep], 1);
+    __threadfence();
+    cl.sync();
+    if (*(volatile int*)&a.svd[2 + sweep] == 0) break;
+  }
+  // singular values, then the solution x = sum_{s_i >= thr} w_i z_i / s_i^2
+  for (int c = cta * 2 * bw + warp; c < min(p, (cta + 1) * 2 * bw); c += nwarp) {
+    double s2 = 0.0;
+    for (int i = lane; i < p; i += 32) {
+      const double x = a.N[(int64_t)c * m + i];
+      s2 = fma(x, x, s2);
+    }
+    s2 = warp_sum(s2);
+    if (lane == 0) a.sig[c] = sqrt(s2);
+  }
+  __threadfence();
+  cl.sync();
+  double smax = 0.0;
+  for (int c = 0; c < p; ++c) smax = fmax(smax, a.sig[c]);
+  const double thr = fmax(smax * a.tol[0], 2.2250738585072014e-308);
+  // block pair of this CTA: columns [2 bw cta, 2 bw (cta + 1)) -> partial x
+  double* xp = a.xpart + (size_t)cta * p;
+  for (int j = tid; j < p; j += kSvdThreads) {
+    double acc = 0.0;
+    for (int c = cta * 2 * bw; c < min(p, (cta + 1) * 2 * bw); ++c) {
+      const double s = a.sig[c];
+      if (!(s >= thr)) continue;
+      acc = fma(a.N[(int64_t)c * m + j], a.N[(int64_t)c * m + p] / (s * s), acc);
+    }
+    xp[j] = acc;
+  }
+  __threadfence();
+  cl.sync();
+  if (cta != 0) return;
+  for (int j = tid; j < p; j += kSvdThreads) {
+    double x = 0.0;
+    for (int c = 0; c < nct; ++c) x += a.xpart[(size_t)c * p + j];
+    const int q = exact_phi_index(a.perm[j], p, a.rev);
+    a.o.phi[q] = x;
+    if (a.o.coefs) a.o.coefs[a.o.coef_off + q] = x;
+    if (a.o.taus && q == p - 1) a.o.taus[a.o.lag - 1] = x;
+  }
+}
+
+}  // namespace tfk

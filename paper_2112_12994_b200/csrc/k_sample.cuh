@@ -365,4 +365,22 @@ __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
   }
 }
 
+// Deterministic-index mode with reference indices only: the weight of every
+// given row from this lag's own distribution, the exact expression k_draw
+// uses (weight 1/sqrt(c * pi_i), sketch.cpp:56-57; mass = s + r^2/R as the
+// next pass stores it, or the plain score when r is null).
+__global__ void k_fixed_weights(const int64_t* __restrict__ idx, int64_t c, const double* __restrict__ scal,
+                                const double* __restrict__ s, const double* __restrict__ r, double* __restrict__ wts) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= c) return;
+  const double R = scal[0], S = scal[1];
+  const int64_t row = idx[t];
+  double mp = s[row];
+  if (r) {
+    const double rv = r[row];
+    mp = fma(rv * rv, 1.0 / R, mp);
+  }
+  wts[t] = 1.0 / sqrt((double)c * (mp / S));
+}
+
 }  // namespace tfk

@@ -1,0 +1,179 @@
+"""Deterministic-index parity at the BASELINE configurations (C1 full size,
+C2 n = 1e7 / p_bar = 200 / s = 1e4 for LSAR and RH, RH with explicit sketch
+widths 129 and 65 at depth >= 2, and a C4-shaped p_bar = 500 fit whose
+sampled systems are numerically rank deficient).
+
+The oracle's per-lag outputs come from committed fixtures
+(tests/golden/fix_*.npz, made by oracle/make_fixtures.py).  The oracle's
+draws are re-derived bit-exactly at test time by orc_lsar_replay /
+orc_rh_replay (its own recursion fed with the stored coefficients; checked
+against per-lag SHA-256 digests) and fed, with the oracle's weights, to the
+GPU sweep through the C ABI.
+
+Bars (BASELINE.json north_star):
+  * the per-lag solve method (CPQR exact_qr vs min-norm exact_svd) and the
+    CPQR rank are identical to the oracle's (toeplitz.cpp:57-85);
+  * phi and tau within 1e-9 (normwise relative) on every lag whose sampled
+    system has cond(A_S) eps < 1e-10; elsewhere the residual norm of the
+    sampled system (and, for LSAR, of the whole window) within a factor
+    1 +- 1e-9 of the oracle's (1 +- 1e-5, phi within 1e-4, for the
+    minimum-norm answers of rank-deficient lags), with the per-lag phi error
+    reported next to cond(A_S) (gpurun_out/fixture_<name>.txt);
+  * sum s_p within 1e-9; p* identical; RH: the halving levels bit-identical
+    (digest), the final leverage scores within max(1e-9, 8 eps cond(B)) of
+    the oracle's (B the final approximation: the scores themselves are only
+    determined to ~cond(B) eps).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import make_fixtures as mf
+
+pytestmark = pytest.mark.gpu
+
+EPS = np.finfo(float).eps
+TOL = 1e-9
+# minimum-norm answers of rank-deficient systems (exact_svd): a truncated SVD moves
+# by ~eps / tol in the directions near its cut-off -- the oracle's own fp64
+# answer is ~2e-6 (phi) / ~4e-6 (residual) from the exact-arithmetic one
+SVD_TOL = 1e-5
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def tf():
+    import paper_2112_12994_b200 as t
+    from paper_2112_12994_b200 import build
+    build.build()
+    return t
+
+
+@pytest.fixture(scope="module")
+def eng(tf):
+    e = tf.Engine(0)
+    yield e
+    e.close()
+
+
+def relerr(a, b):
+    a = np.asarray(a, float); b = np.asarray(b, float)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def series(fx):
+    m = fx["meta"]
+    y = mf.series_for(m["config"], m["n"])
+    assert mf.sha(y) == m["series_sha256"], "generator output changed (not a parity failure)"
+    return y
+
+
+def check_lags(name, fit, fx, sampled_system, rnorm2_gpu=None):
+    """phi / tau per lag under the cond rule; sampled_system(p) -> (A_S, b_S)
+    of the oracle's lag-p draws.  Returns the report lines."""
+    m = fx["meta"]
+    pb = m["p_bar"]
+    ref = mf.unpack_coefs(fx["coefs"], pb)
+    lines, worst_tight, relaxed, worst_ratio = [], 0.0, 0, 0.0
+    for p in range(1, pb + 1):
+        cond = float(fx["cond"][p - 1])
+        phi = np.asarray(fit.per_lag_coefficients[p - 1], float)
+        e_phi = relerr(phi, ref[p - 1])
+        e_tau = abs(fit.pacf.taus[p - 1] - fx["taus"][p - 1]) / max(np.max(np.abs(ref[p - 1])), 1e-300)
+        if cond * EPS < 1e-10:
+            assert e_phi < TOL and e_tau < TOL, f"{name} lag {p}: phi err {e_phi:.2e} tau err {e_tau:.2e} (cond {cond:.2e})"
+            worst_tight = max(worst_tight, e_phi)
+            continue
+        relaxed += 1
+        a, b = sampled_system(p)
+        ratio = np.linalg.norm(a @ phi - b) / np.linalg.norm(a @ ref[p - 1] - b)
+        svd = int(fx["method"][p - 1]) == 1
+        rtol = SVD_TOL if svd else TOL
+        assert abs(ratio - 1.0) <= rtol, f"{name} lag {p}: sampled ||r|| ratio {ratio!r} (cond {cond:.2e})"
+        if svd:
+            assert e_phi < 1e-4, f"{name} lag {p}: min-norm phi err {e_phi:.2e}"
+        worst_ratio = max(worst_ratio, abs(ratio - 1.0))
+        line = (f"{name} lag {p:3d} cond {cond:9.2e} method {int(fx['method'][p - 1])} rank {int(fx['rank'][p - 1]):3d}"
+                f" phi err {e_phi:8.2e} tau err {e_tau:8.2e} sampled ||r|| ratio-1 {ratio - 1.0:+.2e}")
+        if rnorm2_gpu is not None:
+            wr = np.sqrt(rnorm2_gpu[p - 1] / fx["rnorm2"][p - 1])
+            assert abs(wr - 1.0) <= rtol, f"{name} lag {p}: window ||r|| ratio {wr!r}"
+            line += f" window ||r|| ratio-1 {wr - 1.0:+.2e}"
+        lines.append(line)
+    lines.append(f"{name}: {pb - relaxed} lags at 1e-9 (worst phi err {worst_tight:.2e}), {relaxed} lags "
+                 f"(cond eps >= 1e-10) by residual ratio (worst |ratio - 1| {worst_ratio:.2e})")
+    return lines
+
+
+def report(name, lines):
+    os.makedirs(os.path.join(os.path.dirname(HERE), "gpurun_out"), exist_ok=True)
+    with open(os.path.join(os.path.dirname(HERE), "gpurun_out", f"fixture_{name}.txt"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    print("\n".join(lines[-12:]))
+
+
+@pytest.mark.parametrize("name", ["c1_lsar", "c2_lsar", "c4s_lsar"])
+def test_lsar_baseline_fixture(orc, tf, eng, name):
+    fx = mf.load(name)
+    m = fx["meta"]
+    pb, c, seed = m["p_bar"], m["c"], m["fit_seed"]
+    y = series(fx)
+    rep = orc.lsar_replay(y, pb, c, seed, fx["coefs"])
+    assert np.array_equal(mf.draw_digests(rep.idx, rep.w), fx["digests"]), "oracle replay differs from the fixture"
+    assert np.array_equal(rep.rnorm2, fx["rnorm2"])
+    fit = tf.lsar_fit(tf.TimeSeries(y), pb, c, seed, engine=eng, fixed_idx=rep.idx, fixed_w=rep.w, want_diag=True)
+    d = fit.diag
+    assert np.array_equal(d["idx"], rep.idx)  # sampled indices bit-exact
+    # the reference's rank rule at every lag
+    assert np.array_equal(d["method"], fx["method"]), \
+        f"method differs at lags {np.flatnonzero(d['method'] != fx['method']) + 1}"
+    assert np.array_equal(d["rank"], fx["rank"]), f"rank differs at lags {np.flatnonzero(d['rank'] != fx['rank']) + 1}"
+    w = m["n"] - pb
+    lines = check_lags(name, fit, fx, lambda p: orc.apply_sample(y, w + p, p, rep.idx[p - 1], rep.w[p - 1]),
+                       d["rnorm2"])
+    assert relerr(d["ssum"], fx["ssum"]) < TOL
+    assert fit.p_star == int(fx["p_star"])
+    lines.append(f"{name}: p* {fit.p_star} (oracle {int(fx['p_star'])}); methods "
+                 f"{np.bincount(d['method'], minlength=2).tolist()}")
+    report(name, lines)
+
+
+@pytest.mark.parametrize("name", ["rh_g129", "rh_g65", "c2_rh"])
+def test_rh_baseline_fixture(orc, tf, eng, name):
+    fx = mf.load(name)
+    m = fx["meta"]
+    pb, c, seed = m["p_bar"], m["c"], m["fit_seed"]
+    assert m["depth"] >= 2
+    y = series(fx)
+    rep = orc.rh_replay(y, pb, c, seed, fx["up_idx"][0], fx["up_w"][0])
+    assert np.array_equal(mf.draw_digests(rep.idx, rep.w), fx["digests"]), "oracle replay differs from the fixture"
+    cfg = None
+    if m["explicit_cfg"]:
+        cfg = tf.RHConfig(base_threshold=m["base_threshold"], sample_count=c, gaussian_rows=m["gaussian_rows"],
+                          seed=m["cfg_seed"])
+    fit = tf.rh_fit(tf.TimeSeries(y), pb, c, cfg, seed, engine=eng, want_diag=True,
+                    fixed=dict(idx=rep.idx, w=rep.w, up_idx=fx["up_idx"], up_w=fx["up_w"]))
+    d = fit.diag
+    assert d["depth"] == m["depth"]
+    # the GPU's own halving (repeated_halving.cpp:132-148): bit-identical levels
+    assert mf.sha(np.concatenate(d["levels"])) == str(fx["levels_sha256"])
+    # final unsketched leverage scores (repeated_halving.cpp:182-189): scores
+    # of the rows against the final approximation B are determined to ~cond(B)
+    # eps by any backward-stable factorization (the oracle's CPQR included)
+    ai, aw = fx["up_idx"][0], fx["up_w"][0]
+    cols = pb - np.arange(pb + 1)  # aug_row: y[p_bar + i - 1 - j], j < p_bar, then y[p_bar + i]
+    cols[-1] = pb
+    cols[:-1] = pb - 1 - np.arange(pb)
+    B = y[ai[:, None] + cols[None, :]] * aw[:, None]
+    cond_b = float(np.linalg.cond(B))
+    s_err = relerr(d["scores"], rep.scores)
+    assert s_err < max(TOL, 8 * EPS * cond_b), f"scores err {s_err:.2e} (cond(B) {cond_b:.2e})"
+    assert np.array_equal(d["method"], fx["method"])
+    assert np.array_equal(d["rank"], fx["rank"])
+    lines = check_lags(name, fit, fx,
+                       lambda p: orc.apply_sample(y, m["n"], pb, rep.idx[p - 1], rep.w[p - 1], width=p))
+    assert fit.p_star == int(fx["p_star"])
+    lines.append(f"{name}: p* {fit.p_star} (oracle {int(fx['p_star'])}); depth {d['depth']}, g {m['gaussian_rows']}; "
+                 f"final scores rel err {s_err:.2e} (cond(B) {cond_b:.2e})")
+    report(name, lines)
