@@ -191,6 +191,15 @@ def solve_exact(a, b):
     return x, method.value, rank.value
 
 
+def residual_norm_dd(a, b, x) -> float:
+    """||a x - b|| in double-double (exact products, compensated sums)."""
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    b = f64(b); x = f64(x)
+    lib().orc_residual_norm_dd.restype = C.c_double
+    return float(lib().orc_residual_norm_dd(a.ctypes.data_as(_f64p), C.c_int64(a.shape[0]), C.c_int64(a.shape[1]),
+                                            _p(b), _p(x)))
+
+
 def exact_leverage(a) -> np.ndarray:
     a = np.asarray(a, dtype=np.float64)
     rows, cols = a.shape

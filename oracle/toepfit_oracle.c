@@ -557,6 +557,30 @@ static void minnorm_solve(const double* a, int64_t rows, int64_t cols, const dou
   }
 }
 
+/* ||A x - b|| of a column-major system evaluated in double-double (exact
+ * products by fma, TwoSum accumulation): the residual of a given x, free of
+ * the cancellation that swamps a plain fp64 evaluation when ||r|| << ||b||
+ * (C4-like series, |y| ~ 1e19 against unit innovations).  Test helper. */
+static inline void dd_acc_c(double* h, double* l, double a, double b) {
+  const double p = a * b;
+  const double e = fma(a, b, -p);
+  const double s = *h + p;
+  const double bb = s - *h;
+  *l += ((*h - (s - bb)) + (p - bb)) + e;
+  *h = s;
+}
+double orc_residual_norm_dd(const double* a, int64_t rows, int64_t cols, const double* b, const double* x) {
+  double th = 0.0, tl = 0.0;
+  for (int64_t i = 0; i < rows; ++i) {
+    double h = 0.0, l = 0.0;
+    for (int64_t j = 0; j < cols; ++j) dd_acc_c(&h, &l, a[i + j * rows], x[j]);
+    dd_acc_c(&h, &l, b[i], -1.0);
+    const double r = h + l;
+    dd_acc_c(&th, &tl, r, r);
+  }
+  return sqrt(th + tl);
+}
+
 /* toeplitz.cpp:57-85 */
 int orc_solve_exact(const double* a, int64_t rows, int64_t cols, const double* b, double* x,
                     int* method_out, int64_t* rank_out) {

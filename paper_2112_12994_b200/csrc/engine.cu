@@ -477,6 +477,7 @@ static void reserve_exact(tf_context* ctx, int64_t c, int Kmax) {
   b.sig.need(Kmax);
   b.xpart.need((size_t)2 * kSvdMaxCta * Kmax);
   b.tolv.need(2);
+  b.Dd.need((size_t)4 * Kmax);
   b.perm.need(Kmax);
   b.svdf.need(2 + kSvdMaxSweeps + 8);
 }
@@ -508,8 +509,24 @@ static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev,
   pa.tol = b.tolv.get();
   pa.o = o;
   pa.gate = nullptr;
-  k_pchol_dd<<<1, kPcThreads, 0, st>>>(pa);
-  LAUNCH_CHECK("k_pchol_dd");
+  pa.Dh = b.Dd.get();
+  pa.Dl = b.Dd.get() + 2 * K;
+  {
+    const int pc = pchol_ctas(K);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)pc);
+    cfg.blockDim = dim3(kPcThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)pc;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_pchol_dd, pa));
+  }
   int nct, nblk, bw;
   svd_plan(p, nct, nblk, bw);
   SvdArgs sa{};

@@ -43,7 +43,7 @@ struct SolveBufs {
   DBuf<int> flags;
   // rank-revealing solve (k_exact.cuh): double-double Gram partials and
   // planes, pivoted factor, SVD matrix / singular values / partial solutions
-  DBuf<double> Wdd, Gh, Gl, Rh, Rl, Nsv, sig, xpart, tolv;
+  DBuf<double> Wdd, Gh, Gl, Rh, Rl, Dd, Nsv, sig, xpart, tolv;
   DBuf<int> perm, svdf;
 };
 

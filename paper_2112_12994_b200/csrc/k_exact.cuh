@@ -235,7 +235,7 @@ __global__ void k_gram_dd_reduce(const double* __restrict__ W, int npair, int ns
 
 // ---------------------------------------------------------------- 2. pivoted Cholesky
 constexpr int kPcThreads = 1024;
-constexpr int kPcMaxK = 704;  // K <= kExactMaxP + 1 (static shared memory: 6 double + 1 int arrays)
+constexpr int kPcMaxK = 1024;  // K <= kExactMaxP + 1 (static shared memory: 4 double + 1 int arrays)
 
 struct ExactOut {
   double* phi;     // [p] reference order (lag j + 1 at index j)
@@ -255,6 +255,8 @@ struct PcholArgs {
   int64_t rows;    // sampled rows (tolerance max(rows, p) eps)
   double* Rh;      // workspace K x K: Rh[col * K + i] = r_{i, pos(col)} (by original column)
   double* Rl;
+  double* Dh;      // workspace [2][K]: Schur diagonal by original column, double buffered over
+  double* Dl;      //   steps (step k reads buffer k & 1, writes the other: no cross-CTA race)
   double* N;       // SVD input (p + 1) x p, column-major: column i = row i of R', row p = z_i
   int* perm;       // [K] pivot position -> original column
   int* svd;        // [0] rank deficient, [1] rank, [2..] sweep convergence flags (zeroed)
@@ -265,39 +267,54 @@ struct PcholArgs {
 
 __device__ __forceinline__ int exact_phi_index(int col, int p, int rev) { return rev ? col - 1 : p - 1 - col; }
 
+inline int pchol_ctas(int K) { return K > 256 ? 8 : K > 96 ? 4 : 1; }
+
+// One thread-block cluster.  Every CTA keeps an identical copy of the pivot
+// order and of r_kk (it computes the same argmax from the same global Schur
+// diagonal); the positions of row k are split over all warps of the cluster;
+// one cluster barrier per step publishes row k and the updated diagonal.
 __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
+  namespace cg = cooperative_groups;
   if (a.gate && *a.gate == 0) return;
+  cg::cluster_group clu = cg::this_cluster();
   __shared__ int perm[kPcMaxK];
-  __shared__ double dh[kPcMaxK], dl[kPcMaxK];
   __shared__ double ch[kPcMaxK], cl[kPcMaxK];  // pivot column: r_{i,k}, i < k (then reused for z')
   __shared__ double rkh[kPcMaxK], rkl[kPcMaxK];
   __shared__ double wv_h[32], wv_l[32];
   __shared__ int wv_i[32];
-  __shared__ int s_stop, s_rank;
+  __shared__ int s_stop;
   __shared__ double s_x[2];
   const int K = a.K, p = K - 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cta = (int)clu.block_rank(), nct = (int)clu.num_blocks();
+  const int gwarp = cta * (kPcThreads / 32) + warp, nwarps = nct * (kPcThreads / 32);
   const int tc = a.rev ? 0 : p;
-  for (int pos = tid; pos < K; pos += kPcThreads) {
-    const int col = pos == p ? tc : (a.rev ? pos + 1 : pos);
-    perm[pos] = col;
-    dh[pos] = a.Gh[(int64_t)col * K + col];
-    dl[pos] = a.Gl[(int64_t)col * K + col];
+  for (int pos = tid; pos < K; pos += kPcThreads) perm[pos] = pos == p ? tc : (a.rev ? pos + 1 : pos);
+  for (int col = cta * kPcThreads + tid; col < K; col += nct * kPcThreads) {
+    a.Dh[col] = a.Gh[(int64_t)col * K + col];
+    a.Dl[col] = a.Gl[(int64_t)col * K + col];
+    a.Dh[K + col] = a.Dh[col];
+    a.Dl[K + col] = a.Dl[col];
   }
   if (tid == 0) s_stop = p;
-  __syncthreads();
+  __threadfence();
+  clu.sync();
   // Eigen's zero-pivot floor: (max column norm * eps)^2 (ColPivHouseholderQR
   // threshold_helper); pivots below it are exact zeros of a rank-deficient X
   double maxd = 0.0;
-  for (int pos = 0; pos < p; ++pos) maxd = fmax(maxd, dh[pos]);
+  for (int pos = 0; pos < p; ++pos) maxd = fmax(maxd, a.Dh[perm[pos]]);
   const double zfloor = maxd * 4.930380657631324e-32;
   for (int k = 0; k < p; ++k) {
+    const double* Dch = a.Dh + (k & 1) * K;
+    const double* Dcl = a.Dl + (k & 1) * K;
+    double* Dnh = a.Dh + ((k + 1) & 1) * K;
+    double* Dnl = a.Dl + ((k + 1) & 1) * K;
     // (a) pivot: largest Schur diagonal among positions [k, p), ties -> first
     {
       const int pos = k + tid;
       DD v{-INFINITY, 0.0};  // positions past p never win (Schur diagonals may be negative noise)
       int vi = pos;
-      if (pos < p) v = DD{dh[pos], dl[pos]};
+      if (pos < p) v = DD{Dch[perm[pos]], Dcl[perm[pos]]};
 #pragma unroll
       for (int m = 16; m > 0; m >>= 1) {
         const DD o{__shfl_xor_sync(0xffffffffu, v.h, m), __shfl_xor_sync(0xffffffffu, v.l, m)};
@@ -323,18 +340,11 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
             bi = wv_i[w];
           }
         }
-        // swap positions k <-> bi
-        const int tp = perm[k];
+        const int tp = perm[k];  // swap positions k <-> bi (identically in every CTA)
         perm[k] = perm[bi];
         perm[bi] = tp;
-        double t = dh[k];
-        dh[k] = dh[bi];
-        dh[bi] = t;
-        t = dl[k];
-        dl[k] = dl[bi];
-        dl[bi] = t;
-        if (!(dh[k] > zfloor)) s_stop = k;
-        const DD r = dd_sqrt(DD{dh[k], dl[k]});
+        if (!(b.h > zfloor)) s_stop = k;
+        const DD r = dd_sqrt(b);
         rkh[k] = r.h;
         rkl[k] = r.l;
       }
@@ -349,7 +359,7 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
     __syncthreads();
     const DD rkk{rkh[k], rkl[k]};
     // (b) row k: r_kj = (G[ck][col_j] - sum_{i<k} r_ik r_ij) / r_kk, one warp per position j
-    for (int j = k + 1 + warp; j < K; j += kPcThreads / 32) {
+    for (int j = k + 1 + gwarp; j < K; j += nwarps) {
       const int cj = perm[j];
       const double* rjh = a.Rh + (int64_t)cj * K;
       const double* rjl = a.Rl + (int64_t)cj * K;
@@ -362,41 +372,40 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
         a.Rh[(int64_t)cj * K + k] = r.h;
         a.Rl[(int64_t)cj * K + k] = r.l;
         if (j < p) {
-          const DD d = dd_add(DD{dh[j], dl[j]}, dd_neg(dd_mul(r, r)));
-          dh[j] = d.h;
-          dl[j] = d.l;
+          const DD d = dd_add(DD{Dch[cj], Dcl[cj]}, dd_neg(dd_mul(r, r)));
+          Dnh[cj] = d.h;
+          Dnl[cj] = d.l;
         }
       }
     }
-    if (tid == 0) {
+    if (cta == 0 && tid == 0) {
       a.Rh[(int64_t)ck * K + k] = rkk.h;
       a.Rl[(int64_t)ck * K + k] = rkk.l;
     }
-    __syncthreads();
+    __threadfence();
+    clu.sync();
   }
   const int kend = s_stop;  // rows kend.. are exact zeros
   // rank (Eigen ColPivHouseholderQR::rank with the prescribed threshold)
   const double tol = (double)max(a.rows, (int64_t)p) * 2.220446049250313e-16;
-  if (tid == 0) {
-    double mx = 0.0;
-    for (int k = 0; k < kend; ++k) mx = fmax(mx, fabs(rkh[k]));
-    int rk = 0;
-    for (int k = 0; k < kend; ++k) rk += fabs(rkh[k]) > tol * mx;
-    s_rank = rk;
-    a.svd[0] = rk < p ? 1 : 0;
-    a.svd[1] = rk;
+  double mx = 0.0;
+  for (int k = 0; k < kend; ++k) mx = fmax(mx, fabs(rkh[k]));
+  int rank = 0;
+  for (int k = 0; k < kend; ++k) rank += fabs(rkh[k]) > tol * mx;
+  if (cta == 0 && tid == 0) {
+    a.svd[0] = rank < p ? 1 : 0;
+    a.svd[1] = rank;
     a.tol[0] = tol;
     for (int s = 2; s < 66; ++s) a.svd[s] = 0;
-    if (a.o.method) a.o.method[a.o.lag - 1] = rk < p ? 1 : 0;
-    if (a.o.rank) a.o.rank[a.o.lag - 1] = rk;
+    if (a.o.method) a.o.method[a.o.lag - 1] = rank < p ? 1 : 0;
+    if (a.o.rank) a.o.rank[a.o.lag - 1] = rank;
   }
-  __syncthreads();
-  const int rank = s_rank;
-  for (int pos = tid; pos < K; pos += kPcThreads) a.perm[pos] = perm[pos];
+  if (cta == 0)
+    for (int pos = tid; pos < K; pos += kPcThreads) a.perm[pos] = perm[pos];
   if (rank < p) {
     // N = [R'^T; z^T], R' (p x p) in pivot order; zero rows past kend
     const int m = p + 1;
-    for (int64_t e = tid; e < (int64_t)m * p; e += kPcThreads) {
+    for (int64_t e = cta * kPcThreads + tid; e < (int64_t)m * p; e += (int64_t)nct * kPcThreads) {
       const int i = (int)(e / m), j = (int)(e % m);  // column i of N = row i of R'; entry j
       double v = 0.0;
       if (i < kend) {
@@ -407,6 +416,7 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
     }
     return;
   }
+  if (cta != 0) return;
   // full rank: R11 x = z (double-double, column-oriented back substitution)
   for (int i = tid; i < p; i += kPcThreads) {
     ch[i] = a.Rh[(int64_t)tc * K + i];
@@ -484,12 +494,20 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
         }
       }
       __syncthreads();
-      // inner sweep over the 2 bw local columns
+      // round 0 of a sweep (every block sits in exactly one CTA): all pairs of
+      // the 2 bw local columns, so each block's internal pairs run once per
+      // sweep; later rounds: the bw x bw cross pairs of the two blocks only
       const int nl = 2 * bw;
-      for (int sr = 0; sr < nl - 1; ++sr) {
+      const int nsub = r == 0 ? nl - 1 : bw;
+      for (int sr = 0; sr < nsub; ++sr) {
         for (int t = warp; t < bw; t += nwarp) {
           int u, v;
-          rr_pair(nl, sr, t, u, v);
+          if (r == 0) {
+            rr_pair(nl, sr, t, u, v);
+          } else {
+            u = t;
+            v = bw + (t + sr) % bw;
+          }
           const int gu = colof[u / bw] + u % bw, gv = colof[v / bw] + v % bw;
           if (gu >= p || gv >= p) continue;
           double* xu = slot[u / bw] + (size_t)(u % bw) * m;

@@ -21,7 +21,11 @@ int main() {
   ExactOut o{dphi, nullptr, 0, nullptr, dmeth, drank, 1};
   PcholArgs pa{}; pa.Gh = dGh; pa.Gl = dGl; pa.K = K; pa.rev = 0; pa.rows = c; pa.Rh = dRh; pa.Rl = dRl; pa.N = dN;
   pa.perm = dperm; pa.svd = dsvd; pa.tol = dtol; pa.o = o;
-  k_pchol_dd<<<1, kPcThreads>>>(pa);
+  double* dD; cudaMalloc(&dD, 4 * K * 8); pa.Dh = dD; pa.Dl = dD + 2 * K;
+  { int pc = pchol_ctas(K); cudaLaunchConfig_t c0{}; c0.gridDim = dim3(pc); c0.blockDim = dim3(kPcThreads);
+    cudaLaunchAttribute a0[1]; a0[0].id = cudaLaunchAttributeClusterDimension; a0[0].val.clusterDim.x = pc;
+    a0[0].val.clusterDim.y = 1; a0[0].val.clusterDim.z = 1; c0.attrs = a0; c0.numAttrs = 1;
+    cudaLaunchKernelEx(&c0, k_pchol_dd, pa); }
   int nct = std::min(16, std::max(1, (p + 31) / 32)), nblk = 2 * nct, bw = std::max(1, (p + nblk - 1) / nblk);
   SvdArgs a{}; a.N = dN; a.sig = dsig; a.xpart = dx; a.perm = dperm; a.svd = dsvd; a.tol = dtol; a.p = p; a.nblk = nblk;
   a.bw = bw; a.rev = 0; a.o = o;
