@@ -79,6 +79,7 @@ typedef struct {
   double* phase_seconds;    /* [p_bar][3] device time of sampling, solve, fused pass */
   int64_t* launches_out;    /* kernel launches issued by the sweep */
   int* rank_out;            /* [p_bar] CPQR rank of the sampled system (threshold max(c, p) eps) */
+  int* svd_sweeps_out;      /* [p_bar] Jacobi sweeps of the minimum-norm SVD (0 for exact_qr lags) */
 } tf_lsar_diag;
 
 typedef struct {

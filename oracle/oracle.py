@@ -100,6 +100,14 @@ def i64(x) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(x, dtype=np.int64))
 
 
+def set_threads(n: int) -> None:
+    lib().orc_set_threads(C.c_int(int(n)))
+
+
+def max_threads() -> int:
+    return int(lib().orc_max_threads())
+
+
 # ---------------------------------------------------------------- RNG
 def derive_seed(seed: int, tag: int) -> int:
     return int(lib().orc_derive_seed(C.c_uint64(seed), C.c_uint64(tag)))

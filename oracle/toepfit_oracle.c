@@ -100,6 +100,12 @@ uint64_t orc_rng_below(orc_rng* r, uint64_t bound) { /* rng.hpp:59-66 */
   return x % bound;
 }
 
+/* OpenMP thread count of the parallel loops (row / column independent: the
+ * results do not depend on it).  bench.py's single-core CPU baseline sets 1. */
+#include <omp.h>
+void orc_set_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }
+int orc_max_threads(void) { return omp_get_max_threads(); }
+
 uint64_t orc_derive_seed(uint64_t seed, uint64_t tag) { /* rng.hpp:82-84 */
   orc_rng r;
   orc_rng_init(&r, seed);

@@ -32,7 +32,7 @@ class TfLsarDiag(C.Structure):
     _fields_ = [("fixed_idx", _i64p), ("fixed_w", _f64p), ("idx_out", _i64p), ("w_out", _f64p),
                 ("rnorm2_out", _f64p), ("ssum_out", _f64p), ("scores_out", _f64p),
                 ("resid_out", _f64p), ("method_out", _i32p), ("phase_seconds", _f64p),
-                ("launches_out", _i64p), ("rank_out", _i32p)]
+                ("launches_out", _i64p), ("rank_out", _i32p), ("svd_sweeps_out", _i32p)]
 
 
 class TfRhDiag(C.Structure):

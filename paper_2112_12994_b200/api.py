@@ -205,6 +205,10 @@ class Engine:
         self._check(_abi.lib().tf_upload_series(self._ctx, ptr(v), v.size))
         self._series_id = (series,)
 
+    def forget_series(self):
+        """Drop the resident-series cache: the next fit re-uploads (H2D) its series."""
+        self._series_id = None
+
     def upload_device(self, dev_ptr: int, n: int):
         self._check(_abi.lib().tf_upload_series_device(self._ctx, C.c_void_p(dev_ptr), n))
         self._series_id = None
@@ -270,9 +274,10 @@ class Engine:
                 d.fixed_w = ptr(fw)
         if want_diag == "light":  # phases / methods / launches only (no per-row dumps)
             diag = dict(method=np.zeros(pb, np.int32), rank=np.zeros(pb, np.int32), phases=np.zeros((pb, 3)),
-                        launches=np.zeros(1, np.int64))
+                        launches=np.zeros(1, np.int64), svd_sweeps=np.zeros(pb, np.int32))
             d.method_out = ptr(diag["method"], _abi._i32p)
             d.rank_out = ptr(diag["rank"], _abi._i32p)
+            d.svd_sweeps_out = ptr(diag["svd_sweeps"], _abi._i32p)
             d.phase_seconds = ptr(diag["phases"])
             d.launches_out = ptr(diag["launches"], _abi._i64p)
         elif want_diag:
@@ -371,6 +376,12 @@ class Engine:
         out = np.empty(int(n))
         self._check(_abi.lib().tf_download_series(self._ctx, ptr(out), int(n)))
         return out
+
+    def download_series_into(self, out: np.ndarray) -> None:
+        """D2H of the resident series into a caller buffer (e.g. pinned host memory)."""
+        if out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise UsageError("output must be a contiguous float64 array")
+        self._check(_abi.lib().tf_download_series(self._ctx, ptr(out), int(out.size)))
 
     def exact_sweep(self, p_bar: int):
         pb = max(int(p_bar), 1)

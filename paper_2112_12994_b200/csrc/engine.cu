@@ -795,6 +795,7 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
   }
   reserve_exact(ctx, c, p_bar + 1);
   ctx->rank.need(p_bar);
+  ctx->sweeps.need(p_bar);
   ensure_events(ctx, p_bar + 1);
   const bool phases = d && d->phase_seconds;
   while (phases && ctx->pev.size() < 2 * (size_t)p_bar) {
@@ -846,7 +847,7 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
       if (phases) rec(ctx->pev[2 * (p - 1)]);
       // rank-revealing solve of the sampled lag-p system (toeplitz.cpp:57-85)
       ExactOut o{ctx->phi.get(), ctx->coefs.get(), (int64_t)(p - 1) * p / 2, ctx->taus.get(), ctx->method.get(),
-                 ctx->rank.get(), p};
+                 ctx->rank.get(), p, ctx->sweeps.get()};
       solve_exact(ctx, FwdRows{ctx->y.get(), idx, wts, 0}, c, p + 1, /*rev=*/0, o);
       if (phases) rec(ctx->pev[2 * (p - 1) + 1]);
       // residuals of the lag-p window fit + score update s_p = s_{p-1} + r_{p-1}^2/R_{p-1}
@@ -890,6 +891,8 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
     if (d->resid_out) CK(cudaMemcpy(d->resid_out, ctx->r.get(), sizeof(double) * w, cudaMemcpyDeviceToHost));
     if (d->method_out) CK(cudaMemcpy(d->method_out, ctx->method.get(), sizeof(int) * p_bar, cudaMemcpyDeviceToHost));
     if (d->rank_out) CK(cudaMemcpy(d->rank_out, ctx->rank.get(), sizeof(int) * p_bar, cudaMemcpyDeviceToHost));
+    if (d->svd_sweeps_out)
+      CK(cudaMemcpy(d->svd_sweeps_out, ctx->sweeps.get(), sizeof(int) * p_bar, cudaMemcpyDeviceToHost));
     if (d->launches_out) *d->launches_out = launches;
     if (phases)
       for (int p = 1; p <= p_bar; ++p) {
@@ -1286,7 +1289,7 @@ static void solve_sampled_op(tf_context* ctx, const double* y, int64_t n_used, i
   CK(cudaMemcpyAsync(ctx->wts.get(), w, c * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   reserve_exact(ctx, c, p + 1);
   ctx->rank.need(1);
-  ExactOut o{ctx->phi.get(), nullptr, 0, nullptr, ctx->method.get(), ctx->rank.get(), 1};
+  ExactOut o{ctx->phi.get(), nullptr, 0, nullptr, ctx->method.get(), ctx->rank.get(), 1, nullptr};
   solve_exact(ctx, FwdRows{ctx->y.get(), ctx->idx.get(), ctx->wts.get(), 0}, c, p + 1, /*rev=*/0, o);
   CK(cudaMemcpyAsync(phi_out, ctx->phi.get(), p * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   int m = 0;
@@ -1689,6 +1692,7 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
   }
   reserve_exact(ctx, c, K);
   ctx->rank.need(p_bar);
+  ctx->sweeps.need(p_bar);
   bool capturing = false;
   auto rec = [&](cudaEvent_t e) {
     if (capturing) CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
@@ -1714,7 +1718,7 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
       }
       // apply_sample(full, s, p) + solve_compressed (repeated_halving.cpp:221-222)
       ExactOut o{ctx->phi.get(), ctx->coefs.get(), (int64_t)(p - 1) * p / 2, ctx->taus.get(), ctx->method.get(),
-                 ctx->rank.get(), p};
+                 ctx->rank.get(), p, ctx->sweeps.get()};
       solve_exact(ctx, RevRows{y, idx, wts, p_bar}, c, p + 1, /*rev=*/1, o);
       rec(ctx->events[p + 1]);
     }

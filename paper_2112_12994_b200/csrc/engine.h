@@ -66,7 +66,7 @@ struct tf_context {
   tfe::DBuf<int> srht_reject;
   tfe::DBuf<int64_t> idx, fidx, idx_hist;
   tfe::DBuf<double> wts, fw, w_hist;
-  tfe::DBuf<int> status, method, rank;
+  tfe::DBuf<int> status, method, rank, sweeps;
   tfe::SolveBufs sb;
   // RH state
   tfe::DBuf<int> rh_J, rh_cnt, rh_start, rh_fill, rh_bk, rh_pick, rh_ok, rh_flag;

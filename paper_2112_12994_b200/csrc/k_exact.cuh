@@ -245,6 +245,7 @@ struct ExactOut {
   int* method;     // nullable, [lag - 1] = 0 exact_qr / 1 exact_svd (toeplitz.hpp:49-56)
   int* rank;       // nullable, [lag - 1] = CPQR rank
   int lag;
+  int* sweeps;     // nullable, [lag - 1] = Jacobi sweeps of the minimum-norm SVD (0: full rank)
 };
 
 struct PcholArgs {
@@ -399,6 +400,7 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
     for (int s = 2; s < 66; ++s) a.svd[s] = 0;
     if (a.o.method) a.o.method[a.o.lag - 1] = rank < p ? 1 : 0;
     if (a.o.rank) a.o.rank[a.o.lag - 1] = rank;
+    if (a.o.sweeps) a.o.sweeps[a.o.lag - 1] = 0;
   }
   if (cta == 0)
     for (int pos = tid; pos < K; pos += kPcThreads) a.perm[pos] = perm[pos];
@@ -479,7 +481,8 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = kSvdThreads / 32;
   double* slot[2] = {sm, sm + (size_t)bw * m};
   int colof[2];
-  for (int sweep = 0; sweep < kSvdMaxSweeps; ++sweep) {
+  int sweep = 0;
+  for (; sweep < kSvdMaxSweeps; ++sweep) {
     int rotated = 0;
     for (int r = 0; r < nblk - 1; ++r) {
       int ba, bb;
@@ -551,6 +554,7 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
     cl.sync();
     if (*(volatile int*)&a.svd[2 + sweep] == 0) break;
   }
+  if (cta == 0 && tid == 0 && a.o.sweeps) a.o.sweeps[a.o.lag - 1] = sweep + 1;
   // singular values, then the solution x = sum_{s_i >= thr} w_i z_i / s_i^2
   for (int c = cta * 2 * bw + warp; c < min(p, (cta + 1) * 2 * bw); c += nwarp) {
     double s2 = 0.0;

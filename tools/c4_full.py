@@ -21,6 +21,9 @@ w = n - p_bar
 print(f"C4 LSAR n={n} p_bar={p_bar} s={cs[0]}: device {dev:.2f} s (wall {wall:.2f}); "
       f"sample {ph[0]:.2f} s, solve {ph[1]:.2f} s, pass {ph[2]:.2f} s; "
       f"{p_bar * w / dev:.3e} rows*orders/s; p*={pstar}; methods {np.bincount(diag['method'])}")
+sw = diag["svd_sweeps"]
+print("SVD sweeps per lag: mean %.1f, max %d; by p: %s" % (sw[sw > 0].mean() if (sw > 0).any() else 0, sw.max(),
+      [(p, int(sw[p - 1])) for p in (20, 50, 100, 200, 300, 400, 500) if p <= p_bar]))
 fp64 = eng.probe_fp64_peak()
 roof = sum(max(24.0 * w / 6537.3e9, (2.0 * p + 4.0) * w / (fp64 * 1e12)) for p in range(1, p_bar + 1))
 print(f"pass roofline sum {roof:.2f} s (HBM 6537 GB/s, fp64 {fp64:.1f} TF/s) -> pass at {roof / ph[2] * 100:.0f} %")
