@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--n", type=float, default=None, help="override the series length (debug)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the row-sharded NCCL sweep even at one rank (it is the default for N > 1)")
     return ap.parse_args()
 
 
@@ -211,8 +213,11 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
+        if world == 1 and "MASTER_ADDR" not in os.environ:
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29500 + os.getpid() % 1000), RANK="0",
+                              WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl, config = workload(args)
     q, lo, hi, n, p_bar, c, inn, outl = wl
@@ -220,7 +225,7 @@ def run_ours(args):
     roots = gen.ar_roots(q, lo, hi, SEED)
     eng = tf.Engine(local)
     shard = None
-    if world > 1:
+    if dist is not None:
         from paper_2112_12994_b200 import shard as sh
         shard = sh.NcclShard(eng, dist, world, rank, n, p_bar)
     if args.config in ("C3",):  # outliers: host generator, then upload
@@ -340,7 +345,7 @@ def run_ours(args):
                "path": "each rank: H2D of its slice from pinned host memory + tf_lsar_sweep_sharded + D2H"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and not args.sharded:
         est, cwall, desc = cpu_sweep_estimate(wl, threads=1)
         cpu = {"value": ro_step / est, "unit": UNIT, "cores": 1, "kind": "port", "sample": desc,
                "extrapolated_sweep_s": est}
@@ -351,6 +356,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded AR generator on the device; no dataset is named)",
+        "path": "row-sharded NCCL sweep (tf_lsar_sweep_sharded)" if shard else "tf_lsar_sweep",
         "config": config,
         "notes": {"l2": f"the series ({8 * n / 1e9:.1f} GB) and the per-row state (2 x {8 * (n - p_bar) / 1e9:.1f} GB) "
                         "exceed the 126 MB L2: every lag streams them from HBM (no flush needed)",

@@ -188,28 +188,29 @@ int tf_select_order(const double* taus, int p_bar, double bound);
  * DFMA microbenchmark, the denominator of the fp64 roofline. */
 tf_status tf_probe_fp64_peak(tf_context* ctx, double* tflops);
 
-/* ---- row-sharded LSAR steps (one process per GPU) ----
- * The caller owns the collectives (paper_2112_12994_b200/shard.py).  A shard
- * uploads y[row0 .. row0 + w_local + p_bar) with tf_upload_series; its window
- * rows are the global rows row0 .. row0 + w_local.  Per lag p the only
- * cross-rank data are this shard's (sum s, sum r^2) (allgather) and, per
- * CholeskyQR pass, the K x K Gram (allreduce sum, tile-packed layout of
- * tf_tpu_size(K) doubles).  Same recursion as tf_lsar_sweep (lsar.cpp:70-98). */
-tf_status tf_shard_open(tf_context* ctx, int p_bar, int64_t c, int64_t w_local);
-/* fused pass at lag q (phi: q host values, NULL for q = 0) with the global
- * R_{q-1}; out2 = (sum s_q, sum r_q^2) over this shard's rows */
-tf_status tf_shard_pass(tf_context* ctx, int q, const double* phi, double r_prev, double* out2);
-/* draws t of Rng(seed_p) whose global CDF position u_t * s_total falls in this
- * shard's segment [offset, offset + mass) are resolved here (sketch.cpp:20-59);
- * k_out = local draw count (kept in draw order) */
-tf_status tf_shard_sample(tf_context* ctx, uint64_t seed_p, double s_total, double offset, double r_glob,
-                          int is_last, int64_t* k_out);
-/* local Gram of the sampled rows, CholeskyQR pass 0 (Q1 = A T_p), 1 or 2 */
-tf_status tf_shard_gram(tf_context* ctx, int p, int pass, double r_prev, double* G_out);
-/* Cholesky of the reduced Gram; flags3 = (shifted, failed, need pass B) */
-tf_status tf_shard_factor(tf_context* ctx, int p, int pass, const double* G, int64_t c_total, int* flags3);
-/* phi_p (p host values) and tau_p; forms the next lag's preconditioner */
-tf_status tf_shard_finish(tf_context* ctx, int p, double* phi_out, double* tau_out);
+/* ---- row-sharded LSAR sweep of one long series (one process per GPU;
+ *      SURVEY.md 8(e); BASELINE C3 2-GPU, C4 1/2/4/8 GPUs) ----
+ * Rank g holds the window rows [row0_g, row0_g + w_g) of the global window
+ * (w = n - p_bar, contiguous balanced blocks) as the slice
+ * y[row0_g .. row0_g + w_g + p_bar) -- uploaded with tf_upload_series, or
+ * generated whole with tf_generate_series and cut with tf_keep_slice.  The
+ * communicator: rank 0 calls tf_nccl_unique_id, the caller broadcasts the
+ * bytes, every rank calls tf_nccl_init.  tf_lsar_sweep_sharded then runs the
+ * lag loop with NCCL on the context stream (no host round trips; graph
+ * captured): per lag an allgather of every shard's (sum s, sum r^2) -- the
+ * global ||r||^2 and the shards' CDF segments (prefix in rank order); each
+ * rank resolves the draws of Rng(derive_seed(seed, p)) in its segment; an
+ * allgather of the shards' double-double Gram partials, summed in rank order,
+ * so every rank runs the same rank-revealing solve and holds the same phi.
+ * The result equals lsar_fit on the whole series up to the summation order of
+ * the reductions (lsar.cpp:100-124).  Outputs as tf_lsar_sweep (on every rank);
+ * diag: rnorm2 / ssum / method / rank / phases / launches (fixed-index mode is
+ * single-shard only). */
+tf_status tf_nccl_unique_id(unsigned char* out, int bytes);  /* bytes >= 128 (ncclUniqueId) */
+tf_status tf_nccl_init(tf_context* ctx, const unsigned char* id, int world, int rank);
+tf_status tf_keep_slice(tf_context* ctx, int64_t start, int64_t len);
+tf_status tf_lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, const tf_lsar_diag* diag,
+                                double* taus, double* coefs_packed, double* lag_seconds, int* p_star);
 int64_t tf_tpu_size(int K);
 
 /* Device-time span of ctx's last sweep relative to the start of ref's last

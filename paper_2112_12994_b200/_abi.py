@@ -47,8 +47,8 @@ EXPORTS = [
     "tf_version", "tf_create", "tf_destroy", "tf_last_error", "tf_upload_series",
     "tf_upload_series_device", "tf_lsar_sweep", "tf_rh_sweep", "tf_residuals", "tf_sample_rows",
     "tf_apply_sample", "tf_solve_sampled", "tf_select_order", "tf_derive_seed",
-    "tf_probe_fp64_peak", "tf_shard_open", "tf_shard_pass", "tf_shard_sample", "tf_shard_gram",
-    "tf_shard_factor", "tf_shard_finish", "tf_tpu_size", "tf_sweep_span", "tf_exact_sweep", "tf_srht_sweep", "tf_hadamard", "tf_generate_series", "tf_download_series",
+    "tf_probe_fp64_peak", "tf_nccl_unique_id", "tf_nccl_init", "tf_keep_slice", "tf_lsar_sweep_sharded",
+    "tf_tpu_size", "tf_sweep_span", "tf_exact_sweep", "tf_srht_sweep", "tf_hadamard", "tf_generate_series", "tf_download_series",
     "tf_lsar_sweep_batch",
 ]
 
@@ -86,26 +86,28 @@ def lib():
     L.tf_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
     L.tf_derive_seed.restype = C.c_uint64
     L.tf_probe_fp64_peak.argtypes = [C.c_void_p, _f64p]
-    L.tf_shard_open.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64]
-    L.tf_shard_pass.argtypes = [C.c_void_p, C.c_int, _f64p, C.c_double, _f64p]
-    L.tf_shard_sample.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_int,
-                                  C.POINTER(C.c_int64)]
-    L.tf_shard_gram.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, _f64p]
-    L.tf_shard_factor.argtypes = [C.c_void_p, C.c_int, C.c_int, _f64p, C.c_int64, _i32p]
-    L.tf_shard_finish.argtypes = [C.c_void_p, C.c_int, _f64p, _f64p]
-    L.tf_sweep_span.argtypes = [C.c_void_p, C.c_void_p, _f64p, _f64p]
+    L.tf_nccl_unique_id.argtypes = [C.c_char_p, C.c_int]
+    L.tf_nccl_init.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int]
+    L.tf_keep_slice.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
+    L.tf_lsar_sweep_sharded.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.POINTER(TfLsarDiag),
+                                        _f64p, _f64p, _f64p, _i32p]
+    _u64p = C.POINTER(C.c_uint64)
+    L.tf_generate_series.argtypes = [C.c_void_p, _f64p, C.c_int, C.c_int64, C.c_uint64, C.c_int, C.c_int64]
+    L.tf_download_series.argtypes = [C.c_void_p, _f64p, C.c_int64]
+    L.tf_lsar_sweep_batch.argtypes = [C.c_void_p, _f64p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int64, _u64p,
+                                      _i64p, _f64p, _f64p, _f64p, _f64p, _i32p, _i32p]
     L.tf_exact_sweep.argtypes = [C.c_void_p, C.c_int, _f64p, _f64p, _f64p, _i32p]
     L.tf_srht_sweep.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_uint64, _f64p, _f64p, _f64p, _i32p]
     L.tf_hadamard.argtypes = [C.c_void_p, _f64p, C.c_int64]
-    L.tf_download_series.argtypes = [C.c_void_p, _f64p, C.c_int64]
-    L.tf_generate_series.argtypes = [C.c_void_p, _f64p, C.c_int, C.c_int64, C.c_uint64, C.c_int, C.c_int64]
-    L.tf_lsar_sweep_batch.argtypes = [C.c_void_p, _f64p, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int64,
-                                      C.POINTER(C.c_uint64), _i64p, _f64p, _f64p, _f64p, _f64p, _i32p, _i32p]
+    L.tf_sweep_span.argtypes = [C.c_void_p, C.c_void_p, _f64p, _f64p]
+    L.tf_version.argtypes = []
     L.tf_tpu_size.argtypes = [C.c_int]
     L.tf_tpu_size.restype = C.c_int64
     for name in EXPORTS:
         if not hasattr(L, name):
             raise RuntimeError(f"{LIB_PATH} does not export {name}")
+        if name not in ("tf_version",) and getattr(L, name).argtypes is None:
+            raise RuntimeError(f"{name}: no ctypes signature (64-bit arguments would be truncated)")
     _lib = L
     return L
 

@@ -250,7 +250,9 @@ class Engine:
         return taus, coefs, secs, pstar, status
 
     def lsar_sweep(self, p_bar: int, c: int, seed: int, fixed_idx=None, fixed_w=None,
-                   want_diag: bool = False, n: int | None = None):
+                   want_diag: bool = False, n: int | None = None, sharded: bool = False):
+        """tf_lsar_sweep (or, sharded=True, tf_lsar_sweep_sharded on this rank's
+        slice after tf_nccl_init -- see shard.NcclShard)."""
         pb = max(int(p_bar), 1)
         taus = np.zeros(pb)
         coefs = np.zeros(pb * (pb + 1) // 2)
@@ -296,9 +298,9 @@ class Engine:
             d.method_out = ptr(diag["method"], _abi._i32p)
             d.phase_seconds = ptr(diag["phases"])
             d.launches_out = ptr(diag["launches"], _abi._i64p)
-        self._check(_abi.lib().tf_lsar_sweep(self._ctx, int(p_bar), int(c), C.c_uint64(seed),
-                                             C.byref(d), ptr(taus), ptr(coefs), ptr(secs),
-                                             C.byref(pstar)))
+        fn = _abi.lib().tf_lsar_sweep_sharded if sharded else _abi.lib().tf_lsar_sweep
+        self._check(fn(self._ctx, int(p_bar), int(c), C.c_uint64(seed), C.byref(d), ptr(taus), ptr(coefs), ptr(secs),
+                       C.byref(pstar)))
         return taus, coefs, secs, pstar.value, diag
 
     def rh_sweep(self, p_bar: int, c: int, cfg: RHConfig | None, seed: int, fixed=None,

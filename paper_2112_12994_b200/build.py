@@ -20,11 +20,28 @@ def _stale(out, deps):
     return any(os.path.getmtime(os.path.join(HERE, d)) > t for d in deps)
 
 
+def nccl_flags() -> list:
+    """Link the NCCL that torch bundles (nvidia-nccl wheel) when present, with an
+    rpath to it: a process that also loads torch then holds ONE libnccl.so.2
+    (the system 2.27 copy lacks symbols torch 2.11 needs).  Else the system NCCL."""
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia")
+        for base in (spec.submodule_search_locations or []) if spec else []:
+            lib = os.path.join(base, "nccl", "lib")
+            inc = os.path.join(base, "nccl", "include")
+            if os.path.exists(os.path.join(lib, "libnccl.so.2")) and os.path.exists(os.path.join(inc, "nccl.h")):
+                return ["-I", inc, "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
+    except Exception:
+        pass
+    return ["-lnccl"]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     deps = SOURCES + HEADERS
     if force or _stale(OUT, deps):
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-               "-o", OUT, *[os.path.join(HERE, s) for s in SOURCES]]
+               "-o", OUT, *[os.path.join(HERE, s) for s in SOURCES], *nccl_flags()]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd)

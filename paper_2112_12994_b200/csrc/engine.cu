@@ -3,6 +3,7 @@
 // a fixed sequence of kernel launches with no host synchronisation inside the
 // sweep (device-side status flags are read once at the end).
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -37,6 +38,7 @@ static void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw TfError{TF_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
 }
 #define CK(x) cuda_check((x), #x)
+static void nccl_check(ncclResult_t r, const char* what);
 #define LAUNCH_CHECK(name) cuda_check(cudaGetLastError(), name)
 static thread_local int64_t g_launches = 0;
 #define COUNT_LAUNCH() (++g_launches)
@@ -192,7 +194,7 @@ static void qform(tf_context* ctx, const L& ld, int64_t rows, int K, const doubl
 // blocked multi-launch Cholesky for K > kCholinvMaxK (RD output, no inverse)
 static void cholinv_big(tf_context* ctx, const double* G, int K, int pass, int64_t rows, double* RD,
                         const int* gate, int lag, int* status, int force_b) {
-  ctx->sh_buf.need(16);
+  ctx->scratch.need(16);
   ctx->rh_flag.need(8);
   BigChol a;
   a.G = G;
@@ -203,7 +205,7 @@ static void cholinv_big(tf_context* ctx, const double* G, int K, int pass, int64
   a.force_b = force_b;
   a.flags = ctx->sb.flags.get();
   a.work = ctx->rh_flag.get() + 4;
-  a.tr = ctx->sh_buf.get() + 8;
+  a.tr = ctx->scratch.get() + 8;
   a.gate = gate;
   a.status = status;
   a.lag = lag;
@@ -482,19 +484,32 @@ static void reserve_exact(tf_context* ctx, int64_t c, int Kmax) {
   b.svdf.need(2 + kSvdMaxSweeps + 8);
 }
 
+// rows_dev (nullable): the device-side row count (a shard's draws, <= c);
+// sharded: the Gram partials are allgathered over ctx->comm and summed in rank
+// order, so every rank factors the same double-double Gram.
 template <class L>
-static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev, const ExactOut& o) {
+static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev, const ExactOut& o,
+                        const long long* rows_dev = nullptr, bool sharded = false) {
   SolveBufs& b = ctx->sb;
   cudaStream_t st = ctx->stream;
   const int p = K - 1;
   if (p > kExactMaxP) throw TfError{TF_USAGE, "lag order above " + std::to_string(kExactMaxP) + " (rank-revealing solve)"};
   const GramDDPlan g = gram_dd_plan(c, K, ctx->sm_count);
   k_gram_dd<L><<<dim3((unsigned)g.npair, (unsigned)g.nsplit), kDDThreads, 0, st>>>(ld, c, K, g.nblk, g.rps, g.nsplit,
-                                                                                  b.Wdd.get(), nullptr);
+                                                                                  b.Wdd.get(), rows_dev);
   LAUNCH_CHECK("k_gram_dd");
+  const int64_t KK = (int64_t)K * K;
+  double* gh = sharded ? b.Gloc.get() : b.Gh.get();
+  double* gl = sharded ? b.Gloc.get() + KK : b.Gl.get();
   k_gram_dd_reduce<<<(unsigned)(((int64_t)g.npair * 4096 + 255) / 256), 256, 0, st>>>(
-      b.Wdd.get(), g.npair, g.nsplit, g.nblk, K, b.Gh.get(), b.Gl.get(), nullptr);
+      b.Wdd.get(), g.npair, g.nsplit, g.nblk, K, gh, gl, nullptr);
   LAUNCH_CHECK("k_gram_dd_reduce");
+  if (sharded) {
+    nccl_check(ncclAllGather(b.Gloc.get(), b.Gg.get(), (size_t)(2 * KK), ncclDouble, ctx->comm, st), "ncclAllGather");
+    k_dd_sum_ranks<<<(unsigned)((KK + 255) / 256), 256, 0, st>>>(b.Gg.get(), ctx->nc_world, KK, b.Gh.get(), b.Gl.get());
+    LAUNCH_CHECK("k_dd_sum_ranks");
+    g_launches += 1;
+  }
   PcholArgs pa{};
   pa.Gh = b.Gh.get();
   pa.Gl = b.Gl.get();
@@ -1816,200 +1831,190 @@ struct CompactDrawF {
   }
 };
 
-static void shard_check(const tf_context* ctx) {
-  if (ctx->sh_pbar < 1) throw TfError{TF_USAGE, "shard session not open"};
+static void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw TfError{TF_NCCL, std::string(what) + ": " + ncclGetErrorString(r)};
 }
 
-static void shard_open(tf_context* ctx, int p_bar, int64_t c, int64_t w_local) {
+static void nccl_init(tf_context* ctx, const unsigned char* id, int world, int rank) {
+  if (world < 1 || rank < 0 || rank >= world) throw TfError{TF_USAGE, "invalid rank / world size"};
+  if (ctx->comm) {
+    ncclCommDestroy(ctx->comm);
+    ctx->comm = nullptr;
+  }
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof uid);
+  nccl_check(ncclCommInitRank(&ctx->comm, world, uid, rank), "ncclCommInitRank");
+  ctx->nc_world = world;
+  ctx->nc_rank = rank;
+}
+
+// keep y[start, start + len) of the resident series (a shard's slice + halo)
+static void keep_slice(tf_context* ctx, int64_t start, int64_t len) {
+  if (start < 0 || len < 1 || start + len > ctx->n) throw TfError{TF_USAGE, "slice outside the resident series"};
+  tfe::DBuf<double> tmp;
+  tmp.need(len + 64);
+  CK(cudaMemcpyAsync(tmp.get(), ctx->y.get() + start, len * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaMemsetAsync(tmp.get() + len, 0, 64 * sizeof(double), ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  std::swap(ctx->y.p, tmp.p);
+  std::swap(ctx->y.n, tmp.n);
+  ctx->n = len;
+  g_alloc_gen.fetch_add(1);
+}
+
+// Row-sharded LSAR sweep of one long series, one process per
+// GPU: this context holds window rows [row0, row0 + w) of the global window as
+// the slice y[row0 .. row0 + w + p_bar) (uploaded / kept with tf_keep_slice).
+// Per lag, on the context stream, with no host synchronisation (the lag loop
+// is graph-captured, NCCL included):
+//   local fused pass -> (sum s, sum r^2) -> ncclAllGather -> k_shard_scal
+//   (global R, this shard's CDF segment) -> local scan with the global R ->
+//   the draws of Rng(derive_seed(seed, p)) that land in the segment, compacted
+//   in draw order -> double-double Gram of the local sampled rows ->
+//   ncclAllGather of the partials -> rank-ordered double-double sum -> the
+//   rank-revealing solve, identical on every rank -> phi for the next pass.
+static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, const tf_lsar_diag* d,
+                               double* taus, double* coefs, double* lag_seconds, int* p_star) {
+  if (!ctx->comm) throw TfError{TF_USAGE, "no NCCL communicator (tf_nccl_init)"};
   if (p_bar < 1) throw TfError{TF_USAGE, "maximum lag must be at least 1"};
+  if (ctx->n == 0) throw TfError{TF_USAGE, "no series uploaded"};
+  if (ctx->n <= (int64_t)p_bar) throw TfError{TF_DATA, "shard slice shorter than its rows plus the p_bar halo"};
   if (c < p_bar) throw TfError{TF_USAGE, "sample count below maximum lag"};
-  if (w_local < 1 || ctx->n < w_local + p_bar)
-    throw TfError{TF_DATA, "shard slice shorter than its rows plus the p_bar halo"};
-  ctx->sh_pbar = p_bar;
-  ctx->sh_c = c;
-  ctx->sh_w = w_local;
-  ctx->sh_k = 0;
-  alloc_state(ctx, p_bar, c, w_local);
-  reserve_solve(ctx, c, p_bar + 1);
-  ctx->sh_buf.need(8);
+  if (d && d->fixed_idx) throw TfError{TF_USAGE, "deterministic-index mode is single-shard only"};
+  const int world = ctx->nc_world, rank = ctx->nc_rank;
+  const int64_t w = ctx->n - p_bar;  // this shard's window rows
+  const int64_t ntile = (w + kPassTile - 1) / kPassTile;
+  const int K = p_bar + 1;
+  cudaStream_t st = ctx->stream;
+  alloc_state(ctx, p_bar, c, w);
+  reserve_exact(ctx, c, K);
+  ctx->rank.need(p_bar);
+  ctx->sweeps.need(p_bar);
+  ctx->sh_part.need(2);
+  ctx->sh_gath.need((size_t)3 * world);
+  ctx->sh_par.need(4);
+  ctx->sh_dummy.need(4);
   ctx->sh_idx.need(c);
   ctx->sh_wts.need(c);
   ctx->rh_ok.need(c);
-}
-
-static void shard_pass(tf_context* ctx, int q, const double* phi, double r_prev, double out[2]) {
-  shard_check(ctx);
-  cudaStream_t st = ctx->stream;
-  double* dev = ctx->sh_buf.get();
-  if (q > 0) {
-    CK(cudaMemcpyAsync(ctx->phi.get(), phi, q * sizeof(double), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dev + 2, &r_prev, sizeof(double), cudaMemcpyHostToDevice, st));
+  ctx->rh_tsum.need((c + kScanTileN - 1) / kScanTileN + 3);
+  ctx->sb.Gloc.need((size_t)2 * K * K);
+  ctx->sb.Gg.need((size_t)2 * K * K * world);
+  ensure_events(ctx, p_bar + 1);
+  ensure_span_events(ctx);
+  const bool phases = d && d->phase_seconds;
+  while (phases && ctx->pev.size() < 2 * (size_t)p_bar) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ctx->pev.push_back(e);
   }
-  launch_pass(ctx, q, ctx->sh_w, ctx->phi.get(), dev + 2);
-  const int64_t ntile = (ctx->sh_w + kPassTile - 1) / kPassTile;
-  k_sum_tiles<<<1, 1024, 0, st>>>(ctx->tileA.get(), ctx->tileB.get(), ntile, dev);
-  COUNT_LAUNCH();
-  CK(cudaMemcpyAsync(out, dev, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-}
-
-static int64_t shard_sample(tf_context* ctx, uint64_t seed, double s_total, double offset, double r_glob,
-                            int is_last) {
-  shard_check(ctx);
-  cudaStream_t st = ctx->stream;
-  const int64_t w = ctx->sh_w, c = ctx->sh_c;
-  const int64_t ntile = (w + kPassTile - 1) / kPassTile;
-  double* dev = ctx->sh_buf.get();
-  CK(cudaMemcpyAsync(dev + 3, &r_glob, sizeof(double), cudaMemcpyHostToDevice, st));
-  launch_scan(ctx, ntile, 0, 0, 0, dev + 3);  // local tile prefix, mass with the global R
-  DrawArgs a{};
-  a.seed = seed;
-  a.c = c;
-  a.scal = ctx->scal.get();
-  a.OT = ctx->OT.get();
-  a.guide = ctx->guide.get();
-  a.ntile = ntile;
-  a.tA = ctx->tileA.get();
-  a.tB = ctx->tileB.get();
-  a.chunkA = ctx->chunkA.get();
-  a.chunkB = ctx->chunkB.get();
-  a.s = ctx->s.get();
-  a.r = ctx->r.get();
-  a.w = w;
-  a.idx = ctx->idx.get();
-  a.wts = ctx->wts.get();
-  a.seed_ptr = nullptr;
-  a.shard = 1;
-  a.s_total = s_total;
-  a.offset = offset;
-  a.is_last = is_last;
-  a.accept = ctx->rh_ok.get();
-  const int per = kDrawPerCta;
-  k_draw<<<(unsigned)((c + per - 1) / per), kDrawThreads, 0, st>>>(a);
-  LAUNCH_CHECK("k_draw");
-  COUNT_LAUNCH();
-  // draw-order compaction of the accepted draws (deterministic local order)
-  scan_apply(ctx, ctx->rh_ok.get(), c, CompactDrawF{ctx->idx.get(), ctx->wts.get(), ctx->sh_idx.get(), ctx->sh_wts.get()});
+  ctx->seedtab.need(p_bar + 1);
+  {
+    std::vector<uint64_t> seeds(p_bar + 1);
+    for (int p = 0; p <= p_bar; ++p) seeds[p] = derive_seed(seed, (uint64_t)p);
+    CK(cudaMemcpyAsync(ctx->seedtab.get(), seeds.data(), (p_bar + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  CK(cudaMemsetAsync(ctx->sh_par.get(), 0, 4 * sizeof(double), st));
   const int64_t nt = (c + kScanTileN - 1) / kScanTileN;
-  long long k = 0;
-  CK(cudaMemcpyAsync(&k, ctx->rh_tsum.get() + nt + 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  ctx->sh_k = k;
-  return k;
-}
-
-// local Gram of this shard's sampled rows at lag p for CholeskyQR pass `pass`
-static void shard_gram(tf_context* ctx, int p, int pass, double r_prev, double* G_out) {
-  shard_check(ctx);
-  SolveBufs& b = ctx->sb;
-  cudaStream_t st = ctx->stream;
-  const int K = p + 1;
-  const int64_t k = ctx->sh_k, lq = ldq_of(K);
-  const int64_t tsz = tpu_size(K);
-  if (k == 0) {
-    CK(cudaMemsetAsync(b.G.get(), 0, tsz * sizeof(double), st));
-  } else if (K == 2) {
-    FwdRows ld{ctx->y.get(), ctx->sh_idx.get(), ctx->sh_wts.get(), 0};
-    gram(ctx, ld, k, K, b.G.get(), nullptr);
-  } else if (pass == 0) {
-    FwdRows ld{ctx->y.get(), ctx->sh_idx.get(), ctx->sh_wts.get(), 0};
-    double* dev = ctx->sh_buf.get();
-    CK(cudaMemcpyAsync(dev + 4, &r_prev, sizeof(double), cudaMemcpyHostToDevice, st));
-    const double* Sprev = (p & 1) ? b.S0.get() : b.S1.get();
-    k_precond<<<tpu_grid(K), 256, 0, st>>>(Sprev, ctx->phi.get(), dev + 4, b.T.get(), K);
-    COUNT_LAUNCH();
-    qform(ctx, ld, k, K, b.T.get(), b.Q1.get(), nullptr);
-    gram_dense(ctx, b.Q1.get(), lq, k, K, b.G.get(), nullptr);
-  } else if (pass == 1) {
-    trsm_right<false>(ctx, b.Q1.get(), b.RA.get(), b.Q2.get(), k, K, nullptr);
-    gram_dense(ctx, b.Q2.get(), lq, k, K, b.G.get(), nullptr);
-  } else {
-    trsm_right<false>(ctx, b.Q2.get(), b.RB.get(), b.Q1.get(), k, K, nullptr);
-    gram_dense(ctx, b.Q1.get(), lq, k, K, b.G.get(), nullptr);
-  }
-  CK(cudaMemcpyAsync(G_out, b.G.get(), tsz * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-}
-
-// Cholesky of the reduced Gram (identical on every rank)
-static void shard_factor(tf_context* ctx, int p, int pass, const double* G, int64_t c_total, int flags_out[3]) {
-  shard_check(ctx);
-  SolveBufs& b = ctx->sb;
-  cudaStream_t st = ctx->stream;
-  const int K = p + 1;
-  CK(cudaMemcpyAsync(b.G.get(), G, tpu_size(K) * sizeof(double), cudaMemcpyHostToDevice, st));
-  if (K == 2) {
-    CK(cudaMemsetAsync(b.flags.get(), 0, 4 * sizeof(int), st));
-  } else {
-    double* RD = pass == 0 ? b.RA.get() : pass == 1 ? b.RB.get() : b.RC.get();
-    cholinv(ctx, b.G.get(), K, pass, c_total, RD, nullptr, p, ctx->status.get(), 0, 0);
-  }
-  int fl[4];
-  CK(cudaMemcpyAsync(fl, b.flags.get(), 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  const long long* kdev = ctx->rh_tsum.get() + nt + 1;  // this shard's draw count (scan_apply total)
+  bool capturing = false;
+  auto rec = [&](cudaEvent_t e) {
+    if (capturing) CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else CK(cudaEventRecord(e, st));
+  };
+  auto record = [&]() {
+    rec(ctx->ev_begin);
+    rec(ctx->events[0]);
+    launch_pass(ctx, 0, w, ctx->phi.get(), ctx->sh_par.get());  // r_0 = -y, s_0 = 0
+    for (int p = 1; p <= p_bar; ++p) {
+      const int q = p - 1;
+      k_sum_tiles<<<1, 1024, 0, st>>>(ctx->tileA.get(), ctx->tileB.get(), ntile, ctx->sh_part.get());
+      nccl_check(ncclAllGather(ctx->sh_part.get(), ctx->sh_gath.get(), 2, ncclDouble, ctx->comm, st), "ncclAllGather");
+      k_shard_R<<<1, 1, 0, st>>>(ctx->sh_gath.get(), world, ctx->sh_par.get(), ctx->Rhist.get(), q,
+                                 ctx->status.get());
+      // local CDF with the global R (its total S_local lands in scal[1])
+      k_lag_scan<<<1, kScanThreads, 0, st>>>(ctx->tileA.get(), ctx->tileB.get(), ntile, ctx->OT.get(),
+                                             ctx->scal.get(), nullptr, nullptr, q, 0, ctx->sh_dummy.get(), 0,
+                                             ctx->sh_par.get(), ctx->guide.get());
+      nccl_check(ncclAllGather(ctx->scal.get() + 1, ctx->sh_gath.get() + 2 * world, 1, ncclDouble, ctx->comm, st),
+                 "ncclAllGather");
+      k_shard_seg<<<1, 1, 0, st>>>(ctx->sh_gath.get() + 2 * world, world, rank, ctx->sh_par.get(), ctx->Shist.get(), q,
+                                   ctx->status.get());
+      g_launches += 4;
+      DrawArgs a{};
+      a.seed_ptr = ctx->seedtab.get() + p;
+      a.c = c;
+      a.scal = ctx->scal.get();
+      a.OT = ctx->OT.get();
+      a.guide = ctx->guide.get();
+      a.ntile = ntile;
+      a.tA = ctx->tileA.get();
+      a.tB = ctx->tileB.get();
+      a.chunkA = ctx->chunkA.get();
+      a.chunkB = ctx->chunkB.get();
+      a.s = ctx->s.get();
+      a.r = ctx->r.get();
+      a.w = w;
+      a.idx = ctx->idx.get();
+      a.wts = ctx->wts.get();
+      a.shard = 1;
+      a.par = ctx->sh_par.get();
+      a.accept = ctx->rh_ok.get();
+      k_draw<<<(unsigned)((c + kDrawPerCta - 1) / kDrawPerCta), kDrawThreads, 0, st>>>(a);
+      LAUNCH_CHECK("k_draw (shard)");
+      COUNT_LAUNCH();
+      // this shard's draws in draw order (deterministic local row order)
+      scan_apply(ctx, ctx->rh_ok.get(), c, CompactDrawF{ctx->idx.get(), ctx->wts.get(), ctx->sh_idx.get(),
+                                                        ctx->sh_wts.get()});
+      if (phases) rec(ctx->pev[2 * (p - 1)]);
+      ExactOut o{ctx->phi.get(), ctx->coefs.get(), (int64_t)(p - 1) * p / 2, ctx->taus.get(), ctx->method.get(),
+                 ctx->rank.get(), p, ctx->sweeps.get()};
+      solve_exact(ctx, FwdRows{ctx->y.get(), ctx->sh_idx.get(), ctx->sh_wts.get(), 0}, c, p + 1, /*rev=*/0, o, kdev,
+                  /*sharded=*/true);
+      if (phases) rec(ctx->pev[2 * (p - 1) + 1]);
+      launch_pass(ctx, p, w, ctx->phi.get(), ctx->sh_par.get());  // R_{p-1} = par[0]
+      rec(ctx->events[p]);
+    }
+    rec(ctx->ev_end);
+  };
+  const int mode = 64 | (phases ? 4 : 0);
+  const int64_t launches = run_graphed(ctx, ctx->lsar_graph, w, c, p_bar, mode, capturing, record);
   CK(cudaStreamSynchronize(st));
   int sth[3];
   CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
   raise_from_status(sth);
-  flags_out[0] = fl[0];
-  flags_out[1] = fl[1];
-  flags_out[2] = fl[2];
-}
-
-// phi_p from the factors; the next lag's preconditioner is formed on device
-static void shard_finish(tf_context* ctx, int p, double* phi_out, double* tau_out) {
-  shard_check(ctx);
-  SolveBufs& b = ctx->sb;
-  cudaStream_t st = ctx->stream;
-  const int K = p + 1;
-  int* fl = b.flags.get();
-  double* Snext = (p & 1) ? b.S1.get() : b.S0.get();
-  if (K == 2) {
-    PhiSArgs pa;
-    pa.K = 2;
-    pa.SA = pa.SB = pa.SC = nullptr;
-    pa.flags = fl;
-    pa.phi = ctx->phi.get();
-    pa.coefs = nullptr;
-    pa.coef_off = 0;
-    pa.taus = ctx->taus.get();
-    pa.method = ctx->method.get();
-    pa.lag = 1;
-    pa.S_final = Snext;
-    pa.rev = 0;
-    pa.rest_out = nullptr;
-    k_solve_k2<<<1, 1, 0, st>>>(b.G.get(), pa);
-    COUNT_LAUNCH();
-  } else {
-    const unsigned npair = (unsigned)(((K + 31) / 32) * ((K + 31) / 32 + 1) / 2);
-    k_rinv_first_order<<<npair, 64, 0, st>>>(b.RA.get(), b.RI.get(), K, nullptr);
-    trmm_tpu(ctx, b.T.get(), b.RI.get(), b.SA.get(), Snext, K, nullptr);
-    k_rinv_first_order<<<npair, 64, 0, st>>>(b.RB.get(), b.RI.get(), K, fl + 2);
-    trmm_tpu(ctx, b.SA.get(), b.RI.get(), b.SB.get(), Snext, K, fl + 2);
-    k_rinv_first_order<<<npair, 64, 0, st>>>(b.RC.get(), b.RI.get(), K, fl + 0);
-    trmm_tpu(ctx, b.SB.get(), b.RI.get(), b.SC.get(), Snext, K, fl + 0);
-    g_launches += 3;
-    PhiSolveArgs ps;
-    ps.K = K;
-    ps.T = b.T.get();
-    ps.RA = b.RA.get();
-    ps.RB = b.RB.get();
-    ps.RC = b.RC.get();
-    ps.flags = fl;
-    ps.rev = 0;
-    ps.phi = ctx->phi.get();
-    ps.coefs = nullptr;
-    ps.coef_off = 0;
-    ps.taus = ctx->taus.get();
-    ps.method = ctx->method.get();
-    ps.lag = p;
-    ps.rest_out = nullptr;
-    k_phi_solve<<<1, kPhiThreads, (size_t)(2 * K + 32) * sizeof(double), st>>>(ps);
-    LAUNCH_CHECK("k_phi_solve");
-    COUNT_LAUNCH();
+  std::vector<double> t(p_bar);
+  CK(cudaMemcpy(t.data(), ctx->taus.get(), p_bar * sizeof(double), cudaMemcpyDeviceToHost));
+  if (taus) std::memcpy(taus, t.data(), p_bar * sizeof(double));
+  if (coefs)
+    CK(cudaMemcpy(coefs, ctx->coefs.get(), sizeof(double) * (size_t)p_bar * (p_bar + 1) / 2, cudaMemcpyDeviceToHost));
+  if (lag_seconds)
+    for (int p = 1; p <= p_bar; ++p) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ctx->events[p - 1], ctx->events[p]));
+      lag_seconds[p - 1] = ms * 1e-3;
+    }
+  if (p_star) *p_star = tf_select_order(t.data(), p_bar, 1.96 / std::sqrt((double)c));
+  if (d) {
+    if (d->rnorm2_out) CK(cudaMemcpy(d->rnorm2_out, ctx->Rhist.get() + 1, sizeof(double) * p_bar, cudaMemcpyDeviceToHost));
+    if (d->ssum_out) CK(cudaMemcpy(d->ssum_out, ctx->Shist.get() + 1, sizeof(double) * p_bar, cudaMemcpyDeviceToHost));
+    if (d->method_out) CK(cudaMemcpy(d->method_out, ctx->method.get(), sizeof(int) * p_bar, cudaMemcpyDeviceToHost));
+    if (d->rank_out) CK(cudaMemcpy(d->rank_out, ctx->rank.get(), sizeof(int) * p_bar, cudaMemcpyDeviceToHost));
+    if (d->svd_sweeps_out)
+      CK(cudaMemcpy(d->svd_sweeps_out, ctx->sweeps.get(), sizeof(int) * p_bar, cudaMemcpyDeviceToHost));
+    if (d->launches_out) *d->launches_out = launches;
+    if (phases)
+      for (int p = 1; p <= p_bar; ++p) {
+        float a = 0.f, b = 0.f, cc = 0.f;
+        CK(cudaEventElapsedTime(&a, ctx->events[p - 1], ctx->pev[2 * (p - 1)]));
+        CK(cudaEventElapsedTime(&b, ctx->pev[2 * (p - 1)], ctx->pev[2 * (p - 1) + 1]));
+        CK(cudaEventElapsedTime(&cc, ctx->pev[2 * (p - 1) + 1], ctx->events[p]));
+        d->phase_seconds[3 * (p - 1) + 0] = a * 1e-3;
+        d->phase_seconds[3 * (p - 1) + 1] = b * 1e-3;
+        d->phase_seconds[3 * (p - 1) + 2] = cc * 1e-3;
+      }
   }
-  CK(cudaMemcpyAsync(phi_out, ctx->phi.get(), p * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(tau_out, ctx->taus.get() + (p - 1), sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
 }
 
 // ---------------------------------------------------------------------------
@@ -2395,6 +2400,7 @@ void tf_destroy(tf_context* ctx) {
   if (ctx->ev_end) cudaEventDestroy(ctx->ev_end);
   if (ctx->lsar_graph.exec) cudaGraphExecDestroy(ctx->lsar_graph.exec);
   if (ctx->rh_graph.exec) cudaGraphExecDestroy(ctx->rh_graph.exec);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
   cudaStreamDestroy(ctx->stream);
   delete ctx;  // DBuf destructors free every device buffer
 }
@@ -2549,35 +2555,37 @@ tf_status tf_sweep_span(const tf_context* ref, const tf_context* ctx, double* st
   return TF_OK;
 }
 
-tf_status tf_shard_open(tf_context* ctx, int p_bar, int64_t c, int64_t w_local) {
+tf_status tf_nccl_unique_id(unsigned char* out, int bytes) {
+  if (!out || bytes < (int)sizeof(ncclUniqueId)) return TF_USAGE;
+  ncclUniqueId uid;
+  if (ncclGetUniqueId(&uid) != ncclSuccess) return TF_NCCL;
+  std::memcpy(out, &uid, sizeof uid);
+  return TF_OK;
+}
+
+tf_status tf_nccl_init(tf_context* ctx, const unsigned char* id, int world, int rank) {
+  if (!ctx || !id) return TF_USAGE;
+  return guarded(ctx, [&] {
+    cudaSetDevice(ctx->device);
+    tfe::nccl_init(ctx, id, world, rank);
+  });
+}
+
+tf_status tf_keep_slice(tf_context* ctx, int64_t start, int64_t len) {
   if (!ctx) return TF_USAGE;
-  return guarded(ctx, [&] { tfe::shard_open(ctx, p_bar, c, w_local); });
+  return guarded(ctx, [&] {
+    cudaSetDevice(ctx->device);
+    tfe::keep_slice(ctx, start, len);
+  });
 }
 
-tf_status tf_shard_pass(tf_context* ctx, int q, const double* phi, double r_prev, double* out2) {
-  if (!ctx || !out2 || (q > 0 && !phi)) return TF_USAGE;
-  return guarded(ctx, [&] { tfe::shard_pass(ctx, q, phi, r_prev, out2); });
-}
-
-tf_status tf_shard_sample(tf_context* ctx, uint64_t seed_p, double s_total, double offset, double r_glob,
-                          int is_last, int64_t* k_out) {
-  if (!ctx || !k_out) return TF_USAGE;
-  return guarded(ctx, [&] { *k_out = tfe::shard_sample(ctx, seed_p, s_total, offset, r_glob, is_last); });
-}
-
-tf_status tf_shard_gram(tf_context* ctx, int p, int pass, double r_prev, double* G_out) {
-  if (!ctx || !G_out) return TF_USAGE;
-  return guarded(ctx, [&] { tfe::shard_gram(ctx, p, pass, r_prev, G_out); });
-}
-
-tf_status tf_shard_factor(tf_context* ctx, int p, int pass, const double* G, int64_t c_total, int* flags3) {
-  if (!ctx || !G || !flags3) return TF_USAGE;
-  return guarded(ctx, [&] { tfe::shard_factor(ctx, p, pass, G, c_total, flags3); });
-}
-
-tf_status tf_shard_finish(tf_context* ctx, int p, double* phi_out, double* tau_out) {
-  if (!ctx || !phi_out || !tau_out) return TF_USAGE;
-  return guarded(ctx, [&] { tfe::shard_finish(ctx, p, phi_out, tau_out); });
+tf_status tf_lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, const tf_lsar_diag* diag,
+                                double* taus, double* coefs_packed, double* lag_seconds, int* p_star) {
+  if (!ctx) return TF_USAGE;
+  return guarded(ctx, [&] {
+    cudaSetDevice(ctx->device);
+    tfe::lsar_sweep_sharded(ctx, p_bar, c, seed, diag, taus, coefs_packed, lag_seconds, p_star);
+  });
 }
 
 int64_t tf_tpu_size(int K) { return K < 1 ? 0 : tfk::tpu_size(K); }

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <cstdint>
 #include <string>
@@ -44,6 +45,7 @@ struct SolveBufs {
   // rank-revealing solve (k_exact.cuh): double-double Gram partials and
   // planes, pivoted factor, SVD matrix / singular values / partial solutions
   DBuf<double> Wdd, Gh, Gl, Rh, Rl, Dd, Nsv, sig, xpart, tolv;
+  DBuf<double> Gloc, Gg;  // row-sharded sweeps: this shard's Gram partial [2][K*K], the allgathered partials
   DBuf<int> perm, svdf;
 };
 
@@ -74,11 +76,14 @@ struct tf_context {
   tfe::DBuf<int64_t> rh_lvl, rh_aidx, rh_sidx, rh_fup;
   tfe::DBuf<double> rh_scores, rh_aw, rh_sw, rh_fupw, rh_ones, rh_norm, rh_Gp, rh_H0, rh_W, rh_S,
       rh_phis, rh_rest, rh_part;
-  // row-sharded LSAR session (tf_shard_*)
-  int sh_pbar = 0;
-  int64_t sh_c = 0, sh_w = 0, sh_k = 0;
-  tfe::DBuf<double> sh_buf, sh_wts;
+  // row-sharded LSAR sweep (tf_lsar_sweep_sharded): NCCL communicator, the
+  // allgathered shard sums, this shard's CDF segment, its compacted draws
+  ncclComm_t comm = nullptr;
+  int nc_world = 1, nc_rank = 0;
+  tfe::DBuf<double> sh_part, sh_gath, sh_par, sh_wts;
   tfe::DBuf<int64_t> sh_idx;
+  tfe::DBuf<int> sh_dummy;
+  tfe::DBuf<double> scratch;  // blocked Cholesky (cholinv_big) trace scratch
   // batched LSAR sweeps of equal-shape series (tf_lsar_sweep_batch)
   tfe::DBuf<double> bt_y, bt_s, bt_r, bt_cA, bt_cB, bt_tA, bt_tB, bt_OT, bt_scal, bt_Rh, bt_Sh, bt_phi,
       bt_coefs, bt_taus, bt_wts, bt_S0, bt_S1, bt_fw;

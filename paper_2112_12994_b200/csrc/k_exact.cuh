@@ -142,12 +142,12 @@ inline GramDDPlan gram_dd_plan(int64_t rows, int K, int sm_count) {
 // reads).  W[(pair * nsplit + split) * 8192 + {0, 4096} + e] = (hi, lo).
 template <class L>
 __global__ void __launch_bounds__(kDDThreads) k_gram_dd(L ld, int64_t rows, int K, int nblk, int64_t rps, int nsplit,
-                                                        double* __restrict__ W, const int* gate) {
-  if (gate && *gate == 0) return;
+                                                        double* __restrict__ W, const long long* rows_dev) {
   __shared__ double As[kDDSlab][64], Bs[kDDSlab][64];
   int I, J;
   pair_from_index(blockIdx.x, nblk, I, J);
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  if (rows_dev) rows = min(rows, (int64_t)*rows_dev);  // a shard's draw count (row-sharded sweeps)
   const int64_t r0 = (int64_t)blockIdx.y * rps, r1 = min(rows, r0 + rps);
   double h[4][4], l[4][4];
 #pragma unroll
@@ -206,6 +206,19 @@ __global__ void __launch_bounds__(kDDThreads) k_gram_dd(L ld, int64_t rows, int 
       out[e] = h[i][j];
       out[4096 + e] = l[i][j];
     }
+}
+
+// Row-sharded sweeps: the allgathered double-double Gram partials of every
+// shard ([world][2][K*K]: hi plane, lo plane) summed in rank order -- exact to
+// double-double and identical on every rank (an fp64 allreduce would round).
+__global__ void k_dd_sum_ranks(const double* __restrict__ gg, int world, int64_t KK, double* __restrict__ Gh,
+                               double* __restrict__ Gl) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= KK) return;
+  DD s{0.0, 0.0};
+  for (int r = 0; r < world; ++r) s = dd_add(s, DD{gg[(int64_t)r * 2 * KK + e], gg[(int64_t)r * 2 * KK + KK + e]});
+  Gh[e] = s.h;
+  Gl[e] = s.l;
 }
 
 // split partials summed in split order (deterministic) -> full symmetric

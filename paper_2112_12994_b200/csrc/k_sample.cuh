@@ -166,12 +166,13 @@ struct DrawArgs {
   int64_t w;
   int64_t* idx;
   double* wts;
-  // row-sharded mode: this shard holds the global CDF segment
-  // [offset, offset + S); draws outside it are skipped (accept[t] = 0)
+  // row-sharded mode: par = (R, S_total, lo, hi) on the device
+  // (k_shard_scal); draw t belongs to this shard iff lo <= u_t S_total < hi
+  // (the shards' prefix masses in rank order, identical on every rank: each
+  // draw lands in exactly one shard) and is resolved at v = u_t S_total - lo
+  // in the local CDF; accept[t] records it
   int shard;
-  double s_total;
-  double offset;
-  int is_last;
+  const double* par;
   int* accept;
   // batched sweeps: series b = blockIdx.y at base + b * stride
   int64_t bs_w, bs_chunk, bs_tile, bs_seed;
@@ -266,12 +267,13 @@ __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
   const double R = a.scal[0], S = a.scal[1];
   const double invR = 1.0 / R;
   const uint64_t seed = a.seed_ptr ? *a.seed_ptr : a.seed;
-  double v = rng_uniform01(seed, (uint64_t)t) * (a.shard ? a.s_total : S);
+  const double Sw = a.shard ? a.par[1] : S;  // the weights' normaliser: the global score sum
+  double v = rng_uniform01(seed, (uint64_t)t) * Sw;
   if (a.shard) {
-    v -= a.offset;
-    const bool mine = v >= 0.0 && (v < S || a.is_last);
+    const bool mine = v >= a.par[2] && v < a.par[3];
     if (g.sl == 0) a.accept[t] = mine ? 1 : 0;
     if (!mine) return;
+    v -= a.par[2];
   }
   // ---- tile: largest T with OT[T] <= v (the guide table brackets it) ----
   int64_t lo = 0, hi = a.ntile;
@@ -361,8 +363,41 @@ __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
   mp = g.bcast(mp, pick / RPL);
   if (g.sl == 0) {
     a.idx[t] = r0 + pick;
-    a.wts[t] = 1.0 / sqrt((double)a.c * (mp / (a.shard ? a.s_total : S)));
+    a.wts[t] = 1.0 / sqrt((double)a.c * (mp / Sw));
   }
+}
+
+// Row-sharded lag step, part 1: the allgathered (sum s, sum r^2) of every
+// shard -> the global R = ||r||^2 (lsar.cpp:17-25), summed in rank order (the
+// same arithmetic on every rank).
+__global__ void k_shard_R(const double* __restrict__ gath, int world, double* __restrict__ par, double* Rhist,
+                          int lag, int* status) {
+  double R = 0.0;
+  for (int r = 0; r < world; ++r) R += gath[2 * r + 1];
+  par[0] = R;
+  if (Rhist) Rhist[lag] = R;
+  if (R == 0.0) raise_status(status, kErrNumerical, lag + 1, lag == 0 ? kReasonZeroWindow : kReasonZeroResidual);
+}
+
+// part 2: the allgathered local CDF totals (each shard's k_lag_scan total with
+// the global R) -> the global total S and this shard's segment [lo, hi) of
+// the global CDF (prefix in rank order, the last shard's segment open).  Each
+// shard resolves its draws against exactly the CDF it built, and one shard
+// reproduces the single-GPU sweep bit for bit.
+__global__ void k_shard_seg(const double* __restrict__ gS, int world, int rank, double* __restrict__ par,
+                            double* Shist, int lag, int* status) {
+  double S = 0.0, lo = 0.0, hi = 0.0;
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) lo = S;
+    S += gS[r];
+    if (r == rank) hi = S;
+  }
+  if (rank == world - 1) hi = __longlong_as_double(0x7ff0000000000000ll);
+  par[1] = S;
+  par[2] = lo;
+  par[3] = hi;
+  if (Shist) Shist[lag + 1] = S;
+  if (!(S > 0.0)) raise_status(status, kErrNumerical, lag + 1, kReasonZeroScoreSum);
 }
 
 // Deterministic-index mode with reference indices only: the weight of every

@@ -1,28 +1,35 @@
-"""Row-sharded LSAR sweep: one process per GPU.
+"""Row-sharded LSAR sweep of one long series: one process per GPU.
 
 Rows of the LSAR window (w = n - p_bar, lsar.cpp:63) are split into
-contiguous blocks; rank g owns rows [row0_g, row0_g + w_g) and holds the
-series slice y[row0_g .. row0_g + w_g + p_bar) (a p_bar-sample halo).  Per lag
-p the only cross-rank traffic is
+contiguous balanced blocks; rank g owns rows [row0_g, row0_g + w_g) and holds
+the series slice y[row0_g .. row0_g + w_g + p_bar) (a p_bar-sample halo).  Per
+lag p the only cross-rank traffic is
 
   * an allgather of each shard's (sum s_{p-1}, sum r_{p-1}^2)  ->  the global
-    R_{p-1} = ||r_{p-1}||^2 (lsar.cpp:17-25), every shard's CDF mass and its
-    offset (exclusive prefix in rank order);
-  * for every CholeskyQR pass, an allreduce (sum) of the K x K Gram of the
-    locally resolved sampled rows; every rank then factors the same matrix,
-    so phi_p, the pass gates and the next preconditioner agree everywhere.
+    R_{p-1} = ||r_{p-1}||^2 (lsar.cpp:17-25);
+  * an allgather of each shard's local CDF total (built with the global R)
+    -> the global total and this shard's segment [lo, hi) (prefix in rank
+    order);
+  * an allgather of the shards' double-double Gram partials of their sampled
+    rows, summed in rank order, so every rank runs the same rank-revealing
+    solve (toeplitz.cpp:57-85) and holds the same phi_p.
 
 Sampling (sketch.cpp:20-59) stays the reference's: every rank evaluates the
-same counter-RNG uniforms u_t and resolves only the draws whose global CDF
-position u_t * S falls in its segment, keeping them in draw order.
+same counter-RNG uniforms u_t and resolves only the draws with
+lo <= u_t S < hi (compared against the prefix values themselves, so each draw
+lands in exactly one shard), keeping them in draw order.
 
-The orchestration below is backend-agnostic: `GpuShard` drives the CUDA
-kernels through the C ABI (tf_shard_*), and the CPU tests drive the same
-loop with a numpy stand-in over gloo (tests/test_shard.py).
+`NcclShard` is the product path: the lag loop runs inside libtoepfit_b200.so
+(tf_lsar_sweep_sharded) with NCCL on the context stream; torch.distributed
+only carries the NCCL unique id.  `lsar_fit_sharded` restates the same
+protocol in Python over any `comm` (gloo on CPU in tests/test_shard.py, with
+the numpy stand-in of tests/shard_numpy.py for the per-shard steps): it is
+the executable specification the CUDA orchestration follows.
 """
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -42,6 +49,29 @@ def shard_rows(w: int, world: int, rank: int) -> tuple[int, int]:
     return row0, base + (1 if rank < extra else 0)
 
 
+def global_R(ab: np.ndarray) -> float:
+    """k_shard_R: the global ||r||^2 from the allgathered (sum s, sum r^2), rank order."""
+    R = 0.0
+    for r in range(ab.shape[0]):
+        R += float(ab[r, 1])
+    return R
+
+
+def segment(s_loc: np.ndarray, rank: int) -> tuple[float, float, float]:
+    """k_shard_seg: (S, lo, hi) from the allgathered local CDF totals, rank
+    order: the global total and this shard's segment [lo, hi) (last: open)."""
+    S = lo = hi = 0.0
+    for r in range(s_loc.shape[0]):
+        if r == rank:
+            lo = S
+        S += float(s_loc[r])
+        if r == rank:
+            hi = S
+    if rank == s_loc.shape[0] - 1:
+        hi = float("inf")
+    return S, lo, hi
+
+
 class LocalComm:
     """world size 1 (no communication)."""
     rank, world = 0, 1
@@ -49,12 +79,9 @@ class LocalComm:
     def allgather(self, x: np.ndarray) -> np.ndarray:
         return np.asarray(x, dtype=np.float64)[None, :]
 
-    def allreduce_sum(self, x: np.ndarray) -> np.ndarray:
-        return np.asarray(x, dtype=np.float64)
-
 
 class TorchComm:
-    """torch.distributed collectives (gloo on CPU, nccl on GPU tensors)."""
+    """torch.distributed collectives (gloo on CPU) for the protocol model."""
 
     def __init__(self, group=None, device=None):
         import torch
@@ -72,58 +99,51 @@ class TorchComm:
         self._dist.all_gather(out, t, group=self._group)
         return np.stack([o.cpu().numpy() for o in out])
 
-    def allreduce_sum(self, x: np.ndarray) -> np.ndarray:
-        t = self._torch.as_tensor(np.asarray(x, dtype=np.float64), device=self._dev).clone()
-        self._dist.all_reduce(t, op=self._dist.ReduceOp.SUM, group=self._group)
-        return t.cpu().numpy()
 
+class NcclShard:
+    """This rank's part of a row-sharded sweep on its GPU (product path)."""
 
-class GpuShard:
-    """Per-rank device state through tf_shard_* (csrc/engine.cu)."""
+    def __init__(self, engine: Engine, dist, world: int, rank: int, n: int, p_bar: int):
+        import torch
+        self.eng, self.world, self.rank, self.n, self.p_bar = engine, world, rank, int(n), int(p_bar)
+        self.row0, self.w_local = shard_rows(self.n - self.p_bar, world, rank)
+        L = _abi.lib()
+        buf = C.create_string_buffer(128)
+        if rank == 0:
+            engine._check(L.tf_nccl_unique_id(buf, 128))
+        t = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).to(torch.device("cuda", torch.cuda.current_device()))
+        dist.broadcast(t, 0)
+        uid = bytes(t.cpu().numpy().tobytes())
+        engine._check(L.tf_nccl_init(engine._ctx, uid, world, rank))
 
-    def __init__(self, engine: Engine | None = None, device: int = 0):
-        self.eng = engine or Engine(device)
-        self._L = _abi.lib()
+    def generate(self, roots, seed: int, innovations: str = "normal"):
+        """The whole series generated on the device (identical on every rank), then cut to this slice."""
+        self.eng.generate_series(roots, self.n, seed, innovations)
+        self.eng._check(_abi.lib().tf_keep_slice(self.eng._ctx, self.row0, self.w_local + self.p_bar))
+        self.eng._series_id = ("slice", self.row0)
 
-    def _ok(self, st):
-        self.eng._check(st)
-
-    def open(self, y_slice, p_bar: int, c: int, w_local: int):
-        y = np.ascontiguousarray(y_slice, dtype=np.float64)
-        self._ok(self._L.tf_upload_series(self.eng._ctx, ptr(y), y.size))
+    def upload_host(self, y):
+        v = np.ascontiguousarray(np.asarray(y, dtype=np.float64)[self.row0:self.row0 + self.w_local + self.p_bar])
+        self.eng._check(_abi.lib().tf_upload_series(self.eng._ctx, ptr(v), v.size))
         self.eng._series_id = None
-        self._ok(self._L.tf_shard_open(self.eng._ctx, int(p_bar), int(c), int(w_local)))
 
-    def pass_(self, q: int, phi, r_prev: float):
-        out = np.zeros(2)
-        ph = None if q == 0 else np.ascontiguousarray(phi, dtype=np.float64)
-        self._ok(self._L.tf_shard_pass(self.eng._ctx, int(q), ptr(ph) if ph is not None else None,
-                                       float(r_prev), ptr(out)))
-        return float(out[0]), float(out[1])
+    def lsar_sweep(self, c: int, seed: int, want_diag=False):
+        return self.eng.lsar_sweep(self.p_bar, c, seed, want_diag=want_diag, n=self.w_local + self.p_bar,
+                                   sharded=True)
 
-    def sample(self, seed_p: int, s_total: float, offset: float, r_glob: float, is_last: bool) -> int:
-        k = C.c_int64(0)
-        self._ok(self._L.tf_shard_sample(self.eng._ctx, C.c_uint64(seed_p), float(s_total), float(offset),
-                                         float(r_glob), int(is_last), C.byref(k)))
-        return int(k.value)
-
-    def gram(self, p: int, pass_: int, r_prev: float) -> np.ndarray:
-        g = np.zeros(int(self._L.tf_tpu_size(p + 1)))
-        self._ok(self._L.tf_shard_gram(self.eng._ctx, int(p), int(pass_), float(r_prev), ptr(g)))
-        return g
-
-    def factor(self, p: int, pass_: int, G: np.ndarray, c_total: int):
-        fl = np.zeros(3, np.int32)
-        g = np.ascontiguousarray(G, dtype=np.float64)
-        self._ok(self._L.tf_shard_factor(self.eng._ctx, int(p), int(pass_), ptr(g), int(c_total),
-                                         ptr(fl, _abi._i32p)))
-        return [int(v) for v in fl]
-
-    def finish(self, p: int):
-        phi = np.zeros(p)
-        tau = np.zeros(1)
-        self._ok(self._L.tf_shard_finish(self.eng._ctx, int(p), ptr(phi), ptr(tau)))
-        return phi, float(tau[0])
+    def e2e_step(self, c: int, seed: int) -> float:
+        """Wall time of one end-to-end sharded fit: H2D of this rank's slice from
+        pinned host memory, the sweep, D2H of the fit."""
+        import torch
+        m = self.w_local + self.p_bar
+        pinned = torch.empty(m, dtype=torch.float64, pin_memory=True).numpy()
+        self.eng.download_series_into(pinned)
+        torch.cuda.synchronize()
+        t0 = time.time()
+        self.eng._check(_abi.lib().tf_upload_series(self.eng._ctx, ptr(pinned), m))
+        self.lsar_sweep(c, seed)
+        torch.cuda.synchronize()
+        return time.time() - t0
 
 
 @dataclass
@@ -137,10 +157,12 @@ class ShardFit:
 
 
 def lsar_fit_sharded(y, p_bar: int, c: int, seed: int, comm=None, backend=None) -> ShardFit:
-    """lsar.cpp:100-124 over row-sharded shards (every rank passes the full
-    series y -- or at least its slice -- and gets the same result)."""
+    """The sharded protocol (lsar.cpp:100-124 over row blocks) in Python over
+    `comm`, with `backend` doing the per-shard steps (tests: numpy stand-in).
+    tf_lsar_sweep_sharded runs the same steps on the device."""
     comm = comm or LocalComm()
-    backend = backend or GpuShard()
+    if backend is None:
+        raise UsageError("the protocol model needs a per-shard backend (the GPU path is NcclShard)")
     y = np.asarray(y, dtype=np.float64)
     n = y.size
     if p_bar < 1:
@@ -158,26 +180,19 @@ def lsar_fit_sharded(y, p_bar: int, c: int, seed: int, comm=None, backend=None) 
     draws = []
     off_c = 0
     for p in range(1, p_bar + 1):
-        ab = comm.allgather(np.array([a, b]))
-        R = float(np.sum(ab[:, 1]))  # rank order: fixed
+        R = global_R(comm.allgather(np.array([a, b])))
         if not R > 0.0:
             raise NumericalError("all-zero window; leverage undefined (lag 1)" if p == 1 else
                                  f"zero residual norm; sampling distribution undefined (lag {p})")
-        mass = ab[:, 0] + ab[:, 1] / R
-        S = float(np.sum(mass))
-        offset = float(np.sum(mass[:comm.rank]))
-        k = backend.sample(derive_seed(seed, p), S, offset, R, comm.rank == comm.world - 1)
+        S, lo, hi = segment(comm.allgather(np.array([backend.local_total(R)]))[:, 0], comm.rank)
+        k = backend.sample(derive_seed(seed, p), R, S, lo, hi)
         draws.append(k)
-        G = comm.allreduce_sum(backend.gram(p, 0, R))
-        fl = backend.factor(p, 0, G, c)
-        if p >= 2 and fl[2]:
-            G = comm.allreduce_sum(backend.gram(p, 1, R))
-            backend.factor(p, 1, G, c)
-        if p >= 2 and fl[0]:
-            G = comm.allreduce_sum(backend.gram(p, 2, R))
-            backend.factor(p, 2, G, c)
-        phi, tau = backend.finish(p)
-        taus[p - 1] = tau
+        parts = comm.allgather(backend.gram(p))  # this shard's Gram partial
+        G = np.zeros_like(parts[0])
+        for r in range(parts.shape[0]):  # rank order
+            G = G + parts[r]
+        phi = backend.solve(p, G)
+        taus[p - 1] = phi[p - 1]
         coefs[off_c:off_c + p] = phi
         off_c += p
         a, b = backend.pass_(p, phi, R)

@@ -1,5 +1,5 @@
 """CPU stand-in for the per-shard device steps (test infrastructure only):
-the same six operations as paper_2112_12994_b200.shard.GpuShard, in numpy,
+the per-shard steps of the protocol (paper_2112_12994_b200/shard.py), in numpy,
 so the sharded orchestration (collectives, offsets, draw ownership, pass
 gating) is exercised over gloo without a GPU.  Plain normal-equation solve
 of the sampled system; the counter RNG is the reference's (rng.hpp:23-35)."""
@@ -35,15 +35,18 @@ class NumpyShard:
         self.r = rn
         return float(self.s.sum()), float((rn ** 2).sum())
 
-    def sample(self, seed_p, s_total, offset, r_glob, is_last):
+    def local_total(self, r_glob):
+        return float(np.sum(self.s + self.r ** 2 / r_glob))
+
+    def sample(self, seed_p, r_glob, s_total, lo, hi):
         mass = self.s + self.r ** 2 / r_glob
         cum = np.cumsum(mass)
-        m_loc = cum[-1]
         idx, wt = [], []
         for t in range(self.c):
-            v = uniform(seed_p, t) * s_total - offset
-            if v < 0 or (v >= m_loc and not is_last):
+            x = uniform(seed_p, t) * s_total
+            if not (lo <= x < hi):
                 continue
+            v = x - lo
             i = min(int(np.searchsorted(cum, v, side="right")), self.w - 1)
             while mass[i] <= 0 and i > 0:
                 i -= 1
@@ -52,20 +55,15 @@ class NumpyShard:
         self.idx, self.wt = np.array(idx, np.int64), np.array(wt)
         return len(idx)
 
-    def gram(self, p, pass_, r_prev):
+    def gram(self, p):
         K = p + 1
         if self.idx.size == 0:
             return np.zeros(K * K)
         A = self.wt[:, None] * np.stack([self.y[self.idx + a] for a in range(K)], 1)
         return (A.T @ A).ravel()
 
-    def factor(self, p, pass_, G, c_total):
+    def solve(self, p, G):
         K = p + 1
-        self.G = np.asarray(G).reshape(K, K)
-        return [0, 0, 0]
-
-    def finish(self, p):
-        G = self.G
+        G = np.asarray(G).reshape(K, K)
         phi_fwd = np.linalg.solve(G[:p, :p], G[:p, p])  # forward order, target last
-        phi = phi_fwd[::-1].copy()
-        return phi, float(phi[p - 1])
+        return phi_fwd[::-1].copy()

@@ -1,7 +1,10 @@
-"""Row-sharded LSAR orchestration (paper_2112_12994_b200/shard.py): world
-size 2 over gloo on CPU (numpy stand-in for the device steps) must resolve
-exactly the single-shard draws and give the same fit; on a GPU, world size 1
-through tf_shard_* must match tf_lsar_sweep."""
+"""Row-sharded LSAR sweep.  CPU: the protocol of
+paper_2112_12994_b200/shard.py (the steps tf_lsar_sweep_sharded runs on the
+device) at world size 2 over gloo with a numpy stand-in for the per-shard
+steps must resolve exactly the single-shard draws and give the same fit, and
+the CDF segments must partition the draws.  GPU: the in-library NCCL path
+(tf_nccl_init + tf_lsar_sweep_sharded) at world size 1 reproduces
+tf_lsar_sweep bit for bit (only one GPU is available to this build)."""
 import os
 import socket
 
@@ -80,39 +83,70 @@ def test_sharded_numpy_matches_oracle_fixed_draws():
     assert fit.p_star == ref.p_star
 
 
+def test_segments_partition_the_draws():
+    # k_shard_seg: each u S lands in exactly one shard's [lo, hi)
+    from paper_2112_12994_b200.shard import segment
+    rng = np.random.default_rng(5)
+    for world in (2, 3, 8):
+        s_loc = rng.exponential(size=world) * 10 ** rng.uniform(-3, 3, size=world)
+        segs = [segment(s_loc, r) for r in range(world)]
+        S = segs[0][0]
+        assert all(sg[0] == S for sg in segs)
+        u = np.concatenate([rng.random(20000), [0.0, 1.0 - 2 ** -53]])
+        x = u * S
+        owners = np.zeros(x.size, int)
+        for _, lo, hi in segs:
+            owners += (x >= lo) & (x < hi)
+        assert (owners == 1).all()
+
+
+def _nccl_world1():
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    return dist
+
+
 @pytest.mark.gpu
-def test_sharded_gpu_world1_matches_sweep():
+def test_sharded_nccl_world1_matches_sweep_bitwise():
     import paper_2112_12994_b200 as tf
     from paper_2112_12994_b200 import shard
     y = _series(40000, 6)
     p_bar, c, seed = 24, 2000, 5
-    eng = tf.Engine(0)
-    ref = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, seed, engine=eng)
-    fit = shard.lsar_fit_sharded(y, p_bar, c, seed, backend=shard.GpuShard(engine=eng))
-    rel = np.max(np.abs(fit.taus - np.array(ref.pacf.taus)) / np.maximum(np.abs(ref.pacf.taus), 1e-3))
-    assert rel < 1e-9
-    assert fit.p_star == ref.p_star
-    assert fit.local_draws == [c] * p_bar
-    eng.close()
+    ref = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, seed, engine=tf.Engine(0), want_diag=True)
+    dist = _nccl_world1()
+    try:
+        eng = tf.Engine(0)
+        sh = shard.NcclShard(eng, dist, 1, 0, y.size, p_bar)
+        sh.upload_host(y)
+        taus, coefs, secs, pstar, d = sh.lsar_sweep(c, seed, want_diag="light")
+        taus2, *_ = sh.lsar_sweep(c, seed)  # second call: the captured graph
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(taus, np.array(ref.pacf.taus)) and np.array_equal(taus2, taus)
+    assert pstar == ref.p_star
+    assert np.array_equal(d["method"], ref.diag["method"])
 
 
 @pytest.mark.gpu
-def test_sharded_gpu_nccl_world1_matches_sweep():
-    # the NCCL collective path (TorchComm on device tensors) end to end; only
-    # one GPU is available to this build, so world size 1
-    import torch.distributed as dist
+def test_sharded_nccl_world1_generated_slice():
+    # the device generator + tf_keep_slice path (what bench.py --gpus N runs)
     import paper_2112_12994_b200 as tf
-    from paper_2112_12994_b200 import shard
-    y = _series(30000, 8)
-    p_bar, c, seed = 16, 1500, 3
-    eng = tf.Engine(0)
-    ref = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, seed, engine=eng)
-    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1)
+    from paper_2112_12994_b200 import gen, shard
+    roots = gen.ar_roots(6, 1.2, 3.0, 77)
+    n, p_bar, c, seed = 120000, 12, 3000, 9
+    e1 = tf.Engine(0)
+    e1.generate_series(roots, n, 77)
+    taus_ref, _, _, ps_ref, _ = e1.lsar_sweep(p_bar, c, seed, n=n)
+    dist = _nccl_world1()
     try:
-        comm = shard.TorchComm()
-        fit = shard.lsar_fit_sharded(y, p_bar, c, seed, comm=comm, backend=shard.GpuShard(engine=eng))
+        e2 = tf.Engine(0)
+        sh = shard.NcclShard(e2, dist, 1, 0, n, p_bar)
+        sh.generate(roots, 77)
+        taus, _, _, ps, _ = sh.lsar_sweep(c, seed)
+        t_e2e = sh.e2e_step(c, seed)
     finally:
         dist.destroy_process_group()
-    rel = np.max(np.abs(fit.taus - np.array(ref.pacf.taus)) / np.maximum(np.abs(ref.pacf.taus), 1e-3))
-    assert rel < 1e-9 and fit.p_star == ref.p_star
-    eng.close()
+    assert np.array_equal(taus, taus_ref) and ps == ps_ref and t_e2e > 0
