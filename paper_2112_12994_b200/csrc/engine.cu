@@ -480,6 +480,8 @@ static void reserve_exact(tf_context* ctx, int64_t c, int Kmax) {
   b.xpart.need((size_t)2 * kSvdMaxCta * Kmax);
   b.tolv.need(2);
   b.Dd.need((size_t)4 * Kmax);
+  b.cn.need(Kmax);
+  b.cnp.need((size_t)((c + kCnRows - 1) / kCnRows) * Kmax);
   b.perm.need(Kmax);
   b.svdf.need(2 + kSvdMaxSweeps + 8);
 }
@@ -495,8 +497,15 @@ static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev,
   const int p = K - 1;
   if (p > kExactMaxP) throw TfError{TF_USAGE, "lag order above " + std::to_string(kExactMaxP) + " (rank-revealing solve)"};
   const GramDDPlan g = gram_dd_plan(c, K, ctx->sm_count);
+  {  // column sums of squares: the accumulation bias of each Gram element
+    const unsigned ns = (unsigned)((c + kCnRows - 1) / kCnRows);
+    k_colnorm2_part<L><<<dim3((unsigned)((K + 63) / 64), ns), 256, 0, st>>>(ld, c, K, rows_dev, b.cnp.get());
+    k_colnorm2_sum<<<(unsigned)((K + 127) / 128), 128, 0, st>>>(b.cnp.get(), (int)ns, K, b.cn.get());
+    LAUNCH_CHECK("k_colnorm2");
+    g_launches += 2;
+  }
   k_gram_dd<L><<<dim3((unsigned)g.npair, (unsigned)g.nsplit), kDDThreads, 0, st>>>(ld, c, K, g.nblk, g.rps, g.nsplit,
-                                                                                  b.Wdd.get(), rows_dev);
+                                                                                  b.Wdd.get(), rows_dev, b.cn.get());
   LAUNCH_CHECK("k_gram_dd");
   const int64_t KK = (int64_t)K * K;
   double* gh = sharded ? b.Gloc.get() : b.Gh.get();

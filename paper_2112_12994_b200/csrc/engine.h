@@ -44,7 +44,7 @@ struct SolveBufs {
   DBuf<int> flags;
   // rank-revealing solve (k_exact.cuh): double-double Gram partials and
   // planes, pivoted factor, SVD matrix / singular values / partial solutions
-  DBuf<double> Wdd, Gh, Gl, Rh, Rl, Dd, Nsv, sig, xpart, tolv;
+  DBuf<double> Wdd, Gh, Gl, Rh, Rl, Dd, Nsv, sig, xpart, tolv, cn, cnp;
   DBuf<double> Gloc, Gg;  // row-sharded sweeps: this shard's Gram partial [2][K*K], the allgathered partials
   DBuf<int> perm, svdf;
 };

@@ -126,8 +126,9 @@ inline GramDDPlan gram_dd_plan(int64_t rows, int K, int sm_count) {
   GramDDPlan g;
   g.nblk = (K + 63) / 64;
   g.npair = g.nblk * (g.nblk + 1) / 2;
-  const int64_t target = 3LL * sm_count;
-  int64_t ns = (target + g.npair - 1) / g.npair;
+  // one wave: 2 resident CTAs per SM (128 registers) -> at most 2 * SMs CTAs
+  const int64_t target = 2LL * sm_count;
+  int64_t ns = std::max<int64_t>(1, target / g.npair);
   ns = std::max<int64_t>(1, std::min<int64_t>(ns, (rows + 4 * kDDSlab - 1) / (4 * kDDSlab)));
   int64_t rps = (rows + ns - 1) / ns;
   rps = (rps + kDDSlab - 1) / kDDSlab * kDDSlab;
@@ -137,12 +138,53 @@ inline GramDDPlan gram_dd_plan(int64_t rows, int K, int sm_count) {
   return g;
 }
 
+// Column sums of squares n_j = sum_t a_tj^2 of the gathered rows (fp64; only
+// a bound for the Gram's accumulation bias below): partials per (row split,
+// 64-column tile), then a fixed-order sum over the splits.
+constexpr int kCnRows = 2048;
+template <class L>
+__global__ void __launch_bounds__(256) k_colnorm2_part(L ld, int64_t rows, int K, const long long* rows_dev,
+                                                       double* __restrict__ part) {
+  if (rows_dev) rows = min(rows, (int64_t)*rows_dev);
+  __shared__ double red[4][64];
+  const int tid = threadIdx.x, col = 64 * blockIdx.x + (tid & 63), rg = tid >> 6;
+  const int64_t r0 = (int64_t)blockIdx.y * kCnRows, r1 = min(rows, r0 + kCnRows);
+  double s = 0.0;
+  if (col < K)
+    for (int64_t t = r0 + rg; t < r1; t += 4) {
+      const double v = ld(t, col);
+      s = fma(v, v, s);
+    }
+  red[rg][tid & 63] = s;
+  __syncthreads();
+  if (tid < 64 && col < K) part[(int64_t)blockIdx.y * K + col] = (red[0][tid] + red[1][tid]) + (red[2][tid] + red[3][tid]);
+}
+__global__ void k_colnorm2_sum(const double* __restrict__ part, int nsplit, int K, double* __restrict__ cn) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= K) return;
+  double s = 0.0;
+  for (int sp = 0; sp < nsplit; ++sp) s += part[(int64_t)sp * K + j];
+  cn[j] = s;
+}
+// accumulation bias of Gram element (i, j): a power of two >= 4 sqrt(n_i n_j)
+// (Cauchy-Schwarz bounds every partial sum by sqrt(n_i n_j)), so that
+// h = sigma + sum_t a_ti a_tj always satisfies |h| >= |a_ti a_tj| and the
+// error-free update of h is FastTwoSum (3 operations instead of TwoSum's 6).
+__device__ __forceinline__ double dd_bias(double ni, double nj) {
+  const double b = 4.0 * sqrt(ni) * sqrt(nj) * (1.0 + 1e-6);
+  if (!(b > 0.0)) return 0x1.0p-1000;
+  int e;
+  frexp(b, &e);
+  return ldexp(1.0, e);  // 2^e > b
+}
+
 // Partial double-double Gram of one 64 x 64 tile pair (I <= J) over a row
 // range; element (ty + 16 i, tx + 16 j) per thread (conflict-free shared
 // reads).  W[(pair * nsplit + split) * 8192 + {0, 4096} + e] = (hi, lo).
 template <class L>
-__global__ void __launch_bounds__(kDDThreads) k_gram_dd(L ld, int64_t rows, int K, int nblk, int64_t rps, int nsplit,
-                                                        double* __restrict__ W, const long long* rows_dev) {
+__global__ void __launch_bounds__(kDDThreads, 2) k_gram_dd(L ld, int64_t rows, int K, int nblk, int64_t rps, int nsplit,
+                                                        double* __restrict__ W, const long long* rows_dev,
+                                                        const double* __restrict__ cn) {
   __shared__ double As[kDDSlab][64], Bs[kDDSlab][64];
   int I, J;
   pair_from_index(blockIdx.x, nblk, I, J);
@@ -150,10 +192,17 @@ __global__ void __launch_bounds__(kDDThreads) k_gram_dd(L ld, int64_t rows, int 
   if (rows_dev) rows = min(rows, (int64_t)*rows_dev);  // a shard's draw count (row-sharded sweeps)
   const int64_t r0 = (int64_t)blockIdx.y * rps, r1 = min(rows, r0 + rps);
   double h[4][4], l[4][4];
+  auto bias_of = [&](int i, int j) {
+    const int gi = 64 * I + ty + 16 * i, gj = 64 * J + tx + 16 * j;
+    return dd_bias(gi < K ? cn[gi] : 0.0, gj < K ? cn[gj] : 0.0);
+  };
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) h[i][j] = l[i][j] = 0.0;
+    for (int j = 0; j < 4; ++j) {
+      h[i][j] = bias_of(i, j);
+      l[i][j] = 0.0;
+    }
   double ra[4], rb[4];
   auto load = [&](int64_t t0) {
     const int64_t t = t0 + ty;
@@ -186,13 +235,19 @@ __global__ void __launch_bounds__(kDDThreads) k_gram_dd(L ld, int64_t rows, int 
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dd_acc(h[i][j], l[i][j], a[i], b[j]);
+        for (int j = 0; j < 4; ++j) {  // h += a b with |h| >= |a b|: FastTwoSum + the fma product error
+          const double p = __dmul_rn(a[i], b[j]);
+          const double e = fma(a[i], b[j], -p);
+          const double s = __dadd_rn(h[i][j], p);
+          l[i][j] = __dadd_rn(l[i][j], __dadd_rn(__dsub_rn(p, __dsub_rn(s, h[i][j])), e));
+          h[i][j] = s;
+        }
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const DD s = dd_two_sum(h[i][j], l[i][j]);
+      for (int j = 0; j < 4; ++j) {  // fold l into h (|h| >= |l|): keeps |l| <= ulp(h)
+        const DD s = dd_fast(h[i][j], l[i][j]);
         h[i][j] = s.h;
         l[i][j] = s.l;
       }
@@ -202,9 +257,11 @@ __global__ void __launch_bounds__(kDDThreads) k_gram_dd(L ld, int64_t rows, int 
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+      // remove the bias: h - sigma is exact (h in [3 sigma / 4, 5 sigma / 4], Sterbenz)
+      const DD v = dd_two_sum(__dsub_rn(h[i][j], bias_of(i, j)), l[i][j]);
       const int e = (ty + 16 * i) * 64 + tx + 16 * j;
-      out[e] = h[i][j];
-      out[4096 + e] = l[i][j];
+      out[e] = v.h;
+      out[4096 + e] = v.l;
     }
 }
 
