@@ -483,7 +483,7 @@ static void reserve_exact(tf_context* ctx, int64_t c, int Kmax) {
   b.cn.need(Kmax);
   b.cnp.need((size_t)((c + kCnRows - 1) / kCnRows) * Kmax);
   b.perm.need(Kmax);
-  b.svdf.need(2 + kSvdMaxSweeps + 8);
+  b.svdf.need(72);  // [0] deficient, [1] rank, [2..65] sweep flags, [66] nonzero rows of R'
 }
 
 // rows_dev (nullable): the device-side row count (a shard's draws, <= c);

@@ -468,6 +468,7 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
     a.svd[1] = rank;
     a.tol[0] = tol;
     for (int s = 2; s < 66; ++s) a.svd[s] = 0;
+    a.svd[66] = kend;  // nonzero rows of R' (rows past it are Eigen's exact zero pivots)
     if (a.o.method) a.o.method[a.o.lag - 1] = rank < p ? 1 : 0;
     if (a.o.rank) a.o.rank[a.o.lag - 1] = rank;
     if (a.o.sweeps) a.o.sweeps[a.o.lag - 1] = 0;
@@ -546,7 +547,11 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
   if (a.svd[0] == 0) return;  // full rank (uniform over the cluster)
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(128) double sm[];
-  const int p = a.p, m = p + 1, bw = a.bw, nblk = a.nblk;
+  // columns of N = the kend nonzero rows of R' (rows past kend are exact zero
+  // pivots: zero columns, singular value 0 -- dropped); blocks of bw of them
+  const int p = a.p, m = p + 1, nblk = a.nblk;
+  const int ncol = a.svd[66];
+  const int bw = max(1, min(a.bw, (ncol + nblk - 1) / nblk));
   const int cta = (int)cl.block_rank(), nct = nblk / 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = kSvdThreads / 32;
   double* slot[2] = {sm, sm + (size_t)bw * m};
@@ -563,7 +568,7 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
         const int c0 = colof[s];
         for (int e = tid; e < bw * m; e += kSvdThreads) {
           const int c = c0 + e / m;
-          slot[s][e] = c < p ? a.N[(int64_t)c * m + (e % m)] : 0.0;
+          slot[s][e] = c < ncol ? a.N[(int64_t)c * m + (e % m)] : 0.0;
         }
       }
       __syncthreads();
@@ -582,7 +587,7 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
             v = bw + (t + sr) % bw;
           }
           const int gu = colof[u / bw] + u % bw, gv = colof[v / bw] + v % bw;
-          if (gu >= p || gv >= p) continue;
+          if (gu >= ncol || gv >= ncol) continue;
           double* xu = slot[u / bw] + (size_t)(u % bw) * m;
           double* xv = slot[v / bw] + (size_t)(v % bw) * m;
           double al = 0.0, be = 0.0, ga = 0.0;
@@ -612,7 +617,7 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
         const int c0 = colof[s];
         for (int e = tid; e < bw * m; e += kSvdThreads) {
           const int c = c0 + e / m;
-          if (c < p) a.N[(int64_t)c * m + (e % m)] = slot[s][e];
+          if (c < ncol) a.N[(int64_t)c * m + (e % m)] = slot[s][e];
         }
       }
       __threadfence();
@@ -626,7 +631,7 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
   }
   if (cta == 0 && tid == 0 && a.o.sweeps) a.o.sweeps[a.o.lag - 1] = sweep + 1;
   // singular values, then the solution x = sum_{s_i >= thr} w_i z_i / s_i^2
-  for (int c = cta * 2 * bw + warp; c < min(p, (cta + 1) * 2 * bw); c += nwarp) {
+  for (int c = cta * 2 * bw + warp; c < min(ncol, (cta + 1) * 2 * bw); c += nwarp) {
     double s2 = 0.0;
     for (int i = lane; i < p; i += 32) {
       const double x = a.N[(int64_t)c * m + i];
@@ -638,13 +643,13 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
   __threadfence();
   cl.sync();
   double smax = 0.0;
-  for (int c = 0; c < p; ++c) smax = fmax(smax, a.sig[c]);
+  for (int c = 0; c < ncol; ++c) smax = fmax(smax, a.sig[c]);
   const double thr = fmax(smax * a.tol[0], 2.2250738585072014e-308);
   // block pair of this CTA: columns [2 bw cta, 2 bw (cta + 1)) -> partial x
   double* xp = a.xpart + (size_t)cta * p;
   for (int j = tid; j < p; j += kSvdThreads) {
     double acc = 0.0;
-    for (int c = cta * 2 * bw; c < min(p, (cta + 1) * 2 * bw); ++c) {
+    for (int c = cta * 2 * bw; c < min(ncol, (cta + 1) * 2 * bw); ++c) {
       const double s = a.sig[c];
       if (!(s >= thr)) continue;
       acc = fma(a.N[(int64_t)c * m + j], a.N[(int64_t)c * m + p] / (s * s), acc);

@@ -16,7 +16,7 @@ int main() {
   cudaMalloc(&dphi, p * 8); cudaMalloc(&dperm, (p + 1) * 4); cudaMalloc(&dsvd, 80 * 4);
   cudaMemcpy(dN, N.data(), N.size() * 8, cudaMemcpyHostToDevice); cudaMemcpy(dtol, &tol, 8, cudaMemcpyHostToDevice);
   cudaMemcpy(dperm, perm.data(), (p + 1) * 4, cudaMemcpyHostToDevice);
-  std::vector<int> sv(80, 0); sv[0] = 1; cudaMemcpy(dsvd, sv.data(), 320, cudaMemcpyHostToDevice);
+  std::vector<int> sv(80, 0); sv[0] = 1; sv[66] = (int)p; cudaMemcpy(dsvd, sv.data(), 320, cudaMemcpyHostToDevice);
   int nct = std::min(16, std::max(1, (int)(p + 31) / 32)), nblk = 2 * nct, bw = std::max(1, (int)(p + nblk - 1) / nblk);
   SvdArgs a{}; a.N = dN; a.sig = dsig; a.xpart = dx; a.perm = dperm; a.svd = dsvd; a.tol = dtol; a.p = p; a.nblk = nblk;
   a.bw = bw; a.rev = 0; a.o.phi = dphi; a.o.lag = 1;
