@@ -127,6 +127,18 @@ tf_status tf_lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed,
                         const tf_lsar_diag* diag, double* taus, double* coefs_packed,
                         double* lag_seconds, int* p_star);
 
+/* One lag of the LSAR recursion: LsarDriver::first_lag (p = 1) and
+ * LsarDriver::advance (p > 1) (lsar.hpp:65-84, lsar.cpp:70-98).  For p > 1 the
+ * lag-(p-1) state is scores_in / resid_in (w = n - p_bar host values each), or
+ * both NULL to continue from the state the previous tf_lsar_step call left on
+ * the device.  Outputs (nullable): the lag-p scores (the distribution's
+ * weights at lag p), residuals (w each), phi (p values, reference order) and
+ * the solve method.  Errors as lsar_fit; TF_USAGE for p outside 1..p_bar
+ * ("cannot advance past maximum lag"). */
+tf_status tf_lsar_step(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, int p, const double* scores_in,
+                       const double* resid_in, double* scores_out, double* resid_out, double* phi_out,
+                       int* method_out);
+
 /* LSAR order sweeps of a BATCH of independent fits in one pass per lag:
  * series b = y + b * y_stride (n values each; y_stride 0: one series shared
  * by every fit, i.e. B seeds over one series), seed seeds[b], all with the

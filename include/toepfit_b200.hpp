@@ -10,6 +10,7 @@
 //   RHConfig                  repeated_halving.hpp:56-65 (defaults / validate)
 //   lsar_fit                  lsar.hpp:89
 //   rh_fit (5- and 4-arg)     repeated_halving.hpp:97-99
+//   LeverageState, LsarDriver lsar.hpp:17-23, 65-84 (first_lag / advance / row_count)
 //   select_order              toeplitz.hpp:100
 //
 // One device context per host thread (created lazily on device 0, or bound
@@ -202,6 +203,67 @@ inline FitResult lsar_fit(const TimeSeries& series, int p_bar, std::int64_t c, s
              ctx);
   return gpu::finish(PacfMethod::lsar, p_bar, c, taus, packed, std::move(secs), p_star, 0.0);
 }
+
+// State of the lag recursion after the compressed solve at lag p
+// (lsar.hpp:17-23; std::vector instead of Eigen::VectorXd).
+struct LeverageState {
+  int p = 0;
+  std::int64_t m = 0;
+  std::vector<double> scores;        // approximate leverage, length m - p
+  std::vector<double> residuals;     // residuals of the lag-p compressed fit
+  std::vector<double> coefficients;  // compressed phi at lag p
+};
+
+// LsarDriver (lsar.hpp:65-84): the recursion one lag at a time on the GPU
+// (tf_lsar_step).  Like the reference, a state is a value: advance() uploads
+// its scores and residuals (the Python mirror continues from the device-resident
+// vectors when handed the state it just returned).
+class LsarDriver {
+ public:
+  LsarDriver(const TimeSeries& series, int p_bar, std::int64_t c, std::uint64_t seed)
+      : series_(series), p_bar_(p_bar), c_(c), seed_(seed) {
+    if (p_bar < 1) throw UsageError("maximum lag must be at least 1");  // lsar.cpp:55-64
+    if (series.size() <= static_cast<std::size_t>(p_bar) + 1)
+      throw DataError("series too short for maximum lag " + std::to_string(p_bar));
+    if (c < p_bar) throw UsageError("sample count below maximum lag");
+    w_ = static_cast<std::int64_t>(series.size()) - p_bar;
+  }
+  LeverageState first_lag() const { return step(1, nullptr); }
+  LeverageState advance(const LeverageState& state) const {
+    if (state.p < 1 || state.p >= p_bar_) throw UsageError("cannot advance past maximum lag");  // lsar.cpp:90
+    if (state.scores.size() != static_cast<std::size_t>(w_) || state.residuals.size() != static_cast<std::size_t>(w_))
+      throw UsageError("state vectors must hold row_count() values");
+    return step(state.p + 1, &state);
+  }
+  // window system for lag p: the first n - p_bar + p observations (lsar.cpp:66-68)
+  std::int64_t window_length(int p) const { return w_ + p; }
+  std::int64_t row_count() const { return w_; }
+
+ private:
+  LeverageState step(int p, const LeverageState* prev) const {
+    gpu::Context& g = gpu::context();
+    tf_context* ctx = g.get();
+    g.upload(series_);
+    LeverageState st;
+    st.p = p;
+    st.m = w_ + p;
+    st.scores.resize(static_cast<std::size_t>(w_));
+    st.residuals.resize(static_cast<std::size_t>(w_));
+    st.coefficients.resize(static_cast<std::size_t>(p));
+    int method = 0;
+    gpu::raise(tf_lsar_step(ctx, p_bar_, c_, seed_, p, prev ? prev->scores.data() : nullptr,
+                            prev ? prev->residuals.data() : nullptr, st.scores.data(), st.residuals.data(),
+                            st.coefficients.data(), &method),
+               ctx);
+    return st;
+  }
+
+  const TimeSeries& series_;
+  int p_bar_;
+  std::int64_t c_;
+  std::uint64_t seed_;
+  std::int64_t w_ = 0;
+};
 
 // Many independent LSAR fits in one batched sweep (tf_lsar_sweep_batch): fit b
 // = lsar_fit(series[b], p_bar, c, seeds[b]); equal-length series, p_bar <= 63.

@@ -49,7 +49,7 @@ EXPORTS = [
     "tf_apply_sample", "tf_solve_sampled", "tf_select_order", "tf_derive_seed",
     "tf_probe_fp64_peak", "tf_nccl_unique_id", "tf_nccl_init", "tf_keep_slice", "tf_lsar_sweep_sharded",
     "tf_tpu_size", "tf_sweep_span", "tf_exact_sweep", "tf_srht_sweep", "tf_hadamard", "tf_generate_series", "tf_download_series",
-    "tf_lsar_sweep_batch",
+    "tf_lsar_sweep_batch", "tf_lsar_step",
 ]
 
 _lib = None
@@ -101,6 +101,8 @@ def lib():
     L.tf_hadamard.argtypes = [C.c_void_p, _f64p, C.c_int64]
     L.tf_sweep_span.argtypes = [C.c_void_p, C.c_void_p, _f64p, _f64p]
     L.tf_version.argtypes = []
+    L.tf_lsar_step.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_int, _f64p, _f64p, _f64p, _f64p,
+                               _f64p, _i32p]
     L.tf_tpu_size.argtypes = [C.c_int]
     L.tf_tpu_size.restype = C.c_int64
     for name in EXPORTS:

@@ -498,6 +498,68 @@ def _finish(method, taus, coefs, secs, pstar, p_bar, c, upfront=0.0, diag=None) 
     return fit
 
 
+@dataclass
+class LeverageState:
+    """lsar.hpp:17-23: the recursion's state after the compressed solve at lag p."""
+    p: int = 0
+    m: int = 0
+    scores: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    residuals: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    coefficients: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    method: int = 0
+
+
+class LsarDriver:
+    """lsar.hpp:65-84 (LsarDriver): the LSAR recursion one lag at a time on the
+    GPU (tf_lsar_step).  first_lag() / advance(state) return host states like
+    the reference; advance() of the state the previous call returned continues
+    from the device-resident vectors (no upload), any other state is uploaded."""
+
+    def __init__(self, series: TimeSeries, p_bar: int, c: int, seed: int, *, engine: Engine | None = None):
+        if p_bar < 1:
+            raise UsageError("maximum lag must be at least 1")
+        if series.size() <= p_bar + 1:
+            raise DataError(f"series too short for maximum lag {p_bar}")
+        if c < p_bar:
+            raise UsageError("sample count below maximum lag")
+        self.series, self.p_bar, self.c, self.seed = series, int(p_bar), int(c), int(seed)
+        self.eng = engine or default_engine()
+        self._w = series.size() - p_bar
+        self._last = None
+
+    def row_count(self) -> int:
+        return self._w
+
+    def window_length(self, p: int) -> int:
+        """window_system(p) covers the first n - p_bar + p observations (lsar.cpp:66-68)."""
+        return self._w + p
+
+    def _step(self, p: int, prev: LeverageState | None) -> LeverageState:
+        self.eng.upload(self.series)
+        w = self._w
+        sc, rs, phi, m = np.zeros(w), np.zeros(w), np.zeros(p), C.c_int(0)
+        resident = prev is not None and prev is self._last
+        s_in = r_in = None
+        if prev is not None and not resident:
+            s_in = np.ascontiguousarray(prev.scores, dtype=np.float64)
+            r_in = np.ascontiguousarray(prev.residuals, dtype=np.float64)
+            if s_in.size != w or r_in.size != w:
+                raise UsageError("state vectors must hold row_count() values")
+        self.eng._check(_abi.lib().tf_lsar_step(self.eng._ctx, self.p_bar, self.c, C.c_uint64(self.seed), int(p),
+                                                ptr(s_in), ptr(r_in), ptr(sc), ptr(rs), ptr(phi), C.byref(m)))
+        st = LeverageState(p=p, m=w + p, scores=sc, residuals=rs, coefficients=phi, method=m.value)
+        self._last = st
+        return st
+
+    def first_lag(self) -> LeverageState:
+        return self._step(1, None)
+
+    def advance(self, state: LeverageState) -> LeverageState:
+        if state.p < 1 or state.p >= self.p_bar:
+            raise UsageError("cannot advance past maximum lag")  # lsar.cpp:90
+        return self._step(state.p + 1, state)
+
+
 def lsar_fit(series: TimeSeries, p_bar: int, c: int, seed: int, *, engine: Engine | None = None,
              fixed_idx=None, fixed_w=None, want_diag: bool = False) -> FitResult:
     """lsar.cpp:100-124 on the GPU.  fixed_idx/fixed_w ([p_bar][c]) switch to

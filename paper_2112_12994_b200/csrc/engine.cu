@@ -687,6 +687,7 @@ static void launch_fixed_weights(tf_context* ctx, const int64_t* idx, int64_t c,
 }
 
 static void alloc_state(tf_context* ctx, int p_bar, int64_t c, int64_t w) {
+  ctx->step_p = 0;  // the LsarDriver resident state is gone
   const int64_t ntile = (w + kPassTile - 1) / kPassTile;
   const int64_t nchunk = (w + kChunk - 1) / kChunk;
   ctx->s.need(w);
@@ -1194,6 +1195,7 @@ __global__ void k_first_nonfinite(const double* __restrict__ y, int64_t n, unsig
 static void upload_series(tf_context* ctx, const double* y, int64_t n, bool device_src) {
   if (n < 1 || !y) throw TfError{TF_DATA, "series must contain at least one value"};
   ctx->n = 0;  // no valid series until the check below passes (also when the allocation fails)
+  ctx->step_p = 0;
   ctx->y.need(n + 64);
   if (device_src)
     CK(cudaMemcpyAsync(ctx->y.get(), y, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1214,6 +1216,59 @@ static void upload_series(tf_context* ctx, const double* y, int64_t n, bool devi
   }
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->n = n;
+}
+
+// LsarDriver::first_lag / advance (lsar.hpp:65-84, lsar.cpp:70-98): one lag
+// of the recursion on the resident series.  p == 1: scores from
+// init_leverage_p1; p > 1: scores = leverage_update(s_in, r_in) of the given
+// lag-(p-1) state (host vectors of w = n - p_bar values), or -- s_in == r_in ==
+// NULL -- of the device-resident state the previous call left (stepping in
+// order).  Then the draws of Rng(derive_seed(seed, p)), the rank-revealing
+// solve, the lag-p residuals.  Outputs the lag-p state: the scores used at lag
+// p, the residuals, phi (all nullable).
+static void lsar_step(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, int p, const double* s_in,
+                      const double* r_in, double* s_out, double* r_out, double* phi_out, int* method_out) {
+  check_lsar_args(ctx, p_bar, c);
+  if (p < 1 || p > p_bar) throw TfError{TF_USAGE, "cannot advance past maximum lag"};  // lsar.cpp:90
+  const int64_t w = ctx->n - p_bar;
+  const int64_t ntile = (w + kPassTile - 1) / kPassTile;
+  cudaStream_t st = ctx->stream;
+  const bool resident = p > 1 && !s_in && !r_in;
+  if (resident && !(ctx->step_p == p - 1 && ctx->step_w == w))
+    throw TfError{TF_USAGE, "no resident lag-" + std::to_string(p - 1) + " state: pass the previous state"};
+  if (p > 1 && !resident && (!s_in || !r_in)) throw TfError{TF_USAGE, "a lag-p state needs scores and residuals"};
+  if (!resident) {
+    alloc_state(ctx, p_bar, c, w);
+  } else {
+    CK(cudaMemsetAsync(ctx->status.get(), 0, 4 * sizeof(int), st));
+  }
+  ctx->step_p = 0;
+  reserve_exact(ctx, c, p + 1);
+  ctx->rank.need(p_bar);
+  if (p == 1) {
+    launch_pass(ctx, 0, w, ctx->phi.get(), ctx->scal.get());  // r_0 = -y, s_0 = 0 -> s_1 = y^2 / ||y||^2
+  } else if (!resident) {
+    CK(cudaMemcpyAsync(ctx->s.get(), s_in, w * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->r.get(), r_in, w * sizeof(double), cudaMemcpyHostToDevice, st));
+    k_partials<<<(unsigned)ntile, kPassThreads, 0, st>>>(ctx->s.get(), ctx->r.get(), w, ctx->chunkA.get(),
+                                                        ctx->chunkB.get(), ctx->tileA.get(), ctx->tileB.get());
+    LAUNCH_CHECK("k_partials");
+  }
+  launch_scan(ctx, ntile, p - 1, 1);
+  launch_draw(ctx, derive_seed(seed, (uint64_t)p), c, w, ctx->idx.get(), ctx->wts.get());
+  ExactOut o{ctx->phi.get(), nullptr, 0, nullptr, ctx->method.get(), ctx->rank.get(), p, nullptr};
+  solve_exact(ctx, FwdRows{ctx->y.get(), ctx->idx.get(), ctx->wts.get(), 0}, c, p + 1, /*rev=*/0, o);
+  launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());  // s_p = s_{p-1} + r_{p-1}^2 / R_{p-1}, r_p
+  CK(cudaStreamSynchronize(st));
+  int sth[3];
+  CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  raise_from_status(sth);
+  if (s_out) CK(cudaMemcpy(s_out, ctx->s.get(), w * sizeof(double), cudaMemcpyDeviceToHost));
+  if (r_out) CK(cudaMemcpy(r_out, ctx->r.get(), w * sizeof(double), cudaMemcpyDeviceToHost));
+  if (phi_out) CK(cudaMemcpy(phi_out, ctx->phi.get(), p * sizeof(double), cudaMemcpyDeviceToHost));
+  if (method_out) CK(cudaMemcpy(method_out, ctx->method.get() + (p - 1), sizeof(int), cudaMemcpyDeviceToHost));
+  ctx->step_p = p;
+  ctx->step_w = w;
 }
 
 static void residuals_op(tf_context* ctx, const double* y, int64_t n_used, int p, const double* phi,
@@ -2479,6 +2534,15 @@ tf_status tf_lsar_sweep_batch(tf_context* ctx, const double* y, int64_t y_stride
       if (status_out)
         for (int k = 0; k < 3; ++k) status_out[3 * b + k] = stv[3 * b + k];
     }
+  });
+}
+
+tf_status tf_lsar_step(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, int p, const double* scores_in,
+                       const double* resid_in, double* scores_out, double* resid_out, double* phi_out, int* method_out) {
+  if (!ctx) return TF_USAGE;
+  return guarded(ctx, [&] {
+    cudaSetDevice(ctx->device);
+    tfe::lsar_step(ctx, p_bar, c, seed, p, scores_in, resid_in, scores_out, resid_out, phi_out, method_out);
   });
 }
 

@@ -98,4 +98,6 @@ struct tf_context {
   std::vector<cudaEvent_t> events;
   std::vector<cudaEvent_t> pev;  // phase events (2 per lag)
   int64_t launches = 0;
+  int step_p = 0;     // lag of the LsarDriver state resident in s / r (tf_lsar_step), 0: none
+  int64_t step_w = 0;
 };

@@ -42,6 +42,18 @@ int main(int argc, char** argv) {
     print_fit("batch0", fits[0], true);
     print_fit("batch1", fits[1], true);
   }
+  {  // LsarDriver (lsar.hpp:65-84): first_lag / advance, replay determinism
+    toepfit::LsarDriver drv(series, p_bar, c, seed);
+    const toepfit::LeverageState s1 = drv.first_lag();
+    const toepfit::LeverageState s2 = drv.advance(s1);
+    const toepfit::LeverageState r2 = drv.advance(drv.first_lag());
+    double ssum = 0.0;
+    for (double v : s2.scores) ssum += v;
+    std::printf("\"driver\": {\"rows\": %lld, \"m1\": %lld, \"m2\": %lld, \"p2\": %d, \"ssum2\": %.17g, "
+                "\"replay\": %d, \"phi2\": [%.17g, %.17g]},\n",
+                (long long)drv.row_count(), (long long)s1.m, (long long)s2.m, s2.p, ssum,
+                r2.coefficients == s2.coefficients ? 1 : 0, s2.coefficients[0], s2.coefficients[1]);
+  }
   // error mapping (errors.hpp:12-29 types)
   int usage = 0, data = 0, numerical = 0;
   try {

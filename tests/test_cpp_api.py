@@ -41,4 +41,10 @@ def test_cpp_api_matches_python(tmp_path):
     bt = tf.lsar_fit_batch(s, 16, 900, [11, 12], engine=eng)
     assert res["batch0"]["taus"] == bt[0].pacf.taus and res["batch1"]["taus"] == bt[1].pacf.taus
     assert res["batch0"]["p_star"] == bt[0].p_star
+    drv = res["driver"]
+    assert drv["rows"] == y.size - 16 and drv["m1"] == y.size - 15 and drv["m2"] == y.size - 14 and drv["p2"] == 2
+    assert abs(drv["ssum2"] - 2.0) < 1e-12 and drv["replay"] == 1
+    d = tf.LsarDriver(s, 16, 900, 11, engine=eng)
+    st2 = d.advance(d.first_lag())
+    assert np.allclose(drv["phi2"], st2.coefficients, rtol=1e-9, atol=0)
     eng.close()
