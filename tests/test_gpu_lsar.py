@@ -206,16 +206,43 @@ def test_lsar_fixed_index_parity(orc, tf, eng, n, q, p_bar, c):
     assert abs(d["scores"].sum() - p_bar) < 1e-8  # telescoping (acceptance crit. 5)
 
 
+def first_flip(gpu_idx, ref_idx):
+    """First lag whose draws differ, and the positions that differ there."""
+    for p in range(gpu_idx.shape[0]):
+        d = np.flatnonzero(gpu_idx[p] != ref_idx[p])
+        if d.size:
+            return p, d
+    return None, None
+
+
+def check_flip(gpu_idx, ref_idx, c):
+    """A draw can flip only when u_t S lands within rounding of a CDF boundary
+    (the GPU's hierarchical prefix vs the reference's sequential one): a
+    handful of draws of one lag, each moved to a neighbouring row."""
+    p, d = first_flip(gpu_idx, ref_idx)
+    if p is None:
+        return None
+    assert d.size <= max(2, c // 1000), f"{d.size} draws differ at lag {p + 1}: not a rounding flip"
+    assert np.all(np.abs(gpu_idx[p][d] - ref_idx[p][d]) <= 2), "flipped draws are not neighbouring rows"
+    return p
+
+
 def test_lsar_rng_mode_matches_oracle_draws(orc, tf, eng):
-    y = c1_like(30000, seed=8)
-    p_bar, c = 25, 2500
-    ref = orc.lsar_fit(y, p_bar, c, 4242)
-    fit = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, 4242, engine=eng, want_diag=True)
-    # lag 1 samples from the same closed-form scores: draws agree
-    assert np.mean(fit.diag["idx"][0] == ref.idx[0]) >= 0.999
-    if np.array_equal(fit.diag["idx"], ref.idx):
-        assert relerr(fit.pacf.taus, ref.taus) < TOL
-        assert fit.p_star == ref.p_star
+    # sketch.cpp:20-59 with the same counter RNG: identical draws lag after lag
+    # (the chains then coincide to 1e-9); a rounding flip is allowed only as a
+    # few neighbouring-row draws, and every lag before it must match exactly
+    for n, q, p_bar, c, seed in [(30000, 20, 25, 2500, 4242), (60000, 8, 12, 4000, 7), (12000, 4, 6, 900, 99)]:
+        y = c1_like(n, seed=q + 3, q=q)
+        ref = orc.lsar_fit(y, p_bar, c, seed)
+        fit = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, seed, engine=eng, want_diag=True)
+        flip = check_flip(fit.diag["idx"], ref.idx, c)
+        upto = p_bar if flip is None else flip
+        for p in range(upto):
+            assert np.array_equal(fit.diag["idx"][p], ref.idx[p])
+            assert relerr(fit.per_lag_coefficients[p], ref.coefs[p]) < TOL
+        if flip is None:
+            assert relerr(fit.pacf.taus, ref.taus) < TOL
+            assert fit.p_star == ref.p_star
 
 
 def test_lsar_deterministic_and_seed_sensitive(tf, eng):
@@ -235,15 +262,17 @@ def test_lsar_deterministic_and_seed_sensitive(tf, eng):
 
 
 def test_lsar_distribution_over_seeds(orc, tf, eng):
-    """RNG mode: per-lag tau estimates agree with the oracle's in distribution."""
-    y = c1_like(20000, seed=21, q=6)
-    p_bar, c = 10, 400
+    """RNG mode: per-lag tau estimates are distributed as the oracle's --
+    independent seeds on each side (GPU 1000+k, oracle 50000+k), 200 fits
+    each, two-sample Kolmogorov-Smirnov per lag (Bonferroni over the lags)."""
+    from scipy.stats import ks_2samp
+    y = c1_like(8000, seed=21, q=6)
+    p_bar, c, nseed = 8, 300, 200
     s = tf.TimeSeries(y)
-    g = np.array([tf.lsar_fit(s, p_bar, c, 1000 + k, engine=eng).pacf.taus for k in range(24)])
-    r = np.array([orc.lsar_fit(y, p_bar, c, 5000 + k).taus for k in range(24)])
-    se = np.sqrt(g.var(0) / 24 + r.var(0) / 24) + 1e-12
-    z = np.abs(g.mean(0) - r.mean(0)) / se
-    assert (z < 4.5).all(), z
+    g = np.array([tf.lsar_fit(s, p_bar, c, 1000 + k, engine=eng).pacf.taus for k in range(nseed)])
+    r = np.array([orc.lsar_fit(y, p_bar, c, 50000 + k).taus for k in range(nseed)])
+    pv = np.array([ks_2samp(g[:, p], r[:, p]).pvalue for p in range(p_bar)])
+    assert (pv > 1e-3 / p_bar).all(), pv
 
 
 def test_lsar_errors(orc, tf, eng):
