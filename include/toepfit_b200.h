@@ -160,6 +160,27 @@ tf_status tf_rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cf
                       const tf_rh_diag* diag, double* taus, double* coefs_packed,
                       double* lag_seconds, double* upfront_seconds, int* p_star);
 
+/* ---- Repeated Halving over a general row source ----
+ * RowSource (repeated_halving.hpp:17-23): an n x k matrix reached through
+ * gather(user, idx, count, out), which writes rows idx[0..count) into out
+ * (count x k, row-major, host memory). */
+typedef void (*tf_gather_fn)(void* user, const int64_t* idx, int64_t count, double* out);
+/* generalized_leverage (repeated_halving.hpp:76-78, repeated_halving.cpp:54-123):
+ * leverage of the rows of C (rows x c_cols, row-major) through the column space
+ * of B (brows x b_cols): ||R^-T P^T x||^2 (sketch_rows 0) or its sketch with
+ * sketch_rows Gaussian mixes from Rng(sketch_seed).  Errors: TF_USAGE column
+ * count mismatch; TF_NUMERICAL brows < k ("too few rows") or B rank deficient
+ * under the CPQR rule (threshold max(brows, k) eps). */
+tf_status tf_generalized_leverage(tf_context* ctx, const double* c_rows, int64_t rows, int64_t c_cols, const double* b,
+                                  int64_t brows, int64_t b_cols, int64_t sketch_rows, uint64_t sketch_seed, double* out);
+/* repeated_halving(RowSource, RHConfig) (repeated_halving.cpp:126-180): the
+ * downward halving (bit-identical level sets), the sketched upward pass; the
+ * approximation's rows (approx_rows x k, row-major) land in approx_out
+ * (capacity approx_cap rows), levels = halving depth. */
+tf_status tf_repeated_halving(tf_context* ctx, int64_t n, int64_t k, tf_gather_fn gather, void* user,
+                              const tf_rh_cfg* cfg, double* approx_out, int64_t approx_cap, int64_t* approx_rows,
+                              int* levels);
+
 /* Exact per-lag OLS on the full series (bench.cpp:27-48, the reference's
  * "exact" method): lag h uses all n - h rows.  Outputs as tf_lsar_sweep;
  * p_star uses the bound 1.96 / sqrt(n - p_bar). */

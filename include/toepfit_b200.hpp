@@ -11,6 +11,8 @@
 //   lsar_fit                  lsar.hpp:89
 //   rh_fit (5- and 4-arg)     repeated_halving.hpp:97-99
 //   LeverageState, LsarDriver lsar.hpp:17-23, 65-84 (first_lag / advance / row_count)
+//   RowSource, DenseRowSource, repeated_halving.hpp:17-91
+//     GaussianSketch, SpectralApprox, generalized_leverage, repeated_halving
 //   select_order              toeplitz.hpp:100
 //
 // One device context per host thread (created lazily on device 0, or bound
@@ -21,6 +23,7 @@
 #ifndef TOEPFIT_B200_HPP
 #define TOEPFIT_B200_HPP
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <memory>
@@ -264,6 +267,87 @@ class LsarDriver {
   std::uint64_t seed_;
   std::int64_t w_ = 0;
 };
+
+// ---- Repeated Halving over a general row source (repeated_halving.hpp:17-91) ----
+// RowSource: an n x k matrix that may never exist in memory; gather() fills
+// out (idx.size() x k, row-major) with rows idx[t].
+class RowSource {
+ public:
+  virtual ~RowSource() = default;
+  virtual std::int64_t rows() const = 0;
+  virtual std::int64_t cols() const = 0;
+  virtual void gather(const std::vector<std::int64_t>& idx, std::vector<double>& out) const = 0;
+};
+
+class DenseRowSource final : public RowSource {
+ public:
+  // a: rows x cols, row-major
+  DenseRowSource(std::vector<double> a, std::int64_t rows, std::int64_t cols)
+      : a_(std::move(a)), rows_(rows), cols_(cols) {}
+  std::int64_t rows() const override { return rows_; }
+  std::int64_t cols() const override { return cols_; }
+  void gather(const std::vector<std::int64_t>& idx, std::vector<double>& out) const override {
+    out.resize(idx.size() * (std::size_t)cols_);
+    for (std::size_t t = 0; t < idx.size(); ++t)
+      for (std::int64_t j = 0; j < cols_; ++j) out[t * cols_ + j] = a_[(std::size_t)(idx[t] * cols_ + j)];
+  }
+
+ private:
+  std::vector<double> a_;
+  std::int64_t rows_, cols_;
+};
+
+struct GaussianSketch {
+  std::int64_t rows = 0;
+  std::uint64_t seed = 0;
+};
+
+struct SpectralApprox {
+  std::vector<double> rows;  // sample_count x k, row-major
+  int levels = 0;
+  std::int64_t sample_count = 0;
+};
+
+// leverage of the rows of C (rows x k, row-major) through B's column space
+inline std::vector<double> generalized_leverage(const std::vector<double>& c_rows, std::int64_t rows,
+                                                const std::vector<double>& b, std::int64_t brows, std::int64_t k,
+                                                const GaussianSketch* sketch = nullptr) {
+  gpu::Context& g = gpu::context();
+  tf_context* ctx = g.get();
+  std::vector<double> out((std::size_t)(rows > 0 ? rows : 1));
+  gpu::raise(tf_generalized_leverage(ctx, c_rows.data(), rows, k, b.data(), brows, k, sketch ? sketch->rows : 0,
+                                     sketch ? sketch->seed : 0, out.data()),
+             ctx);
+  out.resize((std::size_t)rows);
+  return out;
+}
+
+inline SpectralApprox repeated_halving(const RowSource& x, const RHConfig& config) {
+  config.validate();
+  gpu::Context& g = gpu::context();
+  tf_context* ctx = g.get();
+  struct Shim {
+    const RowSource* src;
+    std::vector<std::int64_t> ids;
+    std::vector<double> buf;
+  } shim{&x, {}, {}};
+  auto cb = [](void* user, const int64_t* idx, int64_t count, double* out) {
+    Shim* s = static_cast<Shim*>(user);
+    s->ids.assign(idx, idx + count);
+    s->src->gather(s->ids, s->buf);
+    std::copy(s->buf.begin(), s->buf.end(), out);
+  };
+  const std::int64_t n = x.rows(), k = x.cols();
+  const std::int64_t cap = std::max<std::int64_t>({config.sample_count, config.base_threshold, std::int64_t(1)});
+  SpectralApprox a;
+  a.rows.resize((std::size_t)(cap * k));
+  const tf_rh_cfg cfg{config.base_threshold, config.sample_count, config.gaussian_rows, config.seed};
+  std::int64_t ar = 0;
+  gpu::raise(tf_repeated_halving(ctx, n, k, cb, &shim, &cfg, a.rows.data(), cap, &ar, &a.levels), ctx);
+  a.rows.resize((std::size_t)(ar * k));
+  a.sample_count = ar;
+  return a;
+}
 
 // Many independent LSAR fits in one batched sweep (tf_lsar_sweep_batch): fit b
 // = lsar_fit(series[b], p_bar, c, seeds[b]); equal-length series, p_bar <= 63.

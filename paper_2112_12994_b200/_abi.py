@@ -43,13 +43,16 @@ class TfRhDiag(C.Structure):
                 ("launches_out", _i64p), ("method_out", _i32p), ("rank_out", _i32p)]
 
 
+# RowSource gather callback (tf_gather_fn): (user, idx, count, out rows x k row-major)
+GATHER_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_int64), C.c_int64, C.POINTER(C.c_double))
+
 EXPORTS = [
     "tf_version", "tf_create", "tf_destroy", "tf_last_error", "tf_upload_series",
     "tf_upload_series_device", "tf_lsar_sweep", "tf_rh_sweep", "tf_residuals", "tf_sample_rows",
     "tf_apply_sample", "tf_solve_sampled", "tf_select_order", "tf_derive_seed",
     "tf_probe_fp64_peak", "tf_nccl_unique_id", "tf_nccl_init", "tf_keep_slice", "tf_lsar_sweep_sharded",
     "tf_tpu_size", "tf_sweep_span", "tf_exact_sweep", "tf_srht_sweep", "tf_hadamard", "tf_generate_series", "tf_download_series",
-    "tf_lsar_sweep_batch", "tf_lsar_step",
+    "tf_lsar_sweep_batch", "tf_lsar_step", "tf_generalized_leverage", "tf_repeated_halving",
 ]
 
 _lib = None
@@ -101,6 +104,10 @@ def lib():
     L.tf_hadamard.argtypes = [C.c_void_p, _f64p, C.c_int64]
     L.tf_sweep_span.argtypes = [C.c_void_p, C.c_void_p, _f64p, _f64p]
     L.tf_version.argtypes = []
+    L.tf_generalized_leverage.argtypes = [C.c_void_p, _f64p, C.c_int64, C.c_int64, _f64p, C.c_int64, C.c_int64,
+                                          C.c_int64, C.c_uint64, _f64p]
+    L.tf_repeated_halving.argtypes = [C.c_void_p, C.c_int64, C.c_int64, GATHER_FN, C.c_void_p, C.POINTER(TfRhCfg),
+                                      _f64p, C.c_int64, _i64p, _i32p]
     L.tf_lsar_step.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_int, _f64p, _f64p, _f64p, _f64p,
                                _f64p, _i32p]
     L.tf_tpu_size.argtypes = [C.c_int]

@@ -560,6 +560,127 @@ class LsarDriver:
         return self._step(state.p + 1, state)
 
 
+# ---------------------------------------------------------------- RowSource / RH over a row source
+@dataclass
+class GaussianSketch:
+    """sketch.hpp GaussianSketch: `rows` Gaussian mixes drawn from Rng(seed)."""
+    rows: int
+    seed: int
+
+
+class RowSource:
+    """repeated_halving.hpp:17-23: read-only row access to an n x k matrix that may
+    never exist in memory.  Subclasses implement rows(), cols(), gather(idx)."""
+
+    def rows(self) -> int:
+        raise NotImplementedError
+
+    def cols(self) -> int:
+        raise NotImplementedError
+
+    def gather(self, idx: np.ndarray) -> np.ndarray:
+        raise NotImplementedError
+
+
+class DenseRowSource(RowSource):
+    def __init__(self, a):
+        self.a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+    def rows(self) -> int:
+        return int(self.a.shape[0])
+
+    def cols(self) -> int:
+        return int(self.a.shape[1])
+
+    def gather(self, idx):
+        return self.a[np.asarray(idx, dtype=np.int64)]
+
+
+class AugmentedRowSource(RowSource):
+    """Rows of the augmented lag-p system [T, b] (repeated_halving.cpp:22-31):
+    row i = (y[p+i-1], ..., y[i], y[p+i]) over the first n_used observations."""
+
+    def __init__(self, series: TimeSeries, p: int, n_used: int | None = None):
+        self.y = series.values()
+        self.p = int(p)
+        self.n_used = int(n_used) if n_used is not None else series.size()
+        if self.p < 1:
+            raise UsageError("lag order must be at least 1")
+        if self.n_used <= self.p:
+            raise DataError("series window too short for lag order")
+
+    def rows(self) -> int:
+        return self.n_used - self.p
+
+    def cols(self) -> int:
+        return self.p + 1
+
+    def gather(self, idx):
+        i = np.asarray(idx, dtype=np.int64)[:, None]
+        cols = np.concatenate([self.p - 1 - np.arange(self.p), [self.p]])
+        return self.y[i + cols[None, :]]
+
+
+@dataclass
+class SpectralApprox:
+    """repeated_halving.hpp:49-53."""
+    rows: np.ndarray
+    levels: int = 0
+    sample_count: int = 0
+
+
+def generalized_leverage(c_rows, b, sketch: GaussianSketch | None = None, *, engine: Engine | None = None):
+    """repeated_halving.hpp:76-78 on the GPU (tf_generalized_leverage)."""
+    eng = engine or default_engine()
+    c_rows = np.ascontiguousarray(np.asarray(c_rows, dtype=np.float64))
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+    if c_rows.ndim != 2 or b.ndim != 2:
+        raise UsageError("matrices must be 2-D")
+    out = np.zeros(max(c_rows.shape[0], 1))
+    g, sd = (int(sketch.rows), int(sketch.seed)) if sketch is not None else (0, 0)
+    eng._check(_abi.lib().tf_generalized_leverage(eng._ctx, ptr(c_rows), c_rows.shape[0], c_rows.shape[1], ptr(b),
+                                                  b.shape[0], b.shape[1], g, C.c_uint64(sd), ptr(out)))
+    return out[:c_rows.shape[0]]
+
+
+def repeated_halving(x: RowSource, config: RHConfig, *, engine: Engine | None = None) -> SpectralApprox:
+    """repeated_halving.hpp:83-86 on the GPU over a host row source (tf_repeated_halving)."""
+    config.validate()
+    eng = engine or default_engine()
+    n, k = int(x.rows()), int(x.cols())
+    errors = []
+
+    def _gather(user, idx, count, out):
+        try:
+            ids = np.ctypeslib.as_array(idx, shape=(count,)).copy() if count else np.zeros(0, np.int64)
+            rows = np.ascontiguousarray(np.asarray(x.gather(ids), dtype=np.float64)).reshape(count, k)
+            if count:
+                np.ctypeslib.as_array(out, shape=(count * k,))[:] = rows.ravel()
+        except Exception as e:  # never unwind through the C ABI
+            errors.append(e)
+
+    cb = _abi.GATHER_FN(_gather)
+    cap = max(config.sample_count, config.base_threshold, n if n <= config.base_threshold else 0, 1)
+    approx = np.zeros((cap, k))
+    arows = C.c_int64(0)
+    lev = C.c_int(0)
+    cfg = _abi.TfRhCfg(config.base_threshold, config.sample_count, config.gaussian_rows, config.seed)
+    st = _abi.lib().tf_repeated_halving(eng._ctx, n, k, cb, None, C.byref(cfg), ptr(approx), cap, C.byref(arows),
+                                        C.byref(lev))
+    if errors:
+        raise errors[0]
+    eng._check(st)
+    return SpectralApprox(rows=approx[:arows.value].copy(), levels=lev.value, sample_count=int(arows.value))
+
+
+def rh_leverage_scores(series: TimeSeries, p: int, config: RHConfig, *, engine: Engine | None = None):
+    """repeated_halving.hpp:88-91: scores of every row of the augmented lag-p
+    system against its RH approximation (final pass unsketched)."""
+    src = AugmentedRowSource(series, p)
+    approx = repeated_halving(src, config, engine=engine)
+    return generalized_leverage(src.gather(np.arange(src.rows())), approx.rows, None, engine=engine)
+
+
 def lsar_fit(series: TimeSeries, p_bar: int, c: int, seed: int, *, engine: Engine | None = None,
              fixed_idx=None, fixed_w=None, want_diag: bool = False) -> FitResult:
     """lsar.cpp:100-124 on the GPU.  fixed_idx/fixed_w ([p_bar][c]) switch to

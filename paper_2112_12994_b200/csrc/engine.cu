@@ -1850,6 +1850,200 @@ static void rh_sweep(tf_context* ctx, int p_bar, int64_t c, const tf_rh_cfg* cfg
 }
 
 // ---------------------------------------------------------------------------
+// Repeated Halving over a general row source (repeated_halving.hpp:17-23,
+// 76-90; repeated_halving.cpp:54-180): rows reached through a host gather
+// callback, staged into dense device buffers; the halving, the leverage
+// kernel (rank check by the pivoted double-double Cholesky = CPQR rule,
+// inverse factor by CholeskyQR), the Gaussian sketch and the row scores are
+// the Toeplitz path's kernels over dense row loaders.
+
+// CPQR rank of a dense reference matrix (rows x K) under Eigen's rule
+// (threshold max(rows, K) eps); LeverageKernel's checks (repeated_halving.cpp:56-64)
+static void leverage_rank_check(tf_context* ctx, const double* B, int64_t rows, int K) {
+  if (rows < K) throw TfError{TF_NUMERICAL, "reference matrix has too few rows"};
+  reserve_exact(ctx, rows, K + 1);
+  ctx->rh_phis.need(K + 2);
+  ctx->rank.need(1);
+  ctx->method.need(1);
+  ExactOut o{ctx->rh_phis.get(), nullptr, 0, nullptr, ctx->method.get(), ctx->rank.get(), 1, nullptr};
+  solve_exact(ctx, DenseRowsZ{B, (int64_t)K, K}, rows, K + 1, /*rev=*/0, o);
+  int rk = 0;
+  CK(cudaMemcpyAsync(&rk, ctx->rank.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (rk != K) throw TfError{TF_NUMERICAL, "reference matrix is rank deficient"};
+}
+
+// scores of the `len` dense rows C (len x K) against the reference matrix B
+// (brows x K): ||R^-T P^T x||^2 (g == 0) or ||G Q R^-T P^T x||^2 / g with the
+// sketch's normals drawn from derive-seeded stream `gseed` (g x brows, column j
+// of G = draws j g .. j g + g - 1, sketch.cpp:241-253)
+static void dense_scores(tf_context* ctx, const double* C, int64_t len, const double* B, int64_t brows, int K, int g,
+                         uint64_t gseed, double* out) {
+  cudaStream_t st = ctx->stream;
+  leverage_rank_check(ctx, B, brows, K);
+  ctx->rh_S.need(tpu_size(K));
+  ctx->rh_phis.need(K + 2);
+  reserve_solve(ctx, brows, K);
+  SolveOut so{ctx->rh_phis.get(), nullptr, 0, nullptr, nullptr, 0, ctx->status.get()};
+  CK(cudaMemsetAsync(ctx->status.get(), 0, 4 * sizeof(int), st));
+  DenseRows bl{B, (int64_t)K};
+  solve_rows(ctx, bl, brows, K, so, nullptr, nullptr, ctx->rh_S.get(), 0, nullptr, nullptr, /*exact=*/true);
+  DenseRows cl{C, (int64_t)K};
+  if (g <= 0) {
+    rowsq_attr<DenseRows, TpuW, true>();
+    const int km = rowsq_main_cols(K);
+    k_rowsq<DenseRows, TpuW, true><<<(unsigned)((len + 63) / 64), kGramThreads, kRowsqSmem, st>>>(
+        cl, len, K, TpuW{ctx->rh_S.get(), K}, km, out);
+    LAUNCH_CHECK("k_rowsq");
+    rowsq_tail(ctx, cl, len, K, TpuW{ctx->rh_S.get(), K}, km, K, out, 1);
+    return;
+  }
+  const int Kp = g + K;
+  const int64_t count = (int64_t)g * brows;
+  const int64_t attempts = (count / 2 + 1) * 135 / 100 + 4096;
+  ctx->rh_norm.need(count);
+  ctx->rh_ok.need(attempts);
+  ctx->rh_tsum.need((attempts + kScanTileN - 1) / kScanTileN + 3);
+  ctx->rh_Gp.need(tpu_size(Kp));
+  ctx->rh_H0.need((size_t)g * K);
+  ctx->rh_W.need((size_t)g * K);
+  reserve_gram(ctx, brows, Kp);
+  k_polar_flags<<<grid_for(attempts, ctx), 256, 0, st>>>(gseed, attempts, ctx->rh_ok.get());
+  scan_apply(ctx, ctx->rh_ok.get(), attempts, PolarF{gseed, count, ctx->rh_norm.get()});
+  k_check_normals<<<1, 1, 0, st>>>(ctx->rh_tsum.get() + ((attempts + kScanTileN - 1) / kScanTileN) + 1, (count + 1) / 2,
+                                   ctx->status.get());
+  ConcatRowsT<DenseRows> cr{ctx->rh_norm.get(), g, bl};
+  gram(ctx, cr, brows, Kp, ctx->rh_Gp.get(), nullptr);
+  k_rh_h0<<<grid_for((int64_t)g * K, ctx), 256, 0, st>>>(ctx->rh_Gp.get(), Kp, g, ctx->rh_S.get(), K, ctx->rh_H0.get());
+  k_rh_w<<<grid_for((int64_t)g * K, ctx), 256, 0, st>>>(ctx->rh_H0.get(), ctx->rh_S.get(), K, g, ctx->rh_W.get());
+  rowsq_attr<DenseRows, DenseW, false>();
+  const int gm = rowsq_main_cols(g);
+  k_rowsq<DenseRows, DenseW, false><<<(unsigned)((len + 63) / 64), kGramThreads, kRowsqSmem, st>>>(
+      cl, len, K, DenseW{ctx->rh_W.get(), g}, gm, out);
+  LAUNCH_CHECK("k_rowsq");
+  rowsq_tail(ctx, cl, len, K, DenseW{ctx->rh_W.get(), g}, gm, g, out, 1);
+  g_launches += 8;
+}
+
+static void generalized_leverage(tf_context* ctx, const double* c_rows, int64_t rows, int64_t c_cols, const double* b,
+                                 int64_t brows, int64_t b_cols, int64_t g, uint64_t gseed, double* out) {
+  if (c_cols != b_cols) throw TfError{TF_USAGE, "column count mismatch"};  // repeated_halving.cpp:100
+  if (rows < 0 || brows < 0 || c_cols < 1) throw TfError{TF_USAGE, "empty matrix"};
+  const int K = (int)c_cols;
+  cudaStream_t st = ctx->stream;
+  DBuf<double> C, B;
+  C.need((size_t)std::max<int64_t>(rows, 1) * K);
+  B.need((size_t)std::max<int64_t>(brows, 1) * K);
+  CK(cudaMemcpyAsync(C.get(), c_rows, sizeof(double) * rows * K, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B.get(), b, sizeof(double) * brows * K, cudaMemcpyHostToDevice, st));
+  ctx->rh_scores.need(std::max<int64_t>(rows, 1));
+  ctx->status.need(4);
+  dense_scores(ctx, C.get(), rows, B.get(), brows, K, (int)g, gseed, ctx->rh_scores.get());
+  CK(cudaMemcpyAsync(out, ctx->rh_scores.get(), sizeof(double) * rows, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int sth[3];
+  CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  raise_from_status(sth);
+}
+
+// repeated_halving(RowSource, RHConfig) (repeated_halving.cpp:126-180)
+static void repeated_halving_src(tf_context* ctx, int64_t n, int64_t k, tf_gather_fn gather, void* user,
+                                 const tf_rh_cfg* cfg, double* approx_out, int64_t cap, int64_t* arows_out,
+                                 int* levels_out) {
+  if (!cfg || !gather) throw TfError{TF_USAGE, "row source and config required"};
+  if (cfg->sample_count < 1) throw TfError{TF_USAGE, "sample count must be positive"};
+  if (cfg->base_threshold < cfg->sample_count) throw TfError{TF_USAGE, "base threshold below sample count"};
+  if (cfg->gaussian_rows < 1) throw TfError{TF_USAGE, "need at least one sketch row"};
+  if (n < 1) throw TfError{TF_USAGE, "empty source"};
+  if (k < 1) throw TfError{TF_USAGE, "empty matrix"};
+  if (n >= (int64_t)INT32_MAX) throw TfError{TF_USAGE, "source too long for the halving index width"};
+  cudaStream_t st = ctx->stream;
+  const int K = (int)k;
+  const int64_t sc = cfg->sample_count;
+  std::vector<int64_t> lsz{n}, loff{0, 0};
+  while (lsz.back() > cfg->base_threshold) {
+    lsz.push_back(lsz.back() / 2);
+    loff.push_back(loff.back() + lsz.back());
+  }
+  const int depth = (int)lsz.size() - 1;
+  const int64_t arows_final = depth > 0 ? sc : n;
+  if (cap < arows_final) throw TfError{TF_USAGE, "approximation buffer too small"};
+  ctx->rh_lvl.need(std::max<int64_t>(loff.back(), 1));
+  if (depth > 0) {
+    ctx->rh_J.need(n / 2 + 1);
+    ctx->rh_bk.need(n / 2 + 1);
+    ctx->rh_cnt.need(n);
+    ctx->rh_start.need(n);
+    ctx->rh_fill.need(n);
+    ctx->rh_pick.need(n);
+    ctx->rh_tsum.need((n + kScanTileN - 1) / kScanTileN + 3);
+  }
+  ctx->rh_flag.need(4);
+  ctx->status.need(4);
+  CK(cudaMemsetAsync(ctx->status.get(), 0, 4 * sizeof(int), st));
+  auto level_ptr = [&](int l) -> int64_t* { return l == 0 ? nullptr : ctx->rh_lvl.get() + loff[l]; };
+  for (int l = 1; l <= depth; ++l)
+    rh_halve(ctx, derive_seed(cfg->seed, 0x10000ull + (uint64_t)l), level_ptr(l - 1), lsz[l - 1], level_ptr(l));
+  std::vector<int64_t> lv((size_t)std::max<int64_t>(loff.back(), 1));
+  if (depth > 0)
+    CK(cudaMemcpyAsync(lv.data(), ctx->rh_lvl.get(), sizeof(int64_t) * loff.back(), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  auto level_rows = [&](int l, std::vector<int64_t>& out) {  // global row ids of level l
+    out.resize((size_t)lsz[l]);
+    if (l == 0) std::iota(out.begin(), out.end(), int64_t(0));
+    else std::copy(lv.begin() + loff[l], lv.begin() + loff[l] + lsz[l], out.begin());
+  };
+  // base approximation: the last level's rows (unweighted)
+  std::vector<int64_t> ids;
+  level_rows(depth, ids);
+  std::vector<double> host((size_t)ids.size() * K);
+  gather(user, ids.data(), (int64_t)ids.size(), host.data());
+  DBuf<double> approx, rowsbuf;
+  approx.need((size_t)std::max<int64_t>(std::max<int64_t>(lsz[depth], sc), 1) * K);
+  CK(cudaMemcpyAsync(approx.get(), host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice, st));
+  int64_t arows = lsz[depth];
+  std::vector<int64_t> sidx((size_t)sc);
+  std::vector<double> sw((size_t)sc);
+  for (int i = depth - 1; i >= 0; --i) {
+    // scores of level i's rows against the approximation (8192-row blocks in
+    // the reference; one block here), sketched with g mixes
+    level_rows(i, ids);
+    const int64_t len = (int64_t)ids.size();
+    host.resize((size_t)len * K);
+    gather(user, ids.data(), len, host.data());
+    rowsbuf.need((size_t)len * K);
+    CK(cudaMemcpyAsync(rowsbuf.get(), host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice, st));
+    ctx->rh_scores.need(len);
+    dense_scores(ctx, rowsbuf.get(), len, approx.get(), arows, K, (int)cfg->gaussian_rows,
+                 derive_seed(cfg->seed, 0x20000ull + (uint64_t)i), ctx->rh_scores.get());
+    // leverage_to_distribution + sample_rows (sketch.cpp:20-59)
+    alloc_state(ctx, 1, sc, len);
+    score_distribution(ctx, ctx->rh_scores.get(), len);
+    launch_draw_on(ctx, ctx->rh_scores.get(), len, derive_seed(cfg->seed, 0x30000ull + (uint64_t)i), sc,
+                   ctx->idx.get(), ctx->wts.get());
+    CK(cudaMemcpyAsync(sidx.data(), ctx->idx.get(), sizeof(int64_t) * sc, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(sw.data(), ctx->wts.get(), sizeof(double) * sc, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int sth[3];
+    CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
+    raise_from_status(sth);
+    // picked rows, weighted: the next approximation
+    std::vector<int64_t> picked((size_t)sc);
+    for (int64_t t = 0; t < sc; ++t) picked[t] = ids[(size_t)sidx[t]];
+    host.resize((size_t)sc * K);
+    gather(user, picked.data(), sc, host.data());
+    for (int64_t t = 0; t < sc; ++t)
+      for (int j = 0; j < K; ++j) host[(size_t)t * K + j] *= sw[t];
+    CK(cudaMemcpyAsync(approx.get(), host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice, st));
+    arows = sc;
+  }
+  CK(cudaMemcpyAsync(approx_out, approx.get(), sizeof(double) * arows * K, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (arows_out) *arows_out = arows;
+  if (levels_out) *levels_out = depth;
+}
+
+// ---------------------------------------------------------------------------
 // Row-sharded LSAR steps.  The caller (paper_2112_12994_b200/
 // shard.py) owns the collectives: per lag an allgather of this shard's
 // (sum s, sum r^2) and, per CholeskyQR pass, an allreduce of the K x K Gram.
@@ -2534,6 +2728,25 @@ tf_status tf_lsar_sweep_batch(tf_context* ctx, const double* y, int64_t y_stride
       if (status_out)
         for (int k = 0; k < 3; ++k) status_out[3 * b + k] = stv[3 * b + k];
     }
+  });
+}
+
+tf_status tf_generalized_leverage(tf_context* ctx, const double* c_rows, int64_t rows, int64_t c_cols, const double* b,
+                                  int64_t brows, int64_t b_cols, int64_t sketch_rows, uint64_t sketch_seed, double* out) {
+  if (!ctx || (rows > 0 && (!c_rows || !out)) || (brows > 0 && !b)) return TF_USAGE;
+  return guarded(ctx, [&] {
+    cudaSetDevice(ctx->device);
+    tfe::generalized_leverage(ctx, c_rows, rows, c_cols, b, brows, b_cols, sketch_rows, sketch_seed, out);
+  });
+}
+
+tf_status tf_repeated_halving(tf_context* ctx, int64_t n, int64_t k, tf_gather_fn gather, void* user,
+                              const tf_rh_cfg* cfg, double* approx_out, int64_t approx_cap, int64_t* approx_rows,
+                              int* levels) {
+  if (!ctx || !approx_out) return TF_USAGE;
+  return guarded(ctx, [&] {
+    cudaSetDevice(ctx->device);
+    tfe::repeated_halving_src(ctx, n, k, gather, user, cfg, approx_out, approx_cap, approx_rows, levels);
   });
 }
 

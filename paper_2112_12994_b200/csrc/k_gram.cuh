@@ -28,6 +28,7 @@ struct DenseRows {
   __device__ __forceinline__ double operator()(int64_t t, int col) const {
     return q[t * ld + col];
   }
+  __device__ __forceinline__ const double* row(int64_t t) const { return q + t * ld; }
 };
 
 constexpr int kGramThreads = 128;

@@ -271,13 +271,24 @@ struct PolarF {
 
 // ---- sketch matrices ----
 // rows of the concatenation [N | B] (N: rows x g row-major normals, B: approx rows)
-struct ConcatRows {
+template <class L>
+struct ConcatRowsT {
   const double* nm;
   int g;
-  FwdRows fr;
+  L fr;
   __device__ __forceinline__ double operator()(int64_t t, int col) const {
     return col < g ? nm[t * g + col] : fr(t, col - g);
   }
+};
+using ConcatRows = ConcatRowsT<FwdRows>;
+
+// a dense row-major matrix with one appended zero column (the rank check of a
+// reference matrix through the pivoted Cholesky, which carries a target column)
+struct DenseRowsZ {
+  const double* q;
+  int64_t ld;
+  int k;
+  __device__ __forceinline__ double operator()(int64_t t, int col) const { return col < k ? q[t * ld + col] : 0.0; }
 };
 
 // H0[i][l] = sum_{a <= l} GB[i][a] S[a][l]; GB[i][a] = Gp(i, g + a) (TPU, Kp = g + K)

@@ -54,6 +54,23 @@ int main(int argc, char** argv) {
                 (long long)drv.row_count(), (long long)s1.m, (long long)s2.m, s2.p, ssum,
                 r2.coefficients == s2.coefficients ? 1 : 0, s2.coefficients[0], s2.coefficients[1]);
   }
+  {  // Repeated Halving over a dense row source (repeated_halving.hpp:17-91)
+    const std::int64_t rows = 512, k = 6;
+    std::vector<double> a((std::size_t)(rows * k));
+    for (std::size_t i = 0; i < a.size(); ++i) a[i] = std::sin(0.37 * (double)i) + 0.01 * (double)(i % 17);
+    toepfit::DenseRowSource src(a, rows, k);
+    toepfit::RHConfig cfg;
+    cfg.base_threshold = 128;
+    cfg.sample_count = 128;
+    cfg.gaussian_rows = 48;
+    cfg.seed = 3;
+    const toepfit::SpectralApprox ap = toepfit::repeated_halving(src, cfg);
+    const std::vector<double> lev = toepfit::generalized_leverage(a, rows, a, rows, k);
+    double lsum = 0.0;
+    for (double v : lev) lsum += v;
+    std::printf("\"rowsource\": {\"levels\": %d, \"rows\": %lld, \"lev_sum\": %.17g},\n", ap.levels,
+                (long long)ap.sample_count, lsum);
+  }
   // error mapping (errors.hpp:12-29 types)
   int usage = 0, data = 0, numerical = 0;
   try {

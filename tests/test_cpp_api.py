@@ -41,6 +41,8 @@ def test_cpp_api_matches_python(tmp_path):
     bt = tf.lsar_fit_batch(s, 16, 900, [11, 12], engine=eng)
     assert res["batch0"]["taus"] == bt[0].pacf.taus and res["batch1"]["taus"] == bt[1].pacf.taus
     assert res["batch0"]["p_star"] == bt[0].p_star
+    rs = res["rowsource"]
+    assert rs["levels"] == 2 and rs["rows"] == 128 and abs(rs["lev_sum"] - 6.0) < 1e-10  # exact leverage sums to k
     drv = res["driver"]
     assert drv["rows"] == y.size - 16 and drv["m1"] == y.size - 15 and drv["m2"] == y.size - 14 and drv["p2"] == 2
     assert abs(drv["ssum2"] - 2.0) < 1e-12 and drv["replay"] == 1
