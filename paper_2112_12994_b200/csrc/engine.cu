@@ -642,13 +642,38 @@ static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, co
 }
 
 static void launch_scan(tf_context* ctx, int64_t ntile, int lag, int check_r, int unit_r = 0,
-                        const double* r_fixed = nullptr) {
-  k_lag_scan<<<1, kScanThreads, 0, ctx->stream>>>(ctx->tileA.get(), ctx->tileB.get(), ntile,
-                                                  ctx->OT.get(), ctx->scal.get(), ctx->Rhist.get(),
-                                                  ctx->Shist.get(), lag, check_r, ctx->status.get(),
-                                                  unit_r, r_fixed, ctx->guide.get());
-  LAUNCH_CHECK("k_lag_scan");
-  COUNT_LAUNCH();
+                        const double* r_fixed = nullptr, double* Rhist = (double*)1, double* Shist = (double*)1,
+                        int* status = nullptr) {
+  cudaStream_t st = ctx->stream;
+  if (Rhist == (double*)1) Rhist = ctx->Rhist.get();
+  if (Shist == (double*)1) Shist = ctx->Shist.get();
+  if (!status) status = ctx->status.get();
+  if (ntile <= kScanSingleMax) {
+    k_lag_scan<<<1, kScanThreads, 0, st>>>(ctx->tileA.get(), ctx->tileB.get(), ntile, ctx->OT.get(), ctx->scal.get(),
+                                           Rhist, Shist, lag, check_r, status, unit_r, r_fixed, ctx->guide.get());
+    LAUNCH_CHECK("k_lag_scan");
+    COUNT_LAUNCH();
+    return;
+  }
+  // long windows: the multi-CTA scan (k_scan_blocks / k_scan_mid / k_scan_ot / k_scan_guide)
+  const int64_t nb = (ntile + kScanBlk - 1) / kScanBlk;
+  ctx->scan_part.need(nb);
+  ctx->scan_boff.need(nb);
+  double* part = ctx->scan_part.get();
+  if (!r_fixed && !unit_r)
+    k_scan_blocks<<<(unsigned)nb, kScanThreads, 0, st>>>(ctx->tileA.get(), ctx->tileB.get(), ntile, ctx->scal.get(), 0,
+                                                         part);
+  k_scan_mid<<<1, kScanThreads, 0, st>>>(part, nb, 0, ctx->scal.get(), Rhist, Shist, lag, check_r, status, unit_r,
+                                         r_fixed, ctx->scan_boff.get());
+  k_scan_blocks<<<(unsigned)nb, kScanThreads, 0, st>>>(ctx->tileA.get(), ctx->tileB.get(), ntile, ctx->scal.get(), 1,
+                                                       part);
+  k_scan_mid<<<1, kScanThreads, 0, st>>>(part, nb, 1, ctx->scal.get(), Rhist, Shist, lag, check_r, status, unit_r,
+                                         r_fixed, ctx->scan_boff.get());
+  k_scan_ot<<<(unsigned)nb, kScanThreads, 0, st>>>(ctx->tileA.get(), ctx->tileB.get(), ntile, ctx->scal.get(),
+                                                   ctx->scan_boff.get(), ctx->OT.get());
+  k_scan_guide<<<(unsigned)((ntile + 255) / 256), 256, 0, st>>>(ctx->OT.get(), ntile, ctx->scal.get(), ctx->guide.get());
+  LAUNCH_CHECK("k_scan");
+  g_launches += 6;
 }
 
 static void launch_draw(tf_context* ctx, uint64_t seed, int64_t c, int64_t w, int64_t* idx,
@@ -2192,14 +2217,12 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
       k_shard_R<<<1, 1, 0, st>>>(ctx->sh_gath.get(), world, ctx->sh_par.get(), ctx->Rhist.get(), q,
                                  ctx->status.get());
       // local CDF with the global R (its total S_local lands in scal[1])
-      k_lag_scan<<<1, kScanThreads, 0, st>>>(ctx->tileA.get(), ctx->tileB.get(), ntile, ctx->OT.get(),
-                                             ctx->scal.get(), nullptr, nullptr, q, 0, ctx->sh_dummy.get(), 0,
-                                             ctx->sh_par.get(), ctx->guide.get());
+      launch_scan(ctx, ntile, q, 0, 0, ctx->sh_par.get(), nullptr, nullptr, ctx->sh_dummy.get());
       nccl_check(ncclAllGather(ctx->scal.get() + 1, ctx->sh_gath.get() + 2 * world, 1, ncclDouble, ctx->comm, st),
                  "ncclAllGather");
       k_shard_seg<<<1, 1, 0, st>>>(ctx->sh_gath.get() + 2 * world, world, rank, ctx->sh_par.get(), ctx->Shist.get(), q,
                                    ctx->status.get());
-      g_launches += 4;
+      g_launches += 3;
       DrawArgs a{};
       a.seed_ptr = ctx->seedtab.get() + p;
       a.c = c;

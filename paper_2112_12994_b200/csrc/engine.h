@@ -63,6 +63,7 @@ struct tf_context {
   // LSAR state
   tfe::DBuf<double> s, r, chunkA, chunkB, tileA, tileB, OT, scal, Rhist, Shist, phi, coefs, taus;
   tfe::DBuf<int> guide;  // draw guide table (k_lag_scan)
+  tfe::DBuf<double> scan_part, scan_boff;  // multi-CTA scan of long windows: block totals, block prefixes
   tfe::DBuf<double> srht_X, srht_D;  // SRHT: transform batch, sampled dense system
   tfe::DBuf<int64_t> srht_draws;
   tfe::DBuf<int> srht_reject;

@@ -367,6 +367,123 @@ __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
   }
 }
 
+// ---- multi-CTA version of k_lag_scan for long windows (ntile > kScanSingleMax:
+//      C4's 488k tiles took 1.3 ms in the single CTA).  Same quantities in a fixed
+//      order: R = sum tB (block sums, then the blocks in order), tile masses
+//      m_t = tA_t + tB_t / R, OT = exclusive prefix (block-local scans offset by the
+//      exclusive prefix of the block totals, each block's total being exactly the
+//      last tile's inclusive value, so OT stays nondecreasing across blocks), and
+//      the guide table from OT.
+constexpr int64_t kScanSingleMax = 16384;
+constexpr int kScanBlk = 2 * kScanThreads;  // tiles per block (2 per thread)
+
+// block-wide inclusive scan of one value per thread (fixed order); returns the
+// exclusive prefix, *tot = the block total
+__device__ __forceinline__ double block_excl_scan(double v, double* wsum, double* tot) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double inc = warp_incl_scan(v);
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const double wi = warp_incl_scan(wsum[lane]);
+    __syncwarp();
+    wsum[lane] = wi;
+  }
+  __syncthreads();
+  const double before = warp ? wsum[warp - 1] : 0.0;
+  *tot = wsum[31];
+  return before + (inc - v);
+}
+
+__device__ __forceinline__ double tile_mass(const double* tA, const double* tB, int64_t t, int64_t ntile, double R,
+                                            int massmode) {
+  if (t >= ntile) return 0.0;
+  return massmode ? tA[t] + tB[t] / R : tB[t];
+}
+
+// per-block totals: massmode 0: sum tB; 1: the scan total of the masses
+__global__ void __launch_bounds__(kScanThreads) k_scan_blocks(const double* __restrict__ tA, const double* __restrict__ tB,
+                                                              int64_t ntile, const double* __restrict__ scal,
+                                                              int massmode, double* __restrict__ part) {
+  __shared__ double wsum[32];
+  const int64_t t0 = (int64_t)blockIdx.x * kScanBlk + 2 * threadIdx.x;
+  const double R = massmode ? scal[0] : 1.0;
+  const double v0 = tile_mass(tA, tB, t0, ntile, R, massmode), v1 = tile_mass(tA, tB, t0 + 1, ntile, R, massmode);
+  double tot;
+  block_excl_scan(v0 + v1, wsum, &tot);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+// one CTA over the block totals.  mode 0: R (or the fixed / unit R) -> scal[0],
+// Rhist, the zero-residual check.  mode 1: exclusive prefix of the block totals
+// -> boff, S -> scal[1], Shist, the score checks.
+__global__ void __launch_bounds__(kScanThreads) k_scan_mid(const double* __restrict__ part, int64_t nb, int mode,
+                                                           double* scal, double* Rhist, double* Shist, int lag,
+                                                           int check_r, int* status, int unit_r,
+                                                           const double* r_fixed, double* __restrict__ boff) {
+  __shared__ double wsum[32];
+  const int tid = threadIdx.x;
+  const int64_t seg = (nb + kScanThreads - 1) / kScanThreads;
+  const int64_t b = min(nb, (int64_t)tid * seg), e = min(nb, b + seg);
+  double ss = 0.0;
+  for (int64_t i = b; i < e; ++i) ss += part[i];
+  double tot;
+  double off = block_excl_scan(ss, wsum, &tot);
+  if (mode == 0) {
+    if (tid == 0) {
+      const double R = r_fixed ? *r_fixed : (unit_r ? 1.0 : tot);
+      scal[0] = R;
+      if (Rhist) Rhist[lag] = R;
+      if (check_r && R == 0.0)
+        raise_status(status, kErrNumerical, lag + 1, lag == 0 ? kReasonZeroWindow : kReasonZeroResidual);
+      if (!(R >= 0.0)) raise_status(status, kErrUsage, lag + 1, kReasonNegativeScore);
+    }
+    return;
+  }
+  for (int64_t i = b; i < e; ++i) {
+    boff[i] = off;
+    off += part[i];
+  }
+  if (tid == 0) {
+    const double S = tot;
+    scal[1] = S;
+    if (Shist) Shist[lag + 1] = S;
+    if (!(S >= 0.0)) raise_status(status, kErrUsage, lag + 1, kReasonNegativeScore);
+    else if (S == 0.0) raise_status(status, kErrNumerical, lag + 1, kReasonZeroScoreSum);
+  }
+}
+
+// OT of every tile: the block-local exclusive scan (the same arithmetic as
+// k_scan_blocks' total) offset by the block's prefix
+__global__ void __launch_bounds__(kScanThreads) k_scan_ot(const double* __restrict__ tA, const double* __restrict__ tB,
+                                                          int64_t ntile, const double* __restrict__ scal,
+                                                          const double* __restrict__ boff, double* __restrict__ OT) {
+  __shared__ double wsum[32];
+  const int64_t t0 = (int64_t)blockIdx.x * kScanBlk + 2 * threadIdx.x;
+  const double R = scal[0];
+  const double v0 = tile_mass(tA, tB, t0, ntile, R, 1), v1 = tile_mass(tA, tB, t0 + 1, ntile, R, 1);
+  double tot;
+  const double ex = block_excl_scan(v0 + v1, wsum, &tot);
+  const double base = boff[blockIdx.x];
+  if (t0 < ntile) OT[t0] = base + ex;
+  if (t0 + 1 < ntile) OT[t0 + 1] = base + (ex + v0);
+}
+
+// guide table from OT: tile t is the first tile of buckets (bucket(OT[t-1]), bucket(OT[t])]
+__global__ void k_scan_guide(const double* __restrict__ OT, int64_t ntile, const double* __restrict__ scal,
+                             int* __restrict__ guide) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntile) return;
+  const int G = guide_buckets(ntile);
+  const double S = scal[1];
+  const double gscale = S > 0.0 ? (double)G / S : 0.0;
+  const int bt = guide_bucket(OT[t], gscale, G);
+  const int bp = t > 0 ? guide_bucket(OT[t - 1], gscale, G) : -1;
+  for (int k = bp + 1; k <= bt; ++k) guide[k] = (int)t;
+  if (t == ntile - 1)
+    for (int k = bt + 1; k <= G; ++k) guide[k] = (int)ntile;
+}
+
 // Row-sharded lag step, part 1: the allgathered (sum s, sum r^2) of every
 // shard -> the global R = ||r||^2 (lsar.cpp:17-25), summed in rank order (the
 // same arithmetic on every rank).

@@ -123,6 +123,22 @@ def test_sample_rows_matches_oracle_draws(orc, eng, n, c):
     assert (s[idx] > 0).all()
 
 
+def test_sample_rows_long_window_multi_cta_scan(orc, eng):
+    # > 16384 tiles of 2048 rows: the multi-CTA CDF scan (k_scan_blocks / k_scan_mid /
+    # k_scan_ot / k_scan_guide) -- the same draws as the reference's sequential CDF
+    n, c = 40_000_000, 20_000
+    rng = np.random.default_rng(17)
+    s = rng.exponential(size=n)
+    s[rng.integers(0, n, size=n // 50)] = 0.0
+    pi = s / s.sum()
+    idx, w = eng.sample_rows(pi, c, 99)
+    idx_r, w_r = orc.sample_rows(pi, c, 99)
+    assert np.mean(idx == idx_r) >= 0.999
+    same = idx == idx_r
+    assert np.allclose(w[same], w_r[same], rtol=1e-9)
+    assert (pi[idx] > 0).all()
+
+
 # ------------------------------------------------------------------ solve
 @pytest.mark.parametrize("p", [1, 2, 5, 31, 32, 33, 63, 64, 65, 100, 129, 200, 216, 217, 230, 300])
 def test_solve_sampled_matches_oracle(orc, eng, p):
