@@ -24,6 +24,7 @@
 #include "k_exact.cuh"
 #include "k_gen.cuh"
 #include "k_gram.cuh"
+#include "k_i8gram.cuh"
 #include "k_pass.cuh"
 #include "k_rh.cuh"
 #include "k_sample.cuh"
@@ -462,15 +463,68 @@ static void svd_plan(int p, int& nct, int& nblk, int& bw) {
   bw = std::max(1, (p + nblk - 1) / nblk);
 }
 
+// INT8 tensor-core Gram (k_i8gram.cuh) or the double-double CUDA-core one
+// (k_gram_dd): both produce the same (hi, lo) Gram to ~1e-27 relative; the
+// tensor-core path pays a fixed slicing cost, so it is taken above a work
+// threshold (c K^2, measured crossover on B200) and while the int32 products
+// are exact (c <= kI8MaxRows).
+constexpr int kI8MaxNbs = 6;  // K <= 768
+static bool use_i8_gram(const tf_context* ctx, int64_t c, int K) {
+  if (ctx->gram_mode == 1 || c > kI8MaxRows || K > kI8MaxNbs * kI8Tile) return false;
+  return ctx->gram_mode == 2 || (double)c * K * K >= kI8MinWork;
+}
+
+static void i8_tables(tf_context* ctx) {
+  SolveBufs& b = ctx->sb;
+  if (!b.i8_ntiles.empty()) return;
+  std::vector<int> tl, tof;
+  b.i8_tile_off.assign(kI8MaxNbs + 1, 0);
+  b.i8_tof_off.assign(kI8MaxNbs + 1, 0);
+  b.i8_ntiles.assign(kI8MaxNbs + 1, 0);
+  for (int nbs = 1; nbs <= kI8MaxNbs; ++nbs) {
+    const int nbt = kI8S * nbs;
+    b.i8_tile_off[nbs] = (int)tl.size() / 2;
+    b.i8_tof_off[nbs] = (int)tof.size();
+    const size_t t0 = tof.size();
+    tof.resize(t0 + (size_t)nbt * nbt, -1);
+    int cnt = 0;
+    for (int I = 0; I < nbt; ++I)
+      for (int J = I; J < nbt; ++J)
+        if (I / nbs + J / nbs <= kI8S - 1) {
+          tof[t0 + (size_t)I * nbt + J] = cnt++;
+          tl.push_back(I);
+          tl.push_back(J);
+        }
+    b.i8_ntiles[nbs] = cnt;
+  }
+  b.i8tiles.need(tl.size());
+  b.i8tof.need(tof.size());
+  CK(cudaMemcpy(b.i8tiles.get(), tl.data(), tl.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b.i8tof.get(), tof.data(), tof.size() * sizeof(int), cudaMemcpyHostToDevice));
+}
+
 static void reserve_exact(tf_context* ctx, int64_t c, int Kmax) {
   SolveBufs& b = ctx->sb;
   size_t wmax = 0;
+  int ki8 = 0;
   for (int K = 2; K <= Kmax; ++K) {
+    if (use_i8_gram(ctx, c, K)) {
+      ki8 = K;
+      continue;
+    }
     const GramDDPlan g = gram_dd_plan(c, K, ctx->sm_count);
     wmax = std::max(wmax, (size_t)g.npair * g.nsplit * 8192);
   }
   const size_t KK = (size_t)Kmax * Kmax;
-  b.Wdd.need(wmax);
+  if (wmax) b.Wdd.need(wmax);
+  if (ki8) {
+    i8_tables(ctx);
+    const int nbs = (ki8 + kI8Tile - 1) / kI8Tile;
+    const int64_t cpad = (c + kI8Tile - 1) / kI8Tile * kI8Tile;
+    b.i8D.need((size_t)kI8S * nbs * kI8Tile * cpad);
+    b.i8E.need((size_t)nbs * kI8Tile);
+    b.i8P.need((size_t)b.i8_ntiles[nbs] * kI8Tile * kI8Tile);
+  }
   b.Gh.need(KK);
   b.Gl.need(KK);
   b.Rh.need(KK);
@@ -496,23 +550,41 @@ static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev,
   cudaStream_t st = ctx->stream;
   const int p = K - 1;
   if (p > kExactMaxP) throw TfError{TF_USAGE, "lag order above " + std::to_string(kExactMaxP) + " (rank-revealing solve)"};
-  const GramDDPlan g = gram_dd_plan(c, K, ctx->sm_count);
-  {  // column sums of squares: the accumulation bias of each Gram element
-    const unsigned ns = (unsigned)((c + kCnRows - 1) / kCnRows);
-    k_colnorm2_part<L><<<dim3((unsigned)((K + 63) / 64), ns), 256, 0, st>>>(ld, c, K, rows_dev, b.cnp.get());
-    k_colnorm2_sum<<<(unsigned)((K + 127) / 128), 128, 0, st>>>(b.cnp.get(), (int)ns, K, b.cn.get());
-    LAUNCH_CHECK("k_colnorm2");
-    g_launches += 2;
-  }
-  k_gram_dd<L><<<dim3((unsigned)g.npair, (unsigned)g.nsplit), kDDThreads, 0, st>>>(ld, c, K, g.nblk, g.rps, g.nsplit,
-                                                                                  b.Wdd.get(), rows_dev, b.cn.get());
-  LAUNCH_CHECK("k_gram_dd");
   const int64_t KK = (int64_t)K * K;
   double* gh = sharded ? b.Gloc.get() : b.Gh.get();
   double* gl = sharded ? b.Gloc.get() + KK : b.Gl.get();
-  k_gram_dd_reduce<<<(unsigned)(((int64_t)g.npair * 4096 + 255) / 256), 256, 0, st>>>(
-      b.Wdd.get(), g.npair, g.nsplit, g.nblk, K, gh, gl, nullptr);
-  LAUNCH_CHECK("k_gram_dd_reduce");
+  const unsigned ns = (unsigned)((c + kCnRows - 1) / kCnRows);
+  if (use_i8_gram(ctx, c, K)) {
+    const int nbs = (K + kI8Tile - 1) / kI8Tile, Kp = nbs * kI8Tile;
+    const int64_t nk = (c + kI8Tile - 1) / kI8Tile;
+    k_i8_colmax_part<L><<<dim3((unsigned)((K + 63) / 64), ns), 256, 0, st>>>(ld, c, K, rows_dev, b.cnp.get());
+    k_i8_colmax_fin<<<(unsigned)((K + 127) / 128), 128, 0, st>>>(b.cnp.get(), (int)ns, K, b.i8E.get());
+    k_i8_slice<L><<<dim3((unsigned)nk, (unsigned)(Kp / 32)), 256, 0, st>>>(ld, c, K, Kp, nk, rows_dev, b.i8E.get(),
+                                                                           (int8_t*)b.i8D.get());
+    LAUNCH_CHECK("k_i8_slice");
+    smem_optin((const void*)k_i8_gemm, kI8Smem);
+    k_i8_gemm<<<(unsigned)b.i8_ntiles[nbs], kI8Threads, kI8Smem, st>>>(
+        (const int8_t*)b.i8D.get(), nk, reinterpret_cast<const int2*>(b.i8tiles.get()) + b.i8_tile_off[nbs],
+        b.i8P.get());
+    LAUNCH_CHECK("k_i8_gemm");
+    k_i8_combine<<<(unsigned)((KK + 255) / 256), 256, 0, st>>>(b.i8P.get(), b.i8tof.get() + b.i8_tof_off[nbs],
+                                                              kI8S * nbs, K, Kp, b.i8E.get(), gh, gl);
+    LAUNCH_CHECK("k_i8_combine");
+    g_launches += 5;
+  } else {
+    const GramDDPlan g = gram_dd_plan(c, K, ctx->sm_count);
+    // column sums of squares: the accumulation bias of each Gram element
+    k_colnorm2_part<L><<<dim3((unsigned)((K + 63) / 64), ns), 256, 0, st>>>(ld, c, K, rows_dev, b.cnp.get());
+    k_colnorm2_sum<<<(unsigned)((K + 127) / 128), 128, 0, st>>>(b.cnp.get(), (int)ns, K, b.cn.get());
+    LAUNCH_CHECK("k_colnorm2");
+    k_gram_dd<L><<<dim3((unsigned)g.npair, (unsigned)g.nsplit), kDDThreads, 0, st>>>(ld, c, K, g.nblk, g.rps, g.nsplit,
+                                                                                    b.Wdd.get(), rows_dev, b.cn.get());
+    LAUNCH_CHECK("k_gram_dd");
+    k_gram_dd_reduce<<<(unsigned)(((int64_t)g.npair * 4096 + 255) / 256), 256, 0, st>>>(
+        b.Wdd.get(), g.npair, g.nsplit, g.nblk, K, gh, gl, nullptr);
+    LAUNCH_CHECK("k_gram_dd_reduce");
+    g_launches += 4;
+  }
   if (sharded) {
     nccl_check(ncclAllGather(b.Gloc.get(), b.Gg.get(), (size_t)(2 * KK), ncclDouble, ctx->comm, st), "ncclAllGather");
     k_dd_sum_ranks<<<(unsigned)((KK + 255) / 256), 256, 0, st>>>(b.Gg.get(), ctx->nc_world, KK, b.Gh.get(), b.Gl.get());
@@ -589,7 +661,7 @@ static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev,
   cfg.attrs = at;
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, k_svd_minnorm, sa));
-  g_launches += 4;
+  g_launches += 2;
 }
 
 // ---------------------------------------------------------------------------
@@ -2659,6 +2731,8 @@ tf_status tf_create(const tf_opts* opts, tf_context** out) {
   {
     const char* v = std::getenv("TF_NO_GRAPHS");  // debugging: launch every sweep eagerly
     ctx->no_graphs = v && v[0] == '1';
+    const char* gm = std::getenv("TF_GRAM");  // "dd" / "i8": force one Gram path (parity tests, benchmarks)
+    ctx->gram_mode = gm && !std::strcmp(gm, "dd") ? 1 : gm && !std::strcmp(gm, "i8") ? 2 : 0;
   }
   int least = 0, greatest = 0;
   cudaDeviceGetStreamPriorityRange(&least, &greatest);

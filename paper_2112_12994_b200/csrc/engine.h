@@ -47,6 +47,11 @@ struct SolveBufs {
   DBuf<double> Wdd, Gh, Gl, Rh, Rl, Dd, Nsv, sig, xpart, tolv, cn, cnp;
   DBuf<double> Gloc, Gg;  // row-sharded sweeps: this shard's Gram partial [2][K*K], the allgathered partials
   DBuf<int> perm, svdf;
+  // INT8 tensor-core Gram (k_i8gram.cuh): pre-tiled digit planes, column
+  // exponents, int32 product tiles, the tile lists of every plane width
+  DBuf<unsigned char> i8D;
+  DBuf<int> i8E, i8P, i8tiles, i8tof;
+  std::vector<int> i8_tile_off, i8_tof_off, i8_ntiles;  // per nbs (host copies of the table layout)
 };
 
 }  // namespace tfe
@@ -96,6 +101,7 @@ struct tf_context {
   tfe::GraphCache lsar_graph, rh_graph;
   tfe::DBuf<uint64_t> seedtab;
   bool no_graphs = false;
+  int gram_mode = 0;  // 0 auto (INT8 tensor-core Gram above a work threshold), 1 double-double CUDA cores, 2 INT8 whenever c fits
   std::vector<cudaEvent_t> events;
   std::vector<cudaEvent_t> pev;  // phase events (2 per lag)
   int64_t launches = 0;

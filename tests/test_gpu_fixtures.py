@@ -10,6 +10,10 @@ orc_rh_replay (its own recursion fed with the stored coefficients; checked
 against per-lag SHA-256 digests) and fed, with the oracle's weights, to the
 GPU sweep through the C ABI.
 
+Each fixture runs on the size-chosen Gram path and, where marked, forced
+onto the INT8 tensor-core Gram (TF_GRAM=i8) or the double-double CUDA-core
+Gram (TF_GRAM=dd): both paths must clear the same bars.
+
 Bars (BASELINE.json north_star):
   * the per-lag solve method (CPQR exact_qr vs min-norm exact_svd) and the
     CPQR rank are identical to the oracle's (toeplitz.cpp:57-85);
@@ -130,8 +134,28 @@ def report(name, lines):
     print("\n".join(lines[-12:]))
 
 
-@pytest.mark.parametrize("name", ["c1_lsar", "c2_lsar", "c4s_lsar"])
-def test_lsar_baseline_fixture(orc, tf, eng, name):
+def engine_for(tf, eng, gram, monkeypatch):
+    """The module engine (Gram path chosen by size: INT8 tensor cores above the
+    work threshold), or a fresh one forced onto one Gram path (TF_GRAM is read
+    at context creation)."""
+    if gram == "auto":
+        return eng, False
+    monkeypatch.setenv("TF_GRAM", gram)
+    return tf.Engine(0), True
+
+
+@pytest.mark.parametrize("name,gram", [("c1_lsar", "auto"), ("c1_lsar", "i8"), ("c2_lsar", "auto"), ("c2_lsar", "i8"),
+                                       ("c2_lsar", "dd"), ("c4s_lsar", "auto"), ("c4s_lsar", "dd")])
+def test_lsar_baseline_fixture(orc, tf, eng, name, gram, monkeypatch):
+    eng, own = engine_for(tf, eng, gram, monkeypatch)
+    try:
+        _lsar_fixture(orc, tf, eng, name)
+    finally:
+        if own:
+            eng.close()
+
+
+def _lsar_fixture(orc, tf, eng, name):
     fx = mf.load(name)
     m = fx["meta"]
     pb, c, seed = m["p_bar"], m["c"], m["fit_seed"]
@@ -156,8 +180,18 @@ def test_lsar_baseline_fixture(orc, tf, eng, name):
     report(name, lines)
 
 
-@pytest.mark.parametrize("name", ["rh_g129", "rh_g65", "c2_rh"])
-def test_rh_baseline_fixture(orc, tf, eng, name):
+@pytest.mark.parametrize("name,gram", [("rh_g129", "auto"), ("rh_g65", "auto"), ("rh_g65", "i8"), ("c2_rh", "auto"),
+                                       ("c2_rh", "i8")])
+def test_rh_baseline_fixture(orc, tf, eng, name, gram, monkeypatch):
+    eng, own = engine_for(tf, eng, gram, monkeypatch)
+    try:
+        _rh_fixture(orc, tf, eng, name)
+    finally:
+        if own:
+            eng.close()
+
+
+def _rh_fixture(orc, tf, eng, name):
     fx = mf.load(name)
     m = fx["meta"]
     pb, c, seed = m["p_bar"], m["c"], m["fit_seed"]
