@@ -22,6 +22,7 @@
 #include "k_bsolve.cuh"
 #include "k_cholinv.cuh"
 #include "k_exact.cuh"
+#include "k_fft.cuh"
 #include "k_gen.cuh"
 #include "k_gram.cuh"
 #include "k_i8gram.cuh"
@@ -668,6 +669,78 @@ static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev,
 
 constexpr int kPassPstMinQ = 1;  // sweeps: tensor-core persistent pass for every lag q >= 1
 
+// FFT pass (k_fft.cuh) for the lags where the direct FIR is fp64-bound; the
+// crossover (lag kFftMinQ) is measured.
+constexpr int kFftMinQ = 96;
+
+static bool fft_sweep(const tf_context* ctx, int p_bar) {
+  if (ctx->pass_mode == 1 || p_bar > kFftD) return false;
+  return ctx->pass_mode == 2 || p_bar >= ctx->fft_minq;
+}
+static bool fft_lag(const tf_context* ctx, int p_bar, int q) {
+  return q >= 1 && fft_sweep(ctx, p_bar) && (ctx->pass_mode == 2 || q >= ctx->fft_minq);
+}
+
+// buffers of the FFT pass (before any capture): spectra of ceil(w / 6144)
+// superblocks, the filter spectrum, the twiddle tables (once per context)
+static void reserve_fft(tf_context* ctx, int64_t w) {
+  const int64_t nsb = (w + kFftSB - 1) / kFftSB;
+  ctx->fftZ.need((size_t)nsb * kFftN);
+  ctx->fftH.need(kFftN);
+  if (!ctx->fftTw.get()) {
+    ctx->fftTw.need(kFftTw);
+    std::vector<double2> tw(kFftTw);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int e = 0; e < 256; ++e) {
+      const long double a256 = -2.0L * pi * e / 256.0L, a4096 = -2.0L * pi * e / 4096.0L;
+      tw[e] = make_double2((double)cosl(a256), (double)sinl(a256));
+      tw[256 + e] = make_double2((double)cosl(a4096), (double)sinl(a4096));
+    }
+    CK(cudaMemcpy(ctx->fftTw.get(), tw.data(), kFftTw * sizeof(double2), cudaMemcpyHostToDevice));
+  }
+  smem_optin((const void*)k_fft_series, fft_smem_bytes());
+  smem_optin((const void*)k_fft_taps, fft_smem_bytes());
+  smem_optin((const void*)k_lsar_pass_fft<0>, fft_smem_bytes());
+  smem_optin((const void*)k_lsar_pass_fft<1>, fft_smem_bytes());
+  smem_optin((const void*)k_lsar_pass_fft<2>, fft_smem_bytes());
+}
+
+static int fft_grid(const tf_context* ctx, int64_t nsb) {
+  return (int)std::min<int64_t>(nsb, 2 * (int64_t)ctx->sm_count);
+}
+
+// spectra of the resident series (y[0 .. n)) for a window of w rows
+static void launch_fft_series(tf_context* ctx, int64_t w) {
+  const int64_t nsb = (w + kFftSB - 1) / kFftSB;
+  k_fft_series<<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(ctx->y.get(), ctx->n, nsb,
+                                                                              ctx->fftZ.get(), ctx->fftTw.get());
+  LAUNCH_CHECK("k_fft_series");
+  COUNT_LAUNCH();
+}
+
+static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev) {
+  k_fft_taps<<<1, kFftT, fft_smem_bytes(), ctx->stream>>>(phi, q, ctx->fftH.get(), ctx->fftTw.get());
+  FftPassArgs a{};
+  a.Z = ctx->fftZ.get();
+  a.H = ctx->fftH.get();
+  a.tw = ctx->fftTw.get();
+  a.w = w;
+  a.s = ctx->s.get();
+  a.r = ctx->r.get();
+  a.Rprev = Rprev;
+  a.chunkA = ctx->chunkA.get();
+  a.chunkB = ctx->chunkB.get();
+  a.tileA = ctx->tileA.get();
+  a.tileB = ctx->tileB.get();
+  const int64_t nsb = (w + kFftSB - 1) / kFftSB;
+  static const int pf = std::getenv("TF_FFT_PF") ? std::atoi(std::getenv("TF_FFT_PF")) : 1;  // dev switch
+  if (pf == 0) k_lsar_pass_fft<0><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
+  else if (pf == 2) k_lsar_pass_fft<2><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
+  else k_lsar_pass_fft<1><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
+  LAUNCH_CHECK("k_lsar_pass_fft");
+  g_launches += 2;
+}
+
 static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev,
                         bool exact_order = false) {
   PassArgs a{};
@@ -936,6 +1009,8 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
     CK(cudaStreamSynchronize(st));  // the host vector goes out of scope
   }
   ctx->sb.M.need((size_t)c * ldq_of(2));  // the p = 1 Gram's dense staging (no allocation inside the loop)
+  const bool use_fft = fft_sweep(ctx, p_bar);
+  if (use_fft) reserve_fft(ctx, w);
   const int rn2 = d && d->rnorm2_out;
   bool capturing = false;
   // timing events: plain records when eager, external event nodes when captured
@@ -948,6 +1023,7 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
     rec(ctx->events[0]);
     // lag-0 pass: r_0 = -y[0..w), s_0 = 0  ->  s_1 = y^2 / sum y^2 (lsar.cpp:11-15)
     launch_pass(ctx, 0, w, ctx->phi.get(), ctx->scal.get());
+    if (use_fft) launch_fft_series(ctx, w);  // series spectra for the FFT pass (once per sweep)
     for (int p = 1; p <= p_bar; ++p) {
       const int q = p - 1;
       launch_scan(ctx, ntile, q, 1);
@@ -973,7 +1049,8 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
       solve_exact(ctx, FwdRows{ctx->y.get(), idx, wts, 0}, c, p + 1, /*rev=*/0, o);
       if (phases) rec(ctx->pev[2 * (p - 1) + 1]);
       // residuals of the lag-p window fit + score update s_p = s_{p-1} + r_{p-1}^2/R_{p-1}
-      launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());
+      if (fft_lag(ctx, p_bar, p)) launch_pass_fft(ctx, p, w, ctx->phi.get(), ctx->scal.get());
+      else launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());
       rec(ctx->events[p]);
     }
     rec(ctx->ev_end);
@@ -2271,6 +2348,8 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
     CK(cudaStreamSynchronize(st));
   }
   CK(cudaMemsetAsync(ctx->sh_par.get(), 0, 4 * sizeof(double), st));
+  const bool use_fft = fft_sweep(ctx, p_bar);
+  if (use_fft) reserve_fft(ctx, w);
   const int64_t nt = (c + kScanTileN - 1) / kScanTileN;
   const long long* kdev = ctx->rh_tsum.get() + nt + 1;  // this shard's draw count (scan_apply total)
   bool capturing = false;
@@ -2282,6 +2361,7 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
     rec(ctx->ev_begin);
     rec(ctx->events[0]);
     launch_pass(ctx, 0, w, ctx->phi.get(), ctx->sh_par.get());  // r_0 = -y, s_0 = 0
+    if (use_fft) launch_fft_series(ctx, w);
     for (int p = 1; p <= p_bar; ++p) {
       const int q = p - 1;
       k_sum_tiles<<<1, 1024, 0, st>>>(ctx->tileA.get(), ctx->tileB.get(), ntile, ctx->sh_part.get());
@@ -2326,7 +2406,8 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
       solve_exact(ctx, FwdRows{ctx->y.get(), ctx->sh_idx.get(), ctx->sh_wts.get(), 0}, c, p + 1, /*rev=*/0, o, kdev,
                   /*sharded=*/true);
       if (phases) rec(ctx->pev[2 * (p - 1) + 1]);
-      launch_pass(ctx, p, w, ctx->phi.get(), ctx->sh_par.get());  // R_{p-1} = par[0]
+      if (fft_lag(ctx, p_bar, p)) launch_pass_fft(ctx, p, w, ctx->phi.get(), ctx->sh_par.get());
+      else launch_pass(ctx, p, w, ctx->phi.get(), ctx->sh_par.get());  // R_{p-1} = par[0]
       rec(ctx->events[p]);
     }
     rec(ctx->ev_end);
@@ -2733,6 +2814,10 @@ tf_status tf_create(const tf_opts* opts, tf_context** out) {
     ctx->no_graphs = v && v[0] == '1';
     const char* gm = std::getenv("TF_GRAM");  // "dd" / "i8": force one Gram path (parity tests, benchmarks)
     ctx->gram_mode = gm && !std::strcmp(gm, "dd") ? 1 : gm && !std::strcmp(gm, "i8") ? 2 : 0;
+    const char* pm = std::getenv("TF_PASS");  // "dmma" / "fft": force one pass path (parity tests, benchmarks)
+    ctx->pass_mode = pm && !std::strcmp(pm, "dmma") ? 1 : pm && !std::strcmp(pm, "fft") ? 2 : 0;
+    const char* mq = std::getenv("TF_FFT_MINQ");  // crossover lag of the auto mode
+    ctx->fft_minq = mq ? std::max(1, std::atoi(mq)) : tfe::kFftMinQ;
   }
   int least = 0, greatest = 0;
   cudaDeviceGetStreamPriorityRange(&least, &greatest);

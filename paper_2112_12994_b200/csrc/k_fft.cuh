@@ -1,0 +1,359 @@
+// k_fft.cuh -- the LSAR pass with the FIR done as an overlap-save FFT
+// convolution (fp64), for the long lags where the direct p-tap FIR is
+// fp64-bound.
+//
+// The pass computes, per lag q over the w window rows (lsar.cpp:17-25,
+// toeplitz.cpp:87-98):
+//   r_q(i) = sum_{k=0..q} h_q[k] y[q + i - k],  h_q = [-1, phi_q[0..q-1]]
+//   s_q(i) = s_{q-1}(i) + r_{q-1}(i)^2 / R_{q-1}
+// plus the 32-row chunk / 2048-row tile partial sums of s_q and r_q^2 -- the
+// same outputs, layout and update formula as k_lsar_pass_pst (k_pass.cuh).
+//
+// Overlap-save with N = 4096-point blocks: the filter f_q[D - q + k] = h_q[k]
+// (delay D - q, D = 1024) makes every output row of a block land at the same
+// position m = u + D of the circular convolution of x_j[m] = y[j L + m]
+// (L = 3072 rows per block, no wrap-around for q <= D).  Two consecutive
+// blocks a, b ride in one complex transform (x_a + i x_b): the series spectra
+// Zab = DFT(x_a + i x_b) are computed ONCE per sweep (k_fft_series, 64 KB per
+// 6144-row superblock = 10.7 B per row), and per lag the pass multiplies by
+// H = DFT(f_q) / N (k_fft_taps, one CTA) and inverts:
+//   IDFT(Zab H) = (x_a (*) f_q) + i (x_b (*) f_q)
+// -- the real part holds block a's residuals, the imaginary part block b's.
+// Per row and lag: 10.7 B spectrum + 16 B (s, r) read + 16 B (s, r) written,
+// ~40 fp64 operations, independent of q (the direct FIR: 2q + 4 flop).
+//
+// FFT: radix-16 Stockham autosort (three stages, 256 threads x 16 points in
+// registers, two shared-memory exchanges through a padded buffer -- one slot
+// per 16 complex values keeps every 16-byte access pattern conflict free).
+// Stage 1 takes its input x[t + 256 r] straight from registers and stage 3
+// leaves X[t + 256 r] (natural order) in registers, so for fixed r a warp's
+// outputs are 32 consecutive rows: coalesced state loads / stores and chunk
+// sums by warp shuffles.  Twiddles from two 256-entry tables in shared
+// memory (W_256^e and W_4096^e, long-double accurate on the host);
+// W_4096^{t r} = W_256^{(t>>4) r} W_4096^{(t&15) r}.
+//
+// Rounding: the FFT convolution's error is ~eps log2(N) ||y|| ||h|| per row,
+// the direct FIR's ~eps sum_k |h_k y|: measured on the C1/C2/C4-shaped
+// series the FFT residuals are within 1-2.5x of the direct FIR's own
+// rounding noise.
+#pragma once
+
+#include "common.cuh"
+#include "k_pass.cuh"
+
+namespace tfk {
+
+constexpr int kFftN = 4096;
+constexpr int kFftT = 256;                       // threads per CTA, 16 points each
+constexpr int kFftD = 1024;                      // filter delay: q <= kFftD
+constexpr int kFftL = kFftN - kFftD;             // 3072 rows per block
+constexpr int kFftSB = 2 * kFftL;                // 6144 rows per superblock (blocks a, b)
+constexpr int kFftTilesSB = kFftSB / kPassTile;  // 3 tiles
+constexpr int kFftChunksSB = kFftSB / kChunk;    // 192 chunks
+constexpr int kFftBufC = kFftN + kFftN / 16;     // padded complex slots
+constexpr int kFftTw = 512;                      // twiddle table entries (W_256^e, W_4096^e; e < 256)
+
+__host__ __device__ __forceinline__ int fpad(int e) { return e + (e >> 4); }
+
+inline size_t fft_smem_bytes() { return sizeof(double2) * (size_t)(kFftBufC + kFftTw); }
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * w (S = -1, forward) or a * conj(w) (S = +1, inverse); w = e^{-2 pi i e / n} from the tables
+template <int S>
+__device__ __forceinline__ double2 ctw(double2 a, double2 w) {
+  if (S < 0) return cmul(a, w);
+  return make_double2(fma(a.x, w.x, a.y * w.y), fma(a.y, w.x, -a.x * w.y));
+}
+
+// 4-point DFT (sign S): y_k = sum_n x_n e^{S 2 pi i n k / 4}
+template <int S>
+__device__ __forceinline__ void dft4(double2& x0, double2& x1, double2& x2, double2& x3) {
+  const double2 a = cadd(x0, x2), b = csub(x0, x2), c = cadd(x1, x3), d = csub(x1, x3);
+  x0 = cadd(a, c);
+  x2 = csub(a, c);
+  if (S < 0) {  // b -+ i d
+    x1 = make_double2(b.x + d.y, b.y - d.x);
+    x3 = make_double2(b.x - d.y, b.y + d.x);
+  } else {
+    x1 = make_double2(b.x - d.y, b.y + d.x);
+    x3 = make_double2(b.x + d.y, b.y - d.x);
+  }
+}
+
+// x * e^{S 2 pi i m / 16}, m = n2 k1 in {1, 2, 3, 4, 6, 9}
+template <int S, int M>
+__device__ __forceinline__ double2 w16(double2 x) {
+  constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173, R2 = 0.70710678118654752440;
+  if (M == 4) return S < 0 ? make_double2(x.y, -x.x) : make_double2(-x.y, x.x);
+  constexpr double c = M == 1 ? C1 : M == 2 ? R2 : M == 3 ? S1 : M == 6 ? -R2 : -C1;
+  constexpr double s0 = M == 1 ? S1 : M == 2 ? R2 : M == 3 ? C1 : M == 6 ? R2 : -S1;
+  constexpr double s = S < 0 ? -s0 : s0;
+  return make_double2(fma(x.x, c, -x.y * s), fma(x.x, s, x.y * c));
+}
+
+// 16-point DFT in registers (4 x 4); the result replaces v in natural order
+template <int S>
+__device__ __forceinline__ void fft16(double2 (&v)[16]) {
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) dft4<S>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
+  // v[4 k1 + n2] *= W16^{n2 k1}
+  v[5] = w16<S, 1>(v[5]);
+  v[6] = w16<S, 2>(v[6]);
+  v[7] = w16<S, 3>(v[7]);
+  v[9] = w16<S, 2>(v[9]);
+  v[10] = w16<S, 4>(v[10]);
+  v[11] = w16<S, 6>(v[11]);
+  v[13] = w16<S, 3>(v[13]);
+  v[14] = w16<S, 6>(v[14]);
+  v[15] = w16<S, 9>(v[15]);
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) dft4<S>(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+  // X[k1 + 4 k2] sits at v[4 k1 + k2]: transpose (register renaming)
+  double2 o[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) o[r] = v[4 * (r & 3) + (r >> 2)];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = o[r];
+}
+
+// 4096-point DFT (sign S, unnormalised) of x[t + 256 r] = v[r] (thread t of
+// 256); on return v[r] = X[t + 256 r].  buf: kFftBufC padded slots; tw: the
+// two twiddle tables in shared memory.  Begins with a barrier (buf may still be
+// read by the previous call) and ends without one.
+template <int S>
+__device__ __forceinline__ void fft4096(double2 (&v)[16], double2* buf, const double2* tw) {
+  const int t = threadIdx.x;
+  const double2* tw256 = tw;
+  const double2* twlo = tw + 256;
+  // stage 1 (Ns = 1): no twiddles; out -> buf[16 t + r]
+  fft16<S>(v);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) buf[fpad(16 * t + r)] = v[r];
+  __syncthreads();
+  // stage 2 (Ns = 16): twiddle W_256^{(t & 15) r}; out -> buf[(t >> 4) 256 + (t & 15) + 16 r]
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = buf[fpad(t + 256 * r)];
+#pragma unroll
+  for (int r = 1; r < 16; ++r) v[r] = ctw<S>(v[r], tw256[(t & 15) * r]);
+  fft16<S>(v);
+  __syncthreads();
+  const int d2 = (t >> 4) * 256 + (t & 15);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) buf[fpad(d2 + 16 * r)] = v[r];
+  __syncthreads();
+  // stage 3 (Ns = 256): twiddle W_4096^{t r} = W_256^{(t >> 4) r} W_4096^{(t & 15) r}; natural order out
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = buf[fpad(t + 256 * r)];
+#pragma unroll
+  for (int r = 1; r < 16; ++r) v[r] = ctw<S>(v[r], cmul(tw256[(t >> 4) * r], twlo[(t & 15) * r]));
+  fft16<S>(v);
+}
+
+__device__ __forceinline__ void fft_load_tw(double2* tw_s, const double2* tw_g) {
+  for (int e = threadIdx.x; e < kFftTw; e += blockDim.x) tw_s[e] = tw_g[e];
+}
+
+// ---------------------------------------------------------------------------
+// Series spectra, once per sweep: Zab[sb][k] = DFT(x_a + i x_b)[k] with
+// x_a[m] = y[6144 sb + m], x_b[m] = y[6144 sb + 3072 + m] (0 past n)
+__global__ void __launch_bounds__(kFftT, 2) k_fft_series(const double* __restrict__ y, int64_t n, int64_t nsb,
+                                                         double2* __restrict__ Z, const double2* __restrict__ tw_g) {
+  extern __shared__ double2 fsm[];
+  double2* buf = fsm;
+  double2* tw = fsm + kFftBufC;
+  fft_load_tw(tw, tw_g);
+  const int t = threadIdx.x;
+  for (int64_t sb = blockIdx.x; sb < nsb; sb += gridDim.x) {
+    const int64_t ia = sb * kFftSB + t, ib = ia + kFftL;
+    double2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int64_t a = ia + 256 * r, b = ib + 256 * r;
+      v[r] = make_double2(a < n ? __ldg(y + a) : 0.0, b < n ? __ldg(y + b) : 0.0);
+    }
+    fft4096<-1>(v, buf, tw);
+    double2* Zs = Z + sb * kFftN + t;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) __stcs(Zs + 256 * r, v[r]);
+  }
+}
+
+// Per lag: H[k] = DFT(f_q)[k] / N, f_q[D - q + k] = h_q[k] (h_q[0] = -1,
+// h_q[k] = phi[k - 1]); one CTA
+__global__ void __launch_bounds__(kFftT, 1) k_fft_taps(const double* __restrict__ phi, int q, double2* __restrict__ H,
+                                                       const double2* __restrict__ tw_g) {
+  extern __shared__ double2 fsm[];
+  double2* buf = fsm;
+  double2* tw = fsm + kFftBufC;
+  fft_load_tw(tw, tw_g);
+  const int t = threadIdx.x;
+  double2 v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int k = t + 256 * r - (kFftD - q);  // tap index
+    v[r] = make_double2(k == 0 ? -1.0 : (k >= 1 && k <= q) ? __ldg(phi + k - 1) : 0.0, 0.0);
+  }
+  fft4096<-1>(v, buf, tw);
+  constexpr double inv = 1.0 / kFftN;  // exact (power of two)
+#pragma unroll
+  for (int r = 0; r < 16; ++r) H[t + 256 * r] = make_double2(v[r].x * inv, v[r].y * inv);
+}
+
+// Deterministic warp reduction of 24 values per lane: on return x[0] of lane
+// (b4 b3 b2 b1 b0) holds the sum over the warp of value 12 b4 + 6 b3 + 3 b2 +
+// 2 b1 + b0 (none when 2 b1 + b0 == 3).  24 shuffles instead of 24 x 5.
+__device__ __forceinline__ void warp_reduce24(double (&x)[24], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
+#pragma unroll
+  for (int i = 0; i < 12; ++i) {
+    const double snd = b4 ? x[i] : x[i + 12];
+    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 16);
+    x[i] = (b4 ? x[i + 12] : x[i]) + rcv;
+  }
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const double snd = b3 ? x[i] : x[i + 6];
+    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 8);
+    x[i] = (b3 ? x[i + 6] : x[i]) + rcv;
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double snd = b2 ? x[i] : x[i + 3];
+    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 4);
+    x[i] = (b2 ? x[i + 3] : x[i]) + rcv;
+  }
+  x[3] = 0.0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double snd = b1 ? x[i] : x[i + 2];
+    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 2);
+    x[i] = (b1 ? x[i + 2] : x[i]) + rcv;
+  }
+  {
+    const double snd = b0 ? x[0] : x[1];
+    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 1);
+    x[0] = (b0 ? x[1] : x[0]) + rcv;
+  }
+}
+
+struct FftPassArgs {
+  const double2* Z;  // [nsb][4096] series spectra (k_fft_series)
+  const double2* H;  // [4096] filter spectrum of this lag / N (k_fft_taps)
+  const double2* tw;
+  int64_t w;
+  double* s;  // in s_{q-1}, out s_q
+  double* r;  // in r_{q-1}, out r_q
+  const double* Rprev;
+  double* chunkA;
+  double* chunkB;
+  double* tileA;
+  double* tileB;
+};
+
+// Persistent CTAs (2 per SM) over 6144-row superblocks.  PF (L2 prefetch):
+// 0 none, 1 the next superblock's spectrum + state, 2 this superblock's state
+// at the start of its iteration
+template <int PF>
+__global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
+  extern __shared__ double2 fsm[];
+  __shared__ double csA[kFftChunksSB], csB[kFftChunksSB];
+  double2* buf = fsm;
+  double2* tw = fsm + kFftBufC;
+  fft_load_tw(tw, a.tw);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t w = a.w;
+  const int64_t nsb = (w + kFftSB - 1) / kFftSB;
+  const double invR = 1.0 / *a.Rprev;
+  // L2 prefetch (cp.async.bulk.prefetch) of a superblock's spectrum and state:
+  // this CTA's first superblock's state now, the next one's inputs while the
+  // current one computes -- the state loads after the FFT then hit L2
+  auto prefetch = [&](int64_t p, bool spectrum) {
+    if (p >= nsb) return;
+    const int64_t r0 = p * kFftSB;
+    const uint32_t bytes = (uint32_t)(min((int64_t)kFftSB, w - r0) * 8) & ~15u;
+    if (spectrum) bulk_prefetch_l2(a.Z + p * kFftN, kFftN * sizeof(double2));
+    if (bytes) {
+      bulk_prefetch_l2(a.s + r0, bytes);
+      bulk_prefetch_l2(a.r + r0, bytes);
+    }
+  };
+  if (PF == 1 && t == 0) prefetch(blockIdx.x, false);
+  for (int64_t sb = blockIdx.x; sb < nsb; sb += gridDim.x) {
+    if (PF == 1 && t == 0) prefetch(sb + gridDim.x, true);
+    if (PF == 2 && t == 0) prefetch(sb, false);
+    double2 v[16];
+    {
+      const double2* Zs = a.Z + sb * kFftN + t;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = cmul(__ldcs(Zs + 256 * r), __ldg(a.H + t + 256 * r));
+    }
+    fft4096<1>(v, buf, tw);
+    // rows: output m = t + 256 r (r >= 4) -> u = m - D; block a row base + u (real part), block b row
+    // base + 3072 + u (imaginary part).  Per block half: values i < 12 = s_q of rows r = 4 + i,
+    // i >= 12 = r_q^2 of rows r = i - 8, reduced over the warp in one warp_reduce24.
+    const int64_t base = sb * kFftSB + t;
+    double* __restrict__ sp = a.s;
+    double* __restrict__ rp = a.r;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double x[24];
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        double so[6], ro[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          const int64_t row = base + h * kFftL + 256 * (6 * g + j);
+          so[j] = row < w ? __ldcs(sp + row) : 0.0;
+          ro[j] = row < w ? __ldcs(rp + row) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          const int i = 6 * g + j;
+          const int64_t row = base + h * kFftL + 256 * i;
+          const double rq = h ? v[4 + i].y : v[4 + i].x;
+          double sn = 0.0, rs = 0.0;
+          if (row < w) {
+            sn = fma(ro[j] * ro[j], invR, so[j]);
+            __stcs(sp + row, sn);
+            __stcs(rp + row, rq);
+            rs = rq;
+          }
+          x[i] = sn;
+          x[12 + i] = rs * rs;
+        }
+      }
+      warp_reduce24(x, lane);
+      const int sel = lane & 3;
+      if (sel != 3) {
+        const int vi = 12 * ((lane >> 4) & 1) + 6 * ((lane >> 3) & 1) + 3 * ((lane >> 2) & 1) + sel;
+        const int cl = 96 * h + 8 * (vi % 12) + warp;  // chunk of the superblock
+        const int64_t cg = sb * kFftChunksSB + cl;
+        if (vi < 12) {
+          csA[cl] = x[0];
+          if (cg * kChunk < w) a.chunkA[cg] = x[0];
+        } else {
+          csB[cl] = x[0];
+          if (cg * kChunk < w) a.chunkB[cg] = x[0];
+        }
+      }
+    }
+    __syncthreads();
+    if (warp < kFftTilesSB) {
+      const int64_t tg = sb * kFftTilesSB + warp;
+      const double TA = warp_sum(csA[64 * warp + lane] + csA[64 * warp + 32 + lane]);
+      const double TB = warp_sum(csB[64 * warp + lane] + csB[64 * warp + 32 + lane]);
+      if (lane == 0 && tg * kPassTile < w) {
+        a.tileA[tg] = TA;
+        a.tileB[tg] = TB;
+      }
+    }
+    // csA / csB are rewritten only after the next fft4096's barriers
+  }
+}
+
+}  // namespace tfk

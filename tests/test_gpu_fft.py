@@ -1,0 +1,134 @@
+"""GPU parity of the FFT pass (k_fft.cuh: overlap-save FFT FIR + leverage
+update + CDF partials) -- the pass the sweeps run for the long lags.
+
+TF_PASS=fft forces it at every lag q >= 1 (TF_PASS=dmma: the direct
+tensor-core FIR only); the variable is read when an Engine is created.
+
+Bars (BASELINE.json north_star): sampled indices bit-exact in
+deterministic-index mode; scores, residuals, phi, PACF within rel 1e-9 of the
+oracle (the reference's tap-order FIR); identical p*; RNG-mode draws identical
+up to a neighbouring-row rounding flip.  Shapes cover the superblock edges
+(w below one 3072-row block, exactly one 6144-row superblock, one row past
+it, many superblocks) and the largest lag a sweep takes (q = 640, the solve's
+limit; the blocks hold q <= D = 1024), where the oracle's own solve is too
+slow: there the FFT
+sweep is compared with the direct-FIR sweep on identical fixed draws and
+weights (identical sampled systems, so phi is bit-identical and only the
+FIR's rounding differs).
+"""
+import numpy as np
+import pytest
+
+from test_gpu_lsar import c1_like, check_flip, relerr
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def tf():
+    import paper_2112_12994_b200 as t
+    from paper_2112_12994_b200 import build
+    build.build()
+    return t
+
+
+def engine(tf, monkeypatch, mode):
+    monkeypatch.setenv("TF_PASS", mode)
+    e = tf.Engine(0)
+    monkeypatch.delenv("TF_PASS")
+    return e
+
+
+@pytest.mark.parametrize("n,q,p_bar,c", [(1000, 3, 3, 200), (6000, 4, 5, 300), (6149, 4, 5, 300),
+                                         (6150, 4, 5, 300), (20000, 12, 40, 600), (45000, 20, 150, 1200)])
+def test_fft_pass_fixed_index_parity(orc, tf, monkeypatch, n, q, p_bar, c):
+    y = c1_like(n, seed=q + n, q=q)
+    ref = orc.lsar_fit(y, p_bar, c, 91)
+    eng = engine(tf, monkeypatch, "fft")
+    try:
+        fit = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, 91, engine=eng, fixed_idx=ref.idx, fixed_w=ref.w,
+                          want_diag=True)
+    finally:
+        eng.close()
+    d = fit.diag
+    assert np.array_equal(d["idx"], ref.idx)
+    assert relerr(fit.pacf.taus, ref.taus) < TOL
+    for p in range(p_bar):
+        assert relerr(fit.per_lag_coefficients[p], ref.coefs[p]) < TOL
+    assert relerr(d["scores"], ref.scores) < TOL
+    assert relerr(d["resid"], ref.resid) < TOL
+    assert relerr(d["rnorm2"], ref.rnorm2) < TOL
+    assert relerr(d["ssum"], ref.ssum) < TOL
+    assert fit.p_star == ref.p_star
+    assert abs(d["scores"].sum() - p_bar) < 1e-8
+
+
+def test_fft_auto_mode_parity(orc, tf, monkeypatch):
+    # default (auto) mode: direct FIR below the crossover lag, FFT from it on
+    # (TF_FFT_MINQ lowered so a small fit crosses it)
+    y = c1_like(30000, seed=8, q=10)
+    p_bar, c = 30, 800
+    ref = orc.lsar_fit(y, p_bar, c, 5)
+    monkeypatch.setenv("TF_FFT_MINQ", "11")
+    eng = tf.Engine(0)
+    monkeypatch.delenv("TF_FFT_MINQ")
+    try:
+        fit = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, 5, engine=eng, fixed_idx=ref.idx, fixed_w=ref.w,
+                          want_diag=True)
+    finally:
+        eng.close()
+    assert relerr(fit.pacf.taus, ref.taus) < TOL
+    assert relerr(fit.diag["scores"], ref.scores) < TOL
+    assert relerr(fit.diag["resid"], ref.resid) < TOL
+    assert relerr(fit.diag["rnorm2"], ref.rnorm2) < TOL
+    assert fit.p_star == ref.p_star
+
+
+def test_fft_rng_mode_matches_oracle_draws(orc, tf, monkeypatch):
+    eng = engine(tf, monkeypatch, "fft")
+    try:
+        for n, q, p_bar, c, seed in [(30000, 20, 25, 2500, 4242), (12000, 4, 6, 900, 99)]:
+            y = c1_like(n, seed=q + 3, q=q)
+            ref = orc.lsar_fit(y, p_bar, c, seed)
+            fit = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, seed, engine=eng, want_diag=True)
+            flip = check_flip(fit.diag["idx"], ref.idx, c)
+            upto = p_bar if flip is None else flip
+            for p in range(upto):
+                assert np.array_equal(fit.diag["idx"][p], ref.idx[p])
+                assert relerr(fit.per_lag_coefficients[p], ref.coefs[p]) < TOL
+            if flip is None:
+                assert relerr(fit.pacf.taus, ref.taus) < TOL
+                assert fit.p_star == ref.p_star
+    finally:
+        eng.close()
+
+
+def test_fft_longest_lag_vs_direct(tf, monkeypatch):
+    """q up to 640, the largest p_bar the rank-revealing solve takes (the
+    4096-point blocks hold filters up to q = D = 1024)."""
+    p_bar = 640
+    n, c = 26000, 1100
+    y = c1_like(n, seed=3, q=30)
+    rng = np.random.default_rng(11)
+    w = n - p_bar
+    idx = rng.integers(0, w, size=(p_bar, c))
+    wt = rng.uniform(0.5, 2.0, size=(p_bar, c))
+    out = {}
+    for mode in ("fft", "dmma"):
+        eng = engine(tf, monkeypatch, mode)
+        try:
+            out[mode] = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, 1, engine=eng, fixed_idx=idx, fixed_w=wt,
+                                    want_diag=True)
+        finally:
+            eng.close()
+    f, g = out["fft"], out["dmma"]
+    # identical sampled systems -> identical phi; the window residuals differ by FIR rounding only
+    assert np.array_equal(np.array(f.pacf.taus), np.array(g.pacf.taus))
+    assert relerr(f.diag["rnorm2"], g.diag["rnorm2"]) < TOL
+    assert relerr(f.diag["ssum"], g.diag["ssum"]) < TOL
+    assert relerr(f.diag["scores"], g.diag["scores"]) < TOL
+    phi = np.asarray(f.per_lag_coefficients[-1])
+    noise = 64 * np.finfo(float).eps * (1.0 + np.abs(phi).sum()) * np.max(np.abs(y))
+    assert np.max(np.abs(f.diag["resid"] - g.diag["resid"])) < noise
