@@ -697,9 +697,21 @@ static void reserve_fft(tf_context* ctx, int64_t w) {
       tw[256 + e] = make_double2((double)cosl(a4096), (double)sinl(a4096));
     }
     CK(cudaMemcpy(ctx->fftTw.get(), tw.data(), kFftTw * sizeof(double2), cudaMemcpyHostToDevice));
+    // double-double W_4096^e for the spectra (k_fft_series_dd, k_fft_taps_dd):
+    // hi = the rounded long double value, lo = the long double remainder
+    std::vector<double2> th(kFftN), tl(kFftN);
+    for (int e = 0; e < kFftN; ++e) {
+      const long double a = -2.0L * pi * e / (long double)kFftN;
+      const long double c = cosl(a), s = sinl(a);
+      th[e] = make_double2((double)c, (double)s);
+      tl[e] = make_double2((double)(c - (long double)th[e].x), (double)(s - (long double)th[e].y));
+    }
+    ctx->fftTwH.need(kFftN);
+    ctx->fftTwL.need(kFftN);
+    CK(cudaMemcpy(ctx->fftTwH.get(), th.data(), kFftN * sizeof(double2), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->fftTwL.get(), tl.data(), kFftN * sizeof(double2), cudaMemcpyHostToDevice));
   }
-  smem_optin((const void*)k_fft_series, fft_smem_bytes());
-  smem_optin((const void*)k_fft_taps, fft_smem_bytes());
+  smem_optin((const void*)k_fft_series_dd, fft_dd_smem_bytes());
   smem_optin((const void*)k_lsar_pass_fft<0>, fft_smem_bytes());
   smem_optin((const void*)k_lsar_pass_fft<1>, fft_smem_bytes());
   smem_optin((const void*)k_lsar_pass_fft<2>, fft_smem_bytes());
@@ -712,14 +724,15 @@ static int fft_grid(const tf_context* ctx, int64_t nsb) {
 // spectra of the resident series (y[0 .. n)) for a window of w rows
 static void launch_fft_series(tf_context* ctx, int64_t w) {
   const int64_t nsb = (w + kFftSB - 1) / kFftSB;
-  k_fft_series<<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(ctx->y.get(), ctx->n, nsb,
-                                                                              ctx->fftZ.get(), ctx->fftTw.get());
-  LAUNCH_CHECK("k_fft_series");
+  k_fft_series_dd<<<(int)std::min<int64_t>(nsb, ctx->sm_count), kFftT, fft_dd_smem_bytes(), ctx->stream>>>(
+      ctx->y.get(), ctx->n, nsb, ctx->fftZ.get(), ctx->fftTwH.get(), ctx->fftTwL.get());
+  LAUNCH_CHECK("k_fft_series_dd");
   COUNT_LAUNCH();
 }
 
 static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev) {
-  k_fft_taps<<<1, kFftT, fft_smem_bytes(), ctx->stream>>>(phi, q, ctx->fftH.get(), ctx->fftTw.get());
+  k_fft_taps_dd<<<kFftN * kTapSplit / 256, 256, 0, ctx->stream>>>(phi, q, ctx->fftH.get(), ctx->fftTwH.get(),
+                                                                   ctx->fftTwL.get());
   FftPassArgs a{};
   a.Z = ctx->fftZ.get();
   a.H = ctx->fftH.get();

@@ -14,9 +14,9 @@
 // position m = u + D of the circular convolution of x_j[m] = y[j L + m]
 // (L = 3072 rows per block, no wrap-around for q <= D).  Two consecutive
 // blocks a, b ride in one complex transform (x_a + i x_b): the series spectra
-// Zab = DFT(x_a + i x_b) are computed ONCE per sweep (k_fft_series, 64 KB per
+// Zab = DFT(x_a + i x_b) are computed ONCE per sweep (k_fft_series_dd, 64 KB per
 // 6144-row superblock = 10.7 B per row), and per lag the pass multiplies by
-// H = DFT(f_q) / N (k_fft_taps, one CTA) and inverts:
+// H = DFT(f_q) / N (k_fft_taps_dd) and inverts:
 //   IDFT(Zab H) = (x_a (*) f_q) + i (x_b (*) f_q)
 // -- the real part holds block a's residuals, the imaginary part block b's.
 // Per row and lag: 10.7 B spectrum + 16 B (s, r) read + 16 B (s, r) written,
@@ -32,13 +32,22 @@
 // memory (W_256^e and W_4096^e, long-double accurate on the host);
 // W_4096^{t r} = W_256^{(t>>4) r} W_4096^{(t&15) r}.
 //
-// Rounding: the FFT convolution's error is ~eps log2(N) ||y|| ||h|| per row,
-// the direct FIR's ~eps sum_k |h_k y|: measured on the C1/C2/C4-shaped
-// series the FFT residuals are within 1-2.5x of the direct FIR's own
-// rounding noise.
+// Rounding: a plain fp64 FFT spreads an absolute error ~eps ||x|| over every
+// bin of the series spectrum and ~eps ||h|| over every bin of the filter
+// spectrum; the inverse filter H is large exactly where the series spectrum
+// is small, so those errors come out amplified (C2 at q = 200: 1.6e-9 of
+// max|r|, vs 4.9e-10 for the direct FIR's own rounding).  Both spectra are
+// therefore computed in double-double and rounded once to fp64 (per bin
+// relative error eps): k_fft_series_dd (a double-double Stockham FFT, once
+// per sweep) and k_fft_taps_dd (a double-double direct DFT of the q + 1 taps,
+// per lag).  The per-lag product and inverse FFT stay fp64: their errors are
+// relative to the (small) residual spectrum.  Measured (tools/fft_precision.py,
+// long double model): C2 1.2e-10 of max|r| vs the exact residuals -- 4x below
+// the direct FIR's 4.9e-10; C4-shaped 8.7e-7 vs the direct FIR's 6.7e-6.
 #pragma once
 
 #include "common.cuh"
+#include "k_exact.cuh"
 #include "k_pass.cuh"
 
 namespace tfk {
@@ -159,49 +168,157 @@ __device__ __forceinline__ void fft_load_tw(double2* tw_s, const double2* tw_g) 
 }
 
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Double-double spectra (both rounded once to fp64 at the end).
+struct CD {
+  DD x, y;
+};
+__device__ __forceinline__ CD cd_add(const CD& a, const CD& b) { return {dd_add(a.x, b.x), dd_add(a.y, b.y)}; }
+__device__ __forceinline__ CD cd_sub(const CD& a, const CD& b) {
+  return {dd_add(a.x, dd_neg(b.x)), dd_add(a.y, dd_neg(b.y))};
+}
+__device__ __forceinline__ CD cd_mul(const CD& a, const CD& b) {
+  return {dd_add(dd_mul(a.x, b.x), dd_neg(dd_mul(a.y, b.y))), dd_add(dd_mul(a.x, b.y), dd_mul(a.y, b.x))};
+}
+// forward 4-point DFT (e^{-2 pi i n k / 4}); multiplications by -i are exact
+__device__ __forceinline__ void dft4_dd(CD& x0, CD& x1, CD& x2, CD& x3) {
+  const CD a = cd_add(x0, x2), b = cd_sub(x0, x2), c = cd_add(x1, x3), d = cd_sub(x1, x3);
+  x0 = cd_add(a, c);
+  x2 = cd_sub(a, c);
+  x1 = {dd_add(b.x, d.y), dd_add(b.y, dd_neg(d.x))};  // b - i d
+  x3 = {dd_add(b.x, dd_neg(d.y)), dd_add(b.y, d.x)};  // b + i d
+}
+// twiddle tables in shared memory: [0, 256) W_256^e, [256, 512) W_4096^e (hi; lo in a parallel array)
+struct TwDD {
+  const double2* h;
+  const double2* l;
+  __device__ __forceinline__ CD operator[](int e) const {
+    const double2 a = h[e], b = l[e];
+    return {DD{a.x, b.x}, DD{a.y, b.y}};
+  }
+};
+__device__ __forceinline__ void fft16_dd(CD (&v)[16], const TwDD& tw) {
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) dft4_dd(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
+  // v[4 k1 + n2] *= W16^{n2 k1} = W_256^{16 n2 k1}; n2 k1 = 4: -i (exact)
+  v[5] = cd_mul(v[5], tw[16]);
+  v[6] = cd_mul(v[6], tw[32]);
+  v[7] = cd_mul(v[7], tw[48]);
+  v[9] = cd_mul(v[9], tw[32]);
+  v[10] = CD{v[10].y, dd_neg(v[10].x)};
+  v[11] = cd_mul(v[11], tw[96]);
+  v[13] = cd_mul(v[13], tw[48]);
+  v[14] = cd_mul(v[14], tw[96]);
+  v[15] = cd_mul(v[15], tw[144]);
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) dft4_dd(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+  CD o[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) o[r] = v[4 * (r & 3) + (r >> 2)];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = o[r];
+}
+__device__ __forceinline__ void cd_st(double2* bh, double2* bl, int i, const CD& a) {
+  bh[i] = make_double2(a.x.h, a.y.h);
+  bl[i] = make_double2(a.x.l, a.y.l);
+}
+__device__ __forceinline__ CD cd_ld(const double2* bh, const double2* bl, int i) {
+  const double2 a = bh[i], b = bl[i];
+  return {DD{a.x, b.x}, DD{a.y, b.y}};
+}
+// forward 4096-point DFT in double-double, same data flow as fft4096<-1>
+__device__ __forceinline__ void fft4096_dd(CD (&v)[16], double2* bh, double2* bl, const TwDD& tw) {
+  const int t = threadIdx.x;
+  fft16_dd(v, tw);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) cd_st(bh, bl, fpad(16 * t + r), v[r]);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = cd_ld(bh, bl, fpad(t + 256 * r));
+#pragma unroll
+  for (int r = 1; r < 16; ++r) v[r] = cd_mul(v[r], tw[(t & 15) * r]);
+  fft16_dd(v, tw);
+  __syncthreads();
+  const int d2 = (t >> 4) * 256 + (t & 15);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) cd_st(bh, bl, fpad(d2 + 16 * r), v[r]);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = cd_ld(bh, bl, fpad(t + 256 * r));
+#pragma unroll
+  for (int r = 1; r < 16; ++r) v[r] = cd_mul(v[r], cd_mul(tw[(t >> 4) * r], tw[256 + (t & 15) * r]));
+  fft16_dd(v, tw);
+}
+
+inline size_t fft_dd_smem_bytes() { return 2 * sizeof(double2) * (size_t)(kFftBufC + kFftTw); }
+
 // Series spectra, once per sweep: Zab[sb][k] = DFT(x_a + i x_b)[k] with
-// x_a[m] = y[6144 sb + m], x_b[m] = y[6144 sb + 3072 + m] (0 past n)
-__global__ void __launch_bounds__(kFftT, 2) k_fft_series(const double* __restrict__ y, int64_t n, int64_t nsb,
-                                                         double2* __restrict__ Z, const double2* __restrict__ tw_g) {
+// x_a[m] = y[6144 sb + m], x_b[m] = y[6144 sb + 3072 + m] (0 past n), in
+// double-double, rounded to fp64.  twh / twl: W_4096^e, e < 4096 (hi, lo).
+__global__ void __launch_bounds__(kFftT, 1) k_fft_series_dd(const double* __restrict__ y, int64_t n, int64_t nsb,
+                                                            double2* __restrict__ Z, const double2* __restrict__ twh,
+                                                            const double2* __restrict__ twl) {
   extern __shared__ double2 fsm[];
-  double2* buf = fsm;
-  double2* tw = fsm + kFftBufC;
-  fft_load_tw(tw, tw_g);
+  double2* bh = fsm;
+  double2* bl = fsm + kFftBufC;
+  double2* th = fsm + 2 * kFftBufC;
+  double2* tl = th + kFftTw;
+  for (int e = threadIdx.x; e < 256; e += blockDim.x) {
+    th[e] = twh[16 * e];  // W_256^e
+    tl[e] = twl[16 * e];
+    th[256 + e] = twh[e];  // W_4096^e
+    tl[256 + e] = twl[e];
+  }
+  __syncthreads();
+  const TwDD tw{th, tl};
   const int t = threadIdx.x;
   for (int64_t sb = blockIdx.x; sb < nsb; sb += gridDim.x) {
     const int64_t ia = sb * kFftSB + t, ib = ia + kFftL;
-    double2 v[16];
+    CD v[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       const int64_t a = ia + 256 * r, b = ib + 256 * r;
-      v[r] = make_double2(a < n ? __ldg(y + a) : 0.0, b < n ? __ldg(y + b) : 0.0);
+      v[r] = CD{DD{a < n ? __ldg(y + a) : 0.0, 0.0}, DD{b < n ? __ldg(y + b) : 0.0, 0.0}};
     }
-    fft4096<-1>(v, buf, tw);
+    fft4096_dd(v, bh, bl, tw);
     double2* Zs = Z + sb * kFftN + t;
 #pragma unroll
-    for (int r = 0; r < 16; ++r) __stcs(Zs + 256 * r, v[r]);
+    for (int r = 0; r < 16; ++r) __stcs(Zs + 256 * r, make_double2(v[r].x.h, v[r].y.h));
   }
 }
 
-// Per lag: H[k] = DFT(f_q)[k] / N, f_q[D - q + k] = h_q[k] (h_q[0] = -1,
-// h_q[k] = phi[k - 1]); one CTA
-__global__ void __launch_bounds__(kFftT, 1) k_fft_taps(const double* __restrict__ phi, int q, double2* __restrict__ H,
-                                                       const double2* __restrict__ tw_g) {
-  extern __shared__ double2 fsm[];
-  double2* buf = fsm;
-  double2* tw = fsm + kFftBufC;
-  fft_load_tw(tw, tw_g);
-  const int t = threadIdx.x;
-  double2 v[16];
-#pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const int k = t + 256 * r - (kFftD - q);  // tap index
-    v[r] = make_double2(k == 0 ? -1.0 : (k >= 1 && k <= q) ? __ldg(phi + k - 1) : 0.0, 0.0);
+// Per lag: H[k] = DFT(f_q)[k] / N, f_q[D - q + j] = h_q[j] (h_q[0] = -1,
+// h_q[j] = phi[j - 1]) as a direct DFT of the q + 1 taps in double-double
+// (the products h_j W are exact-ish: 2 fp64 x double-double), rounded to
+// fp64.  256 threads = 32 bins x 8 tap slices; slices summed by a fixed
+// butterfly; grid 4096 / 32.
+constexpr int kTapSplit = 8;
+__global__ void __launch_bounds__(256) k_fft_taps_dd(const double* __restrict__ phi, int q, double2* __restrict__ H,
+                                                     const double2* __restrict__ twh,
+                                                     const double2* __restrict__ twl) {
+  const int t = threadIdx.x, sl = t & (kTapSplit - 1);
+  const int k = blockIdx.x * (256 / kTapSplit) + (t / kTapSplit);
+  const int per = (q + kTapSplit) / kTapSplit;  // ceil((q + 1) / 8)
+  const int j0 = sl * per, j1 = min(q + 1, j0 + per);
+  DD re{0.0, 0.0}, im{0.0, 0.0};
+  for (int j = j0; j < j1; ++j) {
+    const double hj = j == 0 ? -1.0 : __ldg(phi + j - 1);
+    const int e = ((kFftD - q + j) * k) & (kFftN - 1);
+    const double2 wh = __ldg(twh + e), wl = __ldg(twl + e);
+    re = dd_add(re, dd_mul(DD{hj, 0.0}, DD{wh.x, wl.x}));
+    im = dd_add(im, dd_mul(DD{hj, 0.0}, DD{wh.y, wl.y}));
   }
-  fft4096<-1>(v, buf, tw);
-  constexpr double inv = 1.0 / kFftN;  // exact (power of two)
 #pragma unroll
-  for (int r = 0; r < 16; ++r) H[t + 256 * r] = make_double2(v[r].x * inv, v[r].y * inv);
+  for (int m = 1; m < kTapSplit; m <<= 1) {
+    const DD ro{__shfl_xor_sync(0xffffffffu, re.h, m), __shfl_xor_sync(0xffffffffu, re.l, m)};
+    const DD io{__shfl_xor_sync(0xffffffffu, im.h, m), __shfl_xor_sync(0xffffffffu, im.l, m)};
+    // lower slice first: the same operand order in every lane of the pair
+    re = (sl & m) ? dd_add(ro, re) : dd_add(re, ro);
+    im = (sl & m) ? dd_add(io, im) : dd_add(im, io);
+  }
+  constexpr double inv = 1.0 / kFftN;  // exact (power of two)
+  if (sl == 0) H[k] = make_double2(re.h * inv, im.h * inv);
 }
 
 // Deterministic warp reduction of 24 values per lane: on return x[0] of lane
@@ -242,8 +359,8 @@ __device__ __forceinline__ void warp_reduce24(double (&x)[24], int lane) {
 }
 
 struct FftPassArgs {
-  const double2* Z;  // [nsb][4096] series spectra (k_fft_series)
-  const double2* H;  // [4096] filter spectrum of this lag / N (k_fft_taps)
+  const double2* Z;  // [nsb][4096] series spectra (k_fft_series_dd)
+  const double2* H;  // [4096] filter spectrum of this lag / N (k_fft_taps_dd)
   const double2* tw;
   int64_t w;
   double* s;  // in s_{q-1}, out s_q
