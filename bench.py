@@ -275,7 +275,12 @@ def run_ours(args):
         T = float(t.item())
     value = args.steps * ro_step / T
 
-    # ---- roofline of the fused pass (k_lsar_pass_pst), from the instrumented sweep ----
+    # ---- roofline of the dominant pass kernel, from the instrumented sweep ----
+    # lags q < q_fft run the direct FIR on the fp64 tensor pipe (k_lsar_pass_pst,
+    # fp64-bound above q ~ 70 at C4); lags q >= q_fft the overlap-save FFT FIR
+    # (k_lsar_pass_fft, HBM-bound).  Algorithmic work per window row per lag
+    # (SURVEY 8(d)): 24 B (read y, read s, write s) and, for the direct FIR,
+    # 2p+4 flop.  Per-lag pass times are CUDA events on the sweep's stream.
     fp64_peak = eng.probe_fp64_peak()
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -284,34 +289,55 @@ def run_ours(args):
     hbm_peak = float(peaks.get("hbm_gbs", 6544.0))
     w_rows = (shard.w_local if shard else n - p_bar)
     ph = diag0["phases"]
-    t_pass = float(ph[:, 2].sum())
-    flops = sum((2.0 * p + 4.0) * w_rows for p in range(1, p_bar + 1))
-    byts = 24.0 * w_rows * p_bar
-    t_roof = sum(max(24.0 * w_rows / (hbm_peak * 1e9), (2.0 * p + 4.0) * w_rows / (fp64_peak * 1e12))
-                 for p in range(1, p_bar + 1))
-    traffic = None
-    tp_path = os.path.join(ROOT, "profiles", f"r02_pass_traffic_{args.config}.json")
-    if os.path.exists(tp_path):
+    t_lag = ph[:, 2]
+    t_pass = float(t_lag.sum())
+    q_fft = eng.fft_first_lag(p_bar)
+    lags = np.arange(1, p_bar + 1)
+    dmma, fftl = lags < q_fft, lags >= q_fft
+    t_dmma, t_fft = float(t_lag[dmma].sum()), float(t_lag[fftl].sum())
+    n_fft, n_dmma = int(fftl.sum()), int(dmma.sum())
+
+    def load_traffic(kernel):
+        """DRAM bytes per launch from the committed ncu capture, scaled to this window"""
         try:
-            tj = json.load(open(tp_path))
-            traffic = tj.get("dram_bytes_per_launch_avg")
+            tj = json.load(open(os.path.join(ROOT, "profiles", "r02_pass_traffic.json")))[kernel]
+            return tj["dram_bytes_per_launch"] * w_rows / tj["w"]
         except Exception:
-            traffic = None
-    fp64_ach = flops / t_pass / 1e12
+            return None
+
+    per_kernel = {}
+    if n_fft:
+        ach = 24.0 * w_rows / (t_fft / n_fft) / 1e9
+        per_kernel["k_lsar_pass_fft"] = {
+            "lags": [int(q_fft), int(p_bar)], "launches": n_fft, "avg_ms": t_fft / n_fft * 1e3, "total_s": t_fft,
+            "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+            "traffic": load_traffic("k_lsar_pass_fft"),
+            "algorithmic_per_unit": "24 B per window row per lag (read y, read s, write s); one launch = "
+                                    f"{w_rows} rows; the FIR by FFT is O(log N) flop/row, far below the fp64 peak",
+            "moved_per_unit": "42.7 B per row: the series spectrum (10.7 B, computed once per sweep in "
+                              "double-double) + s, r in + s, r out"}
+    if n_dmma:
+        fl = sum((2.0 * p + 4.0) * w_rows for p in lags[dmma])
+        roof = sum(max(24.0 * w_rows / (hbm_peak * 1e9), (2.0 * p + 4.0) * w_rows / (fp64_peak * 1e12))
+                   for p in lags[dmma])
+        per_kernel["k_lsar_pass_pst"] = {
+            "lags": [1, int(q_fft) - 1], "launches": n_dmma, "avg_ms": t_dmma / n_dmma * 1e3, "total_s": t_dmma,
+            "bound": "tensor", "achieved": fl / t_dmma / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": fl / t_dmma / 1e12 / fp64_peak, "hbm_achieved_gbs": 24.0 * w_rows * n_dmma / t_dmma / 1e9,
+            "per_lag_roofline_frac": roof / t_dmma,
+            "algorithmic_per_unit": "2p+4 flop and 24 B per window row per lag; roofline per lag = "
+                                    "max(24 B/row at the HBM peak, (2p+4) flop/row at the fp64 peak)"}
+    dom = max(per_kernel, key=lambda k: per_kernel[k]["total_s"])
+    d = per_kernel[dom]
     roofline = {
-        "kernel": "k_lsar_pass_pst (fused FIR residual on the fp64 tensor pipe (DMMA) + leverage update + CDF "
-                  "partials)",
-        "bound": "tensor", "achieved": fp64_ach, "peak": fp64_peak, "unit": "TFLOP/s",
-        "frac": fp64_ach / fp64_peak, "traffic": traffic,
-        "peak_source": "fp64 DFMA peak measured in this run (tf_probe_fp64_peak; DMMA m8n8k4 has the same peak; "
-                       "MEASURED_PEAKS.json / B200_PROFILING.md state no fp64 figure)",
-        "algorithmic_per_unit": "per window row per lag: 2p+4 flop, 24 B (read y, read s, write s); "
-                                f"one launch = {w_rows} rows",
-        "hbm_achieved_gbs": byts / t_pass / 1e9, "hbm_peak_gbs": hbm_peak,
-        "hbm_peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)",
-        "sweep_roofline_frac": t_roof / t_pass,
-        "sweep_roofline_note": "sum over lags of max(24 B/row at the HBM peak, (2p+4) flop/row at the fp64 peak) / "
-                               "sum of the measured pass times (per-lag CUDA events on the sweep's stream)",
+        "kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"], "unit": d["unit"],
+        "frac": d["frac"], "traffic": d.get("traffic"),
+        "peak_source": ("MEASURED_PEAKS.json hbm_gbs (copy, burst)" if d["unit"] == "GB/s" else
+                        "fp64 DFMA peak measured in this run (tf_probe_fp64_peak; DMMA m8n8k4 has the same "
+                        "peak; MEASURED_PEAKS.json / B200_PROFILING.md state no fp64 figure)"),
+        "algorithmic_per_unit": d["algorithmic_per_unit"],
+        "pass_kernels": per_kernel,
+        "fp64_peak_tflops": fp64_peak,
         "phase_s": {"sample": float(ph[:, 0].sum()), "solve": float(ph[:, 1].sum()), "pass": t_pass},
         "solve_methods": {"exact_qr": int((diag0["method"] == 0).sum()), "exact_svd": int((diag0["method"] == 1).sum())},
     }

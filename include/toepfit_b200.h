@@ -221,6 +221,12 @@ int tf_select_order(const double* taus, int p_bar, double bound);
  * DFMA microbenchmark, the denominator of the fp64 roofline. */
 tf_status tf_probe_fp64_peak(tf_context* ctx, double* tflops);
 
+/* Diagnostics: the first lag q of a p_bar sweep whose pass runs the FFT FIR
+ * (k_lsar_pass_fft); lags below it run the direct tensor-core FIR.  p_bar + 1
+ * when the sweep takes no FFT lag.  (No reference counterpart: an execution
+ * detail the bench needs for the per-kernel roofline.) */
+tf_status tf_fft_first_lag(tf_context* ctx, int p_bar, int* lag);
+
 /* ---- row-sharded LSAR sweep of one long series (one process per GPU;
  *      SURVEY.md 8(e); BASELINE C3 2-GPU, C4 1/2/4/8 GPUs) ----
  * Rank g holds the window rows [row0_g, row0_g + w_g) of the global window

@@ -50,7 +50,7 @@ EXPORTS = [
     "tf_version", "tf_create", "tf_destroy", "tf_last_error", "tf_upload_series",
     "tf_upload_series_device", "tf_lsar_sweep", "tf_rh_sweep", "tf_residuals", "tf_sample_rows",
     "tf_apply_sample", "tf_solve_sampled", "tf_select_order", "tf_derive_seed",
-    "tf_probe_fp64_peak", "tf_nccl_unique_id", "tf_nccl_init", "tf_keep_slice", "tf_lsar_sweep_sharded",
+    "tf_probe_fp64_peak", "tf_fft_first_lag", "tf_nccl_unique_id", "tf_nccl_init", "tf_keep_slice", "tf_lsar_sweep_sharded",
     "tf_tpu_size", "tf_sweep_span", "tf_exact_sweep", "tf_srht_sweep", "tf_hadamard", "tf_generate_series", "tf_download_series",
     "tf_lsar_sweep_batch", "tf_lsar_step", "tf_generalized_leverage", "tf_repeated_halving",
 ]
@@ -89,6 +89,7 @@ def lib():
     L.tf_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
     L.tf_derive_seed.restype = C.c_uint64
     L.tf_probe_fp64_peak.argtypes = [C.c_void_p, _f64p]
+    L.tf_fft_first_lag.argtypes = [C.c_void_p, C.c_int, _i32p]
     L.tf_nccl_unique_id.argtypes = [C.c_char_p, C.c_int]
     L.tf_nccl_init.argtypes = [C.c_void_p, C.c_char_p, C.c_int, C.c_int]
     L.tf_keep_slice.argtypes = [C.c_void_p, C.c_int64, C.c_int64]

@@ -422,6 +422,12 @@ class Engine:
         self._check(_abi.lib().tf_probe_fp64_peak(self._ctx, C.byref(v)))
         return v.value
 
+    def fft_first_lag(self, p_bar: int) -> int:
+        """First lag of a p_bar sweep whose pass runs the FFT FIR (p_bar + 1: none)."""
+        v = C.c_int(0)
+        self._check(_abi.lib().tf_fft_first_lag(self._ctx, int(p_bar), C.byref(v)))
+        return v.value
+
     # ------------------------------------------------------------ single ops
     def residuals(self, y, n_used: int, p: int, phi) -> np.ndarray:
         y = np.ascontiguousarray(y, dtype=np.float64)

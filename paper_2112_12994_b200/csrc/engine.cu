@@ -715,6 +715,7 @@ static void reserve_fft(tf_context* ctx, int64_t w) {
   smem_optin((const void*)k_lsar_pass_fft<0>, fft_smem_bytes());
   smem_optin((const void*)k_lsar_pass_fft<1>, fft_smem_bytes());
   smem_optin((const void*)k_lsar_pass_fft<2>, fft_smem_bytes());
+  smem_optin((const void*)k_lsar_pass_fft<3>, fft_smem_bytes());
 }
 
 static int fft_grid(const tf_context* ctx, int64_t nsb) {
@@ -746,10 +747,13 @@ static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi
   a.tileA = ctx->tileA.get();
   a.tileB = ctx->tileB.get();
   const int64_t nsb = (w + kFftSB - 1) / kFftSB;
-  static const int pf = std::getenv("TF_FFT_PF") ? std::atoi(std::getenv("TF_FFT_PF")) : 1;  // dev switch
+  // L2 prefetch variant (dev switch TF_FFT_PF, measured in profiles/r02_fft_prefetch.txt): 2 (this
+  // superblock's state at the start of its iteration) is the fastest and moves no extra DRAM bytes
+  static const int pf = std::getenv("TF_FFT_PF") ? std::atoi(std::getenv("TF_FFT_PF")) : 2;
   if (pf == 0) k_lsar_pass_fft<0><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
-  else if (pf == 2) k_lsar_pass_fft<2><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
-  else k_lsar_pass_fft<1><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
+  else if (pf == 1) k_lsar_pass_fft<1><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
+  else if (pf == 3) k_lsar_pass_fft<3><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
+  else k_lsar_pass_fft<2><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   LAUNCH_CHECK("k_lsar_pass_fft");
   g_launches += 2;
 }
@@ -3070,6 +3074,14 @@ tf_status tf_lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t 
 }
 
 int64_t tf_tpu_size(int K) { return K < 1 ? 0 : tfk::tpu_size(K); }
+
+tf_status tf_fft_first_lag(tf_context* ctx, int p_bar, int* lag) {
+  if (!ctx || !lag || p_bar < 1) return TF_USAGE;
+  int q = 1;
+  while (q <= p_bar && !tfe::fft_lag(ctx, p_bar, q)) ++q;
+  *lag = q;
+  return TF_OK;
+}
 
 tf_status tf_probe_fp64_peak(tf_context* ctx, double* tflops) {
   if (!ctx || !tflops) return TF_USAGE;

@@ -374,7 +374,7 @@ struct FftPassArgs {
 
 // Persistent CTAs (2 per SM) over 6144-row superblocks.  PF (L2 prefetch):
 // 0 none, 1 the next superblock's spectrum + state, 2 this superblock's state
-// at the start of its iteration
+// at the start of its iteration, 3 = 2 + the next superblock's spectrum
 template <int PF>
 __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
   extern __shared__ double2 fsm[];
@@ -402,7 +402,9 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
   if (PF == 1 && t == 0) prefetch(blockIdx.x, false);
   for (int64_t sb = blockIdx.x; sb < nsb; sb += gridDim.x) {
     if (PF == 1 && t == 0) prefetch(sb + gridDim.x, true);
-    if (PF == 2 && t == 0) prefetch(sb, false);
+    if ((PF == 2 || PF == 3) && t == 0) prefetch(sb, false);
+    if (PF == 3 && t == 0 && sb + gridDim.x < nsb)
+      bulk_prefetch_l2(a.Z + (sb + gridDim.x) * kFftN, kFftN * sizeof(double2));
     double2 v[16];
     {
       const double2* Zs = a.Z + sb * kFftN + t;
