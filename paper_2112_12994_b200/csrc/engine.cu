@@ -716,6 +716,8 @@ static void reserve_fft(tf_context* ctx, int64_t w) {
   smem_optin((const void*)k_lsar_pass_fft<1>, fft_smem_bytes());
   smem_optin((const void*)k_lsar_pass_fft<2>, fft_smem_bytes());
   smem_optin((const void*)k_lsar_pass_fft<3>, fft_smem_bytes());
+  smem_optin((const void*)k_lsar_pass_fft<4>, fft_smem_bytes());
+
 }
 
 static int fft_grid(const tf_context* ctx, int64_t nsb) {
@@ -747,12 +749,14 @@ static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi
   a.tileA = ctx->tileA.get();
   a.tileB = ctx->tileB.get();
   const int64_t nsb = (w + kFftSB - 1) / kFftSB;
-  // L2 prefetch variant (dev switch TF_FFT_PF, measured in profiles/r02_fft_prefetch.txt): 2 (this
-  // superblock's state at the start of its iteration) is the fastest and moves no extra DRAM bytes
-  static const int pf = std::getenv("TF_FFT_PF") ? std::atoi(std::getenv("TF_FFT_PF")) : 2;
+  // prefetch variant (dev switch TF_FFT_PF, measured in profiles/r02_fft_prefetch.txt): 4 (state of
+  // this superblock and spectrum of the next to L2, the spectrum through shared memory by TMA) is the fastest
+  static const int pf = std::getenv("TF_FFT_PF") ? std::atoi(std::getenv("TF_FFT_PF")) : 4;
   if (pf == 0) k_lsar_pass_fft<0><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   else if (pf == 1) k_lsar_pass_fft<1><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   else if (pf == 3) k_lsar_pass_fft<3><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
+  else if (pf == 4) k_lsar_pass_fft<4><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
+
   else k_lsar_pass_fft<2><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   LAUNCH_CHECK("k_lsar_pass_fft");
   g_launches += 2;

@@ -372,9 +372,11 @@ struct FftPassArgs {
   double* tileB;
 };
 
-// Persistent CTAs (2 per SM) over 6144-row superblocks.  PF (L2 prefetch):
-// 0 none, 1 the next superblock's spectrum + state, 2 this superblock's state
-// at the start of its iteration, 3 = 2 + the next superblock's spectrum
+// Persistent CTAs (2 per SM) over 6144-row superblocks.  PF (prefetch):
+// 0 none, 1 the next superblock's spectrum + state to L2, 2 this superblock's
+// state to L2 at the start of its iteration, 3 = 2 + the next superblock's
+// spectrum to L2, 4 = 3 + the spectrum through shared memory by TMA (the
+// default; profiles/r02_fft_prefetch.txt)
 template <int PF>
 __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
   extern __shared__ double2 fsm[];
@@ -399,19 +401,47 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
       bulk_prefetch_l2(a.r + r0, bytes);
     }
   };
+  // PF 4: the spectrum goes through shared memory -- a TMA bulk copy of the
+  // next superblock's 64 KB spectrum into the (unpadded) transform buffer,
+  // issued once this superblock's last transform stage has read the buffer,
+  // so it lands during the state phase (the spectrum load was the top stall)
+  __shared__ __align__(8) uint64_t zbar;
+  constexpr uint32_t kZBytes = kFftN * sizeof(double2);
+  if (PF == 4) {
+    if (t == 0) mbar_init(&zbar, 1);
+    __syncthreads();
+    if (t == 0 && blockIdx.x < nsb) {
+      mbar_expect_tx(&zbar, kZBytes);
+      bulk_g2s(buf, a.Z + (int64_t)blockIdx.x * kFftN, kZBytes, &zbar);
+    }
+  }
+  uint32_t zphase = 0;
   if (PF == 1 && t == 0) prefetch(blockIdx.x, false);
   for (int64_t sb = blockIdx.x; sb < nsb; sb += gridDim.x) {
     if (PF == 1 && t == 0) prefetch(sb + gridDim.x, true);
-    if ((PF == 2 || PF == 3) && t == 0) prefetch(sb, false);
-    if (PF == 3 && t == 0 && sb + gridDim.x < nsb)
+    if (PF >= 2 && t == 0) prefetch(sb, false);
+    if (PF >= 3 && t == 0 && sb + gridDim.x < nsb)
       bulk_prefetch_l2(a.Z + (sb + gridDim.x) * kFftN, kFftN * sizeof(double2));
     double2 v[16];
-    {
+    if (PF == 4) {
+      mbar_wait(&zbar, zphase);
+      zphase ^= 1u;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = cmul(buf[t + 256 * r], __ldg(a.H + t + 256 * r));
+    } else {
       const double2* Zs = a.Z + sb * kFftN + t;
 #pragma unroll
       for (int r = 0; r < 16; ++r) v[r] = cmul(__ldcs(Zs + 256 * r), __ldg(a.H + t + 256 * r));
     }
     fft4096<1>(v, buf, tw);
+    if (PF == 4) {
+      __syncthreads();  // every thread's last-stage reads of buf are done
+      if (t == 0 && sb + gridDim.x < nsb) {
+        fence_proxy_async_smem();
+        mbar_expect_tx(&zbar, kZBytes);
+        bulk_g2s(buf, a.Z + (sb + gridDim.x) * kFftN, kZBytes, &zbar);
+      }
+    }
     // rows: output m = t + 256 r (r >= 4) -> u = m - D; block a row base + u (real part), block b row
     // base + 3072 + u (imaginary part).  Per block half: values i < 12 = s_q of rows r = 4 + i,
     // i >= 12 = r_q^2 of rows r = i - 8, reduced over the warp in one warp_reduce24.
