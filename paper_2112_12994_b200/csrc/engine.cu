@@ -14,6 +14,7 @@
 #include <new>
 #include <string>
 #include <vector>
+#include <type_traits>
 #include <mutex>
 #include <numeric>
 #include <map>
@@ -488,14 +489,24 @@ static void i8_tables(tf_context* ctx) {
     b.i8_tof_off[nbs] = (int)tof.size();
     const size_t t0 = tof.size();
     tof.resize(t0 + (size_t)nbt * nbt, -1);
-    int cnt = 0;
+    // launch order: B x B blocks of (I, J) tiles, so that the ~148 tiles in
+    // flight read few distinct digit panels (each 128 B x c rows) and stream
+    // them from L2 together instead of re-reading them from DRAM
+    static const int B = std::getenv("TF_I8_BLOCK") ? std::max(1, std::atoi(std::getenv("TF_I8_BLOCK"))) : 8;
+    std::vector<std::pair<int, int>> pairs;
     for (int I = 0; I < nbt; ++I)
       for (int J = I; J < nbt; ++J)
-        if (I / nbs + J / nbs <= kI8S - 1) {
-          tof[t0 + (size_t)I * nbt + J] = cnt++;
-          tl.push_back(I);
-          tl.push_back(J);
-        }
+        if (I / nbs + J / nbs <= kI8S - 1) pairs.emplace_back(I, J);
+    std::stable_sort(pairs.begin(), pairs.end(), [](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+      const int bx = x.first / B, by = y.first / B, cx = x.second / B, cy = y.second / B;
+      return bx != by ? bx < by : cx < cy;
+    });
+    int cnt = 0;
+    for (const auto& ij : pairs) {
+      tof[t0 + (size_t)ij.first * nbt + ij.second] = cnt++;
+      tl.push_back(ij.first);
+      tl.push_back(ij.second);
+    }
     b.i8_ntiles[nbs] = cnt;
   }
   b.i8tiles.need(tl.size());
@@ -545,8 +556,11 @@ static void reserve_exact(tf_context* ctx, int64_t c, int Kmax) {
 // sharded: the Gram partials are allgathered over ctx->comm and summed in rank
 // order, so every rank factors the same double-double Gram.
 template <class L>
+// ybits (nullable, FwdRows only): max |y| of the resident series (k_absmax_bits): the
+// INT8 Gram takes its digit exponents from max |w| * max |y| instead of a column-max pass
 static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev, const ExactOut& o,
-                        const long long* rows_dev = nullptr, bool sharded = false) {
+                        const long long* rows_dev = nullptr, bool sharded = false,
+                        const unsigned long long* ybits = nullptr) {
   SolveBufs& b = ctx->sb;
   cudaStream_t st = ctx->stream;
   const int p = K - 1;
@@ -558,8 +572,17 @@ static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev,
   if (use_i8_gram(ctx, c, K)) {
     const int nbs = (K + kI8Tile - 1) / kI8Tile, Kp = nbs * kI8Tile;
     const int64_t nk = (c + kI8Tile - 1) / kI8Tile;
-    k_i8_colmax_part<L><<<dim3((unsigned)((K + 63) / 64), ns), 256, 0, st>>>(ld, c, K, rows_dev, b.cnp.get());
-    k_i8_colmax_fin<<<(unsigned)((K + 127) / 128), 128, 0, st>>>(b.cnp.get(), (int)ns, K, b.i8E.get());
+    if constexpr (std::is_same<L, FwdRows>::value) {
+      if (ybits) {
+        k_i8_exp_fwd<<<1, 1024, 0, st>>>(ld.wt, c, rows_dev, ybits, K, b.i8E.get());
+      } else {
+        k_i8_colmax_part<L><<<dim3((unsigned)((K + 63) / 64), ns), 256, 0, st>>>(ld, c, K, rows_dev, b.cnp.get());
+        k_i8_colmax_fin<<<(unsigned)((K + 127) / 128), 128, 0, st>>>(b.cnp.get(), (int)ns, K, b.i8E.get());
+      }
+    } else {
+      k_i8_colmax_part<L><<<dim3((unsigned)((K + 63) / 64), ns), 256, 0, st>>>(ld, c, K, rows_dev, b.cnp.get());
+      k_i8_colmax_fin<<<(unsigned)((K + 127) / 128), 128, 0, st>>>(b.cnp.get(), (int)ns, K, b.i8E.get());
+    }
     k_i8_slice<L><<<dim3((unsigned)nk, (unsigned)(Kp / 32)), 256, 0, st>>>(ld, c, K, Kp, nk, rows_dev, b.i8E.get(),
                                                                            (int8_t*)b.i8D.get());
     LAUNCH_CHECK("k_i8_slice");
@@ -760,6 +783,14 @@ static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi
   else k_lsar_pass_fft<2><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   LAUNCH_CHECK("k_lsar_pass_fft");
   g_launches += 2;
+}
+
+// max |y| over the window's series values (y[0 .. rows)) into ctx->ymax (bit pattern)
+static void launch_absmax(tf_context* ctx, int64_t rows, const unsigned long long* dst) {
+  CK(cudaMemsetAsync((void*)dst, 0, sizeof(unsigned long long), ctx->stream));
+  k_absmax_bits<<<2 * ctx->sm_count, 512, 0, ctx->stream>>>(ctx->y.get(), rows, (unsigned long long*)dst);
+  LAUNCH_CHECK("k_absmax_bits");
+  COUNT_LAUNCH();
 }
 
 static void launch_pass(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev,
@@ -1032,6 +1063,8 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
   ctx->sb.M.need((size_t)c * ldq_of(2));  // the p = 1 Gram's dense staging (no allocation inside the loop)
   const bool use_fft = fft_sweep(ctx, p_bar);
   if (use_fft) reserve_fft(ctx, w);
+  ctx->ymax.need(1);
+  const unsigned long long* ybits = ctx->ymax.get();
   const int rn2 = d && d->rnorm2_out;
   bool capturing = false;
   // timing events: plain records when eager, external event nodes when captured
@@ -1044,6 +1077,7 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
     rec(ctx->events[0]);
     // lag-0 pass: r_0 = -y[0..w), s_0 = 0  ->  s_1 = y^2 / sum y^2 (lsar.cpp:11-15)
     launch_pass(ctx, 0, w, ctx->phi.get(), ctx->scal.get());
+    launch_absmax(ctx, w + p_bar, ybits);
     if (use_fft) launch_fft_series(ctx, w);  // series spectra for the FFT pass (once per sweep)
     for (int p = 1; p <= p_bar; ++p) {
       const int q = p - 1;
@@ -1067,7 +1101,7 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
       // rank-revealing solve of the sampled lag-p system (toeplitz.cpp:57-85)
       ExactOut o{ctx->phi.get(), ctx->coefs.get(), (int64_t)(p - 1) * p / 2, ctx->taus.get(), ctx->method.get(),
                  ctx->rank.get(), p, ctx->sweeps.get()};
-      solve_exact(ctx, FwdRows{ctx->y.get(), idx, wts, 0}, c, p + 1, /*rev=*/0, o);
+      solve_exact(ctx, FwdRows{ctx->y.get(), idx, wts, 0}, c, p + 1, /*rev=*/0, o, nullptr, false, ybits);
       if (phases) rec(ctx->pev[2 * (p - 1) + 1]);
       // residuals of the lag-p window fit + score update s_p = s_{p-1} + r_{p-1}^2/R_{p-1}
       if (fft_lag(ctx, p_bar, p)) launch_pass_fft(ctx, p, w, ctx->phi.get(), ctx->scal.get());
@@ -2371,6 +2405,8 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
   CK(cudaMemsetAsync(ctx->sh_par.get(), 0, 4 * sizeof(double), st));
   const bool use_fft = fft_sweep(ctx, p_bar);
   if (use_fft) reserve_fft(ctx, w);
+  ctx->ymax.need(1);
+  const unsigned long long* ybits = ctx->ymax.get();
   const int64_t nt = (c + kScanTileN - 1) / kScanTileN;
   const long long* kdev = ctx->rh_tsum.get() + nt + 1;  // this shard's draw count (scan_apply total)
   bool capturing = false;
@@ -2382,6 +2418,7 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
     rec(ctx->ev_begin);
     rec(ctx->events[0]);
     launch_pass(ctx, 0, w, ctx->phi.get(), ctx->sh_par.get());  // r_0 = -y, s_0 = 0
+    launch_absmax(ctx, w + p_bar, ybits);
     if (use_fft) launch_fft_series(ctx, w);
     for (int p = 1; p <= p_bar; ++p) {
       const int q = p - 1;
@@ -2425,7 +2462,7 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
       ExactOut o{ctx->phi.get(), ctx->coefs.get(), (int64_t)(p - 1) * p / 2, ctx->taus.get(), ctx->method.get(),
                  ctx->rank.get(), p, ctx->sweeps.get()};
       solve_exact(ctx, FwdRows{ctx->y.get(), ctx->sh_idx.get(), ctx->sh_wts.get(), 0}, c, p + 1, /*rev=*/0, o, kdev,
-                  /*sharded=*/true);
+                  /*sharded=*/true, ybits);
       if (phases) rec(ctx->pev[2 * (p - 1) + 1]);
       if (fft_lag(ctx, p_bar, p)) launch_pass_fft(ctx, p, w, ctx->phi.get(), ctx->sh_par.get());
       else launch_pass(ctx, p, w, ctx->phi.get(), ctx->sh_par.get());  // R_{p-1} = par[0]

@@ -105,6 +105,7 @@ struct tf_context {
   // spectrum, twiddle tables; pass_mode 0 auto (FFT for lags >= fft_minq),
   // 1 direct FIR only, 2 FFT at every lag >= 1
   tfe::DBuf<double2> fftZ, fftH, fftTw, fftTwH, fftTwL;  // fftTwH/L: W_4096^e, e < 4096, double-double
+  tfe::DBuf<unsigned long long> ymax;  // max |y| of the resident series (bit pattern), per sweep
   int pass_mode = 0, fft_minq = 0;
   int gram_mode = 0;  // 0 auto (INT8 tensor-core Gram above a work threshold), 1 double-double CUDA cores, 2 INT8 whenever c fits
   std::vector<cudaEvent_t> events;

@@ -41,6 +41,8 @@ constexpr int64_t kI8MaxRows = 1LL << 19;  // |sum of c digit products| <= 2^12 
 constexpr double kI8MinWork = 4e8;         // c K^2 above which the tensor-core Gram is faster (B200)
 constexpr int kI8Bad = 1 << 20;            // E_j of a column holding a NaN / Inf
 
+__device__ __forceinline__ double fmax_nan(double a, double b) { return (b > a || b != b) ? b : a; }  // NaN sticks
+
 __device__ __forceinline__ uint32_t i8_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // column max |a| (partials per row block) -> exponent E_j with max |a| * 2^-E_j < 1/2
@@ -80,6 +82,51 @@ __global__ void k_i8_colmax_fin(const double* __restrict__ part, int nsplit, int
   int e = 0;
   if (m > 0.0) frexp(m, &e);  // m < 2^e
   E[j] = e + 1;               // |a| 2^-E < 1/2
+}
+
+// Window-system rows (FwdRows: a_tj = w_t y[idx_t + j]): one exponent for
+// every column from the bound max_t |w_t| * max_i |y_i| (no pass over the c x K
+// sampled entries).  The bound exceeds a column's own max by a few bits at
+// most (same series, same weights), which the 98-bit digit budget absorbs.
+// ybits: max |y| as the bit pattern of a non-negative double (k_absmax_bits).
+__global__ void k_absmax_bits(const double* __restrict__ y, int64_t n, unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double a = fabs(__ldg(y + i));
+    m = (a > m || a != a) ? a : m;
+  }
+  m = fmax_nan(m, __shfl_xor_sync(0xffffffffu, m, 16));
+  m = fmax_nan(m, __shfl_xor_sync(0xffffffffu, m, 8));
+  m = fmax_nan(m, __shfl_xor_sync(0xffffffffu, m, 4));
+  m = fmax_nan(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  m = fmax_nan(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));  // order-free
+}
+__global__ void __launch_bounds__(1024) k_i8_exp_fwd(const double* __restrict__ wt, int64_t rows,
+                                                     const long long* rows_dev,
+                                                     const unsigned long long* __restrict__ ybits, int K,
+                                                     int* __restrict__ E) {
+  if (rows_dev) rows = min(rows, (int64_t)*rows_dev);
+  __shared__ double red[32];
+  double m = 0.0;
+  for (int64_t t = threadIdx.x; t < rows; t += blockDim.x) {
+    const double a = fabs(wt[t]);
+    m = (a > m || a != a) ? a : m;
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = red[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) red[0] = m;
+  }
+  __syncthreads();
+  const double bound = red[0] * __longlong_as_double((long long)*ybits) * (1.0 + 0x1p-40);
+  int e = 0;
+  if (bound > 0.0 && isfinite(bound)) frexp(bound, &e);
+  const int ev = isfinite(bound) ? e + 1 : kI8Bad;
+  for (int j = threadIdx.x; j < K; j += blockDim.x) E[j] = ev;
 }
 
 __device__ __forceinline__ uint64_t i8_sdesc(uint32_t addr) {

@@ -2,7 +2,7 @@
 the FFT pass (TF_PASS=fft) on a C4-shaped sweep: one instrumented sweep per
 mode (per-lag phase events), printed per lag band, plus the crossover lag.
 
-  python tools/fft_pass_time.py [n] [p_bar] [c]
+  python tools/fft_pass_time.py [n] [p_bar] [c] [modes, e.g. "fft" or "dmma,fft"]
 """
 import json
 import os
@@ -22,7 +22,8 @@ def main():
     c = int(sys.argv[3]) if len(sys.argv) > 3 else 200_000
     roots = gen.ar_roots(100, 1.05, 2.0, 2112_12994)
     res = {}
-    for mode in ("dmma", "fft"):
+    modes = sys.argv[4].split(",") if len(sys.argv) > 4 else ["dmma", "fft"]
+    for mode in modes:
         os.environ["TF_PASS"] = mode
         eng = tf.Engine(0)
         eng.generate_series(roots, n, 2112_12994, "normal")
@@ -36,6 +37,8 @@ def main():
         print(mode, "sweep %.3f s  pass %.3f  solve %.3f  sample %.3f  p* %d" % (
             res[mode]["sweep_s"], sum(res[mode]["pass_s"]), res[mode]["solve_s"], res[mode]["sample_s"], out[3]),
             flush=True)
+    if len(modes) < 2:
+        return
     d = np.array(res["dmma"]["pass_s"]) * 1e3
     f = np.array(res["fft"]["pass_s"]) * 1e3
     w = n - p_bar
