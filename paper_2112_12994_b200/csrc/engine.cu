@@ -459,10 +459,15 @@ static void solve_rows(tf_context* ctx, const L& ld, int64_t c, int K, const Sol
 // the rank rule finds rank < p.  rev = 1: target-first column order (RH).
 constexpr int kExactMaxP = 640;  // the SVD block pair of a 16-CTA cluster fits shared memory up to here
 
-static void svd_plan(int p, int& nct, int& nblk, int& bw) {
+// launch shape of k_svd_minnorm for lag order p: nct CTAs (nblk = 2 nct
+// blocks) cover the worst case ncol = p; bw = the block width the shared
+// memory is sized for (>= p / nblk, up to 32 = a warp per pair, within the
+// opt-in limit) -- the kernel picks its block count from the actual ncol
+static void svd_plan(int p, int smem_max, int& nct, int& nblk, int& bw) {
   nct = std::min(kSvdMaxCta, std::max(1, (p + 31) / 32));
   nblk = 2 * nct;
-  bw = std::max(1, (p + nblk - 1) / nblk);
+  const int fit = (int)((size_t)smem_max / svd_smem_bytes(p, 1));
+  bw = std::max((p + nblk - 1) / nblk, std::min(kSvdThreads / 32, fit));
 }
 
 // INT8 tensor-core Gram (k_i8gram.cuh) or the double-double CUDA-core one
@@ -648,7 +653,7 @@ static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev,
     CK(cudaLaunchKernelEx(&cfg, k_pchol_dd, pa));
   }
   int nct, nblk, bw;
-  svd_plan(p, nct, nblk, bw);
+  svd_plan(p, ctx->smem_optin_max, nct, nblk, bw);
   SvdArgs sa{};
   sa.N = b.Nsv.get();
   sa.sig = b.sig.get();

@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
 }
 
 // ---------------------------------------------------------------- 3. minimum-norm SVD
-constexpr int kSvdThreads = 512;
+constexpr int kSvdThreads = 1024;  // 32 warps: one column pair per warp per sub-round for blocks of <= 32 columns
 constexpr int kSvdMaxCta = 16;
 constexpr int kSvdMaxSweeps = 60;
 
@@ -549,10 +549,36 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
   extern __shared__ __align__(128) double sm[];
   // columns of N = the kend nonzero rows of R' (rows past kend are exact zero
   // pivots: zero columns, singular value 0 -- dropped); blocks of bw of them
-  const int p = a.p, m = p + 1, nblk = a.nblk;
+  // Block count from the actual column count (known only here): the critical
+  // path of a sweep is ~ncol sub-rounds whatever the block count, but every
+  // round costs a block reload and a cluster barrier (few blocks are better
+  // for few columns) while a sub-round's fp64 work grows with the block width
+  // (many blocks = many SMs are better for many columns); blocks stay within
+  // one warp per pair (bw <= 32) and the shared memory (a.bw).  CTAs past
+  // nblk / 2 only join the cluster barriers.
+  const int p = a.p, m = p + 1;
   const int ncol = a.svd[66];
-  const int bw = max(1, min(a.bw, (ncol + nblk - 1) / nblk));
-  const int cta = (int)cl.block_rank(), nct = nblk / 2;
+  const int bcap = min(a.bw, kSvdThreads / 32);
+  int nblk = a.nblk;
+  {
+    // cost model in SM cycles (measured scale, B200): a round = cluster
+    // barrier + reload of two bw x m blocks; a sub-round = max(latency of one
+    // pair, fp64 work of the CTA's bw pairs at 64 lanes / clock)
+    double best = 1e300;
+    for (int nb = 2; nb <= a.nblk; nb += 2) {
+      const int b = (ncol + nb - 1) / nb;
+      if (b > bcap) continue;
+      const double sub = (2.0 * b - 1.0) + (nb - 2.0) * b;
+      const double cost = (nb - 1.0) * (2000.0 + 0.32 * b * m) + sub * fmax(500.0, b * 7.0 * m / 64.0);
+      if (cost < best) {
+        best = cost;
+        nblk = nb;
+      }
+    }
+  }
+  const int bw = max(1, (ncol + nblk - 1) / nblk);
+  const int cta = (int)cl.block_rank(), nct = a.nblk / 2;
+  const bool active = cta < nblk / 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = kSvdThreads / 32;
   double* slot[2] = {sm, sm + (size_t)bw * m};
   int colof[2];
@@ -560,6 +586,11 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
   for (; sweep < kSvdMaxSweeps; ++sweep) {
     int rotated = 0;
     for (int r = 0; r < nblk - 1; ++r) {
+      if (!active) {  // idle CTA: the round's cluster barrier only
+        __threadfence();
+        cl.sync();
+        continue;
+      }
       int ba, bb;
       rr_pair(nblk, r, cta, ba, bb);
       colof[0] = ba * bw;
@@ -602,9 +633,19 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
           ga = warp_sum(ga);
           if (ga == 0.0 || fabs(ga) <= 2.220446049250313e-16 * sqrt(al * be)) continue;
           rotated = 1;
-          const double zeta = (be - al) / (2.0 * ga);
-          const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+          // rotation angle (Rutishauser): MUFU reciprocal / reciprocal square
+          // root + two Newton steps (~1 ulp) instead of IEEE division / sqrt,
+          // which dominate the latency of a sub-round
+          double tt;
+          if (fabs(ga) > 1e-290 && fabs(be - al) < 1e140 * fabs(ga)) {
+            const double zeta = (be - al) * fast_rcp(2.0 * ga);
+            const double z2 = fma(zeta, zeta, 1.0);
+            tt = (zeta >= 0.0 ? 1.0 : -1.0) * fast_rcp(fabs(zeta) + z2 * fast_rsqrt(z2));
+          } else {  // subnormal / extreme ratios: the IEEE formulas
+            const double zeta = (be - al) / (2.0 * ga);
+            tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          }
+          const double cs = fast_rsqrt(fma(tt, tt, 1.0)), sn = cs * tt;
           for (int i = lane; i < m; i += 32) {
             const double x = xu[i], y = xv[i];
             xu[i] = cs * x - sn * y;
