@@ -494,23 +494,28 @@ static void i8_tables(tf_context* ctx) {
     b.i8_tof_off[nbs] = (int)tof.size();
     const size_t t0 = tof.size();
     tof.resize(t0 + (size_t)nbt * nbt, -1);
-    // launch order: B x B blocks of (I, J) tiles, so that the ~148 tiles in
-    // flight read few distinct digit panels (each 128 B x c rows) and stream
-    // them from L2 together instead of re-reading them from DRAM
+    // tiles (I, m) of 128 x 256 (blocks I and 2m, 2m + 1), kept when either
+    // half holds a needed (I <= J, s + u <= S - 1) block pair; launch order:
+    // B x B blocks of tiles, so that the ~148 tiles in flight read few
+    // distinct digit panels (each 128 B x c rows) and stream them from L2
+    // together instead of re-reading them from DRAM
     static const int B = std::getenv("TF_I8_BLOCK") ? std::max(1, std::atoi(std::getenv("TF_I8_BLOCK"))) : 8;
+    auto need = [&](int I, int J) { return I <= J && I / nbs + J / nbs <= kI8S - 1; };
     std::vector<std::pair<int, int>> pairs;
     for (int I = 0; I < nbt; ++I)
-      for (int J = I; J < nbt; ++J)
-        if (I / nbs + J / nbs <= kI8S - 1) pairs.emplace_back(I, J);
+      for (int m = I / 2; m < nbt / 2; ++m)
+        if (need(I, 2 * m) || need(I, 2 * m + 1)) pairs.emplace_back(I, m);
     std::stable_sort(pairs.begin(), pairs.end(), [](const std::pair<int, int>& x, const std::pair<int, int>& y) {
       const int bx = x.first / B, by = y.first / B, cx = x.second / B, cy = y.second / B;
       return bx != by ? bx < by : cx < cy;
     });
     int cnt = 0;
-    for (const auto& ij : pairs) {
-      tof[t0 + (size_t)ij.first * nbt + ij.second] = cnt++;
-      tl.push_back(ij.first);
-      tl.push_back(ij.second);
+    for (const auto& im : pairs) {
+      for (int h = 0; h < 2; ++h)
+        if (need(im.first, 2 * im.second + h)) tof[t0 + (size_t)im.first * nbt + 2 * im.second + h] = 2 * cnt + h;
+      tl.push_back(im.first);
+      tl.push_back(im.second);
+      ++cnt;
     }
     b.i8_ntiles[nbs] = cnt;
   }
@@ -540,7 +545,7 @@ static void reserve_exact(tf_context* ctx, int64_t c, int Kmax) {
     const int64_t cpad = (c + kI8Tile - 1) / kI8Tile * kI8Tile;
     b.i8D.need((size_t)kI8S * nbs * kI8Tile * cpad);
     b.i8E.need((size_t)nbs * kI8Tile);
-    b.i8P.need((size_t)b.i8_ntiles[nbs] * kI8Tile * kI8Tile);
+    b.i8P.need((size_t)b.i8_ntiles[nbs] * kI8Tile * kI8N);
   }
   b.Gh.need(KK);
   b.Gl.need(KK);

@@ -33,9 +33,10 @@ namespace tfk {
 
 constexpr int kI8S = 14;          // digit planes (98 bits)
 constexpr int kI8Tile = 128;      // output tile (stacked columns) and K step (rows)
-constexpr int kI8Stages = 6;
+constexpr int kI8Stages = 4;
 constexpr int kI8Threads = 128;
-constexpr size_t kI8StageBytes = 2 * 128 * 128;  // A + B tile per stage
+constexpr int kI8N = 256;                         // output tile: 128 stacked columns (I) x 256 (J pair)
+constexpr size_t kI8StageBytes = 3 * 128 * 128;  // A block + two B blocks per stage
 constexpr size_t kI8Smem = kI8Stages * kI8StageBytes + 1024;
 constexpr int64_t kI8MaxRows = 1LL << 19;  // |sum of c digit products| <= 2^12 c < 2^31
 constexpr double kI8MinWork = 4e8;         // c K^2 above which the tensor-core Gram is faster (B200)
@@ -189,10 +190,15 @@ __device__ __forceinline__ void i8_mbar_wait(uint32_t bar, uint32_t parity) {
                  : "=r"(done) : "r"(bar), "r"(parity) : "memory");
 }
 
-// P tiles: out[tile][128][128] int32 (row = stacked column of I, col = of J).
-// Warp 0 lane 0 streams the (I, k) / (J, k) blocks with 1-D bulk copies into a
-// kI8Stages ring (full barrier: transaction bytes; empty barrier: the MMAs'
-// commit), warp 1 lane 0 issues the MMAs, all four warps drain TMEM.
+// P tiles: out[tile][128][256] int32 (row = stacked column of block I, col =
+// stacked column of blocks 2m, 2m + 1).  One CTA per tile (I, m): per 128-row
+// K step three 16 KB bulk copies (block I, blocks 2m and 2m + 1, which land
+// contiguously = one 256-row K-major B operand) into a kI8Stages ring; warp 0
+// lane 0 streams (full barrier: transaction bytes; empty barrier: the MMAs'
+// commit), warp 1 lane 0 issues 4 tcgen05.mma (M = 128, N = 256, K = 32) per
+// step; all four warps drain the 256 TMEM columns.  N = 256 halves the operand
+// bytes per MMA of the 128 x 128 version (the kernel was feeding its tensor
+// pipe at 37 % from L2 at 14.8 TB/s; profiles/r02_i8_gemm.txt).
 __global__ void __launch_bounds__(kI8Threads) k_i8_gemm(const int8_t* __restrict__ D, int64_t nk,
                                                         const int2* __restrict__ tiles, int32_t* __restrict__ out) {
   extern __shared__ __align__(1024) unsigned char i8sm[];
@@ -200,13 +206,13 @@ __global__ void __launch_bounds__(kI8Threads) k_i8_gemm(const int8_t* __restrict
   __shared__ uint32_t tmem_base;
   unsigned char* base = i8sm + ((1024 - (i8_smem_u32(i8sm) & 1023)) & 1023);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int2 tp = tiles[blockIdx.x];
-  const bool diag = tp.x == tp.y;
+  const int2 tp = tiles[blockIdx.x];  // (I, m)
   const int8_t* blkA = D + (int64_t)tp.x * nk * 16384;
-  const int8_t* blkB = D + (int64_t)tp.y * nk * 16384;
+  const int8_t* blkB0 = D + (int64_t)(2 * tp.y) * nk * 16384;
+  const int8_t* blkB1 = D + (int64_t)(2 * tp.y + 1) * nk * 16384;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(i8_smem_u32(&tmem_base)),
-                 "r"(128));
+                 "r"(kI8N));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32) {
@@ -222,27 +228,27 @@ __global__ void __launch_bounds__(kI8Threads) k_i8_gemm(const int8_t* __restrict
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
   if (tid == 0) {  // producer
-    const uint32_t bytes = diag ? 16384u : 32768u;
     for (int64_t k = 0; k < nk; ++k) {
       const int st = (int)(k % kI8Stages);
       if (k >= kI8Stages) i8_mbar_wait(i8_smem_u32(&empty[st]), (uint32_t)(((k / kI8Stages) - 1) & 1));
       const uint32_t fb = i8_smem_u32(&full[st]);
       const uint32_t sA = i8_smem_u32(base + (size_t)st * kI8StageBytes);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bytes) : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(3u * 16384u) : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sA),
                    "l"(blkA + k * 16384), "r"(16384), "r"(fb) : "memory");
-      if (!diag)
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         sA + 16384), "l"(blkB + k * 16384), "r"(16384), "r"(fb) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       sA + 16384), "l"(blkB0 + k * 16384), "r"(16384), "r"(fb) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       sA + 32768), "l"(blkB1 + k * 16384), "r"(16384), "r"(fb) : "memory");
     }
   } else if (tid == 32) {  // MMA issuer
-    // instruction descriptor: D s32, A / B s8, K-major, N = 128 (n_dim 16), M = 128 (m_dim 8)
-    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (16u << 17) | (8u << 24);
+    // instruction descriptor: D s32, A / B s8, K-major, N = 256 (n_dim 32), M = 128 (m_dim 8)
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kI8N >> 3) << 17) | (8u << 24);
     for (int64_t k = 0; k < nk; ++k) {
       const int st = (int)(k % kI8Stages);
       i8_mbar_wait(i8_smem_u32(&full[st]), (uint32_t)((k / kI8Stages) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a0 = i8_smem_u32(base + (size_t)st * kI8StageBytes), b0 = diag ? a0 : a0 + 16384;
+      const uint32_t a0 = i8_smem_u32(base + (size_t)st * kI8StageBytes), b0 = a0 + 16384;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {  // K = 32 bytes per MMA: 2 chunks of 16
         const uint64_t da = i8_sdesc(a0 + kk * 256), db = i8_sdesc(b0 + kk * 256);
@@ -259,9 +265,9 @@ __global__ void __launch_bounds__(kI8Threads) k_i8_gemm(const int8_t* __restrict
   __syncwarp();
   i8_mbar_wait(i8_smem_u32(&done), 0u);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  int32_t* o = out + (size_t)blockIdx.x * 128 * 128 + (size_t)(32 * warp + lane) * 128;
+  int32_t* o = out + (size_t)blockIdx.x * 128 * kI8N + (size_t)(32 * warp + lane) * kI8N;
 #pragma unroll 1
-  for (int c0 = 0; c0 < 128; c0 += 8) {
+  for (int c0 = 0; c0 < kI8N; c0 += 8) {
     uint32_t v[8];
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
@@ -272,11 +278,12 @@ __global__ void __launch_bounds__(kI8Threads) k_i8_gemm(const int8_t* __restrict
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kI8N));
 }
 
 // G_ij (i <= j; mirrored) = sum_{s + u <= S-1} 2^{E_i + E_j - 7 (s + u + 2)} P[(s,i),(u,j)]
-// in double-double.  tile_of[I * nbt + J] = index of tile (I, J), I <= J.
+// in double-double.  tile_of[I * nbt + J] = 2 (index of the tile holding
+// (I, J), I <= J) + (J & 1).
 __global__ void k_i8_combine(const int32_t* __restrict__ P, const int* __restrict__ tile_of, int nbt, int K, int Kp,
                              const int* __restrict__ E, double* __restrict__ Gh, double* __restrict__ Gl) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -296,7 +303,9 @@ __global__ void k_i8_combine(const int32_t* __restrict__ P, const int* __restric
           b = t;
         }
         const int I = a / kI8Tile, J = b / kI8Tile;
-        const int32_t v = P[(size_t)tile_of[I * nbt + J] * 128 * 128 + (size_t)(a % kI8Tile) * 128 + (b % kI8Tile)];
+        const int slot = tile_of[I * nbt + J];  // 2 tile + half
+        const int32_t v = P[((size_t)(slot >> 1) * 128 + (size_t)(a % kI8Tile)) * kI8N + (size_t)(slot & 1) * 128 +
+                            (b % kI8Tile)];
         if (v) acc = dd_add(acc, DD{ldexp((double)v, E[i] + E[j] - 7 * (s + u + 2)), 0.0});
       }
   }

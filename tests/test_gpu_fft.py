@@ -132,3 +132,60 @@ def test_fft_longest_lag_vs_direct(tf, monkeypatch):
     phi = np.asarray(f.per_lag_coefficients[-1])
     noise = 64 * np.finfo(float).eps * (1.0 + np.abs(phi).sum()) * np.max(np.abs(y))
     assert np.max(np.abs(f.diag["resid"] - g.diag["resid"])) < noise
+
+
+def _exact_resid(seg, phi):
+    """r(i) = -y[q + i] + sum_j phi[j] y[q - 1 - j + i] in long double (the
+    reference for both fp64 FIRs)"""
+    q = phi.size
+    yl = seg.astype(np.longdouble)
+    rows = seg.size - q
+    r = -yl[q:q + rows].copy()
+    for j in range(q):
+        r += np.longdouble(phi[j]) * yl[q - 1 - j:q - 1 - j + rows]
+    return r
+
+
+def test_fft_spectra_accuracy_c2(orc, tf, monkeypatch):
+    """BASELINE C2 (AR(50), n = 1e7, p_bar = 200): the FFT pass's residuals at
+    the last lag against long-double residuals of the same phi.  The spectra
+    are double-double, rounded once (k_fft_series_dd / k_fft_taps_dd), so the
+    FFT residuals are at least as accurate as the oracle's direct fp64 tap
+    loop (a plain fp64 FFT was at 1.6e-9 of max|r| here; the direct FIR is at
+    4.9e-10)."""
+    from paper_2112_12994_b200 import gen
+    y, _, p_bar, _ = gen.make_config_series("C2")
+    eng = engine(tf, monkeypatch, "fft")
+    try:
+        fit = tf.lsar_fit(tf.TimeSeries(y), p_bar, 10_000, 99, engine=eng, want_diag=True)
+    finally:
+        eng.close()
+    phi = np.asarray(fit.per_lag_coefficients[-1], float)
+    w = y.size - p_bar
+    worst_fft = worst_dir = 0.0
+    for i0 in (0, w // 3, w - 6000):
+        seg = y[i0:i0 + 6000 + p_bar]
+        ex = _exact_resid(seg, phi)
+        scale = float(np.max(np.abs(ex)))
+        worst_fft = max(worst_fft, float(np.max(np.abs(fit.diag["resid"][i0:i0 + 6000] - ex))) / scale)
+        worst_dir = max(worst_dir, float(np.max(np.abs(orc.residuals(seg, seg.size, p_bar, phi) - ex))) / scale)
+    assert worst_fft < 1e-9, worst_fft
+    assert worst_fft <= 1.5 * worst_dir, (worst_fft, worst_dir)
+
+
+def test_fft_first_lag_abi(tf, monkeypatch):
+    """tf_fft_first_lag: the auto crossover, the forced modes, p_bar past the
+    4096-point blocks' filter length (direct FIR only)"""
+    e = tf.Engine(0)
+    try:
+        assert e.fft_first_lag(500) == 96
+        assert e.fft_first_lag(50) == 51  # below the crossover: no FFT lag
+        assert e.fft_first_lag(2000) == 2001  # q > D = 1024: direct FIR only
+    finally:
+        e.close()
+    for mode, want in (("fft", 1), ("dmma", 501)):
+        e = engine(tf, monkeypatch, mode)
+        try:
+            assert e.fft_first_lag(500) == want
+        finally:
+            e.close()

@@ -3,7 +3,7 @@
 double Gram, pivoted-Cholesky cluster, min-norm SVD cluster on a rank-deficient
 C4-generator series), RH sweep (halving, sketch, CholeskyQR factor kernels,
 Hankel row scores), the batched sweep (k_bsolve), exact / SRHT sweeps, the
-LsarDriver step API.  Usage: python tools/sanitize_workload.py"""
+LsarDriver step API, the FFT pass and the INT8 Gram (forced).  Usage: python tools/sanitize_workload.py"""
 import sys
 import os
 
@@ -24,5 +24,11 @@ e = tf.exact_fit(tf.TimeSeries(y[:3000]), 8, engine=eng)
 h = tf.srht_fit(tf.TimeSeries(y[:3000]), 4, 300, 3, engine=eng)
 d = tf.LsarDriver(s, 4, 300, 9, engine=eng)
 st = d.advance(d.first_lag())
+# the FFT pass (double-double spectra, TMA-staged spectrum) and the INT8
+# tensor-core Gram (tcgen05 kind::i8), forced on at this small size
+os.environ["TF_PASS"] = "fft"
+os.environ["TF_GRAM"] = "i8"
+eng2 = tf.Engine(0)
+f5 = tf.lsar_fit(tf.TimeSeries(y4), 40, 800, 7, engine=eng2, want_diag=True)
 print("sanitize workload ok:", f.p_star, r.p_star, f4.p_star, int(np.sum(f4.diag["method"])), b[0].p_star, e.p_star,
-      h.p_star, st.p)
+      h.p_star, st.p, f5.p_star)
