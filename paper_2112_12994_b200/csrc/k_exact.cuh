@@ -401,16 +401,19 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
         wv_i[warp] = vi;
       }
       __syncthreads();
-      if (tid == 0) {
-        DD b{wv_h[0], wv_l[0]};
-        int bi = wv_i[0];
-        for (int w = 1; w < kPcThreads / 32; ++w) {
-          const DD o{wv_h[w], wv_l[w]};
-          if (dd_gt(o, b) || (o.h == b.h && o.l == b.l && wv_i[w] < bi)) {
+      if (warp == 0) {  // the 32 warp candidates, same tie rule (first position wins)
+        DD b{wv_h[lane], wv_l[lane]};
+        int bi = wv_i[lane];
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) {
+          const DD o{__shfl_xor_sync(0xffffffffu, b.h, m), __shfl_xor_sync(0xffffffffu, b.l, m)};
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
+          if (dd_gt(o, b) || (o.h == b.h && o.l == b.l && oi < bi)) {
             b = o;
-            bi = wv_i[w];
+            bi = oi;
           }
         }
+        if (lane == 0) {
         const int tp = perm[k];  // swap positions k <-> bi (identically in every CTA)
         perm[k] = perm[bi];
         perm[bi] = tp;
@@ -418,6 +421,7 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
         const DD r = dd_sqrt(b);
         rkh[k] = r.h;
         rkl[k] = r.l;
+        }
       }
       __syncthreads();
     }
@@ -453,8 +457,7 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
       a.Rh[(int64_t)ck * K + k] = rkk.h;
       a.Rl[(int64_t)ck * K + k] = rkk.l;
     }
-    __threadfence();
-    clu.sync();
+    clu.sync();  // barrier.cluster arrive.release / wait.acquire: row k and the diagonal visible cluster-wide
   }
   const int kend = s_stop;  // rows kend.. are exact zeros
   // rank (Eigen ColPivHouseholderQR::rank with the prescribed threshold)
