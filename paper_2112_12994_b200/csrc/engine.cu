@@ -466,7 +466,7 @@ constexpr int kExactMaxP = 640;  // the SVD block pair of a 16-CTA cluster fits 
 static void svd_plan(int p, int smem_max, int& nct, int& nblk, int& bw) {
   nct = std::min(kSvdMaxCta, std::max(1, (p + 31) / 32));
   nblk = 2 * nct;
-  const int fit = (int)((size_t)smem_max / svd_smem_bytes(p, 1));
+  const int fit = (int)((size_t)(smem_max - 2048) / svd_smem_bytes(p, 1));  // static shared memory: 1 KB
   bw = std::max((p + nblk - 1) / nblk, std::min(kSvdThreads / 32, fit));
 }
 

@@ -584,6 +584,7 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
   const bool active = cta < nblk / 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = kSvdThreads / 32;
   double* slot[2] = {sm, sm + (size_t)bw * m};
+  __shared__ double nrm[2 * (kSvdThreads / 32)];
   int colof[2];
   int sweep = 0;
   for (; sweep < kSvdMaxSweeps; ++sweep) {
@@ -598,12 +599,36 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
       rr_pair(nblk, r, cta, ba, bb);
       colof[0] = ba * bw;
       colof[1] = bb * bw;
+      // a block is bw contiguous columns of N: a flat copy (valid columns
+      // only, zeros past ncol), 8 loads in flight per thread
       for (int s = 0; s < 2; ++s) {
         const int c0 = colof[s];
-        for (int e = tid; e < bw * m; e += kSvdThreads) {
-          const int c = c0 + e / m;
-          slot[s][e] = c < ncol ? a.N[(int64_t)c * m + (e % m)] : 0.0;
+        const int nvalid = max(0, min(bw, ncol - c0)) * m, ntot = bw * m;
+        const double* src = a.N + (int64_t)c0 * m;
+        double* dst = slot[s];
+        for (int e0 = 0; e0 < ntot; e0 += 8 * kSvdThreads) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * kSvdThreads + tid;
+            v[u] = e < nvalid ? src[e] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * kSvdThreads + tid;
+            if (e < ntot) dst[e] = v[u];
+          }
         }
+      }
+      __syncthreads();
+      // squared norms of the 2 bw local columns (rows < p), kept current
+      // through the round by the rotation identities a' = a - t g, b' = b + t g
+      for (int e = warp; e < 2 * bw; e += nwarp) {
+        const double* xe = slot[e / bw] + (size_t)(e % bw) * m;
+        double q = 0.0;
+        for (int i = lane; i < p; i += 32) q = fma(xe[i], xe[i], q);
+        q = warp_sum(q);
+        if (lane == 0) nrm[e] = q;
       }
       __syncthreads();
       // round 0 of a sweep (every block sits in exactly one CTA): all pairs of
@@ -624,16 +649,15 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
           if (gu >= ncol || gv >= ncol) continue;
           double* xu = slot[u / bw] + (size_t)(u % bw) * m;
           double* xv = slot[v / bw] + (size_t)(v % bw) * m;
-          double al = 0.0, be = 0.0, ga = 0.0;
-          for (int i = lane; i < p; i += 32) {
-            const double x = xu[i], y = xv[i];
-            al = fma(x, x, al);
-            be = fma(y, y, be);
-            ga = fma(x, y, ga);
+          const double al = nrm[u], be = nrm[v];
+          double g4[4] = {0.0, 0.0, 0.0, 0.0};  // four chains: the dot's latency, not its length
+          int i = lane;
+          for (; i + 96 < p; i += 128) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) g4[u] = fma(xu[i + 32 * u], xv[i + 32 * u], g4[u]);
           }
-          al = warp_sum(al);
-          be = warp_sum(be);
-          ga = warp_sum(ga);
+          for (; i < p; i += 32) g4[0] = fma(xu[i], xv[i], g4[0]);
+          double ga = warp_sum((g4[0] + g4[1]) + (g4[2] + g4[3]));
           if (ga == 0.0 || fabs(ga) <= 2.220446049250313e-16 * sqrt(al * be)) continue;
           rotated = 1;
           // rotation angle (Rutishauser): MUFU reciprocal / reciprocal square
@@ -654,15 +678,29 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
             xu[i] = cs * x - sn * y;
             xv[i] = sn * x + cs * y;
           }
+          double na = al - tt * ga, nb = be + tt * ga;
+          if (!(na > 1e-2 * al && nb > 1e-2 * be)) {  // cancellation: recompute from the rotated columns
+            __syncwarp();
+            double qa = 0.0, qb = 0.0;
+            for (int i = lane; i < p; i += 32) {
+              qa = fma(xu[i], xu[i], qa);
+              qb = fma(xv[i], xv[i], qb);
+            }
+            na = warp_sum(qa);
+            nb = warp_sum(qb);
+          }
+          if (lane == 0) {
+            nrm[u] = na;
+            nrm[v] = nb;
+          }
         }
         __syncthreads();
       }
       for (int s = 0; s < 2; ++s) {
         const int c0 = colof[s];
-        for (int e = tid; e < bw * m; e += kSvdThreads) {
-          const int c = c0 + e / m;
-          if (c < ncol) a.N[(int64_t)c * m + (e % m)] = slot[s][e];
-        }
+        const int nvalid = max(0, min(bw, ncol - c0)) * m;
+        double* dst = a.N + (int64_t)c0 * m;
+        for (int e = tid; e < nvalid; e += kSvdThreads) dst[e] = slot[s][e];
       }
       __threadfence();
       cl.sync();
