@@ -642,7 +642,14 @@ static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev,
   pa.Dh = b.Dd.get();
   pa.Dl = b.Dd.get() + 2 * K;
   {
-    const int pc = pchol_ctas(K);
+    static const int scheme = std::getenv("TF_PCHOL") ? std::atoi(std::getenv("TF_PCHOL")) : 1;  // dev switch: 0 = at most 8 CTAs
+    const int pc = pchol_ctas(K, scheme);
+    if (pc > 8) {
+      static std::once_flag once;
+      std::call_once(once, [] {
+        CK(cudaFuncSetAttribute((const void*)k_pchol_dd, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      });
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)pc);
     cfg.blockDim = dim3(kPcThreads);

@@ -338,7 +338,10 @@ struct PcholArgs {
 
 __device__ __forceinline__ int exact_phi_index(int col, int p, int rev) { return rev ? col - 1 : p - 1 - col; }
 
-inline int pchol_ctas(int K) { return K > 256 ? 8 : K > 96 ? 4 : 1; }
+inline int pchol_ctas(int K, int scheme = 0) {
+  if (scheme == 1) return K > 256 ? 16 : K > 128 ? 8 : K > 48 ? 4 : 1;
+  return K > 256 ? 8 : K > 96 ? 4 : 1;
+}
 
 // One thread-block cluster.  Every CTA keeps an identical copy of the pivot
 // order and of r_kk (it computes the same argmax from the same global Schur
