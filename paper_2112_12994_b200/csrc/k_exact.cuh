@@ -356,6 +356,8 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
   __shared__ double rkh[kPcMaxK], rkl[kPcMaxK];
   __shared__ double wv_h[32], wv_l[32];
   __shared__ int wv_i[32];
+  __shared__ double cand_h[2][16], cand_l[2][16];  // per-CTA pivot candidates of the cluster, by step parity
+  __shared__ int cand_i[2][16];
   __shared__ int s_stop;
   __shared__ double s_x[2];
   const int K = a.K, p = K - 1;
@@ -383,30 +385,43 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
     const double* Dcl = a.Dl + (k & 1) * K;
     double* Dnh = a.Dh + ((k + 1) & 1) * K;
     double* Dnl = a.Dl + ((k + 1) & 1) * K;
-    // (a) pivot: largest Schur diagonal among positions [k, p), ties -> first
+    // (a) pivot: largest Schur diagonal among positions [k, p), ties -> first.
+    // Step 0 scans the diagonal; later steps reduce the per-CTA candidates
+    // the previous step's row computation left in every CTA's shared memory
+    // (cand[k & 1], written through DSMEM before the cluster barrier).
     {
-      const int pos = k + tid;
-      DD v{-INFINITY, 0.0};  // positions past p never win (Schur diagonals may be negative noise)
-      int vi = pos;
-      if (pos < p) v = DD{Dch[perm[pos]], Dcl[perm[pos]]};
+      if (k == 0) {
+        const int pos = k + tid;
+        DD v{-INFINITY, 0.0};  // positions past p never win (Schur diagonals may be negative noise)
+        int vi = pos;
+        if (pos < p) v = DD{Dch[perm[pos]], Dcl[perm[pos]]};
 #pragma unroll
-      for (int m = 16; m > 0; m >>= 1) {
-        const DD o{__shfl_xor_sync(0xffffffffu, v.h, m), __shfl_xor_sync(0xffffffffu, v.l, m)};
-        const int oi = __shfl_xor_sync(0xffffffffu, vi, m);
-        if (dd_gt(o, v) || (o.h == v.h && o.l == v.l && oi < vi)) {
-          v = o;
-          vi = oi;
+        for (int m = 16; m > 0; m >>= 1) {
+          const DD o{__shfl_xor_sync(0xffffffffu, v.h, m), __shfl_xor_sync(0xffffffffu, v.l, m)};
+          const int oi = __shfl_xor_sync(0xffffffffu, vi, m);
+          if (dd_gt(o, v) || (o.h == v.h && o.l == v.l && oi < vi)) {
+            v = o;
+            vi = oi;
+          }
         }
+        if (lane == 0) {
+          wv_h[warp] = v.h;
+          wv_l[warp] = v.l;
+          wv_i[warp] = vi;
+        }
+        __syncthreads();
       }
-      if (lane == 0) {
-        wv_h[warp] = v.h;
-        wv_l[warp] = v.l;
-        wv_i[warp] = vi;
-      }
-      __syncthreads();
-      if (warp == 0) {  // the 32 warp candidates, same tie rule (first position wins)
-        DD b{wv_h[lane], wv_l[lane]};
-        int bi = wv_i[lane];
+      if (warp == 0) {  // the 32 warp candidates / the cluster's CTA candidates, same tie rule
+        const int cb = k & 1;
+        DD b{-INFINITY, 0.0};
+        int bi = 0x7fffffff;
+        if (k == 0) {
+          b = DD{wv_h[lane], wv_l[lane]};
+          bi = wv_i[lane];
+        } else if (lane < nct) {
+          b = DD{cand_h[cb][lane], cand_l[cb][lane]};
+          bi = cand_i[cb][lane];
+        }
 #pragma unroll
         for (int m = 16; m > 0; m >>= 1) {
           const DD o{__shfl_xor_sync(0xffffffffu, b.h, m), __shfl_xor_sync(0xffffffffu, b.l, m)};
@@ -436,23 +451,34 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
     }
     __syncthreads();
     const DD rkk{rkh[k], rkl[k]};
-    // (b) row k: r_kj = (G[ck][col_j] - sum_{i<k} r_ik r_ij) / r_kk, one warp per position j
+    // (b) row k: r_kj = (G[ck][col_j] - sum_{i<k} r_ik r_ij) / r_kk, one warp per position j;
+    // lane 0 also tracks the warp's best updated diagonal (the next pivot's candidates)
+    DD wb{-INFINITY, 0.0};
+    int wbi = 0x7fffffff;
     for (int j = k + 1 + gwarp; j < K; j += nwarps) {
       const int cj = perm[j];
       const double* rjh = a.Rh + (int64_t)cj * K;
       const double* rjl = a.Rl + (int64_t)cj * K;
+      DD g{0.0, 0.0}, dold{0.0, 0.0};
+      if (lane == 0) {  // issued before the dot: their latency overlaps it
+        g = DD{a.Gh[(int64_t)ck * K + cj], a.Gl[(int64_t)ck * K + cj]};
+        if (j < p) dold = DD{Dch[cj], Dcl[cj]};
+      }
       double sh = 0.0, sl = 0.0;
       for (int i = lane; i < k; i += 32) dd_acc2(sh, sl, DD{ch[i], cl[i]}, DD{rjh[i], rjl[i]});
       DD s = dd_warp_sum(dd_two_sum(sh, sl));
       if (lane == 0) {
-        const DD g{a.Gh[(int64_t)ck * K + cj], a.Gl[(int64_t)ck * K + cj]};
         const DD r = dd_div(dd_add(g, dd_neg(s)), rkk);
         a.Rh[(int64_t)cj * K + k] = r.h;
         a.Rl[(int64_t)cj * K + k] = r.l;
         if (j < p) {
-          const DD d = dd_add(DD{Dch[cj], Dcl[cj]}, dd_neg(dd_mul(r, r)));
+          const DD d = dd_add(dold, dd_neg(dd_mul(r, r)));
           Dnh[cj] = d.h;
           Dnl[cj] = d.l;
+          if (dd_gt(d, wb) || (d.h == wb.h && d.l == wb.l && j < wbi)) {
+            wb = d;
+            wbi = j;
+          }
         }
       }
     }
@@ -460,7 +486,33 @@ __global__ void __launch_bounds__(kPcThreads) k_pchol_dd(PcholArgs a) {
       a.Rh[(int64_t)ck * K + k] = rkk.h;
       a.Rl[(int64_t)ck * K + k] = rkk.l;
     }
-    clu.sync();  // barrier.cluster arrive.release / wait.acquire: row k and the diagonal visible cluster-wide
+    // this CTA's best candidate for step k + 1 -> slot [cta] of cand[(k + 1) & 1] in every CTA
+    if (lane == 0) {
+      wv_h[warp] = wb.h;
+      wv_l[warp] = wb.l;
+      wv_i[warp] = wbi;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      DD b{wv_h[lane], wv_l[lane]};
+      int bi = wv_i[lane];
+#pragma unroll
+      for (int m = 16; m > 0; m >>= 1) {
+        const DD o{__shfl_xor_sync(0xffffffffu, b.h, m), __shfl_xor_sync(0xffffffffu, b.l, m)};
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
+        if (dd_gt(o, b) || (o.h == b.h && o.l == b.l && oi < bi)) {
+          b = o;
+          bi = oi;
+        }
+      }
+      if (lane < nct) {  // lane r writes into CTA r
+        const int nb = (k + 1) & 1;
+        *clu.map_shared_rank(&cand_h[nb][cta], lane) = b.h;
+        *clu.map_shared_rank(&cand_l[nb][cta], lane) = b.l;
+        *clu.map_shared_rank(&cand_i[nb][cta], lane) = bi;
+      }
+    }
+    clu.sync();  // barrier.cluster arrive.release / wait.acquire: row k, the diagonal and the candidates visible
   }
   const int kend = s_stop;  // rows kend.. are exact zeros
   // rank (Eigen ColPivHouseholderQR::rank with the prescribed threshold)
