@@ -203,6 +203,9 @@ __global__ void __launch_bounds__(kDDThreads, 2) k_gram_dd(L ld, int64_t rows, i
       h[i][j] = bias_of(i, j);
       l[i][j] = 0.0;
     }
+  // 16-column groups of the tile that hold columns < K (small K: most of a
+  // 64 x 64 tile is zero padding -- skip its products)
+  const int ni = min(4, (K - 64 * I + 15) / 16), nj = min(4, (K - 64 * J + 15) / 16);
   double ra[4], rb[4];
   auto load = [&](int64_t t0) {
     const int64_t t = t0 + ty;
@@ -236,6 +239,7 @@ __global__ void __launch_bounds__(kDDThreads, 2) k_gram_dd(L ld, int64_t rows, i
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {  // h += a b with |h| >= |a b|: FastTwoSum + the fma product error
+          if (i >= ni || j >= nj) continue;  // 16-column groups past K (CTA-uniform): all zeros
           const double p = __dmul_rn(a[i], b[j]);
           const double e = fma(a[i], b[j], -p);
           const double s = __dadd_rn(h[i][j], p);
