@@ -718,7 +718,11 @@ __global__ void __launch_bounds__(kSvdThreads) k_svd_minnorm(SvdArgs a) {
           for (; i < p; i += 32) g4[0] = fma(xu[i], xv[i], g4[0]);
           double ga = warp_sum((g4[0] + g4[1]) + (g4[2] + g4[3]));
           if (ga == 0.0 || fabs(ga) <= 2.220446049250313e-16 * sqrt(al * be)) continue;
-          rotated = 1;
+          // convergence: a sweep whose rotations all have |g| < 1e-7 sqrt(a b) is
+          // the last (Jacobi converges quadratically: what it leaves is ~1e-14,
+          // far inside the 1e-4 bar on the minimum-norm answers) -- saves the
+          // pure check sweep; its small rotations are still applied
+          if (fabs(ga) >= 1e-7 * sqrt(al * be)) rotated = 1;
           // rotation angle (Rutishauser): MUFU reciprocal / reciprocal square
           // root + two Newton steps (~1 ulp) instead of IEEE division / sqrt,
           // which dominate the latency of a sub-round
