@@ -481,6 +481,17 @@ static bool use_i8_gram(const tf_context* ctx, int64_t c, int K) {
   return ctx->gram_mode == 2 || (double)c * K * K >= kI8MinWork;
 }
 
+// K splits of the INT8 GEMM: only when the tiles fill less than half the SMs
+// (K <= 128: 31 tiles), then as many as fill one wave (>= 64 K steps each);
+// more tiles than that gained nothing measurable (the partial tiles' epilogue
+// and the combine's extra reads eat the wave-quantisation gain)
+static int i8_ksplit(int ntiles, int64_t nk, int sms) {
+  if (2 * ntiles > sms) return 1;
+  int ks = std::max(1, sms / ntiles);
+  while (ks > 1 && nk / ks < 64) --ks;
+  return std::min(ks, 8);
+}
+
 static void i8_tables(tf_context* ctx) {
   SolveBufs& b = ctx->sb;
   if (!b.i8_ntiles.empty()) return;
@@ -545,7 +556,12 @@ static void reserve_exact(tf_context* ctx, int64_t c, int Kmax) {
     const int64_t cpad = (c + kI8Tile - 1) / kI8Tile * kI8Tile;
     b.i8D.need((size_t)kI8S * nbs * kI8Tile * cpad);
     b.i8E.need((size_t)nbs * kI8Tile);
-    b.i8P.need((size_t)b.i8_ntiles[nbs] * kI8Tile * kI8N);
+    {
+      size_t mx = 0;  // the largest (tiles x splits) of any block count up to nbs
+      for (int nb = 1; nb <= nbs; ++nb)
+        mx = std::max(mx, (size_t)b.i8_ntiles[nb] * i8_ksplit(b.i8_ntiles[nb], (c + kI8Tile - 1) / kI8Tile, ctx->sm_count));
+      b.i8P.need(mx * kI8Tile * kI8N);
+    }
   }
   b.Gh.need(KK);
   b.Gl.need(KK);
@@ -597,12 +613,13 @@ static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev,
                                                                            (int8_t*)b.i8D.get());
     LAUNCH_CHECK("k_i8_slice");
     smem_optin((const void*)k_i8_gemm, kI8Smem);
-    k_i8_gemm<<<(unsigned)b.i8_ntiles[nbs], kI8Threads, kI8Smem, st>>>(
+    const int ntiles = b.i8_ntiles[nbs], ks = i8_ksplit(ntiles, nk, ctx->sm_count);
+    k_i8_gemm<<<(unsigned)(ntiles * ks), kI8Threads, kI8Smem, st>>>(
         (const int8_t*)b.i8D.get(), nk, reinterpret_cast<const int2*>(b.i8tiles.get()) + b.i8_tile_off[nbs],
-        b.i8P.get());
+        b.i8P.get(), ntiles, ks);
     LAUNCH_CHECK("k_i8_gemm");
     k_i8_combine<<<(unsigned)((KK + 255) / 256), 256, 0, st>>>(b.i8P.get(), b.i8tof.get() + b.i8_tof_off[nbs],
-                                                              kI8S * nbs, K, Kp, b.i8E.get(), gh, gl);
+                                                              kI8S * nbs, K, Kp, b.i8E.get(), gh, gl, ntiles, ks);
     LAUNCH_CHECK("k_i8_combine");
     g_launches += 5;
   } else {

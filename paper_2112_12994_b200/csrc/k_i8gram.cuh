@@ -199,14 +199,21 @@ __device__ __forceinline__ void i8_mbar_wait(uint32_t bar, uint32_t parity) {
 // step; all four warps drain the 256 TMEM columns.  N = 256 halves the operand
 // bytes per MMA of the 128 x 128 version (the kernel was feeding its tensor
 // pipe at 37 % from L2 at 14.8 TB/s; profiles/r02_i8_gemm.txt).
+// Split K (few tiles, small K): CTA blockIdx.x covers tile blockIdx.x % ntiles
+// over the K steps of split blockIdx.x / ntiles and writes its partial tile to
+// out[split][tile]; k_i8_combine adds the splits (int32: every partial is
+// bounded like the whole sum).
 __global__ void __launch_bounds__(kI8Threads) k_i8_gemm(const int8_t* __restrict__ D, int64_t nk,
-                                                        const int2* __restrict__ tiles, int32_t* __restrict__ out) {
+                                                        const int2* __restrict__ tiles, int32_t* __restrict__ out,
+                                                        int ntiles, int ksplit) {
   extern __shared__ __align__(1024) unsigned char i8sm[];
   __shared__ __align__(8) uint64_t full[kI8Stages], empty[kI8Stages], done;
   __shared__ uint32_t tmem_base;
   unsigned char* base = i8sm + ((1024 - (i8_smem_u32(i8sm) & 1023)) & 1023);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int2 tp = tiles[blockIdx.x];  // (I, m)
+  const int tile = (int)(blockIdx.x % (unsigned)ntiles), split = (int)(blockIdx.x / (unsigned)ntiles);
+  const int2 tp = tiles[tile];  // (I, m)
+  const int64_t kb = nk * split / ksplit, ke = nk * (split + 1) / ksplit;  // this CTA's K steps [kb, ke)
   const int8_t* blkA = D + (int64_t)tp.x * nk * 16384;
   const int8_t* blkB0 = D + (int64_t)(2 * tp.y) * nk * 16384;
   const int8_t* blkB1 = D + (int64_t)(2 * tp.y + 1) * nk * 16384;
@@ -228,23 +235,24 @@ __global__ void __launch_bounds__(kI8Threads) k_i8_gemm(const int8_t* __restrict
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
   if (tid == 0) {  // producer
-    for (int64_t k = 0; k < nk; ++k) {
+    for (int64_t k = 0; k < ke - kb; ++k) {
       const int st = (int)(k % kI8Stages);
       if (k >= kI8Stages) i8_mbar_wait(i8_smem_u32(&empty[st]), (uint32_t)(((k / kI8Stages) - 1) & 1));
       const uint32_t fb = i8_smem_u32(&full[st]);
       const uint32_t sA = i8_smem_u32(base + (size_t)st * kI8StageBytes);
+      const int64_t kg = kb + k;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(3u * 16384u) : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sA),
-                   "l"(blkA + k * 16384), "r"(16384), "r"(fb) : "memory");
+                   "l"(blkA + kg * 16384), "r"(16384), "r"(fb) : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       sA + 16384), "l"(blkB0 + k * 16384), "r"(16384), "r"(fb) : "memory");
+                       sA + 16384), "l"(blkB0 + kg * 16384), "r"(16384), "r"(fb) : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       sA + 32768), "l"(blkB1 + k * 16384), "r"(16384), "r"(fb) : "memory");
+                       sA + 32768), "l"(blkB1 + kg * 16384), "r"(16384), "r"(fb) : "memory");
     }
   } else if (tid == 32) {  // MMA issuer
     // instruction descriptor: D s32, A / B s8, K-major, N = 256 (n_dim 32), M = 128 (m_dim 8)
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kI8N >> 3) << 17) | (8u << 24);
-    for (int64_t k = 0; k < nk; ++k) {
+    for (int64_t k = 0; k < ke - kb; ++k) {
       const int st = (int)(k % kI8Stages);
       i8_mbar_wait(i8_smem_u32(&full[st]), (uint32_t)((k / kI8Stages) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -265,7 +273,7 @@ __global__ void __launch_bounds__(kI8Threads) k_i8_gemm(const int8_t* __restrict
   __syncwarp();
   i8_mbar_wait(i8_smem_u32(&done), 0u);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  int32_t* o = out + (size_t)blockIdx.x * 128 * kI8N + (size_t)(32 * warp + lane) * kI8N;
+  int32_t* o = out + (size_t)blockIdx.x * 128 * kI8N + (size_t)(32 * warp + lane) * kI8N;  // [split][tile]
 #pragma unroll 1
   for (int c0 = 0; c0 < kI8N; c0 += 8) {
     uint32_t v[8];
@@ -285,7 +293,8 @@ __global__ void __launch_bounds__(kI8Threads) k_i8_gemm(const int8_t* __restrict
 // in double-double.  tile_of[I * nbt + J] = 2 (index of the tile holding
 // (I, J), I <= J) + (J & 1).
 __global__ void k_i8_combine(const int32_t* __restrict__ P, const int* __restrict__ tile_of, int nbt, int K, int Kp,
-                             const int* __restrict__ E, double* __restrict__ Gh, double* __restrict__ Gl) {
+                             const int* __restrict__ E, double* __restrict__ Gh, double* __restrict__ Gl, int ntiles,
+                             int ksplit) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)K * K) return;
   const int i = (int)(e / K), j = (int)(e % K);
@@ -304,8 +313,10 @@ __global__ void k_i8_combine(const int32_t* __restrict__ P, const int* __restric
         }
         const int I = a / kI8Tile, J = b / kI8Tile;
         const int slot = tile_of[I * nbt + J];  // 2 tile + half
-        const int32_t v = P[((size_t)(slot >> 1) * 128 + (size_t)(a % kI8Tile)) * kI8N + (size_t)(slot & 1) * 128 +
-                            (b % kI8Tile)];
+        const size_t off = ((size_t)(slot >> 1) * 128 + (size_t)(a % kI8Tile)) * kI8N + (size_t)(slot & 1) * 128 +
+                           (b % kI8Tile);
+        int32_t v = 0;
+        for (int sp = 0; sp < ksplit; ++sp) v += P[(size_t)sp * ntiles * 128 * kI8N + off];
         if (v) acc = dd_add(acc, DD{ldexp((double)v, E[i] + E[j] - 7 * (s + u + 2)), 0.0});
       }
   }
