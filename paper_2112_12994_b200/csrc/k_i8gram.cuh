@@ -160,23 +160,35 @@ __global__ void __launch_bounds__(256) k_i8_slice(L ld, int64_t rows, int K, int
   const int64_t t0 = k * kI8Tile + kb0;
   int ej = j < K ? E[j] : 0;
   if (ej == kI8Bad) ej = 0;  // digits are don't-cares: the column's Gram entries become NaN
+  // 2^-E as a multiplier (exact; ldexp only outside the normal exponent range)
+  const bool plain = ej > -1022 && ej < 1022;
+  const double sc = __longlong_as_double((long long)(1023 - ej) << 52);
   double x[16];
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
     const int64_t t = t0 + u;
-    const double a = (j < K && t < rows) ? ldexp(ld(t, j), -ej) : 0.0;
+    double a = 0.0;
+    if (j < K && t < rows) {
+      const double v = ld(t, j);
+      a = plain ? v * sc : ldexp(v, -ej);
+    }
     x[u] = isfinite(a) && fabs(a) < 0.5 ? a : 0.0;
   }
   const int nbs = Kp / kI8Tile;
+  // d = round-half-even(y) by the 1.5 * 2^52 shifter: y + M holds d in its low
+  // mantissa bits (|y| <= 64) and (y + M) - M = d exactly -- the digits rint /
+  // cvt give, in fp64 adds only
+  constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
 #pragma unroll 1
   for (int s = 0; s < kI8S; ++s) {
     uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const double y = x[u] * 128.0;  // exact (power of two)
-      const double d = rint(y);
-      x[u] = y - d;                   // exact: y and d share the exponent range
-      w[u >> 2] |= ((uint32_t)(uint8_t)(int8_t)(int)d) << (8 * (u & 3));
+      const double m = __dadd_rn(y, kShift);
+      const double d = __dsub_rn(m, kShift);
+      x[u] = __dsub_rn(y, d);         // exact: y and d share the exponent range
+      w[u >> 2] |= ((uint32_t)__double2loint(m) & 0xFFu) << (8 * (u & 3));
     }
     const int64_t Ib = (int64_t)s * nbs + j / kI8Tile;
     *reinterpret_cast<uint4*>(D + (Ib * nk + k) * 16384 + i8_lay(j % kI8Tile, kb0)) = make_uint4(w[0], w[1], w[2], w[3]);
