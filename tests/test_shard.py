@@ -150,3 +150,30 @@ def test_sharded_nccl_world1_generated_slice():
     finally:
         dist.destroy_process_group()
     assert np.array_equal(taus, taus_ref) and ps == ps_ref and t_e2e > 0
+
+
+@pytest.mark.gpu
+def test_sharded_nccl_world1_fft_pass_and_int8_gram(monkeypatch):
+    """The row-sharded sweep on the long-lag kernels (TF_PASS=fft: the FFT pass
+    with its double-double spectra from the shard's slice; TF_GRAM=i8: the INT8
+    Gram with the shard's device-side draw count and the max|w| max|y|
+    exponent bound) equals the single-GPU sweep bit for bit at world size 1."""
+    import paper_2112_12994_b200 as tf
+    from paper_2112_12994_b200 import shard
+    monkeypatch.setenv("TF_PASS", "fft")
+    monkeypatch.setenv("TF_GRAM", "i8")
+    y = _series(50000, 8)
+    p_bar, c, seed = 30, 2500, 13
+    ref = tf.lsar_fit(tf.TimeSeries(y), p_bar, c, seed, engine=tf.Engine(0), want_diag=True)
+    dist = _nccl_world1()
+    try:
+        eng = tf.Engine(0)
+        sh = shard.NcclShard(eng, dist, 1, 0, y.size, p_bar)
+        sh.upload_host(y)
+        taus, coefs, secs, pstar, d = sh.lsar_sweep(c, seed, want_diag="light")
+        taus2, *_ = sh.lsar_sweep(c, seed)
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(taus, np.array(ref.pacf.taus)) and np.array_equal(taus2, taus)
+    assert pstar == ref.p_star
+    assert np.array_equal(d["method"], ref.diag["method"])
