@@ -790,7 +790,56 @@ static void launch_fft_series(tf_context* ctx, int64_t w) {
   COUNT_LAUNCH();
 }
 
-static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev) {
+// Deferred folding plan of one sweep (k_fft.cuh, kFftSlots): q0 = the first
+// FFT lag, K groups; residual r_j (j >= q0 - 1) lives in slot (j - q0 + 1) mod K
+// (slot 0 = ctx->r, where the direct pass of lag q0 - 1 left it).  K = 1: the
+// classic state (s_q, r_q in place every lag).
+struct FoldPlan {
+  int K = 1, q0 = 0;
+  int64_t grid = 1;  // the FFT pass's grid (superblock groups depend on it)
+  double* slot[kFftSlots] = {};
+  double* of(int lag) const { return slot[((lag - q0 + 1) % K + K) % K]; }
+  // last lag <= at at which group g folded (q0 - 1: never, the state the direct pass left)
+  int last_fold(int g, int at) const {
+    if (at < q0 + g) return q0 - 1;
+    return q0 + g + ((at - q0 - g) / K) * K;
+  }
+};
+
+static FoldPlan fold_plan(tf_context* ctx, int p_bar, int64_t w) {
+  FoldPlan f;
+  int q0 = 1;
+  while (q0 <= p_bar && !fft_lag(ctx, p_bar, q0)) ++q0;
+  f.q0 = q0;
+  // groups beyond the FFT lags' count buy nothing
+  f.K = std::max(1, std::min(ctx->fft_slots, p_bar - q0 + 1));
+  f.grid = fft_grid(ctx, (w + kFftSB - 1) / kFftSB);
+  f.slot[0] = ctx->r.get();
+  for (int k = 1; k < f.K; ++k) {
+    ctx->fft_rslot[k - 1].need(w);
+    f.slot[k] = ctx->fft_rslot[k - 1].get();
+  }
+  return f;
+}
+
+// the row-mass state a draw at lag p sees (the pass of lag p - 1 is done); K = 0
+// when that pass was not an FFT pass or K = 1 (the classic s, r)
+static PendState pend_state(const FoldPlan& f, int p, const double* Rhist) {
+  PendState ps{};
+  ps.K = 0;
+  if (f.K <= 1 || p - 1 < f.q0) return ps;
+  ps.K = f.K;
+  ps.sbrows = kFftSB;
+  ps.sbgrid = f.grid;
+  ps.navail = std::min(f.K, p - f.q0 + 1);
+  for (int k = 0; k < ps.navail; ++k) ps.pend[k] = f.of(p - ps.navail + k);
+  ps.Rp = Rhist + (p - ps.navail);
+  for (int g = 0; g < f.K; ++g) ps.npg[g] = p - f.last_fold(g, p - 1);
+  return ps;
+}
+
+static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev,
+                            const FoldPlan& f) {
   k_fft_taps_dd<<<kFftN * kTapSplit / 256, 256, 0, ctx->stream>>>(phi, q, ctx->fftH.get(), ctx->fftTwH.get(),
                                                                    ctx->fftTwL.get());
   FftPassArgs a{};
@@ -799,8 +848,20 @@ static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi
   a.tw = ctx->fftTw.get();
   a.w = w;
   a.s = ctx->s.get();
-  a.r = ctx->r.get();
-  a.Rprev = Rprev;
+  a.K = f.K;
+  if (f.K <= 1) {  // classic: s_q = s_{q-1} + r_{q-1}^2 / R_{q-1}, r_q over r_{q-1}
+    a.fold = 0;
+    a.npend = 1;
+    a.pend[0] = ctx->r.get();
+    a.Rp = Rprev;
+    a.rout = ctx->r.get();
+  } else {
+    a.fold = (q - f.q0) % f.K;
+    a.npend = q - f.last_fold(a.fold, q - 1);
+    for (int k = 0; k < a.npend; ++k) a.pend[k] = f.of(q - a.npend + k);
+    a.Rp = ctx->Rhist.get() + (q - a.npend);
+    a.rout = f.of(q);
+  }
   a.chunkA = ctx->chunkA.get();
   a.chunkB = ctx->chunkB.get();
   a.tileA = ctx->tileA.get();
@@ -813,10 +874,34 @@ static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi
   else if (pf == 1) k_lsar_pass_fft<1><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   else if (pf == 3) k_lsar_pass_fft<3><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   else if (pf == 4) k_lsar_pass_fft<4><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
-
   else k_lsar_pass_fft<2><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   LAUNCH_CHECK("k_lsar_pass_fft");
   g_launches += 2;
+}
+
+// after the last pass (lag p_bar) of a deferred sweep: s_{p_bar} (every group's
+// pending residuals but r_{p_bar} folded) and r_{p_bar} into ctx->s / ctx->r
+__global__ void k_fold_all(double* __restrict__ s, double* __restrict__ r, int64_t w, PendState ps) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= w) return;
+  const double rl = ps.pend[ps.navail - 1][row];
+  ps.navail -= 1;  // r_{p_bar} stays unfolded
+  const int64_t sb = row / ps.sbrows;
+  const int g = (int)((sb + sb / ps.sbgrid) % ps.K);
+  if (g == 0) ps.npg[0] -= 1;
+  else if (g == 1) ps.npg[1] -= 1;
+  else if (g == 2) ps.npg[2] -= 1;
+  else ps.npg[3] -= 1;
+  s[row] = pend_mass(ps, s, row);
+  r[row] = rl;
+}
+
+static void finish_fold(tf_context* ctx, const FoldPlan& f, int p_bar, int64_t w) {
+  const PendState ps = pend_state(f, p_bar + 1, ctx->Rhist.get());
+  if (ps.K <= 1) return;
+  k_fold_all<<<(unsigned)((w + 255) / 256), 256, 0, ctx->stream>>>(ctx->s.get(), ctx->r.get(), w, ps);
+  LAUNCH_CHECK("k_fold_all");
+  COUNT_LAUNCH();
 }
 
 // max |y| over the window's series values (y[0 .. rows)) into ctx->ymax (bit pattern)
@@ -908,8 +993,9 @@ static void launch_scan(tf_context* ctx, int64_t ntile, int lag, int check_r, in
 }
 
 static void launch_draw(tf_context* ctx, uint64_t seed, int64_t c, int64_t w, int64_t* idx,
-                        double* wts, const uint64_t* seed_ptr = nullptr) {
+                        double* wts, const uint64_t* seed_ptr = nullptr, PendState ps = PendState{}) {
   DrawArgs a{};
+  a.ps = ps;
   a.shard = 0;
   a.accept = nullptr;
   a.seed_ptr = nullptr;
@@ -936,8 +1022,8 @@ static void launch_draw(tf_context* ctx, uint64_t seed, int64_t c, int64_t w, in
 }
 
 static void launch_fixed_weights(tf_context* ctx, const int64_t* idx, int64_t c, const double* s, const double* r,
-                                 double* wts) {
-  k_fixed_weights<<<(unsigned)((c + 255) / 256), 256, 0, ctx->stream>>>(idx, c, ctx->scal.get(), s, r, wts);
+                                 double* wts, PendState ps = PendState{}) {
+  k_fixed_weights<<<(unsigned)((c + 255) / 256), 256, 0, ctx->stream>>>(idx, c, ctx->scal.get(), s, r, wts, ps);
   LAUNCH_CHECK("k_fixed_weights");
   COUNT_LAUNCH();
 }
@@ -1097,6 +1183,7 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
   ctx->sb.M.need((size_t)c * ldq_of(2));  // the p = 1 Gram's dense staging (no allocation inside the loop)
   const bool use_fft = fft_sweep(ctx, p_bar);
   if (use_fft) reserve_fft(ctx, w);
+  const FoldPlan fp = use_fft ? fold_plan(ctx, p_bar, w) : FoldPlan{};
   ctx->ymax.need(1);
   const unsigned long long* ybits = ctx->ymax.get();
   const int rn2 = d && d->rnorm2_out;
@@ -1121,9 +1208,9 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
       if (fixed) {
         idx = ctx->fidx.get() + (size_t)(p - 1) * c;
         if (fixed_wts) wts = ctx->fw.get() + (size_t)(p - 1) * c;
-        else launch_fixed_weights(ctx, idx, c, ctx->s.get(), ctx->r.get(), wts);
+        else launch_fixed_weights(ctx, idx, c, ctx->s.get(), ctx->r.get(), wts, pend_state(fp, p, ctx->Rhist.get()));
       } else {
-        launch_draw(ctx, 0, c, w, idx, wts, ctx->seedtab.get() + p);
+        launch_draw(ctx, 0, c, w, idx, wts, ctx->seedtab.get() + p, pend_state(fp, p, ctx->Rhist.get()));
       }
       if (want_hist) {
         CK(cudaMemcpyAsync(ctx->idx_hist.get() + (size_t)(p - 1) * c, idx, c * sizeof(int64_t),
@@ -1138,7 +1225,7 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
       solve_exact(ctx, FwdRows{ctx->y.get(), idx, wts, 0}, c, p + 1, /*rev=*/0, o, nullptr, false, ybits);
       if (phases) rec(ctx->pev[2 * (p - 1) + 1]);
       // residuals of the lag-p window fit + score update s_p = s_{p-1} + r_{p-1}^2/R_{p-1}
-      if (fft_lag(ctx, p_bar, p)) launch_pass_fft(ctx, p, w, ctx->phi.get(), ctx->scal.get());
+      if (fft_lag(ctx, p_bar, p)) launch_pass_fft(ctx, p, w, ctx->phi.get(), ctx->scal.get(), fp);
       else launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());
       rec(ctx->events[p]);
     }
@@ -1149,6 +1236,7 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
   // the buffers: graph capture/replay (run_graphed).
   const int mode = (fixed ? 1 : 0) | (want_hist ? 2 : 0) | (phases ? 4 : 0) | (rn2 ? 8 : 0) | (fixed_wts ? 16 : 0);
   const int64_t launches = run_graphed(ctx, ctx->lsar_graph, w, c, p_bar, mode, capturing, record);
+  if (d && (d->scores_out || d->resid_out)) finish_fold(ctx, fp, p_bar, w);  // s_{p_bar}, r_{p_bar} into s / r
   CK(cudaStreamSynchronize(st));
   int sth[3];
   CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
@@ -2439,6 +2527,7 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
   CK(cudaMemsetAsync(ctx->sh_par.get(), 0, 4 * sizeof(double), st));
   const bool use_fft = fft_sweep(ctx, p_bar);
   if (use_fft) reserve_fft(ctx, w);
+  const FoldPlan fp = use_fft ? fold_plan(ctx, p_bar, w) : FoldPlan{};
   ctx->ymax.need(1);
   const unsigned long long* ybits = ctx->ymax.get();
   const int64_t nt = (c + kScanTileN - 1) / kScanTileN;
@@ -2486,6 +2575,7 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
       a.shard = 1;
       a.par = ctx->sh_par.get();
       a.accept = ctx->rh_ok.get();
+      a.ps = pend_state(fp, p, ctx->Rhist.get());
       k_draw<<<(unsigned)((c + kDrawPerCta - 1) / kDrawPerCta), kDrawThreads, 0, st>>>(a);
       LAUNCH_CHECK("k_draw (shard)");
       COUNT_LAUNCH();
@@ -2498,7 +2588,7 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
       solve_exact(ctx, FwdRows{ctx->y.get(), ctx->sh_idx.get(), ctx->sh_wts.get(), 0}, c, p + 1, /*rev=*/0, o, kdev,
                   /*sharded=*/true, ybits);
       if (phases) rec(ctx->pev[2 * (p - 1) + 1]);
-      if (fft_lag(ctx, p_bar, p)) launch_pass_fft(ctx, p, w, ctx->phi.get(), ctx->sh_par.get());
+      if (fft_lag(ctx, p_bar, p)) launch_pass_fft(ctx, p, w, ctx->phi.get(), ctx->sh_par.get(), fp);
       else launch_pass(ctx, p, w, ctx->phi.get(), ctx->sh_par.get());  // R_{p-1} = par[0]
       rec(ctx->events[p]);
     }
@@ -2910,6 +3000,8 @@ tf_status tf_create(const tf_opts* opts, tf_context** out) {
     ctx->pass_mode = pm && !std::strcmp(pm, "dmma") ? 1 : pm && !std::strcmp(pm, "fft") ? 2 : 0;
     const char* mq = std::getenv("TF_FFT_MINQ");  // crossover lag of the auto mode
     ctx->fft_minq = mq ? std::max(1, std::atoi(mq)) : tfe::kFftMinQ;
+    const char* fs = std::getenv("TF_FFT_SLOTS");  // deferred-folding groups of the FFT pass (1..4)
+    ctx->fft_slots = fs ? std::min(tfk::kFftSlots, std::max(1, std::atoi(fs))) : tfk::kFftSlots;
   }
   int least = 0, greatest = 0;
   cudaDeviceGetStreamPriorityRange(&least, &greatest);

@@ -358,14 +358,38 @@ __device__ __forceinline__ void warp_reduce24(double (&x)[24], int lane) {
   }
 }
 
+// Deferred score folding (kFftSlots residual arrays): the fold of r_j^2 / R_j
+// into s is per row a read-modify-write of s (16 B/row), so it is done for one
+// group of superblocks per lag -- group g = (sb + sb / grid) mod K (each CTA of
+// the persistent grid folds every K-th superblock it visits) folds at the lags
+// q0 + g + m K and then adds its K pending residuals r_{q-K} .. r_{q-1} in lag
+// order (the same fma sequence as one fold per lag: bit-identical s).  The
+// other K - 1 groups only read the spectrum and write r_q (18.7 B/row), their
+// 32-row chunk sums of s advanced by the chunk recurrence A_q = A_{q-1} +
+// B_{q-1} / R_{q-1}.  Residual r_j lives in slot (j - q0 + 1) mod K until every
+// group has folded it; a draw at a row computes the exact s_{q+1}(row) from s
+// and the row group's pending residuals (PendState).  K = 1: one fold per lag
+// for every superblock (s_q and r_q in place).
+constexpr int kFftSlots = 4;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 struct FftPassArgs {
   const double2* Z;  // [nsb][4096] series spectra (k_fft_series_dd)
   const double2* H;  // [4096] filter spectrum of this lag / N (k_fft_taps_dd)
   const double2* tw;
   int64_t w;
-  double* s;  // in s_{q-1}, out s_q
-  double* r;  // in r_{q-1}, out r_q
-  const double* Rprev;
+  double* s;  // the folded scores of the folding group (in place)
+  int K;      // superblock groups (1: every superblock folds every lag)
+  int fold;   // the group folding at this lag
+  int npend;  // its pending residuals (oldest first), 1..K
+  const double* pend[kFftSlots];
+  const double* Rp;  // R of the pending lags [npend]; Rp[npend - 1] = R_{q-1}
+  double* rout;      // r_q (may alias pend[0]: read before written, same thread)
   double* chunkA;
   double* chunkB;
   double* tileA;
@@ -381,13 +405,15 @@ template <int PF>
 __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
   extern __shared__ double2 fsm[];
   __shared__ double csA[kFftChunksSB], csB[kFftChunksSB];
+  __shared__ double coA[kFftChunksSB], coB[kFftChunksSB];  // non-folding superblock: chunk sums of lag q - 1
   double2* buf = fsm;
   double2* tw = fsm + kFftBufC;
   fft_load_tw(tw, a.tw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t w = a.w;
   const int64_t nsb = (w + kFftSB - 1) / kFftSB;
-  const double invR = 1.0 / *a.Rprev;
+  __shared__ double invRp[kFftSlots];  // 1 / R of the pending lags (shared: no registers held)
+  if (t < kFftSlots) invRp[t] = t < a.npend ? 1.0 / a.Rp[t] : 0.0;
   // L2 prefetch (cp.async.bulk.prefetch) of a superblock's spectrum and state:
   // this CTA's first superblock's state now, the next one's inputs while the
   // current one computes -- the state loads after the FFT then hit L2
@@ -396,9 +422,9 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
     const int64_t r0 = p * kFftSB;
     const uint32_t bytes = (uint32_t)(min((int64_t)kFftSB, w - r0) * 8) & ~15u;
     if (spectrum) bulk_prefetch_l2(a.Z + p * kFftN, kFftN * sizeof(double2));
-    if (bytes) {
+    if (bytes && (a.K == 1 || (int)((p + p / gridDim.x) % a.K) == a.fold)) {
       bulk_prefetch_l2(a.s + r0, bytes);
-      bulk_prefetch_l2(a.r + r0, bytes);
+      for (int k = 0; k < a.npend; ++k) bulk_prefetch_l2(a.pend[k] + r0, bytes);
     }
   };
   // PF 4: the spectrum goes through shared memory -- a TMA bulk copy of the
@@ -422,6 +448,15 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
     if (PF >= 2 && t == 0) prefetch(sb, false);
     if (PF >= 3 && t == 0 && sb + gridDim.x < nsb)
       bulk_prefetch_l2(a.Z + (sb + gridDim.x) * kFftN, kFftN * sizeof(double2));
+    // group of sb: (sb + sb / grid) mod K -- each CTA folds every K-th superblock it visits (balanced)
+    const bool fold = a.K == 1 || (int)((sb + sb / gridDim.x) % a.K) == a.fold;
+    if (!fold && t < kFftChunksSB) {  // the previous chunk sums, in flight during the transform
+      const int64_t cg = sb * kFftChunksSB + t;
+      if (cg * kChunk < w) {
+        cp_async8(coA + t, a.chunkA + cg);
+        cp_async8(coB + t, a.chunkB + cg);
+      }
+    }
     double2 v[16];
     if (PF == 4) {
       mbar_wait(&zbar, zphase);
@@ -434,8 +469,9 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
       for (int r = 0; r < 16; ++r) v[r] = cmul(__ldcs(Zs + 256 * r), __ldg(a.H + t + 256 * r));
     }
     fft4096<1>(v, buf, tw);
+    cp_async_wait_all();
+    __syncthreads();  // every thread's last-stage reads of buf are done; coA / coB landed
     if (PF == 4) {
-      __syncthreads();  // every thread's last-stage reads of buf are done
       if (t == 0 && sb + gridDim.x < nsb) {
         fence_proxy_async_smem();
         mbar_expect_tx(&zbar, kZBytes);
@@ -447,18 +483,34 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
     // i >= 12 = r_q^2 of rows r = i - 8, reduced over the warp in one warp_reduce24.
     const int64_t base = sb * kFftSB + t;
     double* __restrict__ sp = a.s;
-    double* __restrict__ rp = a.r;
+    double* rp = a.rout;  // may alias pend[0] (same rows: loaded above, stored below)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       double x[24];
 #pragma unroll
       for (int g = 0; g < 2; ++g) {
-        double so[6], ro[6];
+        double so[6];
+        if (fold) {
+          double ro[6];
 #pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          const int64_t row = base + h * kFftL + 256 * (6 * g + j);
-          so[j] = row < w ? __ldcs(sp + row) : 0.0;
-          ro[j] = row < w ? __ldcs(rp + row) : 0.0;
+          for (int j = 0; j < 6; ++j) {
+            const int64_t row = base + h * kFftL + 256 * (6 * g + j);
+            so[j] = row < w ? __ldcs(sp + row) : 0.0;
+            ro[j] = row < w ? __ldcs(a.pend[0] + row) : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < 6; ++j) so[j] = fma(ro[j] * ro[j], invRp[0], so[j]);
+#pragma unroll
+          for (int k = 1; k < kFftSlots; ++k) {
+            if (k >= a.npend) break;
+#pragma unroll
+            for (int j = 0; j < 6; ++j) {
+              const int64_t row = base + h * kFftL + 256 * (6 * g + j);
+              ro[j] = row < w ? __ldcs(a.pend[k] + row) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 6; ++j) so[j] = fma(ro[j] * ro[j], invRp[k], so[j]);
+          }
         }
 #pragma unroll
         for (int j = 0; j < 6; ++j) {
@@ -467,8 +519,10 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
           const double rq = h ? v[4 + i].y : v[4 + i].x;
           double sn = 0.0, rs = 0.0;
           if (row < w) {
-            sn = fma(ro[j] * ro[j], invR, so[j]);
-            __stcs(sp + row, sn);
+            if (fold) {
+              sn = so[j];
+              __stcs(sp + row, sn);
+            }
             __stcs(rp + row, rq);
             rs = rq;
           }
@@ -478,16 +532,23 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
       }
       warp_reduce24(x, lane);
       const int sel = lane & 3;
+      const int vi = 12 * ((lane >> 4) & 1) + 6 * ((lane >> 3) & 1) + 3 * ((lane >> 2) & 1) + sel;
+      const int cl = 96 * h + 8 * (vi % 12) + warp;  // chunk of the superblock
+      const int64_t cg = sb * kFftChunksSB + cl;
+      const bool live = sel != 3 && cg * kChunk < w;
+      if (!fold) {
+        // chunk sum of s_q by the recurrence A_q = A_{q-1} + B_{q-1} / R_{q-1}
+        double nA = 0.0;
+        if (live && vi < 12) nA = fma(coB[cl], invRp[a.npend - 1], coA[cl]);  // 1 / R_{q-1}
+        if (vi < 12) x[0] = nA;
+      }
       if (sel != 3) {
-        const int vi = 12 * ((lane >> 4) & 1) + 6 * ((lane >> 3) & 1) + 3 * ((lane >> 2) & 1) + sel;
-        const int cl = 96 * h + 8 * (vi % 12) + warp;  // chunk of the superblock
-        const int64_t cg = sb * kFftChunksSB + cl;
         if (vi < 12) {
           csA[cl] = x[0];
-          if (cg * kChunk < w) a.chunkA[cg] = x[0];
+          if (live) a.chunkA[cg] = x[0];
         } else {
           csB[cl] = x[0];
-          if (cg * kChunk < w) a.chunkB[cg] = x[0];
+          if (live) a.chunkB[cg] = x[0];
         }
       }
     }

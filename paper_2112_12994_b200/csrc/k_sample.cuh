@@ -149,6 +149,35 @@ __global__ void __launch_bounds__(kScanThreads)
   }
 }
 
+// Row masses under the FFT pass's deferred folding (k_fft.cuh, kFftSlots):
+// s_{q+1}(row) = s(row) + the row group's pending r_j^2 / R_j in lag order --
+// the fma sequence the classic fold applies once per lag (bit-identical).
+// K <= 1: classic state (s_q, r_q in place; DrawArgs::s / r).
+struct PendState {
+  int K;            // superblock groups
+  int navail;       // residual arrays in pend (oldest first)
+  int64_t sbrows;   // rows per superblock
+  int64_t sbgrid;   // the FFT pass's grid: superblock sb is in group (sb + sb / sbgrid) mod K
+  const double* pend[4];
+  const double* Rp;  // R of the pend lags
+  int npg[4];        // per group: the newest npg[g] arrays are not yet folded into s
+};
+__device__ __forceinline__ double pend_mass(const PendState& ps, const double* __restrict__ s, int64_t row) {
+  double m = s[row];
+  const int64_t sb = row / ps.sbrows;
+  const int g = (int)((sb + sb / ps.sbgrid) % ps.K);
+  const int np = g == 0 ? ps.npg[0] : g == 1 ? ps.npg[1] : g == 2 ? ps.npg[2] : ps.npg[3];
+  const int k0 = ps.navail - np;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k >= k0 && k < ps.navail) {
+      const double rv = ps.pend[k][row];
+      m = fma(rv * rv, 1.0 / ps.Rp[k], m);
+    }
+  }
+  return m;
+}
+
 struct DrawArgs {
   uint64_t seed;        // derive_seed(user_seed, p)
   const uint64_t* seed_ptr;  // nullable: read the seed from device memory (graph replays)
@@ -163,6 +192,7 @@ struct DrawArgs {
   const double* chunkB;
   const double* s;      // s_q
   const double* r;      // r_q (nullable: plain scores, r = 0)
+  PendState ps;         // ps.K > 1: deferred folding (s, r above unused for the row masses)
   int64_t w;
   int64_t* idx;
   double* wts;
@@ -344,7 +374,9 @@ __global__ void __launch_bounds__(kDrawThreads) k_draw(DrawArgs a) {
     const int64_t row = r0 + RPL * g.sl + j;
     mass[j] = 0.0;
     if (row < a.w) {
-      if (a.r) {
+      if (a.ps.K > 1) {
+        mass[j] = pend_mass(a.ps, a.s, row);
+      } else if (a.r) {
         const double rv = a.r[row];
         mass[j] = fma(rv * rv, invR, a.s[row]);  // exactly the s_{q+1} the next pass stores
       } else {
@@ -522,13 +554,16 @@ __global__ void k_shard_seg(const double* __restrict__ gS, int world, int rank, 
 // uses (weight 1/sqrt(c * pi_i), sketch.cpp:56-57; mass = s + r^2/R as the
 // next pass stores it, or the plain score when r is null).
 __global__ void k_fixed_weights(const int64_t* __restrict__ idx, int64_t c, const double* __restrict__ scal,
-                                const double* __restrict__ s, const double* __restrict__ r, double* __restrict__ wts) {
+                                const double* __restrict__ s, const double* __restrict__ r, double* __restrict__ wts,
+                                PendState ps) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= c) return;
   const double R = scal[0], S = scal[1];
   const int64_t row = idx[t];
   double mp = s[row];
-  if (r) {
+  if (ps.K > 1) {
+    mp = pend_mass(ps, s, row);
+  } else if (r) {
     const double rv = r[row];
     mp = fma(rv * rv, 1.0 / R, mp);
   }
