@@ -727,12 +727,16 @@ static void solve_exact(tf_context* ctx, const L& ld, int64_t c, int K, int rev,
 constexpr int kPassPstMinQ = 1;  // sweeps: tensor-core persistent pass for every lag q >= 1
 
 // FFT pass (k_fft.cuh) for the lags where the direct FIR is fp64-bound; the
-// crossover (lag kFftMinQ) is measured.
-constexpr int kFftMinQ = 96;
+// crossover (lag kFftMinQ) is measured (the FFT pass is faster
+// from lag 61 on at C4).  A sweep uses it only when enough lags (kFftMinLags)
+// follow the crossover to pay for the once-per-sweep series spectra (about
+// seven lag passes).
+constexpr int kFftMinQ = 64;
+constexpr int kFftMinLags = 32;
 
 static bool fft_sweep(const tf_context* ctx, int p_bar) {
   if (ctx->pass_mode == 1 || p_bar > kFftD) return false;
-  return ctx->pass_mode == 2 || p_bar >= ctx->fft_minq;
+  return ctx->pass_mode == 2 || p_bar >= ctx->fft_minq + ctx->fft_minlags;
 }
 static bool fft_lag(const tf_context* ctx, int p_bar, int q) {
   return q >= 1 && fft_sweep(ctx, p_bar) && (ctx->pass_mode == 2 || q >= ctx->fft_minq);
@@ -774,6 +778,7 @@ static void reserve_fft(tf_context* ctx, int64_t w) {
   smem_optin((const void*)k_lsar_pass_fft<2>, fft_smem_bytes());
   smem_optin((const void*)k_lsar_pass_fft<3>, fft_smem_bytes());
   smem_optin((const void*)k_lsar_pass_fft<4>, fft_smem_bytes());
+  smem_optin((const void*)k_lsar_pass_fft<4, 1>, fft_smem_bytes());
 
 }
 
@@ -870,7 +875,10 @@ static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi
   // prefetch variant (dev switch TF_FFT_PF, measured in profiles/r02_fft_prefetch.txt): 4 (state of
   // this superblock and spectrum of the next to L2, the spectrum through shared memory by TMA) is the fastest
   static const int pf = std::getenv("TF_FFT_PF") ? std::atoi(std::getenv("TF_FFT_PF")) : 4;
-  if (pf == 0) k_lsar_pass_fft<0><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
+  // twiddles (dev switch TF_FFT_TW): 1 = powers of one table entry per stage formed in registers
+  static const int twm = std::getenv("TF_FFT_TW") ? std::atoi(std::getenv("TF_FFT_TW")) : 1;
+  if (pf == 4 && twm == 1) k_lsar_pass_fft<4, 1><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
+  else if (pf == 0) k_lsar_pass_fft<0><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   else if (pf == 1) k_lsar_pass_fft<1><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   else if (pf == 3) k_lsar_pass_fft<3><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   else if (pf == 4) k_lsar_pass_fft<4><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
@@ -3000,6 +3008,7 @@ tf_status tf_create(const tf_opts* opts, tf_context** out) {
     ctx->pass_mode = pm && !std::strcmp(pm, "dmma") ? 1 : pm && !std::strcmp(pm, "fft") ? 2 : 0;
     const char* mq = std::getenv("TF_FFT_MINQ");  // crossover lag of the auto mode
     ctx->fft_minq = mq ? std::max(1, std::atoi(mq)) : tfe::kFftMinQ;
+    ctx->fft_minlags = mq ? 0 : tfe::kFftMinLags;  // a forced crossover is taken as given
     const char* fs = std::getenv("TF_FFT_SLOTS");  // deferred-folding groups of the FFT pass (1..4)
     ctx->fft_slots = fs ? std::min(tfk::kFftSlots, std::max(1, std::atoi(fs))) : tfk::kFftSlots;
   }

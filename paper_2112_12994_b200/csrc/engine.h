@@ -106,7 +106,7 @@ struct tf_context {
   // 1 direct FIR only, 2 FFT at every lag >= 1
   tfe::DBuf<double2> fftZ, fftH, fftTw, fftTwH, fftTwL;  // fftTwH/L: W_4096^e, e < 4096, double-double
   tfe::DBuf<unsigned long long> ymax;  // max |y| of the resident series (bit pattern), per sweep
-  int pass_mode = 0, fft_minq = 0;
+  int pass_mode = 0, fft_minq = 0, fft_minlags = 0;
   int fft_slots = 4;                // deferred folding groups of the FFT pass (k_fft.cuh kFftSlots; 1 = fold per lag)
   tfe::DBuf<double> fft_rslot[3];   // residual slots 1..3 (slot 0 is r)
   int gram_mode = 0;  // 0 auto (INT8 tensor-core Gram above a work threshold), 1 double-double CUDA cores, 2 INT8 whenever c fits

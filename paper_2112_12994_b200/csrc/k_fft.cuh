@@ -133,7 +133,37 @@ __device__ __forceinline__ void fft16(double2 (&v)[16]) {
 // 256); on return v[r] = X[t + 256 r].  buf: kFftBufC padded slots; tw: the
 // two twiddle tables in shared memory.  Begins with a barrier (buf may still be
 // read by the previous call) and ends without one.
+// v[r] *= w1^r (S = -1) or conj(w1)^r (S = +1), r = 1..15, the powers formed
+// in registers from the one table entry w1: 14 complex products at depth <= 5
+// (w2 = w1^2, w3 = w2 w1, w4 = w2^2, w8 = w4^2, w12 = w8 w4 and the bases times
+// w1..w3) in place of 15 (stage 2) / 30 (stage 3) 16-byte shared-memory loads
+// per thread -- those loads were half of the transform's shared-memory
+// wavefronts (index (t & 15) r: stride-r bank conflicts), on the L1 pipe that
+// bounds the pass.  The powers carry <= ~8 eps of relative error, like the
+// transform's own rounding: relative to the residual spectrum (see Rounding).
 template <int S>
+__device__ __forceinline__ void tw_powers(double2 (&v)[16], double2 w1) {
+  const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1), w4 = cmul(w2, w2);
+  v[1] = ctw<S>(v[1], w1);
+  v[2] = ctw<S>(v[2], w2);
+  v[3] = ctw<S>(v[3], w3);
+  v[4] = ctw<S>(v[4], w4);
+  double2 b = w4;
+#pragma unroll
+  for (int g = 1; g < 4; ++g) {
+    v[4 * g + 1] = ctw<S>(v[4 * g + 1], cmul(b, w1));
+    v[4 * g + 2] = ctw<S>(v[4 * g + 2], cmul(b, w2));
+    v[4 * g + 3] = ctw<S>(v[4 * g + 3], cmul(b, w3));
+    if (g < 3) {
+      b = cmul(b, w4);
+      v[4 * g + 4] = ctw<S>(v[4 * g + 4], b);
+    }
+  }
+}
+
+// TW: 0 twiddles from the two tables (W_256^{(t&15) r}; W_256^{(t>>4) r} W_4096^{(t&15) r}),
+// 1 powers of one table entry per stage (tw_powers)
+template <int S, int TW = 0>
 __device__ __forceinline__ void fft4096(double2 (&v)[16], double2* buf, const double2* tw) {
   const int t = threadIdx.x;
   const double2* tw256 = tw;
@@ -147,8 +177,12 @@ __device__ __forceinline__ void fft4096(double2 (&v)[16], double2* buf, const do
   // stage 2 (Ns = 16): twiddle W_256^{(t & 15) r}; out -> buf[(t >> 4) 256 + (t & 15) + 16 r]
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = buf[fpad(t + 256 * r)];
+  if (TW == 1) {
+    tw_powers<S>(v, tw256[t & 15]);
+  } else {
 #pragma unroll
-  for (int r = 1; r < 16; ++r) v[r] = ctw<S>(v[r], tw256[(t & 15) * r]);
+    for (int r = 1; r < 16; ++r) v[r] = ctw<S>(v[r], tw256[(t & 15) * r]);
+  }
   fft16<S>(v);
   __syncthreads();
   const int d2 = (t >> 4) * 256 + (t & 15);
@@ -158,8 +192,12 @@ __device__ __forceinline__ void fft4096(double2 (&v)[16], double2* buf, const do
   // stage 3 (Ns = 256): twiddle W_4096^{t r} = W_256^{(t >> 4) r} W_4096^{(t & 15) r}; natural order out
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = buf[fpad(t + 256 * r)];
+  if (TW == 1) {
+    tw_powers<S>(v, twlo[t]);  // W_4096^t
+  } else {
 #pragma unroll
-  for (int r = 1; r < 16; ++r) v[r] = ctw<S>(v[r], cmul(tw256[(t >> 4) * r], twlo[(t & 15) * r]));
+    for (int r = 1; r < 16; ++r) v[r] = ctw<S>(v[r], cmul(tw256[(t >> 4) * r], twlo[(t & 15) * r]));
+  }
   fft16<S>(v);
 }
 
@@ -401,7 +439,7 @@ struct FftPassArgs {
 // state to L2 at the start of its iteration, 3 = 2 + the next superblock's
 // spectrum to L2, 4 = 3 + the spectrum through shared memory by TMA (the
 // default; profiles/r02_fft_prefetch.txt)
-template <int PF>
+template <int PF, int TW = 0>
 __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
   extern __shared__ double2 fsm[];
   __shared__ double csA[kFftChunksSB], csB[kFftChunksSB];
@@ -468,7 +506,7 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
 #pragma unroll
       for (int r = 0; r < 16; ++r) v[r] = cmul(__ldcs(Zs + 256 * r), __ldg(a.H + t + 256 * r));
     }
-    fft4096<1>(v, buf, tw);
+    fft4096<1, TW>(v, buf, tw);
     cp_async_wait_all();
     __syncthreads();  // every thread's last-stage reads of buf are done; coA / coB landed
     if (PF == 4) {

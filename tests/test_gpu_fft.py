@@ -178,7 +178,9 @@ def test_fft_first_lag_abi(tf, monkeypatch):
     4096-point blocks' filter length (direct FIR only)"""
     e = tf.Engine(0)
     try:
-        assert e.fft_first_lag(500) == 96
+        assert e.fft_first_lag(500) == 64
+        assert e.fft_first_lag(96) == 64
+        assert e.fft_first_lag(95) == 96  # too few lags past the crossover to pay for the series spectra
         assert e.fft_first_lag(50) == 51  # below the crossover: no FFT lag
         assert e.fft_first_lag(2000) == 2001  # q > D = 1024: direct FIR only
     finally:
