@@ -314,8 +314,13 @@ def run_ours(args):
             "traffic": load_traffic("k_lsar_pass_fft"),
             "algorithmic_per_unit": "24 B per window row per lag (read y, read s, write s); one launch = "
                                     f"{w_rows} rows; the FIR by FFT is O(log N) flop/row, far below the fp64 peak",
-            "moved_per_unit": "42.7 B per row: the series spectrum (10.7 B, computed once per sweep in "
-                              "double-double) + s, r in + s, r out"}
+            "moved_per_unit": "30.7 B per row: the series spectrum (10.7 B, computed once per sweep in "
+                              "double-double) + r_q out (8 B) + the deferred score update (each superblock "
+                              "folds its 4 pending residuals into s every 4th lag: (8 + 4*8 + 8)/4 = 12 B)",
+            "kernels": "k_lsar_pass_fft (transform -> r_q, chunk sums of r_q^2) + k_fft_fold (score update); "
+                       "in the timed sweeps k_fft_fold runs on a second stream beside the lag's solve; in the "
+                       "instrumented sweep these per-lag times come from, it runs on the main stream inside "
+                       "the pass interval, so avg_ms is the two kernels back to back"}
     if n_dmma:
         fl = sum((2.0 * p + 4.0) * w_rows for p in lags[dmma])
         roof = sum(max(24.0 * w_rows / (hbm_peak * 1e9), (2.0 * p + 4.0) * w_rows / (fp64_peak * 1e12))

@@ -778,7 +778,9 @@ static void reserve_fft(tf_context* ctx, int64_t w) {
   smem_optin((const void*)k_lsar_pass_fft<2>, fft_smem_bytes());
   smem_optin((const void*)k_lsar_pass_fft<3>, fft_smem_bytes());
   smem_optin((const void*)k_lsar_pass_fft<4>, fft_smem_bytes());
-  smem_optin((const void*)k_lsar_pass_fft<4, 1>, fft_smem_bytes());
+  smem_optin((const void*)k_lsar_pass_fft<4, 1>, fft_smem_bytes(fft_tw_entries<1>()));
+  // two CTAs of 78 KB: the 164 KB shared-memory carve-out leaves ~92 KB of L1, which keeps H (64 KB) resident
+  CK(cudaFuncSetAttribute((const void*)k_lsar_pass_fft<4, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 72));
 
 }
 
@@ -796,14 +798,16 @@ static void launch_fft_series(tf_context* ctx, int64_t w) {
 }
 
 // Deferred folding plan of one sweep (k_fft.cuh, kFftSlots): q0 = the first
-// FFT lag, K groups; residual r_j (j >= q0 - 1) lives in slot (j - q0 + 1) mod K
-// (slot 0 = ctx->r, where the direct pass of lag q0 - 1 left it).  K = 1: the
-// classic state (s_q, r_q in place every lag).
+// FFT lag, K groups; residual r_j (j >= q0 - 1) lives in slot (j - q0 + 1) mod M,
+// M = K + 1 slots (slot 0 = ctx->r, where the direct pass of lag q0 - 1 left
+// it): r_q's slot is never one of the K pending residuals, so the pass may
+// write r_q before it folds.  K = 1: the classic state (s_q, r_q in place every
+// lag, M = 1).
 struct FoldPlan {
-  int K = 1, q0 = 0;
+  int K = 1, M = 1, q0 = 0;
   int64_t grid = 1;  // the FFT pass's grid (superblock groups depend on it)
-  double* slot[kFftSlots] = {};
-  double* of(int lag) const { return slot[((lag - q0 + 1) % K + K) % K]; }
+  double* slot[kFftSlots + 1] = {};
+  double* of(int lag) const { return slot[((lag - q0 + 1) % M + M) % M]; }
   // last lag <= at at which group g folded (q0 - 1: never, the state the direct pass left)
   int last_fold(int g, int at) const {
     if (at < q0 + g) return q0 - 1;
@@ -819,8 +823,9 @@ static FoldPlan fold_plan(tf_context* ctx, int p_bar, int64_t w) {
   // groups beyond the FFT lags' count buy nothing
   f.K = std::max(1, std::min(ctx->fft_slots, p_bar - q0 + 1));
   f.grid = fft_grid(ctx, (w + kFftSB - 1) / kFftSB);
+  f.M = f.K > 1 ? f.K + 1 : 1;
   f.slot[0] = ctx->r.get();
-  for (int k = 1; k < f.K; ++k) {
+  for (int k = 1; k < f.M; ++k) {
     ctx->fft_rslot[k - 1].need(w);
     f.slot[k] = ctx->fft_rslot[k - 1].get();
   }
@@ -843,10 +848,7 @@ static PendState pend_state(const FoldPlan& f, int p, const double* Rhist) {
   return ps;
 }
 
-static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev,
-                            const FoldPlan& f) {
-  k_fft_taps_dd<<<kFftN * kTapSplit / 256, 256, 0, ctx->stream>>>(phi, q, ctx->fftH.get(), ctx->fftTwH.get(),
-                                                                   ctx->fftTwL.get());
+static FftPassArgs fft_pass_args(tf_context* ctx, int q, int64_t w, const double* Rprev, const FoldPlan& f) {
   FftPassArgs a{};
   a.Z = ctx->fftZ.get();
   a.H = ctx->fftH.get();
@@ -871,13 +873,36 @@ static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi
   a.chunkB = ctx->chunkB.get();
   a.tileA = ctx->tileA.get();
   a.tileB = ctx->tileB.get();
+  a.ggrid = (int)f.grid;
+  return a;
+}
+
+// the scores of lag q (k_fft_fold) on the side stream: everything it reads is there once the draws
+// of lag q are done; the caller orders it after them and joins it before the pass of lag q
+static void launch_fft_fold(tf_context* ctx, int q, int64_t w, const double* Rprev, const FoldPlan& f,
+                            cudaStream_t stream) {
+  FftPassArgs a = fft_pass_args(ctx, q, w, Rprev, f);
+  const int64_t nsb = (w + kFftSB - 1) / kFftSB;
+  k_fft_fold<<<(unsigned)nsb, kFftT, 0, stream>>>(a);
+  LAUNCH_CHECK("k_fft_fold");
+  COUNT_LAUNCH();
+}
+
+// split: the scores were k_fft_fold's (launch_fft_fold); the pass writes r_q and the B sums only
+static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi, const double* Rprev,
+                            const FoldPlan& f, bool split = false) {
+  k_fft_taps_dd<<<kFftN * kTapSplit / 256, 256, 0, ctx->stream>>>(phi, q, ctx->fftH.get(), ctx->fftTwH.get(),
+                                                                   ctx->fftTwL.get());
+  FftPassArgs a = fft_pass_args(ctx, q, w, Rprev, f);
+  a.split = split ? 1 : 0;
   const int64_t nsb = (w + kFftSB - 1) / kFftSB;
   // prefetch variant (dev switch TF_FFT_PF, measured in profiles/r02_fft_prefetch.txt): 4 (state of
   // this superblock and spectrum of the next to L2, the spectrum through shared memory by TMA) is the fastest
   static const int pf = std::getenv("TF_FFT_PF") ? std::atoi(std::getenv("TF_FFT_PF")) : 4;
   // twiddles (dev switch TF_FFT_TW): 1 = powers of one table entry per stage formed in registers
   static const int twm = std::getenv("TF_FFT_TW") ? std::atoi(std::getenv("TF_FFT_TW")) : 1;
-  if (pf == 4 && twm == 1) k_lsar_pass_fft<4, 1><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
+  if (pf == 4 && twm == 1)
+    k_lsar_pass_fft<4, 1><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(fft_tw_entries<1>()), ctx->stream>>>(a);
   else if (pf == 0) k_lsar_pass_fft<0><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   else if (pf == 1) k_lsar_pass_fft<1><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   else if (pf == 3) k_lsar_pass_fft<3><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
@@ -1119,7 +1144,9 @@ static int64_t run_graphed(tf_context* ctx, GraphCache& gc, int64_t w, int64_t c
     }
     capturing = false;
     CK(cudaStreamEndCapture(st, &graph));
-    CK(cudaGraphInstantiate(&gc.exec, graph, 0));
+    // per-node priorities: the nodes captured from the low-priority side stream (k_fft_fold) must not
+    // hold the SMs against the solve's kernels (by default every node takes the launch stream's priority)
+    CK(cudaGraphInstantiateWithFlags(&gc.exec, graph, cudaGraphInstantiateFlagUseNodePriority));
     cudaGraphDestroy(graph);
     gc.launches = g_launches - l0;
     CK(cudaGraphLaunch(gc.exec, st));
@@ -1227,13 +1254,28 @@ static void lsar_sweep(tf_context* ctx, int p_bar, int64_t c, uint64_t seed, con
                            cudaMemcpyDeviceToDevice, st));
       }
       if (phases) rec(ctx->pev[2 * (p - 1)]);
+      // FFT lags with deferred folding: the score update of lag p needs nothing from the solve, so it
+      // runs on the (low-priority) side stream beside it -- the solve's pivoted Cholesky and SVD leave
+      // most SMs idle -- and the pass proper then only transforms and writes r_p
+      // (a sweep that reports per-lag phase times keeps it on the main stream, inside the pass's
+      // interval: those times are then the kernels' own, not what the overlap hides)
+      const bool split = ctx->fft_split && fp.K > 1 && fft_lag(ctx, p_bar, p);
+      const bool overlap = split && !phases;
+      if (overlap) {
+        CK(cudaEventRecord(ctx->ev_fork, st));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        launch_fft_fold(ctx, p, w, ctx->scal.get(), fp, ctx->side);
+        CK(cudaEventRecord(ctx->ev_join, ctx->side));
+      }
       // rank-revealing solve of the sampled lag-p system (toeplitz.cpp:57-85)
       ExactOut o{ctx->phi.get(), ctx->coefs.get(), (int64_t)(p - 1) * p / 2, ctx->taus.get(), ctx->method.get(),
                  ctx->rank.get(), p, ctx->sweeps.get()};
       solve_exact(ctx, FwdRows{ctx->y.get(), idx, wts, 0}, c, p + 1, /*rev=*/0, o, nullptr, false, ybits);
       if (phases) rec(ctx->pev[2 * (p - 1) + 1]);
+      if (overlap) CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+      else if (split) launch_fft_fold(ctx, p, w, ctx->scal.get(), fp, st);
       // residuals of the lag-p window fit + score update s_p = s_{p-1} + r_{p-1}^2/R_{p-1}
-      if (fft_lag(ctx, p_bar, p)) launch_pass_fft(ctx, p, w, ctx->phi.get(), ctx->scal.get(), fp);
+      if (fft_lag(ctx, p_bar, p)) launch_pass_fft(ctx, p, w, ctx->phi.get(), ctx->scal.get(), fp, split);
       else launch_pass(ctx, p, w, ctx->phi.get(), ctx->scal.get());
       rec(ctx->events[p]);
     }
@@ -3009,13 +3051,25 @@ tf_status tf_create(const tf_opts* opts, tf_context** out) {
     const char* mq = std::getenv("TF_FFT_MINQ");  // crossover lag of the auto mode
     ctx->fft_minq = mq ? std::max(1, std::atoi(mq)) : tfe::kFftMinQ;
     ctx->fft_minlags = mq ? 0 : tfe::kFftMinLags;  // a forced crossover is taken as given
+    const char* sp = std::getenv("TF_FFT_SPLIT");  // 0: the score update stays fused into the FFT pass
+    ctx->fft_split = sp ? std::atoi(sp) != 0 : 1;
     const char* fs = std::getenv("TF_FFT_SLOTS");  // deferred-folding groups of the FFT pass (1..4)
     ctx->fft_slots = fs ? std::min(tfk::kFftSlots, std::max(1, std::atoi(fs))) : tfk::kFftSlots;
   }
   int least = 0, greatest = 0;
   cudaDeviceGetStreamPriorityRange(&least, &greatest);
   const int prio = std::max(greatest, least - std::max(0, opts ? opts->priority : 0));
-  if (cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, prio) != cudaSuccess) {
+  // the side stream (the FFT lags' score updates beside the solve) sits one priority step below the
+  // main one, so the solve's kernels take the SMs as soon as they are launched
+  const int main_prio = std::max(greatest, std::min(prio, least - 1));
+  if (cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, main_prio) != cudaSuccess) {
+    delete ctx;
+    return TF_CUDA;
+  }
+  if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, least) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    cudaStreamDestroy(ctx->stream);
     delete ctx;
     return TF_CUDA;
   }
@@ -3034,6 +3088,12 @@ void tf_destroy(tf_context* ctx) {
   if (ctx->lsar_graph.exec) cudaGraphExecDestroy(ctx->lsar_graph.exec);
   if (ctx->rh_graph.exec) cudaGraphExecDestroy(ctx->rh_graph.exec);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->side) {
+    cudaStreamSynchronize(ctx->side);
+    cudaStreamDestroy(ctx->side);
+  }
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   cudaStreamDestroy(ctx->stream);
   delete ctx;  // DBuf destructors free every device buffer
 }

@@ -59,6 +59,11 @@ struct SolveBufs {
 struct tf_context {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // second stream (lowest priority) + fork / join events: the FFT lags' score update (k_fft_fold)
+  // runs beside the lag's solve (engine.cu, lsar_sweep)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int fft_split = 1;
   std::string err;
   int sm_count = 148;
   int smem_optin_max = 232448;  // cudaDevAttrMaxSharedMemoryPerBlockOptin
@@ -108,7 +113,7 @@ struct tf_context {
   tfe::DBuf<unsigned long long> ymax;  // max |y| of the resident series (bit pattern), per sweep
   int pass_mode = 0, fft_minq = 0, fft_minlags = 0;
   int fft_slots = 4;                // deferred folding groups of the FFT pass (k_fft.cuh kFftSlots; 1 = fold per lag)
-  tfe::DBuf<double> fft_rslot[3];   // residual slots 1..3 (slot 0 is r)
+  tfe::DBuf<double> fft_rslot[4];   // residual slots 1..4 (slot 0 is r; K groups use K + 1 slots)
   int gram_mode = 0;  // 0 auto (INT8 tensor-core Gram above a work threshold), 1 double-double CUDA cores, 2 INT8 whenever c fits
   std::vector<cudaEvent_t> events;
   std::vector<cudaEvent_t> pev;  // phase events (2 per lag)

@@ -64,7 +64,7 @@ constexpr int kFftTw = 512;                      // twiddle table entries (W_256
 
 __host__ __device__ __forceinline__ int fpad(int e) { return e + (e >> 4); }
 
-inline size_t fft_smem_bytes() { return sizeof(double2) * (size_t)(kFftBufC + kFftTw); }
+inline size_t fft_smem_bytes(int tw_entries = kFftTw) { return sizeof(double2) * (size_t)(kFftBufC + tw_entries); }
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -163,11 +163,12 @@ __device__ __forceinline__ void tw_powers(double2 (&v)[16], double2 w1) {
 
 // TW: 0 twiddles from the two tables (W_256^{(t&15) r}; W_256^{(t>>4) r} W_4096^{(t&15) r}),
 // 1 powers of one table entry per stage (tw_powers)
+// (the tables then need only W_256^e, e < 16, and W_4096^e, e < 256: fft_tw_entries)
 template <int S, int TW = 0>
 __device__ __forceinline__ void fft4096(double2 (&v)[16], double2* buf, const double2* tw) {
   const int t = threadIdx.x;
   const double2* tw256 = tw;
-  const double2* twlo = tw + 256;
+  const double2* twlo = tw + (TW == 1 ? 16 : 256);
   // stage 1 (Ns = 1): no twiddles; out -> buf[16 t + r]
   fft16<S>(v);
   __syncthreads();
@@ -201,8 +202,16 @@ __device__ __forceinline__ void fft4096(double2 (&v)[16], double2* buf, const do
   fft16<S>(v);
 }
 
+// shared-memory twiddle entries: TW 0 both 256-entry tables, TW 1 W_256^e (e < 16) + W_4096^e (e < 256)
+template <int TW>
+__host__ __device__ constexpr int fft_tw_entries() { return TW == 1 ? 16 + 256 : kFftTw; }
+template <int TW = 0>
 __device__ __forceinline__ void fft_load_tw(double2* tw_s, const double2* tw_g) {
-  for (int e = threadIdx.x; e < kFftTw; e += blockDim.x) tw_s[e] = tw_g[e];
+  if (TW == 1) {
+    for (int e = threadIdx.x; e < 16 + 256; e += blockDim.x) tw_s[e] = tw_g[e < 16 ? e : 256 + (e - 16)];
+  } else {
+    for (int e = threadIdx.x; e < kFftTw; e += blockDim.x) tw_s[e] = tw_g[e];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -359,41 +368,38 @@ __global__ void __launch_bounds__(256) k_fft_taps_dd(const double* __restrict__ 
   if (sl == 0) H[k] = make_double2(re.h * inv, im.h * inv);
 }
 
-// Deterministic warp reduction of 24 values per lane: on return x[0] of lane
-// (b4 b3 b2 b1 b0) holds the sum over the warp of value 12 b4 + 6 b3 + 3 b2 +
-// 2 b1 + b0 (none when 2 b1 + b0 == 3).  24 shuffles instead of 24 x 5.
-__device__ __forceinline__ void warp_reduce24(double (&x)[24], int lane) {
-  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
-#pragma unroll
-  for (int i = 0; i < 12; ++i) {
-    const double snd = b4 ? x[i] : x[i + 12];
-    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 16);
-    x[i] = (b4 ? x[i + 12] : x[i]) + rcv;
-  }
+// Deterministic warp reduction of 12 values per lane: on return x[0] of lane
+// (b4 b3 b2 b1 b0) holds the sum over the warp of value 6 b4 + 3 b3 + 2 b2 + b1
+// (none when 2 b2 + b1 == 3; both b0 lanes hold it).  13 shuffles instead of
+// 12 x 5; every value is summed over the lane pairs xor 16, 8, 4, 2, 1 in that
+// order (a + b on both lanes of a pair: the same bits everywhere).
+__device__ __forceinline__ void warp_reduce12(double (&x)[12], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
-    const double snd = b3 ? x[i] : x[i + 6];
-    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 8);
-    x[i] = (b3 ? x[i + 6] : x[i]) + rcv;
+    const double snd = b4 ? x[i] : x[i + 6];
+    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 16);
+    x[i] = (b4 ? x[i + 6] : x[i]) + rcv;
   }
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    const double snd = b2 ? x[i] : x[i + 3];
-    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 4);
-    x[i] = (b2 ? x[i + 3] : x[i]) + rcv;
+    const double snd = b3 ? x[i] : x[i + 3];
+    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 8);
+    x[i] = (b3 ? x[i + 3] : x[i]) + rcv;
   }
   x[3] = 0.0;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
-    const double snd = b1 ? x[i] : x[i + 2];
-    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 2);
-    x[i] = (b1 ? x[i + 2] : x[i]) + rcv;
+    const double snd = b2 ? x[i] : x[i + 2];
+    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 4);
+    x[i] = (b2 ? x[i + 2] : x[i]) + rcv;
   }
   {
-    const double snd = b0 ? x[0] : x[1];
-    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 1);
-    x[0] = (b0 ? x[1] : x[0]) + rcv;
+    const double snd = b1 ? x[0] : x[1];
+    const double rcv = __shfl_xor_sync(0xffffffffu, snd, 2);
+    x[0] = (b1 ? x[1] : x[0]) + rcv;
   }
+  x[0] += __shfl_xor_sync(0xffffffffu, x[0], 1);
 }
 
 // Deferred score folding (kFftSlots residual arrays): the fold of r_j^2 / R_j
@@ -404,10 +410,13 @@ __device__ __forceinline__ void warp_reduce24(double (&x)[24], int lane) {
 // order (the same fma sequence as one fold per lag: bit-identical s).  The
 // other K - 1 groups only read the spectrum and write r_q (18.7 B/row), their
 // 32-row chunk sums of s advanced by the chunk recurrence A_q = A_{q-1} +
-// B_{q-1} / R_{q-1}.  Residual r_j lives in slot (j - q0 + 1) mod K until every
-// group has folded it; a draw at a row computes the exact s_{q+1}(row) from s
-// and the row group's pending residuals (PendState).  K = 1: one fold per lag
-// for every superblock (s_q and r_q in place).
+// B_{q-1} / R_{q-1}.  Residual r_j lives in slot (j - q0 + 1) mod (K + 1) until
+// every group has folded it (K + 1 slots: r_q never lands on a pending residual,
+// so the pass writes r_q first -- its transform registers are then free -- and
+// folds afterwards with every pending load of 12 rows in flight at once); a
+// draw at a row computes the exact s_{q+1}(row) from s and the row group's
+// pending residuals (PendState).  K = 1: one fold per lag for every superblock
+// (s_q and r_q in place: r_{q-1} is loaded before r_q is stored).
 constexpr int kFftSlots = 4;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -427,12 +436,102 @@ struct FftPassArgs {
   int npend;  // its pending residuals (oldest first), 1..K
   const double* pend[kFftSlots];
   const double* Rp;  // R of the pending lags [npend]; Rp[npend - 1] = R_{q-1}
-  double* rout;      // r_q (may alias pend[0]: read before written, same thread)
+  double* rout;      // r_q (K = 1: aliases pend[0], which is then loaded before the store)
   double* chunkA;
   double* chunkB;
   double* tileA;
   double* tileB;
+  int ggrid;  // the grid the superblock groups are defined on: group(sb) = (sb + sb / ggrid) mod K
+  int split;  // 1: the scores (phase 2 below) are k_fft_fold's, on another stream; the pass writes r_q, B only
 };
+
+__device__ __forceinline__ bool fft_folds(const FftPassArgs& a, int64_t sb) {
+  // (32-bit arithmetic: the superblock index is far below 2^32)
+  return a.K == 1 || (int)(((uint32_t)sb + (uint32_t)sb / (uint32_t)a.ggrid) % (uint32_t)a.K) == a.fold;
+}
+
+// Phase 2 of a superblock (K > 1), by the 256 threads of a CTA: the chunk sums
+// of s_q into csA / chunkA.  Folding superblock: s += the pending r_j^2 / R_j
+// in lag order; per block half every load of s and two pending residuals (36
+// per thread) is in flight at once.  Otherwise the chunk recurrence A_q =
+// A_{q-1} + B_{q-1} / R_{q-1} on (oA, oB) = the chunk sums of lag q - 1.
+// Shared by the fused pass and k_fft_fold: the same operations, the same bits.
+__device__ __forceinline__ void fft_scores_phase(const FftPassArgs& a, int64_t sb, bool fold, double* csA,
+                                                 const double* invRp, double oA, double oB) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t w = a.w;
+  const int64_t base = sb * kFftSB + t;
+  double* __restrict__ sp = a.s;
+  // reduced value i = 6 b4 + 3 b3 + 2 b2 + b1 of warp_reduce12 -> its chunk; one writer lane per value
+  const int vi = 6 * ((lane >> 4) & 1) + 3 * ((lane >> 3) & 1) + ((lane >> 1) & 3);
+  const bool writer = (lane & 1) == 0 && ((lane >> 1) & 3) != 3;
+  if (fold) {
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      double so[12], ra[12], rb[12];
+      const bool two = a.npend > 1;
+#pragma unroll
+      for (int i = 0; i < 12; ++i) {
+        const int64_t row = base + h * kFftL + 256 * i;
+        const bool ok = row < w;
+        so[i] = ok ? __ldcs(sp + row) : 0.0;
+        ra[i] = ok ? __ldcs(a.pend[0] + row) : 0.0;
+        rb[i] = ok && two ? __ldcs(a.pend[1] + row) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 12; ++i) so[i] = fma(ra[i] * ra[i], invRp[0], so[i]);
+      if (two) {
+#pragma unroll
+        for (int i = 0; i < 12; ++i) so[i] = fma(rb[i] * rb[i], invRp[1], so[i]);
+      }
+      if (a.npend > 2) {
+        const bool four = a.npend > 3;
+#pragma unroll
+        for (int i = 0; i < 12; ++i) {
+          const int64_t row = base + h * kFftL + 256 * i;
+          const bool ok = row < w;
+          ra[i] = ok ? __ldcs(a.pend[2] + row) : 0.0;
+          rb[i] = ok && four ? __ldcs(a.pend[3] + row) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 12; ++i) so[i] = fma(ra[i] * ra[i], invRp[2], so[i]);
+        if (four) {
+#pragma unroll
+          for (int i = 0; i < 12; ++i) so[i] = fma(rb[i] * rb[i], invRp[3], so[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 12; ++i) {
+        const int64_t row = base + h * kFftL + 256 * i;
+        if (row < w) __stcs(sp + row, so[i]);
+        else so[i] = 0.0;
+      }
+      warp_reduce12(so, lane);
+      const int cl = 96 * h + 8 * vi + warp;
+      const int64_t cg = sb * kFftChunksSB + cl;
+      if (writer) {
+        csA[cl] = so[0];
+        if (cg * kChunk < w) a.chunkA[cg] = so[0];
+      }
+    }
+  } else if (t < kFftChunksSB) {
+    const int64_t cg = sb * kFftChunksSB + t;
+    const bool live = cg * kChunk < w;
+    const double nA = live ? fma(oB, invRp[a.npend - 1], oA) : 0.0;
+    csA[t] = nA;
+    if (live) a.chunkA[cg] = nA;
+  }
+}
+
+// 2048-row tile sums of a superblock from its 192 chunk sums (warps 0..2, after a barrier)
+__device__ __forceinline__ void fft_tile_sums(const double* cs, double* tile, int64_t sb, int64_t w) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp < kFftTilesSB) {
+    const int64_t tg = sb * kFftTilesSB + warp;
+    const double T = warp_sum(cs[64 * warp + lane] + cs[64 * warp + 32 + lane]);
+    if (lane == 0 && tg * kPassTile < w) tile[tg] = T;
+  }
+}
 
 // Persistent CTAs (2 per SM) over 6144-row superblocks.  PF (prefetch):
 // 0 none, 1 the next superblock's spectrum + state to L2, 2 this superblock's
@@ -442,11 +541,17 @@ struct FftPassArgs {
 template <int PF, int TW = 0>
 __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
   extern __shared__ double2 fsm[];
-  __shared__ double csA[kFftChunksSB], csB[kFftChunksSB];
   __shared__ double coA[kFftChunksSB], coB[kFftChunksSB];  // non-folding superblock: chunk sums of lag q - 1
   double2* buf = fsm;
   double2* tw = fsm + kFftBufC;
-  fft_load_tw(tw, a.tw);
+  // this superblock's chunk sums live in the transform buffer's padding tail (slots 4096 ..: free
+  // from the last transform stage's reads to the next superblock's first exchange; the next
+  // spectrum's bulk copy fills slots [0, 4096) only).  Shared memory per CTA stays under 81 KB, so
+  // two CTAs fit the 164 KB carve-out and the L1 beside it (~92 KB) keeps the 64 KB of H resident.
+  double* csA = reinterpret_cast<double*>(buf + kFftN);
+  double* csB = csA + kFftChunksSB;
+  static_assert(2 * kFftChunksSB * sizeof(double) <= (kFftBufC - kFftN) * sizeof(double2), "chunk sums fit the padding");
+  fft_load_tw<TW>(tw, a.tw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int64_t w = a.w;
   const int64_t nsb = (w + kFftSB - 1) / kFftSB;
@@ -460,7 +565,7 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
     const int64_t r0 = p * kFftSB;
     const uint32_t bytes = (uint32_t)(min((int64_t)kFftSB, w - r0) * 8) & ~15u;
     if (spectrum) bulk_prefetch_l2(a.Z + p * kFftN, kFftN * sizeof(double2));
-    if (bytes && (a.K == 1 || (int)((p + p / gridDim.x) % a.K) == a.fold)) {
+    if (bytes && !a.split && fft_folds(a, p)) {
       bulk_prefetch_l2(a.s + r0, bytes);
       for (int k = 0; k < a.npend; ++k) bulk_prefetch_l2(a.pend[k] + r0, bytes);
     }
@@ -487,8 +592,8 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
     if (PF >= 3 && t == 0 && sb + gridDim.x < nsb)
       bulk_prefetch_l2(a.Z + (sb + gridDim.x) * kFftN, kFftN * sizeof(double2));
     // group of sb: (sb + sb / grid) mod K -- each CTA folds every K-th superblock it visits (balanced)
-    const bool fold = a.K == 1 || (int)((sb + sb / gridDim.x) % a.K) == a.fold;
-    if (!fold && t < kFftChunksSB) {  // the previous chunk sums, in flight during the transform
+    const bool fold = fft_folds(a, sb);
+    if (!a.split && !fold && t < kFftChunksSB) {  // the previous chunk sums, in flight during the transform
       const int64_t cg = sb * kFftChunksSB + t;
       if (cg * kChunk < w) {
         cp_async8(coA + t, a.chunkA + cg);
@@ -517,19 +622,23 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
       }
     }
     // rows: output m = t + 256 r (r >= 4) -> u = m - D; block a row base + u (real part), block b row
-    // base + 3072 + u (imaginary part).  Per block half: values i < 12 = s_q of rows r = 4 + i,
-    // i >= 12 = r_q^2 of rows r = i - 8, reduced over the warp in one warp_reduce24.
+    // base + 3072 + u (imaginary part): for fixed r a warp holds the 32 rows of chunk 96 h + 8 (r - 4) + warp.
     const int64_t base = sb * kFftSB + t;
     double* __restrict__ sp = a.s;
-    double* rp = a.rout;  // may alias pend[0] (same rows: loaded above, stored below)
+    double* rp = a.rout;
+    const bool alias = a.K == 1;  // rout == pend[0]: r_{q-1} comes in before r_q goes out
+    // reduced value i = 6 b4 + 3 b3 + 2 b2 + b1 of warp_reduce12 -> its chunk; one writer lane per value
+    const int vi = 6 * ((lane >> 4) & 1) + 3 * ((lane >> 3) & 1) + ((lane >> 1) & 3);
+    const bool writer = (lane & 1) == 0 && ((lane >> 1) & 3) != 3;
+    // (1) r_q out and the chunk sums of r_q^2 (K = 1: the fold of r_{q-1} first, 6 rows at a time)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      double x[24];
+      double x[12];
+      if (alias) {
+        double xs[12];
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        double so[6];
-        if (fold) {
-          double ro[6];
+        for (int g = 0; g < 2; ++g) {
+          double so[6], ro[6];
 #pragma unroll
           for (int j = 0; j < 6; ++j) {
             const int64_t row = base + h * kFftL + 256 * (6 * g + j);
@@ -537,71 +646,84 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
             ro[j] = row < w ? __ldcs(a.pend[0] + row) : 0.0;
           }
 #pragma unroll
-          for (int j = 0; j < 6; ++j) so[j] = fma(ro[j] * ro[j], invRp[0], so[j]);
-#pragma unroll
-          for (int k = 1; k < kFftSlots; ++k) {
-            if (k >= a.npend) break;
-#pragma unroll
-            for (int j = 0; j < 6; ++j) {
-              const int64_t row = base + h * kFftL + 256 * (6 * g + j);
-              ro[j] = row < w ? __ldcs(a.pend[k] + row) : 0.0;
+          for (int j = 0; j < 6; ++j) {
+            const int i = 6 * g + j;
+            const int64_t row = base + h * kFftL + 256 * i;
+            const double rq = h ? v[4 + i].y : v[4 + i].x;
+            const double sn = fma(ro[j] * ro[j], invRp[0], so[j]);
+            double rs = 0.0;
+            if (row < w) {
+              __stcs(sp + row, sn);
+              __stcs(rp + row, rq);
+              rs = rq;
             }
-#pragma unroll
-            for (int j = 0; j < 6; ++j) so[j] = fma(ro[j] * ro[j], invRp[k], so[j]);
+            xs[i] = row < w ? sn : 0.0;
+            x[i] = rs * rs;
           }
         }
+        warp_reduce12(xs, lane);
+        const int cl = 96 * h + 8 * vi + warp;
+        const int64_t cg = sb * kFftChunksSB + cl;
+        if (writer) {
+          csA[cl] = xs[0];
+          if (cg * kChunk < w) a.chunkA[cg] = xs[0];
+        }
+      } else {
 #pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          const int i = 6 * g + j;
+        for (int i = 0; i < 12; ++i) {
           const int64_t row = base + h * kFftL + 256 * i;
           const double rq = h ? v[4 + i].y : v[4 + i].x;
-          double sn = 0.0, rs = 0.0;
+          double rs = 0.0;
           if (row < w) {
-            if (fold) {
-              sn = so[j];
-              __stcs(sp + row, sn);
-            }
             __stcs(rp + row, rq);
             rs = rq;
           }
-          x[i] = sn;
-          x[12 + i] = rs * rs;
+          x[i] = rs * rs;
         }
       }
-      warp_reduce24(x, lane);
-      const int sel = lane & 3;
-      const int vi = 12 * ((lane >> 4) & 1) + 6 * ((lane >> 3) & 1) + 3 * ((lane >> 2) & 1) + sel;
-      const int cl = 96 * h + 8 * (vi % 12) + warp;  // chunk of the superblock
+      warp_reduce12(x, lane);
+      const int cl = 96 * h + 8 * vi + warp;  // chunk of the superblock
       const int64_t cg = sb * kFftChunksSB + cl;
-      const bool live = sel != 3 && cg * kChunk < w;
-      if (!fold) {
-        // chunk sum of s_q by the recurrence A_q = A_{q-1} + B_{q-1} / R_{q-1}
-        double nA = 0.0;
-        if (live && vi < 12) nA = fma(coB[cl], invRp[a.npend - 1], coA[cl]);  // 1 / R_{q-1}
-        if (vi < 12) x[0] = nA;
-      }
-      if (sel != 3) {
-        if (vi < 12) {
-          csA[cl] = x[0];
-          if (live) a.chunkA[cg] = x[0];
-        } else {
-          csB[cl] = x[0];
-          if (live) a.chunkB[cg] = x[0];
-        }
+      if (writer) {
+        csB[cl] = x[0];
+        if (cg * kChunk < w) a.chunkB[cg] = x[0];
       }
     }
+    // (2) the scores (K > 1; the transform's registers are dead) -- unless k_fft_fold computes them
+    if (!alias && !a.split) fft_scores_phase(a, sb, fold, csA, invRp, t < kFftChunksSB ? coA[t] : 0.0, t < kFftChunksSB ? coB[t] : 0.0);
     __syncthreads();
-    if (warp < kFftTilesSB) {
-      const int64_t tg = sb * kFftTilesSB + warp;
-      const double TA = warp_sum(csA[64 * warp + lane] + csA[64 * warp + 32 + lane]);
-      const double TB = warp_sum(csB[64 * warp + lane] + csB[64 * warp + 32 + lane]);
-      if (lane == 0 && tg * kPassTile < w) {
-        a.tileA[tg] = TA;
-        a.tileB[tg] = TB;
-      }
-    }
+    if (!a.split) fft_tile_sums(csA, a.tileA, sb, w);
+    fft_tile_sums(csB, a.tileB, sb, w);
     // csA / csB are rewritten only after the next fft4096's barriers
   }
+}
+
+// The scores of lag q on their own (FftPassArgs::split): phase 2 of every
+// superblock + the tile sums of s_q, one CTA per superblock.  It depends on
+// nothing the lag's solve produces (the pending residuals, their R and the
+// chunk sums of lag q - 1 are all there once the draws are done), so the sweep
+// runs it on a second stream beside the solve, whose pivoted Cholesky and SVD
+// occupy 16 SMs; the pass proper (transform -> r_q, B) then moves 18.7 B/row.
+// Must finish before the pass of lag q starts (which overwrites chunkB).
+__global__ void __launch_bounds__(kFftT) k_fft_fold(FftPassArgs a) {
+  __shared__ double csA[kFftChunksSB];
+  __shared__ double invRp[kFftSlots];
+  const int t = threadIdx.x;
+  if (t < kFftSlots) invRp[t] = t < a.npend ? 1.0 / a.Rp[t] : 0.0;
+  __syncthreads();
+  const int64_t sb = blockIdx.x;
+  const bool fold = fft_folds(a, sb);
+  double oA = 0.0, oB = 0.0;
+  if (!fold && t < kFftChunksSB) {
+    const int64_t cg = sb * kFftChunksSB + t;
+    if (cg * kChunk < a.w) {
+      oA = a.chunkA[cg];
+      oB = a.chunkB[cg];
+    }
+  }
+  fft_scores_phase(a, sb, fold, csA, invRp, oA, oB);
+  __syncthreads();
+  fft_tile_sums(csA, a.tileA, sb, a.w);
 }
 
 }  // namespace tfk

@@ -191,3 +191,47 @@ def test_fft_first_lag_abi(tf, monkeypatch):
             assert e.fft_first_lag(500) == want
         finally:
             e.close()
+
+
+def test_fft_split_score_update_equals_fused(tf, monkeypatch):
+    """The score update of an FFT lag on its own stream beside the solve
+    (k_fft_fold, TF_FFT_SPLIT=1, the default) against the update fused into the
+    pass (TF_FFT_SPLIT=0): the same device code, so draws, fits, scores and
+    residuals are bit-identical -- in RNG mode, three sweeps each (eager, the
+    graph's capture, its replay).  One fold per lag (TF_FFT_SLOTS=1) gives the
+    same row scores bit for bit (the same fma sequence per row); its chunk sums
+    are reduced from the rows instead of advanced by the chunk recurrence, so
+    the CDF totals -- and through the weights the fit -- agree to rounding."""
+    y = c1_like(60000, seed=17, q=9)
+    p_bar, c = 24, 900
+    out = {}
+    for name, env in (("split", {"TF_FFT_SPLIT": "1"}), ("fused", {"TF_FFT_SPLIT": "0"}),
+                      ("perlag", {"TF_FFT_SPLIT": "0", "TF_FFT_SLOTS": "1"})):
+        monkeypatch.setenv("TF_PASS", "fft")
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        eng = tf.Engine(0)
+        for k in ("TF_PASS", *env):
+            monkeypatch.delenv(k)
+        try:
+            fits = [tf.lsar_fit(tf.TimeSeries(y), p_bar, c, 33, engine=eng, want_diag=True) for _ in range(3)]
+        finally:
+            eng.close()
+        for f in fits[1:]:
+            assert np.array_equal(f.diag["idx"], fits[0].diag["idx"])
+            assert np.array_equal(np.array(f.pacf.taus), np.array(fits[0].pacf.taus))
+            assert np.array_equal(f.diag["scores"], fits[0].diag["scores"])
+        out[name] = fits[-1]
+    a, b, k1 = out["split"], out["fused"], out["perlag"]
+    assert np.array_equal(a.diag["idx"], b.diag["idx"])
+    assert np.array_equal(np.array(a.pacf.taus), np.array(b.pacf.taus))
+    assert np.array_equal(a.diag["scores"], b.diag["scores"])
+    assert np.array_equal(a.diag["resid"], b.diag["resid"])
+    assert np.array_equal(a.diag["ssum"], b.diag["ssum"])
+    assert a.p_star == b.p_star == k1.p_star
+    if np.array_equal(a.diag["idx"], k1.diag["idx"]):
+        assert relerr(a.pacf.taus, k1.pacf.taus) < 1e-11
+        assert relerr(a.diag["scores"], k1.diag["scores"]) < 1e-11
+        assert relerr(a.diag["ssum"], k1.diag["ssum"]) < 1e-12
+    else:
+        check_flip(a.diag["idx"], k1.diag["idx"], c)
