@@ -779,8 +779,10 @@ static void reserve_fft(tf_context* ctx, int64_t w) {
   smem_optin((const void*)k_lsar_pass_fft<3>, fft_smem_bytes());
   smem_optin((const void*)k_lsar_pass_fft<4>, fft_smem_bytes());
   smem_optin((const void*)k_lsar_pass_fft<4, 1>, fft_smem_bytes(fft_tw_entries<1>()));
-  // two CTAs of 78 KB: the 164 KB shared-memory carve-out leaves ~92 KB of L1, which keeps H (64 KB) resident
-  CK(cudaFuncSetAttribute((const void*)k_lsar_pass_fft<4, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 72));
+  smem_optin((const void*)k_lsar_pass_fft_r, fft_smem_bytes(fft_tw_entries<1>()));
+  CK(cudaFuncSetAttribute((const void*)k_lsar_pass_fft_r, cudaFuncAttributePreferredSharedMemoryCarveout, 70));
+  // two CTAs of 78 KB: the 164 KB shared-memory carve-out (70 % of 228 KB rounds up to it; 72 % gave 196 KB) leaves ~92 KB of L1, which keeps H (64 KB) resident
+  CK(cudaFuncSetAttribute((const void*)k_lsar_pass_fft<4, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 70));
 
 }
 
@@ -901,7 +903,12 @@ static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi
   static const int pf = std::getenv("TF_FFT_PF") ? std::atoi(std::getenv("TF_FFT_PF")) : 4;
   // twiddles (dev switch TF_FFT_TW): 1 = powers of one table entry per stage formed in registers
   static const int twm = std::getenv("TF_FFT_TW") ? std::atoi(std::getenv("TF_FFT_TW")) : 1;
-  if (pf == 4 && twm == 1)
+  // split: the pass proper with the next spectrum prefetched into registers (dev switch TF_FFT_RPF=0:
+  // the fused kernel with its score phase skipped)
+  static const int rpf = std::getenv("TF_FFT_RPF") ? std::atoi(std::getenv("TF_FFT_RPF")) : 1;
+  if (split && pf == 4 && twm == 1 && rpf)
+    k_lsar_pass_fft_r<<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(fft_tw_entries<1>()), ctx->stream>>>(a);
+  else if (pf == 4 && twm == 1)
     k_lsar_pass_fft<4, 1><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(fft_tw_entries<1>()), ctx->stream>>>(a);
   else if (pf == 0) k_lsar_pass_fft<0><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
   else if (pf == 1) k_lsar_pass_fft<1><<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(), ctx->stream>>>(a);
@@ -2633,12 +2640,23 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
       scan_apply(ctx, ctx->rh_ok.get(), c, CompactDrawF{ctx->idx.get(), ctx->wts.get(), ctx->sh_idx.get(),
                                                         ctx->sh_wts.get()});
       if (phases) rec(ctx->pev[2 * (p - 1)]);
+      // the shard's score update of an FFT lag beside the (replicated) solve, as in lsar_sweep
+      const bool split = ctx->fft_split && fp.K > 1 && fft_lag(ctx, p_bar, p);
+      const bool overlap = split && !phases;
+      if (overlap) {
+        CK(cudaEventRecord(ctx->ev_fork, st));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        launch_fft_fold(ctx, p, w, ctx->sh_par.get(), fp, ctx->side);
+        CK(cudaEventRecord(ctx->ev_join, ctx->side));
+      }
       ExactOut o{ctx->phi.get(), ctx->coefs.get(), (int64_t)(p - 1) * p / 2, ctx->taus.get(), ctx->method.get(),
                  ctx->rank.get(), p, ctx->sweeps.get()};
       solve_exact(ctx, FwdRows{ctx->y.get(), ctx->sh_idx.get(), ctx->sh_wts.get(), 0}, c, p + 1, /*rev=*/0, o, kdev,
                   /*sharded=*/true, ybits);
       if (phases) rec(ctx->pev[2 * (p - 1) + 1]);
-      if (fft_lag(ctx, p_bar, p)) launch_pass_fft(ctx, p, w, ctx->phi.get(), ctx->sh_par.get(), fp);
+      if (overlap) CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+      else if (split) launch_fft_fold(ctx, p, w, ctx->sh_par.get(), fp, st);
+      if (fft_lag(ctx, p_bar, p)) launch_pass_fft(ctx, p, w, ctx->phi.get(), ctx->sh_par.get(), fp, split);
       else launch_pass(ctx, p, w, ctx->phi.get(), ctx->sh_par.get());  // R_{p-1} = par[0]
       rec(ctx->events[p]);
     }

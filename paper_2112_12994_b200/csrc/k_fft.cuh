@@ -698,6 +698,90 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
   }
 }
 
+// The pass proper when the scores are k_fft_fold's (FftPassArgs::split, K > 1):
+// transform -> r_q and the chunk / tile sums of r_q^2, nothing else.  With no
+// fold in the kernel the transform registers are free as soon as r_q is stored,
+// so the NEXT superblock's spectrum is loaded straight into them (16 coalesced
+// 16-byte loads per thread, L2 hits: the spectrum was prefetched to L2 one
+// superblock earlier) and is in flight over the reductions, the barrier, the
+// tile sums and the loop edge -- no shared-memory staging of the spectrum (the
+// bulk copy's 64 KB write and the 16 LDS.128 per thread were a quarter of the
+// kernel's shared-memory wavefronts), no mbarrier.  Same arithmetic as
+// k_lsar_pass_fft<4, 1>: the same bits.
+__global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft_r(FftPassArgs a) {
+  extern __shared__ double2 fsm[];
+  double2* buf = fsm;
+  double2* tw = fsm + kFftBufC;
+  double* csB = reinterpret_cast<double*>(buf + kFftN);  // the buffer's padding tail (see k_lsar_pass_fft)
+  fft_load_tw<1>(tw, a.tw);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t w = a.w;
+  const int64_t nsb = (w + kFftSB - 1) / kFftSB;
+  const int vi = 6 * ((lane >> 4) & 1) + 3 * ((lane >> 3) & 1) + ((lane >> 1) & 3);
+  const bool writer = (lane & 1) == 0 && ((lane >> 1) & 3) != 3;
+  double2 v[16];
+  if ((int64_t)blockIdx.x < nsb) {
+    const double2* Zs = a.Z + (int64_t)blockIdx.x * kFftN + t;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = __ldcs(Zs + 256 * r);
+    if (t == 0 && (int64_t)blockIdx.x + gridDim.x < nsb)
+      bulk_prefetch_l2(a.Z + ((int64_t)blockIdx.x + gridDim.x) * kFftN, kFftN * sizeof(double2));
+  }
+  for (int64_t sb = blockIdx.x; sb < nsb; sb += gridDim.x) {
+    if (t == 0 && sb + 2 * (int64_t)gridDim.x < nsb)
+      bulk_prefetch_l2(a.Z + (sb + 2 * (int64_t)gridDim.x) * kFftN, kFftN * sizeof(double2));
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = cmul(v[r], __ldg(a.H + t + 256 * r));
+    fft4096<1, 1>(v, buf, tw);
+    __syncthreads();  // every thread's last-stage reads of buf (its tail holds csB) are done
+    const int64_t base = sb * kFftSB + t;
+    double* rp = a.rout;
+    double x0[12], x1[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+      const int64_t row = base + 256 * i;
+      const double rq = v[4 + i].x;
+      double rs = 0.0;
+      if (row < w) {
+        __stcs(rp + row, rq);
+        rs = rq;
+      }
+      x0[i] = rs * rs;
+    }
+#pragma unroll
+    for (int i = 0; i < 12; ++i) {
+      const int64_t row = base + kFftL + 256 * i;
+      const double rq = v[4 + i].y;
+      double rs = 0.0;
+      if (row < w) {
+        __stcs(rp + row, rq);
+        rs = rq;
+      }
+      x1[i] = rs * rs;
+    }
+    if (sb + gridDim.x < nsb) {  // the next spectrum, into the registers the transform just left
+      const double2* Zs = a.Z + (sb + gridDim.x) * kFftN + t;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = __ldcs(Zs + 256 * r);
+    }
+    warp_reduce12(x0, lane);
+    warp_reduce12(x1, lane);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int cl = 96 * h + 8 * vi + warp;  // chunk of the superblock
+      const int64_t cg = sb * kFftChunksSB + cl;
+      const double xv = h ? x1[0] : x0[0];
+      if (writer) {
+        csB[cl] = xv;
+        if (cg * kChunk < w) a.chunkB[cg] = xv;
+      }
+    }
+    __syncthreads();
+    fft_tile_sums(csB, a.tileB, sb, w);
+    // csB is rewritten only after the next fft4096's barriers
+  }
+}
+
 // The scores of lag q on their own (FftPassArgs::split): phase 2 of every
 // superblock + the tile sums of s_q, one CTA per superblock.  It depends on
 // nothing the lag's solve produces (the pending residuals, their R and the
