@@ -903,9 +903,10 @@ static void launch_pass_fft(tf_context* ctx, int q, int64_t w, const double* phi
   static const int pf = std::getenv("TF_FFT_PF") ? std::atoi(std::getenv("TF_FFT_PF")) : 4;
   // twiddles (dev switch TF_FFT_TW): 1 = powers of one table entry per stage formed in registers
   static const int twm = std::getenv("TF_FFT_TW") ? std::atoi(std::getenv("TF_FFT_TW")) : 1;
-  // split: the pass proper with the next spectrum prefetched into registers (dev switch TF_FFT_RPF=0:
-  // the fused kernel with its score phase skipped)
-  static const int rpf = std::getenv("TF_FFT_RPF") ? std::atoi(std::getenv("TF_FFT_RPF")) : 1;
+  // split: the fused kernel with its score phase skipped.  Dev switch TF_FFT_RPF=1: k_lsar_pass_fft_r, the
+  // next spectrum prefetched into registers instead of staged through shared memory by TMA -- measured
+  // slower at C4 (4.69 vs 4.54 s per sweep: profiles/r02_fft_prefetch.txt), so off
+  static const int rpf = std::getenv("TF_FFT_RPF") ? std::atoi(std::getenv("TF_FFT_RPF")) : 0;
   if (split && pf == 4 && twm == 1 && rpf)
     k_lsar_pass_fft_r<<<fft_grid(ctx, nsb), kFftT, fft_smem_bytes(fft_tw_entries<1>()), ctx->stream>>>(a);
   else if (pf == 4 && twm == 1)

@@ -707,7 +707,9 @@ __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft(FftPassArgs a) {
 // tile sums and the loop edge -- no shared-memory staging of the spectrum (the
 // bulk copy's 64 KB write and the 16 LDS.128 per thread were a quarter of the
 // kernel's shared-memory wavefronts), no mbarrier.  Same arithmetic as
-// k_lsar_pass_fft<4, 1>: the same bits.
+// k_lsar_pass_fft<4, 1>: the same bits.  MEASURED SLOWER than the TMA-staged
+// spectrum at C4 (pass 3.66 vs 3.46 s per sweep, profiles/r02_fft_prefetch.txt):
+// kept behind TF_FFT_RPF=1 as the record of the experiment, not the default.
 __global__ void __launch_bounds__(kFftT, 2) k_lsar_pass_fft_r(FftPassArgs a) {
   extern __shared__ double2 fsm[];
   double2* buf = fsm;
