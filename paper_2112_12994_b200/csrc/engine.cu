@@ -885,7 +885,7 @@ static void launch_fft_fold(tf_context* ctx, int q, int64_t w, const double* Rpr
                             cudaStream_t stream) {
   FftPassArgs a = fft_pass_args(ctx, q, w, Rprev, f);
   const int64_t nsb = (w + kFftSB - 1) / kFftSB;
-  k_fft_fold<<<(unsigned)nsb, kFftT, 0, stream>>>(a);
+  k_fft_fold<<<(unsigned)((nsb + kFoldSB - 1) / kFoldSB), kFftT, 0, stream>>>(a);
   LAUNCH_CHECK("k_fft_fold");
   COUNT_LAUNCH();
 }
