@@ -51,7 +51,10 @@ typedef struct tf_context tf_context;
 typedef struct {
   int device;    /* CUDA device ordinal */
   int priority;  /* stream priority: 0 = default, k > 0 = k levels above it (clamped to the
-                    device range) -- lets a latency-bound fit run ahead of concurrent ones */
+                    device range) -- lets a latency-bound fit run ahead of concurrent ones.
+                    The default is one step above the device's lowest priority, which the
+                    context's second stream takes (the FFT lags' score updates, which run
+                    beside the lag's solve and must yield the SMs to it) */
 } tf_opts;
 
 /* RHConfig (repeated_halving.hpp:56-65) */

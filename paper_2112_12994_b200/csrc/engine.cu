@@ -3080,7 +3080,7 @@ tf_status tf_create(const tf_opts* opts, tf_context** out) {
   const int prio = std::max(greatest, least - std::max(0, opts ? opts->priority : 0));
   // the side stream (the FFT lags' score updates beside the solve) sits one priority step below the
   // main one, so the solve's kernels take the SMs as soon as they are launched
-  const int main_prio = std::max(greatest, std::min(prio, least - 1));
+  const int main_prio = std::max(greatest, prio - 1);  // k levels above the default keeps its meaning
   if (cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, main_prio) != cudaSuccess) {
     delete ctx;
     return TF_CUDA;

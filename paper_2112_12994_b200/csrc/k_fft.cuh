@@ -407,7 +407,7 @@ __device__ __forceinline__ void warp_reduce12(double (&x)[12], int lane) {
 // group of superblocks per lag -- group g = (sb + sb / grid) mod K (each CTA of
 // the persistent grid folds every K-th superblock it visits) folds at the lags
 // q0 + g + m K and then adds its K pending residuals r_{q-K} .. r_{q-1} in lag
-// order (the same fma sequence as one fold per lag: bit-identical s).  The
+// order (the same fma sequence per row as one fold per lag).  The
 // other K - 1 groups only read the spectrum and write r_q (18.7 B/row), their
 // 32-row chunk sums of s advanced by the chunk recurrence A_q = A_{q-1} +
 // B_{q-1} / R_{q-1}.  Residual r_j lives in slot (j - q0 + 1) mod (K + 1) until

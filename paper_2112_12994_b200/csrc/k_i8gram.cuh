@@ -184,10 +184,12 @@ __global__ void __launch_bounds__(256) k_i8_slice(L ld, int64_t rows, int K, int
     uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      const double y = x[u] * 128.0;  // exact (power of two)
-      const double m = __dadd_rn(y, kShift);
+      // 128 x is exact (power of two), so the two fused operations round exactly what the
+      // separate multiply + add / subtract did -- the same digits in 3 fp64 operations instead of 4
+      // (the kernel is bound by the fp64 pipe)
+      const double m = __fma_rn(x[u], 128.0, kShift);
       const double d = __dsub_rn(m, kShift);
-      x[u] = __dsub_rn(y, d);         // exact: y and d share the exponent range
+      x[u] = __fma_rn(x[u], 128.0, -d);  // exact: 128 x and d share the exponent range
       w[u >> 2] |= ((uint32_t)__double2loint(m) & 0xFFu) << (8 * (u & 3));
     }
     const int64_t Ib = (int64_t)s * nbs + j / kI8Tile;

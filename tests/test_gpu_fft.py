@@ -198,10 +198,11 @@ def test_fft_split_score_update_equals_fused(tf, monkeypatch):
     (k_fft_fold, TF_FFT_SPLIT=1, the default) against the update fused into the
     pass (TF_FFT_SPLIT=0): the same device code, so draws, fits, scores and
     residuals are bit-identical -- in RNG mode, three sweeps each (eager, the
-    graph's capture, its replay).  One fold per lag (TF_FFT_SLOTS=1) gives the
-    same row scores bit for bit (the same fma sequence per row); its chunk sums
-    are reduced from the rows instead of advanced by the chunk recurrence, so
-    the CDF totals -- and through the weights the fit -- agree to rounding."""
+    graph's capture, its replay).  One fold per lag (TF_FFT_SLOTS=1) applies the
+    same fma sequence per row, but its chunk sums are reduced from the rows
+    instead of advanced by the chunk recurrence, so the CDF totals -- and
+    through the weights the fit, the residuals and the scores -- agree to
+    rounding (1e-11), not bit for bit."""
     y = c1_like(60000, seed=17, q=9)
     p_bar, c = 24, 900
     out = {}
