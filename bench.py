@@ -28,6 +28,8 @@ to the full sweep; rank 0 only.
 from __future__ import annotations
 
 import argparse
+import contextlib
+import io
 import json
 import os
 import subprocess
@@ -443,10 +445,28 @@ def run_reference(args):
 
 def main():
     args = parse()
-    if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_ours(args)
+    # stdout carries the ONE JSON line and nothing else: while the run is under way file descriptor 1
+    # points at stderr (NCCL prints its version banner to stdout from C when a communicator is made),
+    # and the line itself goes to the real stdout
+    sys.stdout.flush()
+    real_out = os.dup(1)
+    os.dup2(2, 1)
+    buf = io.StringIO()
+    try:
+        with contextlib.redirect_stdout(buf):
+            if args.impl == "reference":
+                run_reference(args)
+            else:
+                run_ours(args)
+    finally:
+        sys.stdout.flush()
+        os.dup2(real_out, 1)
+        os.close(real_out)
+    lines = [ln for ln in buf.getvalue().splitlines() if ln.strip()]
+    for ln in lines[:-1]:
+        print(ln, file=sys.stderr)
+    if lines:
+        print(lines[-1], flush=True)
 
 
 if __name__ == "__main__":
