@@ -2595,6 +2595,12 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
     if (capturing) CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
     else CK(cudaEventRecord(e, st));
   };
+  // The score update beside the solve (k_fft_fold on the side stream) in the sharded loop: measured at
+  // C4 through one rank, the captured graph loses the overlap (5.22 s; 4.93 s with the update fused into
+  // the pass) while eager launches keep it (4.62 s) -- the graph's NCCL nodes seem to serialise the
+  // side branch.  So shards long enough that a lag's device time dwarfs its ~25 launches run the lag
+  // loop eagerly with the overlap; shorter ones replay the graph with the fused update.
+  const bool sh_split = ctx->fft_split && use_fft && fp.K > 1 && w >= ((int64_t)1 << 24);
   auto record = [&]() {
     rec(ctx->ev_begin);
     rec(ctx->events[0]);
@@ -2642,7 +2648,7 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
                                                         ctx->sh_wts.get()});
       if (phases) rec(ctx->pev[2 * (p - 1)]);
       // the shard's score update of an FFT lag beside the (replicated) solve, as in lsar_sweep
-      const bool split = ctx->fft_split && fp.K > 1 && fft_lag(ctx, p_bar, p);
+      const bool split = sh_split && fft_lag(ctx, p_bar, p);
       const bool overlap = split && !phases;
       if (overlap) {
         CK(cudaEventRecord(ctx->ev_fork, st));
@@ -2664,7 +2670,16 @@ static void lsar_sweep_sharded(tf_context* ctx, int p_bar, int64_t c, uint64_t s
     rec(ctx->ev_end);
   };
   const int mode = 64 | (phases ? 4 : 0);
-  const int64_t launches = run_graphed(ctx, ctx->lsar_graph, w, c, p_bar, mode, capturing, record);
+  const bool graphs_off = ctx->no_graphs;
+  ctx->no_graphs = graphs_off || sh_split;  // the overlapped sweep is launched eagerly (see sh_split)
+  int64_t launches = 0;
+  try {
+    launches = run_graphed(ctx, ctx->lsar_graph, w, c, p_bar, mode, capturing, record);
+  } catch (...) {
+    ctx->no_graphs = graphs_off;
+    throw;
+  }
+  ctx->no_graphs = graphs_off;
   CK(cudaStreamSynchronize(st));
   int sth[3];
   CK(cudaMemcpy(sth, ctx->status.get(), 3 * sizeof(int), cudaMemcpyDeviceToHost));
