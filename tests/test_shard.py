@@ -177,3 +177,32 @@ def test_sharded_nccl_world1_fft_pass_and_int8_gram(monkeypatch):
     assert np.array_equal(taus, np.array(ref.pacf.taus)) and np.array_equal(taus2, taus)
     assert pstar == ref.p_star
     assert np.array_equal(d["method"], ref.diag["method"])
+
+
+@pytest.mark.gpu
+def test_sharded_nccl_world1_long_shard_overlapped_fold(monkeypatch):
+    """A shard of >= 2^24 rows takes the sharded loop's other branch: eager
+    launches with each FFT lag's score update (k_fft_fold) on the side stream
+    beside the replicated solve.  Same device code as the single-GPU sweep's
+    split, so one rank through NCCL still equals it bit for bit (twice: the
+    sharded loop must not depend on a graph it never captures)."""
+    import paper_2112_12994_b200 as tf
+    from paper_2112_12994_b200 import gen, shard
+    monkeypatch.setenv("TF_PASS", "fft")
+    roots = gen.ar_roots(6, 1.2, 3.0, 78)
+    n, p_bar, c, seed = (1 << 24) + 5000, 10, 3000, 21
+    e1 = tf.Engine(0)
+    e1.generate_series(roots, n, 78)
+    taus_ref, _, _, ps_ref, _ = e1.lsar_sweep(p_bar, c, seed, n=n)
+    e1.close()
+    dist = _nccl_world1()
+    try:
+        e2 = tf.Engine(0)
+        sh = shard.NcclShard(e2, dist, 1, 0, n, p_bar)
+        sh.generate(roots, 78)
+        taus, _, _, ps, _ = sh.lsar_sweep(c, seed)
+        taus2, _, _, ps2, _ = sh.lsar_sweep(c, seed)
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(taus, taus_ref) and ps == ps_ref
+    assert np.array_equal(taus2, taus) and ps2 == ps
